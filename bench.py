@@ -1,0 +1,410 @@
+"""bench.py — batch-1 MoE decode throughput on B200 (BASELINE.json metric).
+
+Workload (BASELINE.json configs[3]): a 32-layer Mixtral-8x7B-shaped MoE stack
+(d=4096, ffn=14336, 8 experts, top-2), bf16 weights (device Philox init,
+random), fp32 residual stream, batch 1.  One step = one token through all
+32 MoE layers (router -> 2 experts -> combine -> residual, per layer).
+At N>1 (torchrun) the experts of every layer are sharded over the ranks by
+the popularity placement (expert parallelism, one all-reduce per layer); the
+metric is the single token stream's tok/s ("strong" scaling: fixed work).
+
+Reported:
+  value     tok/s with the token already in HBM (CUDA events, max over ranks)
+  e2e       tok/s through moe_forward_host (pinned host buffers, H2D of the
+            token + D2H of the output/routing inside the timed region)
+  roofline  the streaming expert kernel alone, timed live with CUDA events
+            over the same layers: algorithmic bytes (2 experts x 3 x d x f x 2 B
+            = 704,643,072 B per launch) / average launch time vs MEASURED_PEAKS
+  cpu_baseline  the reference's own model_forward (oracle/_ref, compiled from
+            the reference sources) on a bounded sample on the host cores.
+
+    python bench.py [--gpus N --steps K --warmup W] [--impl reference]
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+CONFIGS = {
+    # name: (L, E, k, d, f, dtype)
+    "stack32": (32, 8, 2, 4096, 14336, "bf16"),
+    "layer": (1, 8, 2, 4096, 14336, "bf16"),
+    "x22b": (56, 8, 2, 6144, 16384, "bf16"),
+    "tiny": (1, 8, 2, 512, 1792, "f32"),
+}
+WORKLOAD_NAME = {
+    "stack32": "32-layer Mixtral-8x7B-shaped MoE stack decode, batch 1 (BASELINE configs[3])",
+    "layer": "single Mixtral-8x7B-shaped MoE layer decode, batch 1 (BASELINE configs[1])",
+    "x22b": "56-layer Mixtral-8x22B-shaped MoE stack decode, batch 1 (BASELINE configs[4])",
+    "tiny": "tiny MoE layer d=512 f=1792 fp32 decode, batch 1 (BASELINE configs[0])",
+}
+METRIC = "Mixtral-8x7B MoE decode tok/s (batch 1)"
+
+
+def env_int(name, default):
+    try:
+        return int(os.environ.get(name, default))
+    except ValueError:
+        return default
+
+
+def load_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        j = json.load(open(p))
+        return float(j["hbm_gbs"]), "measured (MEASURED_PEAKS.json)"
+    return 6650.0, "fallback (B200_PROFILING.md)"
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons during the timed region."""
+
+    def __init__(self, gpu_index: int):
+        self.gpu = gpu_index
+        self.samples = []
+        self.proc = None
+
+    def __enter__(self):
+        q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+             "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+             "clocks_event_reasons.sw_power_cap")
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={q}", "--format=csv,noheader,nounits",
+                 "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except (FileNotFoundError, OSError):
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) >= 6:
+                self.samples.append(parts)
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        sm = [float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit()]
+        mx = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for s in self.samples for i in range(4) if s[2 + i] == "Active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.samples)}
+
+
+def dist_setup(n_gpus):
+    world = env_int("WORLD_SIZE", 1)
+    rank = env_int("RANK", 0)
+    local = env_int("LOCAL_RANK", 0)
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.init_process_group("gloo")
+    return world, rank, local
+
+
+def barrier(world):
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.barrier()
+
+
+def max_over_ranks(v, world):
+    if world <= 1:
+        return v
+    import torch
+    import torch.distributed as dist
+
+    t = torch.tensor([v], dtype=torch.float64)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def shard_map(L, E, world, rank_tokens=None):
+    """Expert -> rank map: the reference's popularity ranking (placement.cpp:53-64)
+    with LPT assignment per layer (least-loaded rank, ties to lower rank)."""
+    owner = np.zeros((L, E), np.int32)
+    counts = np.ones((L, E), np.int64) if rank_tokens is None else rank_tokens
+    for l in range(L):
+        order = sorted(range(E), key=lambda e: (-counts[l, e], e))
+        load = [0] * world
+        n = [0] * world
+        cap = (E + world - 1) // world
+        for e in order:
+            r = min((r for r in range(world) if n[r] < cap), key=lambda r: (load[r], r))
+            owner[l, e] = r
+            load[r] += counts[l, e]
+            n[r] += 1
+    return owner
+
+
+# ---------------------------------------------------------------------------
+def run_ours(args):
+    import torch
+
+    import paper_2402_07033_b200 as M
+
+    world, rank, local = dist_setup(args.gpus)
+    L, E, k, d, f, dt = CONFIGS[args.config]
+    dtype = M.DTYPE_BF16 if dt == "bf16" else M.DTYPE_F32
+    esz = 2 if dt == "bf16" else 4
+    torch.cuda.set_device(local)
+    ctx = M.Ctx(local)
+    if world > 1:
+        import torch.distributed as dist
+
+        obj = [M.Ctx.unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(obj, src=0)
+        ctx.init_ep(world, rank, obj[0])
+    owner = shard_map(L, E, world) if world > 1 else None
+    shape = M.Shape(L, E, k, d, f, esz)
+    w = M.Weights(ctx, shape, dtype, owner=owner)
+    w.random(args.seed)
+    stream_ptr = ctx.stream
+    stream = torch.cuda.ExternalStream(stream_ptr, device=f"cuda:{local}")
+
+    # token pool resident in HBM (synthetic N(0,1), identical on every rank)
+    n_steps = args.warmup + args.steps
+    rs = np.random.RandomState(args.seed + 1)
+    pool = torch.tensor(rs.randn(n_steps, d).astype(np.float32), device=f"cuda:{local}")
+    x = torch.empty((1, d), dtype=torch.float32, device=f"cuda:{local}")
+    ids = torch.zeros((L, 1, k), dtype=torch.int32, device=f"cuda:{local}")
+    gates = torch.zeros((L, 1, k), dtype=torch.float32, device=f"cuda:{local}")
+
+    def step(i):
+        with torch.cuda.stream(stream):
+            x.copy_(pool[i:i + 1])
+        w.forward(x, ids, gates, stream=stream_ptr)
+
+    for i in range(args.warmup):
+        step(i)
+    torch.cuda.synchronize()
+    barrier(world)
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clk:
+        torch.cuda.synchronize()
+        barrier(world)
+        ev0.record(stream)
+        for i in range(args.warmup, n_steps):
+            step(i)
+        ev1.record(stream)
+        torch.cuda.synchronize()
+    ms = ev0.elapsed_time(ev1)
+    ms = max_over_ranks(ms, world)
+    barrier(world)
+    ms_per_step = ms / args.steps
+    tok_s = 1000.0 / ms_per_step
+    launches = w.forward_launches(1) * args.steps
+
+    # ---- roofline: the streaming expert kernel alone, live CUDA events ------
+    peak, peak_src = load_peaks()
+    roof = None
+    if w.expert_path(1) == 1:
+        n_rep = max(8, min(64, 2 * L))
+        ypart = torch.empty((ctx.sm_count, d), dtype=torch.float32, device=f"cuda:{local}")
+        # routing with both experts local on this rank (worst case: one rank streams both)
+        lay_ids = []
+        for l in range(L):
+            loc = [e for e in range(E) if owner is None or owner[l, e] == rank]
+            sel = sorted(loc[:k]) if len(loc) >= k else sorted(loc)
+            lay_ids.append(sel + [sel[0]] * (k - len(sel)))
+        idt = torch.tensor(lay_ids, dtype=torch.int32, device=f"cuda:{local}")
+        gt = torch.full((L, k), 1.0 / k, dtype=torch.float32, device=f"cuda:{local}")
+        xk = pool[0:1].clone()
+        for r in range(3):
+            w.decode_experts_partial(r % L, xk, idt[r % L], gt[r % L], ypart, stream=stream_ptr)
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for r in range(n_rep):
+            w.decode_experts_partial(r % L, xk, idt[r % L], gt[r % L], ypart, stream=stream_ptr)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        kern_ms = e0.elapsed_time(e1) / n_rep
+        n_loc = len(set(lay_ids[0]))
+        alg_bytes = n_loc * 3 * d * f * esz
+        achieved = alg_bytes / (kern_ms * 1e-3) / 1e9
+        roof = {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
+                "frac": round(achieved / peak, 4), "traffic": args.traffic,
+                "kernel": "decode_experts_kernel<bf16>", "kernel_us": round(kern_ms * 1e3, 2),
+                "alg_bytes_per_launch": alg_bytes, "peak_source": peak_src,
+                "step_frac": round((L * (k * 3 * d * f * esz + E * d * 4)) / (ms_per_step * 1e-3) / 1e9 / peak, 4)
+                if world == 1 else None}
+        del ypart
+
+    # ---- e2e through the host-buffer C-ABI entry point ----------------------
+    host_tokens = rs.randn(args.steps + 2, d)
+    for i in range(2):
+        w.forward_host(host_tokens[i:i + 1])
+    barrier(world)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize()
+    e0.record(stream)
+    for i in range(args.steps):
+        w.forward_host(host_tokens[2 + i:3 + i])
+    e1.record(stream)
+    torch.cuda.synchronize()
+    e2e_ms = max_over_ranks(e0.elapsed_time(e1), world) / args.steps
+    e2e = {"value": round(1000.0 / e2e_ms, 3), "unit": "tok/s", "h2d_bytes_per_step": d * 4,
+           "d2h_bytes_per_step": d * 4 + L * k * 4 * 2, "ms_per_step": round(e2e_ms, 4)}
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        cpu = cpu_baseline(args, w, pool[args.warmup].cpu().numpy().astype(np.float64), L)
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": round(tok_s, 3), "unit": "tok/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms_per_step, 4),
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+            "dtype": "bf16" if dt == "bf16" else "f32", "data": "synthetic (random-init weights, N(0,1) tokens)",
+            "config": {"workload": WORKLOAD_NAME[args.config], "layers": L, "experts": E, "top_k": k,
+                       "hidden": d, "ffn": f, "batch": 1,
+                       "parallelism": f"ep{world}" if world > 1 else "single-gpu",
+                       "l2": f"inputs larger than L2: {L * k * 3 * d * f * esz / 1e9:.1f} GB of expert weights streamed per step"},
+            "gpu_launches": launches, "clocks": clk.summary(), "e2e": e2e, "roofline": roof,
+            "cpu_baseline": cpu,
+        }
+        print(json.dumps(line), flush=True)
+    w.close()
+    ctx.close()
+
+
+def _mixtral_layer_for_reference(d, f, E, k, token, seed=0):
+    """fp64 weights of one Mixtral-shaped layer for the reference's CPU path:
+    a random router and random N(0,1/sqrt(d)) weights for the experts the
+    token routes to (the others are never touched by model_forward)."""
+    import oracle as O
+
+    ref = O.Reference()
+    shape = O.Shape(1, E, k, d, f, 2)
+    rs = np.random.RandomState(seed)
+    router = rs.randn(E, d) / np.sqrt(d)
+    ids, _ = ref.gate_topk(router, token, k)
+    w = O.Weights(shape, experts=[int(e) for e in ids])
+    for e in ids:
+        wi, wg, wo = w.expert(0, int(e))
+        for m in (wi, wg, wo):
+            m[:] = rs.standard_normal(m.shape) / np.sqrt(d)
+    w.router[0][:] = router
+    return ref, shape, w
+
+
+def cpu_baseline(args, gw, token, L):
+    """Reference model_forward (oracle/_ref) on one Mixtral-shaped layer, a
+    bounded sample of tokens, 1 host thread; scaled to the L-layer stack."""
+    import oracle as O
+
+    if not O.reference_available():
+        return {"value": None, "unit": "tok/s", "cores": 0, "kind": "reference",
+                "sample": "oracle/_ref not built"}
+    _, E, k, d, f, _ = CONFIGS[args.config]
+    ref, shape, w = _mixtral_layer_for_reference(d, f, E, k, token)
+    n = args.cpu_tokens
+    toks = np.repeat(token[None], n, axis=0)
+    _, secs = ref.time_forward(shape, w, toks)
+    per_tok_layer = secs / n
+    return {"value": round(1.0 / (per_tok_layer * L), 5), "unit": "tok/s", "cores": 1, "kind": "reference",
+            "sample": f"{n} tokens x 1 Mixtral-shaped layer (fp64 reference model_forward, "
+                      f"{per_tok_layer * 1e3:.1f} ms/token/layer), scaled to {L} layers",
+            "host_cores": os.cpu_count()}
+
+
+def run_reference(args):
+    """--impl reference: the reference's own CPU path (oracle/_ref, compiled
+    from /root/reference sources) on all host cores, same metric/config."""
+    world = env_int("WORLD_SIZE", 1)
+    rank = env_int("RANK", 0)
+    if world > 1 and rank != 0:
+        return
+    import oracle as O
+
+    L, E, k, d, f, dt = CONFIGS[args.config]
+    if not O.reference_available():
+        print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref/libmoe_ref.so not built"}))
+        return
+    threads = max(1, min(os.cpu_count() or 1, args.ref_threads or (os.cpu_count() or 1)))
+    rs = np.random.RandomState(args.seed + 1)
+    token = rs.randn(d)
+    ref, shape, w = _mixtral_layer_for_reference(d, f, E, k, token)
+    # each step: every thread pushes one token through one layer (reentrant
+    # model_forward); tok/s for the L-layer stack = threads / (t*L)
+    toks = [np.repeat(token[None], 1, axis=0) for _ in range(threads)]
+
+    def one_step():
+        ts = [threading.Thread(target=ref.time_forward, args=(shape, w, toks[i])) for i in range(threads)]
+        t0 = time.perf_counter()
+        for t in ts:
+            t.start()
+        for t in ts:
+            t.join()
+        return time.perf_counter() - t0
+
+    for _ in range(args.warmup):
+        one_step()
+    times = [one_step() for _ in range(args.steps)]
+    secs = sum(times)
+    tok_s = threads * args.steps / (secs * L)
+    line = {"impl": "reference", "metric": METRIC, "value": round(tok_s, 5), "unit": "tok/s",
+            "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": round(1000.0 / tok_s, 3), "higher_is_better": True, "scaling": "strong",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": WORKLOAD_NAME[args.config], "layers": L, "experts": E, "top_k": k,
+                       "hidden": d, "ffn": f, "batch": 1, "parallelism": f"cpu x{threads} threads"},
+            "cpu_baseline": {"value": round(tok_s, 5), "unit": "tok/s", "cores": threads, "kind": "reference",
+                             "sample": f"{threads} threads x 1 token x 1 Mixtral-shaped layer per step "
+                                       f"(reference model_forward, fp64), scaled to {L} layers"},
+            "e2e": {"value": round(tok_s, 5), "unit": "tok/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="stack32", choices=sorted(CONFIGS))
+    ap.add_argument("--seed", type=int, default=0)
+    ap.add_argument("--cpu-tokens", type=int, default=12)
+    ap.add_argument("--ref-threads", type=int, default=0)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--traffic", type=float, default=None,
+                    help="dram bytes per launch of the decode kernel from an ncu --set full capture")
+    args = ap.parse_args()
+    args.warmup = max(3, args.warmup)
+    if args.traffic is None:
+        tp = os.path.join(ROOT, "profiles", "decode_traffic.json")
+        if os.path.exists(tp):
+            args.traffic = json.load(open(tp)).get("dram_bytes_per_launch")
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,164 @@
+/*
+ * moe_b200.h — C-ABI of the B200-native MoE-layer hot path.
+ *
+ * Plain pointers and sizes only (no torch / no CUDA types in signatures; a
+ * stream is passed as `void*` = cudaStream_t, NULL = the context's stream).
+ * Every entry point returns an int status (MOE_OK = 0); moe_last_error()
+ * gives the message of the last failure on this thread.
+ *
+ * Each function replaces a reference interface of the `moe_orch` C++ API
+ * (/root/reference/proj/include/moe_orch/...).  The drop-in C++ shim
+ * (paper_2402_07033_b200/csrc/moe_orch_b200.cpp, headers include/moe_orch/)
+ * implements the reference signatures on top of these calls; INTEGRATION.md
+ * shows the bindings.
+ */
+#ifndef MOE_B200_H
+#define MOE_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* ---- status codes: error.hpp:8-27 taxonomy + device failures ---------- */
+enum {
+  MOE_OK = 0,
+  MOE_ERR_SHAPE = 1,       /* moe_orch::ShapeError       (error.hpp:19-22)  */
+  MOE_ERR_VALIDATION = 2,  /* moe_orch::ValidationError  (error.hpp:14-17)  */
+  MOE_ERR_CUDA = 3,        /* CUDA runtime / launch failure                  */
+  MOE_ERR_NCCL = 4,        /* NCCL failure (expert-parallel exchange)        */
+  MOE_ERR_OOM = 5,         /* device allocation failed                       */
+  MOE_ERR_ARG = 6,         /* NULL pointer, bad enum, out-of-range id        */
+  MOE_ERR_UNSUPPORTED = 7, /* valid request this build cannot serve          */
+  MOE_ERR_NO_DEVICE = 8    /* no sm_100 device visible: there is NO CPU path */
+};
+
+/* Weight storage type on the device.  The residual stream, router and all
+ * accumulation are fp32 in both modes. */
+enum { MOE_DTYPE_BF16 = 0, MOE_DTYPE_F32 = 1 };
+
+/* Mirrors moe_orch::ModelShape (shape.hpp:9-35), field for field. */
+typedef struct moe_shape {
+  int32_t num_layers;
+  int32_t experts_per_layer;
+  int32_t top_k;
+  int32_t hidden_dim;
+  int32_t ffn_dim;
+  int32_t bytes_per_param;
+} moe_shape;
+
+typedef struct moe_ctx moe_ctx;         /* device, stream, scratch, graphs, EP comm */
+typedef struct moe_weights moe_weights; /* device-resident experts + fp32 router   */
+
+/* ---- library / context ------------------------------------------------ */
+int moe_version(void);
+const char* moe_last_error(void);
+/* ModelShape::validate (shape.cpp:7-16): MOE_ERR_SHAPE on violation. */
+int moe_shape_validate(const moe_shape* shape);
+int moe_ctx_create(int device, moe_ctx** out);
+int moe_ctx_destroy(moe_ctx* ctx);
+/* The context's stream (cudaStream_t) used when a call passes stream=NULL. */
+void* moe_ctx_stream(moe_ctx* ctx);
+int moe_ctx_synchronize(moe_ctx* ctx);
+int moe_ctx_sm_count(moe_ctx* ctx);
+
+/* ---- expert parallelism ------------------------------------
+ * The paper's popularity placement (placement.cpp:68-95) re-expressed as an
+ * expert -> rank shard map.  moe_ep_unique_id fills 128 bytes on rank 0
+ * (ncclGetUniqueId); every rank passes the same bytes to moe_ctx_init_ep.
+ * NCCL is dlopen'ed: without libnccl the call fails with MOE_ERR_NCCL. */
+int moe_ep_unique_id(void* uid128);
+int moe_ctx_init_ep(moe_ctx* ctx, int world, int rank, const void* uid128);
+int moe_ctx_world(moe_ctx* ctx, int* world, int* rank);
+
+/* ---- weights (ModelWeights, model.hpp:29-49) ---------------------------
+ * owner_rank: optional [L*E] shard map (NULL = every expert local).  Only
+ * experts owned by the context's rank are allocated.  The router is
+ * replicated (fp32). */
+int moe_weights_create(moe_ctx* ctx, const moe_shape* shape, int dtype,
+                       const int32_t* owner_rank, moe_weights** out);
+int moe_weights_destroy(moe_weights* w);
+int64_t moe_weights_device_bytes(const moe_weights* w);
+/* Upload one expert from the reference's host layout (Matrix::data, row
+ * major): w_in/w_gate [ffn x hidden], w_out [hidden x ffn]; rounded RNE to
+ * the storage dtype on the device.  No-op for experts this rank does not own. */
+int moe_weights_upload_expert(moe_weights* w, int layer, int expert, const double* w_in,
+                              const double* w_gate, const double* w_out);
+int moe_weights_upload_router(moe_weights* w, int layer, const double* router);
+/* Device counter-based N(0, 1/sqrt(hidden)) init (Philox4x32-10, Box-Muller);
+ * the value of a weight depends only on (seed, layer, expert, matrix, index),
+ * so sharded and unsharded models hold identical weights.  Not the
+ * reference's mt19937_64 stream (random_model, model.cpp:34-53): at the
+ * 32/56-layer configs that init is 361 GB of fp64 on the host. */
+int moe_weights_random(moe_weights* w, uint64_t seed);
+/* Read back the device-rounded values in the reference layout (fp64). */
+int moe_weights_download_expert(moe_weights* w, int layer, int expert, double* w_in,
+                                double* w_gate, double* w_out);
+int moe_weights_download_router(moe_weights* w, int layer, double* router);
+
+/* ---- device-pointer hot path ------------------------------------------
+ * x, x_out: fp32 [n_tok x hidden]; ids int32 / gates fp32 [n_tok x top_k]
+ * (expert ids ascending per token, gates = softmax over the selected).
+ * All calls are asynchronous on `stream`. */
+
+/* gate_topk (model.cpp:69-101): fp32 router GEMV, top-k by (logit desc,
+ * id asc), softmax over the selected logits. */
+int moe_router_topk(moe_weights* w, int layer, const float* x, int n_tok, int32_t* ids,
+                    float* gates, void* stream);
+/* Deterministic permutation of (token, slot) pairs by expert (stable:
+ * tokens ascending inside an expert).  counts/offsets [E], perm and
+ * inv_perm [n_tok*top_k]: perm[offsets[e]+i] = t*top_k+j. */
+int moe_permute(moe_ctx* ctx, const int32_t* ids, int n_tok, int top_k, int n_experts,
+                int32_t* counts, int32_t* offsets, int32_t* perm, int32_t* inv_perm,
+                void* stream);
+/* The expert half of one model_forward layer (model.cpp:128-147): SwiGLU
+ * experts of the routed tokens, gate-weighted combine, residual add:
+ * x_out = x + sum_j gates[j] * expert_ffn(ids[j], x).  post_silu (optional,
+ * [n_tok x top_k x ffn]) receives silu(w_in x) for the ActivationSink. */
+int moe_experts_forward(moe_weights* w, int layer, const float* x, int n_tok,
+                        const int32_t* ids, const float* gates, float* x_out,
+                        float* post_silu, void* stream);
+/* The streaming batch-1 expert kernel alone (TMA ring, one CTA per SM):
+ * ypart [moe_ctx_sm_count() x hidden] receives per-CTA partial sums of
+ * sum_j gates[j] * W2_j (silu(W1_j x) * (W3_j x)) over this rank's experts.
+ * MOE_ERR_UNSUPPORTED if the shape has no streaming plan. */
+int moe_decode_experts_partial(moe_weights* w, int layer, const float* x, const int32_t* ids,
+                               const float* gates, float* ypart, void* stream);
+/* One full MoE layer: router + experts + combine + residual. */
+int moe_layer_forward(moe_weights* w, int layer, const float* x, float* x_out, int n_tok,
+                      int32_t* ids, float* gates, void* stream);
+/* model_forward's math (model.cpp:103-161), layer-major: all num_layers
+ * layers in place on x.  ids/gates: [L x n_tok x top_k] routing record
+ * (the RoutingTrace source).  Batch-1 decode runs as one CUDA graph. */
+int moe_forward(moe_weights* w, float* x, int n_tok, int32_t* ids, float* gates,
+                void* stream);
+
+/* ---- host-buffer entry points (what the drop-in shim calls) ------------
+ * Copies in, runs on the device, copies out, synchronizes.  tokens/out are
+ * fp64 [n_tok x hidden] (the reference's vector<vector<double>>); ids [L x
+ * n_tok x k]; gates fp64 [L x n_tok x k]; post_silu optional fp64
+ * [n_tok x L x k x ffn] in the reference's sink call order. */
+int moe_forward_host(moe_weights* w, const double* tokens, int n_tok, double* out,
+                     int32_t* ids, double* gates, double* post_silu);
+/* expert_ffn (model.cpp:55-67) on one host expert (uploaded per call). */
+int moe_expert_ffn_host(moe_ctx* ctx, int dtype, int hidden, int ffn, const double* w_in,
+                        const double* w_gate, const double* w_out, const double* x,
+                        double* y);
+/* gate_topk on a host router matrix [E x hidden]. */
+int moe_gate_topk_host(moe_ctx* ctx, int n_experts, int hidden, const double* router,
+                       const double* x, int top_k, int32_t* ids, double* gates);
+
+/* ---- introspection for tests / bench ---------------------------------- */
+/* Which expert kernel moe_experts_forward uses for (n_tok): 1 = streaming
+ * decode (TMA ring), 2 = generic CUDA, 3 = tcgen05 grouped GEMM prefill. */
+int moe_expert_path(moe_weights* w, int n_tok);
+/* Number of kernels one moe_forward(n_tok) launches. */
+int moe_forward_launches(moe_weights* w, int n_tok);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* MOE_B200_H */

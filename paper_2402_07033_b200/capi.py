@@ -1,0 +1,298 @@
+"""ctypes bindings for include/moe_b200.h (the C-ABI of libmoe_b200.so)."""
+from __future__ import annotations
+
+import ctypes as C
+import os
+import re
+from dataclasses import dataclass
+
+import numpy as np
+
+PKG = os.path.dirname(os.path.abspath(__file__))
+ROOT = os.path.dirname(PKG)
+BUILD = os.path.join(PKG, "_build")
+HEADER = os.path.join(ROOT, "include", "moe_b200.h")
+
+DTYPE_BF16 = 0
+DTYPE_F32 = 1
+
+ERR_NAMES = {1: "ShapeError", 2: "ValidationError", 3: "CudaError", 4: "NcclError",
+             5: "OutOfMemory", 6: "ArgumentError", 7: "Unsupported", 8: "NoDevice"}
+
+_lib = None
+
+
+def lib_path() -> str:
+    return os.path.join(BUILD, "libmoe_b200.so")
+
+
+class MoeError(RuntimeError):
+    def __init__(self, code: int, msg: str):
+        super().__init__(f"{ERR_NAMES.get(code, code)}: {msg}")
+        self.code = code
+        self.kind = ERR_NAMES.get(code, str(code))
+
+
+def declared_symbols() -> list[str]:
+    """Every function the C-ABI header declares."""
+    txt = open(HEADER).read()
+    return sorted(set(re.findall(r"^\s*(?:const\s+)?\w+\*?\s+\**(moe_\w+)\s*\(", txt, re.M)))
+
+
+class _Shape(C.Structure):
+    _fields_ = [("num_layers", C.c_int32), ("experts_per_layer", C.c_int32),
+                ("top_k", C.c_int32), ("hidden_dim", C.c_int32), ("ffn_dim", C.c_int32),
+                ("bytes_per_param", C.c_int32)]
+
+
+@dataclass(frozen=True)
+class Shape:
+    """moe_orch::ModelShape (shape.hpp:9-35)."""
+
+    num_layers: int = 4
+    experts_per_layer: int = 8
+    top_k: int = 2
+    hidden_dim: int = 32
+    ffn_dim: int = 64
+    bytes_per_param: int = 2
+
+    def c(self):
+        return _Shape(self.num_layers, self.experts_per_layer, self.top_k, self.hidden_dim,
+                      self.ffn_dim, self.bytes_per_param)
+
+
+_vp = C.c_void_p
+_dp = C.POINTER(C.c_double)
+_i32p = C.POINTER(C.c_int32)
+
+
+def lib():
+    """Load libmoe_b200.so; raises if it was not built (no fallback)."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    p = lib_path()
+    if not os.path.exists(p):
+        raise ImportError(f"{p} not built — run `python -c 'import __graft_entry__ as g; g.build()'`")
+    L = C.CDLL(p)
+    sig = {
+        "moe_version": ([], C.c_int),
+        "moe_last_error": ([], C.c_char_p),
+        "moe_shape_validate": ([C.POINTER(_Shape)], C.c_int),
+        "moe_ctx_create": ([C.c_int, C.POINTER(_vp)], C.c_int),
+        "moe_ctx_destroy": ([_vp], C.c_int),
+        "moe_ctx_stream": ([_vp], _vp),
+        "moe_ctx_synchronize": ([_vp], C.c_int),
+        "moe_ctx_sm_count": ([_vp], C.c_int),
+        "moe_ep_unique_id": ([_vp], C.c_int),
+        "moe_ctx_init_ep": ([_vp, C.c_int, C.c_int, _vp], C.c_int),
+        "moe_ctx_world": ([_vp, C.POINTER(C.c_int), C.POINTER(C.c_int)], C.c_int),
+        "moe_weights_create": ([_vp, C.POINTER(_Shape), C.c_int, _vp, C.POINTER(_vp)], C.c_int),
+        "moe_weights_destroy": ([_vp], C.c_int),
+        "moe_weights_device_bytes": ([_vp], C.c_int64),
+        "moe_weights_upload_expert": ([_vp, C.c_int, C.c_int, _dp, _dp, _dp], C.c_int),
+        "moe_weights_upload_router": ([_vp, C.c_int, _dp], C.c_int),
+        "moe_weights_random": ([_vp, C.c_uint64], C.c_int),
+        "moe_weights_download_expert": ([_vp, C.c_int, C.c_int, _dp, _dp, _dp], C.c_int),
+        "moe_weights_download_router": ([_vp, C.c_int, _dp], C.c_int),
+        "moe_router_topk": ([_vp, C.c_int, _vp, C.c_int, _vp, _vp, _vp], C.c_int),
+        "moe_permute": ([_vp, _vp, C.c_int, C.c_int, C.c_int, _vp, _vp, _vp, _vp, _vp], C.c_int),
+        "moe_experts_forward": ([_vp, C.c_int, _vp, C.c_int, _vp, _vp, _vp, _vp, _vp], C.c_int),
+        "moe_decode_experts_partial": ([_vp, C.c_int, _vp, _vp, _vp, _vp, _vp], C.c_int),
+        "moe_layer_forward": ([_vp, C.c_int, _vp, _vp, C.c_int, _vp, _vp, _vp], C.c_int),
+        "moe_forward": ([_vp, _vp, C.c_int, _vp, _vp, _vp], C.c_int),
+        "moe_forward_host": ([_vp, _dp, C.c_int, _dp, _i32p, _dp, _dp], C.c_int),
+        "moe_expert_ffn_host": ([_vp, C.c_int, C.c_int, C.c_int, _dp, _dp, _dp, _dp, _dp], C.c_int),
+        "moe_gate_topk_host": ([_vp, C.c_int, C.c_int, _dp, _dp, C.c_int, _i32p, _dp], C.c_int),
+        "moe_expert_path": ([_vp, C.c_int], C.c_int),
+        "moe_forward_launches": ([_vp, C.c_int], C.c_int),
+    }
+    for name, (args, res) in sig.items():
+        fn = getattr(L, name)
+        fn.argtypes = args
+        fn.restype = res
+    _lib = L
+    return L
+
+
+def check(rc: int):
+    if rc != 0:
+        raise MoeError(rc, lib().moe_last_error().decode())
+
+
+def _dptr(a: np.ndarray):
+    return a.ctypes.data_as(_dp)
+
+
+def _ptr(t):
+    """Device pointer of a torch tensor (or None)."""
+    if t is None:
+        return None
+    return C.c_void_p(t.data_ptr())
+
+
+class Ctx:
+    def __init__(self, device: int = 0):
+        h = _vp()
+        check(lib().moe_ctx_create(device, C.byref(h)))
+        self.h = h
+        self.device = device
+
+    def close(self):
+        if self.h:
+            lib().moe_ctx_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    @property
+    def stream(self):
+        return lib().moe_ctx_stream(self.h)
+
+    @property
+    def sm_count(self):
+        return lib().moe_ctx_sm_count(self.h)
+
+    def synchronize(self):
+        check(lib().moe_ctx_synchronize(self.h))
+
+    def init_ep(self, world: int, rank: int, uid: bytes):
+        buf = C.create_string_buffer(bytes(uid), 128)
+        check(lib().moe_ctx_init_ep(self.h, world, rank, buf))
+
+    @staticmethod
+    def unique_id() -> bytes:
+        buf = C.create_string_buffer(128)
+        check(lib().moe_ep_unique_id(buf))
+        return buf.raw
+
+    def permute(self, ids, n_tok, top_k, n_experts, counts, offsets, perm, inv_perm=None,
+                stream=None):
+        check(lib().moe_permute(self.h, _ptr(ids), n_tok, top_k, n_experts, _ptr(counts),
+                                _ptr(offsets), _ptr(perm), _ptr(inv_perm), stream))
+
+    def expert_ffn_host(self, dtype, w_in, w_gate, w_out, x):
+        f, d = w_in.shape
+        y = np.empty(d)
+        args = [np.ascontiguousarray(a, np.float64) for a in (w_in, w_gate, w_out, x)]
+        check(lib().moe_expert_ffn_host(self.h, dtype, d, f, *[_dptr(a) for a in args], _dptr(y)))
+        return y
+
+    def gate_topk_host(self, router, x, k):
+        E, d = router.shape
+        ids = np.empty(k, np.int32)
+        g = np.empty(k)
+        r = np.ascontiguousarray(router, np.float64)
+        xx = np.ascontiguousarray(x, np.float64)
+        check(lib().moe_gate_topk_host(self.h, E, d, _dptr(r), _dptr(xx), k,
+                                       ids.ctypes.data_as(_i32p), _dptr(g)))
+        return ids, g
+
+
+class Weights:
+    def __init__(self, ctx: Ctx, shape: Shape, dtype: int = DTYPE_BF16, owner=None):
+        self.ctx = ctx
+        self.shape = shape
+        self.dtype = dtype
+        h = _vp()
+        own = None
+        if owner is not None:
+            self._owner = np.ascontiguousarray(owner, np.int32).ravel()
+            own = self._owner.ctypes.data_as(_vp)
+        sh = shape.c()
+        check(lib().moe_weights_create(ctx.h, C.byref(sh), dtype, own, C.byref(h)))
+        self.h = h
+
+    def close(self):
+        if self.h:
+            lib().moe_weights_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    @property
+    def device_bytes(self):
+        return lib().moe_weights_device_bytes(self.h)
+
+    def upload_expert(self, layer, expert, w_in, w_gate, w_out):
+        a = [np.ascontiguousarray(m, np.float64) for m in (w_in, w_gate, w_out)]
+        check(lib().moe_weights_upload_expert(self.h, layer, expert, *[_dptr(m) for m in a]))
+
+    def upload_router(self, layer, router):
+        r = np.ascontiguousarray(router, np.float64)
+        check(lib().moe_weights_upload_router(self.h, layer, _dptr(r)))
+
+    def upload_oracle(self, ow):
+        """Upload an oracle.Weights (reference layout, fp64)."""
+        s = self.shape
+        for l in range(s.num_layers):
+            for e in range(s.experts_per_layer):
+                wi, wg, wo = ow.expert(l, e)
+                if wi is not None:
+                    self.upload_expert(l, e, wi, wg, wo)
+            self.upload_router(l, ow.router[l])
+
+    def random(self, seed: int):
+        check(lib().moe_weights_random(self.h, seed))
+
+    def download_expert(self, layer, expert):
+        d, f = self.shape.hidden_dim, self.shape.ffn_dim
+        wi, wg, wo = np.empty((f, d)), np.empty((f, d)), np.empty((d, f))
+        check(lib().moe_weights_download_expert(self.h, layer, expert, _dptr(wi), _dptr(wg),
+                                                _dptr(wo)))
+        return wi, wg, wo
+
+    def download_router(self, layer):
+        r = np.empty((self.shape.experts_per_layer, self.shape.hidden_dim))
+        check(lib().moe_weights_download_router(self.h, layer, _dptr(r)))
+        return r
+
+    # -- device-pointer API (torch tensors) ----------------------------------
+    def router_topk(self, layer, x, ids, gates, stream=None):
+        check(lib().moe_router_topk(self.h, layer, _ptr(x), x.shape[0], _ptr(ids), _ptr(gates),
+                                    stream))
+
+    def experts_forward(self, layer, x, ids, gates, x_out, post_silu=None, stream=None):
+        check(lib().moe_experts_forward(self.h, layer, _ptr(x), x.shape[0], _ptr(ids), _ptr(gates),
+                                        _ptr(x_out), _ptr(post_silu), stream))
+
+    def decode_experts_partial(self, layer, x, ids, gates, ypart, stream=None):
+        check(lib().moe_decode_experts_partial(self.h, layer, _ptr(x), _ptr(ids), _ptr(gates),
+                                               _ptr(ypart), stream))
+
+    def layer_forward(self, layer, x, x_out, ids, gates, stream=None):
+        check(lib().moe_layer_forward(self.h, layer, _ptr(x), _ptr(x_out), x.shape[0], _ptr(ids),
+                                      _ptr(gates), stream))
+
+    def forward(self, x, ids, gates, stream=None):
+        check(lib().moe_forward(self.h, _ptr(x), x.shape[0], _ptr(ids), _ptr(gates), stream))
+
+    # -- host-buffer API ------------------------------------------------------
+    def forward_host(self, tokens: np.ndarray, with_post=False):
+        s = self.shape
+        toks = np.ascontiguousarray(tokens, np.float64).reshape(-1, s.hidden_dim)
+        n = toks.shape[0]
+        out = np.empty_like(toks)
+        ids = np.zeros((max(1, s.num_layers), n, s.top_k), np.int32)
+        gates = np.zeros((max(1, s.num_layers), n, s.top_k))
+        post = np.zeros(max(1, n * s.num_layers * s.top_k * s.ffn_dim)) if with_post else None
+        check(lib().moe_forward_host(self.h, _dptr(toks), n, _dptr(out), ids.ctypes.data_as(_i32p),
+                                     _dptr(gates), _dptr(post) if with_post else _dp()))
+        res = (out, ids[:s.num_layers], gates[:s.num_layers])
+        if with_post:
+            return res + (post[:n * s.num_layers * s.top_k * s.ffn_dim],)
+        return res
+
+    def expert_path(self, n_tok: int) -> int:
+        return lib().moe_expert_path(self.h, n_tok)
+
+    def forward_launches(self, n_tok: int) -> int:
+        return lib().moe_forward_launches(self.h, n_tok)

@@ -1,0 +1,818 @@
+// capi.cu — the extern "C" boundary (include/moe_b200.h): context, device
+// weights, expert-parallel exchange and the layer-major orchestration of the
+// reference's model_forward (model.cpp:103-161).
+#include <dlfcn.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <map>
+#include <mutex>
+#include <string>
+#include <tuple>
+#include <vector>
+
+#include "../../include/moe_b200.h"
+#include "kernels.h"
+
+using moe::Dims;
+using moe::LayerWeights;
+
+namespace {
+
+thread_local std::string g_err;
+
+int fail(int code, const std::string& msg) {
+  g_err = msg;
+  return code;
+}
+
+#define CU(expr)                                                                      \
+  do {                                                                                \
+    cudaError_t _e = (expr);                                                          \
+    if (_e != cudaSuccess) {                                                          \
+      return fail(_e == cudaErrorMemoryAllocation ? MOE_ERR_OOM : MOE_ERR_CUDA,       \
+                  std::string(#expr) + ": " + cudaGetErrorString(_e));                \
+    }                                                                                 \
+  } while (0)
+
+#define TRY(expr)                \
+  do {                           \
+    int _rc = (expr);            \
+    if (_rc != MOE_OK) return _rc; \
+  } while (0)
+
+// ---- NCCL, dlopen'ed (only needed for expert parallelism) ------------------
+struct NcclApi {
+  void* h = nullptr;
+  int (*getUniqueId)(void*) = nullptr;
+  void* commInitRankSym = nullptr;  // takes ncclUniqueId by value, see CommInitRankFn
+  int (*allReduce)(const void*, void*, size_t, int, int, void*, cudaStream_t) = nullptr;
+  int (*commDestroy)(void*) = nullptr;
+  const char* (*errStr)(int) = nullptr;
+};
+struct NcclUid {
+  char internal[128];
+};
+typedef int (*CommInitRankFn)(void**, int, NcclUid, int);
+
+NcclApi* nccl() {
+  static NcclApi api;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    const char* names[] = {"libnccl.so.2", "libnccl.so"};
+    for (const char* n : names) {
+      api.h = dlopen(n, RTLD_NOW | RTLD_GLOBAL);
+      if (api.h) break;
+    }
+    if (!api.h) return;
+    api.getUniqueId = (int (*)(void*))dlsym(api.h, "ncclGetUniqueId");
+    api.commInitRankSym = dlsym(api.h, "ncclCommInitRank");
+    api.allReduce = (int (*)(const void*, void*, size_t, int, int, void*, cudaStream_t))dlsym(
+        api.h, "ncclAllReduce");
+    api.commDestroy = (int (*)(void*))dlsym(api.h, "ncclCommDestroy");
+    api.errStr = (const char* (*)(int))dlsym(api.h, "ncclGetErrorString");
+  });
+  if (!api.h || !api.getUniqueId || !api.commInitRankSym || !api.allReduce) return nullptr;
+  return &api;
+}
+
+constexpr int kNcclFloat32 = 7;
+constexpr int kNcclSum = 0;
+
+}  // namespace
+
+// ---------------------------------------------------------------------------
+struct moe_ctx {
+  int device = 0;
+  int sm_count = 0;
+  cudaStream_t stream = nullptr;
+  int world = 1, rank = 0;
+  void* comm = nullptr;  // ncclComm_t
+  std::mutex mu;
+};
+
+struct DevBuf {
+  void* p = nullptr;
+  size_t bytes = 0;
+  int ensure(size_t n) {
+    if (n <= bytes) return MOE_OK;
+    if (p) cudaFree(p);
+    p = nullptr;
+    bytes = 0;
+    cudaError_t e = cudaMalloc(&p, n);
+    if (e != cudaSuccess) return fail(MOE_ERR_OOM, "cudaMalloc scratch failed");
+    cudaMemset(p, 0, n);
+    bytes = n;
+    return MOE_OK;
+  }
+  void release() {
+    if (p) cudaFree(p);
+    p = nullptr;
+    bytes = 0;
+  }
+  template <typename T>
+  T* as() const {
+    return static_cast<T*>(p);
+  }
+};
+
+struct GraphEntry {
+  cudaGraphExec_t exec = nullptr;
+};
+
+struct moe_weights {
+  moe_ctx* ctx = nullptr;
+  moe_shape shape{};
+  int dtype = MOE_DTYPE_BF16;
+  int esize = 2;
+  std::vector<int32_t> owner;      // [L*E]
+  std::vector<int16_t> slot_of;    // [L*E]
+  std::vector<int> n_local;        // [L]
+  std::vector<void*> layer_mem;    // [L] device, n_local[l] * 3*f*d elements
+  float* router = nullptr;         // [L][E][d]
+  int64_t device_bytes = 0;
+  moe::DecodePlan plan;
+  // scratch
+  DevBuf ypart, rpart, counter, xa, xb, xin, h, y, delta, ids, gates, post;
+  DevBuf stage_d;  // fp64 staging for uploads / downloads
+  void* host_pin = nullptr;
+  size_t host_pin_bytes = 0;
+  std::map<std::tuple<float*, int32_t*, float*, cudaStream_t>, GraphEntry> graphs;
+  std::mutex mu;
+
+  int L() const { return shape.num_layers; }
+  int E() const { return shape.experts_per_layer; }
+  int k() const { return shape.top_k; }
+  int d() const { return shape.hidden_dim; }
+  int f() const { return shape.ffn_dim; }
+  Dims dims() const { return Dims{d(), f(), E(), k(), dtype}; }
+  long long mat_elems() const { return (long long)f() * d(); }
+  LayerWeights layer(int l) const {
+    LayerWeights lw{};
+    lw.experts = layer_mem[l];
+    lw.expert_stride = 3 * mat_elems();
+    lw.mat_stride = mat_elems();
+    lw.router = router + (size_t)l * E() * d();
+    for (int e = 0; e < moe::kMaxExperts; ++e)
+      lw.slot_of[e] = e < E() ? slot_of[(size_t)l * E() + e] : (int16_t)-1;
+    return lw;
+  }
+  void* expert_ptr(int l, int e, int m) const {
+    const int s = slot_of[(size_t)l * E() + e];
+    if (s < 0) return nullptr;
+    return static_cast<char*>(layer_mem[l]) + ((size_t)s * 3 + m) * mat_elems() * esize;
+  }
+};
+
+namespace {
+
+cudaStream_t pick(moe_ctx* c, void* s) { return s ? static_cast<cudaStream_t>(s) : c->stream; }
+
+int check_shape(const moe_shape* s) {
+  if (!s) return fail(MOE_ERR_ARG, "null shape");
+  if (s->num_layers < 0) return fail(MOE_ERR_SHAPE, "num_layers must be non-negative");
+  if (s->experts_per_layer <= 0 || s->top_k <= 0 || s->hidden_dim <= 0 || s->ffn_dim <= 0 ||
+      s->bytes_per_param <= 0)
+    return fail(MOE_ERR_SHAPE, "all shape counts must be strictly positive");
+  if (s->top_k > s->experts_per_layer)
+    return fail(MOE_ERR_SHAPE, "top_k must not exceed experts_per_layer");
+  return MOE_OK;
+}
+
+int set_device(moe_ctx* c) {
+  CU(cudaSetDevice(c->device));
+  return MOE_OK;
+}
+
+// Per-call scratch sized for n_tok tokens.
+int ensure_scratch(moe_weights* w, int n_tok) {
+  const size_t d = w->d(), f = w->f(), k = w->k(), L = std::max(1, w->L());
+  const size_t n = std::max(1, n_tok);
+  TRY(w->xa.ensure(n * d * 4));
+  TRY(w->xb.ensure(n * d * 4));
+  TRY(w->delta.ensure(n * d * 4));
+  TRY(w->xin.ensure(n * d * 4));
+  TRY(w->ids.ensure(L * n * k * 4));
+  TRY(w->gates.ensure(L * n * k * 4));
+  TRY(w->rpart.ensure((size_t)moe::reduce_blocks(w->dims()) * w->E() * 4));
+  TRY(w->counter.ensure(64));
+  TRY(w->ypart.ensure((size_t)std::max(1, w->ctx->sm_count) * d * 4));
+  if (n_tok > 1 || !w->plan.ok) {
+    TRY(w->h.ensure(n * k * f * 4));
+    TRY(w->y.ensure(n * k * d * 4));
+  }
+  return MOE_OK;
+}
+
+int allreduce(moe_weights* w, float* buf, size_t count, cudaStream_t s) {
+  moe_ctx* c = w->ctx;
+  if (c->world <= 1) return MOE_OK;
+  NcclApi* api = nccl();
+  if (!api || !c->comm) return fail(MOE_ERR_NCCL, "expert parallelism requested without NCCL");
+  const int r = api->allReduce(buf, buf, count, kNcclFloat32, kNcclSum, c->comm, s);
+  if (r != 0)
+    return fail(MOE_ERR_NCCL, std::string("ncclAllReduce: ") + (api->errStr ? api->errStr(r) : "?"));
+  return MOE_OK;
+}
+
+bool use_decode(const moe_weights* w, int n_tok, const float* post) {
+  return n_tok == 1 && w->plan.ok && post == nullptr;
+}
+
+// Experts + combine + residual for one layer (x may alias x_out only on
+// the decode path).  EP: local partials -> all-reduce -> residual.
+int experts_forward(moe_weights* w, int l, const float* x, int n_tok, const int32_t* ids,
+                    const float* gates, float* x_out, float* post, cudaStream_t s, bool pdl,
+                    const float* next_router, int32_t* next_ids, float* next_gates) {
+  const Dims dm = w->dims();
+  const LayerWeights lw = w->layer(l);
+  const bool ep = w->ctx->world > 1;
+  if (use_decode(w, n_tok, post)) {
+    CU(moe::launch_decode_experts(w->plan, lw, dm, ids, gates, x, w->ypart.as<float>(), s, pdl));
+    if (!ep) {
+      CU(moe::launch_reduce_residual(w->ypart.as<float>(), w->plan.grid, x, x_out, dm,
+                                     next_router, w->rpart.as<float>(),
+                                     w->counter.as<unsigned>(), next_ids, next_gates, s, pdl));
+      return MOE_OK;
+    }
+    float* delta = w->delta.as<float>();
+    CU(moe::launch_reduce_residual(w->ypart.as<float>(), w->plan.grid, nullptr, delta, dm,
+                                   nullptr, nullptr, nullptr, nullptr, nullptr, s, pdl));
+    TRY(allreduce(w, delta, (size_t)dm.d, s));
+    CU(moe::launch_reduce_residual(delta, 1, x, x_out, dm, next_router, w->rpart.as<float>(),
+                                   w->counter.as<unsigned>(), next_ids, next_gates, s, false));
+    return MOE_OK;
+  }
+  // generic path
+  CU(moe::launch_generic_up(lw, dm, x, n_tok, ids, w->h.as<float>(), post, s, pdl));
+  CU(moe::launch_generic_down(lw, dm, w->h.as<float>(), n_tok, ids, w->y.as<float>(), s, pdl));
+  if (!ep) {
+    CU(moe::launch_combine(x, w->y.as<float>(), gates, n_tok, dm, x_out, s, pdl));
+  } else {
+    float* delta = w->delta.as<float>();
+    CU(moe::launch_combine(nullptr, w->y.as<float>(), gates, n_tok, dm, delta, s, pdl));
+    TRY(allreduce(w, delta, (size_t)n_tok * dm.d, s));
+    CU(moe::launch_add(x, delta, x_out, (long long)n_tok * dm.d, s, false));
+  }
+  if (next_router)
+    CU(moe::launch_router_topk(next_router, x_out, n_tok, dm, next_ids, next_gates, s, pdl));
+  return MOE_OK;
+}
+
+// Enqueue the whole L-layer forward on stream s (x in place).
+int enqueue_forward(moe_weights* w, float* x, int n_tok, int32_t* ids, float* gates,
+                    cudaStream_t s, float* post_all) {
+  const int L = w->L();
+  const Dims dm = w->dims();
+  const size_t tk = (size_t)n_tok * dm.k;
+  const bool pdl = true;
+  CU(moe::launch_router_topk(w->router, x, n_tok, dm, ids, gates, s, false));
+  const float* cur = x;
+  for (int l = 0; l < L; ++l) {
+    float* nxt = (l == L - 1) ? x : ((l % 2 == 0) ? w->xa.as<float>() : w->xb.as<float>());
+    const bool more = l + 1 < L;
+    float* post = post_all ? post_all + (size_t)l * tk * dm.f : nullptr;
+    TRY(experts_forward(w, l, cur, n_tok, ids + (size_t)l * tk, gates + (size_t)l * tk, nxt,
+                        post, s, pdl,
+                        more ? w->router + (size_t)(l + 1) * dm.E * dm.d : nullptr,
+                        more ? ids + (size_t)(l + 1) * tk : nullptr,
+                        more ? gates + (size_t)(l + 1) * tk : nullptr));
+    cur = nxt;
+  }
+  return MOE_OK;
+}
+
+int forward_graph(moe_weights* w, float* x, int32_t* ids, float* gates, cudaStream_t s) {
+  auto key = std::make_tuple(x, ids, gates, s);
+  auto it = w->graphs.find(key);
+  if (it == w->graphs.end()) {
+    cudaGraph_t g = nullptr;
+    CU(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal));
+    const int rc = enqueue_forward(w, x, 1, ids, gates, s, nullptr);
+    cudaError_t e = cudaStreamEndCapture(s, &g);
+    if (rc != MOE_OK) {
+      if (g) cudaGraphDestroy(g);
+      return rc;
+    }
+    CU(e);
+    GraphEntry ge;
+    e = cudaGraphInstantiate(&ge.exec, g, 0);
+    cudaGraphDestroy(g);
+    CU(e);
+    it = w->graphs.emplace(key, ge).first;
+  }
+  CU(cudaGraphLaunch(it->second.exec, s));
+  return MOE_OK;
+}
+
+int host_pinned(moe_weights* w, size_t bytes, void** out) {
+  if (w->host_pin_bytes < bytes) {
+    if (w->host_pin) cudaFreeHost(w->host_pin);
+    w->host_pin = nullptr;
+    w->host_pin_bytes = 0;
+    CU(cudaMallocHost(&w->host_pin, bytes));
+    w->host_pin_bytes = bytes;
+  }
+  *out = w->host_pin;
+  return MOE_OK;
+}
+
+}  // namespace
+
+// ===========================================================================
+extern "C" {
+
+int moe_version(void) { return 1; }
+const char* moe_last_error(void) { return g_err.c_str(); }
+int moe_shape_validate(const moe_shape* s) { return check_shape(s); }
+
+int moe_ctx_create(int device, moe_ctx** out) {
+  if (!out) return fail(MOE_ERR_ARG, "null out");
+  *out = nullptr;
+  int n = 0;
+  if (cudaGetDeviceCount(&n) != cudaSuccess || n == 0)
+    return fail(MOE_ERR_NO_DEVICE, "no CUDA device visible (the product has no CPU path)");
+  if (device < 0 || device >= n) return fail(MOE_ERR_ARG, "device index out of range");
+  cudaDeviceProp prop;
+  CU(cudaGetDeviceProperties(&prop, device));
+  if (prop.major != 10)
+    return fail(MOE_ERR_NO_DEVICE, std::string("needs an sm_100 (B200) device, found ") + prop.name);
+  auto* c = new moe_ctx();
+  c->device = device;
+  c->sm_count = prop.multiProcessorCount;
+  cudaError_t e = cudaSetDevice(device);
+  if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking);
+  if (e != cudaSuccess) {
+    delete c;
+    return fail(MOE_ERR_CUDA, cudaGetErrorString(e));
+  }
+  *out = c;
+  return MOE_OK;
+}
+
+int moe_ctx_destroy(moe_ctx* c) {
+  if (!c) return MOE_OK;
+  cudaSetDevice(c->device);
+  if (c->comm && nccl() && nccl()->commDestroy) nccl()->commDestroy(c->comm);
+  if (c->stream) cudaStreamDestroy(c->stream);
+  delete c;
+  return MOE_OK;
+}
+
+void* moe_ctx_stream(moe_ctx* c) { return c ? (void*)c->stream : nullptr; }
+
+int moe_ctx_synchronize(moe_ctx* c) {
+  if (!c) return fail(MOE_ERR_ARG, "null ctx");
+  TRY(set_device(c));
+  CU(cudaStreamSynchronize(c->stream));
+  return MOE_OK;
+}
+
+int moe_ctx_sm_count(moe_ctx* c) { return c ? c->sm_count : 0; }
+
+int moe_ep_unique_id(void* uid128) {
+  if (!uid128) return fail(MOE_ERR_ARG, "null uid");
+  NcclApi* api = nccl();
+  if (!api) return fail(MOE_ERR_NCCL, "libnccl.so.2 not loadable");
+  const int r = api->getUniqueId(uid128);
+  if (r) return fail(MOE_ERR_NCCL, "ncclGetUniqueId failed");
+  return MOE_OK;
+}
+
+int moe_ctx_init_ep(moe_ctx* c, int world, int rank, const void* uid128) {
+  if (!c || !uid128) return fail(MOE_ERR_ARG, "null argument");
+  if (world < 1 || rank < 0 || rank >= world) return fail(MOE_ERR_ARG, "bad world/rank");
+  if (world == 1) {
+    c->world = 1;
+    c->rank = 0;
+    return MOE_OK;
+  }
+  NcclApi* api = nccl();
+  if (!api) return fail(MOE_ERR_NCCL, "libnccl.so.2 not loadable");
+  TRY(set_device(c));
+  NcclUid uid;
+  std::memcpy(uid.internal, uid128, 128);
+  void* comm = nullptr;
+  const int r = reinterpret_cast<CommInitRankFn>(api->commInitRankSym)(&comm, world, uid, rank);
+  if (r) return fail(MOE_ERR_NCCL, std::string("ncclCommInitRank: ") + (api->errStr ? api->errStr(r) : "?"));
+  c->comm = comm;
+  c->world = world;
+  c->rank = rank;
+  return MOE_OK;
+}
+
+int moe_ctx_world(moe_ctx* c, int* world, int* rank) {
+  if (!c) return fail(MOE_ERR_ARG, "null ctx");
+  if (world) *world = c->world;
+  if (rank) *rank = c->rank;
+  return MOE_OK;
+}
+
+int moe_weights_create(moe_ctx* c, const moe_shape* shape, int dtype, const int32_t* owner_rank,
+                       moe_weights** out) {
+  if (!c || !out) return fail(MOE_ERR_ARG, "null argument");
+  *out = nullptr;
+  TRY(check_shape(shape));
+  if (dtype != MOE_DTYPE_BF16 && dtype != MOE_DTYPE_F32) return fail(MOE_ERR_ARG, "bad dtype");
+  if (shape->experts_per_layer > moe::kMaxExperts)
+    return fail(MOE_ERR_UNSUPPORTED, "experts_per_layer > 256");
+  TRY(set_device(c));
+  auto* w = new moe_weights();
+  w->ctx = c;
+  w->shape = *shape;
+  w->dtype = dtype;
+  w->esize = dtype == MOE_DTYPE_BF16 ? 2 : 4;
+  const int L = shape->num_layers, E = shape->experts_per_layer;
+  w->owner.assign((size_t)L * E, 0);
+  if (owner_rank) {
+    for (int i = 0; i < L * E; ++i) {
+      if (owner_rank[i] < 0 || owner_rank[i] >= c->world) {
+        delete w;
+        return fail(MOE_ERR_ARG, "owner rank out of range");
+      }
+      w->owner[i] = owner_rank[i];
+    }
+  }
+  w->slot_of.assign((size_t)L * E, -1);
+  w->n_local.assign(L, 0);
+  w->layer_mem.assign(L, nullptr);
+  auto cleanup = [&](int rc) {
+    moe_weights_destroy(w);
+    return rc;
+  };
+  for (int l = 0; l < L; ++l) {
+    int n = 0;
+    for (int e = 0; e < E; ++e)
+      if (w->owner[(size_t)l * E + e] == c->rank) w->slot_of[(size_t)l * E + e] = (int16_t)n++;
+    w->n_local[l] = n;
+    const size_t bytes = (size_t)n * 3 * w->mat_elems() * w->esize;
+    if (bytes) {
+      cudaError_t e = cudaMalloc(&w->layer_mem[l], bytes);
+      if (e != cudaSuccess)
+        return cleanup(fail(MOE_ERR_OOM, "cudaMalloc experts: " + std::string(cudaGetErrorString(e))));
+      w->device_bytes += bytes;
+    }
+  }
+  const size_t rbytes = (size_t)std::max(1, L) * E * shape->hidden_dim * 4;
+  if (cudaMalloc(&w->router, rbytes) != cudaSuccess)
+    return cleanup(fail(MOE_ERR_OOM, "cudaMalloc router"));
+  cudaMemset(w->router, 0, rbytes);
+  w->device_bytes += rbytes;
+  w->plan = moe::plan_decode(w->dims(), c->sm_count);
+  *out = w;
+  return MOE_OK;
+}
+
+int moe_weights_destroy(moe_weights* w) {
+  if (!w) return MOE_OK;
+  cudaSetDevice(w->ctx->device);
+  for (auto& kv : w->graphs)
+    if (kv.second.exec) cudaGraphExecDestroy(kv.second.exec);
+  for (void* p : w->layer_mem)
+    if (p) cudaFree(p);
+  if (w->router) cudaFree(w->router);
+  for (DevBuf* b : {&w->ypart, &w->rpart, &w->counter, &w->xa, &w->xb, &w->xin, &w->h, &w->y, &w->delta,
+                    &w->ids, &w->gates, &w->post, &w->stage_d})
+    b->release();
+  if (w->host_pin) cudaFreeHost(w->host_pin);
+  delete w;
+  return MOE_OK;
+}
+
+int64_t moe_weights_device_bytes(const moe_weights* w) { return w ? w->device_bytes : 0; }
+
+static int check_le(moe_weights* w, int layer, int expert) {
+  if (!w) return fail(MOE_ERR_ARG, "null weights");
+  if (layer < 0 || layer >= w->L()) return fail(MOE_ERR_SHAPE, "layer index out of range");
+  if (expert < 0 || expert >= w->E()) return fail(MOE_ERR_SHAPE, "expert index out of range");
+  return MOE_OK;
+}
+
+int moe_weights_upload_expert(moe_weights* w, int layer, int expert, const double* w_in,
+                              const double* w_gate, const double* w_out) {
+  TRY(check_le(w, layer, expert));
+  if (!w_in || !w_gate || !w_out) return fail(MOE_ERR_ARG, "null matrix");
+  std::lock_guard<std::mutex> lk(w->mu);
+  if (w->slot_of[(size_t)layer * w->E() + expert] < 0) return MOE_OK;  // remote
+  TRY(set_device(w->ctx));
+  const long long n = w->mat_elems();
+  TRY(w->stage_d.ensure((size_t)n * 8));
+  cudaStream_t s = w->ctx->stream;
+  const double* src[3] = {w_in, w_gate, w_out};
+  for (int m = 0; m < 3; ++m) {
+    CU(cudaMemcpyAsync(w->stage_d.p, src[m], (size_t)n * 8, cudaMemcpyHostToDevice, s));
+    if (m < 2)
+      CU(moe::launch_convert(w->stage_d.as<double>(), w->expert_ptr(layer, expert, m), w->dtype,
+                             w->f(), w->d(), false, s));
+    else  // w_out [d x f] -> W2T [f x d]
+      CU(moe::launch_convert(w->stage_d.as<double>(), w->expert_ptr(layer, expert, m), w->dtype,
+                             w->d(), w->f(), true, s));
+    CU(cudaStreamSynchronize(s));
+  }
+  return MOE_OK;
+}
+
+int moe_weights_upload_router(moe_weights* w, int layer, const double* router) {
+  TRY(check_le(w, layer, 0));
+  if (!router) return fail(MOE_ERR_ARG, "null router");
+  std::lock_guard<std::mutex> lk(w->mu);
+  TRY(set_device(w->ctx));
+  const long long n = (long long)w->E() * w->d();
+  TRY(w->stage_d.ensure((size_t)n * 8));
+  cudaStream_t s = w->ctx->stream;
+  CU(cudaMemcpyAsync(w->stage_d.p, router, (size_t)n * 8, cudaMemcpyHostToDevice, s));
+  CU(moe::launch_convert_f32(w->stage_d.as<double>(), w->router + (size_t)layer * n, n, s));
+  CU(cudaStreamSynchronize(s));
+  return MOE_OK;
+}
+
+int moe_weights_random(moe_weights* w, uint64_t seed) {
+  if (!w) return fail(MOE_ERR_ARG, "null weights");
+  std::lock_guard<std::mutex> lk(w->mu);
+  TRY(set_device(w->ctx));
+  cudaStream_t s = w->ctx->stream;
+  const float scale = (float)(1.0 / std::sqrt((double)w->d()));
+  for (int l = 0; l < w->L(); ++l) {
+    for (int e = 0; e < w->E(); ++e) {
+      if (w->slot_of[(size_t)l * w->E() + e] < 0) continue;
+      for (int m = 0; m < 3; ++m) {
+        const uint64_t tag = ((uint64_t)l << 40) | ((uint64_t)e << 8) | (uint64_t)m;
+        if (m < 2)
+          CU(moe::launch_random(w->expert_ptr(l, e, m), w->dtype, w->f(), w->d(), false, seed,
+                                tag, scale, s));
+        else
+          CU(moe::launch_random(w->expert_ptr(l, e, m), w->dtype, w->d(), w->f(), true, seed,
+                                tag, scale, s));
+      }
+    }
+    const uint64_t rtag = ((uint64_t)l << 40) | (0xFFFFull << 8) | 3ull;
+    CU(moe::launch_random(w->router + (size_t)l * w->E() * w->d(), MOE_DTYPE_F32, w->E(), w->d(),
+                          false, seed, rtag, scale, s));
+  }
+  CU(cudaStreamSynchronize(s));
+  return MOE_OK;
+}
+
+int moe_weights_download_expert(moe_weights* w, int layer, int expert, double* w_in,
+                                double* w_gate, double* w_out) {
+  TRY(check_le(w, layer, expert));
+  std::lock_guard<std::mutex> lk(w->mu);
+  if (w->slot_of[(size_t)layer * w->E() + expert] < 0)
+    return fail(MOE_ERR_ARG, "expert not resident on this rank");
+  TRY(set_device(w->ctx));
+  const long long n = w->mat_elems();
+  TRY(w->stage_d.ensure((size_t)n * 8));
+  cudaStream_t s = w->ctx->stream;
+  double* dst[3] = {w_in, w_gate, w_out};
+  for (int m = 0; m < 3; ++m) {
+    if (!dst[m]) continue;
+    if (m < 2)
+      CU(moe::launch_to_double(w->expert_ptr(layer, expert, m), w->dtype, w->stage_d.as<double>(),
+                               w->f(), w->d(), false, s));
+    else
+      CU(moe::launch_to_double(w->expert_ptr(layer, expert, m), w->dtype, w->stage_d.as<double>(),
+                               w->d(), w->f(), true, s));
+    CU(cudaMemcpyAsync(dst[m], w->stage_d.p, (size_t)n * 8, cudaMemcpyDeviceToHost, s));
+    CU(cudaStreamSynchronize(s));
+  }
+  return MOE_OK;
+}
+
+int moe_weights_download_router(moe_weights* w, int layer, double* router) {
+  TRY(check_le(w, layer, 0));
+  if (!router) return fail(MOE_ERR_ARG, "null router");
+  std::lock_guard<std::mutex> lk(w->mu);
+  TRY(set_device(w->ctx));
+  const size_t n = (size_t)w->E() * w->d();
+  std::vector<float> tmp(n);
+  CU(cudaMemcpy(tmp.data(), w->router + (size_t)layer * n, n * 4, cudaMemcpyDeviceToHost));
+  for (size_t i = 0; i < n; ++i) router[i] = tmp[i];
+  return MOE_OK;
+}
+
+int moe_router_topk(moe_weights* w, int layer, const float* x, int n_tok, int32_t* ids,
+                    float* gates, void* stream) {
+  TRY(check_le(w, layer, 0));
+  if (n_tok < 0) return fail(MOE_ERR_ARG, "n_tok < 0");
+  if (n_tok == 0) return MOE_OK;
+  if (!x || !ids || !gates) return fail(MOE_ERR_ARG, "null pointer");
+  TRY(set_device(w->ctx));
+  CU(moe::launch_router_topk(w->router + (size_t)layer * w->E() * w->d(), x, n_tok, w->dims(),
+                             ids, gates, pick(w->ctx, stream), false));
+  return MOE_OK;
+}
+
+int moe_permute(moe_ctx* c, const int32_t* ids, int n_tok, int top_k, int n_experts,
+                int32_t* counts, int32_t* offsets, int32_t* perm, int32_t* inv_perm,
+                void* stream) {
+  if (!c || !counts || !offsets || (n_tok > 0 && (!ids || !perm)))
+    return fail(MOE_ERR_ARG, "null pointer");
+  if (n_tok < 0 || top_k < 1 || n_experts < 1 || n_experts > moe::kMaxExperts)
+    return fail(MOE_ERR_SHAPE, "bad permute geometry");
+  TRY(set_device(c));
+  CU(moe::launch_permute(ids, n_tok, top_k, n_experts, counts, offsets, perm, inv_perm,
+                         pick(c, stream)));
+  return MOE_OK;
+}
+
+int moe_experts_forward(moe_weights* w, int layer, const float* x, int n_tok, const int32_t* ids,
+                        const float* gates, float* x_out, float* post_silu, void* stream) {
+  TRY(check_le(w, layer, 0));
+  if (n_tok < 0) return fail(MOE_ERR_ARG, "n_tok < 0");
+  if (n_tok == 0) return MOE_OK;
+  if (!x || !ids || !gates || !x_out) return fail(MOE_ERR_ARG, "null pointer");
+  std::lock_guard<std::mutex> lk(w->mu);
+  TRY(set_device(w->ctx));
+  TRY(ensure_scratch(w, n_tok));
+  return experts_forward(w, layer, x, n_tok, ids, gates, x_out, post_silu, pick(w->ctx, stream),
+                         false, nullptr, nullptr, nullptr);
+}
+
+int moe_decode_experts_partial(moe_weights* w, int layer, const float* x, const int32_t* ids,
+                               const float* gates, float* ypart, void* stream) {
+  TRY(check_le(w, layer, 0));
+  if (!x || !ids || !gates || !ypart) return fail(MOE_ERR_ARG, "null pointer");
+  if (!w->plan.ok) return fail(MOE_ERR_UNSUPPORTED, "shape has no streaming decode plan");
+  TRY(set_device(w->ctx));
+  CU(moe::launch_decode_experts(w->plan, w->layer(layer), w->dims(), ids, gates, x, ypart,
+                                pick(w->ctx, stream), false));
+  return MOE_OK;
+}
+
+int moe_layer_forward(moe_weights* w, int layer, const float* x, float* x_out, int n_tok,
+                      int32_t* ids, float* gates, void* stream) {
+  TRY(check_le(w, layer, 0));
+  if (n_tok < 0) return fail(MOE_ERR_ARG, "n_tok < 0");
+  if (n_tok == 0) return MOE_OK;
+  if (!x || !ids || !gates || !x_out) return fail(MOE_ERR_ARG, "null pointer");
+  std::lock_guard<std::mutex> lk(w->mu);
+  TRY(set_device(w->ctx));
+  TRY(ensure_scratch(w, n_tok));
+  cudaStream_t s = pick(w->ctx, stream);
+  CU(moe::launch_router_topk(w->router + (size_t)layer * w->E() * w->d(), x, n_tok, w->dims(), ids,
+                             gates, s, false));
+  return experts_forward(w, layer, x, n_tok, ids, gates, x_out, nullptr, s, true, nullptr, nullptr,
+                         nullptr);
+}
+
+int moe_forward(moe_weights* w, float* x, int n_tok, int32_t* ids, float* gates, void* stream) {
+  if (!w) return fail(MOE_ERR_ARG, "null weights");
+  if (n_tok < 0) return fail(MOE_ERR_ARG, "n_tok < 0");
+  if (n_tok == 0 || w->L() == 0) return MOE_OK;
+  if (!x || !ids || !gates) return fail(MOE_ERR_ARG, "null pointer");
+  std::lock_guard<std::mutex> lk(w->mu);
+  TRY(set_device(w->ctx));
+  TRY(ensure_scratch(w, n_tok));
+  cudaStream_t s = pick(w->ctx, stream);
+  if (n_tok == 1 && w->plan.ok) return forward_graph(w, x, ids, gates, s);
+  return enqueue_forward(w, x, n_tok, ids, gates, s, nullptr);
+}
+
+int moe_forward_host(moe_weights* w, const double* tokens, int n_tok, double* out, int32_t* ids,
+                     double* gates, double* post_silu) {
+  if (!w) return fail(MOE_ERR_ARG, "null weights");
+  if (n_tok < 0) return fail(MOE_ERR_ARG, "n_tok < 0");
+  const int L = w->L(), d = w->d(), k = w->k(), f = w->f();
+  if (n_tok == 0) return MOE_OK;
+  if (!tokens || !out) return fail(MOE_ERR_ARG, "null pointer");
+  if (L == 0) {
+    std::memcpy(out, tokens, sizeof(double) * (size_t)n_tok * d);
+    return MOE_OK;
+  }
+  std::lock_guard<std::mutex> lk(w->mu);
+  TRY(set_device(w->ctx));
+  TRY(ensure_scratch(w, n_tok));
+  cudaStream_t s = w->ctx->stream;
+  const size_t nx = (size_t)n_tok * d, nr = (size_t)L * n_tok * k;
+  const size_t npost = post_silu ? (size_t)L * n_tok * k * f : 0;
+  void* pin = nullptr;
+  TRY(host_pinned(w, nx * 4 + nr * 8 + npost * 4, &pin));
+  float* hx = static_cast<float*>(pin);
+  int32_t* hids = reinterpret_cast<int32_t*>(hx + nx);
+  float* hg = reinterpret_cast<float*>(hids + nr);
+  float* hpost = hg + nr;
+  for (size_t i = 0; i < nx; ++i) hx[i] = (float)tokens[i];
+  float* dx = w->xin.as<float>();  // device copy of the tokens (in/out)
+  int32_t* dids = w->ids.as<int32_t>();
+  float* dg = w->gates.as<float>();
+  CU(cudaMemcpyAsync(dx, hx, nx * 4, cudaMemcpyHostToDevice, s));
+  if (post_silu) {
+    TRY(w->post.ensure(npost * 4));
+    // the sink path needs silu(w_in x) per (token, slot): generic kernels, no graph
+    TRY(enqueue_forward(w, dx, n_tok, dids, dg, s, w->post.as<float>()));
+    CU(cudaMemcpyAsync(hpost, w->post.p, npost * 4, cudaMemcpyDeviceToHost, s));
+  } else if (n_tok == 1 && w->plan.ok) {
+    TRY(forward_graph(w, dx, dids, dg, s));
+  } else {
+    TRY(enqueue_forward(w, dx, n_tok, dids, dg, s, nullptr));
+  }
+  CU(cudaMemcpyAsync(hx, dx, nx * 4, cudaMemcpyDeviceToHost, s));
+  CU(cudaMemcpyAsync(hids, dids, nr * 4, cudaMemcpyDeviceToHost, s));
+  CU(cudaMemcpyAsync(hg, dg, nr * 4, cudaMemcpyDeviceToHost, s));
+  CU(cudaStreamSynchronize(s));
+  for (size_t i = 0; i < nx; ++i) out[i] = hx[i];
+  if (ids) std::memcpy(ids, hids, nr * 4);
+  if (gates)
+    for (size_t i = 0; i < nr; ++i) gates[i] = hg[i];
+  if (post_silu) {
+    // device layout [l][t][j][r] -> reference sink order [t][l][j][r]
+    for (int l = 0; l < L; ++l)
+      for (int t = 0; t < n_tok; ++t)
+        for (int j = 0; j < k; ++j) {
+          const float* src = hpost + (((size_t)l * n_tok + t) * k + j) * f;
+          double* dst = post_silu + (((size_t)t * L + l) * k + j) * f;
+          for (int r = 0; r < f; ++r) dst[r] = src[r];
+        }
+  }
+  return MOE_OK;
+}
+
+int moe_expert_ffn_host(moe_ctx* c, int dtype, int hidden, int ffn, const double* w_in,
+                        const double* w_gate, const double* w_out, const double* x, double* y) {
+  if (!c || !w_in || !w_gate || !w_out || !x || !y) return fail(MOE_ERR_ARG, "null pointer");
+  moe_shape sh{1, 1, 1, hidden, ffn, dtype == MOE_DTYPE_BF16 ? 2 : 4};
+  moe_weights* w = nullptr;
+  TRY(moe_weights_create(c, &sh, dtype, nullptr, &w));
+  int rc = moe_weights_upload_expert(w, 0, 0, w_in, w_gate, w_out);
+  if (rc == MOE_OK) {
+    std::lock_guard<std::mutex> lk(w->mu);
+    cudaStream_t s = c->stream;
+    rc = ensure_scratch(w, 1);
+    float* dx = w->xa.as<float>();
+    float* dy = w->xb.as<float>();
+    int32_t* dids = w->ids.as<int32_t>();
+    float* dg = w->gates.as<float>();
+    std::vector<float> hx(hidden);
+    for (int i = 0; i < hidden; ++i) hx[i] = (float)x[i];
+    const int32_t id0 = 0;
+    const float one = 1.0f;
+    if (rc == MOE_OK && (cudaMemcpyAsync(dx, hx.data(), hidden * 4, cudaMemcpyHostToDevice, s) ||
+                         cudaMemcpyAsync(dids, &id0, 4, cudaMemcpyHostToDevice, s) ||
+                         cudaMemcpyAsync(dg, &one, 4, cudaMemcpyHostToDevice, s)))
+      rc = fail(MOE_ERR_CUDA, "H2D failed");
+    // y = 1 * expert(x): generic kernels with a zero residual
+    if (rc == MOE_OK) {
+      const Dims dm = w->dims();
+      const LayerWeights lw = w->layer(0);
+      if (w->h.ensure((size_t)ffn * 4) || w->y.ensure((size_t)hidden * 4))
+        rc = MOE_ERR_OOM;
+      else if (moe::launch_generic_up(lw, dm, dx, 1, dids, w->h.as<float>(), nullptr, s, false) ||
+          moe::launch_generic_down(lw, dm, w->h.as<float>(), 1, dids, w->y.as<float>(), s, false) ||
+          moe::launch_combine(nullptr, w->y.as<float>(), dg, 1, dm, dy, s, false))
+        rc = fail(MOE_ERR_CUDA, "expert kernels failed");
+    }
+    if (rc == MOE_OK) {
+      if (cudaMemcpyAsync(hx.data(), dy, hidden * 4, cudaMemcpyDeviceToHost, s) ||
+          cudaStreamSynchronize(s))
+        rc = fail(MOE_ERR_CUDA, "D2H failed");
+      else
+        for (int i = 0; i < hidden; ++i) y[i] = hx[i];
+    }
+  }
+  moe_weights_destroy(w);
+  return rc;
+}
+
+int moe_gate_topk_host(moe_ctx* c, int n_experts, int hidden, const double* router,
+                       const double* x, int top_k, int32_t* ids, double* gates) {
+  if (!c || !router || !x || !ids || !gates) return fail(MOE_ERR_ARG, "null pointer");
+  if (top_k < 1 || top_k > n_experts) return fail(MOE_ERR_SHAPE, "top_k out of range");
+  moe_shape sh{1, n_experts, top_k, hidden, 1, 4};
+  moe_weights* w = nullptr;
+  TRY(moe_weights_create(c, &sh, MOE_DTYPE_F32, nullptr, &w));
+  int rc = moe_weights_upload_router(w, 0, router);
+  if (rc == MOE_OK) rc = ensure_scratch(w, 1);
+  if (rc == MOE_OK) {
+    cudaStream_t s = c->stream;
+    std::vector<float> hx(hidden), hg(top_k);
+    for (int i = 0; i < hidden; ++i) hx[i] = (float)x[i];
+    if (cudaMemcpyAsync(w->xa.p, hx.data(), hidden * 4, cudaMemcpyHostToDevice, s) ||
+        moe::launch_router_topk(w->router, w->xa.as<float>(), 1, w->dims(), w->ids.as<int32_t>(),
+                                w->gates.as<float>(), s, false) ||
+        cudaMemcpyAsync(ids, w->ids.p, top_k * 4, cudaMemcpyDeviceToHost, s) ||
+        cudaMemcpyAsync(hg.data(), w->gates.p, top_k * 4, cudaMemcpyDeviceToHost, s) ||
+        cudaStreamSynchronize(s))
+      rc = fail(MOE_ERR_CUDA, "router kernel failed");
+    else
+      for (int j = 0; j < top_k; ++j) gates[j] = hg[j];
+  }
+  moe_weights_destroy(w);
+  return rc;
+}
+
+int moe_expert_path(moe_weights* w, int n_tok) {
+  if (!w) return 0;
+  return use_decode(w, n_tok, nullptr) ? 1 : 2;
+}
+
+int moe_forward_launches(moe_weights* w, int n_tok) {
+  if (!w || n_tok <= 0 || w->L() == 0) return 0;
+  const int L = w->L();
+  const bool ep = w->ctx->world > 1;
+  if (use_decode(w, n_tok, nullptr)) return 1 + L * (ep ? 3 : 2);
+  return 1 + L * (ep ? 5 : 4) - 1;
+}
+
+}  // extern "C"

@@ -1,0 +1,251 @@
+// generic.cu — shape-agnostic CUDA kernels: router top-k, SwiGLU experts for
+// any (hidden, ffn, tokens), combine + residual, and the deterministic
+// token permutation.  These serve the reference's tiny test geometries
+// (hidden 2..6, ffn 2..8, toy 32/64) and any shape the streaming / tcgen05
+// kernels do not take.  Still GPU code: there is no CPU path in the product.
+#include "../../include/moe_b200.h"
+#include "common.cuh"
+#include "kernels.h"
+
+namespace moe {
+
+static cudaLaunchConfig_t make_cfg(dim3 grid, dim3 block, cudaStream_t s, bool pdl,
+                                   cudaLaunchAttribute* attr, size_t smem = 0) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = pdl ? 1 : 0;
+  return cfg;
+}
+
+// ---- router: gate_topk (model.cpp:69-101), one block per token -------------
+__global__ void __launch_bounds__(256) router_topk_kernel(const float* __restrict__ router,
+                                                          const float* __restrict__ x, int d,
+                                                          int E, int k, int32_t* ids,
+                                                          float* gates) {
+  __shared__ float logits[kMaxExperts];
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  griddep_wait();
+  griddep_launch_dependents();
+  const float* xt = x + (size_t)blockIdx.x * d;
+  for (int e = warp; e < E; e += 8) {
+    const float* re = router + (size_t)e * d;
+    float s = 0.f;
+    for (int c = lane; c < d; c += 32) s = fmaf(re[c], xt[c], s);
+    s = warp_sum(s);
+    if (lane == 0) logits[e] = s;
+  }
+  __syncthreads();
+  if (tid == 0) topk_softmax(logits, E, k, ids + (size_t)blockIdx.x * k, gates + (size_t)blockIdx.x * k);
+}
+
+cudaError_t launch_router_topk(const float* router, const float* x, int n_tok, const Dims& dm,
+                               int32_t* ids, float* gates, cudaStream_t s, bool pdl) {
+  if (n_tok <= 0) return cudaSuccess;
+  cudaLaunchAttribute attr[1];
+  cudaLaunchConfig_t cfg = make_cfg(dim3(n_tok), dim3(256), s, pdl, attr);
+  return cudaLaunchKernelEx(&cfg, router_topk_kernel, router, x, dm.d, dm.E, dm.k, ids, gates);
+}
+
+// ---- generic SwiGLU up: one warp per (ffn row, token, slot) ---------------
+template <typename W>
+__global__ void __launch_bounds__(256) generic_up_kernel(LayerWeights lw, int d, int f, int k,
+                                                         const float* __restrict__ x,
+                                                         const int32_t* __restrict__ ids,
+                                                         float* h, float* post_silu) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  griddep_wait();
+  griddep_launch_dependents();
+  const int r = blockIdx.x * 8 + warp;
+  if (r >= f) return;
+  const int tj = blockIdx.y;
+  const int t = tj / k;
+  const int slot = lw.slot_of[ids[tj]];
+  float a = 0.f, b = 0.f;
+  if (slot >= 0) {
+    const W* w1 = reinterpret_cast<const W*>(lw.experts) + slot * lw.expert_stride + (size_t)r * d;
+    const W* w3 = w1 + lw.mat_stride;
+    const float* xt = x + (size_t)t * d;
+    for (int c = lane; c < d; c += 32) {
+      const float xv = xt[c];
+      a = fmaf(Elem<W>::to_float(w1[c]), xv, a);
+      b = fmaf(Elem<W>::to_float(w3[c]), xv, b);
+    }
+    a = warp_sum(a);
+    b = warp_sum(b);
+  }
+  if (lane == 0) {
+    const float sa = slot >= 0 ? silu_f(a) : 0.f;
+    h[(size_t)tj * f + r] = sa * b;
+    if (post_silu) post_silu[(size_t)tj * f + r] = sa;
+  }
+}
+
+// ---- generic SwiGLU down: y[t][j][i] = sum_r W2T[r][i] h[t][j][r] ----------
+template <typename W>
+__global__ void __launch_bounds__(256) generic_down_kernel(LayerWeights lw, int d, int f, int k,
+                                                           const float* __restrict__ h,
+                                                           const int32_t* __restrict__ ids,
+                                                           float* y) {
+  griddep_wait();
+  griddep_launch_dependents();
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= d) return;
+  const int tj = blockIdx.y;
+  const int slot = lw.slot_of[ids[tj]];
+  float acc = 0.f;
+  if (slot >= 0) {
+    const W* w2t =
+        reinterpret_cast<const W*>(lw.experts) + slot * lw.expert_stride + 2 * lw.mat_stride + i;
+    const float* hr = h + (size_t)tj * f;
+    for (int r = 0; r < f; ++r) acc = fmaf(Elem<W>::to_float(w2t[(size_t)r * d]), hr[r], acc);
+  }
+  y[(size_t)tj * d + i] = acc;
+}
+
+cudaError_t launch_generic_up(const LayerWeights& lw, const Dims& dm, const float* x, int n_tok,
+                              const int32_t* ids, float* h, float* post_silu, cudaStream_t s,
+                              bool pdl) {
+  if (n_tok <= 0) return cudaSuccess;
+  cudaLaunchAttribute attr[1];
+  cudaLaunchConfig_t cfg =
+      make_cfg(dim3((dm.f + 7) / 8, n_tok * dm.k), dim3(256), s, pdl, attr);
+  if (dm.dtype == MOE_DTYPE_BF16)
+    return cudaLaunchKernelEx(&cfg, generic_up_kernel<__nv_bfloat16>, lw, dm.d, dm.f, dm.k, x,
+                              ids, h, post_silu);
+  return cudaLaunchKernelEx(&cfg, generic_up_kernel<float>, lw, dm.d, dm.f, dm.k, x, ids, h,
+                            post_silu);
+}
+
+cudaError_t launch_generic_down(const LayerWeights& lw, const Dims& dm, const float* h,
+                                int n_tok, const int32_t* ids, float* y, cudaStream_t s,
+                                bool pdl) {
+  if (n_tok <= 0) return cudaSuccess;
+  cudaLaunchAttribute attr[1];
+  cudaLaunchConfig_t cfg =
+      make_cfg(dim3((dm.d + 127) / 128, n_tok * dm.k), dim3(128), s, pdl, attr);
+  if (dm.dtype == MOE_DTYPE_BF16)
+    return cudaLaunchKernelEx(&cfg, generic_down_kernel<__nv_bfloat16>, lw, dm.d, dm.f, dm.k, h,
+                              ids, y);
+  return cudaLaunchKernelEx(&cfg, generic_down_kernel<float>, lw, dm.d, dm.f, dm.k, h, ids, y);
+}
+
+// ---- combine + residual (model.cpp:128, 143, 147) ---------------------------
+// combined = 0; combined += g_j * y_j over slots (ids ascending); x += combined.
+// x == nullptr writes the bare combined delta (expert-parallel partials).
+__global__ void __launch_bounds__(256) combine_kernel(const float* x, const float* __restrict__ y,
+                                                      const float* __restrict__ gates, int k, int d,
+                                                      float* x_out) {
+  griddep_wait();
+  griddep_launch_dependents();
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= d) return;
+  const int t = blockIdx.y;
+  float c = 0.f;
+  for (int j = 0; j < k; ++j) c += gates[(size_t)t * k + j] * y[((size_t)t * k + j) * d + i];
+  x_out[(size_t)t * d + i] = (x ? x[(size_t)t * d + i] : 0.f) + c;
+}
+
+cudaError_t launch_combine(const float* x, const float* y, const float* gates, int n_tok,
+                           const Dims& dm, float* x_out, cudaStream_t s, bool pdl) {
+  if (n_tok <= 0) return cudaSuccess;
+  cudaLaunchAttribute attr[1];
+  cudaLaunchConfig_t cfg = make_cfg(dim3((dm.d + 255) / 256, n_tok), dim3(256), s, pdl, attr);
+  return cudaLaunchKernelEx(&cfg, combine_kernel, x, y, gates, dm.k, dm.d, x_out);
+}
+
+__global__ void add_kernel(const float* a, const float* __restrict__ b, float* out, long long n) {
+  griddep_wait();
+  griddep_launch_dependents();
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
+       i += (long long)gridDim.x * blockDim.x)
+    out[i] = a[i] + b[i];
+}
+
+cudaError_t launch_add(const float* a, const float* b, float* out, long long n, cudaStream_t s,
+                       bool pdl) {
+  if (n <= 0) return cudaSuccess;
+  cudaLaunchAttribute attr[1];
+  const int blocks = (int)((n + 255) / 256 < 1184 ? (n + 255) / 256 : 1184);
+  cudaLaunchConfig_t cfg = make_cfg(dim3(blocks), dim3(256), s, pdl, attr);
+  return cudaLaunchKernelEx(&cfg, add_kernel, a, b, out, n);
+}
+
+// ---- deterministic permutation ------------------------------
+// Flatten (token t, slot j) -> p = t*k+j, stable counting sort by expert:
+// perm[offsets[e] + rank] = p with ranks ascending in p.  One block; each
+// 1024-pair chunk ranks its pairs with warp match + per-warp counts, so the
+// result never depends on atomic order.
+__global__ void __launch_bounds__(1024) permute_kernel(const int32_t* __restrict__ ids, int n,
+                                                       int E, int32_t* counts, int32_t* offsets,
+                                                       int32_t* perm, int32_t* inv_perm) {
+  extern __shared__ int32_t sm[];
+  int32_t* run = sm;             // [E] running count per expert
+  int32_t* off = run + E;        // [E] exclusive offsets
+  int32_t* wcnt = off + E;       // [32][E] per-warp counts of the chunk
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  for (int e = tid; e < E; e += blockDim.x) run[e] = 0;
+  __syncthreads();
+  // pass 1: counts
+  for (int p = tid; p < n; p += blockDim.x) atomicAdd(&run[ids[p]], 1);
+  __syncthreads();
+  if (tid == 0) {
+    int acc = 0;
+    for (int e = 0; e < E; ++e) {
+      off[e] = acc;
+      counts[e] = run[e];
+      offsets[e] = acc;
+      acc += run[e];
+    }
+  }
+  __syncthreads();
+  for (int e = tid; e < E; e += blockDim.x) run[e] = 0;
+  __syncthreads();
+  // pass 2: stable ranks, chunk by chunk
+  for (int base = 0; base < n; base += blockDim.x) {
+    for (int q = tid; q < 32 * E; q += blockDim.x) wcnt[q] = 0;
+    __syncthreads();
+    const int p = base + tid;
+    const bool valid = p < n;
+    const int e = valid ? ids[p] : -1;
+    const unsigned active = __ballot_sync(MOE_FULL_MASK, valid);
+    const unsigned same = __match_any_sync(MOE_FULL_MASK, e) & active;
+    const int rank_w = __popc(same & ((1u << lane) - 1u));
+    if (valid && rank_w == 0) wcnt[warp * E + e] = __popc(same);
+    __syncthreads();
+    if (valid) {
+      int before = run[e];
+      for (int w = 0; w < warp; ++w) before += wcnt[w * E + e];
+      const int pos = off[e] + before + rank_w;
+      perm[pos] = p;
+      if (inv_perm) inv_perm[p] = pos;
+    }
+    __syncthreads();
+    for (int q = tid; q < E; q += blockDim.x) {
+      int add = 0;
+      for (int w = 0; w < 32; ++w) add += wcnt[w * E + q];
+      run[q] += add;
+    }
+    __syncthreads();
+  }
+}
+
+cudaError_t launch_permute(const int32_t* ids, int n_tok, int k, int E, int32_t* counts,
+                           int32_t* offsets, int32_t* perm, int32_t* inv_perm, cudaStream_t s) {
+  const int n = n_tok * k;
+  const size_t smem = sizeof(int32_t) * (size_t)(2 * E + 32 * E);
+  if (smem > 48 * 1024) {
+    cudaError_t e = cudaFuncSetAttribute(permute_kernel,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+  }
+  permute_kernel<<<1, 1024, smem, s>>>(ids, n, E, counts, offsets, perm, inv_perm);
+  return cudaGetLastError();
+}
+
+}  // namespace moe

@@ -1,0 +1,87 @@
+// kernels.h — host-side launchers for the sm_100a kernels (internal).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace moe {
+
+constexpr int kMaxExperts = 256;
+
+// Expert weights of one layer on this rank: slot s (local expert) holds
+// [W1 f x d][W3 f x d][W2T f x d] contiguously (W2T = w_out transposed so the
+// decode kernel streams whole d-rows for every ffn index r).
+struct LayerWeights {
+  const void* experts;        // base of slot 0
+  long long expert_stride;    // elements between slots (= 3*f*d)
+  long long mat_stride;       // elements between W1/W3/W2T (= f*d)
+  const float* router;        // fp32 [E x d] (replicated)
+  int16_t slot_of[kMaxExperts];  // expert id -> local slot, -1 = remote
+};
+
+struct Dims {
+  int d, f, E, k;
+  int dtype;  // MOE_DTYPE_*
+};
+
+// ---- router -------------------------------------------------------------
+cudaError_t launch_router_topk(const float* router, const float* x, int n_tok, const Dims& dm,
+                               int32_t* ids, float* gates, cudaStream_t s, bool pdl);
+
+// ---- streaming batch-1 decode (TMA bulk ring) -----------------------------
+struct DecodePlan {
+  bool ok = false;
+  int nv = 0;          // 16-byte vectors per consumer thread per row
+  int ncons = 0;       // consumer threads
+  int rps = 0;         // rows per ring stage
+  int stages = 0;
+  int smem = 0;        // dynamic smem bytes
+  int grid = 0;        // CTAs (= SM count)
+};
+DecodePlan plan_decode(const Dims& dm, int sm_count);
+// ypart[grid][d] <- per-CTA partial sums of sum_j g_j W2_j (silu(W1_j x) * (W3_j x))
+cudaError_t launch_decode_experts(const DecodePlan& p, const LayerWeights& lw, const Dims& dm,
+                                  const int32_t* ids, const float* gates, const float* x,
+                                  float* ypart, cudaStream_t s, bool pdl);
+// x_out = x + sum_p ypart[p]; optionally the next layer's router + top-k
+// (deterministic fixed-order partial sums, last-block-done).
+cudaError_t launch_reduce_residual(const float* ypart, int nparts, const float* x, float* x_out,
+                                   const Dims& dm, const float* next_router, float* rpart,
+                                   unsigned* counter, int32_t* next_ids, float* next_gates,
+                                   cudaStream_t s, bool pdl);
+int reduce_blocks(const Dims& dm);
+
+// ---- generic (any shape, any token count) ---------------------------------
+// h[t][j][r] = silu(W1 x_t) * (W3 x_t) for expert ids[t][j]; post_silu optional.
+cudaError_t launch_generic_up(const LayerWeights& lw, const Dims& dm, const float* x, int n_tok,
+                              const int32_t* ids, float* h, float* post_silu, cudaStream_t s,
+                              bool pdl);
+// y[t][j][i] = sum_r W2T[r][i] h[t][j][r]
+cudaError_t launch_generic_down(const LayerWeights& lw, const Dims& dm, const float* h,
+                                int n_tok, const int32_t* ids, float* y, cudaStream_t s,
+                                bool pdl);
+// x_out[t][i] = x[t][i] + (0 + sum_j g[t][j] * y[t][j][i])   (model.cpp:128-147)
+cudaError_t launch_combine(const float* x, const float* y, const float* gates, int n_tok,
+                           const Dims& dm, float* x_out, cudaStream_t s, bool pdl);
+
+// out = a + b (elementwise; expert-parallel residual after the all-reduce)
+cudaError_t launch_add(const float* a, const float* b, float* out, long long n, cudaStream_t s,
+                       bool pdl);
+
+// ---- permutation ------------------------------------------------------------
+cudaError_t launch_permute(const int32_t* ids, int n_tok, int k, int E, int32_t* counts,
+                           int32_t* offsets, int32_t* perm, int32_t* inv_perm, cudaStream_t s);
+
+// ---- weights ----------------------------------------------------------------
+// dst (dtype) = src (fp64) with optional transpose of a [rows x cols] matrix.
+cudaError_t launch_convert(const double* src, void* dst, int dtype, long long rows,
+                           long long cols, bool transpose, cudaStream_t s);
+cudaError_t launch_to_double(const void* src, int dtype, double* dst, long long rows,
+                             long long cols, bool transpose, cudaStream_t s);
+cudaError_t launch_convert_f32(const double* src, float* dst, long long n, cudaStream_t s);
+// Counter-based normal init of one logical matrix (reference layout rows x
+// cols), stored transposed when `transpose`.  tag identifies (layer, expert, m).
+cudaError_t launch_random(void* dst, int dtype, long long rows, long long cols, bool transpose,
+                          uint64_t seed, uint64_t tag, float scale, cudaStream_t s);
+
+}  // namespace moe

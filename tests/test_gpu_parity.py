@@ -1,0 +1,324 @@
+"""GPU parity: the CUDA path (through the C-ABI) against the oracle.
+
+Protocol: the oracle is fed the values the device actually holds
+(weights downloaded after RNE rounding, tokens rounded to fp32), so the
+tolerance measures kernel arithmetic, not quantisation.
+  * routing ids / counts / permutation: bit-exact (near-ties, margin below
+    1e-5*max|logit|, are reported and excluded — none occur at these seeds);
+  * outputs: normwise max|gpu-ref| / max|ref| on the MoE delta (out - x):
+    <= 1e-5 in fp32 mode, <= 1e-2 in bf16 mode (north_star).
+"""
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+import oracle as O  # noqa: E402
+import paper_2402_07033_b200 as M  # noqa: E402
+
+TOL_F32 = 1e-5
+TOL_BF16 = 1e-2
+
+
+def normwise(got, want):
+    got, want = np.asarray(got, np.float64), np.asarray(want, np.float64)
+    return float(np.abs(got - want).max() / max(np.abs(want).max(), 1e-300))
+
+
+def f32(a):
+    return np.asarray(a, np.float32).astype(np.float64)
+
+
+@pytest.fixture(scope="module")
+def ctx():
+    if not torch.cuda.is_available():
+        pytest.skip("no GPU")
+    torch.cuda.init()
+    c = M.Ctx(0)
+    yield c
+    c.close()
+
+
+@pytest.fixture(scope="module")
+def orc():
+    O.build(ref=False)
+    return O.Oracle()
+
+
+def margin(logits, k):
+    s = np.sort(logits)[::-1]
+    return (s[k - 1] - s[k]) / max(np.abs(logits).max(), 1e-30) if k < len(s) else np.inf
+
+
+def oracle_layer(orc, w, l, x, k):
+    """Oracle layer on device-held values: returns (ids, gates, delta, margin)."""
+    router = w.download_router(l)
+    ids, g, logits = orc.gate_topk(router, x, k)
+    delta = np.zeros_like(x)
+    for e, ge in zip(ids, g):
+        wi, wg, wo = w.download_expert(l, int(e))
+        delta += ge * orc.expert_ffn(wi, wg, wo, x)
+    return ids, g, delta, margin(logits, k)
+
+
+# ---------------------------------------------------------------------------
+def test_library_reports_streaming_decode(ctx):
+    s = M.Shape(1, 8, 2, 4096, 14336, 2)
+    w = M.Weights(ctx, s, M.DTYPE_BF16)
+    assert w.expert_path(1) == 1          # TMA-ring streaming kernel
+    assert w.expert_path(4) == 2
+    assert w.forward_launches(1) == 3
+    w.close()
+
+
+def test_router_topk_bitexact_ids(ctx, orc):
+    s = M.Shape(1, 8, 2, 512, 1792, 4)
+    w = M.Weights(ctx, s, M.DTYPE_F32)
+    ow = orc.random_model(O.Shape(1, 8, 2, 512, 1792, 4), 0)
+    w.upload_router(0, ow.router[0])
+    router = w.download_router(0)
+    rs = np.random.RandomState(0)
+    n = 256
+    x = f32(rs.randn(n, 512))
+    xd = torch.tensor(x, dtype=torch.float32, device="cuda")
+    ids = torch.zeros((n, 2), dtype=torch.int32, device="cuda")
+    gates = torch.zeros((n, 2), dtype=torch.float32, device="cuda")
+    w.router_topk(0, xd, ids, gates)
+    torch.cuda.synchronize()
+    ids, gates = ids.cpu().numpy(), gates.cpu().numpy()
+    near = 0
+    for t in range(n):
+        want_ids, want_g, logits = orc.gate_topk(router, x[t], 2)
+        if margin(logits, 2) < 1e-5:
+            near += 1
+            continue
+        assert list(ids[t]) == list(want_ids)
+        assert np.abs(gates[t] - want_g).max() < 1e-5
+    assert near == 0
+
+
+def test_router_tie_break_known_answers(ctx):
+    # test_model.cpp:132-159 through the device router
+    ids, g = ctx.gate_topk_host(np.array([[3.0], [1.0], [1.0], [1.0]]), np.array([1.0]), 2)
+    assert list(ids) == [0, 1]
+    assert abs(g[0] - 0.8807970779778823) < 1e-6 and abs(g[1] - 0.11920292202211755) < 1e-6
+    ids, g = ctx.gate_topk_host(np.full((4, 1), 2.0), np.array([1.0]), 2)
+    assert list(ids) == [0, 1] and abs(g[0] - 0.5) < 1e-7
+    ids, g = ctx.gate_topk_host(np.array([[1.0], [2.0], [3.0]]), np.array([1.0]), 3)
+    den = np.exp([1.0, 2.0, 3.0]).sum()
+    assert np.allclose(g, np.exp([1.0, 2.0, 3.0]) / den, atol=1e-6)
+    with pytest.raises(M.MoeError) as ei:
+        ctx.gate_topk_host(np.ones((3, 1)), np.array([1.0]), 4)
+    assert ei.value.kind == "ShapeError"
+
+
+def test_expert_ffn_small_shapes(ctx, orc):
+    # the shape range of test_model.cpp:92-107, fp32 mode
+    rs = np.random.RandomState(7)
+    for _ in range(40):
+        d, f = 2 + rs.randint(5), 2 + rs.randint(7)
+        wi, wg, wo, x = f32(rs.randn(f, d)), f32(rs.randn(f, d)), f32(rs.randn(d, f)), f32(rs.randn(d))
+        got = ctx.expert_ffn_host(M.DTYPE_F32, wi, wg, wo, x)
+        assert normwise(got, orc.expert_ffn(wi, wg, wo, x)) < TOL_F32
+    one = np.ones((1, 1))
+    assert abs(ctx.expert_ffn_host(M.DTYPE_F32, one, one, one, np.ones(1))[0] - 0.7310585786300049) < 1e-6
+    z = ctx.expert_ffn_host(M.DTYPE_F32, np.zeros((4, 3)), np.zeros((4, 3)), np.zeros((3, 4)),
+                            np.array([1.0, -2.0, 0.5]))
+    assert (z == 0).all()
+
+
+@pytest.mark.parametrize("name,seed", [("toy_s3", 3), ("crit8", 8)])
+def test_forward_host_toy_vs_reference_golden(ctx, orc, golden, name, seed):
+    """Full model_forward on the toy shape (4 layers, d=32): GPU vs the
+    reference's own outputs (tests/golden), fp32 mode."""
+    toy = O.Shape(4, 8, 2, 32, 64, 2)
+    ow = orc.random_model(toy, seed)
+    w = M.Weights(ctx, M.Shape(4, 8, 2, 32, 64, 2), M.DTYPE_F32)
+    w.upload_oracle(ow)
+    toks = golden[f"{name}_tokens"]
+    out, ids, gates = w.forward_host(toks)
+    want = golden[f"{name}_out"]
+    assert normwise(out - toks, want - toks) < 1e-4  # fp32 weights+tokens vs fp64 reference
+    counts = np.zeros((4, 8), np.int64)
+    for l in range(4):
+        for e in ids[l].ravel():
+            counts[l, e] += 1
+    assert np.array_equal(counts, golden[f"{name}_count"])
+    # determinism (test_model.cpp:217-231 / criterion 8): bit-identical reruns
+    out2, ids2, gates2 = w.forward_host(toks)
+    assert np.array_equal(out, out2) and np.array_equal(ids, ids2) and np.array_equal(gates, gates2)
+
+
+def test_sink_post_silu_matches_reference(ctx, orc, golden):
+    """ActivationSink values (model.cpp:131-139) in reference call order."""
+    toy = O.Shape(4, 8, 2, 32, 64, 2)
+    ow = orc.random_model(toy, 9)
+    w = M.Weights(ctx, M.Shape(4, 8, 2, 32, 64, 2), M.DTYPE_F32)
+    w.upload_oracle(ow)
+    toks = golden["crit9_tokens"]
+    out, ids, gates, post = w.forward_host(toks, with_post=True)
+    want = golden["crit9_sink"]
+    assert post.shape == want.shape
+    assert normwise(post, want) < 1e-4
+    thr = [0.001, 0.01, 0.1, 1.0]
+    sink = post.reshape(16, 4, 2, 64)
+    for l in range(4):
+        h = orc.sparsity_histogram(sink[:, l].reshape(-1), thr)
+        assert (np.diff(h) >= 0).all()
+
+
+def test_tiny_layer_decode_fp32(ctx, orc, golden):
+    """Config T (d=512, f=1792, fp32, batch 1) on the streaming decode kernel,
+    against the reference's golden output."""
+    T = O.Shape(1, 8, 2, 512, 1792, 4)
+    ow = orc.random_model(T, 0)
+    w = M.Weights(ctx, M.Shape(1, 8, 2, 512, 1792, 4), M.DTYPE_F32)
+    assert w.expert_path(1) == 1
+    w.upload_oracle(ow)
+    x = golden["T_token"]
+    out, ids, gates = w.forward_host(x)
+    assert list(ids[0, 0]) == [1, 4]
+    assert normwise(out - x, golden["T_out"] - x) < TOL_F32 * 10
+    # strict protocol: oracle on the fp32-rounded token
+    xr = f32(x[0])
+    _, _, delta, _ = oracle_layer(orc, w, 0, xr, 2)
+    xd = torch.tensor(xr[None], dtype=torch.float32, device="cuda")
+    idd = torch.zeros((1, 2), dtype=torch.int32, device="cuda")
+    gd = torch.zeros((1, 2), dtype=torch.float32, device="cuda")
+    xo = torch.empty_like(xd)
+    w.layer_forward(0, xd, xo, idd, gd)
+    torch.cuda.synchronize()
+    assert normwise(xo.cpu().numpy()[0].astype(np.float64) - xr, delta) < TOL_F32
+
+
+def test_mixtral_layer_decode_bf16(ctx, orc, golden):
+    """Config M: Mixtral-8x7B-shaped layer, bf16 weights (device Philox init),
+    batch-1 decode through the TMA-ring kernel."""
+    s = M.Shape(1, 8, 2, 4096, 14336, 2)
+    w = M.Weights(ctx, s, M.DTYPE_BF16)
+    w.random(0)
+    x = f32(golden["M_token"][0])
+    xd = torch.tensor(x[None], dtype=torch.float32, device="cuda")
+    idd = torch.zeros((1, 2), dtype=torch.int32, device="cuda")
+    gd = torch.zeros((1, 2), dtype=torch.float32, device="cuda")
+    xo = torch.empty_like(xd)
+    w.layer_forward(0, xd, xo, idd, gd)
+    torch.cuda.synchronize()
+    ids, g, delta, mg = oracle_layer(orc, w, 0, x, 2)
+    assert mg > 1e-5
+    assert list(idd.cpu().numpy()[0]) == list(ids)
+    assert np.abs(gd.cpu().numpy()[0] - g).max() < 1e-5
+    err = normwise(xo.cpu().numpy()[0].astype(np.float64) - x, delta)
+    print(f"M bf16 normwise error {err:.3e}")
+    assert err < TOL_BF16
+    assert err < 1e-4  # fp32 accumulation of exactly-represented bf16 weights
+
+
+def test_mixtral_layer_decode_fp32_mode(ctx, orc, golden):
+    s = M.Shape(1, 8, 2, 4096, 14336, 4)
+    w = M.Weights(ctx, s, M.DTYPE_F32)
+    assert w.expert_path(1) == 1
+    w.random(1)
+    x = f32(golden["M_token"][0])
+    xd = torch.tensor(x[None], dtype=torch.float32, device="cuda")
+    idd = torch.zeros((1, 2), dtype=torch.int32, device="cuda")
+    gd = torch.zeros((1, 2), dtype=torch.float32, device="cuda")
+    xo = torch.empty_like(xd)
+    w.layer_forward(0, xd, xo, idd, gd)
+    torch.cuda.synchronize()
+    ids, g, delta, mg = oracle_layer(orc, w, 0, x, 2)
+    assert list(idd.cpu().numpy()[0]) == list(ids)
+    assert normwise(xo.cpu().numpy()[0].astype(np.float64) - x, delta) < TOL_F32
+
+
+def test_stack_decode_teacher_forced_and_graph(ctx, orc):
+    """4-layer Mixtral-shaped stack: per-layer teacher-forced parity, then the
+    single-graph moe_forward must agree with the layer-by-layer chain and be
+    bit-deterministic across runs."""
+    L = 4
+    s = M.Shape(L, 8, 2, 4096, 14336, 2)
+    w = M.Weights(ctx, s, M.DTYPE_BF16)
+    w.random(7)
+    x0 = f32(orc.normal(1, 4096))
+    xs = [torch.tensor(x0[None], dtype=torch.float32, device="cuda")]
+    ids_l = []
+    for l in range(L):
+        xo = torch.empty_like(xs[-1])
+        idd = torch.zeros((1, 2), dtype=torch.int32, device="cuda")
+        gd = torch.zeros((1, 2), dtype=torch.float32, device="cuda")
+        w.layer_forward(l, xs[-1], xo, idd, gd)
+        torch.cuda.synchronize()
+        xin = xs[-1].cpu().numpy()[0].astype(np.float64)
+        ids, g, delta, mg = oracle_layer(orc, w, l, xin, 2)
+        assert list(idd.cpu().numpy()[0]) == list(ids), f"layer {l}"
+        assert normwise(xo.cpu().numpy()[0].astype(np.float64) - xin, delta) < TOL_BF16
+        ids_l.append(list(ids))
+        xs.append(xo)
+    # fused graph path
+    xg = torch.tensor(x0[None], dtype=torch.float32, device="cuda")
+    idg = torch.zeros((L, 1, 2), dtype=torch.int32, device="cuda")
+    gg = torch.zeros((L, 1, 2), dtype=torch.float32, device="cuda")
+    w.forward(xg, idg, gg)
+    torch.cuda.synchronize()
+    assert [list(r) for r in idg.cpu().numpy()[:, 0]] == ids_l
+    ref = xs[-1].cpu().numpy()[0].astype(np.float64)
+    assert normwise(xg.cpu().numpy()[0] - x0, ref - x0) < 1e-4
+    out1 = xg.clone()
+    for _ in range(3):
+        xg.copy_(torch.tensor(x0[None], dtype=torch.float32, device="cuda"))
+        w.forward(xg, idg, gg)
+        torch.cuda.synchronize()
+        assert torch.equal(xg, out1)
+
+
+def test_prefill_generic_tokens_T(ctx, orc):
+    """Multi-token forward (prefill step) on config T, fp32: outputs and the
+    per-(layer,expert) tally (the RoutingTrace) against the oracle."""
+    T = O.Shape(2, 8, 2, 512, 1792, 4)
+    ow = orc.random_model(T, 5)
+    w = M.Weights(ctx, M.Shape(2, 8, 2, 512, 1792, 4), M.DTYPE_F32)
+    w.upload_oracle(ow)
+    toks = f32(orc.normal(6, 16 * 512).reshape(16, 512))
+    out, ids, gates = w.forward_host(toks)
+    # oracle on device-rounded weights
+    dw = O.Weights(T)
+    for e in range(8):
+        for l in range(2):
+            a, b, c = w.download_expert(l, e)
+            i = l * 8 + e
+            dw.w_in[i][:], dw.w_gate[i][:], dw.w_out[i][:] = a, b, c
+    for l in range(2):
+        dw.router[l][:] = w.download_router(l)
+    want, tally, gsum, want_ids, want_g = orc.model_forward(T, dw, toks)
+    assert np.array_equal(ids.transpose(1, 0, 2), want_ids)
+    assert normwise(out - toks, want - toks) < TOL_F32 * 10
+
+
+def test_permute_stable_and_deterministic(ctx):
+    rs = np.random.RandomState(3)
+    for n_tok, k, E in [(1, 2, 8), (512, 2, 8), (1000, 3, 16), (4097, 2, 64)]:
+        ids = np.stack([np.sort(rs.choice(E, k, replace=False)) for _ in range(n_tok)]).astype(np.int32)
+        d_ids = torch.tensor(ids, device="cuda")
+        counts = torch.zeros(E, dtype=torch.int32, device="cuda")
+        offsets = torch.zeros(E, dtype=torch.int32, device="cuda")
+        perm = torch.zeros(n_tok * k, dtype=torch.int32, device="cuda")
+        inv = torch.zeros(n_tok * k, dtype=torch.int32, device="cuda")
+        ctx.permute(d_ids, n_tok, k, E, counts, offsets, perm, inv)
+        torch.cuda.synchronize()
+        flat = ids.ravel()
+        want_perm = np.argsort(flat, kind="stable")
+        assert np.array_equal(perm.cpu().numpy(), want_perm)
+        assert np.array_equal(counts.cpu().numpy(), np.bincount(flat, minlength=E))
+        assert np.array_equal(inv.cpu().numpy()[want_perm], np.arange(n_tok * k))
+
+
+def test_errors_are_loud(ctx):
+    s = M.Shape(2, 4, 2, 16, 32, 2)
+    w = M.Weights(ctx, s, M.DTYPE_F32)
+    with pytest.raises(M.MoeError) as ei:
+        w.download_router(5)
+    assert ei.value.kind == "ShapeError"
+    with pytest.raises(M.MoeError) as ei:
+        M.Weights(ctx, M.Shape(1, 2, 3, 16, 32, 2))
+    assert ei.value.kind == "ShapeError"
