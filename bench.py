@@ -284,6 +284,8 @@ def run_ours(args):
             "config": {"workload": WORKLOAD_NAME[args.config], "layers": L, "experts": E, "top_k": k,
                        "hidden": d, "ffn": f, "batch": 1,
                        "parallelism": f"ep{world}" if world > 1 else "single-gpu",
+                       "path": "persistent stack kernel (1 launch/token)" if w.forward_launches(1) == 1
+                       else f"per-layer kernels ({w.forward_launches(1)} launches/token, CUDA graph + PDL)",
                        "l2": f"inputs larger than L2: {L * k * 3 * d * f * esz / 1e9:.1f} GB of expert weights streamed per step"},
             "gpu_launches": launches, "clocks": clk.summary(), "e2e": e2e, "roofline": roof,
             "cpu_baseline": cpu,
@@ -384,7 +386,7 @@ def run_reference(args):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--steps", type=int, default=300)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default="stack32", choices=sorted(CONFIGS))
@@ -392,6 +394,8 @@ def main():
     ap.add_argument("--cpu-tokens", type=int, default=12)
     ap.add_argument("--ref-threads", type=int, default=0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-stack", action="store_true",
+                    help="per-layer 2-kernel graph instead of the persistent stack kernel")
     ap.add_argument("--traffic", type=float, default=None,
                     help="dram bytes per launch of the decode kernel from an ncu --set full capture")
     args = ap.parse_args()
@@ -400,6 +404,8 @@ def main():
         tp = os.path.join(ROOT, "profiles", "decode_traffic.json")
         if os.path.exists(tp):
             args.traffic = json.load(open(tp)).get("dram_bytes_per_launch")
+    if args.no_stack:
+        os.environ["MOE_B200_STACK"] = "0"
     if args.impl == "reference":
         run_reference(args)
     else:

@@ -136,6 +136,8 @@ struct moe_weights {
   moe::DecodePlan plan;
   // scratch
   DevBuf ypart, rpart, counter, xa, xb, xin, h, y, delta, ids, gates, post;
+  DevBuf xbuf2, gbar, dev_layers, dev_slots;  // persistent stack kernel
+  bool stack_enabled = true;
   DevBuf stage_d;  // fp64 staging for uploads / downloads
   void* host_pin = nullptr;
   size_t host_pin_bytes = 0;
@@ -186,8 +188,29 @@ int set_device(moe_ctx* c) {
   return MOE_OK;
 }
 
-// Per-call scratch sized for n_tok tokens.
+void drop_graphs(moe_weights* w) {
+  for (auto& kv : w->graphs)
+    if (kv.second.exec) cudaGraphExecDestroy(kv.second.exec);
+  w->graphs.clear();
+}
+
+int ensure_scratch_impl(moe_weights* w, int n_tok);
+
+// Per-call scratch sized for n_tok tokens; captured graphs hold scratch
+// pointers, so any reallocation invalidates them.
 int ensure_scratch(moe_weights* w, int n_tok) {
+  const void* before[] = {w->xa.p, w->xb.p, w->delta.p, w->ypart.p, w->rpart.p, w->counter.p};
+  TRY(ensure_scratch_impl(w, n_tok));
+  const void* after[] = {w->xa.p, w->xb.p, w->delta.p, w->ypart.p, w->rpart.p, w->counter.p};
+  for (int i = 0; i < 6; ++i)
+    if (before[i] != after[i]) {
+      drop_graphs(w);
+      break;
+    }
+  return MOE_OK;
+}
+
+int ensure_scratch_impl(moe_weights* w, int n_tok) {
   const size_t d = w->d(), f = w->f(), k = w->k(), L = std::max(1, w->L());
   const size_t n = std::max(1, n_tok);
   TRY(w->xa.ensure(n * d * 4));
@@ -196,7 +219,7 @@ int ensure_scratch(moe_weights* w, int n_tok) {
   TRY(w->xin.ensure(n * d * 4));
   TRY(w->ids.ensure(L * n * k * 4));
   TRY(w->gates.ensure(L * n * k * 4));
-  TRY(w->rpart.ensure((size_t)moe::reduce_blocks(w->dims()) * w->E() * 4));
+  TRY(w->rpart.ensure((size_t)std::max(w->ctx->sm_count, moe::reduce_blocks(w->dims())) * w->E() * 4));
   TRY(w->counter.ensure(64));
   TRY(w->ypart.ensure((size_t)std::max(1, w->ctx->sm_count) * d * 4));
   if (n_tok > 1 || !w->plan.ok) {
@@ -219,6 +242,25 @@ int allreduce(moe_weights* w, float* buf, size_t count, cudaStream_t s) {
 
 bool use_decode(const moe_weights* w, int n_tok, const float* post) {
   return n_tok == 1 && w->plan.ok && post == nullptr;
+}
+
+// Whole-token persistent kernel: single GPU (no exchange inside a layer).
+bool use_stack(const moe_weights* w, int n_tok) {
+  return use_decode(w, n_tok, nullptr) && w->ctx->world == 1 && w->stack_enabled && w->L() > 0;
+}
+
+int enqueue_stack(moe_weights* w, float* x, int32_t* ids, float* gates, cudaStream_t s) {
+  moe::StackDesc sd;
+  sd.layer_experts = w->dev_layers.as<const void* const>();
+  sd.slot_of = w->dev_slots.as<const int16_t>();
+  sd.expert_stride = 3 * w->mat_elems();
+  sd.mat_stride = w->mat_elems();
+  sd.router = w->router;
+  sd.L = w->L();
+  CU(moe::launch_decode_stack(w->plan, sd, w->dims(), x, w->xbuf2.as<float>(),
+                              w->ypart.as<float>(), w->rpart.as<float>(), ids, gates,
+                              w->gbar.as<unsigned>(), s));
+  return MOE_OK;
 }
 
 // Experts + combine + residual for one layer (x may alias x_out only on
@@ -290,7 +332,8 @@ int forward_graph(moe_weights* w, float* x, int32_t* ids, float* gates, cudaStre
   if (it == w->graphs.end()) {
     cudaGraph_t g = nullptr;
     CU(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal));
-    const int rc = enqueue_forward(w, x, 1, ids, gates, s, nullptr);
+    const int rc = use_stack(w, 1) ? enqueue_stack(w, x, ids, gates, s)
+                                   : enqueue_forward(w, x, 1, ids, gates, s, nullptr);
     cudaError_t e = cudaStreamEndCapture(s, &g);
     if (rc != MOE_OK) {
       if (g) cudaGraphDestroy(g);
@@ -461,6 +504,19 @@ int moe_weights_create(moe_ctx* c, const moe_shape* shape, int dtype, const int3
   cudaMemset(w->router, 0, rbytes);
   w->device_bytes += rbytes;
   w->plan = moe::plan_decode(w->dims(), c->sm_count);
+  if (const char* env = getenv("MOE_B200_STACK")) w->stack_enabled = env[0] != '0';
+  {
+    // device-side tables for the persistent stack kernel
+    const int Lm = std::max(1, L);
+    if (w->dev_layers.ensure(sizeof(void*) * Lm) || w->dev_slots.ensure(sizeof(int16_t) * Lm * E) ||
+        w->xbuf2.ensure(sizeof(float) * 2 * shape->hidden_dim) || w->gbar.ensure(64) ||
+        w->rpart.ensure(sizeof(float) * (size_t)std::max(c->sm_count, moe::reduce_blocks(w->dims())) * E))
+      return cleanup(fail(MOE_ERR_OOM, "cudaMalloc stack tables"));
+    if (L > 0 &&
+        (cudaMemcpy(w->dev_layers.p, w->layer_mem.data(), sizeof(void*) * L, cudaMemcpyHostToDevice) ||
+         cudaMemcpy(w->dev_slots.p, w->slot_of.data(), sizeof(int16_t) * L * E, cudaMemcpyHostToDevice)))
+      return cleanup(fail(MOE_ERR_CUDA, "upload stack tables"));
+  }
   *out = w;
   return MOE_OK;
 }
@@ -474,7 +530,8 @@ int moe_weights_destroy(moe_weights* w) {
     if (p) cudaFree(p);
   if (w->router) cudaFree(w->router);
   for (DevBuf* b : {&w->ypart, &w->rpart, &w->counter, &w->xa, &w->xb, &w->xin, &w->h, &w->y, &w->delta,
-                    &w->ids, &w->gates, &w->post, &w->stage_d})
+                    &w->ids, &w->gates, &w->post, &w->stage_d, &w->xbuf2, &w->gbar,
+                    &w->dev_layers, &w->dev_slots})
     b->release();
   if (w->host_pin) cudaFreeHost(w->host_pin);
   delete w;
@@ -811,6 +868,7 @@ int moe_forward_launches(moe_weights* w, int n_tok) {
   if (!w || n_tok <= 0 || w->L() == 0) return 0;
   const int L = w->L();
   const bool ep = w->ctx->world > 1;
+  if (use_stack(w, n_tok)) return 1;
   if (use_decode(w, n_tok, nullptr)) return 1 + L * (ep ? 3 : 2);
   return 1 + L * (ep ? 5 : 4) - 1;
 }

@@ -3,12 +3,12 @@
 // Replaces the reference's per-token expert loop (model.cpp:125-147:
 // gate_topk -> expert_ffn x k -> gate-weighted combine -> residual), whose
 // cost is matvec's inner loop (model.cpp:26).  At batch 1 the layer is a pure
-// weight stream (704.8 MB per Mixtral layer), so the kernel is
+// weight stream (704.8 MB per Mixtral layer), so the kernels are
 // built around HBM bandwidth:
 //
-//  * One persistent CTA per SM.  The k selected experts' ffn rows
-//    (k*f "rows", each = W1 row, W3 row, W2T row of d elements) are split
-//    evenly over the CTAs (split over ffn, not over hidden).
+//  * One CTA per SM.  The k selected experts' ffn rows (k*f "rows", each =
+//    W1 row, W3 row, W2T row of d elements) are split evenly over the CTAs
+//    (split over ffn, not over hidden).
 //  * A producer warp streams each CTA's rows into a shared-memory ring with
 //    1-D TMA bulk copies (cp.async.bulk, L2 evict_first) completing on
 //    mbarriers — ~190 KB in flight per SM, independent of register pressure.
@@ -17,10 +17,17 @@
 //    one cross-warp smem step, apply silu(a)*b*gate, then immediately AXPY
 //    the matching W2T rows into per-thread partial outputs.  h never leaves
 //    the SM; each CTA emits one partial d-vector.
-//  * reduce_residual_kernel sums the per-CTA partials in a fixed order
-//    (deterministic), adds the residual (model.cpp:147) and computes the next
-//    layer's router logits + top-k (model.cpp:69-101) with a last-block-done
-//    reduction, so a layer is 2 launches chained with PDL inside one graph.
+//
+// Two drivers share that core:
+//  * decode_experts_kernel + reduce_residual_kernel: one layer = 2 launches
+//    (PDL-chained); the reduce sums the per-CTA partials in a fixed order,
+//    adds the residual (model.cpp:147) and fuses the next layer's router +
+//    top-k (model.cpp:69-101) via last-block-done.  Used per layer and for
+//    expert parallelism (an NCCL all-reduce sits between the two).
+//  * decode_stack_kernel: the whole L-layer token in ONE persistent
+//    cooperative launch with two grid barriers per layer; routing of layer
+//    l+1 is computed redundantly by every CTA from per-CTA router partials,
+//    so the producer warps start streaming layer l+1 without another launch.
 #include <algorithm>
 
 #include "../../include/moe_b200.h"
@@ -30,145 +37,88 @@
 namespace moe {
 
 constexpr int kBatch = 16;      // ffn rows per up/down batch
-constexpr int kMaxSlots = 16;   // top_k limit of the streaming kernel
+constexpr int kMaxSlots = 16;   // top_k limit of the streaming kernels
 constexpr int kMaxConsWarps = 8;
 
-struct DecodeArgs {
-  LayerWeights lw;
-  const int32_t* ids;
-  const float* gates;
-  const float* x;
-  float* ypart;
-  int d, f, k;
-  int row_bytes, rps, stages, stage_bytes;
+// ---------------------------------------------------------------------------
+// shared streaming core
+struct Ring {
+  uint8_t* buf;
+  uint64_t* full;
+  uint64_t* empty;
+  int rps, stages, stage_bytes, row_bytes;
+};
+struct Cursor {
+  int slot = 0, stage = 0;
+  uint32_t phase = 0;
+  __device__ __forceinline__ void next_stage(int stages) {
+    slot = 0;
+    if (++stage == stages) {
+      stage = 0;
+      phase ^= 1;
+    }
+  }
 };
 
-template <typename W, int NV>
-__global__ void __launch_bounds__(kMaxConsWarps * 32 + 32, 1)
-    decode_experts_kernel(const __grid_constant__ DecodeArgs a) {
-  constexpr int VEC = Elem<W>::kVec;
-  extern __shared__ __align__(128) uint8_t smem[];
-  uint8_t* ring = smem;
-  uint64_t* full = reinterpret_cast<uint64_t*>(smem + (size_t)a.stages * a.stage_bytes);
-  uint64_t* empty = full + a.stages;
-  float* red = reinterpret_cast<float*>(empty + a.stages);  // [kMaxConsWarps][32]
-  float* h_s = red + kMaxConsWarps * 32;                      // [kBatch]
-  __shared__ int s_slot[kMaxSlots];
-  __shared__ float s_gate[kMaxSlots];
-  __shared__ int s_nloc;
-
-  const int ncons = blockDim.x - 32;
-  const int ncw = ncons >> 5;
-  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-
-  if (tid == 0) {
-    for (int s = 0; s < a.stages; ++s) {
-      mbar_init(&full[s], 1);
-      mbar_init(&empty[s], ncw);
-    }
-    fence_mbar_init();
-  }
-  __syncthreads();
-  griddep_wait();
-  griddep_launch_dependents();
-  if (tid == 0) {
-    int n = 0;
-    for (int j = 0; j < a.k; ++j) {
-      const int slot = a.lw.slot_of[a.ids[j]];
-      if (slot >= 0) {
-        s_slot[n] = slot;
-        s_gate[n] = a.gates[j];
-        ++n;
-      }
-    }
-    s_nloc = n;
-  }
-  __syncthreads();
-
-  const long long T = (long long)s_nloc * a.f;
-  const long long g0 = (long long)blockIdx.x * T / gridDim.x;
-  const long long g1 = (long long)(blockIdx.x + 1) * T / gridDim.x;
+// Producer: stream rows [g0, g1) of the layer (row g = slot j, ffn index r)
+// as [W1 rows | W3 rows | W2T rows] per batch of <= kBatch rows.
+template <typename W>
+__device__ __forceinline__ void produce_rows(const Ring& R, Cursor& cur, const W* wbase,
+                                             long long expert_stride, long long mat_stride,
+                                             const int* s_slot, int f, int d, long long g0,
+                                             long long g1, uint64_t pol) {
   const int total_vec = (int)(3 * (g1 - g0));
-  const W* wbase = reinterpret_cast<const W*>(a.lw.experts);
-
-  if (warp == ncw) {
-    // ===== producer: one lane streams the CTA's rows into the ring =====
-    if (lane == 0 && total_vec > 0) {
-      const uint64_t pol = l2_evict_first_policy();
-      int c_slot = 0, c_stage = 0, p = 0;
-      uint32_t c_phase = 0;
-      for (long long g = g0; g < g1;) {
-        const int jj = (int)(g / a.f);
-        const int r = (int)(g - (long long)jj * a.f);
-        const int nb = (int)min((long long)kBatch, min(g1 - g, (long long)(a.f - r)));
-        const W* eb = wbase + (long long)s_slot[jj] * a.lw.expert_stride;
-        for (int m = 0; m < 3; ++m) {
-          const W* src = eb + m * a.lw.mat_stride + (long long)r * a.d;
-          for (int q = 0; q < nb; ++q) {
-            if (c_slot == 0) {
-              mbar_wait(&empty[c_stage], c_phase ^ 1);
-              const int nvec = min(a.rps, total_vec - p);
-              mbar_arrive_expect_tx(&full[c_stage], (uint32_t)(nvec * a.row_bytes));
-            }
-            bulk_g2s(ring + (size_t)c_stage * a.stage_bytes + (size_t)c_slot * a.row_bytes,
-                     src + (long long)q * a.d, (uint32_t)a.row_bytes, &full[c_stage], pol);
-            ++p;
-            if (++c_slot == a.rps) {
-              c_slot = 0;
-              if (++c_stage == a.stages) {
-                c_stage = 0;
-                c_phase ^= 1;
-              }
-            }
-          }
+  int p = 0;
+  for (long long g = g0; g < g1;) {
+    const int jj = (int)(g / f);
+    const int r = (int)(g - (long long)jj * f);
+    const int nb = (int)min((long long)kBatch, min(g1 - g, (long long)(f - r)));
+    const W* eb = wbase + (long long)s_slot[jj] * expert_stride;
+    for (int m = 0; m < 3; ++m) {
+      const W* src = eb + m * mat_stride + (long long)r * d;
+      for (int q = 0; q < nb; ++q) {
+        if (cur.slot == 0) {
+          mbar_wait(&R.empty[cur.stage], cur.phase ^ 1);
+          const int nvec = min(R.rps, total_vec - p);
+          mbar_arrive_expect_tx(&R.full[cur.stage], (uint32_t)(nvec * R.row_bytes));
         }
-        g += nb;
+        bulk_g2s(R.buf + (size_t)cur.stage * R.stage_bytes + (size_t)cur.slot * R.row_bytes,
+                 src + (long long)q * d, (uint32_t)R.row_bytes, &R.full[cur.stage], pol);
+        ++p;
+        if (++cur.slot == R.rps) cur.next_stage(R.stages);
       }
     }
-    return;
+    g += nb;
   }
+  if (cur.slot != 0) cur.next_stage(R.stages);
+}
 
-  // ===== consumers =====
-  float xr[NV * VEC];
-#pragma unroll
-  for (int m = 0; m < NV; ++m) {
-    const float4* xp = reinterpret_cast<const float4*>(a.x + (size_t)(tid + m * ncons) * VEC);
-#pragma unroll
-    for (int v = 0; v < VEC / 4; ++v) {
-      const float4 t = xp[v];
-      xr[m * VEC + 4 * v + 0] = t.x;
-      xr[m * VEC + 4 * v + 1] = t.y;
-      xr[m * VEC + 4 * v + 2] = t.z;
-      xr[m * VEC + 4 * v + 3] = t.w;
-    }
-  }
-  float yacc[NV * VEC];
-#pragma unroll
-  for (int i = 0; i < NV * VEC; ++i) yacc[i] = 0.f;
-
-  int c_slot = 0, c_stage = 0, p = 0;
-  uint32_t c_phase = 0;
+// Consumers: accumulate yacc += sum over rows of gate*silu(W1 x)*(W3 x)*W2T.
+template <typename W, int NV>
+__device__ __forceinline__ void consume_rows(const Ring& R, Cursor& cur, const float* xr,
+                                             float* yacc, const float* s_gate, int f,
+                                             long long g0, long long g1, float* red, float* h_s,
+                                             int tid, int ncons, int bar_id) {
+  constexpr int VEC = Elem<W>::kVec;
+  const int warp = tid >> 5, lane = tid & 31, ncw = ncons >> 5;
+  const int total_vec = (int)(3 * (g1 - g0));
+  int p = 0;
   auto acquire = [&]() -> const uint8_t* {
-    if (c_slot == 0) mbar_wait(&full[c_stage], c_phase);
-    return ring + (size_t)c_stage * a.stage_bytes + (size_t)c_slot * a.row_bytes;
+    if (cur.slot == 0) mbar_wait(&R.full[cur.stage], cur.phase);
+    return R.buf + (size_t)cur.stage * R.stage_bytes + (size_t)cur.slot * R.row_bytes;
   };
   auto release = [&]() {
     ++p;
-    if (++c_slot == a.rps || p == total_vec) {
+    if (++cur.slot == R.rps || p == total_vec) {
       __syncwarp();
-      if (lane == 0) mbar_arrive(&empty[c_stage]);
-      c_slot = 0;
-      if (++c_stage == a.stages) {
-        c_stage = 0;
-        c_phase ^= 1;
-      }
+      if (lane == 0) mbar_arrive(&R.empty[cur.stage]);
+      cur.next_stage(R.stages);
     }
   };
-
   for (long long g = g0; g < g1;) {
-    const int jj = (int)(g / a.f);
-    const int r = (int)(g - (long long)jj * a.f);
-    const int nb = (int)min((long long)kBatch, min(g1 - g, (long long)(a.f - r)));
+    const int jj = (int)(g / f);
+    const int r = (int)(g - (long long)jj * f);
+    const int nb = (int)min((long long)kBatch, min(g1 - g, (long long)(f - r)));
     const float gate = s_gate[jj];
 
     // -- up: W1 rows [0,nb) then W3 rows [0,nb) of this batch
@@ -203,14 +153,14 @@ __global__ void __launch_bounds__(kMaxConsWarps * 32 + 32, 1)
       }
     }
     red[warp * 32 + lane] = acc[0];
-    named_bar_sync(1, ncons);
+    named_bar_sync(bar_id, ncons);
     if (warp == 0) {
       float tot = 0.f;
       for (int w = 0; w < ncw; ++w) tot += red[w * 32 + lane];
       const float b = __shfl_down_sync(MOE_FULL_MASK, tot, kBatch);
       if (lane < nb) h_s[lane] = gate * (silu_f(tot) * b);
     }
-    named_bar_sync(1, ncons);
+    named_bar_sync(bar_id, ncons);
 
     // -- down: W2T rows [0,nb): y += h[q] * W2T[r+q][:]
 #pragma unroll
@@ -231,8 +181,28 @@ __global__ void __launch_bounds__(kMaxConsWarps * 32 + 32, 1)
     }
     g += nb;
   }
+}
 
-  float* out = a.ypart + (size_t)blockIdx.x * a.d;
+template <typename W, int NV>
+__device__ __forceinline__ void load_x(const float* x, float* xr, int tid, int ncons) {
+  constexpr int VEC = Elem<W>::kVec;
+#pragma unroll
+  for (int m = 0; m < NV; ++m) {
+    const float4* xp = reinterpret_cast<const float4*>(x + (size_t)(tid + m * ncons) * VEC);
+#pragma unroll
+    for (int v = 0; v < VEC / 4; ++v) {
+      const float4 t = __ldcg(xp + v);
+      xr[m * VEC + 4 * v + 0] = t.x;
+      xr[m * VEC + 4 * v + 1] = t.y;
+      xr[m * VEC + 4 * v + 2] = t.z;
+      xr[m * VEC + 4 * v + 3] = t.w;
+    }
+  }
+}
+
+template <typename W, int NV>
+__device__ __forceinline__ void store_y(float* out, const float* yacc, int tid, int ncons) {
+  constexpr int VEC = Elem<W>::kVec;
 #pragma unroll
   for (int m = 0; m < NV; ++m) {
     float4* op = reinterpret_cast<float4*>(out + (size_t)(tid + m * ncons) * VEC);
@@ -241,6 +211,84 @@ __global__ void __launch_bounds__(kMaxConsWarps * 32 + 32, 1)
       op[v] = make_float4(yacc[m * VEC + 4 * v], yacc[m * VEC + 4 * v + 1],
                           yacc[m * VEC + 4 * v + 2], yacc[m * VEC + 4 * v + 3]);
   }
+}
+
+// ---------------------------------------------------------------------------
+// per-layer kernel
+struct DecodeArgs {
+  LayerWeights lw;
+  const int32_t* ids;
+  const float* gates;
+  const float* x;
+  float* ypart;
+  int d, f, k;
+  int row_bytes, rps, stages, stage_bytes;
+};
+
+template <typename W, int NV>
+__global__ void __launch_bounds__(kMaxConsWarps * 32 + 32, 1)
+    decode_experts_kernel(const __grid_constant__ DecodeArgs a) {
+  constexpr int VEC = Elem<W>::kVec;
+  extern __shared__ __align__(128) uint8_t smem[];
+  Ring R;
+  R.buf = smem;
+  R.full = reinterpret_cast<uint64_t*>(smem + (size_t)a.stages * a.stage_bytes);
+  R.empty = R.full + a.stages;
+  R.rps = a.rps;
+  R.stages = a.stages;
+  R.stage_bytes = a.stage_bytes;
+  R.row_bytes = a.row_bytes;
+  __shared__ float red[kMaxConsWarps * 32];
+  __shared__ float h_s[kBatch];
+  __shared__ int s_slot[kMaxSlots];
+  __shared__ float s_gate[kMaxSlots];
+  __shared__ int s_nloc;
+
+  const int ncons = blockDim.x - 32;
+  const int ncw = ncons >> 5;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+
+  if (tid == 0) {
+    for (int s = 0; s < a.stages; ++s) {
+      mbar_init(&R.full[s], 1);
+      mbar_init(&R.empty[s], ncw);
+    }
+    fence_mbar_init();
+  }
+  __syncthreads();
+  griddep_wait();
+  griddep_launch_dependents();
+  if (tid == 0) {
+    int n = 0;
+    for (int j = 0; j < a.k; ++j) {
+      const int slot = a.lw.slot_of[a.ids[j]];
+      if (slot >= 0) {
+        s_slot[n] = slot;
+        s_gate[n] = a.gates[j];
+        ++n;
+      }
+    }
+    s_nloc = n;
+  }
+  __syncthreads();
+
+  const long long T = (long long)s_nloc * a.f;
+  const long long g0 = (long long)blockIdx.x * T / gridDim.x;
+  const long long g1 = (long long)(blockIdx.x + 1) * T / gridDim.x;
+  Cursor cur;
+  if (warp == ncw) {
+    if (lane == 0 && g1 > g0)
+      produce_rows<W>(R, cur, reinterpret_cast<const W*>(a.lw.experts), a.lw.expert_stride,
+                      a.lw.mat_stride, s_slot, a.f, a.d, g0, g1, l2_evict_first_policy());
+    return;
+  }
+  float xr[NV * VEC];
+  load_x<W, NV>(a.x, xr, tid, ncons);
+  float yacc[NV * VEC];
+#pragma unroll
+  for (int i = 0; i < NV * VEC; ++i) yacc[i] = 0.f;
+  consume_rows<W, NV>(R, cur, xr, yacc, s_gate, a.f, g0, g1, red, h_s, tid, ncons, 1);
+  store_y<W, NV>(a.ypart + (size_t)blockIdx.x * a.d, yacc, tid, ncons);
 }
 
 // Fixed-order reduction of the per-CTA partials + residual, fused with the
@@ -298,6 +346,195 @@ __global__ void __launch_bounds__(256) reduce_residual_kernel(
   }
 }
 
+// ---------------------------------------------------------------------------
+// persistent whole-stack kernel
+struct StackArgs {
+  const void* const* layer_experts;  // [L] expert base per layer
+  const int16_t* slot_of;            // [L][E]
+  long long expert_stride, mat_stride;
+  const float* router;               // [L][E][d]
+  float* x;                          // in: x_0, out: x_L
+  float* xbuf;                       // [2][d]
+  float* ypart;                      // [G][d]
+  float* rpart;                      // [G][E]
+  int32_t* ids_out;                  // [L][k]
+  float* gates_out;                  // [L][k]
+  unsigned* gbar;                    // grid barrier counter (0 at launch)
+  int L, d, f, E, k;
+  int row_bytes, rps, stages, stage_bytes;
+};
+
+__device__ __forceinline__ void grid_sync(unsigned* bar, unsigned target, int ncons) {
+  named_bar_sync(2, ncons);
+  if (threadIdx.x == 0) {
+    __threadfence();
+    asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(bar) : "memory");
+    unsigned v;
+    do {
+      asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(bar) : "memory");
+    } while (v < target);
+    __threadfence();
+  }
+  named_bar_sync(2, ncons);
+}
+
+template <typename W, int NV>
+__global__ void __launch_bounds__(kMaxConsWarps * 32 + 32, 1)
+    decode_stack_kernel(const __grid_constant__ StackArgs a) {
+  constexpr int VEC = Elem<W>::kVec;
+  extern __shared__ __align__(128) uint8_t smem[];
+  Ring R;
+  R.buf = smem;
+  R.full = reinterpret_cast<uint64_t*>(smem + (size_t)a.stages * a.stage_bytes);
+  R.empty = R.full + a.stages;
+  R.rps = a.rps;
+  R.stages = a.stages;
+  R.stage_bytes = a.stage_bytes;
+  R.row_bytes = a.row_bytes;
+  __shared__ uint64_t route_bar;
+  __shared__ float red[kMaxConsWarps * 32];
+  __shared__ float h_s[kBatch];
+  __shared__ float logits[kMaxExperts];
+  __shared__ float racc[kMaxExperts];
+  __shared__ float xs[32];
+  __shared__ int32_t s_ids[kMaxSlots];
+  __shared__ float s_g[kMaxSlots];
+  __shared__ int s_slot[kMaxSlots];
+  __shared__ float s_gate[kMaxSlots];
+  __shared__ int s_nloc;
+
+  const int ncons = blockDim.x - 32;
+  const int ncw = ncons >> 5;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int G = gridDim.x, c = blockIdx.x;
+  const int d = a.d, E = a.E, k = a.k;
+
+  if (tid == 0) {
+    for (int s = 0; s < a.stages; ++s) {
+      mbar_init(&R.full[s], 1);
+      mbar_init(&R.empty[s], ncw);
+    }
+    mbar_init(&route_bar, 1);
+    fence_mbar_init();
+  }
+  __syncthreads();
+  griddep_wait();
+
+  if (warp == ncw) {
+    // ===== producer =====
+    if (lane != 0) return;
+    const uint64_t pol = l2_evict_first_policy();
+    Cursor cur;
+    for (int l = 0; l < a.L; ++l) {
+      mbar_wait(&route_bar, (uint32_t)(l & 1));
+      const long long T = (long long)s_nloc * a.f;
+      const long long g0 = (long long)c * T / G, g1 = (long long)(c + 1) * T / G;
+      if (g1 > g0)
+        produce_rows<W>(R, cur, reinterpret_cast<const W*>(a.layer_experts[l]), a.expert_stride,
+                        a.mat_stride, s_slot, a.f, d, g0, g1, pol);
+    }
+    return;
+  }
+
+  // ===== consumers =====
+  unsigned gen = 0;
+  Cursor cur;
+  const int cc0 = (int)((long long)c * d / G), cc1 = (int)((long long)(c + 1) * d / G);
+  for (int l = 0; l < a.L; ++l) {
+    const float* xl = (l == 0) ? a.x : a.xbuf + (size_t)(l & 1) * d;
+    float* xn = (l == a.L - 1) ? a.x : a.xbuf + (size_t)((l + 1) & 1) * d;
+    // ---- A: routing of layer l (identical in every CTA) ----
+    if (l == 0) {
+      const float* r0 = a.router;
+      for (int e = warp; e < E; e += ncw) {
+        const float* re = r0 + (size_t)e * d;
+        float s = 0.f;
+        for (int i = lane; i < d; i += 32) s = fmaf(re[i], __ldcg(&xl[i]), s);
+        s = warp_sum(s);
+        if (lane == 0) logits[e] = s;
+      }
+    } else {
+      for (int e = warp; e < E; e += ncw) {
+        float s = 0.f;
+        for (int p = lane; p < G; p += 32) s += __ldcg(&a.rpart[(size_t)p * E + e]);
+        s = warp_sum(s);
+        if (lane == 0) logits[e] = s;
+      }
+    }
+    named_bar_sync(2, ncons);
+    if (tid == 0) {
+      topk_softmax(logits, E, k, s_ids, s_g);
+      const int16_t* so = a.slot_of + (size_t)l * E;
+      int n = 0;
+      for (int j = 0; j < k; ++j) {
+        const int slot = so[s_ids[j]];
+        if (slot >= 0) {
+          s_slot[n] = slot;
+          s_gate[n] = s_g[j];
+          ++n;
+        }
+        if (c == 0) {
+          a.ids_out[(size_t)l * k + j] = s_ids[j];
+          a.gates_out[(size_t)l * k + j] = s_g[j];
+        }
+      }
+      s_nloc = n;
+      mbar_arrive(&route_bar);  // release: the producer may stream layer l
+    }
+    named_bar_sync(2, ncons);
+
+    // ---- B: stream this CTA's rows ----
+    float xr[NV * VEC];
+    load_x<W, NV>(xl, xr, tid, ncons);
+    float yacc[NV * VEC];
+#pragma unroll
+    for (int i = 0; i < NV * VEC; ++i) yacc[i] = 0.f;
+    const long long T = (long long)s_nloc * a.f;
+    const long long g0 = (long long)c * T / G, g1 = (long long)(c + 1) * T / G;
+    consume_rows<W, NV>(R, cur, xr, yacc, s_gate, a.f, g0, g1, red, h_s, tid, ncons, 1);
+    store_y<W, NV>(a.ypart + (size_t)c * d, yacc, tid, ncons);
+    grid_sync(a.gbar, (++gen) * (unsigned)G, ncons);
+
+    // ---- C: reduce this CTA's column chunk, residual, next router partials ----
+    const bool more = l + 1 < a.L;
+    const float* rn = more ? a.router + (size_t)(l + 1) * E * d : nullptr;
+    for (int e = tid; e < E; e += ncons) racc[e] = 0.f;
+    for (int base = cc0; base < cc1; base += 32) {
+      const int col = base + lane;
+      const bool valid = col < cc1;
+      float s = 0.f;
+      if (valid)
+        for (int p = warp; p < G; p += ncw) s += __ldcg(&a.ypart[(size_t)p * d + col]);
+      red[warp * 32 + lane] = s;
+      named_bar_sync(2, ncons);
+      if (warp == 0) {
+        float tot = 0.f;
+        for (int w = 0; w < ncw; ++w) tot += red[w * 32 + lane];
+        float xo = 0.f;
+        if (valid) {
+          xo = __ldcg(&xl[col]) + tot;
+          xn[col] = xo;
+        }
+        xs[lane] = xo;
+      }
+      named_bar_sync(2, ncons);
+      if (more) {
+        for (int e = warp; e < E; e += ncw) {
+          const float v = valid ? rn[(size_t)e * d + col] * xs[lane] : 0.f;
+          const float t = warp_sum(v);
+          if (lane == 0) racc[e] += t;
+        }
+      }
+      named_bar_sync(2, ncons);
+    }
+    if (more) {
+      for (int e = tid; e < E; e += ncons) a.rpart[(size_t)c * E + e] = racc[e];
+      grid_sync(a.gbar, (++gen) * (unsigned)G, ncons);
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
 int reduce_blocks(const Dims& dm) { return (dm.d + 31) / 32; }
 
 DecodePlan plan_decode(const Dims& dm, int sm_count) {
@@ -322,10 +559,18 @@ DecodePlan plan_decode(const Dims& dm, int sm_count) {
   const int budget = 200 * 1024;
   p.stages = std::min(8, budget / stage);
   if (p.stages < 2) return p;
-  p.smem = p.stages * stage + 2 * p.stages * 8 + (kMaxConsWarps * 32 + kBatch) * 4;
+  p.smem = p.stages * stage + 2 * p.stages * 8;
   p.grid = sm_count;
   p.ok = true;
   return p;
+}
+
+static void fill_ring_args(const DecodePlan& p, const Dims& dm, int& row_bytes, int& rps,
+                           int& stages, int& stage_bytes) {
+  row_bytes = dm.d * (dm.dtype == MOE_DTYPE_BF16 ? 2 : 4);
+  rps = p.rps;
+  stages = p.stages;
+  stage_bytes = p.rps * row_bytes;
 }
 
 template <typename W, int NV>
@@ -347,17 +592,32 @@ static cudaError_t launch_decode_t(const DecodePlan& p, const DecodeArgs& a, cud
   return cudaLaunchKernelEx(&cfg, kern, a);
 }
 
-template <typename W>
-static cudaError_t dispatch_nv(const DecodePlan& p, const DecodeArgs& a, cudaStream_t s,
-                               bool pdl) {
-  switch (p.nv) {
-    case 1: return launch_decode_t<W, 1>(p, a, s, pdl);
-    case 2: return launch_decode_t<W, 2>(p, a, s, pdl);
-    case 3: return launch_decode_t<W, 3>(p, a, s, pdl);
-    case 4: return launch_decode_t<W, 4>(p, a, s, pdl);
-  }
-  return cudaErrorInvalidValue;
+template <typename W, int NV>
+static cudaError_t launch_stack_t(const DecodePlan& p, const StackArgs& a, cudaStream_t s) {
+  auto kern = decode_stack_kernel<W, NV>;
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, p.smem);
+  if (e != cudaSuccess) return e;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(p.grid);
+  cfg.blockDim = dim3(p.ncons + 32);
+  cfg.dynamicSmemBytes = p.smem;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeCooperative;
+  attr[0].val.cooperative = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, kern, a);
 }
+
+#define MOE_DISPATCH_NV(FN, W, ...)        \
+  switch (p.nv) {                         \
+    case 1: return FN<W, 1>(__VA_ARGS__); \
+    case 2: return FN<W, 2>(__VA_ARGS__); \
+    case 3: return FN<W, 3>(__VA_ARGS__); \
+    case 4: return FN<W, 4>(__VA_ARGS__); \
+  }                                       \
+  return cudaErrorInvalidValue;
 
 cudaError_t launch_decode_experts(const DecodePlan& p, const LayerWeights& lw, const Dims& dm,
                                   const int32_t* ids, const float* gates, const float* x,
@@ -371,12 +631,42 @@ cudaError_t launch_decode_experts(const DecodePlan& p, const LayerWeights& lw, c
   a.d = dm.d;
   a.f = dm.f;
   a.k = dm.k;
-  a.row_bytes = dm.d * (dm.dtype == MOE_DTYPE_BF16 ? 2 : 4);
-  a.rps = p.rps;
-  a.stages = p.stages;
-  a.stage_bytes = p.rps * a.row_bytes;
-  if (dm.dtype == MOE_DTYPE_BF16) return dispatch_nv<__nv_bfloat16>(p, a, s, pdl);
-  return dispatch_nv<float>(p, a, s, pdl);
+  fill_ring_args(p, dm, a.row_bytes, a.rps, a.stages, a.stage_bytes);
+  if (dm.dtype == MOE_DTYPE_BF16) {
+    MOE_DISPATCH_NV(launch_decode_t, __nv_bfloat16, p, a, s, pdl)
+  }
+  MOE_DISPATCH_NV(launch_decode_t, float, p, a, s, pdl)
+}
+
+cudaError_t launch_decode_stack(const DecodePlan& p, const StackDesc& sd, const Dims& dm,
+                                float* x, float* xbuf, float* ypart, float* rpart,
+                                int32_t* ids_out, float* gates_out, unsigned* gbar,
+                                cudaStream_t s) {
+  StackArgs a;
+  a.layer_experts = sd.layer_experts;
+  a.slot_of = sd.slot_of;
+  a.expert_stride = sd.expert_stride;
+  a.mat_stride = sd.mat_stride;
+  a.router = sd.router;
+  a.x = x;
+  a.xbuf = xbuf;
+  a.ypart = ypart;
+  a.rpart = rpart;
+  a.ids_out = ids_out;
+  a.gates_out = gates_out;
+  a.gbar = gbar;
+  a.L = sd.L;
+  a.d = dm.d;
+  a.f = dm.f;
+  a.E = dm.E;
+  a.k = dm.k;
+  fill_ring_args(p, dm, a.row_bytes, a.rps, a.stages, a.stage_bytes);
+  cudaError_t e = cudaMemsetAsync(gbar, 0, sizeof(unsigned), s);
+  if (e != cudaSuccess) return e;
+  if (dm.dtype == MOE_DTYPE_BF16) {
+    MOE_DISPATCH_NV(launch_stack_t, __nv_bfloat16, p, a, s)
+  }
+  MOE_DISPATCH_NV(launch_stack_t, float, p, a, s)
 }
 
 cudaError_t launch_reduce_residual(const float* ypart, int nparts, const float* x, float* x_out,

@@ -43,6 +43,18 @@ DecodePlan plan_decode(const Dims& dm, int sm_count);
 cudaError_t launch_decode_experts(const DecodePlan& p, const LayerWeights& lw, const Dims& dm,
                                   const int32_t* ids, const float* gates, const float* x,
                                   float* ypart, cudaStream_t s, bool pdl);
+// The whole L-layer batch-1 forward in one persistent cooperative launch.
+struct StackDesc {
+  const void* const* layer_experts;  // device array [L]
+  const int16_t* slot_of;            // device array [L][E]
+  long long expert_stride, mat_stride;
+  const float* router;               // [L][E][d]
+  int L;
+};
+cudaError_t launch_decode_stack(const DecodePlan& p, const StackDesc& sd, const Dims& dm,
+                                float* x, float* xbuf, float* ypart, float* rpart,
+                                int32_t* ids_out, float* gates_out, unsigned* gbar,
+                                cudaStream_t s);
 // x_out = x + sum_p ypart[p]; optionally the next layer's router + top-k
 // (deterministic fixed-order partial sums, last-block-done).
 cudaError_t launch_reduce_residual(const float* ypart, int nparts, const float* x, float* x_out,

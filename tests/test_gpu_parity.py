@@ -322,3 +322,35 @@ def test_errors_are_loud(ctx):
     with pytest.raises(M.MoeError) as ei:
         M.Weights(ctx, M.Shape(1, 2, 3, 16, 32, 2))
     assert ei.value.kind == "ShapeError"
+
+
+@pytest.mark.parametrize("L,d,f,dt", [(4, 4096, 14336, M.DTYPE_BF16), (3, 512, 1792, M.DTYPE_F32),
+                                      (2, 6144, 16384, M.DTYPE_BF16)])
+def test_persistent_stack_matches_per_layer_path(ctx, orc, L, d, f, dt, monkeypatch):
+    """The one-launch persistent stack kernel against the per-layer 2-kernel
+    path on identical weights: same routing, outputs within fp32 rounding."""
+    s = M.Shape(L, 8, 2, d, f, 2 if dt == M.DTYPE_BF16 else 4)
+    w_stack = M.Weights(ctx, s, dt)
+    monkeypatch.setenv("MOE_B200_STACK", "0")
+    w_layer = M.Weights(ctx, s, dt)
+    monkeypatch.delenv("MOE_B200_STACK")
+    assert w_stack.forward_launches(1) == 1 and w_layer.forward_launches(1) == 1 + 2 * L
+    w_stack.random(11)
+    w_layer.random(11)
+    x0 = f32(orc.normal(2, d))
+    outs, idss = [], []
+    for w in (w_stack, w_layer):
+        x = torch.tensor(x0[None], dtype=torch.float32, device="cuda")
+        ids = torch.zeros((L, 1, 2), dtype=torch.int32, device="cuda")
+        g = torch.zeros((L, 1, 2), dtype=torch.float32, device="cuda")
+        w.forward(x, ids, g)
+        torch.cuda.synchronize()
+        outs.append(x.cpu().numpy()[0].astype(np.float64))
+        idss.append(ids.cpu().numpy())
+    assert np.array_equal(idss[0], idss[1])
+    assert normwise(outs[0] - x0, outs[1] - x0) < 1e-4
+    # teacher-forced oracle check of the stack's first layer
+    ids, gts, delta, mg = oracle_layer(orc, w_stack, 0, x0, 2)
+    assert list(idss[0][0, 0]) == list(ids)
+    w_stack.close()
+    w_layer.close()
