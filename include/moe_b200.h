@@ -156,6 +156,13 @@ int moe_gate_topk_host(moe_ctx* ctx, int n_experts, int hidden, const double* ro
 int moe_expert_path(moe_weights* w, int n_tok);
 /* Number of kernels one moe_forward(n_tok) launches. */
 int moe_forward_launches(moe_weights* w, int n_tok);
+/* Diagnostics: one batch-1 moe_forward through the persistent stack kernel
+ * with per-CTA %globaltimer stamps.  trace receives [L][sm_count][8] u64:
+ * 0 layer start, 1 first ring stage landed, 2 stream done, 3 after grid
+ * barrier 1, 4 reduce done, 5 after grid barrier 2, 6 producer released,
+ * 7 producer issued last copy.  Synchronous. */
+int moe_debug_trace_forward(moe_weights* w, float* x, int32_t* ids, float* gates,
+                            uint64_t* trace, int64_t cap);
 
 #ifdef __cplusplus
 }

@@ -106,6 +106,7 @@ def lib():
         "moe_gate_topk_host": ([_vp, C.c_int, C.c_int, _dp, _dp, C.c_int, _i32p, _dp], C.c_int),
         "moe_expert_path": ([_vp, C.c_int], C.c_int),
         "moe_forward_launches": ([_vp, C.c_int], C.c_int),
+        "moe_debug_trace_forward": ([_vp, _vp, _vp, _vp, C.POINTER(C.c_uint64), C.c_int64], C.c_int),
     }
     for name, (args, res) in sig.items():
         fn = getattr(L, name)
@@ -129,6 +130,20 @@ def _ptr(t):
     if t is None:
         return None
     return C.c_void_p(t.data_ptr())
+
+
+def _stream(stream, *tensors):
+    """Default for device-pointer calls on torch tensors: torch's current
+    stream on the tensors' device, so the kernels are ordered after the
+    torch ops that produced their inputs."""
+    if stream is not None:
+        return stream
+    for t in tensors:
+        if t is not None and hasattr(t, "device") and getattr(t.device, "type", "") == "cuda":
+            import torch
+
+            return C.c_void_p(torch.cuda.current_stream(t.device).cuda_stream)
+    return None
 
 
 class Ctx:
@@ -173,7 +188,7 @@ class Ctx:
     def permute(self, ids, n_tok, top_k, n_experts, counts, offsets, perm, inv_perm=None,
                 stream=None):
         check(lib().moe_permute(self.h, _ptr(ids), n_tok, top_k, n_experts, _ptr(counts),
-                                _ptr(offsets), _ptr(perm), _ptr(inv_perm), stream))
+                                _ptr(offsets), _ptr(perm), _ptr(inv_perm), _stream(stream, ids)))
 
     def expert_ffn_host(self, dtype, w_in, w_gate, w_out, x):
         f, d = w_in.shape
@@ -258,22 +273,23 @@ class Weights:
     # -- device-pointer API (torch tensors) ----------------------------------
     def router_topk(self, layer, x, ids, gates, stream=None):
         check(lib().moe_router_topk(self.h, layer, _ptr(x), x.shape[0], _ptr(ids), _ptr(gates),
-                                    stream))
+                                    _stream(stream, x)))
 
     def experts_forward(self, layer, x, ids, gates, x_out, post_silu=None, stream=None):
         check(lib().moe_experts_forward(self.h, layer, _ptr(x), x.shape[0], _ptr(ids), _ptr(gates),
-                                        _ptr(x_out), _ptr(post_silu), stream))
+                                        _ptr(x_out), _ptr(post_silu), _stream(stream, x)))
 
     def decode_experts_partial(self, layer, x, ids, gates, ypart, stream=None):
         check(lib().moe_decode_experts_partial(self.h, layer, _ptr(x), _ptr(ids), _ptr(gates),
-                                               _ptr(ypart), stream))
+                                               _ptr(ypart), _stream(stream, x)))
 
     def layer_forward(self, layer, x, x_out, ids, gates, stream=None):
         check(lib().moe_layer_forward(self.h, layer, _ptr(x), _ptr(x_out), x.shape[0], _ptr(ids),
-                                      _ptr(gates), stream))
+                                      _ptr(gates), _stream(stream, x)))
 
     def forward(self, x, ids, gates, stream=None):
-        check(lib().moe_forward(self.h, _ptr(x), x.shape[0], _ptr(ids), _ptr(gates), stream))
+        check(lib().moe_forward(self.h, _ptr(x), x.shape[0], _ptr(ids), _ptr(gates),
+                                _stream(stream, x)))
 
     # -- host-buffer API ------------------------------------------------------
     def forward_host(self, tokens: np.ndarray, with_post=False):
@@ -290,6 +306,13 @@ class Weights:
         if with_post:
             return res + (post[:n * s.num_layers * s.top_k * s.ffn_dim],)
         return res
+
+    def debug_trace_forward(self, x, ids, gates):
+        n = self.shape.num_layers * self.ctx.sm_count * 8
+        tr = np.zeros(n, np.uint64)
+        check(lib().moe_debug_trace_forward(self.h, _ptr(x), _ptr(ids), _ptr(gates),
+                                            tr.ctypes.data_as(C.POINTER(C.c_uint64)), n))
+        return tr.reshape(self.shape.num_layers, self.ctx.sm_count, 8)
 
     def expert_path(self, n_tok: int) -> int:
         return lib().moe_expert_path(self.h, n_tok)

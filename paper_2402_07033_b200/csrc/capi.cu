@@ -249,8 +249,10 @@ bool use_stack(const moe_weights* w, int n_tok) {
   return use_decode(w, n_tok, nullptr) && w->ctx->world == 1 && w->stack_enabled && w->L() > 0;
 }
 
-int enqueue_stack(moe_weights* w, float* x, int32_t* ids, float* gates, cudaStream_t s) {
+int enqueue_stack(moe_weights* w, float* x, int32_t* ids, float* gates, cudaStream_t s,
+                  unsigned long long* trace = nullptr) {
   moe::StackDesc sd;
+  sd.trace = trace;
   sd.layer_experts = w->dev_layers.as<const void* const>();
   sd.slot_of = w->dev_slots.as<const int16_t>();
   sd.expert_stride = 3 * w->mat_elems();
@@ -862,6 +864,26 @@ int moe_gate_topk_host(moe_ctx* c, int n_experts, int hidden, const double* rout
 int moe_expert_path(moe_weights* w, int n_tok) {
   if (!w) return 0;
   return use_decode(w, n_tok, nullptr) ? 1 : 2;
+}
+
+int moe_debug_trace_forward(moe_weights* w, float* x, int32_t* ids, float* gates,
+                            uint64_t* trace, int64_t cap) {
+  if (!w || !x || !ids || !gates || !trace) return fail(MOE_ERR_ARG, "null pointer");
+  if (!use_stack(w, 1)) return fail(MOE_ERR_UNSUPPORTED, "no persistent stack plan");
+  const size_t n = (size_t)w->L() * w->ctx->sm_count * 8;
+  if ((size_t)cap < n) return fail(MOE_ERR_ARG, "trace buffer too small");
+  std::lock_guard<std::mutex> lk(w->mu);
+  TRY(set_device(w->ctx));
+  TRY(ensure_scratch(w, 1));
+  DevBuf buf;
+  TRY(buf.ensure(n * 8));
+  cudaStream_t s = w->ctx->stream;
+  int rc = enqueue_stack(w, x, ids, gates, s, buf.as<unsigned long long>());
+  if (rc == MOE_OK && (cudaMemcpyAsync(trace, buf.p, n * 8, cudaMemcpyDeviceToHost, s) ||
+                       cudaStreamSynchronize(s)))
+    rc = fail(MOE_ERR_CUDA, "trace copy failed");
+  buf.release();
+  return rc;
 }
 
 int moe_forward_launches(moe_weights* w, int n_tok) {

@@ -98,13 +98,15 @@ template <typename W, int NV>
 __device__ __forceinline__ void consume_rows(const Ring& R, Cursor& cur, const float* xr,
                                              float* yacc, const float* s_gate, int f,
                                              long long g0, long long g1, float* red, float* h_s,
-                                             int tid, int ncons, int bar_id) {
+                                             int tid, int ncons, int bar_id,
+                                             unsigned long long* t_first = nullptr) {
   constexpr int VEC = Elem<W>::kVec;
   const int warp = tid >> 5, lane = tid & 31, ncw = ncons >> 5;
   const int total_vec = (int)(3 * (g1 - g0));
   int p = 0;
   auto acquire = [&]() -> const uint8_t* {
     if (cur.slot == 0) mbar_wait(&R.full[cur.stage], cur.phase);
+    if (t_first != nullptr && p == 0 && tid == 0) *t_first = globaltimer();
     return R.buf + (size_t)cur.stage * R.stage_bytes + (size_t)cur.slot * R.row_bytes;
   };
   auto release = [&]() {
@@ -360,6 +362,7 @@ struct StackArgs {
   int32_t* ids_out;                  // [L][k]
   float* gates_out;                  // [L][k]
   unsigned* gbar;                    // grid barrier counter (0 at launch)
+  unsigned long long* trace;         // optional [L][G][8] globaltimer stamps
   int L, d, f, E, k;
   int row_bytes, rps, stages, stage_bytes;
 };
@@ -427,11 +430,13 @@ __global__ void __launch_bounds__(kMaxConsWarps * 32 + 32, 1)
     Cursor cur;
     for (int l = 0; l < a.L; ++l) {
       mbar_wait(&route_bar, (uint32_t)(l & 1));
+      if (a.trace) a.trace[((size_t)l * G + c) * 8 + 6] = globaltimer();
       const long long T = (long long)s_nloc * a.f;
       const long long g0 = (long long)c * T / G, g1 = (long long)(c + 1) * T / G;
       if (g1 > g0)
         produce_rows<W>(R, cur, reinterpret_cast<const W*>(a.layer_experts[l]), a.expert_stride,
                         a.mat_stride, s_slot, a.f, d, g0, g1, pol);
+      if (a.trace) a.trace[((size_t)l * G + c) * 8 + 7] = globaltimer();
     }
     return;
   }
@@ -443,6 +448,8 @@ __global__ void __launch_bounds__(kMaxConsWarps * 32 + 32, 1)
   for (int l = 0; l < a.L; ++l) {
     const float* xl = (l == 0) ? a.x : a.xbuf + (size_t)(l & 1) * d;
     float* xn = (l == a.L - 1) ? a.x : a.xbuf + (size_t)((l + 1) & 1) * d;
+    unsigned long long* tr = a.trace ? a.trace + ((size_t)l * G + c) * 8 : nullptr;
+    if (tr && tid == 0) tr[0] = globaltimer();
     // ---- A: routing of layer l (identical in every CTA) ----
     if (l == 0) {
       const float* r0 = a.router;
@@ -491,9 +498,12 @@ __global__ void __launch_bounds__(kMaxConsWarps * 32 + 32, 1)
     for (int i = 0; i < NV * VEC; ++i) yacc[i] = 0.f;
     const long long T = (long long)s_nloc * a.f;
     const long long g0 = (long long)c * T / G, g1 = (long long)(c + 1) * T / G;
-    consume_rows<W, NV>(R, cur, xr, yacc, s_gate, a.f, g0, g1, red, h_s, tid, ncons, 1);
+    consume_rows<W, NV>(R, cur, xr, yacc, s_gate, a.f, g0, g1, red, h_s, tid, ncons, 1,
+                        tr ? tr + 1 : nullptr);
+    if (tr && tid == 0) tr[2] = globaltimer();
     store_y<W, NV>(a.ypart + (size_t)c * d, yacc, tid, ncons);
     grid_sync(a.gbar, (++gen) * (unsigned)G, ncons);
+    if (tr && tid == 0) tr[3] = globaltimer();
 
     // ---- C: reduce this CTA's column chunk, residual, next router partials ----
     const bool more = l + 1 < a.L;
@@ -527,10 +537,12 @@ __global__ void __launch_bounds__(kMaxConsWarps * 32 + 32, 1)
       }
       named_bar_sync(2, ncons);
     }
+    if (tr && tid == 0) tr[4] = globaltimer();
     if (more) {
       for (int e = tid; e < E; e += ncons) a.rpart[(size_t)c * E + e] = racc[e];
       grid_sync(a.gbar, (++gen) * (unsigned)G, ncons);
     }
+    if (tr && tid == 0) tr[5] = globaltimer();
   }
 }
 
@@ -655,6 +667,7 @@ cudaError_t launch_decode_stack(const DecodePlan& p, const StackDesc& sd, const 
   a.ids_out = ids_out;
   a.gates_out = gates_out;
   a.gbar = gbar;
+  a.trace = sd.trace;
   a.L = sd.L;
   a.d = dm.d;
   a.f = dm.f;

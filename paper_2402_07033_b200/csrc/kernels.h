@@ -50,6 +50,7 @@ struct StackDesc {
   long long expert_stride, mat_stride;
   const float* router;               // [L][E][d]
   int L;
+  unsigned long long* trace = nullptr;  // optional [L][G][8] globaltimer stamps
 };
 cudaError_t launch_decode_stack(const DecodePlan& p, const StackDesc& sd, const Dims& dm,
                                 float* x, float* xbuf, float* ypart, float* rpart,
