@@ -368,17 +368,36 @@ struct StackArgs {
 };
 
 __device__ __forceinline__ void grid_sync(unsigned* bar, unsigned target, int ncons) {
+  // bar.sync orders the CTA's prior writes before thread 0's release (the
+  // release is cumulative); cross-CTA data is then read with ld.cg (L2).
   named_bar_sync(2, ncons);
   if (threadIdx.x == 0) {
-    __threadfence();
     asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(bar) : "memory");
     unsigned v;
     do {
       asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(bar) : "memory");
     } while (v < target);
-    __threadfence();
   }
   named_bar_sync(2, ncons);
+}
+
+// Fixed-order sum of up to 8*ncw*kSumUnroll strided values with all loads in
+// flight at once (one L2 round trip instead of one per value).
+constexpr int kSumUnroll = 24;
+__device__ __forceinline__ float strided_sum(const float* base, int first, int count, int step,
+                                             size_t stride) {
+  float s = 0.f;
+  for (int p0 = first; p0 < count; p0 += kSumUnroll * step) {
+    float v[kSumUnroll];
+#pragma unroll
+    for (int i = 0; i < kSumUnroll; ++i) {
+      const int p = p0 + i * step;
+      v[i] = p < count ? __ldcg(base + (size_t)p * stride) : 0.f;
+    }
+#pragma unroll
+    for (int i = 0; i < kSumUnroll; ++i) s += v[i];
+  }
+  return s;
 }
 
 template <typename W, int NV>
@@ -461,9 +480,9 @@ __global__ void __launch_bounds__(kMaxConsWarps * 32 + 32, 1)
         if (lane == 0) logits[e] = s;
       }
     } else {
+      // rpart is [E][G]: lanes read consecutive CTAs' partials (coalesced)
       for (int e = warp; e < E; e += ncw) {
-        float s = 0.f;
-        for (int p = lane; p < G; p += 32) s += __ldcg(&a.rpart[(size_t)p * E + e]);
+        float s = strided_sum(a.rpart + (size_t)e * G, lane, G, 32, 1);
         s = warp_sum(s);
         if (lane == 0) logits[e] = s;
       }
@@ -512,9 +531,7 @@ __global__ void __launch_bounds__(kMaxConsWarps * 32 + 32, 1)
     for (int base = cc0; base < cc1; base += 32) {
       const int col = base + lane;
       const bool valid = col < cc1;
-      float s = 0.f;
-      if (valid)
-        for (int p = warp; p < G; p += ncw) s += __ldcg(&a.ypart[(size_t)p * d + col]);
+      const float s = valid ? strided_sum(a.ypart + col, warp, G, ncw, (size_t)d) : 0.f;
       red[warp * 32 + lane] = s;
       named_bar_sync(2, ncons);
       if (warp == 0) {
@@ -539,7 +556,7 @@ __global__ void __launch_bounds__(kMaxConsWarps * 32 + 32, 1)
     }
     if (tr && tid == 0) tr[4] = globaltimer();
     if (more) {
-      for (int e = tid; e < E; e += ncons) a.rpart[(size_t)c * E + e] = racc[e];
+      for (int e = tid; e < E; e += ncons) a.rpart[(size_t)e * G + c] = racc[e];
       grid_sync(a.gbar, (++gen) * (unsigned)G, ncons);
     }
     if (tr && tid == 0) tr[5] = globaltimer();
