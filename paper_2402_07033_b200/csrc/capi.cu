@@ -511,7 +511,7 @@ int moe_weights_create(moe_ctx* c, const moe_shape* shape, int dtype, const int3
     // device-side tables for the persistent stack kernel
     const int Lm = std::max(1, L);
     if (w->dev_layers.ensure(sizeof(void*) * Lm) || w->dev_slots.ensure(sizeof(int16_t) * Lm * E) ||
-        w->xbuf2.ensure(sizeof(float) * 2 * shape->hidden_dim) || w->gbar.ensure(64) ||
+        w->xbuf2.ensure(sizeof(float) * 2 * shape->hidden_dim) || w->gbar.ensure(256) ||
         w->rpart.ensure(sizeof(float) * (size_t)std::max(c->sm_count, moe::reduce_blocks(w->dims())) * E))
       return cleanup(fail(MOE_ERR_OOM, "cudaMalloc stack tables"));
     if (L > 0 &&

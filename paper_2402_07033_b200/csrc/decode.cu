@@ -370,13 +370,22 @@ struct StackArgs {
 __device__ __forceinline__ void grid_sync(unsigned* bar, unsigned target, int ncons) {
   // bar.sync orders the CTA's prior writes before thread 0's release (the
   // release is cumulative); cross-CTA data is then read with ld.cg (L2).
+  // Arrivals go to bar[0]; the last arriver publishes the generation on a
+  // separate 128-byte line (bar[32]) that everyone else polls, so polling
+  // never contends with the arrival atomics.
   named_bar_sync(2, ncons);
   if (threadIdx.x == 0) {
-    asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(bar) : "memory");
-    unsigned v;
-    do {
-      asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(bar) : "memory");
-    } while (v < target);
+    const unsigned gen = target / gridDim.x;
+    unsigned old;
+    asm volatile("atom.acq_rel.gpu.global.add.u32 %0, [%1], 1;" : "=r"(old) : "l"(bar) : "memory");
+    if (old == target - 1) {
+      asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(bar + 32), "r"(gen) : "memory");
+    } else {
+      unsigned v;
+      do {
+        asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(bar + 32) : "memory");
+      } while (v < gen);
+    }
   }
   named_bar_sync(2, ncons);
 }
@@ -424,6 +433,7 @@ __global__ void __launch_bounds__(kMaxConsWarps * 32 + 32, 1)
   __shared__ int s_slot[kMaxSlots];
   __shared__ float s_gate[kMaxSlots];
   __shared__ int s_nloc;
+  __shared__ int16_t s_so[kMaxExperts];  // slot map of the layer being routed
 
   const int ncons = blockDim.x - 32;
   const int ncw = ncons >> 5;
@@ -464,6 +474,7 @@ __global__ void __launch_bounds__(kMaxConsWarps * 32 + 32, 1)
   unsigned gen = 0;
   Cursor cur;
   const int cc0 = (int)((long long)c * d / G), cc1 = (int)((long long)(c + 1) * d / G);
+  for (int e = tid; e < E; e += ncons) s_so[e] = a.slot_of[e];
   for (int l = 0; l < a.L; ++l) {
     const float* xl = (l == 0) ? a.x : a.xbuf + (size_t)(l & 1) * d;
     float* xn = (l == a.L - 1) ? a.x : a.xbuf + (size_t)((l + 1) & 1) * d;
@@ -490,7 +501,7 @@ __global__ void __launch_bounds__(kMaxConsWarps * 32 + 32, 1)
     named_bar_sync(2, ncons);
     if (tid == 0) {
       topk_softmax(logits, E, k, s_ids, s_g);
-      const int16_t* so = a.slot_of + (size_t)l * E;
+      const int16_t* so = s_so;
       int n = 0;
       for (int j = 0; j < k; ++j) {
         const int slot = so[s_ids[j]];
@@ -527,7 +538,10 @@ __global__ void __launch_bounds__(kMaxConsWarps * 32 + 32, 1)
     // ---- C: reduce this CTA's column chunk, residual, next router partials ----
     const bool more = l + 1 < a.L;
     const float* rn = more ? a.router + (size_t)(l + 1) * E * d : nullptr;
-    for (int e = tid; e < E; e += ncons) racc[e] = 0.f;
+    for (int e = tid; e < E; e += ncons) {
+      racc[e] = 0.f;
+      if (more) s_so[e] = a.slot_of[(size_t)(l + 1) * E + e];  // prefetch next layer's map
+    }
     for (int base = cc0; base < cc1; base += 32) {
       const int col = base + lane;
       const bool valid = col < cc1;
@@ -691,7 +705,7 @@ cudaError_t launch_decode_stack(const DecodePlan& p, const StackDesc& sd, const 
   a.E = dm.E;
   a.k = dm.k;
   fill_ring_args(p, dm, a.row_bytes, a.rps, a.stages, a.stage_bytes);
-  cudaError_t e = cudaMemsetAsync(gbar, 0, sizeof(unsigned), s);
+  cudaError_t e = cudaMemsetAsync(gbar, 0, 256, s);  // arrival counter + release line
   if (e != cudaSuccess) return e;
   if (dm.dtype == MOE_DTYPE_BF16) {
     MOE_DISPATCH_NV(launch_stack_t, __nv_bfloat16, p, a, s)
