@@ -370,28 +370,19 @@ struct StackArgs {
 __device__ __forceinline__ void grid_sync(unsigned* bar, unsigned target, int ncons) {
   // bar.sync orders the CTA's prior writes before thread 0's release (the
   // release is cumulative); cross-CTA data is then read with ld.cg (L2).
-  // Arrivals go to bar[0]; the last arriver publishes the generation on a
-  // separate 128-byte line (bar[32]) that everyone else polls, so polling
-  // never contends with the arrival atomics.
   named_bar_sync(2, ncons);
   if (threadIdx.x == 0) {
-    const unsigned gen = target / gridDim.x;
-    unsigned old;
-    asm volatile("atom.acq_rel.gpu.global.add.u32 %0, [%1], 1;" : "=r"(old) : "l"(bar) : "memory");
-    if (old == target - 1) {
-      asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(bar + 32), "r"(gen) : "memory");
-    } else {
-      unsigned v;
-      do {
-        asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(bar + 32) : "memory");
-      } while (v < gen);
-    }
+    asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(bar) : "memory");
+    unsigned v;
+    do {
+      asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(bar) : "memory");
+    } while (v < target);
   }
   named_bar_sync(2, ncons);
 }
 
-// Fixed-order sum of up to 8*ncw*kSumUnroll strided values with all loads in
-// flight at once (one L2 round trip instead of one per value).
+// Fixed-order sum of strided values with all loads in flight at once (one L2
+// round trip instead of one per value).
 constexpr int kSumUnroll = 24;
 __device__ __forceinline__ float strided_sum(const float* base, int first, int count, int step,
                                              size_t stride) {
@@ -409,6 +400,13 @@ __device__ __forceinline__ float strided_sum(const float* base, int first, int c
   return s;
 }
 
+// Routing is linear in x, so the next layer's logits are assembled from
+// per-CTA partials written BEFORE the first grid barrier:
+//   logits_{l+1} = R_{l+1} x_{l+1} = R_{l+1} x_l + sum_c R_{l+1} ypart_c,
+// CTA c contributing z_c = R_{l+1} (ypart_c [+ x_l if c == 0]).  Right after
+// barrier 1 every CTA sums the G partials in a fixed order, picks the top-k
+// and releases its producer warp — the residual reduction and the second
+// barrier (needed only by the consumers, for x_{l+1}) overlap the ring fill.
 template <typename W, int NV>
 __global__ void __launch_bounds__(kMaxConsWarps * 32 + 32, 1)
     decode_stack_kernel(const __grid_constant__ StackArgs a) {
@@ -426,8 +424,7 @@ __global__ void __launch_bounds__(kMaxConsWarps * 32 + 32, 1)
   __shared__ float red[kMaxConsWarps * 32];
   __shared__ float h_s[kBatch];
   __shared__ float logits[kMaxExperts];
-  __shared__ float racc[kMaxExperts];
-  __shared__ float xs[32];
+  __shared__ float zred[kMaxConsWarps * kMaxExperts];
   __shared__ int32_t s_ids[kMaxSlots];
   __shared__ float s_g[kMaxSlots];
   __shared__ int s_slot[kMaxSlots];
@@ -471,56 +468,52 @@ __global__ void __launch_bounds__(kMaxConsWarps * 32 + 32, 1)
   }
 
   // ===== consumers =====
+  // top-k of `logits` for layer l -> smem routing + release of the producer
+  auto commit_route = [&](int l) {
+    topk_softmax(logits, E, k, s_ids, s_g);
+    int n = 0;
+    for (int j = 0; j < k; ++j) {
+      const int slot = s_so[s_ids[j]];
+      if (slot >= 0) {
+        s_slot[n] = slot;
+        s_gate[n] = s_g[j];
+        ++n;
+      }
+      if (c == 0) {
+        a.ids_out[(size_t)l * k + j] = s_ids[j];
+        a.gates_out[(size_t)l * k + j] = s_g[j];
+      }
+    }
+    s_nloc = n;
+    mbar_arrive(&route_bar);
+  };
+
   unsigned gen = 0;
   Cursor cur;
   const int cc0 = (int)((long long)c * d / G), cc1 = (int)((long long)(c + 1) * d / G);
+  if (a.trace && tid == 0) a.trace[(size_t)c * 8 + 0] = globaltimer();
+  // routing of layer 0: the router GEMV itself, redundantly in every CTA
   for (int e = tid; e < E; e += ncons) s_so[e] = a.slot_of[e];
-  for (int l = 0; l < a.L; ++l) {
-    const float* xl = (l == 0) ? a.x : a.xbuf + (size_t)(l & 1) * d;
-    float* xn = (l == a.L - 1) ? a.x : a.xbuf + (size_t)((l + 1) & 1) * d;
-    unsigned long long* tr = a.trace ? a.trace + ((size_t)l * G + c) * 8 : nullptr;
-    if (tr && tid == 0) tr[0] = globaltimer();
-    // ---- A: routing of layer l (identical in every CTA) ----
-    if (l == 0) {
-      const float* r0 = a.router;
-      for (int e = warp; e < E; e += ncw) {
-        const float* re = r0 + (size_t)e * d;
-        float s = 0.f;
-        for (int i = lane; i < d; i += 32) s = fmaf(re[i], __ldcg(&xl[i]), s);
-        s = warp_sum(s);
-        if (lane == 0) logits[e] = s;
-      }
-    } else {
-      // rpart is [E][G]: lanes read consecutive CTAs' partials (coalesced)
-      for (int e = warp; e < E; e += ncw) {
-        float s = strided_sum(a.rpart + (size_t)e * G, lane, G, 32, 1);
-        s = warp_sum(s);
-        if (lane == 0) logits[e] = s;
-      }
-    }
-    named_bar_sync(2, ncons);
-    if (tid == 0) {
-      topk_softmax(logits, E, k, s_ids, s_g);
-      const int16_t* so = s_so;
-      int n = 0;
-      for (int j = 0; j < k; ++j) {
-        const int slot = so[s_ids[j]];
-        if (slot >= 0) {
-          s_slot[n] = slot;
-          s_gate[n] = s_g[j];
-          ++n;
-        }
-        if (c == 0) {
-          a.ids_out[(size_t)l * k + j] = s_ids[j];
-          a.gates_out[(size_t)l * k + j] = s_g[j];
-        }
-      }
-      s_nloc = n;
-      mbar_arrive(&route_bar);  // release: the producer may stream layer l
-    }
-    named_bar_sync(2, ncons);
+  for (int e = warp; e < E; e += ncw) {
+    const float* re = a.router + (size_t)e * d;
+    float s = 0.f;
+    for (int i = lane; i < d; i += 32) s = fmaf(re[i], __ldcg(&a.x[i]), s);
+    s = warp_sum(s);
+    if (lane == 0) logits[e] = s;
+  }
+  named_bar_sync(2, ncons);
+  if (tid == 0) commit_route(0);
+  named_bar_sync(2, ncons);
 
-    // ---- B: stream this CTA's rows ----
+  for (int l = 0; l < a.L; ++l) {
+    const bool more = l + 1 < a.L;
+    const float* xl = (l == 0) ? a.x : a.xbuf + (size_t)(l & 1) * d;
+    float* xn = more ? a.xbuf + (size_t)((l + 1) & 1) * d : a.x;
+    unsigned long long* tr = a.trace ? a.trace + ((size_t)l * G + c) * 8 : nullptr;
+    if (more)
+      for (int e = tid; e < E; e += ncons) s_so[e] = a.slot_of[(size_t)(l + 1) * E + e];
+
+    // ---- B: stream this CTA's rows of layer l ----
     float xr[NV * VEC];
     load_x<W, NV>(xl, xr, tid, ncons);
     float yacc[NV * VEC];
@@ -532,48 +525,82 @@ __global__ void __launch_bounds__(kMaxConsWarps * 32 + 32, 1)
                         tr ? tr + 1 : nullptr);
     if (tr && tid == 0) tr[2] = globaltimer();
     store_y<W, NV>(a.ypart + (size_t)c * d, yacc, tid, ncons);
+
+    // ---- z_c = R_{l+1} (ypart_c [+ x_l]) : next layer's router partial ----
+    if (more) {
+      const float* rn = a.router + (size_t)(l + 1) * E * d;
+      float v[NV * VEC];
+#pragma unroll
+      for (int i = 0; i < NV * VEC; ++i) v[i] = c == 0 ? yacc[i] + xr[i] : yacc[i];
+      for (int e0 = 0; e0 < E; e0 += 8) {
+        float part[8];
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+          part[q] = 0.f;
+          if (e0 + q < E) {
+            const float* re = rn + (size_t)(e0 + q) * d;
+#pragma unroll
+            for (int m = 0; m < NV; ++m) {
+              const float4* rp = reinterpret_cast<const float4*>(re + (size_t)(tid + m * ncons) * VEC);
+#pragma unroll
+              for (int u = 0; u < VEC / 4; ++u) {
+                const float4 rv = __ldg(rp + u);
+                const float* vv = v + m * VEC + 4 * u;
+                part[q] = fmaf(rv.x, vv[0], part[q]);
+                part[q] = fmaf(rv.y, vv[1], part[q]);
+                part[q] = fmaf(rv.z, vv[2], part[q]);
+                part[q] = fmaf(rv.w, vv[3], part[q]);
+              }
+            }
+          }
+        }
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+          const float t = warp_sum(part[q]);
+          if (lane == 0 && e0 + q < E) zred[warp * kMaxExperts + e0 + q] = t;
+        }
+      }
+      named_bar_sync(2, ncons);
+      for (int e = tid; e < E; e += ncons) {
+        float t = 0.f;
+        for (int w = 0; w < ncw; ++w) t += zred[w * kMaxExperts + e];
+        a.rpart[(size_t)e * G + c] = t;
+      }
+    }
     grid_sync(a.gbar, (++gen) * (unsigned)G, ncons);
     if (tr && tid == 0) tr[3] = globaltimer();
 
-    // ---- C: reduce this CTA's column chunk, residual, next router partials ----
-    const bool more = l + 1 < a.L;
-    const float* rn = more ? a.router + (size_t)(l + 1) * E * d : nullptr;
-    for (int e = tid; e < E; e += ncons) {
-      racc[e] = 0.f;
-      if (more) s_so[e] = a.slot_of[(size_t)(l + 1) * E + e];  // prefetch next layer's map
+    // ---- A(l+1): route the next layer and release the producer ----
+    if (more) {
+      for (int e = warp; e < E; e += ncw) {
+        float s = strided_sum(a.rpart + (size_t)e * G, lane, G, 32, 1);
+        s = warp_sum(s);
+        if (lane == 0) logits[e] = s;
+      }
+      named_bar_sync(2, ncons);
+      if (tid == 0) commit_route(l + 1);
     }
+
+    // ---- C: this CTA's column chunk of x_{l+1} = x_l + sum_c ypart_c ----
     for (int base = cc0; base < cc1; base += 32) {
       const int col = base + lane;
       const bool valid = col < cc1;
       const float s = valid ? strided_sum(a.ypart + col, warp, G, ncw, (size_t)d) : 0.f;
       red[warp * 32 + lane] = s;
       named_bar_sync(2, ncons);
-      if (warp == 0) {
+      if (warp == 0 && valid) {
         float tot = 0.f;
         for (int w = 0; w < ncw; ++w) tot += red[w * 32 + lane];
-        float xo = 0.f;
-        if (valid) {
-          xo = __ldcg(&xl[col]) + tot;
-          xn[col] = xo;
-        }
-        xs[lane] = xo;
-      }
-      named_bar_sync(2, ncons);
-      if (more) {
-        for (int e = warp; e < E; e += ncw) {
-          const float v = valid ? rn[(size_t)e * d + col] * xs[lane] : 0.f;
-          const float t = warp_sum(v);
-          if (lane == 0) racc[e] += t;
-        }
+        xn[col] = __ldcg(&xl[col]) + tot;
       }
       named_bar_sync(2, ncons);
     }
     if (tr && tid == 0) tr[4] = globaltimer();
-    if (more) {
-      for (int e = tid; e < E; e += ncons) a.rpart[(size_t)e * G + c] = racc[e];
-      grid_sync(a.gbar, (++gen) * (unsigned)G, ncons);
+    if (more) grid_sync(a.gbar, (++gen) * (unsigned)G, ncons);
+    if (tr && tid == 0) {
+      tr[5] = globaltimer();
+      if (more) a.trace[((size_t)(l + 1) * G + c) * 8 + 0] = tr[3];
     }
-    if (tr && tid == 0) tr[5] = globaltimer();
   }
 }
 
