@@ -308,11 +308,11 @@ class Weights:
         return res
 
     def debug_trace_forward(self, x, ids, gates):
-        n = self.shape.num_layers * self.ctx.sm_count * 8
+        n = self.shape.num_layers * self.ctx.sm_count * 16
         tr = np.zeros(n, np.uint64)
         check(lib().moe_debug_trace_forward(self.h, _ptr(x), _ptr(ids), _ptr(gates),
                                             tr.ctypes.data_as(C.POINTER(C.c_uint64)), n))
-        return tr.reshape(self.shape.num_layers, self.ctx.sm_count, 8)
+        return tr.reshape(self.shape.num_layers, self.ctx.sm_count, 16)
 
     def expert_path(self, n_tok: int) -> int:
         return lib().moe_expert_path(self.h, n_tok)

@@ -870,7 +870,7 @@ int moe_debug_trace_forward(moe_weights* w, float* x, int32_t* ids, float* gates
                             uint64_t* trace, int64_t cap) {
   if (!w || !x || !ids || !gates || !trace) return fail(MOE_ERR_ARG, "null pointer");
   if (!use_stack(w, 1)) return fail(MOE_ERR_UNSUPPORTED, "no persistent stack plan");
-  const size_t n = (size_t)w->L() * w->ctx->sm_count * 8;
+  const size_t n = (size_t)w->L() * w->ctx->sm_count * 16;
   if ((size_t)cap < n) return fail(MOE_ERR_ARG, "trace buffer too small");
   std::lock_guard<std::mutex> lk(w->mu);
   TRY(set_device(w->ctx));

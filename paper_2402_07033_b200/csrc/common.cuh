@@ -129,38 +129,73 @@ __device__ __forceinline__ void named_bar_sync(int id, int nthreads) {
   asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
 }
 
-// ---- top-k selection with the reference tie-break ---------------------------
-// gate_topk (model.cpp:79-99): pick k by (logit desc, id asc), report ids
-// ascending, softmax over the selected logits (max-subtracted) in ascending-id
-// order.  Single thread; E <= 256.
-__device__ __forceinline__ void topk_softmax(const float* logits, int E, int k, int32_t* ids,
-                                             float* gates) {
-  uint32_t taken[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+// ---- warp-wide top-k (registers only; no local-memory arrays) --------------
+// Same semantics as topk_softmax below / gate_topk (model.cpp:79-99): k
+// rounds of a warp argmax with (logit desc, id asc) ordering, ids emitted
+// ascending, softmax over the selected logits with the denominator summed
+// sequentially in ascending-id order.  Called by all 32 lanes of one warp;
+// logits in shared/global memory, E <= 256, k <= 32.  Lanes j < k write
+// ids[j] / gates[j].
+__device__ __forceinline__ void warp_topk_softmax(const float* logits, int E, int k,
+                                                  int32_t* ids, float* gates) {
+  const int lane = threadIdx.x & 31;
+  float v[8];
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    const int e = lane + 32 * i;
+    v[i] = e < E ? logits[e] : 0.f;
+  }
+  unsigned taken = 0u;  // bit i: expert lane+32i selected
   for (int j = 0; j < k; ++j) {
-    int best = -1;
     float bv = 0.f;
-    for (int e = 0; e < E; ++e) {
-      if (taken[e >> 5] & (1u << (e & 31))) continue;
-      const float v = logits[e];
-      if (best < 0 || v > bv) {
-        best = e;
-        bv = v;
+    int be = 0x7fffffff;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      const int e = lane + 32 * i;
+      if (e < E && !(taken & (1u << i)) && (be == 0x7fffffff || v[i] > bv)) {
+        bv = v[i];
+        be = e;
       }
     }
-    taken[best >> 5] |= 1u << (best & 31);
+#pragma unroll
+    for (int s = 16; s >= 1; s >>= 1) {
+      const float ov = __shfl_xor_sync(MOE_FULL_MASK, bv, s);
+      const int oe = __shfl_xor_sync(MOE_FULL_MASK, be, s);
+      const bool better = (oe != 0x7fffffff) &&
+                          (be == 0x7fffffff || ov > bv || (ov == bv && oe < be));
+      if (better) {
+        bv = ov;
+        be = oe;
+      }
+    }
+    if ((be & 31) == lane) taken |= 1u << (be >> 5);
   }
-  int n = 0;
-  for (int e = 0; e < E && n < k; ++e)
-    if (taken[e >> 5] & (1u << (e & 31))) ids[n++] = e;
-  float mx = logits[ids[0]];
-  for (int j = 1; j < k; ++j) mx = fmaxf(mx, logits[ids[j]]);
+  // emit ids ascending: block i of 32 experts in lane order
+  int base = 0;
+  int my_id = -1;
+  float my_logit = 0.f;
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    const unsigned m = __ballot_sync(MOE_FULL_MASK, (taken >> i) & 1u);
+    if ((taken >> i) & 1u) {
+      const int pos = base + __popc(m & ((1u << lane) - 1u));
+      ids[pos] = lane + 32 * i;
+    }
+    base += __popc(m);
+  }
+  __syncwarp();
+  if (lane < k) {
+    my_id = ids[lane];
+    my_logit = logits[my_id];
+  }
+  float mx = lane < k ? my_logit : -INFINITY;
+#pragma unroll
+  for (int s = 16; s >= 1; s >>= 1) mx = fmaxf(mx, __shfl_xor_sync(MOE_FULL_MASK, mx, s));
+  const float w = lane < k ? expf(my_logit - mx) : 0.f;
   float denom = 0.f;
-  for (int j = 0; j < k; ++j) {
-    const float v = expf(logits[ids[j]] - mx);
-    denom += v;
-    gates[j] = v;
-  }
-  for (int j = 0; j < k; ++j) gates[j] = gates[j] / denom;
+  for (int j = 0; j < k; ++j) denom += __shfl_sync(MOE_FULL_MASK, w, j);
+  if (lane < k) gates[lane] = w / denom;
+  __syncwarp();
 }
 
 }  // namespace moe

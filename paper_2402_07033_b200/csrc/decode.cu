@@ -342,10 +342,8 @@ __global__ void __launch_bounds__(256) reduce_residual_kernel(
     logits[e] = l;
   }
   __syncthreads();
-  if (tid == 0) {
-    topk_softmax(logits, E, k, next_ids, next_gates);
-    *counter = 0u;
-  }
+  if (warp == 0) warp_topk_softmax(logits, E, k, next_ids, next_gates);
+  if (tid == 0) *counter = 0u;
 }
 
 // ---------------------------------------------------------------------------
@@ -456,21 +454,22 @@ __global__ void __launch_bounds__(kMaxConsWarps * 32 + 32, 1)
     Cursor cur;
     for (int l = 0; l < a.L; ++l) {
       mbar_wait(&route_bar, (uint32_t)(l & 1));
-      if (a.trace) a.trace[((size_t)l * G + c) * 8 + 6] = globaltimer();
+      if (a.trace) a.trace[((size_t)l * G + c) * 16 + 6] = globaltimer();
       const long long T = (long long)s_nloc * a.f;
       const long long g0 = (long long)c * T / G, g1 = (long long)(c + 1) * T / G;
       if (g1 > g0)
         produce_rows<W>(R, cur, reinterpret_cast<const W*>(a.layer_experts[l]), a.expert_stride,
                         a.mat_stride, s_slot, a.f, d, g0, g1, pol);
-      if (a.trace) a.trace[((size_t)l * G + c) * 8 + 7] = globaltimer();
+      if (a.trace) a.trace[((size_t)l * G + c) * 16 + 7] = globaltimer();
     }
     return;
   }
 
   // ===== consumers =====
   // top-k of `logits` for layer l -> smem routing + release of the producer
-  auto commit_route = [&](int l) {
-    topk_softmax(logits, E, k, s_ids, s_g);
+  auto commit_route = [&](int l) {  // called by warp 0
+    warp_topk_softmax(logits, E, k, s_ids, s_g);
+    if (lane != 0) return;
     int n = 0;
     for (int j = 0; j < k; ++j) {
       const int slot = s_so[s_ids[j]];
@@ -491,7 +490,7 @@ __global__ void __launch_bounds__(kMaxConsWarps * 32 + 32, 1)
   unsigned gen = 0;
   Cursor cur;
   const int cc0 = (int)((long long)c * d / G), cc1 = (int)((long long)(c + 1) * d / G);
-  if (a.trace && tid == 0) a.trace[(size_t)c * 8 + 0] = globaltimer();
+  if (a.trace && tid == 0) a.trace[(size_t)c * 16 + 0] = globaltimer();
   // routing of layer 0: the router GEMV itself, redundantly in every CTA
   for (int e = tid; e < E; e += ncons) s_so[e] = a.slot_of[e];
   for (int e = warp; e < E; e += ncw) {
@@ -502,14 +501,14 @@ __global__ void __launch_bounds__(kMaxConsWarps * 32 + 32, 1)
     if (lane == 0) logits[e] = s;
   }
   named_bar_sync(2, ncons);
-  if (tid == 0) commit_route(0);
+  if (warp == 0) commit_route(0);
   named_bar_sync(2, ncons);
 
   for (int l = 0; l < a.L; ++l) {
     const bool more = l + 1 < a.L;
     const float* xl = (l == 0) ? a.x : a.xbuf + (size_t)(l & 1) * d;
     float* xn = more ? a.xbuf + (size_t)((l + 1) & 1) * d : a.x;
-    unsigned long long* tr = a.trace ? a.trace + ((size_t)l * G + c) * 8 : nullptr;
+    unsigned long long* tr = a.trace ? a.trace + ((size_t)l * G + c) * 16 : nullptr;
     if (more)
       for (int e = tid; e < E; e += ncons) s_so[e] = a.slot_of[(size_t)(l + 1) * E + e];
 
@@ -567,6 +566,7 @@ __global__ void __launch_bounds__(kMaxConsWarps * 32 + 32, 1)
         a.rpart[(size_t)e * G + c] = t;
       }
     }
+    if (tr && tid == 0) tr[11] = globaltimer();
     grid_sync(a.gbar, (++gen) * (unsigned)G, ncons);
     if (tr && tid == 0) tr[3] = globaltimer();
 
@@ -577,8 +577,11 @@ __global__ void __launch_bounds__(kMaxConsWarps * 32 + 32, 1)
         s = warp_sum(s);
         if (lane == 0) logits[e] = s;
       }
+      if (tr && tid == 0) tr[8] = globaltimer();
       named_bar_sync(2, ncons);
-      if (tid == 0) commit_route(l + 1);
+      if (tr && tid == 0) tr[9] = globaltimer();
+      if (warp == 0) commit_route(l + 1);
+      if (tr && tid == 0) tr[10] = globaltimer();
     }
 
     // ---- C: this CTA's column chunk of x_{l+1} = x_l + sum_c ypart_c ----
@@ -599,7 +602,7 @@ __global__ void __launch_bounds__(kMaxConsWarps * 32 + 32, 1)
     if (more) grid_sync(a.gbar, (++gen) * (unsigned)G, ncons);
     if (tr && tid == 0) {
       tr[5] = globaltimer();
-      if (more) a.trace[((size_t)(l + 1) * G + c) * 8 + 0] = tr[3];
+      if (more) a.trace[((size_t)(l + 1) * G + c) * 16 + 0] = tr[3];
     }
   }
 }

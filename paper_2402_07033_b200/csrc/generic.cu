@@ -41,7 +41,7 @@ __global__ void __launch_bounds__(256) router_topk_kernel(const float* __restric
     if (lane == 0) logits[e] = s;
   }
   __syncthreads();
-  if (tid == 0) topk_softmax(logits, E, k, ids + (size_t)blockIdx.x * k, gates + (size_t)blockIdx.x * k);
+  if (warp == 0) warp_topk_softmax(logits, E, k, ids + (size_t)blockIdx.x * k, gates + (size_t)blockIdx.x * k);
 }
 
 cudaError_t launch_router_topk(const float* router, const float* x, int n_tok, const Dims& dm,

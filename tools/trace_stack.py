@@ -56,6 +56,12 @@ def main():
                 "reduce_ns": np.median(t[:, 4] - t[:, 3]),
                 "barrier2_ns": np.median(t[:, 5] - t[:, 4]),
                 "issue_done_before_stream_end_ns": np.median(t[:, 2] - t[:, 7]),
+                "z_ns": np.median(t[:, 11] - t[:, 2]),
+                "route_sum_ns": np.median(t[:, 8] - t[:, 0]),
+                "route_bar_ns": np.median(t[:, 9] - t[:, 8]),
+                "route_topk_ns": np.median(t[:, 10] - t[:, 9]),
+                "route_wake_ns": np.median(t[:, 6] - t[:, 10]),
+                "barrier1_after_last_z_ns": t[:, 3].max() - t[:, 11].max(),
             })
         total = tr[L - 1, :, 5].max() - t0
         avg = {k: float(np.mean([r[k] for r in rows[1:]])) for k in rows[0]}
