@@ -103,7 +103,9 @@ struct DevBuf {
     bytes = 0;
     cudaError_t e = cudaMalloc(&p, n);
     if (e != cudaSuccess) return fail(MOE_ERR_OOM, "cudaMalloc scratch failed");
-    cudaMemset(p, 0, n);
+    // legacy-stream memset: wait for it, the kernels run on non-blocking streams
+    if (cudaMemset(p, 0, n) != cudaSuccess || cudaDeviceSynchronize() != cudaSuccess)
+      return fail(MOE_ERR_CUDA, "scratch memset failed");
     bytes = n;
     return MOE_OK;
   }
@@ -503,7 +505,8 @@ int moe_weights_create(moe_ctx* c, const moe_shape* shape, int dtype, const int3
   const size_t rbytes = (size_t)std::max(1, L) * E * shape->hidden_dim * 4;
   if (cudaMalloc(&w->router, rbytes) != cudaSuccess)
     return cleanup(fail(MOE_ERR_OOM, "cudaMalloc router"));
-  cudaMemset(w->router, 0, rbytes);
+  if (cudaMemset(w->router, 0, rbytes) != cudaSuccess || cudaDeviceSynchronize() != cudaSuccess)
+    return cleanup(fail(MOE_ERR_CUDA, "router memset failed"));
   w->device_bytes += rbytes;
   w->plan = moe::plan_decode(w->dims(), c->sm_count);
   if (const char* env = getenv("MOE_B200_STACK")) w->stack_enabled = env[0] != '0';
