@@ -106,7 +106,7 @@ __device__ __forceinline__ void consume_rows(const Ring& R, Cursor& cur, const f
   int p = 0;
   auto acquire = [&]() -> const uint8_t* {
     if (cur.slot == 0) mbar_wait(&R.full[cur.stage], cur.phase);
-    if (t_first != nullptr && p == 0 && tid == 0) *t_first = globaltimer();
+    if (t_first != nullptr && p == 0 && tid == 0) *t_first = clock64();
     return R.buf + (size_t)cur.stage * R.stage_bytes + (size_t)cur.slot * R.row_bytes;
   };
   auto release = [&]() {
@@ -454,13 +454,13 @@ __global__ void __launch_bounds__(kMaxConsWarps * 32 + 32, 1)
     Cursor cur;
     for (int l = 0; l < a.L; ++l) {
       mbar_wait(&route_bar, (uint32_t)(l & 1));
-      if (a.trace) a.trace[((size_t)l * G + c) * 16 + 6] = globaltimer();
+      if (a.trace) a.trace[((size_t)l * G + c) * 16 + 6] = clock64();
       const long long T = (long long)s_nloc * a.f;
       const long long g0 = (long long)c * T / G, g1 = (long long)(c + 1) * T / G;
       if (g1 > g0)
         produce_rows<W>(R, cur, reinterpret_cast<const W*>(a.layer_experts[l]), a.expert_stride,
                         a.mat_stride, s_slot, a.f, d, g0, g1, pol);
-      if (a.trace) a.trace[((size_t)l * G + c) * 16 + 7] = globaltimer();
+      if (a.trace) a.trace[((size_t)l * G + c) * 16 + 7] = clock64();
     }
     return;
   }
@@ -490,7 +490,11 @@ __global__ void __launch_bounds__(kMaxConsWarps * 32 + 32, 1)
   unsigned gen = 0;
   Cursor cur;
   const int cc0 = (int)((long long)c * d / G), cc1 = (int)((long long)(c + 1) * d / G);
-  if (a.trace && tid == 0) a.trace[(size_t)c * 16 + 0] = globaltimer();
+  if (a.trace && tid == 0) {
+    a.trace[(size_t)c * 16 + 12] = clock64();
+    a.trace[(size_t)c * 16 + 13] = globaltimer();
+    a.trace[(size_t)c * 16 + 0] = clock64();
+  }
   // routing of layer 0: the router GEMV itself, redundantly in every CTA
   for (int e = tid; e < E; e += ncons) s_so[e] = a.slot_of[e];
   for (int e = warp; e < E; e += ncw) {
@@ -522,7 +526,7 @@ __global__ void __launch_bounds__(kMaxConsWarps * 32 + 32, 1)
     const long long g0 = (long long)c * T / G, g1 = (long long)(c + 1) * T / G;
     consume_rows<W, NV>(R, cur, xr, yacc, s_gate, a.f, g0, g1, red, h_s, tid, ncons, 1,
                         tr ? tr + 1 : nullptr);
-    if (tr && tid == 0) tr[2] = globaltimer();
+    if (tr && tid == 0) tr[2] = clock64();
     store_y<W, NV>(a.ypart + (size_t)c * d, yacc, tid, ncons);
 
     // ---- z_c = R_{l+1} (ypart_c [+ x_l]) : next layer's router partial ----
@@ -566,9 +570,9 @@ __global__ void __launch_bounds__(kMaxConsWarps * 32 + 32, 1)
         a.rpart[(size_t)e * G + c] = t;
       }
     }
-    if (tr && tid == 0) tr[11] = globaltimer();
+    if (tr && tid == 0) tr[11] = clock64();
     grid_sync(a.gbar, (++gen) * (unsigned)G, ncons);
-    if (tr && tid == 0) tr[3] = globaltimer();
+    if (tr && tid == 0) tr[3] = clock64();
 
     // ---- A(l+1): route the next layer and release the producer ----
     if (more) {
@@ -577,11 +581,11 @@ __global__ void __launch_bounds__(kMaxConsWarps * 32 + 32, 1)
         s = warp_sum(s);
         if (lane == 0) logits[e] = s;
       }
-      if (tr && tid == 0) tr[8] = globaltimer();
+      if (tr && tid == 0) tr[8] = clock64();
       named_bar_sync(2, ncons);
-      if (tr && tid == 0) tr[9] = globaltimer();
+      if (tr && tid == 0) tr[9] = clock64();
       if (warp == 0) commit_route(l + 1);
-      if (tr && tid == 0) tr[10] = globaltimer();
+      if (tr && tid == 0) tr[10] = clock64();
     }
 
     // ---- C: this CTA's column chunk of x_{l+1} = x_l + sum_c ypart_c ----
@@ -598,10 +602,14 @@ __global__ void __launch_bounds__(kMaxConsWarps * 32 + 32, 1)
       }
       named_bar_sync(2, ncons);
     }
-    if (tr && tid == 0) tr[4] = globaltimer();
+    if (tr && tid == 0) tr[4] = clock64();
     if (more) grid_sync(a.gbar, (++gen) * (unsigned)G, ncons);
     if (tr && tid == 0) {
-      tr[5] = globaltimer();
+      tr[5] = clock64();
+      if (!more) {  // calibration pair at the end (row of layer 0)
+        a.trace[(size_t)c * 16 + 14] = clock64();
+        a.trace[(size_t)c * 16 + 15] = globaltimer();
+      }
       if (more) a.trace[((size_t)(l + 1) * G + c) * 16 + 0] = tr[3];
     }
   }

@@ -1,10 +1,15 @@
-"""Per-phase timing of the persistent stack kernel from %globaltimer stamps.
+"""Per-phase timing of the persistent stack kernel (moe_debug_trace_forward).
 
-    python tools/trace_stack.py [--layers 32] [--reps 3]
+    python tools/trace_stack.py [--layers 32] [--reps 3] [--out f.json]
 
-Stamps per (layer, CTA): 0 layer start, 1 first ring stage landed, 2 stream
-done, 3 after grid barrier 1, 4 reduce done, 5 after grid barrier 2,
-6 producer released, 7 producer issued last copy (see moe_debug_trace_forward).
+Stamps are SM clock64 values per (layer, CTA) (slot meanings below); slots
+12..15 of layer 0 hold (clock64, globaltimer) pairs at kernel start/end used
+to convert cycles to ns and to align CTAs (alignment error ~1 us; intra-CTA
+intervals are cycle-exact).
+  0 routing start (after the previous layer's barrier 1)   6 producer released
+  1 first ring stage landed   2 stream done   11 router partial (z) written
+  3 after barrier 1   8 logits summed   9 after CTA barrier   10 top-k committed
+  4 residual chunk done   5 after barrier 2   7 producer issued its last copy
 """
 import argparse
 import json
@@ -14,6 +19,15 @@ import sys
 import numpy as np
 
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+
+
+def to_ns(tr):
+    """[L][G][16] clock64 -> ns on a common timeline."""
+    c0, g0, c1, g1 = (tr[0, :, i].astype(np.float64) for i in (12, 13, 14, 15))
+    rate = (c1 - c0) / np.maximum(g1 - g0, 1.0)  # cycles per ns, per CTA
+    off = g0 - g0.min()
+    out = (tr.astype(np.float64) - c0[None, :, None]) / rate[None, :, None] + off[None, :, None]
+    return out, float(np.median(rate))
 
 
 def main():
@@ -40,32 +54,33 @@ def main():
     torch.cuda.synchronize()
     res = []
     for _ in range(args.reps):
-        tr = w.debug_trace_forward(x, ids, g).astype(np.float64)  # [L][G][8] ns
-        t0 = tr[0, :, 0].min()
+        raw = w.debug_trace_forward(x, ids, g)
+        t, ghz = to_ns(raw)
+        med = lambda a: float(np.median(a))  # noqa: E731
         rows = []
-        for l in range(L):
-            t = tr[l]
-            start = t[:, 0].min()
+        for l in range(1, L - 1):
+            tl = t[l]
             rows.append({
-                "layer_ns": (tr[l + 1, :, 0].min() if l + 1 < L else t[:, 5].max()) - start,
-                "route_ns": np.median(t[:, 6] - t[:, 0]),
-                "first_stage_ns": np.median(t[:, 1] - t[:, 6]),
-                "stream_med_ns": np.median(t[:, 2] - t[:, 1]),
-                "stream_end_spread_ns": t[:, 2].max() - t[:, 2].min(),
-                "barrier1_after_last_ns": t[:, 3].max() - t[:, 2].max(),
-                "reduce_ns": np.median(t[:, 4] - t[:, 3]),
-                "barrier2_ns": np.median(t[:, 5] - t[:, 4]),
-                "issue_done_before_stream_end_ns": np.median(t[:, 2] - t[:, 7]),
-                "z_ns": np.median(t[:, 11] - t[:, 2]),
-                "route_sum_ns": np.median(t[:, 8] - t[:, 0]),
-                "route_bar_ns": np.median(t[:, 9] - t[:, 8]),
-                "route_topk_ns": np.median(t[:, 10] - t[:, 9]),
-                "route_wake_ns": np.median(t[:, 6] - t[:, 10]),
-                "barrier1_after_last_z_ns": t[:, 3].max() - t[:, 11].max(),
+                "layer_ns": t[l + 1, :, 0].min() - tl[:, 0].min(),
+                "route_sum_ns": med(tl[:, 8] - tl[:, 0]) if l > 0 else 0.0,
+                "route_bar_ns": med(tl[:, 9] - tl[:, 8]),
+                "route_topk_ns": med(tl[:, 10] - tl[:, 9]),
+                "producer_wake_ns": med(t[l + 1, :, 6] - tl[:, 10]),
+                "first_stage_after_release_ns": med(tl[:, 1] - tl[:, 6]),
+                "stream_ns": med(tl[:, 2] - tl[:, 1]),
+                "stream_end_spread_ns": tl[:, 2].max() - tl[:, 2].min(),
+                "z_ns": med(tl[:, 11] - tl[:, 2]),
+                "barrier1_after_last_ns": tl[:, 3].max() - tl[:, 11].max(),
+                "barrier1_wait_med_ns": med(tl[:, 3] - tl[:, 11]),
+                "route_plus_reduce_ns": med(tl[:, 4] - tl[:, 3]),
+                "barrier2_ns": med(tl[:, 5] - tl[:, 4]),
+                "consumer_restart_ns": med(t[l + 1, :, 1] - tl[:, 5]),
+                "issue_done_before_stream_end_ns": med(tl[:, 2] - tl[:, 7]),
             })
-        total = tr[L - 1, :, 5].max() - t0
-        avg = {k: float(np.mean([r[k] for r in rows[1:]])) for k in rows[0]}
-        res.append({"total_us": total / 1e3, "per_layer_avg_ns_excl_l0": avg})
+        total = t[L - 1, :, 5].max() - t[0, :, 0].min()
+        avg = {k: round(float(np.mean([r[k] for r in rows])), 1) for k in rows[0]}
+        res.append({"total_us": round(total / 1e3, 2), "sm_ghz": round(ghz, 3),
+                    "per_layer_avg_ns_layers_1_to_L-2": avg})
     print(json.dumps(res[-1], indent=1))
     if args.out:
         json.dump(res, open(args.out, "w"), indent=1)
