@@ -123,38 +123,24 @@ __device__ __forceinline__ void consume_rows(const Ring& R, Cursor& cur, const f
     const int nb = (int)min((long long)kBatch, min(g1 - g, (long long)(f - r)));
     const float gate = s_gate[jj];
 
-    // -- up: W1 rows [0,nb) then W3 rows [0,nb) of this batch
-    float acc[2 * kBatch];
+    // -- up: W1 rows [0,nb) then W3 rows [0,nb) of this batch.  Rolled loops
+    //    (small code: the layer-boundary code stays I-cache resident); each
+    //    row's partial dot is warp-reduced at once, lane 0 parks it in smem.
+    for (int q = 0; q < 2 * nb; ++q) {
+      const uint8_t* row = acquire();
+      float s = 0.f;
 #pragma unroll
-    for (int q = 0; q < 2 * kBatch; ++q) {
-      acc[q] = 0.f;
-      if ((q & (kBatch - 1)) < nb) {
-        const uint8_t* row = acquire();
-        float s = 0.f;
+      for (int m = 0; m < NV; ++m) {
+        const uint4 v = lds128(row + (size_t)(tid + m * ncons) * 16);
+        float w[VEC];
+        Elem<W>::unpack(v, w);
 #pragma unroll
-        for (int m = 0; m < NV; ++m) {
-          const uint4 v = lds128(row + (size_t)(tid + m * ncons) * 16);
-          float w[VEC];
-          Elem<W>::unpack(v, w);
-#pragma unroll
-          for (int i = 0; i < VEC; ++i) s = fmaf(w[i], xr[m * VEC + i], s);
-        }
-        acc[q] = s;
-        release();
+        for (int i = 0; i < VEC; ++i) s = fmaf(w[i], xr[m * VEC + i], s);
       }
+      release();
+      s = warp_sum(s);
+      if (lane == 0) red[warp * 32 + (q < nb ? q : kBatch + q - nb)] = s;
     }
-    // butterfly reduce-scatter: lane l ends with the warp sum of item l
-#pragma unroll
-    for (int s = 16; s >= 1; s >>= 1) {
-      const bool hi = (lane & s) != 0;
-#pragma unroll
-      for (int i = 0; i < s; ++i) {
-        const float send = hi ? acc[i] : acc[i + s];
-        const float keep = hi ? acc[i + s] : acc[i];
-        acc[i] = keep + __shfl_xor_sync(MOE_FULL_MASK, send, s);
-      }
-    }
-    red[warp * 32 + lane] = acc[0];
     named_bar_sync(bar_id, ncons);
     if (warp == 0) {
       float tot = 0.f;
@@ -165,21 +151,18 @@ __device__ __forceinline__ void consume_rows(const Ring& R, Cursor& cur, const f
     named_bar_sync(bar_id, ncons);
 
     // -- down: W2T rows [0,nb): y += h[q] * W2T[r+q][:]
+    for (int q = 0; q < nb; ++q) {
+      const uint8_t* row = acquire();
+      const float hq = h_s[q];
 #pragma unroll
-    for (int q = 0; q < kBatch; ++q) {
-      if (q < nb) {
-        const uint8_t* row = acquire();
-        const float hq = h_s[q];
+      for (int m = 0; m < NV; ++m) {
+        const uint4 v = lds128(row + (size_t)(tid + m * ncons) * 16);
+        float w[VEC];
+        Elem<W>::unpack(v, w);
 #pragma unroll
-        for (int m = 0; m < NV; ++m) {
-          const uint4 v = lds128(row + (size_t)(tid + m * ncons) * 16);
-          float w[VEC];
-          Elem<W>::unpack(v, w);
-#pragma unroll
-          for (int i = 0; i < VEC; ++i) yacc[m * VEC + i] = fmaf(hq, w[i], yacc[m * VEC + i]);
-        }
-        release();
+        for (int i = 0; i < VEC; ++i) yacc[m * VEC + i] = fmaf(hq, w[i], yacc[m * VEC + i]);
       }
+      release();
     }
     g += nb;
   }
