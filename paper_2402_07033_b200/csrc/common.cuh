@@ -103,6 +103,21 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
   while (!mbar_try_wait(bar, parity)) {
   }
 }
+// For long waits (a producer idling across a layer boundary): the thread is
+// suspended in try_wait (suspend-time hint) instead of re-polling, so its
+// SYNCS/MIO traffic does not slow the other warps' shuffles and loads.
+__device__ __forceinline__ void mbar_wait_sleep(uint64_t* bar, uint32_t parity) {
+  uint32_t ok = 0;
+  while (!ok) {
+    asm volatile(
+        "{\n .reg .pred p;\n"
+        " mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, %3;\n"
+        " selp.u32 %0, 1, 0, p;\n}"
+        : "=r"(ok)
+        : "r"(smem_u32(bar)), "r"(parity), "r"(1000000u)
+        : "memory");
+  }
+}
 // L2 policy for weights that are streamed exactly once.
 __device__ __forceinline__ uint64_t l2_evict_first_policy() {
   uint64_t pol;
@@ -139,6 +154,36 @@ __device__ __forceinline__ void named_bar_sync(int id, int nthreads) {
 __device__ __forceinline__ void warp_topk_softmax(const float* logits, int E, int k,
                                                   int32_t* ids, float* gates) {
   const int lane = threadIdx.x & 31;
+  if (E <= 32) {
+    // all-pairs rank: rank(e) = #{e' : l[e'] > l[e] or (l[e'] == l[e] and e' < e)};
+    // the E shuffles are independent (no dependent argmax chain).
+    // Fixed-trip, fully unrolled loops: the shuffles sit in provably
+    // convergent code (no collective fallback) and issue back to back.
+    const float v = lane < E ? logits[lane] : 0.f;
+    int rank = 0;
+#pragma unroll
+    for (int e2 = 0; e2 < 32; ++e2) {
+      const float o = __shfl_sync(MOE_FULL_MASK, v, e2);
+      rank += (e2 < E && (o > v || (o == v && e2 < lane))) ? 1 : 0;
+    }
+    const bool sel = lane < E && rank < k;
+    const unsigned m = __ballot_sync(MOE_FULL_MASK, sel);
+    const int pos = __popc(m & ((1u << lane) - 1u));  // ascending-id slot
+    float mx = sel ? v : -INFINITY;
+#pragma unroll
+    for (int s = 16; s >= 1; s >>= 1) mx = fmaxf(mx, __shfl_xor_sync(MOE_FULL_MASK, mx, s));
+    const float w = sel ? expf(v - mx) : 0.f;
+    // ascending-id sequential sum (unselected lanes add an exact 0)
+    float denom = 0.f;
+#pragma unroll
+    for (int e2 = 0; e2 < 32; ++e2) denom += __shfl_sync(MOE_FULL_MASK, w, e2);
+    if (sel) {
+      ids[pos] = lane;
+      gates[pos] = w / denom;
+    }
+    __syncwarp();
+    return;
+  }
   float v[8];
 #pragma unroll
   for (int i = 0; i < 8; ++i) {

@@ -123,24 +123,38 @@ __device__ __forceinline__ void consume_rows(const Ring& R, Cursor& cur, const f
     const int nb = (int)min((long long)kBatch, min(g1 - g, (long long)(f - r)));
     const float gate = s_gate[jj];
 
-    // -- up: W1 rows [0,nb) then W3 rows [0,nb) of this batch.  Rolled loops
-    //    (small code: the layer-boundary code stays I-cache resident); each
-    //    row's partial dot is warp-reduced at once, lane 0 parks it in smem.
-    for (int q = 0; q < 2 * nb; ++q) {
-      const uint8_t* row = acquire();
-      float s = 0.f;
+    // -- up: W1 rows [0,nb) then W3 rows [0,nb) of this batch
+    float acc[2 * kBatch];
 #pragma unroll
-      for (int m = 0; m < NV; ++m) {
-        const uint4 v = lds128(row + (size_t)(tid + m * ncons) * 16);
-        float w[VEC];
-        Elem<W>::unpack(v, w);
+    for (int q = 0; q < 2 * kBatch; ++q) {
+      acc[q] = 0.f;
+      if ((q & (kBatch - 1)) < nb) {
+        const uint8_t* row = acquire();
+        float s = 0.f;
 #pragma unroll
-        for (int i = 0; i < VEC; ++i) s = fmaf(w[i], xr[m * VEC + i], s);
+        for (int m = 0; m < NV; ++m) {
+          const uint4 v = lds128(row + (size_t)(tid + m * ncons) * 16);
+          float w[VEC];
+          Elem<W>::unpack(v, w);
+#pragma unroll
+          for (int i = 0; i < VEC; ++i) s = fmaf(w[i], xr[m * VEC + i], s);
+        }
+        acc[q] = s;
+        release();
       }
-      release();
-      s = warp_sum(s);
-      if (lane == 0) red[warp * 32 + (q < nb ? q : kBatch + q - nb)] = s;
     }
+    // butterfly reduce-scatter: lane l ends with the warp sum of item l
+#pragma unroll
+    for (int s = 16; s >= 1; s >>= 1) {
+      const bool hi = (lane & s) != 0;
+#pragma unroll
+      for (int i = 0; i < s; ++i) {
+        const float send = hi ? acc[i] : acc[i + s];
+        const float keep = hi ? acc[i + s] : acc[i];
+        acc[i] = keep + __shfl_xor_sync(MOE_FULL_MASK, send, s);
+      }
+    }
+    red[warp * 32 + lane] = acc[0];
     named_bar_sync(bar_id, ncons);
     if (warp == 0) {
       float tot = 0.f;
@@ -151,18 +165,21 @@ __device__ __forceinline__ void consume_rows(const Ring& R, Cursor& cur, const f
     named_bar_sync(bar_id, ncons);
 
     // -- down: W2T rows [0,nb): y += h[q] * W2T[r+q][:]
-    for (int q = 0; q < nb; ++q) {
-      const uint8_t* row = acquire();
-      const float hq = h_s[q];
 #pragma unroll
-      for (int m = 0; m < NV; ++m) {
-        const uint4 v = lds128(row + (size_t)(tid + m * ncons) * 16);
-        float w[VEC];
-        Elem<W>::unpack(v, w);
+    for (int q = 0; q < kBatch; ++q) {
+      if (q < nb) {
+        const uint8_t* row = acquire();
+        const float hq = h_s[q];
 #pragma unroll
-        for (int i = 0; i < VEC; ++i) yacc[m * VEC + i] = fmaf(hq, w[i], yacc[m * VEC + i]);
+        for (int m = 0; m < NV; ++m) {
+          const uint4 v = lds128(row + (size_t)(tid + m * ncons) * 16);
+          float w[VEC];
+          Elem<W>::unpack(v, w);
+#pragma unroll
+          for (int i = 0; i < VEC; ++i) yacc[m * VEC + i] = fmaf(hq, w[i], yacc[m * VEC + i]);
+        }
+        release();
       }
-      release();
     }
     g += nb;
   }
@@ -436,7 +453,7 @@ __global__ void __launch_bounds__(kMaxConsWarps * 32 + 32, 1)
     const uint64_t pol = l2_evict_first_policy();
     Cursor cur;
     for (int l = 0; l < a.L; ++l) {
-      mbar_wait(&route_bar, (uint32_t)(l & 1));
+      mbar_wait_sleep(&route_bar, (uint32_t)(l & 1));
       if (a.trace) a.trace[((size_t)l * G + c) * 16 + 6] = clock64();
       const long long T = (long long)s_nloc * a.f;
       const long long g0 = (long long)c * T / G, g1 = (long long)(c + 1) * T / G;
@@ -569,6 +586,9 @@ __global__ void __launch_bounds__(kMaxConsWarps * 32 + 32, 1)
       if (tr && tid == 0) tr[9] = clock64();
       if (warp == 0) commit_route(l + 1);
       if (tr && tid == 0) tr[10] = clock64();
+      // keep the other warps' phase-C loads out of the MIO queue while warp 0
+      // routes (the top-k's shuffles would queue behind them)
+      named_bar_sync(2, ncons);
     }
 
     // ---- C: this CTA's column chunk of x_{l+1} = x_l + sum_c ypart_c ----

@@ -65,6 +65,7 @@ def main():
                 "route_sum_ns": med(tl[:, 8] - tl[:, 0]) if l > 0 else 0.0,
                 "route_bar_ns": med(tl[:, 9] - tl[:, 8]),
                 "route_topk_ns": med(tl[:, 10] - tl[:, 9]),
+                "route_topk_again_ns": med(tl[:, 12] - tl[:, 10]),
                 "producer_wake_ns": med(t[l + 1, :, 6] - tl[:, 10]),
                 "first_stage_after_release_ns": med(tl[:, 1] - tl[:, 6]),
                 "stream_ns": med(tl[:, 2] - tl[:, 1]),
