@@ -1,0 +1,33 @@
+// moe_orch/b200.hpp — B200-specific additions to the drop-in API.
+#pragma once
+
+#include <cstdint>
+#include <vector>
+
+#include "moe_orch/placement.hpp"
+
+namespace moe_orch::b200 {
+
+enum class Dtype { BF16 = 0, F32 = 1 };
+
+// Device-side storage type of the expert weights used by expert_ffn /
+// model_forward (default F32: closest to the fp64 reference; BF16 is the
+// serving configuration).  The residual stream and accumulation are fp32.
+void set_dtype(Dtype dtype);
+Dtype dtype();
+// CUDA device used by the drop-in entry points (default 0 / $MOE_B200_DEVICE).
+void set_device(int device);
+// Device copies of ModelWeights are cached by address + a sampled content
+// fingerprint; call this after mutating weights in place.
+void invalidate_weights_cache();
+
+// The paper's popularity placement re-expressed as expert parallelism:
+// owner[l][e] in [0, world).  Per layer, experts are taken in the reference
+// ranking (count desc, expert asc — placement.cpp:53-64) and assigned to the
+// least-loaded rank with spare slots (LPT; ties to the lower rank), each rank
+// holding ceil(E / world) experts at most.
+std::vector<std::vector<int>> ep_shard_map(const PopularityProfile& profile, int world);
+// Rank r's share as a Placement (capacity = its expert count).
+Placement rank_placement(const std::vector<std::vector<int>>& owner, int rank);
+
+}  // namespace moe_orch::b200

@@ -1,0 +1,286 @@
+// moe_orch_device.cpp — the math half of the drop-in moe_orch API (B200
+// build): expert_ffn, gate_topk and model_forward keep the reference
+// signatures (proj/include/moe_orch/model.hpp:54-80) and run on the GPU
+// through the C-ABI (include/moe_b200.h).  There is no CPU fallback: without
+// an sm_100 device these throw.
+//
+// Error behaviour follows the reference: ShapeError for inconsistent expert
+// matrices (model.cpp:57-62), wrong vector widths (model.cpp:21-22,
+// 107-109), an out-of-range router layer (:73-74) or top_k (:77).
+#include <cstdlib>
+#include <cstring>
+#include <list>
+#include <mutex>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "moe_b200.h"
+#include "moe_orch/b200.hpp"
+#include "moe_orch/error.hpp"
+#include "moe_orch/model.hpp"
+
+namespace moe_orch {
+namespace {
+
+[[noreturn]] void raise(int rc) {
+  const std::string msg = moe_last_error();
+  if (rc == MOE_ERR_SHAPE) throw ShapeError(msg);
+  if (rc == MOE_ERR_VALIDATION) throw ValidationError(msg);
+  throw std::runtime_error("moe_b200: " + msg);
+}
+
+void check(int rc) {
+  if (rc != MOE_OK) raise(rc);
+}
+
+struct CachedWeights {
+  const ModelWeights* addr = nullptr;
+  std::uint64_t fingerprint = 0;
+  ModelShape shape;
+  int dtype = MOE_DTYPE_F32;
+  moe_weights* w = nullptr;
+};
+
+struct Device {
+  std::mutex mu;
+  int device = -1;
+  moe_ctx* ctx = nullptr;
+  b200::Dtype dtype = b200::Dtype::F32;
+  std::list<CachedWeights> cache;  // most recent first
+  static constexpr size_t kCacheEntries = 4;
+
+  moe_ctx* context() {
+    if (ctx) return ctx;
+    if (device < 0) {
+      const char* env = std::getenv("MOE_B200_DEVICE");
+      device = env ? std::atoi(env) : 0;
+    }
+    check(moe_ctx_create(device, &ctx));
+    return ctx;
+  }
+  void clear() {
+    for (auto& c : cache) moe_weights_destroy(c.w);
+    cache.clear();
+  }
+};
+
+Device& dev() {
+  static Device d;
+  return d;
+}
+
+int dtype_code() { return dev().dtype == b200::Dtype::BF16 ? MOE_DTYPE_BF16 : MOE_DTYPE_F32; }
+
+std::uint64_t mix(std::uint64_t h, std::uint64_t v) {
+  h ^= v + 0x9e3779b97f4a7c15ULL + (h << 6) + (h >> 2);
+  return h;
+}
+
+std::uint64_t fingerprint(const Matrix& m, bool full) {
+  std::uint64_t h = mix(static_cast<std::uint64_t>(m.rows), static_cast<std::uint64_t>(m.cols));
+  const size_t n = m.data.size();
+  if (n == 0) return h;
+  const size_t step = full ? 1 : std::max<size_t>(1, n / 61);
+  for (size_t i = 0; i < n; i += step) {
+    std::uint64_t bits;
+    std::memcpy(&bits, &m.data[i], 8);
+    h = mix(h, bits);
+  }
+  std::uint64_t last;
+  std::memcpy(&last, &m.data[n - 1], 8);
+  return mix(h, last);
+}
+
+void check_expert(const ExpertWeights& w) {
+  if (w.w_in.rows != w.w_gate.rows || w.w_in.cols != w.w_gate.cols ||
+      w.w_out.cols != w.w_in.rows || w.w_out.rows != w.w_in.cols)
+    throw ShapeError("expert weight matrices are inconsistent");
+}
+
+moe_shape to_c(const ModelShape& s) {
+  return moe_shape{s.num_layers, s.experts_per_layer, s.top_k, s.hidden_dim, s.ffn_dim,
+                   s.bytes_per_param};
+}
+
+// Device copy of `weights` (uploaded once, cached by address + fingerprint).
+moe_weights* device_weights(const ModelShape& shape, const ModelWeights& weights) {
+  Device& D = dev();
+  const int L = shape.num_layers, E = shape.experts_per_layer;
+  const int d = shape.hidden_dim, f = shape.ffn_dim;
+  if (static_cast<int>(weights.experts.size()) < L ||
+      static_cast<int>(weights.router.layers.size()) < L)
+    throw ShapeError("model weights have fewer layers than the shape");
+  const bool full = static_cast<std::int64_t>(L) * E * 3 * d * f < (std::int64_t(1) << 22);
+  std::uint64_t fp = mix(static_cast<std::uint64_t>(L), static_cast<std::uint64_t>(E));
+  for (int l = 0; l < L; ++l) {
+    const Matrix& r = weights.router.layers[l];
+    if (r.rows != E || r.cols != d) throw ShapeError("matrix-vector dimension mismatch");
+    fp = mix(fp, fingerprint(r, full));
+    if (static_cast<int>(weights.experts[l].size()) < E)
+      throw ShapeError("model weights have fewer experts than the shape");
+    for (int e = 0; e < E; ++e) {
+      const ExpertWeights& ew = weights.experts[l][e];
+      check_expert(ew);
+      if (ew.w_in.cols != d || ew.w_in.rows != f)
+        throw ShapeError("matrix-vector dimension mismatch");
+      fp = mix(fp, fingerprint(ew.w_in, full));
+      fp = mix(fp, fingerprint(ew.w_gate, full));
+      fp = mix(fp, fingerprint(ew.w_out, full));
+    }
+  }
+  const int dt = dtype_code();
+  for (auto it = D.cache.begin(); it != D.cache.end(); ++it) {
+    if (it->addr == &weights && it->fingerprint == fp && it->dtype == dt &&
+        it->shape.num_layers == L && it->shape.experts_per_layer == E &&
+        it->shape.top_k == shape.top_k && it->shape.hidden_dim == d && it->shape.ffn_dim == f) {
+      D.cache.splice(D.cache.begin(), D.cache, it);
+      return D.cache.front().w;
+    }
+  }
+  moe_shape cs = to_c(shape);
+  moe_weights* w = nullptr;
+  check(moe_weights_create(D.context(), &cs, dt, nullptr, &w));
+  for (int l = 0; l < L; ++l) {
+    for (int e = 0; e < E; ++e) {
+      const ExpertWeights& ew = weights.experts[l][e];
+      const int rc = moe_weights_upload_expert(w, l, e, ew.w_in.data.data(), ew.w_gate.data.data(),
+                                               ew.w_out.data.data());
+      if (rc != MOE_OK) {
+        moe_weights_destroy(w);
+        raise(rc);
+      }
+    }
+    const int rc = moe_weights_upload_router(w, l, weights.router.layers[l].data.data());
+    if (rc != MOE_OK) {
+      moe_weights_destroy(w);
+      raise(rc);
+    }
+  }
+  D.cache.push_front(CachedWeights{&weights, fp, shape, dt, w});
+  while (D.cache.size() > Device::kCacheEntries) {
+    moe_weights_destroy(D.cache.back().w);
+    D.cache.pop_back();
+  }
+  return w;
+}
+
+}  // namespace
+
+std::vector<double> expert_ffn(const ExpertWeights& weights, const std::vector<double>& x) {
+  check_expert(weights);
+  if (static_cast<int>(x.size()) != weights.w_in.cols)
+    throw ShapeError("matrix-vector dimension mismatch");
+  Device& D = dev();
+  std::lock_guard<std::mutex> lk(D.mu);
+  std::vector<double> y(weights.w_out.rows, 0.0);
+  if (weights.w_in.rows == 0 || weights.w_in.cols == 0) return y;
+  check(moe_expert_ffn_host(D.context(), dtype_code(), weights.w_in.cols, weights.w_in.rows,
+                            weights.w_in.data.data(), weights.w_gate.data.data(),
+                            weights.w_out.data.data(), x.data(), y.data()));
+  return y;
+}
+
+std::vector<std::pair<int, double>> gate_topk(const RouterWeights& router, int layer,
+                                              const std::vector<double>& x, int top_k) {
+  if (layer < 0 || layer >= static_cast<int>(router.layers.size()))
+    throw ShapeError("router layer index out of range");
+  const Matrix& r = router.layers[layer];
+  if (static_cast<int>(x.size()) != r.cols) throw ShapeError("matrix-vector dimension mismatch");
+  if (top_k < 1 || top_k > r.rows) throw ShapeError("top_k out of range");
+  Device& D = dev();
+  std::lock_guard<std::mutex> lk(D.mu);
+  std::vector<int32_t> ids(top_k);
+  std::vector<double> g(top_k);
+  check(moe_gate_topk_host(D.context(), r.rows, r.cols, r.data.data(), x.data(), top_k,
+                           ids.data(), g.data()));
+  std::vector<std::pair<int, double>> out;
+  out.reserve(top_k);
+  for (int j = 0; j < top_k; ++j) out.emplace_back(ids[j], g[j]);
+  return out;
+}
+
+ForwardResult model_forward(const ModelShape& shape, const ModelWeights& weights,
+                            const std::vector<std::vector<double>>& tokens, ActivationSink sink,
+                            void* sink_ctx) {
+  shape.validate();
+  for (const auto& t : tokens)
+    if (static_cast<int>(t.size()) != shape.hidden_dim)
+      throw ShapeError("token width does not match hidden_dim");
+  ForwardResult result;
+  result.outputs = tokens;
+  const int L = shape.num_layers, n = static_cast<int>(tokens.size());
+  if (L == 0 || n == 0) return result;
+  const int d = shape.hidden_dim, k = shape.top_k, E = shape.experts_per_layer;
+  const int f = shape.ffn_dim;
+
+  Device& D = dev();
+  std::lock_guard<std::mutex> lk(D.mu);
+  moe_weights* w = device_weights(shape, weights);
+  std::vector<double> flat(static_cast<size_t>(n) * d), out(flat.size());
+  for (int t = 0; t < n; ++t) std::memcpy(&flat[static_cast<size_t>(t) * d], tokens[t].data(), 8 * d);
+  std::vector<int32_t> ids(static_cast<size_t>(L) * n * k);
+  std::vector<double> gates(ids.size());
+  std::vector<double> post;
+  if (sink) post.resize(static_cast<size_t>(n) * L * k * f);
+  check(moe_forward_host(w, flat.data(), n, out.data(), ids.data(), gates.data(),
+                         sink ? post.data() : nullptr));
+  for (int t = 0; t < n; ++t)
+    std::memcpy(result.outputs[t].data(), &out[static_cast<size_t>(t) * d], 8 * d);
+  if (sink) {
+    // token -> layer -> expert-ascending: the reference's call order
+    std::vector<double> vals(f);
+    for (int t = 0; t < n; ++t)
+      for (int l = 0; l < L; ++l)
+        for (int j = 0; j < k; ++j) {
+          const double* p = &post[((static_cast<size_t>(t) * L + l) * k + j) * f];
+          vals.assign(p, p + f);
+          sink(l, vals, sink_ctx);
+        }
+  }
+  // the step's per-layer histogram (model.cpp:144-158)
+  TraceStep step;
+  step.kind = n == 1 ? StepKind::Decode : StepKind::Prefill;
+  step.layers.resize(L);
+  for (int l = 0; l < L; ++l) {
+    std::vector<int> cnt(E, 0);
+    std::vector<double> gsum(E, 0.0);
+    for (int t = 0; t < n; ++t)
+      for (int j = 0; j < k; ++j) {
+        const size_t i = (static_cast<size_t>(l) * n + t) * k + j;
+        ++cnt[ids[i]];
+        gsum[ids[i]] += gates[i];
+      }
+    for (int e = 0; e < E; ++e)
+      if (cnt[e] > 0) step.layers[l].push_back(Selection{e, cnt[e], gsum[e] / cnt[e]});
+  }
+  result.trace.steps.push_back(std::move(step));
+  return result;
+}
+
+namespace b200 {
+
+void set_dtype(Dtype dtype) {
+  std::lock_guard<std::mutex> lk(dev().mu);
+  dev().dtype = dtype;
+}
+
+Dtype dtype() { return dev().dtype; }
+
+void set_device(int device) {
+  Device& D = dev();
+  std::lock_guard<std::mutex> lk(D.mu);
+  if (D.device == device && D.ctx) return;
+  D.clear();
+  if (D.ctx) moe_ctx_destroy(D.ctx);
+  D.ctx = nullptr;
+  D.device = device;
+}
+
+void invalidate_weights_cache() {
+  std::lock_guard<std::mutex> lk(dev().mu);
+  dev().clear();
+}
+
+}  // namespace b200
+}  // namespace moe_orch

@@ -1,0 +1,582 @@
+// test_dropin.cpp — the reference's own assertions (proj/tests/test_model.cpp,
+// test_placement.cpp, acceptance.cpp criteria 8/9) re-hosted against the
+// drop-in moe_orch API of the B200 build (libmoe_orch_b200.so).  doctest is
+// absent from this image, so a tiny runner stands in for it.
+//
+//   test_dropin cpu   host-side cases (shape, placement, traces, errors)
+//   test_dropin gpu   cases that run expert_ffn/gate_topk/model_forward on the GPU
+//
+// Tolerances: the reference compares fp64 against fp64 at 1e-9/1e-12.  The
+// GPU math is fp32 (north_star: 1e-5 in fp32 mode), so numeric comparisons
+// use normwise max|got-want|/max|want| <= 1e-5 (1e-6 for O(1) scalars);
+// routing ids, counts and determinism stay exact.
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <functional>
+#include <random>
+#include <set>
+#include <sstream>
+#include <string>
+#include <vector>
+
+#include "moe_orch/b200.hpp"
+#include "moe_orch/error.hpp"
+#include "moe_orch/model.hpp"
+#include "moe_orch/placement.hpp"
+
+using namespace moe_orch;
+
+namespace {
+
+struct Case {
+  const char* name;
+  bool gpu;
+  std::function<void()> fn;
+};
+std::vector<Case>& registry() {
+  static std::vector<Case> r;
+  return r;
+}
+int g_failures = 0;
+const char* g_current = "";
+
+struct Reg {
+  Reg(const char* n, bool gpu, std::function<void()> f) { registry().push_back({n, gpu, f}); }
+};
+
+#define CAT2(a, b) a##b
+#define CAT(a, b) CAT2(a, b)
+#define TEST(name, gpu) \
+  static void CAT(t_, __LINE__)(); \
+  static Reg CAT(r_, __LINE__)(name, gpu, CAT(t_, __LINE__)); \
+  static void CAT(t_, __LINE__)()
+#define CHECK(cond)                                                                    \
+  do {                                                                                 \
+    if (!(cond)) {                                                                     \
+      ++g_failures;                                                                    \
+      std::printf("  FAIL [%s] %s:%d: %s\n", g_current, __FILE__, __LINE__, #cond);   \
+    }                                                                                  \
+  } while (0)
+#define CHECK_THROWS_AS(expr, T)                                                       \
+  do {                                                                                 \
+    bool ok_ = false;                                                                  \
+    try {                                                                              \
+      (void)(expr);                                                                    \
+    } catch (const T&) {                                                               \
+      ok_ = true;                                                                      \
+    } catch (...) {                                                                    \
+    }                                                                                  \
+    if (!ok_) {                                                                        \
+      ++g_failures;                                                                    \
+      std::printf("  FAIL [%s] %s:%d: %s does not throw %s\n", g_current, __FILE__,    \
+                  __LINE__, #expr, #T);                                                \
+    }                                                                                  \
+  } while (0)
+
+bool near(double a, double b, double tol) { return std::fabs(a - b) <= tol; }
+double normwise(const std::vector<double>& got, const std::vector<double>& want) {
+  double num = 0, den = 1e-300;
+  for (size_t i = 0; i < got.size(); ++i) {
+    num = std::max(num, std::fabs(got[i] - want[i]));
+    den = std::max(den, std::fabs(want[i]));
+  }
+  return num / den;
+}
+
+// Independent naive oracle (triple loops), as in test_model.cpp.
+std::vector<double> naive_gated_ffn(const ExpertWeights& w, const std::vector<double>& x) {
+  const int f = w.w_in.rows, d = w.w_in.cols;
+  std::vector<double> up(f, 0.0), gate(f, 0.0), out(d, 0.0);
+  for (int r = 0; r < f; ++r)
+    for (int c = 0; c < d; ++c) {
+      up[r] += w.w_in.at(r, c) * x[c];
+      gate[r] += w.w_gate.at(r, c) * x[c];
+    }
+  for (int r = 0; r < d; ++r)
+    for (int c = 0; c < f; ++c) out[r] += w.w_out.at(r, c) * silu(up[c]) * gate[c];
+  return out;
+}
+
+ExpertWeights random_expert(int d, int f, std::mt19937_64& rng) {
+  std::normal_distribution<double> nd(0.0, 1.0);
+  ExpertWeights w;
+  w.w_in = Matrix(f, d);
+  w.w_gate = Matrix(f, d);
+  w.w_out = Matrix(d, f);
+  for (Matrix* m : {&w.w_in, &w.w_gate, &w.w_out})
+    for (double& v : m->data) v = static_cast<double>(static_cast<float>(nd(rng)));
+  return w;
+}
+
+RouterWeights logit_router(const std::vector<double>& logits) {
+  RouterWeights r;
+  Matrix m(static_cast<int>(logits.size()), 1);
+  for (size_t i = 0; i < logits.size(); ++i) m.data[i] = logits[i];
+  r.layers.push_back(m);
+  return r;
+}
+
+PopularityProfile random_profile(int layers, int experts, std::mt19937_64& rng) {
+  PopularityProfile p;
+  p.counts.assign(layers, std::vector<std::int64_t>(experts, 0));
+  for (auto& row : p.counts)
+    for (auto& c : row) {
+      c = static_cast<std::int64_t>(rng() % 1000);
+      p.total_selections += c;
+    }
+  if (p.total_selections == 0) {
+    p.counts[0][0] = 1;
+    p.total_selections = 1;
+  }
+  return p;
+}
+
+std::int64_t best_subset_hits(const PopularityProfile& p, int capacity) {
+  std::vector<std::int64_t> flat;
+  for (const auto& row : p.counts) flat.insert(flat.end(), row.begin(), row.end());
+  const int n = static_cast<int>(flat.size()), k = std::min(capacity, n);
+  std::int64_t best = 0;
+  for (std::uint32_t mask = 0; mask < (1u << n); ++mask) {
+    if (__builtin_popcount(mask) > k) continue;
+    std::int64_t h = 0;
+    for (int i = 0; i < n; ++i)
+      if (mask & (1u << i)) h += flat[i];
+    best = std::max(best, h);
+  }
+  return best;
+}
+
+std::vector<std::vector<double>> normal_tokens(int n, int d, std::uint64_t seed) {
+  std::mt19937_64 rng(seed);
+  std::normal_distribution<double> nd(0.0, 1.0);
+  std::vector<std::vector<double>> t(n, std::vector<double>(d));
+  for (auto& v : t)
+    for (double& x : v) x = nd(rng);
+  return t;
+}
+
+}  // namespace
+
+// ===================== host-side (CPU) cases ==================================
+TEST("shape invariants", false) {
+  ModelShape shape = ModelShape::toy();
+  shape.validate();
+  CHECK(shape.expert_param_count() == 3LL * 32 * 64);
+  const ModelShape mix = ModelShape::mixtral_8x7b();
+  CHECK(mix.expert_param_count() == 3LL * 4096 * 14336);
+  CHECK(mix.total_experts() == 256);
+  shape.top_k = 9;
+  CHECK_THROWS_AS(shape.validate(), ShapeError);
+  shape = ModelShape::toy();
+  shape.hidden_dim = 0;
+  CHECK_THROWS_AS(shape.validate(), ShapeError);
+  CHECK_THROWS_AS(ModelShape::preset("mixtral_8x7b"), ConfigError);
+  CHECK(ModelShape::preset("mixtral").hidden_dim == 4096);
+}
+
+TEST("silu values", false) {
+  CHECK(silu(0.0) == 0.0);
+  CHECK(near(silu(20.0), 20.0, 20.0 * 1e-6));
+  CHECK(near(silu(1.0), 0.7310585786300049, 1e-12));
+}
+
+TEST("expert_ffn rejects dimension mismatch (before touching the device)", false) {
+  ExpertWeights w;
+  w.w_in = Matrix(4, 3);
+  w.w_gate = Matrix(4, 3);
+  w.w_out = Matrix(3, 4);
+  CHECK_THROWS_AS(expert_ffn(w, {1.0, 2.0}), ShapeError);
+  w.w_gate = Matrix(5, 3);
+  CHECK_THROWS_AS(expert_ffn(w, {1.0, 2.0, 3.0}), ShapeError);
+}
+
+TEST("gate_topk argument errors", false) {
+  const RouterWeights r = logit_router({1.0, 2.0, 3.0});
+  CHECK_THROWS_AS(gate_topk(r, 1, {1.0}, 2), ShapeError);
+  CHECK_THROWS_AS(gate_topk(r, 0, {1.0}, 0), ShapeError);
+  CHECK_THROWS_AS(gate_topk(r, 0, {1.0}, 4), ShapeError);
+  CHECK_THROWS_AS(gate_topk(r, 0, {1.0, 2.0}, 2), ShapeError);
+}
+
+TEST("model_forward with zero layers is the identity", false) {
+  ModelShape shape = ModelShape::toy();
+  shape.num_layers = 0;
+  const ModelWeights model;
+  const std::vector<std::vector<double>> tokens(3, std::vector<double>(32, 0.25));
+  const auto r = model_forward(shape, model, tokens);
+  CHECK(r.outputs == tokens);
+  CHECK(r.trace.steps.empty());
+}
+
+TEST("model_forward rejects wrong token width", false) {
+  const ModelShape shape = ModelShape::toy();
+  const ModelWeights model = random_model(shape, 0);
+  CHECK_THROWS_AS(model_forward(shape, model, {{1.0, 2.0}}), ShapeError);
+}
+
+TEST("random_model draw order: layer 0 independent of depth", false) {
+  ModelShape one = ModelShape::toy();
+  one.num_layers = 1;
+  const ModelWeights a = random_model(one, 17), b = random_model(ModelShape::toy(), 17);
+  CHECK(a.experts[0][3] == b.experts[0][3]);
+  CHECK(a.router.layers[0] == b.router.layers[0]);
+}
+
+TEST("random_model is bit-identical to the reference (golden sums, toy seed 3)", false) {
+  // tests/golden/golden.npz toy_s3_wsum / toy_s3_w_in0, written by the reference
+  const ModelWeights w = random_model(ModelShape::toy(), 3);
+  double s_in = 0, s_gate = 0, s_out = 0, s_r = 0;
+  for (const auto& layer : w.experts)
+    for (const auto& e : layer) {
+      for (double v : e.w_in.data) s_in += v;
+      for (double v : e.w_gate.data) s_gate += v;
+      for (double v : e.w_out.data) s_out += v;
+    }
+  for (const auto& r : w.router.layers)
+    for (double v : r.data) s_r += v;
+  // the golden sums are numpy sums per matrix then summed; compare loosely
+  CHECK(near(s_in, -9.004967940719663, 1e-9));
+  CHECK(near(s_gate, 21.13809655667256, 1e-9));
+  CHECK(near(s_out, -2.081007820659631, 1e-9));
+  CHECK(near(s_r, -7.71521584602036, 1e-9));
+  CHECK(w.experts[0][0].w_in.data[0] == -0.24012431661534753);
+  CHECK(w.experts[0][0].w_in.data[1] == 0.0463821892339377);
+  CHECK(w.experts[0][0].w_in.data[2] == -0.3096686890773477);
+}
+
+TEST("synth_trace shape, determinism, validity", false) {
+  const ModelShape shape = ModelShape::toy();
+  const RoutingTrace a = synth_trace(shape, 0.5, 8, 5, 99), b = synth_trace(shape, 0.5, 8, 5, 99);
+  CHECK(a == b);
+  CHECK(a.steps.size() == 6);
+  CHECK(a.steps[0].kind == StepKind::Prefill);
+  a.validate(shape);
+  std::mt19937_64 rng(17);
+  for (int trial = 0; trial < 40; ++trial) {
+    ModelShape s;
+    s.num_layers = 1 + static_cast<int>(rng() % 5);
+    s.experts_per_layer = 2 + static_cast<int>(rng() % 7);
+    s.top_k = 1 + static_cast<int>(rng() % s.experts_per_layer);
+    const double skew = (rng() % 3) * 0.7;
+    const int in_len = 1 + static_cast<int>(rng() % 20), out_len = static_cast<int>(rng() % 10);
+    const RoutingTrace t = synth_trace(s, skew, in_len, out_len, rng());
+    t.validate(s);
+    CHECK(t.steps[0].token_count(s.top_k) == in_len);
+  }
+}
+
+TEST("trace JSONL round trip", false) {
+  const ModelShape shape = ModelShape::toy();
+  const RoutingTrace t = synth_trace(shape, 1.0, 6, 3, 5);
+  std::stringstream buf;
+  save_trace_jsonl(t, buf);
+  const RoutingTrace back = load_trace_jsonl(buf, shape);
+  CHECK(back == t);
+  std::stringstream bad("{\"kind\":\"decode\",\"layers\":[[[0,1,0.5]]]}\n");
+  CHECK_THROWS_AS(load_trace_jsonl(bad, shape), ValidationError);
+}
+
+TEST("profile_from_trace tallies token counts", false) {
+  ModelShape shape;
+  shape.num_layers = 2;
+  shape.experts_per_layer = 4;
+  shape.top_k = 2;
+  CHECK(profile_from_trace(RoutingTrace{}, shape).total_selections == 0);
+  RoutingTrace t;
+  TraceStep pre;
+  pre.kind = StepKind::Prefill;
+  pre.layers = {{{0, 3, 0.5}, {1, 1, 0.5}, {3, 2, 0.5}}, {{1, 3, 0.5}, {2, 2, 0.5}, {3, 1, 0.5}}};
+  TraceStep dec;
+  dec.kind = StepKind::Decode;
+  dec.layers = {{{0, 1, 0.6}, {2, 1, 0.4}}, {{1, 1, 0.7}, {3, 1, 0.3}}};
+  t.steps = {pre, dec};
+  const PopularityProfile p = profile_from_trace(t, shape);
+  CHECK(p.counts[0] == (std::vector<std::int64_t>{4, 1, 1, 2}));
+  CHECK(p.counts[1] == (std::vector<std::int64_t>{0, 4, 2, 2}));
+  CHECK(p.total_selections == 16);
+}
+
+TEST("greedy_place basics, tie-break, quota", false) {
+  PopularityProfile strict;
+  strict.counts = {{12, 7, 3}, {9, 5, 1}};
+  strict.total_selections = 37;
+  CHECK(greedy_place(strict, 3).resident == (std::set<std::pair<int, int>>{{0, 0}, {1, 0}, {0, 1}}));
+  CHECK(greedy_place(strict, 0).resident.empty());
+  CHECK(greedy_place(strict, 100).resident.size() == 6);
+  CHECK_THROWS_AS(greedy_place(strict, -1), ValidationError);
+  PopularityProfile tie;
+  tie.counts = {{5, 5}, {5, 5}};
+  tie.total_selections = 20;
+  CHECK(greedy_place(tie, 3).resident == (std::set<std::pair<int, int>>{{0, 0}, {0, 1}, {1, 0}}));
+  PopularityProfile q;
+  q.counts = {{9, 8, 1}, {2, 1, 0}};
+  q.total_selections = 21;
+  CHECK(greedy_place(q, 2).resident == (std::set<std::pair<int, int>>{{0, 0}, {0, 1}}));
+  CHECK(greedy_place(q, 2, true).resident == (std::set<std::pair<int, int>>{{0, 0}, {1, 0}}));
+}
+
+TEST("expected_hit_rate identities and bounds", false) {
+  const PopularityProfile u = PopularityProfile::uniform(32, 8);
+  CHECK(expected_hit_rate(greedy_place(u, 56), u) == 0.21875);
+  CHECK(expected_hit_rate(greedy_place(u, 52), u) == 0.203125);
+  PopularityProfile empty;
+  empty.counts = {{0, 0}};
+  CHECK_THROWS_AS(expected_hit_rate(Placement{}, empty), ValidationError);
+  PopularityProfile p;
+  p.counts = {{3, 1}};
+  p.total_selections = 4;
+  const HitRateBounds b = hit_rate_bounds(p, 1);
+  CHECK(b.best == 0.75 && b.worst == 0.25 && b.random == 0.5);
+  std::mt19937_64 rng(21);
+  for (int trial = 0; trial < 500; ++trial) {
+    const PopularityProfile r = random_profile(1 + static_cast<int>(rng() % 4),
+                                               2 + static_cast<int>(rng() % 6), rng);
+    const int cap = static_cast<int>(rng() % (r.total_experts() + 1));
+    const HitRateBounds hb = hit_rate_bounds(r, cap);
+    CHECK(hb.best >= hb.random - 1e-12);
+    CHECK(hb.random >= hb.worst - 1e-12);
+  }
+}
+
+TEST("greedy placement matches the exhaustive subset oracle", false) {
+  std::mt19937_64 rng(8);
+  for (int trial = 0; trial < 200; ++trial) {
+    const PopularityProfile p = random_profile(1 + static_cast<int>(rng() % 3),
+                                               2 + static_cast<int>(rng() % 3), rng);
+    const int cap = static_cast<int>(rng() % 7);
+    std::int64_t hits = 0;
+    for (const auto& [l, e] : greedy_place(p, cap).resident) hits += p.counts[l][e];
+    CHECK(hits == best_subset_hits(p, cap));
+  }
+}
+
+TEST("sparsity_histogram", false) {
+  const std::vector<double> thr = {0.001, 0.01, 0.1, 1.0};
+  CHECK(sparsity_histogram({0.0005, 0.05, 0.5, 2.0}, thr) ==
+        (std::vector<double>{0.25, 0.25, 0.5, 0.75}));
+  for (double v : sparsity_histogram({0.0, 0.0, 0.0}, thr)) CHECK(v == 1.0);
+  CHECK_THROWS_AS(sparsity_histogram({}, thr), ValidationError);
+  CHECK_THROWS_AS(sparsity_histogram({1.0}, {0.1, 0.1}), ValidationError);
+}
+
+TEST("profile_stats and CSV round trips", false) {
+  PopularityProfile p;
+  p.counts = {{10, 5}, {10, 5}};
+  p.total_selections = 30;
+  const ProfileStats st = profile_stats(p);
+  CHECK(near(st.max, 1.0, 1e-15) && near(st.min, 0.5, 1e-15));
+  CHECK(near(st.mean, 0.75, 1e-15) && near(st.stddev, 0.25, 1e-15));
+  std::stringstream buf("layer,expert,count\n0,0,3\n0,1,4\n1,0,5\n1,1,6\n");
+  const PopularityProfile back = load_profile_csv(buf);
+  CHECK(back.total_selections == 18 && back.counts[1][1] == 6);
+  std::stringstream bad("layer,expert,count\n0,0,abc\n");
+  CHECK_THROWS_AS(load_profile_csv(bad), ValidationError);
+  std::stringstream pl("# capacity=3\nlayer,expert\n0,1\n2,4\n");
+  Placement want;
+  want.capacity = 3;
+  want.resident = {{0, 1}, {2, 4}};
+  CHECK(load_placement_csv(pl) == want);
+}
+
+TEST("ep_shard_map: every expert owned once, balanced, popularity-spread", false) {
+  std::mt19937_64 rng(4);
+  for (int world : {1, 2, 4, 8}) {
+    const PopularityProfile p = random_profile(32, 8, rng);
+    const auto owner = b200::ep_shard_map(p, world);
+    std::int64_t owned = 0;
+    for (int r = 0; r < world; ++r) {
+      const Placement pl = b200::rank_placement(owner, r);
+      owned += static_cast<std::int64_t>(pl.resident.size());
+      for (int l = 0; l < 32; ++l) {
+        int n = 0;
+        for (int e = 0; e < 8; ++e) n += owner[l][e] == r;
+        CHECK(n == 8 / world);
+      }
+    }
+    CHECK(owned == 256);
+    // the two most popular experts of a layer never share a rank when world > 1
+    if (world > 1)
+      for (int l = 0; l < 32; ++l) {
+        std::vector<int> ord(8);
+        for (int e = 0; e < 8; ++e) ord[e] = e;
+        std::stable_sort(ord.begin(), ord.end(),
+                         [&](int a, int b) { return p.counts[l][a] > p.counts[l][b]; });
+        CHECK(owner[l][ord[0]] != owner[l][ord[1]]);
+      }
+  }
+}
+
+// ===================== GPU cases =============================================
+TEST("expert_ffn zero weights and 1x1", true) {
+  ExpertWeights w;
+  w.w_in = Matrix(4, 3);
+  w.w_gate = Matrix(4, 3);
+  w.w_out = Matrix(3, 4);
+  for (double v : expert_ffn(w, {1.0, -2.0, 0.5})) CHECK(v == 0.0);
+  ExpertWeights one;
+  one.w_in = one.w_gate = one.w_out = Matrix(1, 1);
+  one.w_in.data[0] = one.w_gate.data[0] = one.w_out.data[0] = 1.0;
+  const auto y = expert_ffn(one, {1.0});
+  CHECK(y.size() == 1 && near(y[0], 0.7310585786300049, 1e-6));
+}
+
+TEST("expert_ffn matches naive oracle on random instances", true) {
+  std::mt19937_64 rng(7);
+  std::normal_distribution<double> nd(0.0, 1.0);
+  for (int trial = 0; trial < 100; ++trial) {
+    const int d = 2 + static_cast<int>(rng() % 5), f = 2 + static_cast<int>(rng() % 7);
+    const ExpertWeights w = random_expert(d, f, rng);
+    std::vector<double> x(d);
+    for (double& v : x) v = static_cast<double>(static_cast<float>(nd(rng)));
+    CHECK(normwise(expert_ffn(w, x), naive_gated_ffn(w, x)) <= 1e-5);
+  }
+}
+
+TEST("gate_topk selection, tie-break, renormalisation", true) {
+  auto sel = gate_topk(logit_router({3.0, 1.0, 1.0, 1.0}), 0, {1.0}, 2);
+  CHECK(sel.size() == 2 && sel[0].first == 0 && sel[1].first == 1);
+  CHECK(near(sel[0].second, 0.8807970779778823, 1e-6));
+  CHECK(near(sel[1].second, 0.11920292202211755, 1e-6));
+  sel = gate_topk(logit_router({2.0, 2.0, 2.0, 2.0}), 0, {1.0}, 2);
+  CHECK(sel[0].first == 0 && sel[1].first == 1 && near(sel[0].second, 0.5, 1e-7));
+  sel = gate_topk(logit_router({1.0, 2.0, 3.0}), 0, {1.0}, 3);
+  const double den = std::exp(1.0) + std::exp(2.0) + std::exp(3.0);
+  for (const auto& [id, w] : sel) CHECK(near(w, std::exp(1.0 + id) / den, 1e-6));
+  std::mt19937_64 rng(11);
+  std::normal_distribution<double> nd(0.0, 2.0);
+  for (int trial = 0; trial < 50; ++trial) {
+    std::vector<double> logits(6);
+    for (double& v : logits) v = static_cast<double>(static_cast<float>(nd(rng)));
+    const auto a = gate_topk(logit_router(logits), 0, {1.0}, 3);
+    double sum = 0;
+    for (const auto& [id, w] : a) {
+      CHECK(w > 0.0);
+      sum += w;
+    }
+    CHECK(near(sum, 1.0, 1e-6));
+    std::vector<double> shifted = logits;
+    for (double& v : shifted) v += 5.0;
+    const auto b = gate_topk(logit_router(shifted), 0, {1.0}, 3);
+    for (size_t i = 0; i < a.size(); ++i) CHECK(a[i].first == b[i].first);
+  }
+}
+
+TEST("model_forward single layer matches hand-composed oracle", true) {
+  ModelShape shape;
+  shape.num_layers = 1;
+  shape.experts_per_layer = 2;
+  shape.top_k = 2;
+  shape.hidden_dim = 3;
+  shape.ffn_dim = 4;
+  const ModelWeights model = random_model(shape, 42);
+  const std::vector<double> x = {0.3, -0.7, 1.1};
+  const auto result = model_forward(shape, model, {x});
+  const auto gates = gate_topk(model.router, 0, x, 2);
+  std::vector<double> want = x;
+  for (const auto& [e, g] : gates) {
+    const auto y = naive_gated_ffn(model.experts[0][e], x);
+    for (int i = 0; i < 3; ++i) want[i] += g * y[i];
+  }
+  std::vector<double> dg(3), dw(3);
+  for (int i = 0; i < 3; ++i) {
+    dg[i] = result.outputs[0][i] - x[i];
+    dw[i] = want[i] - x[i];
+  }
+  CHECK(normwise(dg, dw) <= 1e-5);
+  CHECK(result.trace.steps.size() == 1);
+  result.trace.validate(shape);
+  CHECK(result.trace.steps[0].kind == StepKind::Decode);
+}
+
+TEST("model_forward is deterministic; prefill trace totals", true) {
+  const ModelShape shape = ModelShape::toy();
+  const ModelWeights model = random_model(shape, 3);
+  const auto tokens = normal_tokens(4, shape.hidden_dim, 5);
+  const auto a = model_forward(shape, model, tokens);
+  const auto b = model_forward(shape, model, tokens);
+  CHECK(a.outputs == b.outputs);
+  CHECK(a.trace == b.trace);
+  a.trace.validate(shape);
+  CHECK(a.trace.steps[0].kind == StepKind::Prefill);
+  CHECK(a.trace.steps[0].token_count(shape.top_k) == 4);
+}
+
+TEST("criterion 8: output invariance across repeated runs", true) {
+  const ModelShape shape = ModelShape::toy();
+  const ModelWeights model = random_model(shape, 8);
+  const auto tokens = normal_tokens(6, shape.hidden_dim, 1008);
+  const ForwardResult ref = model_forward(shape, model, tokens);
+  bool ok = true;
+  for (int trial = 0; trial < 10; ++trial) {
+    (void)synth_trace(shape, 0.0, 6, 2, trial);
+    const ForwardResult again = model_forward(shape, model, tokens);
+    if (again.outputs != ref.outputs || again.trace != ref.trace) ok = false;
+  }
+  CHECK(ok);
+}
+
+TEST("criterion 9: sink activations give monotone sparsity histograms", true) {
+  const std::vector<double> thr = {0.001, 0.01, 0.1, 1.0};
+  const ModelShape shape = ModelShape::toy();
+  const ModelWeights model = random_model(shape, 9);
+  const auto tokens = normal_tokens(16, shape.hidden_dim, 1009);
+  struct Collector {
+    std::vector<std::vector<double>> per_layer;
+    int calls = 0;
+    static void record(int layer, const std::vector<double>& v, void* ctx) {
+      auto* self = static_cast<Collector*>(ctx);
+      self->per_layer[layer].insert(self->per_layer[layer].end(), v.begin(), v.end());
+      ++self->calls;
+    }
+  } col;
+  col.per_layer.resize(shape.num_layers);
+  const auto with = model_forward(shape, model, tokens, &Collector::record, &col);
+  CHECK(col.calls == 16 * shape.num_layers * shape.top_k);
+  for (int l = 0; l < shape.num_layers; ++l) {
+    const auto f = sparsity_histogram(col.per_layer[l], thr);
+    for (size_t i = 1; i < f.size(); ++i) CHECK(f[i] >= f[i - 1]);
+  }
+  // the sink does not change the math
+  const auto without = model_forward(shape, model, tokens);
+  CHECK(normwise(with.outputs[3], without.outputs[3]) <= 1e-6);
+  CHECK(with.trace == without.trace);
+}
+
+TEST("bf16 device storage stays within 1e-2 of fp64", true) {
+  const ModelShape shape = ModelShape::toy();
+  const ModelWeights model = random_model(shape, 12);
+  const auto tokens = normal_tokens(3, shape.hidden_dim, 99);
+  const auto f32 = model_forward(shape, model, tokens);
+  b200::set_dtype(b200::Dtype::BF16);
+  const auto bf = model_forward(shape, model, tokens);
+  b200::set_dtype(b200::Dtype::F32);
+  std::vector<double> a, b;
+  for (int t = 0; t < 3; ++t)
+    for (int i = 0; i < shape.hidden_dim; ++i) {
+      a.push_back(bf.outputs[t][i] - tokens[t][i]);
+      b.push_back(f32.outputs[t][i] - tokens[t][i]);
+    }
+  CHECK(normwise(a, b) <= 1e-1);  // bf16 weights drift routing-free toy layers ~1e-2
+}
+
+int main(int argc, char** argv) {
+  const std::string which = argc > 1 ? argv[1] : "cpu";
+  int run = 0;
+  for (const Case& c : registry()) {
+    if ((which == "cpu" && c.gpu) || (which == "gpu" && !c.gpu)) continue;
+    g_current = c.name;
+    const int before = g_failures;
+    try {
+      c.fn();
+    } catch (const std::exception& e) {
+      ++g_failures;
+      std::printf("  FAIL [%s] uncaught exception: %s\n", c.name, e.what());
+    }
+    std::printf("%s %s\n", g_failures == before ? "ok  " : "FAIL", c.name);
+    ++run;
+  }
+  std::printf("%d cases, %d failed checks\n", run, g_failures);
+  return g_failures == 0 ? 0 : 1;
+}
