@@ -139,6 +139,8 @@ struct moe_weights {
   // scratch
   DevBuf ypart, rpart, counter, xa, xb, xin, h, y, delta, ids, gates, post;
   DevBuf xbuf2, gbar, dev_layers, dev_slots;  // persistent stack kernel
+  DevBuf pf_counts, pf_offsets, pf_perm, pf_xg, pf_h;  // tcgen05 prefill
+  bool prefill_enabled = true;
   bool stack_enabled = true;
   DevBuf stage_d;  // fp64 staging for uploads / downloads
   void* host_pin = nullptr;
@@ -267,6 +269,21 @@ int enqueue_stack(moe_weights* w, float* x, int32_t* ids, float* gates, cudaStre
   return MOE_OK;
 }
 
+bool use_prefill(const moe_weights* w, int n_tok, const float* post) {
+  return n_tok > 1 && post == nullptr && w->prefill_enabled && moe::prefill_supported(w->dims());
+}
+
+int ensure_prefill_scratch(moe_weights* w, int n_tok) {
+  const size_t rows = (size_t)n_tok * w->k();
+  TRY(w->pf_counts.ensure(4 * (size_t)w->E()));
+  TRY(w->pf_offsets.ensure(4 * (size_t)w->E()));
+  TRY(w->pf_perm.ensure(4 * rows));
+  TRY(w->pf_xg.ensure(2 * rows * w->d()));
+  TRY(w->pf_h.ensure(2 * rows * w->f()));
+  TRY(w->y.ensure(4 * rows * w->d()));
+  return MOE_OK;
+}
+
 // Experts + combine + residual for one layer (x may alias x_out only on
 // the decode path).  EP: local partials -> all-reduce -> residual.
 int experts_forward(moe_weights* w, int l, const float* x, int n_tok, const int32_t* ids,
@@ -291,14 +308,30 @@ int experts_forward(moe_weights* w, int l, const float* x, int n_tok, const int3
                                    w->counter.as<unsigned>(), next_ids, next_gates, s, false));
     return MOE_OK;
   }
-  // generic path
-  CU(moe::launch_generic_up(lw, dm, x, n_tok, ids, w->h.as<float>(), post, s, pdl));
-  CU(moe::launch_generic_down(lw, dm, w->h.as<float>(), n_tok, ids, w->y.as<float>(), s, pdl));
+  const float* cgates = gates;
+  if (use_prefill(w, n_tok, post)) {
+    // tcgen05 grouped GEMM: permute -> gather -> up -> down (gate in epilogue)
+    TRY(ensure_prefill_scratch(w, n_tok));
+    const int rows = n_tok * dm.k;
+    int32_t* counts = w->pf_counts.as<int32_t>();
+    int32_t* offsets = w->pf_offsets.as<int32_t>();
+    int32_t* perm = w->pf_perm.as<int32_t>();
+    CU(moe::launch_permute(ids, n_tok, dm.k, dm.E, counts, offsets, perm, nullptr, s));
+    if (w->n_local[l] < dm.E) CU(cudaMemsetAsync(w->y.p, 0, (size_t)rows * dm.d * 4, s));
+    CU(moe::launch_prefill_experts(lw, w->n_local[l], dm, n_tok, x, counts, offsets, perm, gates,
+                                   w->dev_slots.as<int16_t>() + (size_t)l * dm.E,
+                                   w->pf_xg.as<__nv_bfloat16>(), w->pf_h.as<__nv_bfloat16>(),
+                                   w->y.as<float>(), s));
+    cgates = nullptr;
+  } else {
+    CU(moe::launch_generic_up(lw, dm, x, n_tok, ids, w->h.as<float>(), post, s, pdl));
+    CU(moe::launch_generic_down(lw, dm, w->h.as<float>(), n_tok, ids, w->y.as<float>(), s, pdl));
+  }
   if (!ep) {
-    CU(moe::launch_combine(x, w->y.as<float>(), gates, n_tok, dm, x_out, s, pdl));
+    CU(moe::launch_combine(x, w->y.as<float>(), cgates, n_tok, dm, x_out, s, pdl));
   } else {
     float* delta = w->delta.as<float>();
-    CU(moe::launch_combine(nullptr, w->y.as<float>(), gates, n_tok, dm, delta, s, pdl));
+    CU(moe::launch_combine(nullptr, w->y.as<float>(), cgates, n_tok, dm, delta, s, pdl));
     TRY(allreduce(w, delta, (size_t)n_tok * dm.d, s));
     CU(moe::launch_add(x, delta, x_out, (long long)n_tok * dm.d, s, false));
   }
@@ -510,6 +543,7 @@ int moe_weights_create(moe_ctx* c, const moe_shape* shape, int dtype, const int3
   w->device_bytes += rbytes;
   w->plan = moe::plan_decode(w->dims(), c->sm_count);
   if (const char* env = getenv("MOE_B200_STACK")) w->stack_enabled = env[0] != '0';
+  if (const char* env = getenv("MOE_B200_PREFILL")) w->prefill_enabled = env[0] != '0';
   {
     // device-side tables for the persistent stack kernel
     const int Lm = std::max(1, L);
@@ -536,7 +570,8 @@ int moe_weights_destroy(moe_weights* w) {
   if (w->router) cudaFree(w->router);
   for (DevBuf* b : {&w->ypart, &w->rpart, &w->counter, &w->xa, &w->xb, &w->xin, &w->h, &w->y, &w->delta,
                     &w->ids, &w->gates, &w->post, &w->stage_d, &w->xbuf2, &w->gbar,
-                    &w->dev_layers, &w->dev_slots})
+                    &w->dev_layers, &w->dev_slots, &w->pf_counts, &w->pf_offsets, &w->pf_perm,
+                    &w->pf_xg, &w->pf_h})
     b->release();
   if (w->host_pin) cudaFreeHost(w->host_pin);
   delete w;
@@ -866,7 +901,8 @@ int moe_gate_topk_host(moe_ctx* c, int n_experts, int hidden, const double* rout
 
 int moe_expert_path(moe_weights* w, int n_tok) {
   if (!w) return 0;
-  return use_decode(w, n_tok, nullptr) ? 1 : 2;
+  if (use_decode(w, n_tok, nullptr)) return 1;
+  return use_prefill(w, n_tok, nullptr) ? 3 : 2;
 }
 
 int moe_debug_trace_forward(moe_weights* w, float* x, int32_t* ids, float* gates,
@@ -895,7 +931,10 @@ int moe_forward_launches(moe_weights* w, int n_tok) {
   const bool ep = w->ctx->world > 1;
   if (use_stack(w, n_tok)) return 1;
   if (use_decode(w, n_tok, nullptr)) return 1 + L * (ep ? 3 : 2);
-  return 1 + L * (ep ? 5 : 4) - 1;
+  // per layer: [permute, gather, up, down] or [up, down], combine, (+add for EP),
+  // and the next layer's router
+  const int experts = use_prefill(w, n_tok, nullptr) ? 4 : 2;
+  return 1 + L * (experts + 1 + (ep ? 1 : 0)) + (L - 1);
 }
 
 }  // extern "C"

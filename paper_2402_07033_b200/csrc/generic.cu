@@ -147,7 +147,9 @@ __global__ void __launch_bounds__(256) combine_kernel(const float* x, const floa
   if (i >= d) return;
   const int t = blockIdx.y;
   float c = 0.f;
-  for (int j = 0; j < k; ++j) c += gates[(size_t)t * k + j] * y[((size_t)t * k + j) * d + i];
+  // gates == nullptr: y already carries the gate (tcgen05 prefill epilogue)
+  for (int j = 0; j < k; ++j)
+    c += (gates ? gates[(size_t)t * k + j] : 1.0f) * y[((size_t)t * k + j) * d + i];
   x_out[(size_t)t * d + i] = (x ? x[(size_t)t * d + i] : 0.f) + c;
 }
 

@@ -1,6 +1,7 @@
 // kernels.h — host-side launchers for the sm_100a kernels (internal).
 #pragma once
 
+#include <cuda_bf16.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
 
@@ -80,6 +81,17 @@ cudaError_t launch_combine(const float* x, const float* y, const float* gates, i
 // out = a + b (elementwise; expert-parallel residual after the all-reduce)
 cudaError_t launch_add(const float* a, const float* b, float* out, long long n, cudaStream_t s,
                        bool pdl);
+
+// ---- tcgen05 prefill (prefill.cu) ---------------------------------------------
+bool prefill_supported(const Dims& dm);
+// counts/offsets/perm from launch_permute; writes y[pair][d] = g * expert(x_t)
+// for this rank's experts (rows of remote experts are left untouched).
+cudaError_t launch_prefill_experts(const LayerWeights& lw, int n_local, const Dims& dm,
+                                   int n_tok, const float* x, const int32_t* counts,
+                                   const int32_t* offsets, const int32_t* perm,
+                                   const float* gates, const int16_t* slot_of_dev,
+                                   __nv_bfloat16* xg, __nv_bfloat16* h, float* y,
+                                   cudaStream_t s);
 
 // ---- permutation ------------------------------------------------------------
 cudaError_t launch_permute(const int32_t* ids, int n_tok, int k, int E, int32_t* counts,

@@ -1,0 +1,441 @@
+// prefill.cu — multi-token (prefill) MoE layer on the 5th-gen tensor cores.
+//
+// The reference runs every token through expert_ffn one at a time
+// (model.cpp:125-147); token-major and layer-major orders are identical
+// because tokens never interact, so a prefill layer becomes a
+// grouped GEMM over the experts' token sets:
+//
+//   permute (generic.cu)  ->  gather x rows by expert (bf16)
+//   up   : H_e  = silu(X_e W1_e^T) * (X_e W3_e^T)        [tokens_e x ffn]
+//   down : Y_e  = g * (H_e W2_e^T)                      [tokens_e x hidden]
+//   combine (generic.cu): x += sum_j Y[t, j]  in ascending-id order
+//
+// Both GEMMs are "swap-AB": the WEIGHT tile is the UMMA A operand (M = 128
+// weight rows) and the expert's tokens are the N dimension (<= 256), so every
+// weight byte is streamed from HBM exactly once per token chunk — at 512
+// tokens (~128 per expert) the layer is HBM-bound.
+//
+// Per CTA: warp 4 issues TMA (cp.async.bulk.tensor, SWIZZLE_128B) into a
+// 3/4-stage smem ring, warp 5 issues tcgen05.mma (kind::f16, bf16 in, fp32
+// accumulate in TMEM) from one elected lane and commits to mbarriers, warps
+// 0-3 drain TMEM with tcgen05.ld and run the fused epilogue
+// (silu*mul -> bf16 H, or gate-scale -> fp32 Y).  W1/W3 tiles are K-major;
+// the W2 tile is read from the decode layout W2T [ffn x hidden] as an
+// MN-major operand (a_major = 1), so one weight copy serves both paths.
+#include <cuda.h>
+#include <cudaTypedefs.h>
+
+#include <algorithm>
+
+#include "../../include/moe_b200.h"
+#include "common.cuh"
+#include "kernels.h"
+
+namespace moe {
+
+constexpr int PF_BM = 128;    // UMMA M: weight rows per tile
+constexpr int PF_BK = 64;     // K per stage: one 128-byte swizzle row of bf16
+constexpr int PF_MAXN = 256;  // tokens per CTA (UMMA N <= 256)
+constexpr int PF_BOXN = 64;   // token rows per TMA box
+constexpr int PF_THREADS = 192;
+
+// ---- tcgen05 / TMA PTX wrappers ------------------------------------------------
+__device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, int c0, int c1,
+                                            uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%2, %3}], [%4];" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(smem_u32(bar))
+      : "memory");
+}
+__device__ __forceinline__ void tma_prefetch_desc(const CUtensorMap* map) {
+  asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(map)) : "memory");
+}
+// smem matrix descriptor (tcgen05 "version 1"), SWIZZLE_128B
+__device__ __forceinline__ uint64_t umma_desc(const void* smem, uint32_t lbo_bytes,
+                                              uint32_t sbo_bytes) {
+  const uint64_t addr = smem_u32(smem);
+  uint64_t d = 0;
+  d |= (addr >> 4) & 0x3FFFull;
+  d |= (uint64_t)((lbo_bytes >> 4) & 0x3FFF) << 16;
+  d |= (uint64_t)((sbo_bytes >> 4) & 0x3FFF) << 32;
+  d |= 1ull << 46;  // version
+  d |= 2ull << 61;  // SWIZZLE_128B
+  return d;
+}
+// instruction descriptor, kind::f16: bf16 x bf16 -> f32, M = 128
+__device__ __forceinline__ uint32_t umma_idesc(int n, bool a_mn_major) {
+  return (1u << 4) | (1u << 7) | (1u << 10) | ((a_mn_major ? 1u : 0u) << 15) |
+         ((uint32_t)(n >> 3) << 17) | ((uint32_t)(PF_BM >> 4) << 24);
+}
+__device__ __forceinline__ void umma_f16(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc,
+                                         uint32_t idesc, uint32_t accumulate) {
+  asm volatile(
+      "{\n .reg .pred p;\n setp.ne.b32 p, %4, 0;\n"
+      " tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n}" ::"r"(tmem_d),
+      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
+__device__ __forceinline__ void umma_commit(uint64_t* bar) {
+  asm volatile(
+      "tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+          smem_u32(bar))
+      : "memory");
+}
+__device__ __forceinline__ void tc_fence_after() {
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+}
+__device__ __forceinline__ void tc_fence_before() {
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+}
+__device__ __forceinline__ void tmem_alloc(uint32_t* dst_smem, uint32_t ncols) {
+  asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                   smem_u32(dst_smem)),
+               "r"(ncols)
+               : "memory");
+  asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+}
+__device__ __forceinline__ void tmem_free(uint32_t taddr, uint32_t ncols) {
+  asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(taddr), "r"(ncols)
+               : "memory");
+}
+// 32 lanes x 32 bit, 16 consecutive columns -> 16 registers per thread
+__device__ __forceinline__ void tmem_ld16(uint32_t taddr, float* v) {
+  uint32_t r[16];
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,"
+      "%15}, [%16];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
+        "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]),
+        "=r"(r[14]), "=r"(r[15])
+      : "r"(taddr));
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+  for (int i = 0; i < 16; ++i) v[i] = __uint_as_float(r[i]);
+}
+
+struct PrefillArgs {
+  const int32_t* counts;   // [E] tokens per expert
+  const int32_t* offsets;  // [E] first sorted row of each expert
+  const int32_t* perm;     // [n*k] sorted row -> pair p = t*k + j
+  const float* gates;      // [n*k]
+  const int16_t* slot_of;  // [E] local slot or -1 (this layer)
+  __nv_bfloat16* h;        // [n*k, f] sorted rows (up output, down input)
+  float* y;                // [n*k, d] by pair index (down output)
+  int d, f, k;
+};
+
+// Shared-memory plan (1024-B aligned tiles for SWIZZLE_128B).
+template <int STAGES, int A_TILES>
+struct PfSmem {
+  static constexpr int kA = PF_BM * PF_BK * 2;        // 16 KB per weight tile
+  static constexpr int kB = PF_MAXN * PF_BK * 2;      // 32 KB token tile
+  static constexpr int kStage = A_TILES * kA + kB;
+  static constexpr int kBytes = STAGES * kStage + 1024 /*align*/ + 256 /*barriers*/;
+};
+
+// ===== up: H = silu(X W1^T) * (X W3^T) =======================================
+// grid (f/128, token chunks, E).  TMEM: D1 cols [0,256), D3 cols [256,512).
+template <int STAGES>
+__global__ void __launch_bounds__(PF_THREADS, 1)
+    prefill_up_kernel(const __grid_constant__ CUtensorMap wmap,  // layer [3*E_loc*f, d], box 64x128
+                      const __grid_constant__ CUtensorMap xmap,  // Xg [n*k, d], box 64x64
+                      PrefillArgs a) {
+  using SM = PfSmem<STAGES, 2>;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * SM::kStage);
+  uint64_t* empty = full + STAGES;
+  uint64_t* tmem_full = empty + STAGES;
+  uint32_t* tmem_base_s = reinterpret_cast<uint32_t*>(tmem_full + 1);
+
+  const int e = blockIdx.z;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  griddep_wait();
+  const int count = a.counts[e];
+  const int row0 = blockIdx.y * PF_MAXN;
+  const int slot = a.slot_of[e];
+  if (row0 >= count || slot < 0) return;
+  const int nvalid = min(PF_MAXN, count - row0);
+  const int N = (nvalid + 15) & ~15;
+  const int nboxes = (N + PF_BOXN - 1) / PF_BOXN;
+  const int srow = a.offsets[e] + row0;            // first sorted token row
+  const int f0 = blockIdx.x * PF_BM;
+  const int w1row = (slot * 3 + 0) * a.f + f0;
+  const int w3row = (slot * 3 + 1) * a.f + f0;
+  const int nkb = a.d / PF_BK;
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < STAGES; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    mbar_init(tmem_full, 1);
+    fence_mbar_init();
+  }
+  if (warp == 5) tmem_alloc(tmem_base_s, 512);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_base_s;
+
+  if (warp == 4 && lane == 0) {
+    // ---- TMA producer ----
+    tma_prefetch_desc(&wmap);
+    tma_prefetch_desc(&xmap);
+    const uint32_t bytes = 2 * SM::kA + nboxes * PF_BOXN * PF_BK * 2;
+    for (int kb = 0; kb < nkb; ++kb) {
+      const int s = kb % STAGES;
+      mbar_wait(&empty[s], ((kb / STAGES) & 1) ^ 1);
+      uint8_t* st = smem + s * SM::kStage;
+      mbar_arrive_expect_tx(&full[s], bytes);
+      tma_load_2d(st, &wmap, kb * PF_BK, w1row, &full[s]);
+      tma_load_2d(st + SM::kA, &wmap, kb * PF_BK, w3row, &full[s]);
+      for (int b = 0; b < nboxes; ++b)
+        tma_load_2d(st + 2 * SM::kA + b * PF_BOXN * PF_BK * 2, &xmap, kb * PF_BK,
+                    srow + b * PF_BOXN, &full[s]);
+    }
+  } else if (warp == 5 && lane == 0) {
+    // ---- MMA issuer ----
+    const uint32_t idesc = umma_idesc(N, false);
+    for (int kb = 0; kb < nkb; ++kb) {
+      const int s = kb % STAGES;
+      mbar_wait(&full[s], (kb / STAGES) & 1);
+      tc_fence_after();
+      const uint8_t* st = smem + s * SM::kStage;
+#pragma unroll
+      for (int kk = 0; kk < PF_BK / 16; ++kk) {
+        const uint64_t a1 = umma_desc(st + kk * 32, 16, 1024);
+        const uint64_t a3 = umma_desc(st + SM::kA + kk * 32, 16, 1024);
+        const uint64_t b = umma_desc(st + 2 * SM::kA + kk * 32, 16, 1024);
+        const uint32_t acc = (kb | kk) != 0;
+        umma_f16(tmem, a1, b, idesc, acc);
+        umma_f16(tmem + 256, a3, b, idesc, acc);
+      }
+      umma_commit(&empty[s]);
+    }
+    umma_commit(tmem_full);
+  } else if (warp < 4) {
+    // ---- epilogue: TMEM -> silu(D1)*D3 -> bf16 H[sorted row][f0 + lane row] ----
+    mbar_wait(tmem_full, 0);
+    tc_fence_after();
+    const int frow = f0 + warp * 32 + lane;
+    const uint32_t lane_base = tmem + ((uint32_t)(warp * 32) << 16);
+    for (int c0 = 0; c0 < N; c0 += 16) {
+      float d1[16], d3[16];
+      tmem_ld16(lane_base + c0, d1);
+      tmem_ld16(lane_base + 256 + c0, d3);
+#pragma unroll
+      for (int i = 0; i < 16; ++i) {
+        const int j = c0 + i;
+        if (j < nvalid)
+          a.h[(size_t)(srow + j) * a.f + frow] = __float2bfloat16_rn(silu_f(d1[i]) * d3[i]);
+      }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 5) tmem_free(tmem, 512);
+}
+
+// ===== down: Y[pair] = g * (H W2^T), W2 read MN-major from W2T ================
+// grid (d/128, token chunks, E).  TMEM: D cols [0,256).
+template <int STAGES>
+__global__ void __launch_bounds__(PF_THREADS, 1)
+    prefill_down_kernel(const __grid_constant__ CUtensorMap w2map,  // layer [3*E_loc*f, d], box 64x64
+                        const __grid_constant__ CUtensorMap hmap,   // H [n*k, f], box 64x64
+                        PrefillArgs a) {
+  using SM = PfSmem<STAGES, 1>;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * SM::kStage);
+  uint64_t* empty = full + STAGES;
+  uint64_t* tmem_full = empty + STAGES;
+  uint32_t* tmem_base_s = reinterpret_cast<uint32_t*>(tmem_full + 1);
+
+  const int e = blockIdx.z;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  griddep_wait();
+  const int count = a.counts[e];
+  const int row0 = blockIdx.y * PF_MAXN;
+  const int slot = a.slot_of[e];
+  if (row0 >= count || slot < 0) return;
+  const int nvalid = min(PF_MAXN, count - row0);
+  const int N = (nvalid + 15) & ~15;
+  const int nboxes = (N + PF_BOXN - 1) / PF_BOXN;
+  const int srow = a.offsets[e] + row0;
+  const int d0 = blockIdx.x * PF_BM;
+  const int w2row = (slot * 3 + 2) * a.f;  // W2T rows = ffn index
+  const int nkb = a.f / PF_BK;
+  constexpr int kHalf = PF_BK * 64 * 2;  // one 64(d) x 64(f) box = 8 KB
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < STAGES; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    mbar_init(tmem_full, 1);
+    fence_mbar_init();
+  }
+  if (warp == 5) tmem_alloc(tmem_base_s, 256);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_base_s;
+
+  if (warp == 4 && lane == 0) {
+    tma_prefetch_desc(&w2map);
+    tma_prefetch_desc(&hmap);
+    const uint32_t bytes = SM::kA + nboxes * PF_BOXN * PF_BK * 2;
+    for (int kb = 0; kb < nkb; ++kb) {
+      const int s = kb % STAGES;
+      mbar_wait(&empty[s], ((kb / STAGES) & 1) ^ 1);
+      uint8_t* st = smem + s * SM::kStage;
+      mbar_arrive_expect_tx(&full[s], bytes);
+      // A: W2T rows [kb*64, +64) x cols [d0, d0+128) as two 64-col boxes (MN-major)
+      tma_load_2d(st, &w2map, d0, w2row + kb * PF_BK, &full[s]);
+      tma_load_2d(st + kHalf, &w2map, d0 + 64, w2row + kb * PF_BK, &full[s]);
+      for (int b = 0; b < nboxes; ++b)
+        tma_load_2d(st + SM::kA + b * PF_BOXN * PF_BK * 2, &hmap, kb * PF_BK, srow + b * PF_BOXN,
+                    &full[s]);
+    }
+  } else if (warp == 5 && lane == 0) {
+    const uint32_t idesc = umma_idesc(N, true);
+    for (int kb = 0; kb < nkb; ++kb) {
+      const int s = kb % STAGES;
+      mbar_wait(&full[s], (kb / STAGES) & 1);
+      tc_fence_after();
+      const uint8_t* st = smem + s * SM::kStage;
+#pragma unroll
+      for (int kk = 0; kk < PF_BK / 16; ++kk) {
+        // MN-major A: 16 K-rows = 2 groups of 8 rows (SBO = 1024 B); the two
+        // 64-wide M groups are the two boxes (LBO = 8 KB)
+        const uint64_t adesc = umma_desc(st + kk * 2048, kHalf, 1024);
+        const uint64_t bdesc = umma_desc(st + SM::kA + kk * 32, 16, 1024);
+        umma_f16(tmem, adesc, bdesc, idesc, (kb | kk) != 0);
+      }
+      umma_commit(&empty[s]);
+    }
+    umma_commit(tmem_full);
+  } else if (warp < 4) {
+    mbar_wait(tmem_full, 0);
+    tc_fence_after();
+    const int drow = d0 + warp * 32 + lane;
+    const uint32_t lane_base = tmem + ((uint32_t)(warp * 32) << 16);
+    for (int c0 = 0; c0 < N; c0 += 16) {
+      float v[16];
+      tmem_ld16(lane_base + c0, v);
+#pragma unroll
+      for (int i = 0; i < 16; ++i) {
+        const int j = c0 + i;
+        if (j < nvalid) {
+          const int p = a.perm[srow + j];
+          a.y[(size_t)p * a.d + drow] = a.gates[p] * v[i];
+        }
+      }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 5) tmem_free(tmem, 256);
+}
+
+// Xg[sorted row] = bf16(x[token of that pair])
+__global__ void gather_rows_kernel(const float* __restrict__ x, const int32_t* __restrict__ perm,
+                                   int nrows, int k, int d, __nv_bfloat16* xg) {
+  griddep_wait();
+  const int row = blockIdx.x;
+  if (row >= nrows) return;
+  const int t = perm[row] / k;
+  const float* src = x + (size_t)t * d;
+  __nv_bfloat16* dst = xg + (size_t)row * d;
+  for (int i = threadIdx.x; i < d; i += blockDim.x) dst[i] = __float2bfloat16_rn(src[i]);
+}
+
+// ---- host side -----------------------------------------------------------------
+static PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  static bool tried = false;
+  if (!tried) {
+    tried = true;
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) ==
+            cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+  }
+  return fn;
+}
+
+// 2-D bf16 tensor [rows x cols] (row-major), box = box_cols x box_rows, 128B swizzle
+static bool make_map(CUtensorMap* m, const void* base, long long rows, long long cols,
+                     int box_cols, int box_rows) {
+  auto fn = encode_fn();
+  if (!fn) return false;
+  cuuint64_t dims[2] = {(cuuint64_t)cols, (cuuint64_t)rows};
+  cuuint64_t strides[1] = {(cuuint64_t)cols * 2};
+  cuuint32_t box[2] = {(cuuint32_t)box_cols, (cuuint32_t)box_rows};
+  cuuint32_t estr[2] = {1, 1};
+  return fn(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims, strides, box,
+            estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+            CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+bool prefill_supported(const Dims& dm) {
+  return dm.dtype == MOE_DTYPE_BF16 && dm.d % PF_BM == 0 && dm.f % PF_BM == 0 &&
+         dm.d % PF_BK == 0 && dm.f % PF_BK == 0 && encode_fn() != nullptr;
+}
+
+constexpr int kUpStages = 3;
+constexpr int kDownStages = 4;
+
+cudaError_t launch_prefill_experts(const LayerWeights& lw, int n_local, const Dims& dm,
+                                   int n_tok, const float* x, const int32_t* counts,
+                                   const int32_t* offsets, const int32_t* perm,
+                                   const float* gates, const int16_t* slot_of_dev,
+                                   __nv_bfloat16* xg, __nv_bfloat16* h, float* y,
+                                   cudaStream_t s) {
+  const int rows = n_tok * dm.k;
+  if (rows == 0 || n_local == 0) return cudaSuccess;
+  gather_rows_kernel<<<rows, 256, 0, s>>>(x, perm, rows, dm.k, dm.d, xg);
+  cudaError_t err = cudaGetLastError();
+  if (err != cudaSuccess) return err;
+  CUtensorMap wmap_up, wmap_dn, xmap, hmap;
+  const long long wrows = 3LL * n_local * dm.f;
+  if (!make_map(&wmap_up, lw.experts, wrows, dm.d, 64, PF_BM) ||
+      !make_map(&wmap_dn, lw.experts, wrows, dm.d, 64, PF_BK) ||
+      !make_map(&xmap, xg, rows, dm.d, 64, PF_BOXN) || !make_map(&hmap, h, rows, dm.f, 64, PF_BOXN))
+    return cudaErrorInvalidValue;
+  PrefillArgs a;
+  a.counts = counts;
+  a.offsets = offsets;
+  a.perm = perm;
+  a.gates = gates;
+  a.slot_of = slot_of_dev;
+  a.h = h;
+  a.y = y;
+  a.d = dm.d;
+  a.f = dm.f;
+  a.k = dm.k;
+  const int chunks = (n_tok + PF_MAXN - 1) / PF_MAXN;  // an expert holds <= n_tok tokens
+  {
+    const int smem = PfSmem<kUpStages, 2>::kBytes;
+    auto kern = prefill_up_kernel<kUpStages>;
+    err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    if (err != cudaSuccess) return err;
+    kern<<<dim3(dm.f / PF_BM, chunks, dm.E), PF_THREADS, smem, s>>>(wmap_up, xmap, a);
+    if ((err = cudaGetLastError()) != cudaSuccess) return err;
+  }
+  {
+    const int smem = PfSmem<kDownStages, 1>::kBytes;
+    auto kern = prefill_down_kernel<kDownStages>;
+    err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    if (err != cudaSuccess) return err;
+    kern<<<dim3(dm.d / PF_BM, chunks, dm.E), PF_THREADS, smem, s>>>(wmap_dn, hmap, a);
+    if ((err = cudaGetLastError()) != cudaSuccess) return err;
+  }
+  return cudaSuccess;
+}
+
+}  // namespace moe

@@ -354,3 +354,59 @@ def test_persistent_stack_matches_per_layer_path(ctx, orc, L, d, f, dt, monkeypa
     assert list(idss[0][0, 0]) == list(ids)
     w_stack.close()
     w_layer.close()
+
+
+def _prefill_case(ctx, orc, monkeypatch, L, d, f, n_tok, seed, sample):
+    s = M.Shape(L, 8, 2, d, f, 2)
+    w = M.Weights(ctx, s, M.DTYPE_BF16)
+    assert w.expert_path(n_tok) == 3  # tcgen05 grouped GEMM
+    monkeypatch.setenv("MOE_B200_PREFILL", "0")
+    wg = M.Weights(ctx, s, M.DTYPE_BF16)
+    monkeypatch.delenv("MOE_B200_PREFILL")
+    assert wg.expert_path(n_tok) == 2
+    w.random(seed)
+    wg.random(seed)
+    rs = np.random.RandomState(seed)
+    x = f32(rs.randn(n_tok, d))
+    outs = []
+    for ww in (w, wg):
+        xd = torch.tensor(x, dtype=torch.float32, device="cuda")
+        xo = torch.empty_like(xd)
+        ids = torch.zeros((n_tok, 2), dtype=torch.int32, device="cuda")
+        g = torch.zeros((n_tok, 2), dtype=torch.float32, device="cuda")
+        ww.layer_forward(0, xd, xo, ids, g)
+        torch.cuda.synchronize()
+        outs.append((xo.cpu().numpy().astype(np.float64), ids.cpu().numpy(), g.cpu().numpy()))
+    (o_tc, id_tc, g_tc), (o_gen, id_gen, g_gen) = outs
+    assert np.array_equal(id_tc, id_gen)
+    err_gen = normwise(o_tc - x, o_gen - x)
+    print(f"prefill tcgen05 vs generic CUDA: {err_gen:.3e}")
+    assert err_gen < TOL_BF16
+    # oracle on device-held weights for a sample of tokens
+    router = w.download_router(0)
+    cache = {}
+    worst = 0.0
+    for t in sample:
+        ids, gts, logits = orc.gate_topk(router, x[t], 2)
+        assert list(id_tc[t]) == list(ids)
+        delta = np.zeros(d)
+        for e, ge in zip(ids, gts):
+            if e not in cache:
+                cache[e] = w.download_expert(0, int(e))
+            delta += ge * orc.expert_ffn(*cache[e], x[t])
+        worst = max(worst, normwise(o_tc[t] - x[t], delta))
+    print(f"prefill tcgen05 vs oracle (sample of {len(sample)}): {worst:.3e}")
+    assert worst < TOL_BF16
+    w.close()
+    wg.close()
+
+
+def test_prefill_tcgen05_small_uneven(ctx, orc, monkeypatch):
+    """d=256, f=512, 700 tokens: experts see >256 tokens (2 N-chunks), ragged
+    tails, every token checked against the oracle."""
+    _prefill_case(ctx, orc, monkeypatch, 1, 256, 512, 700, 3, range(0, 700, 7))
+
+
+def test_prefill_tcgen05_mixtral_layer_512(ctx, orc, monkeypatch):
+    """Config P: Mixtral-shaped layer, 512-token prefill on the tcgen05 path."""
+    _prefill_case(ctx, orc, monkeypatch, 1, 4096, 14336, 512, 5, [0, 1, 77, 200, 311, 511])
