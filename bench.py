@@ -295,6 +295,65 @@ def run_ours(args):
     ctx.close()
 
 
+def run_prefill(args):
+    """BASELINE configs[2]: one Mixtral-shaped layer, 512-token prefill, bf16,
+    on the tcgen05 grouped-GEMM path.  Reports tok/s and both rooflines."""
+    import torch
+
+    import paper_2402_07033_b200 as M
+
+    L, E, k, d, f = 1, 8, 2, 4096, 14336
+    n = args.prefill_tokens
+    torch.cuda.set_device(0)
+    ctx = M.Ctx(0)
+    w = M.Weights(ctx, M.Shape(L, E, k, d, f, 2), M.DTYPE_BF16)
+    w.random(args.seed)
+    assert w.expert_path(n) == 3, "tcgen05 prefill path not selected"
+    sp = ctx.stream
+    stream = torch.cuda.ExternalStream(sp, device="cuda:0")
+    n_batches = args.warmup + args.steps
+    gen = torch.Generator(device="cuda:0").manual_seed(args.seed + 1)
+    with torch.cuda.stream(stream):
+        xs = torch.randn((n_batches, n, d), generator=gen, device="cuda:0")
+        xo = torch.empty((n, d), device="cuda:0")
+        ids = torch.zeros((n, k), dtype=torch.int32, device="cuda:0")
+        g = torch.zeros((n, k), dtype=torch.float32, device="cuda:0")
+    torch.cuda.synchronize()
+    for i in range(args.warmup):
+        w.layer_forward(0, xs[i], xo, ids, g, stream=sp)
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(0) as clk:
+        e0.record(stream)
+        for i in range(args.warmup, n_batches):
+            w.layer_forward(0, xs[i], xo, ids, g, stream=sp)
+        e1.record(stream)
+        torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1) / args.steps
+    active = len(set(ids.cpu().numpy().ravel().tolist()))
+    bytes_ = active * 3 * d * f * 2 + E * d * 4 + n * d * 4 * 2
+    flops = 2.0 * 3 * d * f * n * k
+    peak_bw, src = load_peaks()
+    peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json"))) if os.path.exists(
+        os.path.join(ROOT, "MEASURED_PEAKS.json")) else {"bf16_tflops": 1590.0}
+    bw = bytes_ / (ms * 1e-3) / 1e9
+    tf = flops / (ms * 1e-3) / 1e12
+    print(json.dumps({
+        "metric": "Mixtral-8x7B MoE layer prefill tok/s (512 tokens, 1 layer)", "value": round(n / (ms * 1e-3), 1),
+        "unit": "tok/s", "n_gpus": 1, "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms, 4),
+        "higher_is_better": True, "dtype": "bf16", "data": "synthetic",
+        "config": {"workload": "Mixtral-8x7B-shaped MoE layer prefill, 512 tokens (BASELINE configs[2])",
+                   "path": "tcgen05/TMEM grouped GEMM (swap-AB), TMA SW128", "active_experts": active},
+        "gpu_launches": w.forward_launches(n) * args.steps, "clocks": clk.summary(),
+        "roofline": {"bound": "hbm", "achieved": round(bw, 1), "peak": peak_bw, "unit": "GB/s",
+                     "frac": round(bw / peak_bw, 4), "traffic": None, "alg_bytes_per_step": bytes_,
+                     "tensor_tflops": round(tf, 1), "tensor_frac": round(tf / peaks["bf16_tflops"], 4),
+                     "peak_source": src},
+    }), flush=True)
+    w.close()
+    ctx.close()
+
+
 def _mixtral_layer_for_reference(d, f, E, k, token, seed=0):
     """fp64 weights of one Mixtral-shaped layer for the reference's CPU path:
     a random router and random N(0,1/sqrt(d)) weights for the experts the
@@ -389,7 +448,8 @@ def main():
     ap.add_argument("--steps", type=int, default=300)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--config", default="stack32", choices=sorted(CONFIGS))
+    ap.add_argument("--config", default="stack32", choices=sorted(CONFIGS) + ["prefill512"])
+    ap.add_argument("--prefill-tokens", type=int, default=512)
     ap.add_argument("--seed", type=int, default=0)
     ap.add_argument("--cpu-tokens", type=int, default=12)
     ap.add_argument("--ref-threads", type=int, default=0)
@@ -408,6 +468,8 @@ def main():
         os.environ["MOE_B200_STACK"] = "0"
     if args.impl == "reference":
         run_reference(args)
+    elif args.config == "prefill512":
+        run_prefill(args)
     else:
         run_ours(args)
 
