@@ -44,10 +44,53 @@ __global__ void __launch_bounds__(256) router_topk_kernel(const float* __restric
   if (warp == 0) warp_topk_softmax(logits, E, k, ids + (size_t)blockIdx.x * k, gates + (size_t)blockIdx.x * k);
 }
 
+// Multi-token router: kRouterTok tokens per block, so each router row is read
+// once per block instead of once per token.  Per (token, expert) the
+// arithmetic order is exactly router_topk_kernel's (lane-strided fma, then
+// warp_sum), so batch-1 and prefill routing agree bit for bit.
+constexpr int kRouterTok = 16;
+__global__ void __launch_bounds__(256) router_topk_multi_kernel(const float* __restrict__ router,
+                                                                const float* __restrict__ x,
+                                                                int n_tok, int d, int E, int k,
+                                                                int32_t* ids, float* gates) {
+  __shared__ float logits[kRouterTok][kMaxExperts];
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  griddep_wait();
+  griddep_launch_dependents();
+  const int t0 = blockIdx.x * kRouterTok;
+  const int nt = min(kRouterTok, n_tok - t0);
+  for (int e = warp; e < E; e += 8) {
+    const float* re = router + (size_t)e * d;
+    float s[kRouterTok];
+#pragma unroll
+    for (int t = 0; t < kRouterTok; ++t) s[t] = 0.f;
+    for (int c = lane; c < d; c += 32) {
+      const float r = re[c];
+#pragma unroll
+      for (int t = 0; t < kRouterTok; ++t)
+        if (t < nt) s[t] = fmaf(r, x[(size_t)(t0 + t) * d + c], s[t]);
+    }
+#pragma unroll
+    for (int t = 0; t < kRouterTok; ++t) {
+      const float v = warp_sum(s[t]);
+      if (lane == 0) logits[t][e] = v;
+    }
+  }
+  __syncthreads();
+  for (int t = warp; t < nt; t += 8)
+    warp_topk_softmax(logits[t], E, k, ids + (size_t)(t0 + t) * k, gates + (size_t)(t0 + t) * k);
+}
+
 cudaError_t launch_router_topk(const float* router, const float* x, int n_tok, const Dims& dm,
                                int32_t* ids, float* gates, cudaStream_t s, bool pdl) {
   if (n_tok <= 0) return cudaSuccess;
   cudaLaunchAttribute attr[1];
+  if (n_tok >= 2 * kRouterTok) {
+    cudaLaunchConfig_t cfg =
+        make_cfg(dim3((n_tok + kRouterTok - 1) / kRouterTok), dim3(256), s, pdl, attr);
+    return cudaLaunchKernelEx(&cfg, router_topk_multi_kernel, router, x, n_tok, dm.d, dm.E, dm.k,
+                              ids, gates);
+  }
   cudaLaunchConfig_t cfg = make_cfg(dim3(n_tok), dim3(256), s, pdl, attr);
   return cudaLaunchKernelEx(&cfg, router_topk_kernel, router, x, dm.d, dm.E, dm.k, ids, gates);
 }
