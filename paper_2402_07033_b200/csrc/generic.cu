@@ -48,7 +48,7 @@ __global__ void __launch_bounds__(256) router_topk_kernel(const float* __restric
 // once per block instead of once per token.  Per (token, expert) the
 // arithmetic order is exactly router_topk_kernel's (lane-strided fma, then
 // warp_sum), so batch-1 and prefill routing agree bit for bit.
-constexpr int kRouterTok = 16;
+constexpr int kRouterTok = 4;
 __global__ void __launch_bounds__(256) router_topk_multi_kernel(const float* __restrict__ router,
                                                                 const float* __restrict__ x,
                                                                 int n_tok, int d, int E, int k,
@@ -64,6 +64,7 @@ __global__ void __launch_bounds__(256) router_topk_multi_kernel(const float* __r
     float s[kRouterTok];
 #pragma unroll
     for (int t = 0; t < kRouterTok; ++t) s[t] = 0.f;
+#pragma unroll 4
     for (int c = lane; c < d; c += 32) {
       const float r = re[c];
 #pragma unroll
@@ -85,7 +86,7 @@ cudaError_t launch_router_topk(const float* router, const float* x, int n_tok, c
                                int32_t* ids, float* gates, cudaStream_t s, bool pdl) {
   if (n_tok <= 0) return cudaSuccess;
   cudaLaunchAttribute attr[1];
-  if (n_tok >= 2 * kRouterTok) {
+  if (n_tok >= 4096) {  // only once one-token-per-block would exceed ~28 waves
     cudaLaunchConfig_t cfg =
         make_cfg(dim3((n_tok + kRouterTok - 1) / kRouterTok), dim3(256), s, pdl, attr);
     return cudaLaunchKernelEx(&cfg, router_topk_multi_kernel, router, x, n_tok, dm.d, dm.E, dm.k,
