@@ -410,3 +410,30 @@ def test_prefill_tcgen05_small_uneven(ctx, orc, monkeypatch):
 def test_prefill_tcgen05_mixtral_layer_512(ctx, orc, monkeypatch):
     """Config P: Mixtral-shaped layer, 512-token prefill on the tcgen05 path."""
     _prefill_case(ctx, orc, monkeypatch, 1, 4096, 14336, 512, 5, [0, 1, 77, 200, 311, 511])
+
+
+def test_router_many_tokens_batched_kernel(ctx, orc):
+    """n_tok >= 4096 takes the batched router (4 tokens per block); its ids
+    and gates must equal the one-token-per-block kernel's bit for bit."""
+    s = M.Shape(1, 8, 2, 512, 1792, 4)
+    w = M.Weights(ctx, s, M.DTYPE_F32)
+    ow = orc.random_model(O.Shape(1, 8, 2, 512, 1792, 4), 1)
+    w.upload_router(0, ow.router[0])
+    n = 4100
+    x = torch.randn(n, 512, device="cuda")
+    ids = torch.zeros((n, 2), dtype=torch.int32, device="cuda")
+    g = torch.zeros((n, 2), dtype=torch.float32, device="cuda")
+    w.router_topk(0, x, ids, g)
+    ids1 = torch.zeros((n, 2), dtype=torch.int32, device="cuda")
+    g1 = torch.zeros((n, 2), dtype=torch.float32, device="cuda")
+    for c0 in range(0, n, 1000):  # < 4096 per call -> per-token kernel
+        c1 = min(n, c0 + 1000)
+        w.router_topk(0, x[c0:c1], ids1[c0:c1], g1[c0:c1])
+    torch.cuda.synchronize()
+    assert torch.equal(ids, ids1) and torch.equal(g, g1)
+    router = w.download_router(0)
+    xs = x.cpu().numpy().astype(np.float64)
+    for t in range(0, n, 97):
+        want, _, logits = orc.gate_topk(router, xs[t], 2)
+        if margin(logits, 2) > 1e-5:
+            assert list(ids[t].cpu().numpy()) == list(want)
