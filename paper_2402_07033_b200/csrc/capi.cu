@@ -141,6 +141,10 @@ struct moe_weights {
   DevBuf xbuf2, gbar, dev_layers, dev_slots;  // persistent stack kernel
   DevBuf pf_counts, pf_offsets, pf_perm, pf_xg, pf_h;  // tcgen05 prefill
   bool prefill_enabled = true;
+  // router projections R_{l+1} W2 for the stack kernel's z partials
+  std::vector<DevBuf> rw_mem;  // [L-1]
+  DevBuf dev_rw;               // device [L] pointers
+  bool rw_enabled = false, rw_dirty = true;
   bool stack_enabled = true;
   DevBuf stage_d;  // fp64 staging for uploads / downloads
   void* host_pin = nullptr;
@@ -253,10 +257,25 @@ bool use_stack(const moe_weights* w, int n_tok) {
   return use_decode(w, n_tok, nullptr) && w->ctx->world == 1 && w->stack_enabled && w->L() > 0;
 }
 
+// Recompute rw = R_{l+1} W2 after any weight/router change (outside capture).
+int refresh_projection(moe_weights* w) {
+  if (!w->rw_enabled || !w->rw_dirty || !use_stack(w, 1)) return MOE_OK;
+  cudaStream_t s = w->ctx->stream;
+  const Dims dm = w->dims();
+  for (int l = 0; l + 1 < w->L(); ++l)
+    CU(moe::launch_router_projection(w->layer_mem[l], w->n_local[l], dm,
+                                     w->router + (size_t)(l + 1) * dm.E * dm.d,
+                                     w->rw_mem[l].as<float>(), s));
+  CU(cudaStreamSynchronize(s));
+  w->rw_dirty = false;
+  return MOE_OK;
+}
+
 int enqueue_stack(moe_weights* w, float* x, int32_t* ids, float* gates, cudaStream_t s,
                   unsigned long long* trace = nullptr) {
   moe::StackDesc sd;
   sd.trace = trace;
+  sd.rw = w->rw_enabled ? w->dev_rw.as<const float* const>() : nullptr;
   sd.layer_experts = w->dev_layers.as<const void* const>();
   sd.slot_of = w->dev_slots.as<const int16_t>();
   sd.expert_stride = 3 * w->mat_elems();
@@ -542,6 +561,24 @@ int moe_weights_create(moe_ctx* c, const moe_shape* shape, int dtype, const int3
     return cleanup(fail(MOE_ERR_CUDA, "router memset failed"));
   w->device_bytes += rbytes;
   w->plan = moe::plan_decode(w->dims(), c->sm_count);
+  {
+    const char* env = getenv("MOE_B200_RW");
+    w->rw_enabled = w->plan.ok && c->world == 1 && L >= 2 && E <= 8 &&
+                    (size_t)E * shape->hidden_dim * 4 <= 200 * 1024 && !(env && env[0] == '0');
+    if (w->rw_enabled) {
+      w->rw_mem.resize(L - 1);
+      std::vector<const float*> ptrs(L, nullptr);
+      for (int l = 0; l + 1 < L; ++l) {
+        if (w->rw_mem[l].ensure(sizeof(float) * (size_t)std::max(1, w->n_local[l]) * shape->ffn_dim * E))
+          return cleanup(fail(MOE_ERR_OOM, "cudaMalloc router projections"));
+        ptrs[l] = w->rw_mem[l].as<float>();
+        w->device_bytes += (int64_t)w->rw_mem[l].bytes;
+      }
+      if (w->dev_rw.ensure(sizeof(void*) * L) ||
+          cudaMemcpy(w->dev_rw.p, ptrs.data(), sizeof(void*) * L, cudaMemcpyHostToDevice))
+        return cleanup(fail(MOE_ERR_CUDA, "upload projection table"));
+    }
+  }
   if (const char* env = getenv("MOE_B200_STACK")) w->stack_enabled = env[0] != '0';
   if (const char* env = getenv("MOE_B200_PREFILL")) w->prefill_enabled = env[0] != '0';
   {
@@ -565,6 +602,8 @@ int moe_weights_destroy(moe_weights* w) {
   cudaSetDevice(w->ctx->device);
   for (auto& kv : w->graphs)
     if (kv.second.exec) cudaGraphExecDestroy(kv.second.exec);
+  for (DevBuf& b : w->rw_mem) b.release();
+  w->dev_rw.release();
   for (void* p : w->layer_mem)
     if (p) cudaFree(p);
   if (w->router) cudaFree(w->router);
@@ -590,6 +629,7 @@ static int check_le(moe_weights* w, int layer, int expert) {
 int moe_weights_upload_expert(moe_weights* w, int layer, int expert, const double* w_in,
                               const double* w_gate, const double* w_out) {
   TRY(check_le(w, layer, expert));
+  w->rw_dirty = true;
   if (!w_in || !w_gate || !w_out) return fail(MOE_ERR_ARG, "null matrix");
   std::lock_guard<std::mutex> lk(w->mu);
   if (w->slot_of[(size_t)layer * w->E() + expert] < 0) return MOE_OK;  // remote
@@ -613,6 +653,7 @@ int moe_weights_upload_expert(moe_weights* w, int layer, int expert, const doubl
 
 int moe_weights_upload_router(moe_weights* w, int layer, const double* router) {
   TRY(check_le(w, layer, 0));
+  w->rw_dirty = true;
   if (!router) return fail(MOE_ERR_ARG, "null router");
   std::lock_guard<std::mutex> lk(w->mu);
   TRY(set_device(w->ctx));
@@ -627,6 +668,7 @@ int moe_weights_upload_router(moe_weights* w, int layer, const double* router) {
 
 int moe_weights_random(moe_weights* w, uint64_t seed) {
   if (!w) return fail(MOE_ERR_ARG, "null weights");
+  w->rw_dirty = true;
   std::lock_guard<std::mutex> lk(w->mu);
   TRY(set_device(w->ctx));
   cudaStream_t s = w->ctx->stream;
@@ -763,7 +805,10 @@ int moe_forward(moe_weights* w, float* x, int n_tok, int32_t* ids, float* gates,
   TRY(set_device(w->ctx));
   TRY(ensure_scratch(w, n_tok));
   cudaStream_t s = pick(w->ctx, stream);
-  if (n_tok == 1 && w->plan.ok) return forward_graph(w, x, ids, gates, s);
+  if (n_tok == 1 && w->plan.ok) {
+    TRY(refresh_projection(w));
+    return forward_graph(w, x, ids, gates, s);
+  }
   return enqueue_forward(w, x, n_tok, ids, gates, s, nullptr);
 }
 
@@ -801,6 +846,7 @@ int moe_forward_host(moe_weights* w, const double* tokens, int n_tok, double* ou
     TRY(enqueue_forward(w, dx, n_tok, dids, dg, s, w->post.as<float>()));
     CU(cudaMemcpyAsync(hpost, w->post.p, npost * 4, cudaMemcpyDeviceToHost, s));
   } else if (n_tok == 1 && w->plan.ok) {
+    TRY(refresh_projection(w));
     TRY(forward_graph(w, dx, dids, dg, s));
   } else {
     TRY(enqueue_forward(w, dx, n_tok, dids, dg, s, nullptr));
@@ -914,6 +960,7 @@ int moe_debug_trace_forward(moe_weights* w, float* x, int32_t* ids, float* gates
   std::lock_guard<std::mutex> lk(w->mu);
   TRY(set_device(w->ctx));
   TRY(ensure_scratch(w, 1));
+  TRY(refresh_projection(w));
   DevBuf buf;
   TRY(buf.ensure(n * 8));
   cudaStream_t s = w->ctx->stream;

@@ -94,12 +94,20 @@ __device__ __forceinline__ void produce_rows(const Ring& R, Cursor& cur, const W
 }
 
 // Consumers: accumulate yacc += sum over rows of gate*silu(W1 x)*(W3 x)*W2T.
+// Optional router projection (z): with rw = R_{l+1} W2 precomputed per expert
+// as [f][E] fp32 (E <= kZMax), warp 0 also accumulates
+//   z[e] += sum_r h'_r * rw[r][e]        (h'_r = gate * silu(a_r) * b_r)
+// i.e. this CTA's share of the next layer's router logits, with no extra
+// pass over W2 and the rw rows prefetched at batch start.
+constexpr int kZMax = 8;
 template <typename W, int NV>
 __device__ __forceinline__ void consume_rows(const Ring& R, Cursor& cur, const float* xr,
                                              float* yacc, const float* s_gate, int f,
                                              long long g0, long long g1, float* red, float* h_s,
                                              int tid, int ncons, int bar_id,
-                                             unsigned long long* t_first = nullptr) {
+                                             unsigned long long* t_first = nullptr,
+                                             const float* rw = nullptr, const int* s_slot = nullptr,
+                                             int E = 0, float* zreg = nullptr) {
   constexpr int VEC = Elem<W>::kVec;
   const int warp = tid >> 5, lane = tid & 31, ncw = ncons >> 5;
   const int total_vec = (int)(3 * (g1 - g0));
@@ -122,6 +130,12 @@ __device__ __forceinline__ void consume_rows(const Ring& R, Cursor& cur, const f
     const int r = (int)(g - (long long)jj * f);
     const int nb = (int)min((long long)kBatch, min(g1 - g, (long long)(f - r)));
     const float gate = s_gate[jj];
+    float rwv[kZMax];
+    if (rw != nullptr && warp == 0) {  // prefetch: consumed after this batch's up phase
+      const float* rp = rw + ((size_t)s_slot[jj] * f + r + lane) * E;
+#pragma unroll
+      for (int e = 0; e < kZMax; ++e) rwv[e] = (lane < nb && e < E) ? __ldg(rp + e) : 0.f;
+    }
 
     // -- up: W1 rows [0,nb) then W3 rows [0,nb) of this batch
     float acc[2 * kBatch];
@@ -160,7 +174,12 @@ __device__ __forceinline__ void consume_rows(const Ring& R, Cursor& cur, const f
       float tot = 0.f;
       for (int w = 0; w < ncw; ++w) tot += red[w * 32 + lane];
       const float b = __shfl_down_sync(MOE_FULL_MASK, tot, kBatch);
-      if (lane < nb) h_s[lane] = gate * (silu_f(tot) * b);
+      const float hq = lane < nb ? gate * (silu_f(tot) * b) : 0.f;
+      if (lane < nb) h_s[lane] = hq;
+      if (rw != nullptr) {
+#pragma unroll
+        for (int e = 0; e < kZMax; ++e) zreg[e] += warp_sum(hq * rwv[e]);
+      }
     }
     named_bar_sync(bar_id, ncons);
 
@@ -360,7 +379,8 @@ struct StackArgs {
   int32_t* ids_out;                  // [L][k]
   float* gates_out;                  // [L][k]
   unsigned* gbar;                    // grid barrier counter (0 at launch)
-  unsigned long long* trace;         // optional [L][G][8] globaltimer stamps
+  unsigned long long* trace;         // optional [L][G][16] clock64 stamps
+  const float* const* rw;            // [L] R_{l+1} W2 per local expert [f][E] (nullptr: off)
   int L, d, f, E, k;
   int row_bytes, rps, stages, stage_bytes;
 };
@@ -508,6 +528,23 @@ __global__ void __launch_bounds__(kMaxConsWarps * 32 + 32, 1)
   if (warp == 0) commit_route(0);
   named_bar_sync(2, ncons);
 
+  // z bookkeeping (warp 0 registers): zreg = this CTA's sum_r h'_r rw[r][:],
+  // xt = R_{l+1}[:, chunk] . x_l[chunk] (its share of the x_l term)
+  const bool use_rw = a.rw != nullptr;
+  float zreg[kZMax], xt[kZMax];
+#pragma unroll
+  for (int e = 0; e < kZMax; ++e) zreg[e] = xt[e] = 0.f;
+  if (use_rw && warp == 0 && a.L > 1) {
+    const float* r1 = a.router + (size_t)E * d;
+    for (int base = cc0; base < cc1; base += 32) {
+      const int col = base + lane;
+      const float xv = col < cc1 ? __ldcg(&a.x[col]) : 0.f;
+#pragma unroll
+      for (int e = 0; e < kZMax; ++e)
+        xt[e] += warp_sum((col < cc1 && e < E) ? r1[(size_t)e * d + col] * xv : 0.f);
+    }
+  }
+
   for (int l = 0; l < a.L; ++l) {
     const bool more = l + 1 < a.L;
     const float* xl = (l == 0) ? a.x : a.xbuf + (size_t)(l & 1) * d;
@@ -524,13 +561,23 @@ __global__ void __launch_bounds__(kMaxConsWarps * 32 + 32, 1)
     for (int i = 0; i < NV * VEC; ++i) yacc[i] = 0.f;
     const long long T = (long long)s_nloc * a.f;
     const long long g0 = (long long)c * T / G, g1 = (long long)(c + 1) * T / G;
+    const float* rwl = (use_rw && more) ? a.rw[l] : nullptr;
     consume_rows<W, NV>(R, cur, xr, yacc, s_gate, a.f, g0, g1, red, h_s, tid, ncons, 1,
-                        tr ? tr + 1 : nullptr);
+                        tr ? tr + 1 : nullptr, rwl, s_slot, E, zreg);
     if (tr && tid == 0) tr[2] = clock64();
     store_y<W, NV>(a.ypart + (size_t)c * d, yacc, tid, ncons);
 
-    // ---- z_c = R_{l+1} (ypart_c [+ x_l]) : next layer's router partial ----
-    if (more) {
+    // ---- z_c: this CTA's partial of the next layer's router logits ----
+    if (more && use_rw) {
+      if (warp == 0) {
+#pragma unroll
+        for (int e = 0; e < kZMax; ++e) {
+          if (lane == e && e < E) a.rpart[(size_t)e * G + c] = zreg[e] + xt[e];
+          zreg[e] = 0.f;
+          xt[e] = 0.f;
+        }
+      }
+    } else if (more) {  // fallback (E > kZMax): z_c = R_{l+1} (ypart_c [+ x_l])
       const float* rn = a.router + (size_t)(l + 1) * E * d;
       float v[NV * VEC];
 #pragma unroll
@@ -592,16 +639,31 @@ __global__ void __launch_bounds__(kMaxConsWarps * 32 + 32, 1)
     }
 
     // ---- C: this CTA's column chunk of x_{l+1} = x_l + sum_c ypart_c ----
+    const bool next_xt = use_rw && l + 2 < a.L;
+    const float* r2 = next_xt ? a.router + (size_t)(l + 2) * E * d : nullptr;
     for (int base = cc0; base < cc1; base += 32) {
       const int col = base + lane;
       const bool valid = col < cc1;
+      float rv[kZMax];
+      if (next_xt && warp == 0) {  // issued before the partial sums: latency overlaps
+#pragma unroll
+        for (int e = 0; e < kZMax; ++e) rv[e] = (valid && e < E) ? __ldg(r2 + (size_t)e * d + col) : 0.f;
+      }
       const float s = valid ? strided_sum(a.ypart + col, warp, G, ncw, (size_t)d) : 0.f;
       red[warp * 32 + lane] = s;
       named_bar_sync(2, ncons);
-      if (warp == 0 && valid) {
-        float tot = 0.f;
-        for (int w = 0; w < ncw; ++w) tot += red[w * 32 + lane];
-        xn[col] = __ldcg(&xl[col]) + tot;
+      if (warp == 0) {
+        float xo = 0.f;
+        if (valid) {
+          float tot = 0.f;
+          for (int w = 0; w < ncw; ++w) tot += red[w * 32 + lane];
+          xo = __ldcg(&xl[col]) + tot;
+          xn[col] = xo;
+        }
+        if (next_xt) {
+#pragma unroll
+          for (int e = 0; e < kZMax; ++e) xt[e] += warp_sum(rv[e] * xo);
+        }
       }
       named_bar_sync(2, ncons);
     }
@@ -740,6 +802,7 @@ cudaError_t launch_decode_stack(const DecodePlan& p, const StackDesc& sd, const 
   a.gates_out = gates_out;
   a.gbar = gbar;
   a.trace = sd.trace;
+  a.rw = sd.rw;
   a.L = sd.L;
   a.d = dm.d;
   a.f = dm.f;

@@ -51,8 +51,12 @@ struct StackDesc {
   long long expert_stride, mat_stride;
   const float* router;               // [L][E][d]
   int L;
-  unsigned long long* trace = nullptr;  // optional [L][G][8] globaltimer stamps
+  unsigned long long* trace = nullptr;  // optional [L][G][16] clock64 stamps
+  const float* const* rw = nullptr;     // device [L]: R_{l+1} W2 per local expert, [f][E]
 };
+// rw[slot][r][e] = sum_i R_next[e][i] * W2T[slot][r][i]   (fp32; E <= 8)
+cudaError_t launch_router_projection(const void* layer_experts, int n_local, const Dims& dm,
+                                     const float* router_next, float* rw, cudaStream_t s);
 cudaError_t launch_decode_stack(const DecodePlan& p, const StackDesc& sd, const Dims& dm,
                                 float* x, float* xbuf, float* ypart, float* rpart,
                                 int32_t* ids_out, float* gates_out, unsigned* gbar,

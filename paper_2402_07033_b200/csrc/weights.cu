@@ -108,6 +108,66 @@ cudaError_t launch_convert_f32(const double* src, float* dst, long long n, cudaS
   return cudaGetLastError();
 }
 
+// ---- router projection: rw[slot][r][:] = R_next · W2T[slot][r][:] ---------------
+// The next layer's router applied to each ffn column of W2 (decode.cu uses it
+// to assemble the next layer's logits during the down projection).  R_next is
+// staged in shared memory; one warp per ffn row, fixed summation order.
+constexpr int kProjE = 8;
+template <typename W>
+__global__ void __launch_bounds__(256) router_projection_kernel(const W* __restrict__ experts,
+                                                                long long expert_stride,
+                                                                long long mat_stride, int d, int f,
+                                                                int E, const float* __restrict__ rn,
+                                                                float* __restrict__ rw) {
+  extern __shared__ float rs[];  // [E][d]
+  for (int i = threadIdx.x; i < E * d; i += blockDim.x) rs[i] = rn[i];
+  __syncthreads();
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int slot = blockIdx.y;
+  const W* w2t = experts + slot * expert_stride + 2 * mat_stride;
+  for (int r = blockIdx.x * 8 + warp; r < f; r += gridDim.x * 8) {
+    float acc[kProjE];
+#pragma unroll
+    for (int e = 0; e < kProjE; ++e) acc[e] = 0.f;
+    const W* row = w2t + (size_t)r * d;
+    for (int i = lane; i < d; i += 32) {
+      const float w = Elem<W>::to_float(row[i]);
+#pragma unroll
+      for (int e = 0; e < kProjE; ++e)
+        if (e < E) acc[e] = fmaf(w, rs[e * d + i], acc[e]);
+    }
+#pragma unroll
+    for (int e = 0; e < kProjE; ++e) {
+      const float v = warp_sum(acc[e]);
+      if (lane == 0 && e < E) rw[((size_t)slot * f + r) * E + e] = v;
+    }
+  }
+}
+
+cudaError_t launch_router_projection(const void* layer_experts, int n_local, const Dims& dm,
+                                     const float* router_next, float* rw, cudaStream_t s) {
+  if (n_local == 0) return cudaSuccess;
+  if (dm.E > kProjE) return cudaErrorInvalidValue;
+  const size_t smem = sizeof(float) * (size_t)dm.E * dm.d;
+  const dim3 grid((unsigned)std::min(148 * 2, (dm.f + 7) / 8), (unsigned)n_local);
+  const long long es = 3LL * dm.f * dm.d, ms = (long long)dm.f * dm.d;
+  cudaError_t e;
+  if (dm.dtype == MOE_DTYPE_BF16) {
+    e = cudaFuncSetAttribute(router_projection_kernel<__nv_bfloat16>,
+                             cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    router_projection_kernel<__nv_bfloat16><<<grid, 256, smem, s>>>(
+        static_cast<const __nv_bfloat16*>(layer_experts), es, ms, dm.d, dm.f, dm.E, router_next, rw);
+  } else {
+    e = cudaFuncSetAttribute(router_projection_kernel<float>,
+                             cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    router_projection_kernel<float><<<grid, 256, smem, s>>>(
+        static_cast<const float*>(layer_experts), es, ms, dm.d, dm.f, dm.E, router_next, rw);
+  }
+  return cudaGetLastError();
+}
+
 // ---- Philox4x32-10 ----------------------------------------------------------
 __device__ __forceinline__ uint4 philox(uint4 c, uint2 k) {
 #pragma unroll
