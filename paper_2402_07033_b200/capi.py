@@ -23,7 +23,8 @@ _lib = None
 
 
 def lib_path() -> str:
-    return os.path.join(BUILD, "libmoe_b200.so")
+    # MOE_B200_LIB: an alternative in-tree build (A/B experiments)
+    return os.environ.get("MOE_B200_LIB") or os.path.join(BUILD, "libmoe_b200.so")
 
 
 class MoeError(RuntimeError):

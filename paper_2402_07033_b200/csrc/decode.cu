@@ -170,18 +170,20 @@ __device__ __forceinline__ void consume_rows(const Ring& R, Cursor& cur, const f
     }
     red[warp * 32 + lane] = acc[0];
     named_bar_sync(bar_id, ncons);
+    float hq = 0.f;
     if (warp == 0) {
       float tot = 0.f;
       for (int w = 0; w < ncw; ++w) tot += red[w * 32 + lane];
       const float b = __shfl_down_sync(MOE_FULL_MASK, tot, kBatch);
-      const float hq = lane < nb ? gate * (silu_f(tot) * b) : 0.f;
+      hq = lane < nb ? gate * (silu_f(tot) * b) : 0.f;
       if (lane < nb) h_s[lane] = hq;
-      if (rw != nullptr) {
-#pragma unroll
-        for (int e = 0; e < kZMax; ++e) zreg[e] += warp_sum(hq * rwv[e]);
-      }
     }
     named_bar_sync(bar_id, ncons);
+    // z accumulation after the barrier: the other warps are not held up
+    if (rw != nullptr && warp == 0) {
+#pragma unroll
+      for (int e = 0; e < kZMax; ++e) zreg[e] += warp_sum(hq * rwv[e]);
+    }
 
     // -- down: W2T rows [0,nb): y += h[q] * W2T[r+q][:]
 #pragma unroll
