@@ -44,6 +44,11 @@ struct Elem<float> {
 
 __device__ __forceinline__ float silu_f(float a) { return a / (1.0f + expf(-a)); }
 
+// Broadcast from lane 0: the compiler then treats the value (and branches on
+// it) as warp-uniform, so shuffles under `if (warp == ...)` need no
+// WARPSYNC.COLLECTIVE emulation.
+__device__ __forceinline__ int warp_uniform(int v) { return __shfl_sync(MOE_FULL_MASK, v, 0); }
+
 __device__ __forceinline__ float warp_sum(float v) {
 #pragma unroll
   for (int s = 16; s >= 1; s >>= 1) v += __shfl_xor_sync(MOE_FULL_MASK, v, s);

@@ -109,7 +109,7 @@ __device__ __forceinline__ void consume_rows(const Ring& R, Cursor& cur, const f
                                              const float* rw = nullptr, const int* s_slot = nullptr,
                                              int E = 0, float* zreg = nullptr) {
   constexpr int VEC = Elem<W>::kVec;
-  const int warp = tid >> 5, lane = tid & 31, ncw = ncons >> 5;
+  const int warp = warp_uniform(tid >> 5), lane = tid & 31, ncw = ncons >> 5;
   const int total_vec = (int)(3 * (g1 - g0));
   int p = 0;
   auto acquire = [&]() -> const uint8_t* {
@@ -269,7 +269,8 @@ __global__ void __launch_bounds__(kMaxConsWarps * 32 + 32, 1)
 
   const int ncons = blockDim.x - 32;
   const int ncw = ncons >> 5;
-  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int tid = threadIdx.x, lane = tid & 31;
+  const int warp = warp_uniform(tid >> 5);  // provably warp-uniform: no collective fallback
 
   if (tid == 0) {
     for (int s = 0; s < a.stages; ++s) {
@@ -324,7 +325,8 @@ __global__ void __launch_bounds__(256) reduce_residual_kernel(
   __shared__ float xs[32];
   __shared__ float logits[kMaxExperts];
   __shared__ int s_last;
-  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int tid = threadIdx.x, lane = tid & 31;
+  const int warp = warp_uniform(tid >> 5);  // provably warp-uniform: no collective fallback
   griddep_wait();
   griddep_launch_dependents();
   const int i = blockIdx.x * 32 + lane;
@@ -454,7 +456,8 @@ __global__ void __launch_bounds__(kMaxConsWarps * 32 + 32, 1)
 
   const int ncons = blockDim.x - 32;
   const int ncw = ncons >> 5;
-  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int tid = threadIdx.x, lane = tid & 31;
+  const int warp = warp_uniform(tid >> 5);  // provably warp-uniform: no collective fallback
   const int G = gridDim.x, c = blockIdx.x;
   const int d = a.d, E = a.E, k = a.k;
 
@@ -513,6 +516,9 @@ __global__ void __launch_bounds__(kMaxConsWarps * 32 + 32, 1)
   Cursor cur;
   const int cc0 = (int)((long long)c * d / G), cc1 = (int)((long long)(c + 1) * d / G);
   if (a.trace && tid == 0) {
+    unsigned smid;
+    asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+    if (a.L > 1) a.trace[((size_t)1 * G + c) * 16 + 13] = smid;  // layer-1 row, slot 13
     a.trace[(size_t)c * 16 + 12] = clock64();
     a.trace[(size_t)c * 16 + 13] = globaltimer();
     a.trace[(size_t)c * 16 + 0] = clock64();

@@ -29,7 +29,8 @@ __global__ void __launch_bounds__(256) router_topk_kernel(const float* __restric
                                                           int E, int k, int32_t* ids,
                                                           float* gates) {
   __shared__ float logits[kMaxExperts];
-  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int tid = threadIdx.x, lane = tid & 31;
+  const int warp = warp_uniform(tid >> 5);
   griddep_wait();
   griddep_launch_dependents();
   const float* xt = x + (size_t)blockIdx.x * d;
@@ -54,7 +55,8 @@ __global__ void __launch_bounds__(256) router_topk_multi_kernel(const float* __r
                                                                 int n_tok, int d, int E, int k,
                                                                 int32_t* ids, float* gates) {
   __shared__ float logits[kRouterTok][kMaxExperts];
-  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int tid = threadIdx.x, lane = tid & 31;
+  const int warp = warp_uniform(tid >> 5);
   griddep_wait();
   griddep_launch_dependents();
   const int t0 = blockIdx.x * kRouterTok;
@@ -102,7 +104,7 @@ __global__ void __launch_bounds__(256) generic_up_kernel(LayerWeights lw, int d,
                                                          const float* __restrict__ x,
                                                          const int32_t* __restrict__ ids,
                                                          float* h, float* post_silu) {
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int warp = warp_uniform(threadIdx.x >> 5), lane = threadIdx.x & 31;
   griddep_wait();
   griddep_launch_dependents();
   const int r = blockIdx.x * 8 + warp;
@@ -234,7 +236,8 @@ __global__ void __launch_bounds__(1024) permute_kernel(const int32_t* __restrict
   int32_t* run = sm;             // [E] running count per expert
   int32_t* off = run + E;        // [E] exclusive offsets
   int32_t* wcnt = off + E;       // [32][E] per-warp counts of the chunk
-  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int tid = threadIdx.x, lane = tid & 31;
+  const int warp = warp_uniform(tid >> 5);
   for (int e = tid; e < E; e += blockDim.x) run[e] = 0;
   __syncthreads();
   // pass 1: counts

@@ -150,7 +150,7 @@ __global__ void __launch_bounds__(PF_THREADS, 1)
   uint32_t* tmem_base_s = reinterpret_cast<uint32_t*>(tmem_full + 1);
 
   const int e = blockIdx.z;
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int warp = warp_uniform(threadIdx.x >> 5), lane = threadIdx.x & 31;
   griddep_wait();
   const int count = a.counts[e];
   const int row0 = blockIdx.y * PF_MAXN;
@@ -254,7 +254,7 @@ __global__ void __launch_bounds__(PF_THREADS, 1)
   uint32_t* tmem_base_s = reinterpret_cast<uint32_t*>(tmem_full + 1);
 
   const int e = blockIdx.z;
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int warp = warp_uniform(threadIdx.x >> 5), lane = threadIdx.x & 31;
   griddep_wait();
   const int count = a.counts[e];
   const int row0 = blockIdx.y * PF_MAXN;

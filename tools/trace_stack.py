@@ -54,7 +54,7 @@ def main():
     torch.cuda.synchronize()
     res = []
     for _ in range(args.reps):
-        raw = w.debug_trace_forward(x, ids, g)
+        raw = w.debug_trace_forward(x, ids, g).copy()
         t, ghz = to_ns(raw)
         med = lambda a: float(np.median(a))  # noqa: E731
         rows = []
@@ -85,6 +85,7 @@ def main():
     print(json.dumps(res[-1], indent=1))
     if args.out:
         json.dump(res, open(args.out, "w"), indent=1)
+        np.save(args.out.replace(".json", "") + "_raw.npy", raw)
 
 
 if __name__ == "__main__":
