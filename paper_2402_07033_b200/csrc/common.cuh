@@ -159,46 +159,6 @@ __device__ __forceinline__ void named_bar_sync(int id, int nthreads) {
 __device__ __forceinline__ void warp_topk_softmax(const float* logits, int E, int k,
                                                   int32_t* ids, float* gates) {
   const int lane = threadIdx.x & 31;
-  if (E <= 8 && k <= 8) {
-    // lane 0, registers only (no shuffles): the common 8-expert router
-    if (lane == 0) {
-      float v[8];
-#pragma unroll
-      for (int e = 0; e < 8; ++e) v[e] = e < E ? logits[e] : 0.f;
-      unsigned taken = 0u;
-      for (int j = 0; j < k; ++j) {
-        int best = -1;
-        float bv = 0.f;
-#pragma unroll
-        for (int e = 0; e < 8; ++e) {
-          const bool ok = e < E && !((taken >> e) & 1u) && (best < 0 || v[e] > bv);
-          best = ok ? e : best;
-          bv = ok ? v[e] : bv;
-        }
-        taken |= 1u << best;
-      }
-      float mx = -INFINITY;
-#pragma unroll
-      for (int e = 0; e < 8; ++e)
-        if ((taken >> e) & 1u) mx = fmaxf(mx, v[e]);
-      float w[8], denom = 0.f;
-#pragma unroll
-      for (int e = 0; e < 8; ++e) {  // ascending-id order, like the reference
-        w[e] = ((taken >> e) & 1u) ? expf(v[e] - mx) : 0.f;
-        if ((taken >> e) & 1u) denom += w[e];
-      }
-      int pos = 0;
-#pragma unroll
-      for (int e = 0; e < 8; ++e)
-        if ((taken >> e) & 1u) {
-          ids[pos] = e;
-          gates[pos] = w[e] / denom;
-          ++pos;
-        }
-    }
-    __syncwarp();
-    return;
-  }
   if (E <= 32) {
     // all-pairs rank: rank(e) = #{e' : l[e'] > l[e] or (l[e'] == l[e] and e' < e)};
     // the E shuffles are independent (no dependent argmax chain).
