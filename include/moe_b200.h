@@ -72,6 +72,11 @@ int moe_ctx_sm_count(moe_ctx* ctx);
 int moe_ep_unique_id(void* uid128);
 int moe_ctx_init_ep(moe_ctx* ctx, int world, int rank, const void* uid128);
 int moe_ctx_world(moe_ctx* ctx, int* world, int* rank);
+/* Testing hook: give this context an expert-parallel (world, rank) with NO
+ * communicator.  Weights created on it hold only rank `rank`'s experts and
+ * the per-layer exchange is skipped, so x_out = x + (this rank's partial
+ * delta); a test sums the ranks' partials itself (e.g. W contexts on one GPU). */
+int moe_ctx_set_virtual_rank(moe_ctx* ctx, int world, int rank);
 
 /* ---- weights (ModelWeights, model.hpp:29-49) ---------------------------
  * owner_rank: optional [L*E] shard map (NULL = every expert local).  Only

@@ -88,6 +88,7 @@ def lib():
         "moe_ep_unique_id": ([_vp], C.c_int),
         "moe_ctx_init_ep": ([_vp, C.c_int, C.c_int, _vp], C.c_int),
         "moe_ctx_world": ([_vp, C.POINTER(C.c_int), C.POINTER(C.c_int)], C.c_int),
+        "moe_ctx_set_virtual_rank": ([_vp, C.c_int, C.c_int], C.c_int),
         "moe_weights_create": ([_vp, C.POINTER(_Shape), C.c_int, _vp, C.POINTER(_vp)], C.c_int),
         "moe_weights_destroy": ([_vp], C.c_int),
         "moe_weights_device_bytes": ([_vp], C.c_int64),
@@ -179,6 +180,9 @@ class Ctx:
     def init_ep(self, world: int, rank: int, uid: bytes):
         buf = C.create_string_buffer(bytes(uid), 128)
         check(lib().moe_ctx_init_ep(self.h, world, rank, buf))
+
+    def set_virtual_rank(self, world: int, rank: int):
+        check(lib().moe_ctx_set_virtual_rank(self.h, world, rank))
 
     @staticmethod
     def unique_id() -> bytes:
