@@ -140,8 +140,9 @@ struct moe_weights {
   // scratch
   DevBuf ypart, rpart, counter, xa, xb, xin, h, y, delta, ids, gates, post;
   DevBuf xbuf2, gbar, dev_layers, dev_slots;  // persistent stack kernel
-  DevBuf pf_counts, pf_offsets, pf_perm, pf_xg, pf_h;  // tcgen05 prefill
+  DevBuf pf_counts, pf_offsets, pf_perm, pf_xg, pf_h, pf_sync;  // tcgen05 prefill
   bool prefill_enabled = true;
+  int prefill_splits = 2;  // K splits of the down GEMM in the grouped kernel (0: 2-kernel path)
   // router projections R_{l+1} W2 for the stack kernel's z partials
   std::vector<DevBuf> rw_mem;  // [L-1]
   DevBuf dev_rw;               // device [L] pointers
@@ -300,7 +301,8 @@ int ensure_prefill_scratch(moe_weights* w, int n_tok) {
   TRY(w->pf_perm.ensure(4 * rows));
   TRY(w->pf_xg.ensure(2 * rows * w->d()));
   TRY(w->pf_h.ensure(2 * rows * w->f()));
-  TRY(w->y.ensure(4 * rows * w->d()));
+  TRY(w->y.ensure(4 * rows * w->d() * (size_t)std::max(1, w->prefill_splits)));
+  TRY(w->pf_sync.ensure(4 * (1 + (size_t)w->E() * ((n_tok + 255) / 256))));
   return MOE_OK;
 }
 
@@ -329,6 +331,7 @@ int experts_forward(moe_weights* w, int l, const float* x, int n_tok, const int3
     return MOE_OK;
   }
   const float* cgates = gates;
+  int nsplit = 1;
   if (use_prefill(w, n_tok, post)) {
     // tcgen05 grouped GEMM: permute -> gather -> up -> down (gate in epilogue)
     TRY(ensure_prefill_scratch(w, n_tok));
@@ -337,21 +340,25 @@ int experts_forward(moe_weights* w, int l, const float* x, int n_tok, const int3
     int32_t* offsets = w->pf_offsets.as<int32_t>();
     int32_t* perm = w->pf_perm.as<int32_t>();
     CU(moe::launch_permute(ids, n_tok, dm.k, dm.E, counts, offsets, perm, nullptr, s));
-    if (w->n_local[l] < dm.E) CU(cudaMemsetAsync(w->y.p, 0, (size_t)rows * dm.d * 4, s));
+    const int S = w->prefill_splits;
+    if (w->n_local[l] < dm.E)
+      CU(cudaMemsetAsync(w->y.p, 0, (size_t)std::max(1, S) * rows * dm.d * 4, s));
     CU(moe::launch_prefill_experts(lw, w->n_local[l], dm, n_tok, x, counts, offsets, perm, gates,
                                    w->dev_slots.as<int16_t>() + (size_t)l * dm.E,
                                    w->pf_xg.as<__nv_bfloat16>(), w->pf_h.as<__nv_bfloat16>(),
-                                   w->y.as<float>(), s));
+                                   w->y.as<float>(), w->pf_sync.as<int>(), w->ctx->sm_count, S,
+                                   s));
     cgates = nullptr;
+    nsplit = std::max(1, S);
   } else {
     CU(moe::launch_generic_up(lw, dm, x, n_tok, ids, w->h.as<float>(), post, s, pdl));
     CU(moe::launch_generic_down(lw, dm, w->h.as<float>(), n_tok, ids, w->y.as<float>(), s, pdl));
   }
   if (!ep) {
-    CU(moe::launch_combine(x, w->y.as<float>(), cgates, n_tok, dm, x_out, s, pdl));
+    CU(moe::launch_combine(x, w->y.as<float>(), cgates, n_tok, dm, x_out, s, pdl, nsplit));
   } else {
     float* delta = w->delta.as<float>();
-    CU(moe::launch_combine(nullptr, w->y.as<float>(), cgates, n_tok, dm, delta, s, pdl));
+    CU(moe::launch_combine(nullptr, w->y.as<float>(), cgates, n_tok, dm, delta, s, pdl, nsplit));
     TRY(allreduce(w, delta, (size_t)n_tok * dm.d, s));
     CU(moe::launch_add(x, delta, x_out, (long long)n_tok * dm.d, s, false));
   }
@@ -592,6 +599,7 @@ int moe_weights_create(moe_ctx* c, const moe_shape* shape, int dtype, const int3
   }
   if (const char* env = getenv("MOE_B200_STACK")) w->stack_enabled = env[0] != '0';
   if (const char* env = getenv("MOE_B200_PREFILL")) w->prefill_enabled = env[0] != '0';
+  if (const char* env = getenv("MOE_B200_PREFILL_SPLITS")) w->prefill_splits = atoi(env);
   {
     // device-side tables for the persistent stack kernel
     const int Lm = std::max(1, L);
@@ -621,7 +629,7 @@ int moe_weights_destroy(moe_weights* w) {
   for (DevBuf* b : {&w->ypart, &w->rpart, &w->counter, &w->xa, &w->xb, &w->xin, &w->h, &w->y, &w->delta,
                     &w->ids, &w->gates, &w->post, &w->stage_d, &w->xbuf2, &w->gbar,
                     &w->dev_layers, &w->dev_slots, &w->pf_counts, &w->pf_offsets, &w->pf_perm,
-                    &w->pf_xg, &w->pf_h})
+                    &w->pf_xg, &w->pf_h, &w->pf_sync})
     b->release();
   if (w->host_pin) cudaFreeHost(w->host_pin);
   delete w;

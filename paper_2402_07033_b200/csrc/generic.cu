@@ -186,7 +186,7 @@ cudaError_t launch_generic_down(const LayerWeights& lw, const Dims& dm, const fl
 // x == nullptr writes the bare combined delta (expert-parallel partials).
 __global__ void __launch_bounds__(256) combine_kernel(const float* x, const float* __restrict__ y,
                                                       const float* __restrict__ gates, int k, int d,
-                                                      float* x_out) {
+                                                      float* x_out, int nsplit, long long sstride) {
   griddep_wait();
   griddep_launch_dependents();
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
@@ -194,17 +194,21 @@ __global__ void __launch_bounds__(256) combine_kernel(const float* x, const floa
   const int t = blockIdx.y;
   float c = 0.f;
   // gates == nullptr: y already carries the gate (tcgen05 prefill epilogue)
-  for (int j = 0; j < k; ++j)
-    c += (gates ? gates[(size_t)t * k + j] : 1.0f) * y[((size_t)t * k + j) * d + i];
+  for (int j = 0; j < k; ++j) {
+    const float g = gates ? gates[(size_t)t * k + j] : 1.0f;
+    for (int sp = 0; sp < nsplit; ++sp)  // K-split partials, fixed order
+      c += g * y[sp * sstride + ((size_t)t * k + j) * d + i];
+  }
   x_out[(size_t)t * d + i] = (x ? x[(size_t)t * d + i] : 0.f) + c;
 }
 
 cudaError_t launch_combine(const float* x, const float* y, const float* gates, int n_tok,
-                           const Dims& dm, float* x_out, cudaStream_t s, bool pdl) {
+                           const Dims& dm, float* x_out, cudaStream_t s, bool pdl, int nsplit) {
   if (n_tok <= 0) return cudaSuccess;
   cudaLaunchAttribute attr[1];
   cudaLaunchConfig_t cfg = make_cfg(dim3((dm.d + 255) / 256, n_tok), dim3(256), s, pdl, attr);
-  return cudaLaunchKernelEx(&cfg, combine_kernel, x, y, gates, dm.k, dm.d, x_out);
+  const long long sstride = (long long)n_tok * dm.k * dm.d;
+  return cudaLaunchKernelEx(&cfg, combine_kernel, x, y, gates, dm.k, dm.d, x_out, nsplit, sstride);
 }
 
 __global__ void add_kernel(const float* a, const float* __restrict__ b, float* out, long long n) {

@@ -80,7 +80,8 @@ cudaError_t launch_generic_down(const LayerWeights& lw, const Dims& dm, const fl
                                 bool pdl);
 // x_out[t][i] = x[t][i] + (0 + sum_j g[t][j] * y[t][j][i])   (model.cpp:128-147)
 cudaError_t launch_combine(const float* x, const float* y, const float* gates, int n_tok,
-                           const Dims& dm, float* x_out, cudaStream_t s, bool pdl);
+                           const Dims& dm, float* x_out, cudaStream_t s, bool pdl,
+                           int nsplit = 1);
 
 // out = a + b (elementwise; expert-parallel residual after the all-reduce)
 cudaError_t launch_add(const float* a, const float* b, float* out, long long n, cudaStream_t s,
@@ -94,8 +95,10 @@ cudaError_t launch_prefill_experts(const LayerWeights& lw, int n_local, const Di
                                    int n_tok, const float* x, const int32_t* counts,
                                    const int32_t* offsets, const int32_t* perm,
                                    const float* gates, const int16_t* slot_of_dev,
-                                   __nv_bfloat16* xg, __nv_bfloat16* h, float* y,
-                                   cudaStream_t s);
+                                   __nv_bfloat16* xg, __nv_bfloat16* h, float* y, int* sync,
+                                   int sm_count, int splits, cudaStream_t s);
+// splits > 0: persistent grouped kernel, y is [splits][n*k][d] (sum the splits);
+// splits == 0: two-kernel path, y is [n*k][d].  sync: 1 + E*ceil(n_tok/256) ints.
 
 // ---- permutation ------------------------------------------------------------
 cudaError_t launch_permute(const int32_t* ids, int n_tok, int k, int E, int32_t* counts,

@@ -340,6 +340,310 @@ __global__ void __launch_bounds__(PF_THREADS, 1)
   if (warp == 5) tmem_free(tmem, 256);
 }
 
+// ===== persistent grouped kernel: up AND down tiles of all experts =========
+// One CTA per SM pulls tiles from a global atomic counter (dynamic balance,
+// no wave quantisation).  Tile order: every up tile (expert-major, then token
+// chunk, then ffn tile), then every down tile (expert, chunk, hidden tile,
+// K split).  A down tile of (e, chunk) waits until all ffn tiles of that
+// (e, chunk) have published H (per-(e,chunk) counter, release/acquire +
+// fence.proxy.async before its TMA reads).  Up tiles never wait, so the
+// schedule cannot deadlock.  The producer warp runs ahead into the next tile
+// while the epilogue warps drain TMEM, so the ring refills behind the epilogue.
+constexpr int GP_STAGES = 3;
+constexpr int GP_STAGE = 2 * PF_BM * PF_BK * 2 + PF_MAXN * PF_BK * 2;  // 64 KB
+constexpr int GP_QN = 2;
+constexpr int GP_SMEM = GP_STAGES * GP_STAGE + 1024 /*align*/ + 4096 /*barriers, queue, tables*/;
+
+struct GroupedArgs {
+  const int32_t* counts;
+  const int32_t* offsets;
+  const int32_t* perm;
+  const float* gates;
+  const int16_t* slot_of;  // [E] of this layer
+  __nv_bfloat16* h;        // [rows, f]
+  float* y;                // [S][rows, d]
+  int* done;               // [E][max_chunks], zero at launch
+  unsigned* tile_counter;  // zero at launch
+  int d, f, k, E, rows, S, max_chunks;
+};
+
+struct GTile {
+  int up, e, c, t1, s;  // t1: ffn tile (up) or hidden tile (down)
+};
+
+__device__ __forceinline__ GTile gp_decode(int t, int total_up, const int* upb, const int* dnb,
+                                           int E, int n_ft, int n_dt, int S) {
+  GTile g;
+  if (t < total_up) {
+    int e = 0;
+    while (upb[e + 1] <= t) ++e;
+    const int loc = t - upb[e];
+    g.up = 1;
+    g.e = e;
+    g.c = loc / n_ft;
+    g.t1 = loc % n_ft;
+    g.s = 0;
+  } else {
+    const int t2 = t - total_up;
+    int e = 0;
+    while (dnb[e + 1] <= t2) ++e;
+    const int loc = t2 - dnb[e];
+    g.up = 0;
+    g.e = e;
+    g.c = loc / (n_dt * S);
+    const int rem = loc % (n_dt * S);
+    g.t1 = rem / S;
+    g.s = rem % S;
+  }
+  return g;
+}
+
+__global__ void __launch_bounds__(PF_THREADS, 1)
+    prefill_grouped_kernel(const __grid_constant__ CUtensorMap wmap_up,  // box 64 x 128
+                           const __grid_constant__ CUtensorMap wmap_dn,  // box 64 x 64
+                           const __grid_constant__ CUtensorMap xmap,     // Xg, box 64 x 64
+                           const __grid_constant__ CUtensorMap hmap,     // H,  box 64 x 64
+                           GroupedArgs a) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                             ~uintptr_t(1023));
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + GP_STAGES * GP_STAGE);
+  uint64_t* empty = full + GP_STAGES;
+  uint64_t* tmem_full = empty + GP_STAGES;
+  uint64_t* tmem_empty = tmem_full + 1;
+  uint64_t* qfull = tmem_empty + 1;
+  uint64_t* qempty = qfull + GP_QN;
+  uint32_t* tmem_base_s = reinterpret_cast<uint32_t*>(qempty + GP_QN);
+  int* q_tile = reinterpret_cast<int*>(tmem_base_s + 1);
+  int* upb = q_tile + GP_QN;          // [E+1] up tiles before expert e
+  int* dnb = upb + kMaxExperts + 1;   // [E+1] down tiles before expert e
+  __shared__ int s_total_up, s_total;
+
+  const int warp = warp_uniform(threadIdx.x >> 5), lane = threadIdx.x & 31;
+  const int n_ft = a.f / PF_BM, n_dt = a.d / PF_BM;
+  griddep_wait();
+  if (threadIdx.x == 0) {
+    upb[0] = dnb[0] = 0;
+    for (int e = 0; e < a.E; ++e) {
+      const int ch = a.slot_of[e] >= 0 ? (a.counts[e] + PF_MAXN - 1) / PF_MAXN : 0;
+      upb[e + 1] = upb[e] + ch * n_ft;
+      dnb[e + 1] = dnb[e] + ch * n_dt * a.S;
+    }
+    s_total_up = upb[a.E];
+    s_total = upb[a.E] + dnb[a.E];
+    for (int i = 0; i < GP_STAGES; ++i) {
+      mbar_init(&full[i], 1);
+      mbar_init(&empty[i], 1);
+    }
+    mbar_init(tmem_full, 1);
+    mbar_init(tmem_empty, 1);
+    for (int i = 0; i < GP_QN; ++i) {
+      mbar_init(&qfull[i], 1);
+      mbar_init(&qempty[i], 2);  // MMA lane + epilogue thread 0
+    }
+    fence_mbar_init();
+  }
+  if (warp == 5) tmem_alloc(tmem_base_s, 512);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_base_s;
+  const int total_up = s_total_up, total = s_total;
+  const int nkb_up = a.d / PF_BK, nkb_dn = a.f / PF_BK;
+  constexpr int kA = PF_BM * PF_BK * 2;
+  constexpr int kBox = PF_BOXN * PF_BK * 2;
+
+  auto chunk_geom = [&](const GTile& g, int& nvalid, int& N, int& nboxes, int& srow) {
+    const int row0 = g.c * PF_MAXN;
+    nvalid = min(PF_MAXN, a.counts[g.e] - row0);
+    N = (nvalid + 15) & ~15;
+    nboxes = (N + PF_BOXN - 1) / PF_BOXN;
+    srow = a.offsets[g.e] + row0;
+  };
+
+  if (warp == 4) {
+    // ===== producer =====
+    if (lane == 0) {
+      tma_prefetch_desc(&wmap_up);
+      tma_prefetch_desc(&wmap_dn);
+      tma_prefetch_desc(&xmap);
+      tma_prefetch_desc(&hmap);
+      uint32_t kc = 0;
+      int qi = 0;
+      uint32_t qph = 0;
+      while (true) {
+        const int t = (int)atomicAdd(a.tile_counter, 1u);
+        mbar_wait(&qempty[qi], qph ^ 1);
+        q_tile[qi] = t;
+        mbar_arrive(&qfull[qi]);
+        if (++qi == GP_QN) {
+          qi = 0;
+          qph ^= 1;
+        }
+        if (t >= total) break;
+        const GTile g = gp_decode(t, total_up, upb, dnb, a.E, n_ft, n_dt, a.S);
+        int nvalid, N, nboxes, srow;
+        chunk_geom(g, nvalid, N, nboxes, srow);
+        const int slot = a.slot_of[g.e];
+        if (g.up) {
+          const int w1row = (slot * 3 + 0) * a.f + g.t1 * PF_BM;
+          const int w3row = (slot * 3 + 1) * a.f + g.t1 * PF_BM;
+          const uint32_t bytes = 2 * kA + nboxes * kBox;
+          for (int kb = 0; kb < nkb_up; ++kb, ++kc) {
+            const int st = kc % GP_STAGES;
+            mbar_wait(&empty[st], ((kc / GP_STAGES) & 1) ^ 1);
+            uint8_t* sp = smem + st * GP_STAGE;
+            mbar_arrive_expect_tx(&full[st], bytes);
+            tma_load_2d(sp, &wmap_up, kb * PF_BK, w1row, &full[st]);
+            tma_load_2d(sp + kA, &wmap_up, kb * PF_BK, w3row, &full[st]);
+            for (int b = 0; b < nboxes; ++b)
+              tma_load_2d(sp + 2 * kA + b * kBox, &xmap, kb * PF_BK, srow + b * PF_BOXN, &full[st]);
+          }
+        } else {
+          // wait for every ffn tile of (e, chunk): H complete
+          const int* flag = a.done + g.e * a.max_chunks + g.c;
+          int v;
+          do {
+            asm volatile("ld.acquire.gpu.global.s32 %0, [%1];" : "=r"(v) : "l"(flag) : "memory");
+            if (v < n_ft) __nanosleep(64);
+          } while (v < n_ft);
+          asm volatile("fence.proxy.async.global;" ::: "memory");
+          const int d0 = g.t1 * PF_BM;
+          const int w2row = (slot * 3 + 2) * a.f;
+          const int kb0 = g.s * nkb_dn / a.S, kb1 = (g.s + 1) * nkb_dn / a.S;
+          const uint32_t bytes = kA + nboxes * kBox;
+          for (int kb = kb0; kb < kb1; ++kb, ++kc) {
+            const int st = kc % GP_STAGES;
+            mbar_wait(&empty[st], ((kc / GP_STAGES) & 1) ^ 1);
+            uint8_t* sp = smem + st * GP_STAGE;
+            mbar_arrive_expect_tx(&full[st], bytes);
+            tma_load_2d(sp, &wmap_dn, d0, w2row + kb * PF_BK, &full[st]);
+            tma_load_2d(sp + kA / 2, &wmap_dn, d0 + 64, w2row + kb * PF_BK, &full[st]);
+            for (int b = 0; b < nboxes; ++b)
+              tma_load_2d(sp + kA + b * kBox, &hmap, kb * PF_BK, srow + b * PF_BOXN, &full[st]);
+          }
+        }
+      }
+    }
+  } else if (warp == 5) {
+    // ===== MMA issuer =====
+    if (lane == 0) {
+      uint32_t kc = 0, acc_ph = 0;
+      int qi = 0;
+      uint32_t qph = 0;
+      while (true) {
+        mbar_wait(&qfull[qi], qph);
+        const int t = q_tile[qi];
+        mbar_arrive(&qempty[qi]);
+        if (++qi == GP_QN) {
+          qi = 0;
+          qph ^= 1;
+        }
+        if (t >= total) break;
+        const GTile g = gp_decode(t, total_up, upb, dnb, a.E, n_ft, n_dt, a.S);
+        int nvalid, N, nboxes, srow;
+        chunk_geom(g, nvalid, N, nboxes, srow);
+        mbar_wait(tmem_empty, acc_ph ^ 1);
+        tc_fence_after();
+        if (g.up) {
+          const uint32_t idesc = umma_idesc(N, false);
+          for (int kb = 0; kb < nkb_up; ++kb, ++kc) {
+            const int st = kc % GP_STAGES;
+            mbar_wait(&full[st], (kc / GP_STAGES) & 1);
+            tc_fence_after();
+            const uint8_t* sp = smem + st * GP_STAGE;
+#pragma unroll
+            for (int kk = 0; kk < PF_BK / 16; ++kk) {
+              const uint64_t b = umma_desc(sp + 2 * kA + kk * 32, 16, 1024);
+              const uint32_t acc = (kb | kk) != 0;
+              umma_f16(tmem, umma_desc(sp + kk * 32, 16, 1024), b, idesc, acc);
+              umma_f16(tmem + 256, umma_desc(sp + kA + kk * 32, 16, 1024), b, idesc, acc);
+            }
+            umma_commit(&empty[st]);
+          }
+        } else {
+          const uint32_t idesc = umma_idesc(N, true);
+          const int nk = (g.s + 1) * nkb_dn / a.S - g.s * nkb_dn / a.S;
+          for (int kb = 0; kb < nk; ++kb, ++kc) {
+            const int st = kc % GP_STAGES;
+            mbar_wait(&full[st], (kc / GP_STAGES) & 1);
+            tc_fence_after();
+            const uint8_t* sp = smem + st * GP_STAGE;
+#pragma unroll
+            for (int kk = 0; kk < PF_BK / 16; ++kk)
+              umma_f16(tmem, umma_desc(sp + kk * 2048, kA / 2, 1024),
+                       umma_desc(sp + kA + kk * 32, 16, 1024), idesc, (kb | kk) != 0);
+            umma_commit(&empty[st]);
+          }
+        }
+        umma_commit(tmem_full);
+        acc_ph ^= 1;
+      }
+    }
+  } else {
+    // ===== epilogue (warps 0-3) =====
+    uint32_t acc_ph = 0;
+    int qi = 0;
+    uint32_t qph = 0;
+    const uint32_t lane_base = tmem + ((uint32_t)(warp * 32) << 16);
+    while (true) {
+      mbar_wait(&qfull[qi], qph);
+      const int t = q_tile[qi];
+      named_bar_sync(3, 128);
+      if (threadIdx.x == 0) mbar_arrive(&qempty[qi]);
+      if (++qi == GP_QN) {
+        qi = 0;
+        qph ^= 1;
+      }
+      if (t >= total) break;
+      const GTile g = gp_decode(t, total_up, upb, dnb, a.E, n_ft, n_dt, a.S);
+      int nvalid, N, nboxes, srow;
+      chunk_geom(g, nvalid, N, nboxes, srow);
+      mbar_wait(tmem_full, acc_ph);
+      tc_fence_after();
+      if (g.up) {
+        const int frow = g.t1 * PF_BM + warp * 32 + lane;
+        for (int c0 = 0; c0 < N; c0 += 16) {
+          float d1[16], d3[16];
+          tmem_ld16(lane_base + c0, d1);
+          tmem_ld16(lane_base + 256 + c0, d3);
+#pragma unroll
+          for (int i = 0; i < 16; ++i)
+            if (c0 + i < nvalid)
+              a.h[(size_t)(srow + c0 + i) * a.f + frow] = __float2bfloat16_rn(silu_f(d1[i]) * d3[i]);
+        }
+      } else {
+        const int drow = g.t1 * PF_BM + warp * 32 + lane;
+        float* ys = a.y + (size_t)g.s * a.rows * a.d;
+        for (int c0 = 0; c0 < N; c0 += 16) {
+          float v[16];
+          tmem_ld16(lane_base + c0, v);
+#pragma unroll
+          for (int i = 0; i < 16; ++i)
+            if (c0 + i < nvalid) {
+              const int p = a.perm[srow + c0 + i];
+              ys[(size_t)p * a.d + drow] = a.gates[p] * v[i];
+            }
+        }
+      }
+      tc_fence_before();
+      named_bar_sync(3, 128);
+      if (threadIdx.x == 0) {
+        mbar_arrive(tmem_empty);
+        if (g.up) {
+          __threadfence();
+          asm volatile("red.release.gpu.global.add.s32 [%0], 1;" ::"l"(a.done + g.e * a.max_chunks + g.c)
+                       : "memory");
+        }
+      }
+      acc_ph ^= 1;
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 5) tmem_free(tmem, 512);
+}
+
 // Xg[sorted row] = bf16(x[token of that pair])
 __global__ void gather_rows_kernel(const float* __restrict__ x, const int32_t* __restrict__ perm,
                                    int nrows, int k, int d, __nv_bfloat16* xg) {
@@ -394,8 +698,8 @@ cudaError_t launch_prefill_experts(const LayerWeights& lw, int n_local, const Di
                                    int n_tok, const float* x, const int32_t* counts,
                                    const int32_t* offsets, const int32_t* perm,
                                    const float* gates, const int16_t* slot_of_dev,
-                                   __nv_bfloat16* xg, __nv_bfloat16* h, float* y,
-                                   cudaStream_t s) {
+                                   __nv_bfloat16* xg, __nv_bfloat16* h, float* y, int* sync,
+                                   int sm_count, int splits, cudaStream_t s) {
   const int rows = n_tok * dm.k;
   if (rows == 0 || n_local == 0) return cudaSuccess;
   gather_rows_kernel<<<rows, 256, 0, s>>>(x, perm, rows, dm.k, dm.d, xg);
@@ -407,6 +711,34 @@ cudaError_t launch_prefill_experts(const LayerWeights& lw, int n_local, const Di
       !make_map(&wmap_dn, lw.experts, wrows, dm.d, 64, PF_BK) ||
       !make_map(&xmap, xg, rows, dm.d, 64, PF_BOXN) || !make_map(&hmap, h, rows, dm.f, 64, PF_BOXN))
     return cudaErrorInvalidValue;
+  const int chunks = (n_tok + PF_MAXN - 1) / PF_MAXN;  // an expert holds <= n_tok tokens
+  if (splits > 0) {
+    // persistent grouped kernel (default)
+    GroupedArgs g;
+    g.counts = counts;
+    g.offsets = offsets;
+    g.perm = perm;
+    g.gates = gates;
+    g.slot_of = slot_of_dev;
+    g.h = h;
+    g.y = y;
+    g.done = sync + 1;
+    g.tile_counter = reinterpret_cast<unsigned*>(sync);
+    g.d = dm.d;
+    g.f = dm.f;
+    g.k = dm.k;
+    g.E = dm.E;
+    g.rows = rows;
+    g.S = splits;
+    g.max_chunks = chunks;
+    err = cudaMemsetAsync(sync, 0, sizeof(int) * (1 + (size_t)dm.E * chunks), s);
+    if (err != cudaSuccess) return err;
+    err = cudaFuncSetAttribute(prefill_grouped_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               GP_SMEM);
+    if (err != cudaSuccess) return err;
+    prefill_grouped_kernel<<<sm_count, PF_THREADS, GP_SMEM, s>>>(wmap_up, wmap_dn, xmap, hmap, g);
+    return cudaGetLastError();
+  }
   PrefillArgs a;
   a.counts = counts;
   a.offsets = offsets;
@@ -418,7 +750,6 @@ cudaError_t launch_prefill_experts(const LayerWeights& lw, int n_local, const Di
   a.d = dm.d;
   a.f = dm.f;
   a.k = dm.k;
-  const int chunks = (n_tok + PF_MAXN - 1) / PF_MAXN;  // an expert holds <= n_tok tokens
   {
     const int smem = PfSmem<kUpStages, 2>::kBytes;
     auto kern = prefill_up_kernel<kUpStages>;
