@@ -26,6 +26,7 @@
 #include <cudaTypedefs.h>
 
 #include <algorithm>
+#include <cstdlib>
 
 #include "../../include/moe_b200.h"
 #include "common.cuh"
@@ -113,6 +114,42 @@ __device__ __forceinline__ void tmem_ld16(uint32_t taddr, float* v) {
 #pragma unroll
   for (int i = 0; i < 16; ++i) v[i] = __uint_as_float(r[i]);
 }
+
+// 32 lanes x 32 bit, 32 consecutive columns; call tmem_ld_wait() before use
+__device__ __forceinline__ void tmem_ld32_nowait(uint32_t taddr, uint32_t* r) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,"
+      "%15,%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
+        "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]),
+        "=r"(r[14]), "=r"(r[15]), "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]),
+        "=r"(r[21]), "=r"(r[22]), "=r"(r[23]), "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]),
+        "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+      : "r"(taddr));
+}
+__device__ __forceinline__ void tmem_ld_wait() {
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+}
+
+// TMEM double buffering for the grouped kernel: 2 buffers x 256 columns.  A
+// tile takes one buffer (down; up with N <= 128 as D1|D3) or both (up with
+// N > 128: D1 in one, D3 in the other).  The MMA warp and the epilogue warps
+// replay the same assignment from the same tile sequence.
+struct TmemSched {
+  uint32_t next = 0, uses0 = 0, uses1 = 0;
+  __device__ __forceinline__ int take(bool wide, int* b, uint32_t* par) {
+    b[0] = next;
+    b[1] = next ^ 1;
+    const int n = wide ? 2 : 1;
+    for (int i = 0; i < n; ++i) {
+      uint32_t& u = b[i] ? uses1 : uses0;
+      par[i] = u & 1;
+      ++u;
+    }
+    if (!wide) next ^= 1;
+    return n;
+  }
+};
 
 struct PrefillArgs {
   const int32_t* counts;   // [E] tokens per expert
@@ -365,6 +402,7 @@ struct GroupedArgs {
   int* done;               // [E][max_chunks], zero at launch
   unsigned* tile_counter;  // zero at launch
   int d, f, k, E, rows, S, max_chunks;
+  int debug;  // timing experiments only: bit0 skip up epilogue, bit1 skip down epilogue
 };
 
 struct GTile {
@@ -409,9 +447,9 @@ __global__ void __launch_bounds__(PF_THREADS, 1)
                                              ~uintptr_t(1023));
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + GP_STAGES * GP_STAGE);
   uint64_t* empty = full + GP_STAGES;
-  uint64_t* tmem_full = empty + GP_STAGES;
-  uint64_t* tmem_empty = tmem_full + 1;
-  uint64_t* qfull = tmem_empty + 1;
+  uint64_t* tmem_full = empty + GP_STAGES;  // [2]
+  uint64_t* tmem_empty = tmem_full + 2;      // [2]
+  uint64_t* qfull = tmem_empty + 2;
   uint64_t* qempty = qfull + GP_QN;
   uint32_t* tmem_base_s = reinterpret_cast<uint32_t*>(qempty + GP_QN);
   int* q_tile = reinterpret_cast<int*>(tmem_base_s + 1);
@@ -435,8 +473,10 @@ __global__ void __launch_bounds__(PF_THREADS, 1)
       mbar_init(&full[i], 1);
       mbar_init(&empty[i], 1);
     }
-    mbar_init(tmem_full, 1);
-    mbar_init(tmem_empty, 1);
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&tmem_full[i], 1);
+      mbar_init(&tmem_empty[i], 1);
+    }
     for (int i = 0; i < GP_QN; ++i) {
       mbar_init(&qfull[i], 1);
       mbar_init(&qempty[i], 2);  // MMA lane + epilogue thread 0
@@ -528,7 +568,8 @@ __global__ void __launch_bounds__(PF_THREADS, 1)
   } else if (warp == 5) {
     // ===== MMA issuer =====
     if (lane == 0) {
-      uint32_t kc = 0, acc_ph = 0;
+      uint32_t kc = 0;
+      TmemSched ts;
       int qi = 0;
       uint32_t qph = 0;
       while (true) {
@@ -543,8 +584,13 @@ __global__ void __launch_bounds__(PF_THREADS, 1)
         const GTile g = gp_decode(t, total_up, upb, dnb, a.E, n_ft, n_dt, a.S);
         int nvalid, N, nboxes, srow;
         chunk_geom(g, nvalid, N, nboxes, srow);
-        mbar_wait(tmem_empty, acc_ph ^ 1);
+        int bufs[2];
+        uint32_t par[2];
+        const int nb = ts.take(g.up && N > 128, bufs, par);
+        for (int i = 0; i < nb; ++i) mbar_wait(&tmem_empty[bufs[i]], par[i] ^ 1);
         tc_fence_after();
+        const uint32_t c1 = tmem + bufs[0] * 256;
+        const uint32_t c3 = nb == 2 ? tmem + bufs[1] * 256 : c1 + 128;
         if (g.up) {
           const uint32_t idesc = umma_idesc(N, false);
           for (int kb = 0; kb < nkb_up; ++kb, ++kc) {
@@ -556,8 +602,8 @@ __global__ void __launch_bounds__(PF_THREADS, 1)
             for (int kk = 0; kk < PF_BK / 16; ++kk) {
               const uint64_t b = umma_desc(sp + 2 * kA + kk * 32, 16, 1024);
               const uint32_t acc = (kb | kk) != 0;
-              umma_f16(tmem, umma_desc(sp + kk * 32, 16, 1024), b, idesc, acc);
-              umma_f16(tmem + 256, umma_desc(sp + kA + kk * 32, 16, 1024), b, idesc, acc);
+              umma_f16(c1, umma_desc(sp + kk * 32, 16, 1024), b, idesc, acc);
+              umma_f16(c3, umma_desc(sp + kA + kk * 32, 16, 1024), b, idesc, acc);
             }
             umma_commit(&empty[st]);
           }
@@ -571,21 +617,20 @@ __global__ void __launch_bounds__(PF_THREADS, 1)
             const uint8_t* sp = smem + st * GP_STAGE;
 #pragma unroll
             for (int kk = 0; kk < PF_BK / 16; ++kk)
-              umma_f16(tmem, umma_desc(sp + kk * 2048, kA / 2, 1024),
+              umma_f16(c1, umma_desc(sp + kk * 2048, kA / 2, 1024),
                        umma_desc(sp + kA + kk * 32, 16, 1024), idesc, (kb | kk) != 0);
             umma_commit(&empty[st]);
           }
         }
-        umma_commit(tmem_full);
-        acc_ph ^= 1;
+        for (int i = 0; i < nb; ++i) umma_commit(&tmem_full[bufs[i]]);
       }
     }
   } else {
     // ===== epilogue (warps 0-3) =====
-    uint32_t acc_ph = 0;
+    TmemSched ts;
     int qi = 0;
     uint32_t qph = 0;
-    const uint32_t lane_base = tmem + ((uint32_t)(warp * 32) << 16);
+    const uint32_t lane_off = (uint32_t)(warp * 32) << 16;
     while (true) {
       mbar_wait(&qfull[qi], qph);
       const int t = q_tile[qi];
@@ -599,44 +644,56 @@ __global__ void __launch_bounds__(PF_THREADS, 1)
       const GTile g = gp_decode(t, total_up, upb, dnb, a.E, n_ft, n_dt, a.S);
       int nvalid, N, nboxes, srow;
       chunk_geom(g, nvalid, N, nboxes, srow);
-      mbar_wait(tmem_full, acc_ph);
+      int bufs[2];
+      uint32_t par[2];
+      const int nb = ts.take(g.up && N > 128, bufs, par);
+      for (int i = 0; i < nb; ++i) mbar_wait(&tmem_full[bufs[i]], par[i]);
       tc_fence_after();
-      if (g.up) {
+      const uint32_t c1 = tmem + lane_off + bufs[0] * 256;
+      const uint32_t c3 = nb == 2 ? tmem + lane_off + bufs[1] * 256 : c1 + 128;
+      if (g.up && (a.debug & 1)) {
+      } else if (!g.up && (a.debug & 2)) {
+      } else if (g.up) {
         const int frow = g.t1 * PF_BM + warp * 32 + lane;
-        for (int c0 = 0; c0 < N; c0 += 16) {
-          float d1[16], d3[16];
-          tmem_ld16(lane_base + c0, d1);
-          tmem_ld16(lane_base + 256 + c0, d3);
+        __nv_bfloat16* hcol = a.h + (size_t)srow * a.f + frow;
+        for (int c0 = 0; c0 < N; c0 += 32) {
+          uint32_t r1[32], r3[32];
+          tmem_ld32_nowait(c1 + c0, r1);
+          tmem_ld32_nowait(c3 + c0, r3);
+          tmem_ld_wait();
 #pragma unroll
-          for (int i = 0; i < 16; ++i)
-            if (c0 + i < nvalid)
-              a.h[(size_t)(srow + c0 + i) * a.f + frow] = __float2bfloat16_rn(silu_f(d1[i]) * d3[i]);
+          for (int i = 0; i < 32; ++i)
+            if (c0 + i < nvalid) {
+              const float u = __uint_as_float(r1[i]);
+              const float sv = __fdividef(u, 1.0f + __expf(-u));
+              hcol[(size_t)(c0 + i) * a.f] = __float2bfloat16_rn(sv * __uint_as_float(r3[i]));
+            }
         }
       } else {
         const int drow = g.t1 * PF_BM + warp * 32 + lane;
-        float* ys = a.y + (size_t)g.s * a.rows * a.d;
-        for (int c0 = 0; c0 < N; c0 += 16) {
-          float v[16];
-          tmem_ld16(lane_base + c0, v);
+        float* ys = a.y + (size_t)g.s * a.rows * a.d + drow;
+        for (int c0 = 0; c0 < N; c0 += 32) {
+          uint32_t r[32];
+          tmem_ld32_nowait(c1 + c0, r);
+          tmem_ld_wait();
 #pragma unroll
-          for (int i = 0; i < 16; ++i)
+          for (int i = 0; i < 32; ++i)
             if (c0 + i < nvalid) {
-              const int p = a.perm[srow + c0 + i];
-              ys[(size_t)p * a.d + drow] = a.gates[p] * v[i];
+              const int p = __ldg(a.perm + srow + c0 + i);
+              ys[(size_t)p * a.d] = __ldg(a.gates + p) * __uint_as_float(r[i]);
             }
         }
       }
       tc_fence_before();
       named_bar_sync(3, 128);
       if (threadIdx.x == 0) {
-        mbar_arrive(tmem_empty);
+        for (int i = 0; i < nb; ++i) mbar_arrive(&tmem_empty[bufs[i]]);
         if (g.up) {
           __threadfence();
           asm volatile("red.release.gpu.global.add.s32 [%0], 1;" ::"l"(a.done + g.e * a.max_chunks + g.c)
                        : "memory");
         }
       }
-      acc_ph ^= 1;
     }
   }
   tc_fence_before();
@@ -731,6 +788,7 @@ cudaError_t launch_prefill_experts(const LayerWeights& lw, int n_local, const Di
     g.rows = rows;
     g.S = splits;
     g.max_chunks = chunks;
+    g.debug = getenv("MOE_B200_PF_DEBUG") ? atoi(getenv("MOE_B200_PF_DEBUG")) : 0;
     err = cudaMemsetAsync(sync, 0, sizeof(int) * (1 + (size_t)dm.E * chunks), s);
     if (err != cudaSuccess) return err;
     err = cudaFuncSetAttribute(prefill_grouped_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
