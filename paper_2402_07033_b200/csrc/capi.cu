@@ -142,7 +142,7 @@ struct moe_weights {
   DevBuf xbuf2, gbar, dev_layers, dev_slots;  // persistent stack kernel
   DevBuf pf_counts, pf_offsets, pf_perm, pf_xg, pf_h, pf_sync;  // tcgen05 prefill
   bool prefill_enabled = true;
-  int prefill_splits = 2;  // K splits of the down GEMM in the grouped kernel (0: 2-kernel path)
+  int prefill_splits = 1;  // K splits of the down GEMM in the grouped kernel (0: 2-kernel path)
   // router projections R_{l+1} W2 for the stack kernel's z partials
   std::vector<DevBuf> rw_mem;  // [L-1]
   DevBuf dev_rw;               // device [L] pointers

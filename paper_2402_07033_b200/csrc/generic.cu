@@ -202,10 +202,44 @@ __global__ void __launch_bounds__(256) combine_kernel(const float* x, const floa
   x_out[(size_t)t * d + i] = (x ? x[(size_t)t * d + i] : 0.f) + c;
 }
 
+// float4 variant (d % 4 == 0): same per-element arithmetic order
+__global__ void __launch_bounds__(256) combine4_kernel(const float* x, const float* __restrict__ y,
+                                                       const float* __restrict__ gates, int k, int d,
+                                                       float* x_out, int nsplit, long long sstride) {
+  griddep_wait();
+  griddep_launch_dependents();
+  const int i4 = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i4 * 4 >= d) return;
+  const int t = blockIdx.y;
+  float4 c = make_float4(0.f, 0.f, 0.f, 0.f);
+  for (int j = 0; j < k; ++j) {
+    const float g = gates ? gates[(size_t)t * k + j] : 1.0f;
+    for (int sp = 0; sp < nsplit; ++sp) {
+      const float4 v = __ldg(reinterpret_cast<const float4*>(y + sp * sstride + ((size_t)t * k + j) * d) + i4);
+      c.x += g * v.x;
+      c.y += g * v.y;
+      c.z += g * v.z;
+      c.w += g * v.w;
+    }
+  }
+  float4 o = c;
+  if (x) {
+    const float4 xv = reinterpret_cast<const float4*>(x + (size_t)t * d)[i4];
+    o = make_float4(xv.x + c.x, xv.y + c.y, xv.z + c.z, xv.w + c.w);
+  }
+  reinterpret_cast<float4*>(x_out + (size_t)t * d)[i4] = o;
+}
+
 cudaError_t launch_combine(const float* x, const float* y, const float* gates, int n_tok,
                            const Dims& dm, float* x_out, cudaStream_t s, bool pdl, int nsplit) {
   if (n_tok <= 0) return cudaSuccess;
   cudaLaunchAttribute attr[1];
+  if (dm.d % 4 == 0) {
+    cudaLaunchConfig_t cfg = make_cfg(dim3((dm.d / 4 + 255) / 256, n_tok), dim3(256), s, pdl, attr);
+    const long long sstride = (long long)n_tok * dm.k * dm.d;
+    return cudaLaunchKernelEx(&cfg, combine4_kernel, x, y, gates, dm.k, dm.d, x_out, nsplit,
+                              sstride);
+  }
   cudaLaunchConfig_t cfg = make_cfg(dim3((dm.d + 255) / 256, n_tok), dim3(256), s, pdl, attr);
   const long long sstride = (long long)n_tok * dm.k * dm.d;
   return cudaLaunchKernelEx(&cfg, combine_kernel, x, y, gates, dm.k, dm.d, x_out, nsplit, sstride);

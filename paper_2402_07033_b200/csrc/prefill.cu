@@ -701,16 +701,20 @@ __global__ void __launch_bounds__(PF_THREADS, 1)
   if (warp == 5) tmem_free(tmem, 512);
 }
 
-// Xg[sorted row] = bf16(x[token of that pair])
+// Xg[sorted row] = bf16(x[token of that pair]); float4 in, 4 x bf16 out
 __global__ void gather_rows_kernel(const float* __restrict__ x, const int32_t* __restrict__ perm,
                                    int nrows, int k, int d, __nv_bfloat16* xg) {
   griddep_wait();
   const int row = blockIdx.x;
   if (row >= nrows) return;
   const int t = perm[row] / k;
-  const float* src = x + (size_t)t * d;
-  __nv_bfloat16* dst = xg + (size_t)row * d;
-  for (int i = threadIdx.x; i < d; i += blockDim.x) dst[i] = __float2bfloat16_rn(src[i]);
+  const float4* src = reinterpret_cast<const float4*>(x + (size_t)t * d);
+  uint2* dst = reinterpret_cast<uint2*>(xg + (size_t)row * d);
+  for (int i = threadIdx.x; i < d / 4; i += blockDim.x) {
+    const float4 v = __ldg(src + i);
+    const __nv_bfloat162 a = __floats2bfloat162_rn(v.x, v.y), b = __floats2bfloat162_rn(v.z, v.w);
+    dst[i] = make_uint2(*reinterpret_cast<const uint32_t*>(&a), *reinterpret_cast<const uint32_t*>(&b));
+  }
 }
 
 // ---- host side -----------------------------------------------------------------
@@ -759,7 +763,7 @@ cudaError_t launch_prefill_experts(const LayerWeights& lw, int n_local, const Di
                                    int sm_count, int splits, cudaStream_t s) {
   const int rows = n_tok * dm.k;
   if (rows == 0 || n_local == 0) return cudaSuccess;
-  gather_rows_kernel<<<rows, 256, 0, s>>>(x, perm, rows, dm.k, dm.d, xg);
+  gather_rows_kernel<<<rows, 128, 0, s>>>(x, perm, rows, dm.k, dm.d, xg);  // d % 128 == 0
   cudaError_t err = cudaGetLastError();
   if (err != cudaSuccess) return err;
   CUtensorMap wmap_up, wmap_dn, xmap, hmap;
