@@ -441,12 +441,16 @@ def run_reference(args):
     rs = np.random.RandomState(args.seed + 1)
     token = rs.randn(d)
     ref, shape, w = _mixtral_layer_for_reference(d, f, E, k, token)
-    # each step: every thread pushes one token through one layer (reentrant
-    # model_forward); tok/s for the L-layer stack = threads / (t*L)
+    # each step: every thread pushes one token through one layer of ONE shared
+    # reference model (model_forward is reentrant);
+    # tok/s for the L-layer stack = threads / (t*L)
+    handle = ref.model_create(shape, w)
+    del w
     toks = [np.repeat(token[None], 1, axis=0) for _ in range(threads)]
 
     def one_step():
-        ts = [threading.Thread(target=ref.time_forward, args=(shape, w, toks[i])) for i in range(threads)]
+        ts = [threading.Thread(target=ref.model_forward_timed, args=(handle, toks[i]))
+              for i in range(threads)]
         t0 = time.perf_counter()
         for t in ts:
             t.start()
@@ -457,6 +461,7 @@ def run_reference(args):
     for _ in range(args.warmup):
         one_step()
     times = [one_step() for _ in range(args.steps)]
+    ref.model_destroy(handle)
     secs = sum(times)
     tok_s = threads * args.steps / (secs * L)
     line = {"impl": "reference", "metric": METRIC, "value": round(tok_s, 5), "unit": "tok/s",

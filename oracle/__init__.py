@@ -252,6 +252,10 @@ class Reference(_Base):
         L.ref_expected_hit_rate.argtypes = [C.c_int, C.c_int, _i64p, C.c_int64, _u8p, _dp]
         L.ref_hit_rate_bounds.argtypes = [C.c_int, C.c_int, _i64p, C.c_int64, C.c_int, _dp]
         L.ref_sparsity_histogram.argtypes = [_dp, C.c_int64, _dp, C.c_int, _dp]
+        L.ref_model_create.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]
+        L.ref_model_create.restype = C.c_void_p
+        L.ref_model_destroy.argtypes = [C.c_void_p]
+        L.ref_model_forward_timed.argtypes = [C.c_void_p, C.c_int, _dp, _dp, _dp]
         L.ref_shape_validate.argtypes = [C.c_void_p]
         L.ref_shape_preset.argtypes = [C.c_char_p, _i32p]
 
@@ -316,6 +320,24 @@ class Reference(_Base):
         self._check(self.lib.ref_time_forward(shape.arr(), a, b, c, r, toks.shape[0], _p(toks),
                                               _p(out), C.byref(secs)))
         return out, secs.value
+
+    def model_create(self, shape: Shape, w: Weights):
+        """Persistent reference ModelWeights (built once, shared by threads)."""
+        a, b, c, r = w.ptrs()
+        h = self.lib.ref_model_create(shape.arr(), a, b, c, r)
+        if not h:
+            raise RuntimeError(self.lib.ref_last_error().decode())
+        return h
+
+    def model_destroy(self, h):
+        self.lib.ref_model_destroy(h)
+
+    def model_forward_timed(self, h, tokens):
+        """model_forward on the shared model; releases the GIL (ctypes)."""
+        toks = np.ascontiguousarray(tokens, dtype=np.float64)
+        secs = C.c_double()
+        self._check(self.lib.ref_model_forward_timed(h, toks.shape[0], _p(toks), _dp(), C.byref(secs)))
+        return secs.value
 
     def greedy_place(self, counts, capacity, per_layer_quota=False, total=None):
         counts = np.ascontiguousarray(counts, dtype=np.int64)

@@ -250,6 +250,50 @@ int ref_time_forward(const int32_t* shape, const double* const* w_in,
   }
 }
 
+// Persistent reference model for the CPU baseline: the weights are built
+// once and shared (const) by concurrent model_forward calls — the reference
+// is reentrant, so N host threads each push their own tokens.
+struct RefModel {
+  ModelShape shape;
+  ModelWeights weights;
+};
+
+void* ref_model_create(const int32_t* shape, const double* const* w_in,
+                       const double* const* w_gate, const double* const* w_out,
+                       const double* const* router) {
+  try {
+    auto* m = new RefModel();
+    m->shape = to_shape(shape);
+    m->weights = to_weights(m->shape, w_in, w_gate, w_out, router);
+    return m;
+  } catch (...) {
+    map_exc();
+    return nullptr;
+  }
+}
+
+void ref_model_destroy(void* h) { delete static_cast<RefModel*>(h); }
+
+// model_forward on n_tok tokens of the shared model; wall seconds in *seconds.
+int ref_model_forward_timed(void* h, int n_tok, const double* tokens, double* outputs,
+                            double* seconds) {
+  try {
+    const RefModel* m = static_cast<const RefModel*>(h);
+    const int d = m->shape.hidden_dim;
+    std::vector<std::vector<double>> toks(n_tok);
+    for (int t = 0; t < n_tok; ++t) toks[t].assign(tokens + (size_t)t * d, tokens + (size_t)(t + 1) * d);
+    const auto t0 = std::chrono::steady_clock::now();
+    const ForwardResult r = model_forward(m->shape, m->weights, toks);
+    const auto t1 = std::chrono::steady_clock::now();
+    *seconds = std::chrono::duration<double>(t1 - t0).count();
+    if (outputs)
+      for (int t = 0; t < n_tok; ++t) std::memcpy(outputs + (size_t)t * d, r.outputs[t].data(), d * 8);
+    return 0;
+  } catch (...) {
+    return map_exc();
+  }
+}
+
 // ---- placement (placement.cpp) ----
 static PopularityProfile to_profile(int L, int E, const int64_t* counts, int64_t total) {
   PopularityProfile p;

@@ -999,7 +999,8 @@ int moe_forward_launches(moe_weights* w, int n_tok) {
   if (use_decode(w, n_tok, nullptr)) return 1 + L * (ep ? 3 : 2);
   // per layer: [permute, gather, up, down] or [up, down], combine, (+add for EP),
   // and the next layer's router
-  const int experts = use_prefill(w, n_tok, nullptr) ? 4 : 2;
+  const int experts =
+      use_prefill(w, n_tok, nullptr) ? (w->prefill_splits > 0 ? 3 : 4) : 2;  // grouped: permute, gather, GEMM
   return 1 + L * (experts + 1 + (ep ? 1 : 0)) + (L - 1);
 }
 
