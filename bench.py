@@ -179,6 +179,8 @@ def run_ours(args):
         obj = [M.Ctx.unique_id() if rank == 0 else None]
         dist.broadcast_object_list(obj, src=0)
         ctx.init_ep(world, rank, obj[0])
+    elif os.environ.get("MOE_B200_FORCE_EP") == "1":
+        ctx.init_ep(1, 0, M.Ctx.unique_id())  # 1-rank NCCL: the EP code path on one GPU
     owner = shard_map(L, E, world) if world > 1 else None
     shape = M.Shape(L, E, k, d, f, esz)
     w = M.Weights(ctx, shape, dtype, owner=owner)

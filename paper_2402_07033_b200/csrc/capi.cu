@@ -91,6 +91,8 @@ struct moe_ctx {
   int world = 1, rank = 0;
   void* comm = nullptr;  // ncclComm_t
   bool virtual_ep = false;  // sharded math without a communicator (testing hook)
+  bool ep_forced = false;   // world == 1 but the EP path + NCCL exchange (MOE_B200_FORCE_EP)
+  bool ep() const { return world > 1 || ep_forced; }
   std::mutex mu;
 };
 
@@ -241,7 +243,7 @@ int ensure_scratch_impl(moe_weights* w, int n_tok) {
 
 int allreduce(moe_weights* w, float* buf, size_t count, cudaStream_t s) {
   moe_ctx* c = w->ctx;
-  if (c->world <= 1 || c->virtual_ep) return MOE_OK;  // virtual: caller sums the partials
+  if (!c->ep() || c->virtual_ep) return MOE_OK;  // virtual: caller sums the partials
   NcclApi* api = nccl();
   if (!api || !c->comm) return fail(MOE_ERR_NCCL, "expert parallelism requested without NCCL");
   const int r = api->allReduce(buf, buf, count, kNcclFloat32, kNcclSum, c->comm, s);
@@ -256,7 +258,7 @@ bool use_decode(const moe_weights* w, int n_tok, const float* post) {
 
 // Whole-token persistent kernel: single GPU (no exchange inside a layer).
 bool use_stack(const moe_weights* w, int n_tok) {
-  return use_decode(w, n_tok, nullptr) && w->ctx->world == 1 && w->stack_enabled && w->L() > 0;
+  return use_decode(w, n_tok, nullptr) && !w->ctx->ep() && w->stack_enabled && w->L() > 0;
 }
 
 // Recompute rw = R_{l+1} W2 after any weight/router change (outside capture).
@@ -313,7 +315,7 @@ int experts_forward(moe_weights* w, int l, const float* x, int n_tok, const int3
                     const float* next_router, int32_t* next_ids, float* next_gates) {
   const Dims dm = w->dims();
   const LayerWeights lw = w->layer(l);
-  const bool ep = w->ctx->world > 1;
+  const bool ep = w->ctx->ep();
   if (use_decode(w, n_tok, post)) {
     CU(moe::launch_decode_experts(w->plan, lw, dm, ids, gates, x, w->ypart.as<float>(), s, pdl));
     if (!ep) {
@@ -491,11 +493,13 @@ int moe_ep_unique_id(void* uid128) {
 int moe_ctx_init_ep(moe_ctx* c, int world, int rank, const void* uid128) {
   if (!c || !uid128) return fail(MOE_ERR_ARG, "null argument");
   if (world < 1 || rank < 0 || rank >= world) return fail(MOE_ERR_ARG, "bad world/rank");
-  if (world == 1) {
+  const char* force = getenv("MOE_B200_FORCE_EP");
+  if (world == 1 && !(force && force[0] == '1')) {
     c->world = 1;
     c->rank = 0;
     return MOE_OK;
   }
+  c->ep_forced = world == 1;  // 1-rank communicator: exercises the EP path on one GPU
   NcclApi* api = nccl();
   if (!api) return fail(MOE_ERR_NCCL, "libnccl.so.2 not loadable");
   TRY(set_device(c));
@@ -581,7 +585,7 @@ int moe_weights_create(moe_ctx* c, const moe_shape* shape, int dtype, const int3
   w->plan = moe::plan_decode(w->dims(), c->sm_count);
   {
     const char* env = getenv("MOE_B200_RW");
-    w->rw_enabled = w->plan.ok && c->world == 1 && L >= 2 && E <= 8 &&
+    w->rw_enabled = w->plan.ok && !c->ep() && L >= 2 && E <= 8 &&
                     (size_t)E * shape->hidden_dim * 4 <= 200 * 1024 && !(env && env[0] == '0');
     if (w->rw_enabled) {
       w->rw_mem.resize(L - 1);
@@ -994,7 +998,7 @@ int moe_debug_trace_forward(moe_weights* w, float* x, int32_t* ids, float* gates
 int moe_forward_launches(moe_weights* w, int n_tok) {
   if (!w || n_tok <= 0 || w->L() == 0) return 0;
   const int L = w->L();
-  const bool ep = w->ctx->world > 1;
+  const bool ep = w->ctx->ep();
   if (use_stack(w, n_tok)) return 1;
   if (use_decode(w, n_tok, nullptr)) return 1 + L * (ep ? 3 : 2);
   // per layer: [permute, gather, up, down] or [up, down], combine, (+add for EP),
