@@ -144,7 +144,7 @@ struct moe_weights {
   DevBuf xbuf2, gbar, dev_layers, dev_slots;  // persistent stack kernel
   DevBuf pf_counts, pf_offsets, pf_perm, pf_xg, pf_h, pf_sync;  // tcgen05 prefill
   bool prefill_enabled = true;
-  int prefill_splits = 1;  // K splits of the down GEMM in the grouped kernel (0: 2-kernel path)
+  int prefill_splits = 2;  // max K splits of the down GEMM in the grouped kernel (0: 2-kernel path)
   // router projections R_{l+1} W2 for the stack kernel's z partials
   std::vector<DevBuf> rw_mem;  // [L-1]
   DevBuf dev_rw;               // device [L] pointers
@@ -304,7 +304,7 @@ int ensure_prefill_scratch(moe_weights* w, int n_tok) {
   TRY(w->pf_xg.ensure(2 * rows * w->d()));
   TRY(w->pf_h.ensure(2 * rows * w->f()));
   TRY(w->y.ensure(4 * rows * w->d() * (size_t)std::max(1, w->prefill_splits)));
-  TRY(w->pf_sync.ensure(4 * (1 + (size_t)w->E() * ((n_tok + 255) / 256))));
+  TRY(w->pf_sync.ensure(4 * (1 + (size_t)w->E() * ((n_tok + 255) / 256) + w->E())));
   return MOE_OK;
 }
 
@@ -334,6 +334,7 @@ int experts_forward(moe_weights* w, int l, const float* x, int n_tok, const int3
   }
   const float* cgates = gates;
   int nsplit = 1;
+  const int32_t* split_of = nullptr;  // per-expert K splits of the grouped prefill
   if (use_prefill(w, n_tok, post)) {
     // tcgen05 grouped GEMM: permute -> gather -> up -> down (gate in epilogue)
     TRY(ensure_prefill_scratch(w, n_tok));
@@ -352,15 +353,18 @@ int experts_forward(moe_weights* w, int l, const float* x, int n_tok, const int3
                                    s));
     cgates = nullptr;
     nsplit = std::max(1, S);
+    if (S > 0) split_of = moe::prefill_split_of(w->pf_sync.as<int>(), dm.E, n_tok);
   } else {
     CU(moe::launch_generic_up(lw, dm, x, n_tok, ids, w->h.as<float>(), post, s, pdl));
     CU(moe::launch_generic_down(lw, dm, w->h.as<float>(), n_tok, ids, w->y.as<float>(), s, pdl));
   }
   if (!ep) {
-    CU(moe::launch_combine(x, w->y.as<float>(), cgates, n_tok, dm, x_out, s, pdl, nsplit));
+    CU(moe::launch_combine(x, w->y.as<float>(), cgates, n_tok, dm, x_out, s, pdl, nsplit, ids,
+                           split_of));
   } else {
     float* delta = w->delta.as<float>();
-    CU(moe::launch_combine(nullptr, w->y.as<float>(), cgates, n_tok, dm, delta, s, pdl, nsplit));
+    CU(moe::launch_combine(nullptr, w->y.as<float>(), cgates, n_tok, dm, delta, s, pdl, nsplit, ids,
+                           split_of));
     TRY(allreduce(w, delta, (size_t)n_tok * dm.d, s));
     CU(moe::launch_add(x, delta, x_out, (long long)n_tok * dm.d, s, false));
   }

@@ -23,37 +23,22 @@ static cudaLaunchConfig_t make_cfg(dim3 grid, dim3 block, cudaStream_t s, bool p
   return cfg;
 }
 
-// ---- router: gate_topk (model.cpp:69-101), one block per token -------------
-__global__ void __launch_bounds__(256) router_topk_kernel(const float* __restrict__ router,
-                                                          const float* __restrict__ x, int d,
-                                                          int E, int k, int32_t* ids,
-                                                          float* gates) {
-  __shared__ float logits[kMaxExperts];
-  const int tid = threadIdx.x, lane = tid & 31;
-  const int warp = warp_uniform(tid >> 5);
-  griddep_wait();
-  griddep_launch_dependents();
-  const float* xt = x + (size_t)blockIdx.x * d;
-  for (int e = warp; e < E; e += 8) {
-    const float* re = router + (size_t)e * d;
-    float s = 0.f;
-    for (int c = lane; c < d; c += 32) s = fmaf(re[c], xt[c], s);
-    s = warp_sum(s);
-    if (lane == 0) logits[e] = s;
-  }
-  __syncthreads();
-  if (warp == 0) warp_topk_softmax(logits, E, k, ids + (size_t)blockIdx.x * k, gates + (size_t)blockIdx.x * k);
-}
-
-// Multi-token router: kRouterTok tokens per block, so each router row is read
-// once per block instead of once per token.  Per (token, expert) the
-// arithmetic order is exactly router_topk_kernel's (lane-strided fma, then
-// warp_sum), so batch-1 and prefill routing agree bit for bit.
+// ---- router: gate_topk (model.cpp:69-101) ----------------------------------
+// kRouterTok tokens per block; the 256 threads stride the hidden dimension
+// (column c belongs to thread c % 256), each thread holding 8 experts x
+// kRouterTok fp32 partial dot products, so a token's GEMV is spread over the
+// whole block (short dependent chains: latency, not one warp's serial loop,
+// bounds it).  Per (token, expert) the summation order is fixed — per-thread
+// chain in ascending c, warp butterfly, then the 8 warp partials in warp
+// order — and does not depend on n_tok or the token's slot in the block, so
+// every caller (batch-1 decode, prefill, any chunking) routes a token bit for
+// bit identically.
 constexpr int kRouterTok = 4;
-__global__ void __launch_bounds__(256) router_topk_multi_kernel(const float* __restrict__ router,
-                                                                const float* __restrict__ x,
-                                                                int n_tok, int d, int E, int k,
-                                                                int32_t* ids, float* gates) {
+__global__ void __launch_bounds__(256) router_topk_kernel(const float* __restrict__ router,
+                                                          const float* __restrict__ x, int n_tok,
+                                                          int d, int E, int k, int32_t* ids,
+                                                          float* gates) {
+  __shared__ float part[8][kRouterTok][8];
   __shared__ float logits[kRouterTok][kMaxExperts];
   const int tid = threadIdx.x, lane = tid & 31;
   const int warp = warp_uniform(tid >> 5);
@@ -61,25 +46,131 @@ __global__ void __launch_bounds__(256) router_topk_multi_kernel(const float* __r
   griddep_launch_dependents();
   const int t0 = blockIdx.x * kRouterTok;
   const int nt = min(kRouterTok, n_tok - t0);
-  for (int e = warp; e < E; e += 8) {
-    const float* re = router + (size_t)e * d;
-    float s[kRouterTok];
+  const float* xt = x + (size_t)t0 * d;
+  for (int e0 = 0; e0 < E; e0 += 8) {
+    const int ne = min(8, E - e0);
+    float acc[8][kRouterTok];
 #pragma unroll
-    for (int t = 0; t < kRouterTok; ++t) s[t] = 0.f;
+    for (int j = 0; j < 8; ++j)
+#pragma unroll
+      for (int t = 0; t < kRouterTok; ++t) acc[j][t] = 0.f;
 #pragma unroll 4
-    for (int c = lane; c < d; c += 32) {
-      const float r = re[c];
+    for (int c = tid; c < d; c += 256) {
+      float xv[kRouterTok];
 #pragma unroll
-      for (int t = 0; t < kRouterTok; ++t)
-        if (t < nt) s[t] = fmaf(r, x[(size_t)(t0 + t) * d + c], s[t]);
+      for (int t = 0; t < kRouterTok; ++t) xv[t] = t < nt ? __ldg(xt + (size_t)t * d + c) : 0.f;
+#pragma unroll
+      for (int j = 0; j < 8; ++j)
+        if (j < ne) {
+          const float r = __ldg(router + (size_t)(e0 + j) * d + c);
+#pragma unroll
+          for (int t = 0; t < kRouterTok; ++t) acc[j][t] = fmaf(r, xv[t], acc[j][t]);
+        }
     }
 #pragma unroll
-    for (int t = 0; t < kRouterTok; ++t) {
-      const float v = warp_sum(s[t]);
-      if (lane == 0) logits[t][e] = v;
+    for (int j = 0; j < 8; ++j)
+#pragma unroll
+      for (int t = 0; t < kRouterTok; ++t) {
+        const float v = warp_sum(acc[j][t]);
+        if (lane == 0) part[warp][t][j] = v;
+      }
+    __syncthreads();
+    if (tid < 8 * kRouterTok) {
+      const int j = tid & 7, t = tid >> 3;
+      if (j < ne && t < nt) {
+        float sum = part[0][t][j];
+#pragma unroll
+        for (int w = 1; w < 8; ++w) sum += part[w][t][j];
+        logits[t][e0 + j] = sum;
+      }
     }
+    __syncthreads();
+  }
+  for (int t = warp; t < nt; t += 8)
+    warp_topk_softmax(logits[t], E, k, ids + (size_t)(t0 + t) * k, gates + (size_t)(t0 + t) * k);
+}
+
+// Same arithmetic, for d % 256 == 0: the block's token rows and router rows
+// are staged in shared memory by bulk copies (cp.async.bulk, one DRAM round
+// trip per column chunk) instead of each thread's 16+ dependent global loads,
+// which left the per-thread loop latency-bound (~30 us at 512 tokens).
+constexpr int kRouterChunk = 2048;  // columns per chunk (multiple of 256)
+__global__ void __launch_bounds__(256, 1) router_topk_bulk_kernel(const float* __restrict__ router,
+                                                                  const float* __restrict__ x,
+                                                                  int n_tok, int d, int E, int k,
+                                                                  int32_t* ids, float* gates) {
+  extern __shared__ float4 rt_smem4[];
+  float* xs = reinterpret_cast<float*>(rt_smem4);  // [kRouterTok][kRouterChunk]
+  float* rs = xs + kRouterTok * kRouterChunk;      // [8][kRouterChunk]
+  __shared__ float part[8][kRouterTok][8];
+  __shared__ float logits[kRouterTok][kMaxExperts];
+  __shared__ __align__(8) uint64_t bar;
+  const int tid = threadIdx.x, lane = tid & 31;
+  const int warp = warp_uniform(tid >> 5);
+  if (tid == 0) {
+    mbar_init(&bar, 1);
+    fence_mbar_init();
   }
   __syncthreads();
+  griddep_wait();
+  griddep_launch_dependents();
+  const int t0 = blockIdx.x * kRouterTok;
+  const int nt = min(kRouterTok, n_tok - t0);
+  uint64_t pol_keep, pol_norm;
+  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol_keep));
+  asm volatile("createpolicy.fractional.L2::evict_normal.b64 %0, 1.0;" : "=l"(pol_norm));
+  uint32_t phase = 0;
+  for (int e0 = 0; e0 < E; e0 += 8) {
+    const int ne = min(8, E - e0);
+    float acc[8][kRouterTok];
+#pragma unroll
+    for (int j = 0; j < 8; ++j)
+#pragma unroll
+      for (int t = 0; t < kRouterTok; ++t) acc[j][t] = 0.f;
+    for (int c0 = 0; c0 < d; c0 += kRouterChunk) {
+      const int cw = min(kRouterChunk, d - c0);
+      if (tid == 0) {
+        mbar_arrive_expect_tx(&bar, (uint32_t)((nt + ne) * cw * 4));
+        for (int t = 0; t < nt; ++t)
+          bulk_g2s(xs + t * kRouterChunk, x + (size_t)(t0 + t) * d + c0, cw * 4, &bar, pol_norm);
+        for (int j = 0; j < ne; ++j)
+          bulk_g2s(rs + j * kRouterChunk, router + (size_t)(e0 + j) * d + c0, cw * 4, &bar, pol_keep);
+      }
+      mbar_wait(&bar, phase);
+      phase ^= 1;
+#pragma unroll 2
+      for (int c = tid; c < cw; c += 256) {
+        float xv[kRouterTok];
+#pragma unroll
+        for (int t = 0; t < kRouterTok; ++t) xv[t] = xs[t * kRouterChunk + c];
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          const float r = rs[j * kRouterChunk + c];
+#pragma unroll
+          for (int t = 0; t < kRouterTok; ++t) acc[j][t] = fmaf(r, xv[t], acc[j][t]);
+        }
+      }
+      __syncthreads();  // the next chunk's copies overwrite xs / rs
+    }
+#pragma unroll
+    for (int j = 0; j < 8; ++j)
+#pragma unroll
+      for (int t = 0; t < kRouterTok; ++t) {
+        const float v = warp_sum(acc[j][t]);
+        if (lane == 0) part[warp][t][j] = v;
+      }
+    __syncthreads();
+    if (tid < 8 * kRouterTok) {
+      const int j = tid & 7, t = tid >> 3;
+      if (j < ne && t < nt) {
+        float sum = part[0][t][j];
+#pragma unroll
+        for (int w = 1; w < 8; ++w) sum += part[w][t][j];
+        logits[t][e0 + j] = sum;
+      }
+    }
+    __syncthreads();
+  }
   for (int t = warp; t < nt; t += 8)
     warp_topk_softmax(logits[t], E, k, ids + (size_t)(t0 + t) * k, gates + (size_t)(t0 + t) * k);
 }
@@ -88,14 +179,19 @@ cudaError_t launch_router_topk(const float* router, const float* x, int n_tok, c
                                int32_t* ids, float* gates, cudaStream_t s, bool pdl) {
   if (n_tok <= 0) return cudaSuccess;
   cudaLaunchAttribute attr[1];
-  if (n_tok >= 4096) {  // only once one-token-per-block would exceed ~28 waves
-    cudaLaunchConfig_t cfg =
-        make_cfg(dim3((n_tok + kRouterTok - 1) / kRouterTok), dim3(256), s, pdl, attr);
-    return cudaLaunchKernelEx(&cfg, router_topk_multi_kernel, router, x, n_tok, dm.d, dm.E, dm.k,
+  const dim3 grid((n_tok + kRouterTok - 1) / kRouterTok);
+  if (dm.d % 256 == 0) {
+    const size_t smem = (size_t)(kRouterTok + 8) * kRouterChunk * sizeof(float);
+    cudaError_t e = cudaFuncSetAttribute(router_topk_bulk_kernel,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    cudaLaunchConfig_t cfg = make_cfg(grid, dim3(256), s, pdl, attr, smem);
+    return cudaLaunchKernelEx(&cfg, router_topk_bulk_kernel, router, x, n_tok, dm.d, dm.E, dm.k,
                               ids, gates);
   }
-  cudaLaunchConfig_t cfg = make_cfg(dim3(n_tok), dim3(256), s, pdl, attr);
-  return cudaLaunchKernelEx(&cfg, router_topk_kernel, router, x, dm.d, dm.E, dm.k, ids, gates);
+  cudaLaunchConfig_t cfg = make_cfg(grid, dim3(256), s, pdl, attr);
+  return cudaLaunchKernelEx(&cfg, router_topk_kernel, router, x, n_tok, dm.d, dm.E, dm.k, ids,
+                            gates);
 }
 
 // ---- generic SwiGLU up: one warp per (ffn row, token, slot) ---------------
@@ -186,7 +282,9 @@ cudaError_t launch_generic_down(const LayerWeights& lw, const Dims& dm, const fl
 // x == nullptr writes the bare combined delta (expert-parallel partials).
 __global__ void __launch_bounds__(256) combine_kernel(const float* x, const float* __restrict__ y,
                                                       const float* __restrict__ gates, int k, int d,
-                                                      float* x_out, int nsplit, long long sstride) {
+                                                      float* x_out, int nsplit, long long sstride,
+                                                      const int32_t* __restrict__ ids,
+                                                      const int32_t* __restrict__ split_of) {
   griddep_wait();
   griddep_launch_dependents();
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
@@ -196,7 +294,8 @@ __global__ void __launch_bounds__(256) combine_kernel(const float* x, const floa
   // gates == nullptr: y already carries the gate (tcgen05 prefill epilogue)
   for (int j = 0; j < k; ++j) {
     const float g = gates ? gates[(size_t)t * k + j] : 1.0f;
-    for (int sp = 0; sp < nsplit; ++sp)  // K-split partials, fixed order
+    const int ns = split_of ? split_of[ids[(size_t)t * k + j]] : nsplit;
+    for (int sp = 0; sp < ns; ++sp)  // K-split partials, fixed order
       c += g * y[sp * sstride + ((size_t)t * k + j) * d + i];
   }
   x_out[(size_t)t * d + i] = (x ? x[(size_t)t * d + i] : 0.f) + c;
@@ -205,7 +304,9 @@ __global__ void __launch_bounds__(256) combine_kernel(const float* x, const floa
 // float4 variant (d % 4 == 0): same per-element arithmetic order
 __global__ void __launch_bounds__(256) combine4_kernel(const float* x, const float* __restrict__ y,
                                                        const float* __restrict__ gates, int k, int d,
-                                                       float* x_out, int nsplit, long long sstride) {
+                                                       float* x_out, int nsplit, long long sstride,
+                                                       const int32_t* __restrict__ ids,
+                                                       const int32_t* __restrict__ split_of) {
   griddep_wait();
   griddep_launch_dependents();
   const int i4 = blockIdx.x * blockDim.x + threadIdx.x;
@@ -214,7 +315,8 @@ __global__ void __launch_bounds__(256) combine4_kernel(const float* x, const flo
   float4 c = make_float4(0.f, 0.f, 0.f, 0.f);
   for (int j = 0; j < k; ++j) {
     const float g = gates ? gates[(size_t)t * k + j] : 1.0f;
-    for (int sp = 0; sp < nsplit; ++sp) {
+    const int ns = split_of ? split_of[ids[(size_t)t * k + j]] : nsplit;
+    for (int sp = 0; sp < ns; ++sp) {
       const float4 v = __ldg(reinterpret_cast<const float4*>(y + sp * sstride + ((size_t)t * k + j) * d) + i4);
       c.x += g * v.x;
       c.y += g * v.y;
@@ -231,18 +333,20 @@ __global__ void __launch_bounds__(256) combine4_kernel(const float* x, const flo
 }
 
 cudaError_t launch_combine(const float* x, const float* y, const float* gates, int n_tok,
-                           const Dims& dm, float* x_out, cudaStream_t s, bool pdl, int nsplit) {
+                           const Dims& dm, float* x_out, cudaStream_t s, bool pdl, int nsplit,
+                           const int32_t* ids, const int32_t* split_of) {
   if (n_tok <= 0) return cudaSuccess;
   cudaLaunchAttribute attr[1];
   if (dm.d % 4 == 0) {
     cudaLaunchConfig_t cfg = make_cfg(dim3((dm.d / 4 + 255) / 256, n_tok), dim3(256), s, pdl, attr);
     const long long sstride = (long long)n_tok * dm.k * dm.d;
     return cudaLaunchKernelEx(&cfg, combine4_kernel, x, y, gates, dm.k, dm.d, x_out, nsplit,
-                              sstride);
+                              sstride, ids, split_of);
   }
   cudaLaunchConfig_t cfg = make_cfg(dim3((dm.d + 255) / 256, n_tok), dim3(256), s, pdl, attr);
   const long long sstride = (long long)n_tok * dm.k * dm.d;
-  return cudaLaunchKernelEx(&cfg, combine_kernel, x, y, gates, dm.k, dm.d, x_out, nsplit, sstride);
+  return cudaLaunchKernelEx(&cfg, combine_kernel, x, y, gates, dm.k, dm.d, x_out, nsplit, sstride,
+                            ids, split_of);
 }
 
 __global__ void add_kernel(const float* a, const float* __restrict__ b, float* out, long long n) {

@@ -80,8 +80,13 @@ cudaError_t launch_generic_down(const LayerWeights& lw, const Dims& dm, const fl
                                 bool pdl);
 // x_out[t][i] = x[t][i] + (0 + sum_j g[t][j] * y[t][j][i])   (model.cpp:128-147)
 cudaError_t launch_combine(const float* x, const float* y, const float* gates, int n_tok,
-                           const Dims& dm, float* x_out, cudaStream_t s, bool pdl,
-                           int nsplit = 1);
+                           const Dims& dm, float* x_out, cudaStream_t s, bool pdl, int nsplit = 1,
+                           const int32_t* ids = nullptr, const int32_t* split_of = nullptr);
+// The grouped prefill kernel's per-expert K-split record inside its sync
+// buffer (sync = [tile counter][E x chunks done flags][E splits]).
+inline int32_t* prefill_split_of(int* sync, int E, int n_tok) {
+  return sync + 1 + E * ((n_tok + 255) / 256);
+}
 
 // out = a + b (elementwise; expert-parallel residual after the all-reduce)
 cudaError_t launch_add(const float* a, const float* b, float* out, long long n, cudaStream_t s,

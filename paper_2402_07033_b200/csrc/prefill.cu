@@ -26,7 +26,9 @@
 #include <cudaTypedefs.h>
 
 #include <algorithm>
+#include <cstdio>
 #include <cstdlib>
+#include <vector>
 
 #include "../../include/moe_b200.h"
 #include "common.cuh"
@@ -389,7 +391,11 @@ __global__ void __launch_bounds__(PF_THREADS, 1)
 constexpr int GP_STAGES = 3;
 constexpr int GP_STAGE = 2 * PF_BM * PF_BK * 2 + PF_MAXN * PF_BK * 2;  // 64 KB
 constexpr int GP_QN = 2;
-constexpr int GP_SMEM = GP_STAGES * GP_STAGE + 1024 /*align*/ + 4096 /*barriers, queue, tables*/;
+// epilogue staging: 32 token rows x 128 columns, fp32 (down) or bf16 (up)
+constexpr int GP_STG = 32 * PF_BM * 4;  // 16 KB
+constexpr int GP_SMEM = GP_STAGES * GP_STAGE + GP_STG + 1024 /*align*/ + 4096 /*barriers, queue, tables*/ +
+                        2 * PF_MAXN * 4 /*down tile: pair index + gate per token row*/ +
+                        kMaxExperts * 4 /*splits per expert*/;
 
 struct GroupedArgs {
   const int32_t* counts;
@@ -400,17 +406,28 @@ struct GroupedArgs {
   __nv_bfloat16* h;        // [rows, f]
   float* y;                // [S][rows, d]
   int* done;               // [E][max_chunks], zero at launch
+  int* split_of;           // [E] out: K splits used for each expert's down tiles (combine reads it)
   unsigned* tile_counter;  // zero at launch
   int d, f, k, E, rows, S, max_chunks;
   int debug;  // timing experiments only: bit0 skip up epilogue, bit1 skip down epilogue
+  // diagnostics (MOE_B200_PF_TRACE): per CTA, per tile, 4 x u64:
+  // [tile | N << 32], producer got tile, MMA issued last MMA, epilogue done
+  unsigned long long* trace;
+  int trace_cap;  // tiles per CTA
 };
+
+__device__ __forceinline__ void gp_stamp(const GroupedArgs& a, int i, int field,
+                                         unsigned long long v) {
+  if (a.trace && i < a.trace_cap)
+    a.trace[((size_t)blockIdx.x * a.trace_cap + i) * 4 + field] = v;
+}
 
 struct GTile {
   int up, e, c, t1, s;  // t1: ffn tile (up) or hidden tile (down)
 };
 
 __device__ __forceinline__ GTile gp_decode(int t, int total_up, const int* upb, const int* dnb,
-                                           int E, int n_ft, int n_dt, int S) {
+                                           int E, int n_ft, int n_dt, const int* split) {
   GTile g;
   if (t < total_up) {
     int e = 0;
@@ -428,6 +445,7 @@ __device__ __forceinline__ GTile gp_decode(int t, int total_up, const int* upb, 
     const int loc = t2 - dnb[e];
     g.up = 0;
     g.e = e;
+    const int S = split[e];
     g.c = loc / (n_dt * S);
     const int rem = loc % (n_dt * S);
     g.t1 = rem / S;
@@ -445,7 +463,8 @@ __global__ void __launch_bounds__(PF_THREADS, 1)
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                              ~uintptr_t(1023));
-  uint64_t* full = reinterpret_cast<uint64_t*>(smem + GP_STAGES * GP_STAGE);
+  uint8_t* stg = smem + GP_STAGES * GP_STAGE;  // epilogue staging (GP_STG bytes)
+  uint64_t* full = reinterpret_cast<uint64_t*>(stg + GP_STG);
   uint64_t* empty = full + GP_STAGES;
   uint64_t* tmem_full = empty + GP_STAGES;  // [2]
   uint64_t* tmem_empty = tmem_full + 2;      // [2]
@@ -455,17 +474,34 @@ __global__ void __launch_bounds__(PF_THREADS, 1)
   int* q_tile = reinterpret_cast<int*>(tmem_base_s + 1);
   int* upb = q_tile + GP_QN;          // [E+1] up tiles before expert e
   int* dnb = upb + kMaxExperts + 1;   // [E+1] down tiles before expert e
+  int* s_pair = dnb + kMaxExperts + 1;                            // [PF_MAXN]
+  float* s_gate = reinterpret_cast<float*>(s_pair + PF_MAXN);     // [PF_MAXN]
+  int* s_split = reinterpret_cast<int*>(s_gate + PF_MAXN);        // [E]
   __shared__ int s_total_up, s_total;
 
   const int warp = warp_uniform(threadIdx.x >> 5), lane = threadIdx.x & 31;
-  const int n_ft = a.f / PF_BM, n_dt = a.d / PF_BM;
+  // down tiles cover 2 x 128 hidden rows (two weight tiles per stage, like
+  // up's W1/W3 pair), so both tile kinds stream 32 KB of weights per K-block
+  const int n_ft = a.f / PF_BM, n_dt = a.d / (2 * PF_BM);
   griddep_wait();
   if (threadIdx.x == 0) {
+    // K splits per expert: the down tiles are scheduled last, so the last
+    // ~3/8 of the active experts take the finest split (a.S) and the rest
+    // half of it: large tiles early, small tiles in the final wave (tail).
+    int n_act = 0;
+    for (int e = 0; e < a.E; ++e) n_act += (a.slot_of[e] >= 0 && a.counts[e] > 0);
+    const int n_late = (3 * n_act + 7) / 8;
+    const int s_hi = min(a.S, a.f / PF_BK), s_lo = max(1, s_hi / 2);
     upb[0] = dnb[0] = 0;
-    for (int e = 0; e < a.E; ++e) {
+    for (int e = 0, i = 0; e < a.E; ++e) {
+      const bool act = a.slot_of[e] >= 0 && a.counts[e] > 0;
+      const int S = act ? (i >= n_act - n_late ? s_hi : s_lo) : 1;
+      i += act;
+      s_split[e] = S;
+      if (blockIdx.x == 0) a.split_of[e] = S;
       const int ch = a.slot_of[e] >= 0 ? (a.counts[e] + PF_MAXN - 1) / PF_MAXN : 0;
       upb[e + 1] = upb[e] + ch * n_ft;
-      dnb[e + 1] = dnb[e] + ch * n_dt * a.S;
+      dnb[e + 1] = dnb[e] + ch * n_dt * S;
     }
     s_total_up = upb[a.E];
     s_total = upb[a.E] + dnb[a.E];
@@ -509,7 +545,7 @@ __global__ void __launch_bounds__(PF_THREADS, 1)
       tma_prefetch_desc(&xmap);
       tma_prefetch_desc(&hmap);
       uint32_t kc = 0;
-      int qi = 0;
+      int qi = 0, ntile = 0;
       uint32_t qph = 0;
       while (true) {
         const int t = (int)atomicAdd(a.tile_counter, 1u);
@@ -521,9 +557,12 @@ __global__ void __launch_bounds__(PF_THREADS, 1)
           qph ^= 1;
         }
         if (t >= total) break;
-        const GTile g = gp_decode(t, total_up, upb, dnb, a.E, n_ft, n_dt, a.S);
+        const GTile g = gp_decode(t, total_up, upb, dnb, a.E, n_ft, n_dt, s_split);
         int nvalid, N, nboxes, srow;
         chunk_geom(g, nvalid, N, nboxes, srow);
+        gp_stamp(a, ntile, 0, (unsigned long long)t | ((unsigned long long)N << 32));
+        gp_stamp(a, ntile, 1, globaltimer());
+        ++ntile;
         const int slot = a.slot_of[g.e];
         if (g.up) {
           const int w1row = (slot * 3 + 0) * a.f + g.t1 * PF_BM;
@@ -548,19 +587,22 @@ __global__ void __launch_bounds__(PF_THREADS, 1)
             if (v < n_ft) __nanosleep(64);
           } while (v < n_ft);
           asm volatile("fence.proxy.async.global;" ::: "memory");
-          const int d0 = g.t1 * PF_BM;
+          const int d0 = g.t1 * 2 * PF_BM;
           const int w2row = (slot * 3 + 2) * a.f;
-          const int kb0 = g.s * nkb_dn / a.S, kb1 = (g.s + 1) * nkb_dn / a.S;
-          const uint32_t bytes = kA + nboxes * kBox;
+          const int S = s_split[g.e];
+          const int kb0 = g.s * nkb_dn / S, kb1 = (g.s + 1) * nkb_dn / S;
+          const uint32_t bytes = 2 * kA + nboxes * kBox;
           for (int kb = kb0; kb < kb1; ++kb, ++kc) {
             const int st = kc % GP_STAGES;
             mbar_wait(&empty[st], ((kc / GP_STAGES) & 1) ^ 1);
             uint8_t* sp = smem + st * GP_STAGE;
             mbar_arrive_expect_tx(&full[st], bytes);
-            tma_load_2d(sp, &wmap_dn, d0, w2row + kb * PF_BK, &full[st]);
-            tma_load_2d(sp + kA / 2, &wmap_dn, d0 + 64, w2row + kb * PF_BK, &full[st]);
+            // W2T rows [kb*64, +64) x hidden cols [d0, d0+256): 4 boxes of 64 cols
+#pragma unroll
+            for (int q = 0; q < 4; ++q)
+              tma_load_2d(sp + q * (kA / 2), &wmap_dn, d0 + q * 64, w2row + kb * PF_BK, &full[st]);
             for (int b = 0; b < nboxes; ++b)
-              tma_load_2d(sp + kA + b * kBox, &hmap, kb * PF_BK, srow + b * PF_BOXN, &full[st]);
+              tma_load_2d(sp + 2 * kA + b * kBox, &hmap, kb * PF_BK, srow + b * PF_BOXN, &full[st]);
           }
         }
       }
@@ -570,7 +612,7 @@ __global__ void __launch_bounds__(PF_THREADS, 1)
     if (lane == 0) {
       uint32_t kc = 0;
       TmemSched ts;
-      int qi = 0;
+      int qi = 0, ntile = 0;
       uint32_t qph = 0;
       while (true) {
         mbar_wait(&qfull[qi], qph);
@@ -581,12 +623,12 @@ __global__ void __launch_bounds__(PF_THREADS, 1)
           qph ^= 1;
         }
         if (t >= total) break;
-        const GTile g = gp_decode(t, total_up, upb, dnb, a.E, n_ft, n_dt, a.S);
+        const GTile g = gp_decode(t, total_up, upb, dnb, a.E, n_ft, n_dt, s_split);
         int nvalid, N, nboxes, srow;
         chunk_geom(g, nvalid, N, nboxes, srow);
         int bufs[2];
         uint32_t par[2];
-        const int nb = ts.take(g.up && N > 128, bufs, par);
+        const int nb = ts.take(N > 128, bufs, par);
         for (int i = 0; i < nb; ++i) mbar_wait(&tmem_empty[bufs[i]], par[i] ^ 1);
         tc_fence_after();
         const uint32_t c1 = tmem + bufs[0] * 256;
@@ -609,26 +651,33 @@ __global__ void __launch_bounds__(PF_THREADS, 1)
           }
         } else {
           const uint32_t idesc = umma_idesc(N, true);
-          const int nk = (g.s + 1) * nkb_dn / a.S - g.s * nkb_dn / a.S;
+          const int S = s_split[g.e];
+          const int nk = (g.s + 1) * nkb_dn / S - g.s * nkb_dn / S;
           for (int kb = 0; kb < nk; ++kb, ++kc) {
             const int st = kc % GP_STAGES;
             mbar_wait(&full[st], (kc / GP_STAGES) & 1);
             tc_fence_after();
             const uint8_t* sp = smem + st * GP_STAGE;
 #pragma unroll
-            for (int kk = 0; kk < PF_BK / 16; ++kk)
-              umma_f16(c1, umma_desc(sp + kk * 2048, kA / 2, 1024),
-                       umma_desc(sp + kA + kk * 32, 16, 1024), idesc, (kb | kk) != 0);
+            for (int kk = 0; kk < PF_BK / 16; ++kk) {
+              // MN-major A: 16 K-rows = 2 groups of 8 rows (SBO = 1024 B); the
+              // two 64-wide M groups of a 128-row tile are adjacent boxes (LBO = 8 KB)
+              const uint64_t b = umma_desc(sp + 2 * kA + kk * 32, 16, 1024);
+              const uint32_t acc = (kb | kk) != 0;
+              umma_f16(c1, umma_desc(sp + kk * 2048, kA / 2, 1024), b, idesc, acc);
+              umma_f16(c3, umma_desc(sp + kA + kk * 2048, kA / 2, 1024), b, idesc, acc);
+            }
             umma_commit(&empty[st]);
           }
         }
         for (int i = 0; i < nb; ++i) umma_commit(&tmem_full[bufs[i]]);
+        gp_stamp(a, ntile++, 2, globaltimer());
       }
     }
   } else {
     // ===== epilogue (warps 0-3) =====
     TmemSched ts;
-    int qi = 0;
+    int qi = 0, ntile = 0;
     uint32_t qph = 0;
     const uint32_t lane_off = (uint32_t)(warp * 32) << 16;
     while (true) {
@@ -641,12 +690,20 @@ __global__ void __launch_bounds__(PF_THREADS, 1)
         qph ^= 1;
       }
       if (t >= total) break;
-      const GTile g = gp_decode(t, total_up, upb, dnb, a.E, n_ft, n_dt, a.S);
+      const GTile g = gp_decode(t, total_up, upb, dnb, a.E, n_ft, n_dt, s_split);
       int nvalid, N, nboxes, srow;
       chunk_geom(g, nvalid, N, nboxes, srow);
+      if (!g.up) {
+        // the rows' pair indices and gates, fetched while the MMAs still run
+        for (int j = threadIdx.x; j < nvalid; j += 128) {
+          const int p = __ldg(a.perm + srow + j);
+          s_pair[j] = p;
+          s_gate[j] = __ldg(a.gates + p);
+        }
+      }
       int bufs[2];
       uint32_t par[2];
-      const int nb = ts.take(g.up && N > 128, bufs, par);
+      const int nb = ts.take(N > 128, bufs, par);
       for (int i = 0; i < nb; ++i) mbar_wait(&tmem_full[bufs[i]], par[i]);
       tc_fence_after();
       const uint32_t c1 = tmem + lane_off + bufs[0] * 256;
@@ -654,40 +711,72 @@ __global__ void __launch_bounds__(PF_THREADS, 1)
       if (g.up && (a.debug & 1)) {
       } else if (!g.up && (a.debug & 2)) {
       } else if (g.up) {
-        const int frow = g.t1 * PF_BM + warp * 32 + lane;
-        __nv_bfloat16* hcol = a.h + (size_t)srow * a.f + frow;
+        // silu(D1)*D3 -> bf16, transposed through smem so that each token row
+        // of H (128 contiguous ffn values = 256 B) leaves as 16 B vector stores
+        const int f0 = g.t1 * PF_BM;
+        __nv_bfloat16* st16 = reinterpret_cast<__nv_bfloat16*>(stg);
         for (int c0 = 0; c0 < N; c0 += 32) {
           uint32_t r1[32], r3[32];
           tmem_ld32_nowait(c1 + c0, r1);
           tmem_ld32_nowait(c3 + c0, r3);
           tmem_ld_wait();
 #pragma unroll
-          for (int i = 0; i < 32; ++i)
-            if (c0 + i < nvalid) {
-              const float u = __uint_as_float(r1[i]);
-              const float sv = __fdividef(u, 1.0f + __expf(-u));
-              hcol[(size_t)(c0 + i) * a.f] = __float2bfloat16_rn(sv * __uint_as_float(r3[i]));
-            }
+          for (int i = 0; i < 32; ++i) {
+            const float u = __uint_as_float(r1[i]);
+            const float sv = __fdividef(u, 1.0f + __expf(-u));
+            st16[i * PF_BM + warp * 32 + lane] = __float2bfloat16_rn(sv * __uint_as_float(r3[i]));
+          }
+          named_bar_sync(3, 128);
+          const int nrow = min(32, nvalid - c0);
+#pragma unroll
+          for (int it = 0; it < 4; ++it) {
+            const int u = it * 128 + threadIdx.x;  // 32 rows x 16 x 16 B
+            const int row = u >> 4, c16 = u & 15;
+            if (row < nrow)
+              *reinterpret_cast<uint4*>(a.h + (size_t)(srow + c0 + row) * a.f + f0 + c16 * 8) =
+                  lds128(st16 + row * PF_BM + c16 * 8);
+          }
+          named_bar_sync(3, 128);
         }
       } else {
-        const int drow = g.t1 * PF_BM + warp * 32 + lane;
-        float* ys = a.y + (size_t)g.s * a.rows * a.d + drow;
-        for (int c0 = 0; c0 < N; c0 += 32) {
-          uint32_t r[32];
-          tmem_ld32_nowait(c1 + c0, r);
-          tmem_ld_wait();
+        // gate * D -> fp32 Y[pair], same transpose: 512 B per token row, for
+        // the tile's two 128-row hidden halves (D in c1 and c3)
+        float* st32 = reinterpret_cast<float*>(stg);
+        for (int half = 0; half < 2; ++half) {
+          const uint32_t cd = half ? c3 : c1;
+          float* ys = a.y + (size_t)g.s * a.rows * a.d + g.t1 * 2 * PF_BM + half * PF_BM;
+          for (int c0 = 0; c0 < N; c0 += 32) {
+            uint32_t r[32];
+            tmem_ld32_nowait(cd + c0, r);
+            tmem_ld_wait();
 #pragma unroll
-          for (int i = 0; i < 32; ++i)
-            if (c0 + i < nvalid) {
-              const int p = __ldg(a.perm + srow + c0 + i);
-              ys[(size_t)p * a.d] = __ldg(a.gates + p) * __uint_as_float(r[i]);
+            for (int i = 0; i < 32; ++i) st32[i * PF_BM + warp * 32 + lane] = __uint_as_float(r[i]);
+            named_bar_sync(3, 128);
+            const int nrow = min(32, nvalid - c0);
+#pragma unroll
+            for (int it = 0; it < 8; ++it) {
+              const int row = it * 4 + warp;  // one token row per warp per step
+              if (row < nrow) {
+                const int p = s_pair[c0 + row];
+                const float gt = s_gate[c0 + row];
+                float4 v = *reinterpret_cast<const float4*>(st32 + row * PF_BM + lane * 4);
+                v.x *= gt;
+                v.y *= gt;
+                v.z *= gt;
+                v.w *= gt;
+                *reinterpret_cast<float4*>(ys + (size_t)p * a.d + lane * 4) = v;
+              }
             }
+            named_bar_sync(3, 128);
+          }
         }
       }
       tc_fence_before();
       named_bar_sync(3, 128);
       if (threadIdx.x == 0) {
         for (int i = 0; i < nb; ++i) mbar_arrive(&tmem_empty[bufs[i]]);
+        gp_stamp(a, ntile, 3, globaltimer());
+        ++ntile;
         if (g.up) {
           __threadfence();
           asm volatile("red.release.gpu.global.add.s32 [%0], 1;" ::"l"(a.done + g.e * a.max_chunks + g.c)
@@ -748,7 +837,7 @@ static bool make_map(CUtensorMap* m, const void* base, long long rows, long long
 }
 
 bool prefill_supported(const Dims& dm) {
-  return dm.dtype == MOE_DTYPE_BF16 && dm.d % PF_BM == 0 && dm.f % PF_BM == 0 &&
+  return dm.dtype == MOE_DTYPE_BF16 && dm.d % (2 * PF_BM) == 0 && dm.f % PF_BM == 0 &&
          dm.d % PF_BK == 0 && dm.f % PF_BK == 0 && encode_fn() != nullptr;
 }
 
@@ -784,6 +873,7 @@ cudaError_t launch_prefill_experts(const LayerWeights& lw, int n_local, const Di
     g.h = h;
     g.y = y;
     g.done = sync + 1;
+    g.split_of = sync + 1 + dm.E * chunks;  // see prefill_split_of()
     g.tile_counter = reinterpret_cast<unsigned*>(sync);
     g.d = dm.d;
     g.f = dm.f;
@@ -793,13 +883,37 @@ cudaError_t launch_prefill_experts(const LayerWeights& lw, int n_local, const Di
     g.S = splits;
     g.max_chunks = chunks;
     g.debug = getenv("MOE_B200_PF_DEBUG") ? atoi(getenv("MOE_B200_PF_DEBUG")) : 0;
+    g.trace = nullptr;
+    g.trace_cap = 0;
+    const char* trace_path = getenv("MOE_B200_PF_TRACE");
+    static unsigned long long* trace_buf = nullptr;
+    if (trace_path) {
+      g.trace_cap = 32;
+      const size_t tb = (size_t)sm_count * g.trace_cap * 4 * sizeof(unsigned long long);
+      if (!trace_buf && cudaMalloc(&trace_buf, tb) != cudaSuccess) return cudaErrorMemoryAllocation;
+      if ((err = cudaMemsetAsync(trace_buf, 0, tb, s)) != cudaSuccess) return err;
+      g.trace = trace_buf;
+    }
     err = cudaMemsetAsync(sync, 0, sizeof(int) * (1 + (size_t)dm.E * chunks), s);
     if (err != cudaSuccess) return err;
     err = cudaFuncSetAttribute(prefill_grouped_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                GP_SMEM);
     if (err != cudaSuccess) return err;
     prefill_grouped_kernel<<<sm_count, PF_THREADS, GP_SMEM, s>>>(wmap_up, wmap_dn, xmap, hmap, g);
-    return cudaGetLastError();
+    if ((err = cudaGetLastError()) != cudaSuccess || !trace_path) return err;
+    // diagnostics only: synchronous dump (appends one record per launch)
+    const size_t n = (size_t)sm_count * g.trace_cap * 4;
+    std::vector<unsigned long long> h(n);
+    if ((err = cudaMemcpyAsync(h.data(), trace_buf, n * 8, cudaMemcpyDeviceToHost, s)) != cudaSuccess ||
+        (err = cudaStreamSynchronize(s)) != cudaSuccess)
+      return err;
+    if (FILE* fp = fopen(trace_path, "ab")) {
+      const int hdr[4] = {sm_count, g.trace_cap, 0, 0};
+      fwrite(hdr, sizeof(int), 4, fp);
+      fwrite(h.data(), 8, n, fp);
+      fclose(fp);
+    }
+    return cudaSuccess;
   }
   PrefillArgs a;
   a.counts = counts;

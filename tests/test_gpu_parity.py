@@ -413,8 +413,9 @@ def test_prefill_tcgen05_mixtral_layer_512(ctx, orc, monkeypatch):
 
 
 def test_router_many_tokens_batched_kernel(ctx, orc):
-    """n_tok >= 4096 takes the batched router (4 tokens per block); its ids
-    and gates must equal the one-token-per-block kernel's bit for bit."""
+    """The router's per-token arithmetic does not depend on n_tok or on the
+    token's slot in a block: one 4100-token call equals 1000-token chunks bit
+    for bit, and ids match the fp64 oracle away from near-ties."""
     s = M.Shape(1, 8, 2, 512, 1792, 4)
     w = M.Weights(ctx, s, M.DTYPE_F32)
     ow = orc.random_model(O.Shape(1, 8, 2, 512, 1792, 4), 1)
@@ -426,8 +427,8 @@ def test_router_many_tokens_batched_kernel(ctx, orc):
     w.router_topk(0, x, ids, g)
     ids1 = torch.zeros((n, 2), dtype=torch.int32, device="cuda")
     g1 = torch.zeros((n, 2), dtype=torch.float32, device="cuda")
-    for c0 in range(0, n, 1000):  # < 4096 per call -> per-token kernel
-        c1 = min(n, c0 + 1000)
+    for c0 in range(0, n, 1001):  # chunks that shift the block alignment
+        c1 = min(n, c0 + 1001)
         w.router_topk(0, x[c0:c1], ids1[c0:c1], g1[c0:c1])
     torch.cuda.synchronize()
     assert torch.equal(ids, ids1) and torch.equal(g, g1)
