@@ -72,6 +72,19 @@ int moe_ctx_sm_count(moe_ctx* ctx);
 int moe_ep_unique_id(void* uid128);
 int moe_ctx_init_ep(moe_ctx* ctx, int world, int rank, const void* uid128);
 int moe_ctx_world(moe_ctx* ctx, int* world, int* rank);
+/* Peer-memory combine (SURVEY §8e "native path"): the batch-1 per-layer
+ * exchange runs as ONE kernel that pushes this rank's reduced delta into
+ * every peer's HBM window over NVLink (P2P stores), releases per-block flags
+ * and sums all ranks' deltas in rank order (bit-identical on every rank), in
+ * place of ncclAllReduce.  Multi-process: every rank calls
+ * moe_ctx_peer_window (exports a 64-byte CUDA IPC handle), the host
+ * all-gathers the handles, then moe_ctx_open_peers.  In one process (several
+ * contexts, e.g. on one GPU for testing): moe_ctx_link_peers.  Waits are
+ * bounded; moe_ctx_peer_check reports a rank that never arrived. */
+int moe_ctx_peer_window(moe_ctx* ctx, int world, int max_hidden, void* ipc_handle64);
+int moe_ctx_open_peers(moe_ctx* ctx, int world, int rank, const void* handles64);
+int moe_ctx_link_peers(moe_ctx* const* ctxs, int world, int max_hidden);
+int moe_ctx_peer_check(moe_ctx* ctx);
 /* Testing hook: give this context an expert-parallel (world, rank) with NO
  * communicator.  Weights created on it hold only rank `rank`'s experts and
  * the per-layer exchange is skipped, so x_out = x + (this rank's partial
@@ -84,6 +97,15 @@ int moe_ctx_set_virtual_rank(moe_ctx* ctx, int world, int rank);
  * replicated (fp32). */
 int moe_weights_create(moe_ctx* ctx, const moe_shape* shape, int dtype,
                        const int32_t* owner_rank, moe_weights** out);
+/* Tensor parallelism: every rank of the context's (world,
+ * rank) holds ffn rows [rank*f/world, (rank+1)*f/world) of EVERY expert (W1 /
+ * W3 rows, W2 columns), so at batch 1 all ranks stream 1/world of each routed
+ * expert and the per-layer exchange sums their partial deltas — the split
+ * that uses every GPU's HBM bandwidth, where expert parallelism streams on at
+ * most top_k owner GPUs.  upload/download/random take and give the reference
+ * layout; download fills only this rank's slice of the full-size buffers. */
+int moe_weights_create_tp(moe_ctx* ctx, const moe_shape* shape, int dtype, moe_weights** out);
+int moe_weights_tp(const moe_weights* w, int* tp_world, int* tp_rank, int* ffn_local);
 int moe_weights_destroy(moe_weights* w);
 int64_t moe_weights_device_bytes(const moe_weights* w);
 /* Upload one expert from the reference's host layout (Matrix::data, row

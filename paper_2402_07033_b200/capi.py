@@ -89,7 +89,13 @@ def lib():
         "moe_ctx_init_ep": ([_vp, C.c_int, C.c_int, _vp], C.c_int),
         "moe_ctx_world": ([_vp, C.POINTER(C.c_int), C.POINTER(C.c_int)], C.c_int),
         "moe_ctx_set_virtual_rank": ([_vp, C.c_int, C.c_int], C.c_int),
+        "moe_ctx_peer_window": ([_vp, C.c_int, C.c_int, _vp], C.c_int),
+        "moe_ctx_open_peers": ([_vp, C.c_int, C.c_int, _vp], C.c_int),
+        "moe_ctx_link_peers": ([C.POINTER(_vp), C.c_int, C.c_int], C.c_int),
+        "moe_ctx_peer_check": ([_vp], C.c_int),
         "moe_weights_create": ([_vp, C.POINTER(_Shape), C.c_int, _vp, C.POINTER(_vp)], C.c_int),
+        "moe_weights_create_tp": ([_vp, C.POINTER(_Shape), C.c_int, C.POINTER(_vp)], C.c_int),
+        "moe_weights_tp": ([_vp, C.POINTER(C.c_int), C.POINTER(C.c_int), C.POINTER(C.c_int)], C.c_int),
         "moe_weights_destroy": ([_vp], C.c_int),
         "moe_weights_device_bytes": ([_vp], C.c_int64),
         "moe_weights_upload_expert": ([_vp, C.c_int, C.c_int, _dp, _dp, _dp], C.c_int),
@@ -184,6 +190,27 @@ class Ctx:
     def set_virtual_rank(self, world: int, rank: int):
         check(lib().moe_ctx_set_virtual_rank(self.h, world, rank))
 
+    # ---- peer-memory combine (NVLink P2P / CUDA IPC) ----
+    def peer_window(self, world: int, max_hidden: int) -> bytes:
+        """Allocate this rank's exchange window; returns its 64-byte IPC handle."""
+        buf = C.create_string_buffer(64)
+        check(lib().moe_ctx_peer_window(self.h, world, max_hidden, buf))
+        return buf.raw
+
+    def open_peers(self, world: int, rank: int, handles: list):
+        """handles: every rank's peer_window() bytes, in rank order."""
+        blob = C.create_string_buffer(b"".join(bytes(h) for h in handles), 64 * world)
+        check(lib().moe_ctx_open_peers(self.h, world, rank, blob))
+
+    @staticmethod
+    def link_peers(ctxs: list, max_hidden: int):
+        """In-process peers (several contexts, same or peer-capable GPUs)."""
+        arr = (_vp * len(ctxs))(*[c.h for c in ctxs])
+        check(lib().moe_ctx_link_peers(arr, len(ctxs), max_hidden))
+
+    def peer_check(self):
+        check(lib().moe_ctx_peer_check(self.h))
+
     @staticmethod
     def unique_id() -> bytes:
         buf = C.create_string_buffer(128)
@@ -214,18 +241,30 @@ class Ctx:
 
 
 class Weights:
-    def __init__(self, ctx: Ctx, shape: Shape, dtype: int = DTYPE_BF16, owner=None):
+    def __init__(self, ctx: Ctx, shape: Shape, dtype: int = DTYPE_BF16, owner=None, tp=False):
+        """owner: expert-parallel [L x E] shard map; tp=True: tensor-parallel
+        shard (ffn rows of every expert) over the context's (world, rank)."""
         self.ctx = ctx
         self.shape = shape
         self.dtype = dtype
         h = _vp()
-        own = None
-        if owner is not None:
-            self._owner = np.ascontiguousarray(owner, np.int32).ravel()
-            own = self._owner.ctypes.data_as(_vp)
         sh = shape.c()
-        check(lib().moe_weights_create(ctx.h, C.byref(sh), dtype, own, C.byref(h)))
+        if tp:
+            check(lib().moe_weights_create_tp(ctx.h, C.byref(sh), dtype, C.byref(h)))
+        else:
+            own = None
+            if owner is not None:
+                self._owner = np.ascontiguousarray(owner, np.int32).ravel()
+                own = self._owner.ctypes.data_as(_vp)
+            check(lib().moe_weights_create(ctx.h, C.byref(sh), dtype, own, C.byref(h)))
         self.h = h
+
+    @property
+    def tp(self):
+        """(tp_world, tp_rank, ffn rows resident on this rank)."""
+        a, b, c = C.c_int(), C.c_int(), C.c_int()
+        check(lib().moe_weights_tp(self.h, C.byref(a), C.byref(b), C.byref(c)))
+        return a.value, b.value, c.value
 
     def close(self):
         if self.h:

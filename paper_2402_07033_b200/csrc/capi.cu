@@ -93,6 +93,12 @@ struct moe_ctx {
   bool virtual_ep = false;  // sharded math without a communicator (testing hook)
   bool ep_forced = false;   // world == 1 but the EP path + NCCL exchange (MOE_B200_FORCE_EP)
   bool ep() const { return world > 1 || ep_forced; }
+  // peer-memory exchange window (NVLink P2P / CUDA IPC; kernels.h PeerArgs)
+  void* win = nullptr;
+  int win_world = 0, win_hidden = 0;
+  bool peers = false;
+  moe::PeerArgs pa{};
+  std::vector<void*> ipc_opened;
   std::mutex mu;
 };
 
@@ -106,8 +112,10 @@ struct DevBuf {
     bytes = 0;
     cudaError_t e = cudaMalloc(&p, n);
     if (e != cudaSuccess) return fail(MOE_ERR_OOM, "cudaMalloc scratch failed");
-    // legacy-stream memset: wait for it, the kernels run on non-blocking streams
-    if (cudaMemset(p, 0, n) != cudaSuccess || cudaDeviceSynchronize() != cudaSuccess)
+    // legacy-stream memset, waited for on that stream only (the kernels run on
+    // non-blocking streams; a device-wide sync would also wait for a peer-linked
+    // rank's exchange kernel that is spinning on this process's other ranks)
+    if (cudaMemset(p, 0, n) != cudaSuccess || cudaStreamSynchronize(cudaStreamLegacy) != cudaSuccess)
       return fail(MOE_ERR_CUDA, "scratch memset failed");
     bytes = n;
     return MOE_OK;
@@ -160,7 +168,12 @@ struct moe_weights {
   int E() const { return shape.experts_per_layer; }
   int k() const { return shape.top_k; }
   int d() const { return shape.hidden_dim; }
-  int f() const { return shape.ffn_dim; }
+  // tensor parallelism: this rank holds ffn rows [tp_rank*f_local, +f_local)
+  // of every expert (W1/W3 rows, W2 columns); tp == 1 otherwise
+  int tp = 1, tp_rank = 0, f_local = 0;
+  int f() const { return f_local; }      // ffn rows resident on this rank
+  int f_glob() const { return shape.ffn_dim; }
+  long long r0() const { return (long long)tp_rank * f_local; }
   Dims dims() const { return Dims{d(), f(), E(), k(), dtype}; }
   long long mat_elems() const { return (long long)f() * d(); }
   LayerWeights layer(int l) const {
@@ -324,6 +337,13 @@ int experts_forward(moe_weights* w, int l, const float* x, int n_tok, const int3
                                      w->counter.as<unsigned>(), next_ids, next_gates, s, pdl));
       return MOE_OK;
     }
+    if (w->ctx->peers && dm.d <= w->ctx->win_hidden) {
+      // fused combine over peer memory: reduce + push + rank-ordered sum + residual + router
+      CU(moe::launch_reduce_exchange(w->ypart.as<float>(), w->plan.grid, x, x_out, dm, next_router,
+                                     w->rpart.as<float>(), w->counter.as<unsigned>(), next_ids,
+                                     next_gates, w->ctx->pa, s, pdl));
+      return MOE_OK;
+    }
     float* delta = w->delta.as<float>();
     CU(moe::launch_reduce_residual(w->ypart.as<float>(), w->plan.grid, nullptr, delta, dm,
                                    nullptr, nullptr, nullptr, nullptr, nullptr, s, pdl));
@@ -469,6 +489,8 @@ int moe_ctx_destroy(moe_ctx* c) {
   if (!c) return MOE_OK;
   cudaSetDevice(c->device);
   if (c->comm && nccl() && nccl()->commDestroy) nccl()->commDestroy(c->comm);
+  for (void* p : c->ipc_opened) cudaIpcCloseMemHandle(p);
+  if (c->win) cudaFree(c->win);
   if (c->stream) cudaStreamDestroy(c->stream);
   delete c;
   return MOE_OK;
@@ -528,6 +550,123 @@ int moe_ctx_set_virtual_rank(moe_ctx* c, int world, int rank) {
   return MOE_OK;
 }
 
+static int alloc_window(moe_ctx* c, int world, int max_hidden) {
+  if (world < 1 || world > moe::kMaxRanks) return fail(MOE_ERR_ARG, "world must be 1..8");
+  if (max_hidden < 1) return fail(MOE_ERR_ARG, "max_hidden < 1");
+  if (c->win && (c->win_world != world || c->win_hidden < max_hidden))
+    return fail(MOE_ERR_ARG, "peer window already allocated with another geometry");
+  if (!c->win) {
+    TRY(set_device(c));
+    const size_t bytes = moe::peer_window_bytes(world, max_hidden);
+    CU(cudaMalloc(&c->win, bytes));
+    CU(cudaMemset(c->win, 0, bytes));
+    CU(cudaDeviceSynchronize());
+    c->win_world = world;
+    c->win_hidden = max_hidden;
+  }
+  return MOE_OK;
+}
+
+static void set_own_parts(moe_ctx* c, int world, int rank) {
+  float* inbox;
+  unsigned *flags, *seq, *err;
+  moe::peer_window_parts(c->win, world, c->win_hidden, &inbox, &flags, &seq, &err);
+  c->pa.inbox[rank] = inbox;
+  c->pa.flags[rank] = flags;
+  c->pa.seq = seq;
+  c->pa.err = err;
+  c->pa.world = world;
+  c->pa.rank = rank;
+}
+
+int moe_ctx_peer_window(moe_ctx* c, int world, int max_hidden, void* ipc_handle) {
+  if (!c) return fail(MOE_ERR_ARG, "null ctx");
+  TRY(alloc_window(c, world, max_hidden));
+  if (ipc_handle) {
+    cudaIpcMemHandle_t h;
+    CU(cudaIpcGetMemHandle(&h, c->win));
+    std::memcpy(ipc_handle, &h, sizeof(h));
+  }
+  return MOE_OK;
+}
+
+int moe_ctx_open_peers(moe_ctx* c, int world, int rank, const void* handles) {
+  if (!c || !handles) return fail(MOE_ERR_ARG, "null argument");
+  if (!c->win || c->win_world != world) return fail(MOE_ERR_ARG, "call moe_ctx_peer_window first");
+  if (rank < 0 || rank >= world) return fail(MOE_ERR_ARG, "bad rank");
+  if (c->comm && (c->world != world || c->rank != rank))
+    return fail(MOE_ERR_ARG, "world/rank differ from the NCCL communicator's");
+  TRY(set_device(c));
+  set_own_parts(c, world, rank);
+  for (int r = 0; r < world; ++r) {
+    if (r == rank) continue;
+    cudaIpcMemHandle_t h;
+    std::memcpy(&h, static_cast<const char*>(handles) + (size_t)r * sizeof(h), sizeof(h));
+    void* p = nullptr;
+    CU(cudaIpcOpenMemHandle(&p, h, cudaIpcMemLazyEnablePeerAccess));
+    c->ipc_opened.push_back(p);
+    float* inbox;
+    unsigned* flags;
+    moe::peer_window_parts(p, world, c->win_hidden, &inbox, &flags, nullptr, nullptr);
+    c->pa.inbox[r] = inbox;
+    c->pa.flags[r] = flags;
+  }
+  c->world = world;
+  c->rank = rank;
+  c->virtual_ep = false;
+  c->peers = true;
+  return MOE_OK;
+}
+
+int moe_ctx_link_peers(moe_ctx* const* ctxs, int world, int max_hidden) {
+  if (!ctxs) return fail(MOE_ERR_ARG, "null ctxs");
+  if (world < 2 || world > moe::kMaxRanks) return fail(MOE_ERR_ARG, "world must be 2..8");
+  for (int r = 0; r < world; ++r) {
+    if (!ctxs[r]) return fail(MOE_ERR_ARG, "null ctx");
+    if (ctxs[r]->comm) return fail(MOE_ERR_ARG, "context already has a communicator");
+    TRY(alloc_window(ctxs[r], world, max_hidden));
+  }
+  for (int r = 0; r < world; ++r)
+    for (int q = 0; q < world; ++q) {
+      const int dr = ctxs[r]->device, dq = ctxs[q]->device;
+      if (dr == dq) continue;
+      int ok = 0;
+      CU(cudaDeviceCanAccessPeer(&ok, dr, dq));
+      if (!ok) return fail(MOE_ERR_UNSUPPORTED, "no peer access between the contexts' devices");
+      CU(cudaSetDevice(dr));
+      const cudaError_t e = cudaDeviceEnablePeerAccess(dq, 0);
+      if (e != cudaSuccess && e != cudaErrorPeerAccessAlreadyEnabled) CU(e);
+      cudaGetLastError();
+    }
+  for (int r = 0; r < world; ++r) {
+    moe_ctx* c = ctxs[r];
+    set_own_parts(c, world, r);
+    for (int q = 0; q < world; ++q) {
+      if (q == r) continue;
+      float* inbox;
+      unsigned* flags;
+      moe::peer_window_parts(ctxs[q]->win, world, c->win_hidden, &inbox, &flags, nullptr, nullptr);
+      c->pa.inbox[q] = inbox;
+      c->pa.flags[q] = flags;
+    }
+    c->world = world;
+    c->rank = r;
+    c->virtual_ep = false;
+    c->peers = true;
+  }
+  return MOE_OK;
+}
+
+int moe_ctx_peer_check(moe_ctx* c) {
+  if (!c) return fail(MOE_ERR_ARG, "null ctx");
+  if (!c->peers) return MOE_OK;
+  TRY(set_device(c));
+  unsigned err = 0;
+  CU(cudaMemcpy(&err, c->pa.err, 4, cudaMemcpyDeviceToHost));
+  if (err) return fail(MOE_ERR_NCCL, "peer exchange timed out: a rank never published its slice");
+  return MOE_OK;
+}
+
 int moe_ctx_world(moe_ctx* c, int* world, int* rank) {
   if (!c) return fail(MOE_ERR_ARG, "null ctx");
   if (world) *world = c->world;
@@ -535,11 +674,15 @@ int moe_ctx_world(moe_ctx* c, int* world, int* rank) {
   return MOE_OK;
 }
 
-int moe_weights_create(moe_ctx* c, const moe_shape* shape, int dtype, const int32_t* owner_rank,
-                       moe_weights** out) {
+static int weights_create(moe_ctx* c, const moe_shape* shape, int dtype,
+                          const int32_t* owner_rank, bool tensor_parallel, moe_weights** out) {
   if (!c || !out) return fail(MOE_ERR_ARG, "null argument");
   *out = nullptr;
   TRY(check_shape(shape));
+  if (tensor_parallel && owner_rank)
+    return fail(MOE_ERR_ARG, "tensor parallelism shards every expert: no owner map");
+  if (tensor_parallel && shape->ffn_dim % c->world != 0)
+    return fail(MOE_ERR_SHAPE, "ffn_dim must be divisible by the tensor-parallel world");
   if (dtype != MOE_DTYPE_BF16 && dtype != MOE_DTYPE_F32) return fail(MOE_ERR_ARG, "bad dtype");
   if (shape->experts_per_layer > moe::kMaxExperts)
     return fail(MOE_ERR_UNSUPPORTED, "experts_per_layer > 256");
@@ -549,8 +692,11 @@ int moe_weights_create(moe_ctx* c, const moe_shape* shape, int dtype, const int3
   w->shape = *shape;
   w->dtype = dtype;
   w->esize = dtype == MOE_DTYPE_BF16 ? 2 : 4;
+  w->tp = tensor_parallel ? c->world : 1;
+  w->tp_rank = tensor_parallel ? c->rank : 0;
+  w->f_local = shape->ffn_dim / w->tp;
   const int L = shape->num_layers, E = shape->experts_per_layer;
-  w->owner.assign((size_t)L * E, 0);
+  w->owner.assign((size_t)L * E, tensor_parallel ? c->rank : 0);
   if (owner_rank) {
     for (int i = 0; i < L * E; ++i) {
       if (owner_rank[i] < 0 || owner_rank[i] >= c->world) {
@@ -595,7 +741,7 @@ int moe_weights_create(moe_ctx* c, const moe_shape* shape, int dtype, const int3
       w->rw_mem.resize(L - 1);
       std::vector<const float*> ptrs(L, nullptr);
       for (int l = 0; l + 1 < L; ++l) {
-        if (w->rw_mem[l].ensure(sizeof(float) * (size_t)std::max(1, w->n_local[l]) * shape->ffn_dim * E))
+        if (w->rw_mem[l].ensure(sizeof(float) * (size_t)std::max(1, w->n_local[l]) * w->f() * E))
           return cleanup(fail(MOE_ERR_OOM, "cudaMalloc router projections"));
         ptrs[l] = w->rw_mem[l].as<float>();
         w->device_bytes += (int64_t)w->rw_mem[l].bytes;
@@ -621,6 +767,23 @@ int moe_weights_create(moe_ctx* c, const moe_shape* shape, int dtype, const int3
       return cleanup(fail(MOE_ERR_CUDA, "upload stack tables"));
   }
   *out = w;
+  return MOE_OK;
+}
+
+int moe_weights_create(moe_ctx* c, const moe_shape* shape, int dtype, const int32_t* owner_rank,
+                       moe_weights** out) {
+  return weights_create(c, shape, dtype, owner_rank, false, out);
+}
+
+int moe_weights_create_tp(moe_ctx* c, const moe_shape* shape, int dtype, moe_weights** out) {
+  return weights_create(c, shape, dtype, nullptr, true, out);
+}
+
+int moe_weights_tp(const moe_weights* w, int* tp_world, int* tp_rank, int* ffn_local) {
+  if (!w) return fail(MOE_ERR_ARG, "null weights");
+  if (tp_world) *tp_world = w->tp;
+  if (tp_rank) *tp_rank = w->tp_rank;
+  if (ffn_local) *ffn_local = w->f_local;
   return MOE_OK;
 }
 
@@ -666,7 +829,13 @@ int moe_weights_upload_expert(moe_weights* w, int layer, int expert, const doubl
   cudaStream_t s = w->ctx->stream;
   const double* src[3] = {w_in, w_gate, w_out};
   for (int m = 0; m < 3; ++m) {
-    CU(cudaMemcpyAsync(w->stage_d.p, src[m], (size_t)n * 8, cudaMemcpyHostToDevice, s));
+    if (m < 2)  // this rank's rows [r0, r0 + f_local) of the [f x d] matrix
+      CU(cudaMemcpyAsync(w->stage_d.p, src[m] + w->r0() * w->d(), (size_t)n * 8,
+                         cudaMemcpyHostToDevice, s));
+    else  // columns [r0, r0 + f_local) of w_out [d x f]
+      CU(cudaMemcpy2DAsync(w->stage_d.p, (size_t)w->f() * 8, src[m] + w->r0(),
+                           (size_t)w->f_glob() * 8, (size_t)w->f() * 8, (size_t)w->d(),
+                           cudaMemcpyHostToDevice, s));
     if (m < 2)
       CU(moe::launch_convert(w->stage_d.as<double>(), w->expert_ptr(layer, expert, m), w->dtype,
                              w->f(), w->d(), false, s));
@@ -707,10 +876,10 @@ int moe_weights_random(moe_weights* w, uint64_t seed) {
         const uint64_t tag = ((uint64_t)l << 40) | ((uint64_t)e << 8) | (uint64_t)m;
         if (m < 2)
           CU(moe::launch_random(w->expert_ptr(l, e, m), w->dtype, w->f(), w->d(), false, seed,
-                                tag, scale, s));
-        else
+                                tag, scale, s, w->d(), w->r0() * w->d()));
+        else  // w_out [d x f]: this rank's columns, stored transposed
           CU(moe::launch_random(w->expert_ptr(l, e, m), w->dtype, w->d(), w->f(), true, seed,
-                                tag, scale, s));
+                                tag, scale, s, w->f_glob(), w->r0()));
       }
     }
     const uint64_t rtag = ((uint64_t)l << 40) | (0xFFFFull << 8) | 3ull;
@@ -740,7 +909,13 @@ int moe_weights_download_expert(moe_weights* w, int layer, int expert, double* w
     else
       CU(moe::launch_to_double(w->expert_ptr(layer, expert, m), w->dtype, w->stage_d.as<double>(),
                                w->d(), w->f(), true, s));
-    CU(cudaMemcpyAsync(dst[m], w->stage_d.p, (size_t)n * 8, cudaMemcpyDeviceToHost, s));
+    if (m < 2)  // tensor parallel: only this rank's slice of the full-size buffer
+      CU(cudaMemcpyAsync(dst[m] + w->r0() * w->d(), w->stage_d.p, (size_t)n * 8,
+                         cudaMemcpyDeviceToHost, s));
+    else
+      CU(cudaMemcpy2DAsync(dst[m] + w->r0(), (size_t)w->f_glob() * 8, w->stage_d.p,
+                           (size_t)w->f() * 8, (size_t)w->f() * 8, (size_t)w->d(),
+                           cudaMemcpyDeviceToHost, s));
     CU(cudaStreamSynchronize(s));
   }
   return MOE_OK;
@@ -786,6 +961,8 @@ int moe_permute(moe_ctx* c, const int32_t* ids, int n_tok, int top_k, int n_expe
 int moe_experts_forward(moe_weights* w, int layer, const float* x, int n_tok, const int32_t* ids,
                         const float* gates, float* x_out, float* post_silu, void* stream) {
   TRY(check_le(w, layer, 0));
+  if (post_silu && w->tp > 1)
+    return fail(MOE_ERR_UNSUPPORTED, "post-SiLU capture of a tensor-parallel shard");
   if (n_tok < 0) return fail(MOE_ERR_ARG, "n_tok < 0");
   if (n_tok == 0) return MOE_OK;
   if (!x || !ids || !gates || !x_out) return fail(MOE_ERR_ARG, "null pointer");
@@ -855,6 +1032,8 @@ int moe_forward_host(moe_weights* w, const double* tokens, int n_tok, double* ou
   TRY(ensure_scratch(w, n_tok));
   cudaStream_t s = w->ctx->stream;
   const size_t nx = (size_t)n_tok * d, nr = (size_t)L * n_tok * k;
+  if (post_silu && w->tp > 1)
+    return fail(MOE_ERR_UNSUPPORTED, "post-SiLU capture of a tensor-parallel shard");
   const size_t npost = post_silu ? (size_t)L * n_tok * k * f : 0;
   void* pin = nullptr;
   TRY(host_pinned(w, nx * 4 + nr * 8 + npost * 4, &pin));
@@ -1004,7 +1183,8 @@ int moe_forward_launches(moe_weights* w, int n_tok) {
   const int L = w->L();
   const bool ep = w->ctx->ep();
   if (use_stack(w, n_tok)) return 1;
-  if (use_decode(w, n_tok, nullptr)) return 1 + L * (ep ? 3 : 2);
+  if (use_decode(w, n_tok, nullptr))  // experts + reduce (+ NCCL all-reduce + residual)
+    return 1 + L * (ep && !(w->ctx->peers && w->d() <= w->ctx->win_hidden) ? 3 : 2);
   // per layer: [permute, gather, up, down] or [up, down], combine, (+add for EP),
   // and the next layer's router
   const int experts =

@@ -369,6 +369,99 @@ __global__ void __launch_bounds__(256) reduce_residual_kernel(
   if (tid == 0) *counter = 0u;
 }
 
+// Expert-parallel variant: the reduced 32-column slice of this rank's delta
+// is pushed to every rank's inbox, and the residual adds the rank-ordered sum
+// of all ranks' slices (see launch_reduce_exchange in kernels.h).
+__device__ __forceinline__ void st_release_sys(unsigned* p, unsigned v) {
+  asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ unsigned ld_acquire_sys(const unsigned* p) {
+  unsigned v;
+  asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+
+__global__ void __launch_bounds__(256) reduce_exchange_kernel(
+    const float* __restrict__ ypart, int nparts, const float* x, float* x_out, int d,
+    const float* __restrict__ next_router, int E, int k, float* rpart, unsigned* counter,
+    int32_t* next_ids, float* next_gates, PeerArgs pa) {
+  __shared__ float red[8][33];
+  __shared__ float xs[32];
+  __shared__ float logits[kMaxExperts];
+  __shared__ int s_last;
+  const int tid = threadIdx.x, lane = tid & 31;
+  const int warp = warp_uniform(tid >> 5);
+  const int b = blockIdx.x, nblk = gridDim.x;
+  griddep_wait();
+  const int i = b * 32 + lane;
+  float s = 0.f;
+  if (i < d)
+    for (int p = warp; p < nparts; p += 8) s += ypart[(size_t)p * d + i];
+  red[warp][lane] = s;
+  __syncthreads();
+  if (warp == 0) {
+    float tot = 0.f;
+#pragma unroll
+    for (int w = 0; w < 8; ++w) tot += red[w][lane];
+    const unsigned seq = __shfl_sync(MOE_FULL_MASK, lane == 0 ? pa.seq[b] + 1u : 0u, 0);
+    const size_t par = seq & 1u;
+    // push this rank's slice to every rank (P2P stores), then release flags
+    if (i < d)
+      for (int r = 0; r < pa.world; ++r) pa.inbox[r][(par * pa.world + pa.rank) * d + i] = tot;
+    __threadfence_system();
+    __syncwarp();
+    if (lane < pa.world) st_release_sys(pa.flags[lane] + (size_t)pa.rank * nblk + b, seq);
+    // wait for every rank's slice of this block (bounded: a missing peer is
+    // reported through pa.err instead of hanging the GPU)
+    if (lane < pa.world) {
+      const unsigned* f = pa.flags[pa.rank] + (size_t)lane * nblk + b;
+      unsigned spins = 0;
+      while ((int)(ld_acquire_sys(f) - seq) < 0) {
+        if (++spins > (1u << 22)) {
+          atomicExch(pa.err, 1u);
+          break;
+        }
+        if (spins > 64) __nanosleep(128);
+      }
+    }
+    __syncwarp();
+    float all = 0.f;
+    if (i < d) {
+      const float* in = pa.inbox[pa.rank] + par * pa.world * d + i;
+      for (int r = 0; r < pa.world; ++r) all += __ldcv(in + (size_t)r * d);  // rank order
+    }
+    float xo = 0.f;
+    if (i < d) {
+      xo = (x ? x[i] : 0.f) + all;
+      x_out[i] = xo;
+    }
+    xs[lane] = xo;
+    if (lane == 0) pa.seq[b] = seq;
+  }
+  __syncthreads();
+  griddep_launch_dependents();  // only after the peers arrived (see launch_reduce_exchange)
+  if (next_router == nullptr) return;
+  for (int e = warp; e < E; e += 8) {
+    const float v = (i < d) ? next_router[(size_t)e * d + i] * xs[lane] : 0.f;
+    const float t = warp_sum(v);
+    if (lane == 0) rpart[(size_t)blockIdx.x * E + e] = t;
+  }
+  __threadfence();
+  __syncthreads();
+  if (tid == 0) s_last = (atomicAdd(counter, 1u) == gridDim.x - 1);
+  __syncthreads();
+  if (!s_last) return;
+  __threadfence();
+  for (int e = tid; e < E; e += blockDim.x) {
+    float l = 0.f;
+    for (int bb = 0; bb < (int)gridDim.x; ++bb) l += __ldcg(&rpart[(size_t)bb * E + e]);
+    logits[e] = l;
+  }
+  __syncthreads();
+  if (warp == 0) warp_topk_softmax(logits, E, k, next_ids, next_gates);
+  if (tid == 0) *counter = 0u;
+}
+
 // ---------------------------------------------------------------------------
 // persistent whole-stack kernel
 struct StackArgs {
@@ -840,6 +933,41 @@ cudaError_t launch_reduce_residual(const float* ypart, int nparts, const float* 
   cfg.numAttrs = pdl ? 1 : 0;
   return cudaLaunchKernelEx(&cfg, reduce_residual_kernel, ypart, nparts, x, x_out, dm.d,
                             next_router, dm.E, dm.k, rpart, counter, next_ids, next_gates);
+}
+
+size_t peer_window_bytes(int world, int max_hidden) {
+  const size_t nblk = (size_t)(max_hidden + 31) / 32;
+  return 2 * (size_t)world * max_hidden * 4 + (size_t)world * nblk * 4 + nblk * 4 + 64;
+}
+
+void peer_window_parts(void* base, int world, int max_hidden, float** inbox, unsigned** flags,
+                       unsigned** seq, unsigned** err) {
+  const size_t nblk = (size_t)(max_hidden + 31) / 32;
+  char* p = static_cast<char*>(base);
+  *inbox = reinterpret_cast<float*>(p);
+  p += 2 * (size_t)world * max_hidden * 4;
+  *flags = reinterpret_cast<unsigned*>(p);
+  p += (size_t)world * nblk * 4;
+  if (seq) *seq = reinterpret_cast<unsigned*>(p);
+  p += nblk * 4;
+  if (err) *err = reinterpret_cast<unsigned*>(p);
+}
+
+cudaError_t launch_reduce_exchange(const float* ypart, int nparts, const float* x, float* x_out,
+                                   const Dims& dm, const float* next_router, float* rpart,
+                                   unsigned* counter, int32_t* next_ids, float* next_gates,
+                                   const PeerArgs& pa, cudaStream_t s, bool pdl) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(reduce_blocks(dm));
+  cfg.blockDim = dim3(256);
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = pdl ? 1 : 0;
+  return cudaLaunchKernelEx(&cfg, reduce_exchange_kernel, ypart, nparts, x, x_out, dm.d,
+                            next_router, dm.E, dm.k, rpart, counter, next_ids, next_gates, pa);
 }
 
 }  // namespace moe

@@ -69,6 +69,33 @@ cudaError_t launch_reduce_residual(const float* ypart, int nparts, const float* 
                                    cudaStream_t s, bool pdl);
 int reduce_blocks(const Dims& dm);
 
+// ---- expert-parallel combine over peer memory (NVLink P2P / IPC) -----------
+// Every rank owns one "exchange window" in its HBM:
+//   inbox [2 parity][world][d] fp32 | flags [world][nblk] u32 | seq [nblk] u32 | err u32
+// and holds device pointers to every peer's window (its own included).
+constexpr int kMaxRanks = 8;
+struct PeerArgs {
+  float* inbox[kMaxRanks];     // rank r's inbox base
+  unsigned* flags[kMaxRanks];  // rank r's flags base
+  unsigned* seq;               // own per-block exchange counters
+  unsigned* err;               // own: set when a peer never arrives (bounded wait)
+  int world, rank;
+};
+size_t peer_window_bytes(int world, int max_hidden);
+// Carve a window allocation into its parts (same layout on every rank).
+void peer_window_parts(void* base, int world, int max_hidden, float** inbox, unsigned** flags,
+                       unsigned** seq, unsigned** err);
+// x_out = x + sum_{r in rank order} delta_r, where delta_r = this layer's
+// fixed-order sum of rank r's per-CTA partials.  Each block reduces 32 hidden
+// columns, stores them into every peer's inbox (P2P stores), releases a
+// per-(rank, block) flag, waits for all ranks' flags and sums the inbox in
+// rank order — so every rank computes bit-identical x_out (consistent
+// routing) with no NCCL call.  Fused with the next layer's router + top-k.
+cudaError_t launch_reduce_exchange(const float* ypart, int nparts, const float* x, float* x_out,
+                                   const Dims& dm, const float* next_router, float* rpart,
+                                   unsigned* counter, int32_t* next_ids, float* next_gates,
+                                   const PeerArgs& pa, cudaStream_t s, bool pdl);
+
 // ---- generic (any shape, any token count) ---------------------------------
 // h[t][j][r] = silu(W1 x_t) * (W3 x_t) for expert ids[t][j]; post_silu optional.
 cudaError_t launch_generic_up(const LayerWeights& lw, const Dims& dm, const float* x, int n_tok,
@@ -118,7 +145,11 @@ cudaError_t launch_to_double(const void* src, int dtype, double* dst, long long 
 cudaError_t launch_convert_f32(const double* src, float* dst, long long n, cudaStream_t s);
 // Counter-based normal init of one logical matrix (reference layout rows x
 // cols), stored transposed when `transpose`.  tag identifies (layer, expert, m).
+// Element (r, c) takes variate #(r * ld + c + off) of the stream, so a
+// [rows x cols] slice of a larger matrix (ld = its row length, off = the
+// slice origin) holds exactly the values of the full matrix (ld <= 0: cols).
 cudaError_t launch_random(void* dst, int dtype, long long rows, long long cols, bool transpose,
-                          uint64_t seed, uint64_t tag, float scale, cudaStream_t s);
+                          uint64_t seed, uint64_t tag, float scale, cudaStream_t s,
+                          long long ld = 0, long long off = 0);
 
 }  // namespace moe

@@ -198,31 +198,42 @@ __device__ __forceinline__ float normal_at(uint64_t seed, uint64_t tag, unsigned
 
 template <typename W>
 __global__ void random_kernel(W* __restrict__ dst, long long rows, long long cols, bool transpose,
-                              uint64_t seed, uint64_t tag, float scale) {
+                              uint64_t seed, uint64_t tag, float scale, long long ld,
+                              long long off) {
   const long long n = rows * cols;
   for (long long o = blockIdx.x * (long long)blockDim.x + threadIdx.x; o < n;
        o += (long long)gridDim.x * blockDim.x) {
     // o indexes the STORED layout; recover the logical (reference) index.
-    long long logical = o;
+    // (r, c) is the element of this [rows x cols] block, which sits at column
+    // offset / row stride (off, ld) inside the full reference matrix (a
+    // tensor-parallel rank holds a slice of every expert).
+    long long r, c;
     if (transpose) {
-      const long long c = o / rows, r = o - c * rows;  // stored [cols x rows]
-      logical = r * cols + c;
+      c = o / rows;  // stored [cols x rows]
+      r = o - c * rows;
+    } else {
+      r = o / cols;
+      c = o - r * cols;
     }
+    const long long logical = r * ld + c + off;
     dst[o] = Elem<W>::from_float(normal_at(seed, tag, (unsigned long long)logical) * scale);
   }
 }
 
 cudaError_t launch_random(void* dst, int dtype, long long rows, long long cols, bool transpose,
-                          uint64_t seed, uint64_t tag, float scale, cudaStream_t s) {
+                          uint64_t seed, uint64_t tag, float scale, cudaStream_t s, long long ld,
+                          long long off) {
+  if (ld <= 0) ld = cols;
   const long long n = rows * cols;
   if (n <= 0) return cudaSuccess;
   const int blocks = (int)std::min<long long>((n + 255) / 256, 148 * 16);
   if (dtype == MOE_DTYPE_BF16)
     random_kernel<__nv_bfloat16><<<blocks, 256, 0, s>>>(static_cast<__nv_bfloat16*>(dst), rows,
-                                                         cols, transpose, seed, tag, scale);
+                                                         cols, transpose, seed, tag, scale, ld,
+                                                         off);
   else
     random_kernel<float><<<blocks, 256, 0, s>>>(static_cast<float*>(dst), rows, cols, transpose,
-                                                seed, tag, scale);
+                                                seed, tag, scale, ld, off);
   return cudaGetLastError();
 }
 
