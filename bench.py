@@ -178,12 +178,18 @@ def run_ours(args):
 
         obj = [M.Ctx.unique_id() if rank == 0 else None]
         dist.broadcast_object_list(obj, src=0)
-        ctx.init_ep(world, rank, obj[0])
+        ctx.init_ep(world, rank, obj[0])  # NCCL: multi-token exchange (and fallback)
+        if not args.nccl_combine:
+            # fused batch-1 combine over NVLink peer memory: all-gather the
+            # ranks' exchange-window IPC handles, map every peer's window
+            handles = [None] * world
+            dist.all_gather_object(handles, ctx.peer_window(world, d))
+            ctx.open_peers(world, rank, handles)
     elif os.environ.get("MOE_B200_FORCE_EP") == "1":
         ctx.init_ep(1, 0, M.Ctx.unique_id())  # 1-rank NCCL: the EP code path on one GPU
-    owner = shard_map(L, E, world) if world > 1 else None
     shape = M.Shape(L, E, k, d, f, esz)
-    w = M.Weights(ctx, shape, dtype, owner=owner)
+    owner = shard_map(L, E, world) if world > 1 and args.shard == "ep" else None
+    w = M.Weights(ctx, shape, dtype, owner=owner, tp=(world > 1 and args.shard == "tp"))
     w.random(args.seed)
     stream_ptr = ctx.stream
     stream = torch.cuda.ExternalStream(stream_ptr, device=f"cuda:{local}")
@@ -252,7 +258,7 @@ def run_ours(args):
         torch.cuda.synchronize()
         kern_ms = e0.elapsed_time(e1) / n_rep
         n_loc = len(set(lay_ids[0]))
-        alg = n_loc * 3 * d * f * esz
+        alg = n_loc * 3 * d * w.tp[2] * esz  # ffn rows resident on this rank (tp: f / N)
         ach = alg / (kern_ms * 1e-3) / 1e9
         expert_kernel = {"kernel": "decode_experts_kernel", "achieved": round(ach, 1),
                          "frac": round(ach / peak, 4), "kernel_us": round(kern_ms * 1e3, 2),
@@ -315,7 +321,9 @@ def run_ours(args):
             "dtype": "bf16" if dt == "bf16" else "f32", "data": "synthetic (random-init weights, N(0,1) tokens)",
             "config": {"workload": WORKLOAD_NAME[args.config], "layers": L, "experts": E, "top_k": k,
                        "hidden": d, "ffn": f, "batch": 1,
-                       "parallelism": f"ep{world}" if world > 1 else "single-gpu",
+                       "parallelism": f"{args.shard}{world}" if world > 1 else "single-gpu",
+                       "combine": None if world == 1 else
+                       ("ncclAllReduce" if args.nccl_combine else "fused peer-memory exchange (NVLink P2P)"),
                        "path": "persistent stack kernel (1 launch/token)" if w.forward_launches(1) == 1
                        else f"per-layer kernels ({w.forward_launches(1)} launches/token, CUDA graph + PDL)",
                        "l2": f"inputs larger than L2: {L * k * 3 * d * f * esz / 1e9:.1f} GB of expert weights streamed per step"},
@@ -491,6 +499,11 @@ def main():
     ap.add_argument("--cpu-tokens", type=int, default=12)
     ap.add_argument("--ref-threads", type=int, default=0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--shard", default="ep", choices=["ep", "tp"],
+                    help="N>1: expert parallelism (popularity shard map) or tensor parallelism "
+                         "(ffn rows of every expert split over the GPUs)")
+    ap.add_argument("--nccl-combine", action="store_true",
+                    help="N>1: ncclAllReduce instead of the fused peer-memory combine")
     ap.add_argument("--no-stack", action="store_true",
                     help="per-layer 2-kernel graph instead of the persistent stack kernel")
     ap.add_argument("--traffic", type=float, default=None,

@@ -140,6 +140,25 @@ int moe_router_topk(moe_weights* w, int layer, const float* x, int n_tok, int32_
 int moe_permute(moe_ctx* ctx, const int32_t* ids, int n_tok, int top_k, int n_experts,
                 int32_t* counts, int32_t* offsets, int32_t* perm, int32_t* inv_perm,
                 void* stream);
+/* Device routing histogram (profile_from_trace, placement.cpp:30-43):
+ * counts[l][e] (int64, device, [n_layers x n_experts]) += the number of
+ * (token, slot) pairs of layer l routed to expert e, from an ids record
+ * [n_layers x n_tok x top_k] (moe_forward's).  Accumulates across calls, so
+ * a serving loop profiles popularity on the device and reads it back only to
+ * recompute the placement / expert-parallel shard map. */
+int moe_routing_histogram(moe_ctx* ctx, const int32_t* ids, int n_layers, int n_tok, int top_k,
+                          int n_experts, int64_t* counts, void* stream);
+/* One RoutingTrace step (model.cpp:120-158, trace.hpp:18-47) from a device
+ * routing record ids/gates [n_layers x n_tok x top_k] (on the context's
+ * stream; synchronous): host token_count / gate_weight [n_layers x n_experts]
+ * = per (layer, expert) the number of routed (token, slot) pairs and their
+ * mean gate (fp64 sum in token order / count; 0 where count is 0).  The
+ * Selection rows of the step are the entries with count > 0, ascending
+ * expert; the step is a decode step iff n_tok == 1 (model.cpp:116).  See
+ * paper_2402_07033_b200.trace for the JSONL emitter (trace.cpp:90-108). */
+int moe_routing_trace_step(moe_ctx* ctx, const int32_t* ids, const float* gates, int n_layers,
+                           int n_tok, int top_k, int n_experts, int32_t* token_count,
+                           double* gate_weight);
 /* The expert half of one model_forward layer (model.cpp:128-147): SwiGLU
  * experts of the routed tokens, gate-weighted combine, residual add:
  * x_out = x + sum_j gates[j] * expert_ffn(ids[j], x).  post_silu (optional,

@@ -27,6 +27,10 @@ void invalidate_weights_cache();
 // least-loaded rank with spare slots (LPT; ties to the lower rank), each rank
 // holding ceil(E / world) experts at most.
 std::vector<std::vector<int>> ep_shard_map(const PopularityProfile& profile, int world);
+// profile_from_trace (placement.cpp:30-43) from per-(layer, expert) selection
+// counts, e.g. a device routing histogram (moe_routing_histogram) read back
+// after a calibration run; ValidationError on ragged rows or negative counts.
+PopularityProfile profile_from_counts(const std::vector<std::vector<std::int64_t>>& counts);
 // Rank r's share as a Placement (capacity = its expert count).
 Placement rank_placement(const std::vector<std::vector<int>>& owner, int rank);
 

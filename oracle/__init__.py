@@ -258,6 +258,7 @@ class Reference(_Base):
         L.ref_model_forward_timed.argtypes = [C.c_void_p, C.c_int, _dp, _dp, _dp]
         L.ref_shape_validate.argtypes = [C.c_void_p]
         L.ref_shape_preset.argtypes = [C.c_char_p, _i32p]
+        L.ref_load_trace_jsonl.argtypes = [C.c_char_p, C.c_void_p, _i32p]
 
     def _check(self, rc):
         if rc == 1:
@@ -266,6 +267,12 @@ class Reference(_Base):
             raise ValueError("ValidationError: " + self.lib.ref_last_error().decode())
         if rc:
             raise RuntimeError(self.lib.ref_last_error().decode())
+
+    def load_trace_jsonl(self, path: str, shape: Shape) -> int:
+        """The reference's loader + validator (trace.cpp:110-141); returns the step count."""
+        n = C.c_int()
+        self._check(self.lib.ref_load_trace_jsonl(path.encode(), shape.arr(), C.byref(n)))
+        return n.value
 
     def random_model(self, shape: Shape, seed: int, experts=None) -> Weights:
         w = Weights(shape, experts)

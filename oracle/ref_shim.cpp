@@ -18,6 +18,7 @@
 #include "moe_orch/placement.hpp"
 #include "moe_orch/shape.hpp"
 #include "moe_orch/trace.hpp"
+#include "moe_orch/trace.hpp"
 
 using namespace moe_orch;
 
@@ -350,6 +351,18 @@ int ref_sparsity_histogram(const double* acts, int64_t n, const double* thr, int
     const auto f = sparsity_histogram(std::vector<double>(acts, acts + n),
                                       std::vector<double>(thr, thr + nthr));
     std::memcpy(out, f.data(), f.size() * 8);
+    return 0;
+  } catch (...) {
+    return map_exc();
+  }
+}
+
+// load_trace_jsonl (trace.cpp:110-141): parses AND validates a JSONL trace
+// against the shape; returns the number of steps in *n_steps.
+int ref_load_trace_jsonl(const char* path, const int32_t* shape, int* n_steps) {
+  try {
+    const RoutingTrace t = load_trace_jsonl(std::string(path), to_shape(shape));
+    *n_steps = (int)t.steps.size();
     return 0;
   } catch (...) {
     return map_exc();

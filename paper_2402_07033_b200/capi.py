@@ -104,6 +104,8 @@ def lib():
         "moe_weights_download_expert": ([_vp, C.c_int, C.c_int, _dp, _dp, _dp], C.c_int),
         "moe_weights_download_router": ([_vp, C.c_int, _dp], C.c_int),
         "moe_router_topk": ([_vp, C.c_int, _vp, C.c_int, _vp, _vp, _vp], C.c_int),
+        "moe_routing_histogram": ([_vp, _vp, C.c_int, C.c_int, C.c_int, C.c_int, _vp, _vp], C.c_int),
+        "moe_routing_trace_step": ([_vp, _vp, _vp, C.c_int, C.c_int, C.c_int, C.c_int, _i32p, _dp], C.c_int),
         "moe_permute": ([_vp, _vp, C.c_int, C.c_int, C.c_int, _vp, _vp, _vp, _vp, _vp], C.c_int),
         "moe_experts_forward": ([_vp, C.c_int, _vp, C.c_int, _vp, _vp, _vp, _vp, _vp], C.c_int),
         "moe_decode_experts_partial": ([_vp, C.c_int, _vp, _vp, _vp, _vp, _vp], C.c_int),
@@ -221,6 +223,21 @@ class Ctx:
                 stream=None):
         check(lib().moe_permute(self.h, _ptr(ids), n_tok, top_k, n_experts, _ptr(counts),
                                 _ptr(offsets), _ptr(perm), _ptr(inv_perm), _stream(stream, ids)))
+
+    def routing_histogram(self, ids, counts, stream=None):
+        """counts[l][e] += selections in ids [L x n_tok x k] (int64 device tensor [L x E])."""
+        L, n, k = ids.shape
+        check(lib().moe_routing_histogram(self.h, _ptr(ids), L, n, k, counts.shape[1], _ptr(counts),
+                                          _stream(stream, ids)))
+
+    def routing_trace_step(self, ids, gates, n_experts):
+        """(token_count [L x E] int32, gate_weight [L x E] fp64) of one step."""
+        L, n, k = ids.shape
+        cnt = np.zeros((L, n_experts), np.int32)
+        gw = np.zeros((L, n_experts), np.float64)
+        check(lib().moe_routing_trace_step(self.h, _ptr(ids), _ptr(gates), L, n, k, n_experts,
+                                           cnt.ctypes.data_as(_i32p), _dptr(gw)))
+        return cnt, gw
 
     def expert_ffn_host(self, dtype, w_in, w_gate, w_out, x):
         f, d = w_in.shape

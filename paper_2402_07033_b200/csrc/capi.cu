@@ -958,6 +958,44 @@ int moe_permute(moe_ctx* c, const int32_t* ids, int n_tok, int top_k, int n_expe
   return MOE_OK;
 }
 
+int moe_routing_histogram(moe_ctx* c, const int32_t* ids, int n_layers, int n_tok, int top_k,
+                          int n_experts, int64_t* counts, void* stream) {
+  if (!c || !counts || (n_layers > 0 && n_tok > 0 && !ids)) return fail(MOE_ERR_ARG, "null pointer");
+  if (n_layers < 0 || n_tok < 0 || top_k < 1 || n_experts < 1 || n_experts > moe::kMaxExperts)
+    return fail(MOE_ERR_SHAPE, "bad histogram geometry");
+  TRY(set_device(c));
+  CU(moe::launch_routing_histogram(ids, n_layers, n_tok, top_k, n_experts, counts,
+                                   pick(c, stream)));
+  return MOE_OK;
+}
+
+int moe_routing_trace_step(moe_ctx* c, const int32_t* ids, const float* gates, int n_layers,
+                           int n_tok, int top_k, int n_experts, int32_t* token_count,
+                           double* gate_weight) {
+  if (!c || !token_count || !gate_weight || (n_layers > 0 && n_tok > 0 && (!ids || !gates)))
+    return fail(MOE_ERR_ARG, "null pointer");
+  if (n_layers < 0 || n_tok < 1 || top_k < 1 || n_experts < 1 || n_experts > moe::kMaxExperts)
+    return fail(MOE_ERR_SHAPE, "bad trace geometry");
+  TRY(set_device(c));
+  const size_t le = (size_t)n_layers * n_experts;
+  if (le == 0) return MOE_OK;
+  void* buf = nullptr;
+  CU(cudaMallocAsync(&buf, le * 12, c->stream));
+  int32_t* dc = static_cast<int32_t*>(buf);
+  double* dg = reinterpret_cast<double*>(static_cast<char*>(buf) + le * 4 + (le % 2) * 4);
+  cudaError_t e = moe::launch_trace_step(ids, gates, n_layers, n_tok, top_k, n_experts, dc, dg,
+                                         c->stream);
+  if (e == cudaSuccess)
+    e = cudaMemcpyAsync(token_count, dc, le * 4, cudaMemcpyDeviceToHost, c->stream);
+  if (e == cudaSuccess) e = cudaMemcpyAsync(gate_weight, dg, le * 8, cudaMemcpyDeviceToHost, c->stream);
+  cudaFreeAsync(buf, c->stream);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(c->stream);
+  CU(e);
+  for (size_t i = 0; i < le; ++i)
+    gate_weight[i] = token_count[i] > 0 ? gate_weight[i] / token_count[i] : 0.0;
+  return MOE_OK;
+}
+
 int moe_experts_forward(moe_weights* w, int layer, const float* x, int n_tok, const int32_t* ids,
                         const float* gates, float* x_out, float* post_silu, void* stream) {
   TRY(check_le(w, layer, 0));

@@ -3,6 +3,8 @@
 // token permutation.  These serve the reference's tiny test geometries
 // (hidden 2..6, ffn 2..8, toy 32/64) and any shape the streaming / tcgen05
 // kernels do not take.  Still GPU code: there is no CPU path in the product.
+#include <algorithm>
+
 #include "../../include/moe_b200.h"
 #include "common.cuh"
 #include "kernels.h"
@@ -436,6 +438,66 @@ cudaError_t launch_permute(const int32_t* ids, int n_tok, int k, int E, int32_t*
     if (e != cudaSuccess) return e;
   }
   permute_kernel<<<1, 1024, smem, s>>>(ids, n, E, counts, offsets, perm, inv_perm);
+  return cudaGetLastError();
+}
+
+// ---- routing histogram (profile_from_trace, placement.cpp:30-43) -------------
+// counts[l][e] += |{(t, j) : ids[l][t][j] == e}|: the per-(layer, expert)
+// selection counts a PopularityProfile accumulates, kept on the device across
+// forwards (integer atomics: order-independent, exact).
+__global__ void __launch_bounds__(256) routing_histogram_kernel(const int32_t* __restrict__ ids,
+                                                                int n, int E,
+                                                                unsigned long long* counts) {
+  extern __shared__ unsigned hist_sm[];
+  const int l = blockIdx.y;
+  for (int e = threadIdx.x; e < E; e += blockDim.x) hist_sm[e] = 0u;
+  __syncthreads();
+  const int32_t* row = ids + (size_t)l * n;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    const int e = row[i];
+    if (e >= 0 && e < E) atomicAdd(&hist_sm[e], 1u);
+  }
+  __syncthreads();
+  for (int e = threadIdx.x; e < E; e += blockDim.x)
+    if (hist_sm[e]) atomicAdd(&counts[(size_t)l * E + e], (unsigned long long)hist_sm[e]);
+}
+
+cudaError_t launch_routing_histogram(const int32_t* ids, int L, int n_tok, int k, int E,
+                                     int64_t* counts, cudaStream_t s) {
+  const int n = n_tok * k;
+  if (L <= 0 || n <= 0) return cudaSuccess;
+  const int bx = std::min((n + 255) / 256, 64);
+  routing_histogram_kernel<<<dim3(bx, L), 256, E * sizeof(unsigned), s>>>(
+      ids, n, E, reinterpret_cast<unsigned long long*>(counts));
+  return cudaGetLastError();
+}
+
+// ---- one RoutingTrace step (model.cpp:120-158) -------------------------------
+// For each (layer, expert): the number of (token, slot) pairs routed to it and
+// the sum of their gates, accumulated in fp64 in token order — the order of
+// the reference's tally / gate_sum loop — so gate_weight = sum / count.
+__global__ void trace_step_kernel(const int32_t* __restrict__ ids, const float* __restrict__ gates,
+                                  int L, int n, int k, int E, int32_t* count, double* gsum) {
+  const int le = blockIdx.x * blockDim.x + threadIdx.x;
+  if (le >= L * E) return;
+  const int l = le / E, e = le - l * E;
+  const int32_t* id = ids + (size_t)l * n * k;
+  const float* g = gates + (size_t)l * n * k;
+  int c = 0;
+  double sacc = 0.0;
+  for (int i = 0; i < n * k; ++i)
+    if (id[i] == e) {
+      ++c;
+      sacc += (double)g[i];
+    }
+  count[le] = c;
+  gsum[le] = sacc;
+}
+
+cudaError_t launch_trace_step(const int32_t* ids, const float* gates, int L, int n_tok, int k,
+                              int E, int32_t* count, double* gsum, cudaStream_t s) {
+  if (L <= 0) return cudaSuccess;
+  trace_step_kernel<<<(L * E + 127) / 128, 128, 0, s>>>(ids, gates, L, n_tok, k, E, count, gsum);
   return cudaGetLastError();
 }
 

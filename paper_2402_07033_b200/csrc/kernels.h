@@ -132,6 +132,14 @@ cudaError_t launch_prefill_experts(const LayerWeights& lw, int n_local, const Di
 // splits > 0: persistent grouped kernel, y is [splits][n*k][d] (sum the splits);
 // splits == 0: two-kernel path, y is [n*k][d].  sync: 1 + E*ceil(n_tok/256) ints.
 
+// ---- routing histogram: counts[l][e] += selections (int64, device) ----------
+cudaError_t launch_routing_histogram(const int32_t* ids, int L, int n_tok, int k, int E,
+                                     int64_t* counts, cudaStream_t s);
+
+// count[l][e] / gsum[l][e] of one trace step from ids/gates [L x n_tok x k]
+cudaError_t launch_trace_step(const int32_t* ids, const float* gates, int L, int n_tok, int k,
+                              int E, int32_t* count, double* gsum, cudaStream_t s);
+
 // ---- permutation ------------------------------------------------------------
 cudaError_t launch_permute(const int32_t* ids, int n_tok, int k, int E, int32_t* counts,
                            int32_t* offsets, int32_t* perm, int32_t* inv_perm, cudaStream_t s);

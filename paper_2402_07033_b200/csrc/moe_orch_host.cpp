@@ -629,6 +629,19 @@ std::vector<std::vector<int>> ep_shard_map(const PopularityProfile& profile, int
   return owner;
 }
 
+PopularityProfile profile_from_counts(const std::vector<std::vector<std::int64_t>>& counts) {
+  PopularityProfile p;
+  p.counts = counts;
+  for (const auto& row : counts) {
+    if (row.size() != counts.front().size()) throw ValidationError("ragged routing counts");
+    for (std::int64_t c : row) {
+      if (c < 0) throw ValidationError("negative routing count");
+      p.total_selections += c;
+    }
+  }
+  return p;
+}
+
 Placement rank_placement(const std::vector<std::vector<int>>& owner, int rank) {
   Placement pl;
   for (size_t l = 0; l < owner.size(); ++l)

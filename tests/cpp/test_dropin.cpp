@@ -408,6 +408,26 @@ TEST("ep_shard_map: every expert owned once, balanced, popularity-spread", false
   }
 }
 
+TEST("profile_from_counts == profile_from_trace on the same routing", false) {
+  ModelShape shape;
+  shape.num_layers = 2;
+  shape.experts_per_layer = 4;
+  shape.top_k = 2;
+  shape.hidden_dim = 8;
+  shape.ffn_dim = 16;
+  RoutingTrace tr;
+  TraceStep st;
+  st.kind = StepKind::Prefill;
+  st.layers = {{{0, 3, 0.5}, {2, 1, 0.5}, {3, 2, 0.5}}, {{0, 1, 0.5}, {1, 3, 0.5}, {3, 2, 0.5}}};
+  tr.steps.push_back(st);
+  const PopularityProfile want = profile_from_trace(tr, shape);
+  const PopularityProfile got = b200::profile_from_counts({{3, 0, 1, 2}, {1, 3, 0, 2}});
+  CHECK(got.counts == want.counts && got.total_selections == want.total_selections);
+  CHECK(b200::ep_shard_map(got, 2) == b200::ep_shard_map(want, 2));
+  CHECK_THROWS_AS(b200::profile_from_counts({{1, 2}, {3}}), ValidationError);
+  CHECK_THROWS_AS(b200::profile_from_counts({{1, -2}}), ValidationError);
+}
+
 // ===================== GPU cases =============================================
 TEST("expert_ffn zero weights and 1x1", true) {
   ExpertWeights w;

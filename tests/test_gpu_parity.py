@@ -438,3 +438,34 @@ def test_router_many_tokens_batched_kernel(ctx, orc):
         want, _, logits = orc.gate_topk(router, xs[t], 2)
         if margin(logits, 2) > 1e-5:
             assert list(ids[t].cpu().numpy()) == list(want)
+
+
+def test_routing_histogram_and_shard_map(ctx):
+    """Device routing histogram (f1): counts over a multi-layer forward's ids
+    equal a host bincount, accumulate across calls, and feed the shard map."""
+    import importlib.util
+    import os
+    L, E, k, d, f, n = 3, 8, 2, 512, 1792, 200
+    w = M.Weights(ctx, M.Shape(L, E, k, d, f, 4), M.DTYPE_F32)
+    w.random(5)
+    x = torch.randn(n, d, device="cuda")
+    ids = torch.zeros((L, n, k), dtype=torch.int32, device="cuda")
+    g = torch.zeros((L, n, k), device="cuda")
+    w.forward(x, ids, g)
+    counts = torch.zeros((L, E), dtype=torch.int64, device="cuda")
+    ctx.routing_histogram(ids, counts)
+    ctx.routing_histogram(ids, counts)
+    torch.cuda.synchronize()
+    host = ids.cpu().numpy()
+    want = np.stack([np.bincount(host[l].ravel(), minlength=E) for l in range(L)])
+    assert np.array_equal(counts.cpu().numpy(), 2 * want)
+    spec = importlib.util.spec_from_file_location(
+        "bench", os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "bench.py"))
+    b = importlib.util.module_from_spec(spec)
+    spec.loader.exec_module(b)
+    owner = b.shard_map(L, E, 2, rank_tokens=counts.cpu().numpy())
+    for l in range(L):
+        top2 = np.argsort(-want[l], kind="stable")[:2]
+        assert owner[l, top2[0]] != owner[l, top2[1]]  # the two hottest experts split
+        assert np.bincount(owner[l], minlength=2).tolist() == [4, 4]
+    w.close()
