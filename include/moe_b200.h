@@ -181,6 +181,21 @@ int moe_layer_forward(moe_weights* w, int layer, const float* x, float* x_out, i
 int moe_forward(moe_weights* w, float* x, int n_tok, int32_t* ids, float* gates,
                 void* stream);
 
+/* model_forward (as moe_forward, no graph) that also counts activation
+ * sparsity in the up-projection epilogues: counts (int64,
+ * device, [num_layers x n_thresholds], accumulated) += per layer the number
+ * of post-SiLU values silu(w_in x) — the ActivationSink values of
+ * model.cpp:131-139, over every (token, selected expert, ffn row) — with
+ * |v| < thresholds[i], compared in fp32.  Dividing by n_tok*top_k*ffn gives
+ * sparsity_histogram (placement.cpp:126-142) with no D2H of the values.
+ * thresholds strictly increasing (else MOE_ERR_VALIDATION), at most 8.
+ * Counted by the tcgen05 grouped-GEMM epilogue (prefill) or the generic up
+ * kernel (other shapes / batch 1).  Under tensor or expert parallelism each
+ * rank counts its resident rows / experts: sum the ranks' counts. */
+int moe_forward_sparsity(moe_weights* w, float* x, int n_tok, int32_t* ids, float* gates,
+                         const double* thresholds, int n_thresholds, int64_t* counts,
+                         void* stream);
+
 /* ---- host-buffer entry points (what the drop-in shim calls) ------------
  * Copies in, runs on the device, copies out, synchronizes.  tokens/out are
  * fp64 [n_tok x hidden] (the reference's vector<vector<double>>); ids [L x

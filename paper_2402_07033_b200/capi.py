@@ -111,6 +111,7 @@ def lib():
         "moe_decode_experts_partial": ([_vp, C.c_int, _vp, _vp, _vp, _vp, _vp], C.c_int),
         "moe_layer_forward": ([_vp, C.c_int, _vp, _vp, C.c_int, _vp, _vp, _vp], C.c_int),
         "moe_forward": ([_vp, _vp, C.c_int, _vp, _vp, _vp], C.c_int),
+        "moe_forward_sparsity": ([_vp, _vp, C.c_int, _vp, _vp, _dp, C.c_int, _vp, _vp], C.c_int),
         "moe_forward_host": ([_vp, _dp, C.c_int, _dp, _i32p, _dp, _dp], C.c_int),
         "moe_expert_ffn_host": ([_vp, C.c_int, C.c_int, C.c_int, _dp, _dp, _dp, _dp, _dp], C.c_int),
         "moe_gate_topk_host": ([_vp, C.c_int, C.c_int, _dp, _dp, C.c_int, _i32p, _dp], C.c_int),
@@ -353,6 +354,12 @@ class Weights:
                                 _stream(stream, x)))
 
     # -- host-buffer API ------------------------------------------------------
+    def forward_sparsity(self, x, ids, gates, thresholds, counts, stream=None):
+        """forward + fused sparsity counters: counts [L x n_thr] int64 device tensor."""
+        thr = np.ascontiguousarray(thresholds, np.float64)
+        check(lib().moe_forward_sparsity(self.h, _ptr(x), x.shape[0], _ptr(ids), _ptr(gates), _dptr(thr),
+                                         len(thr), _ptr(counts), _stream(stream, x)))
+
     def forward_host(self, tokens: np.ndarray, with_post=False):
         s = self.shape
         toks = np.ascontiguousarray(tokens, np.float64).reshape(-1, s.hidden_dim)

@@ -158,6 +158,9 @@ struct moe_weights {
   DevBuf dev_rw;               // device [L] pointers
   bool rw_enabled = false, rw_dirty = true;
   bool stack_enabled = true;
+  // fused sparsity counters of the call in flight (moe_forward_sparsity):
+  // counts [L][sp.n]; layer l adds into sp.counts + l * sp.n
+  moe::SparsityCounters sp;
   DevBuf stage_d;  // fp64 staging for uploads / downloads
   void* host_pin = nullptr;
   size_t host_pin_bytes = 0;
@@ -266,7 +269,7 @@ int allreduce(moe_weights* w, float* buf, size_t count, cudaStream_t s) {
 }
 
 bool use_decode(const moe_weights* w, int n_tok, const float* post) {
-  return n_tok == 1 && w->plan.ok && post == nullptr;
+  return n_tok == 1 && w->plan.ok && post == nullptr && w->sp.counts == nullptr;
 }
 
 // Whole-token persistent kernel: single GPU (no exchange inside a layer).
@@ -306,7 +309,8 @@ int enqueue_stack(moe_weights* w, float* x, int32_t* ids, float* gates, cudaStre
 }
 
 bool use_prefill(const moe_weights* w, int n_tok, const float* post) {
-  return n_tok > 1 && post == nullptr && w->prefill_enabled && moe::prefill_supported(w->dims());
+  return n_tok > 1 && post == nullptr && w->prefill_enabled && moe::prefill_supported(w->dims()) &&
+         (w->sp.counts == nullptr || w->prefill_splits > 0);  // counters: grouped kernel only
 }
 
 int ensure_prefill_scratch(moe_weights* w, int n_tok) {
@@ -329,6 +333,8 @@ int experts_forward(moe_weights* w, int l, const float* x, int n_tok, const int3
   const Dims dm = w->dims();
   const LayerWeights lw = w->layer(l);
   const bool ep = w->ctx->ep();
+  moe::SparsityCounters sp = w->sp;
+  if (sp.counts) sp.counts += (size_t)l * sp.n;
   if (use_decode(w, n_tok, post)) {
     CU(moe::launch_decode_experts(w->plan, lw, dm, ids, gates, x, w->ypart.as<float>(), s, pdl));
     if (!ep) {
@@ -370,12 +376,12 @@ int experts_forward(moe_weights* w, int l, const float* x, int n_tok, const int3
                                    w->dev_slots.as<int16_t>() + (size_t)l * dm.E,
                                    w->pf_xg.as<__nv_bfloat16>(), w->pf_h.as<__nv_bfloat16>(),
                                    w->y.as<float>(), w->pf_sync.as<int>(), w->ctx->sm_count, S,
-                                   s));
+                                   s, sp));
     cgates = nullptr;
     nsplit = std::max(1, S);
     if (S > 0) split_of = moe::prefill_split_of(w->pf_sync.as<int>(), dm.E, n_tok);
   } else {
-    CU(moe::launch_generic_up(lw, dm, x, n_tok, ids, w->h.as<float>(), post, s, pdl));
+    CU(moe::launch_generic_up(lw, dm, x, n_tok, ids, w->h.as<float>(), post, s, pdl, sp));
     CU(moe::launch_generic_down(lw, dm, w->h.as<float>(), n_tok, ids, w->y.as<float>(), s, pdl));
   }
   if (!ep) {
@@ -1052,6 +1058,30 @@ int moe_forward(moe_weights* w, float* x, int n_tok, int32_t* ids, float* gates,
     return forward_graph(w, x, ids, gates, s);
   }
   return enqueue_forward(w, x, n_tok, ids, gates, s, nullptr);
+}
+
+int moe_forward_sparsity(moe_weights* w, float* x, int n_tok, int32_t* ids, float* gates,
+                         const double* thresholds, int n_thresholds, int64_t* counts,
+                         void* stream) {
+  if (!w) return fail(MOE_ERR_ARG, "null weights");
+  if (n_tok < 0) return fail(MOE_ERR_ARG, "n_tok < 0");
+  if (!thresholds || !counts) return fail(MOE_ERR_ARG, "null pointer");
+  if (n_thresholds < 1 || n_thresholds > moe::kMaxThresholds)
+    return fail(MOE_ERR_ARG, "1..8 thresholds");
+  for (int i = 1; i < n_thresholds; ++i)  // placement.cpp:130-132
+    if (thresholds[i] <= thresholds[i - 1])
+      return fail(MOE_ERR_VALIDATION, "thresholds must be strictly increasing");
+  if (n_tok == 0 || w->L() == 0) return MOE_OK;
+  if (!x || !ids || !gates) return fail(MOE_ERR_ARG, "null pointer");
+  std::lock_guard<std::mutex> lk(w->mu);
+  TRY(set_device(w->ctx));
+  TRY(ensure_scratch(w, n_tok));
+  w->sp.counts = reinterpret_cast<unsigned long long*>(counts);
+  w->sp.n = n_thresholds;
+  for (int i = 0; i < n_thresholds; ++i) w->sp.thr[i] = (float)thresholds[i];
+  const int rc = enqueue_forward(w, x, n_tok, ids, gates, pick(w->ctx, stream), nullptr);
+  w->sp = moe::SparsityCounters();
+  return rc;
 }
 
 int moe_forward_host(moe_weights* w, const double* tokens, int n_tok, double* out, int32_t* ids,

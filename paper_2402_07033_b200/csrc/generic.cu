@@ -201,13 +201,26 @@ template <typename W>
 __global__ void __launch_bounds__(256) generic_up_kernel(LayerWeights lw, int d, int f, int k,
                                                          const float* __restrict__ x,
                                                          const int32_t* __restrict__ ids,
-                                                         float* h, float* post_silu) {
+                                                         float* h, float* post_silu,
+                                                         SparsityCounters sp) {
+  __shared__ unsigned sp_blk[kMaxThresholds];
   const int warp = warp_uniform(threadIdx.x >> 5), lane = threadIdx.x & 31;
   griddep_wait();
   griddep_launch_dependents();
+  if (sp.counts) {
+    if (threadIdx.x < kMaxThresholds) sp_blk[threadIdx.x] = 0u;
+    __syncthreads();
+  }
   const int r = blockIdx.x * 8 + warp;
-  if (r >= f) return;
   const int tj = blockIdx.y;
+  if (r >= f) {
+    if (sp.counts) {
+      __syncthreads();
+      if (threadIdx.x < sp.n && sp_blk[threadIdx.x])
+        atomicAdd(&sp.counts[threadIdx.x], (unsigned long long)sp_blk[threadIdx.x]);
+    }
+    return;
+  }
   const int t = tj / k;
   const int slot = lw.slot_of[ids[tj]];
   float a = 0.f, b = 0.f;
@@ -227,6 +240,14 @@ __global__ void __launch_bounds__(256) generic_up_kernel(LayerWeights lw, int d,
     const float sa = slot >= 0 ? silu_f(a) : 0.f;
     h[(size_t)tj * f + r] = sa * b;
     if (post_silu) post_silu[(size_t)tj * f + r] = sa;
+    if (sp.counts && slot >= 0)
+      for (int i = 0; i < sp.n; ++i)
+        if (fabsf(sa) < sp.thr[i]) atomicAdd(&sp_blk[i], 1u);
+  }
+  if (sp.counts) {
+    __syncthreads();
+    if (threadIdx.x < sp.n && sp_blk[threadIdx.x])
+      atomicAdd(&sp.counts[threadIdx.x], (unsigned long long)sp_blk[threadIdx.x]);
   }
 }
 
@@ -254,16 +275,16 @@ __global__ void __launch_bounds__(256) generic_down_kernel(LayerWeights lw, int 
 
 cudaError_t launch_generic_up(const LayerWeights& lw, const Dims& dm, const float* x, int n_tok,
                               const int32_t* ids, float* h, float* post_silu, cudaStream_t s,
-                              bool pdl) {
+                              bool pdl, const SparsityCounters& sp) {
   if (n_tok <= 0) return cudaSuccess;
   cudaLaunchAttribute attr[1];
   cudaLaunchConfig_t cfg =
       make_cfg(dim3((dm.f + 7) / 8, n_tok * dm.k), dim3(256), s, pdl, attr);
   if (dm.dtype == MOE_DTYPE_BF16)
     return cudaLaunchKernelEx(&cfg, generic_up_kernel<__nv_bfloat16>, lw, dm.d, dm.f, dm.k, x,
-                              ids, h, post_silu);
+                              ids, h, post_silu, sp);
   return cudaLaunchKernelEx(&cfg, generic_up_kernel<float>, lw, dm.d, dm.f, dm.k, x, ids, h,
-                            post_silu);
+                            post_silu, sp);
 }
 
 cudaError_t launch_generic_down(const LayerWeights& lw, const Dims& dm, const float* h,

@@ -25,6 +25,16 @@ struct Dims {
   int dtype;  // MOE_DTYPE_*
 };
 
+// Fused activation-sparsity counters (sparsity_histogram, placement.cpp:126-142,
+// over the ActivationSink values of model.cpp:131-139): the up-projection
+// epilogues add |{v : |silu(w_in x)| < thr[i]}| into counts[i] (one layer).
+constexpr int kMaxThresholds = 8;
+struct SparsityCounters {
+  unsigned long long* counts = nullptr;  // [n] device, accumulated; nullptr = off
+  float thr[kMaxThresholds] = {};
+  int n = 0;
+};
+
 // ---- router -------------------------------------------------------------
 cudaError_t launch_router_topk(const float* router, const float* x, int n_tok, const Dims& dm,
                                int32_t* ids, float* gates, cudaStream_t s, bool pdl);
@@ -100,7 +110,7 @@ cudaError_t launch_reduce_exchange(const float* ypart, int nparts, const float* 
 // h[t][j][r] = silu(W1 x_t) * (W3 x_t) for expert ids[t][j]; post_silu optional.
 cudaError_t launch_generic_up(const LayerWeights& lw, const Dims& dm, const float* x, int n_tok,
                               const int32_t* ids, float* h, float* post_silu, cudaStream_t s,
-                              bool pdl);
+                              bool pdl, const SparsityCounters& sp = SparsityCounters());
 // y[t][j][i] = sum_r W2T[r][i] h[t][j][r]
 cudaError_t launch_generic_down(const LayerWeights& lw, const Dims& dm, const float* h,
                                 int n_tok, const int32_t* ids, float* y, cudaStream_t s,
@@ -128,7 +138,8 @@ cudaError_t launch_prefill_experts(const LayerWeights& lw, int n_local, const Di
                                    const int32_t* offsets, const int32_t* perm,
                                    const float* gates, const int16_t* slot_of_dev,
                                    __nv_bfloat16* xg, __nv_bfloat16* h, float* y, int* sync,
-                                   int sm_count, int splits, cudaStream_t s);
+                                   int sm_count, int splits, cudaStream_t s,
+                                   const SparsityCounters& sp = SparsityCounters());
 // splits > 0: persistent grouped kernel, y is [splits][n*k][d] (sum the splits);
 // splits == 0: two-kernel path, y is [n*k][d].  sync: 1 + E*ceil(n_tok/256) ints.
 

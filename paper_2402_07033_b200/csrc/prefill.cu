@@ -393,9 +393,9 @@ constexpr int GP_STAGE = 2 * PF_BM * PF_BK * 2 + PF_MAXN * PF_BK * 2;  // 64 KB
 constexpr int GP_QN = 2;
 // epilogue staging: 32 token rows x 128 columns, fp32 (down) or bf16 (up)
 constexpr int GP_STG = 32 * PF_BM * 4;  // 16 KB
-constexpr int GP_SMEM = GP_STAGES * GP_STAGE + GP_STG + 1024 /*align*/ + 4096 /*barriers, queue, tables*/ +
-                        2 * PF_MAXN * 4 /*down tile: pair index + gate per token row*/ +
-                        kMaxExperts * 4 /*splits per expert*/;
+constexpr int GP_SMEM = GP_STAGES * GP_STAGE + GP_STG + 1024 /*align*/ + 256 /*barriers, queue*/ +
+                        (5 * kMaxExperts + 1) * 4 /*schedule segments [2E+1] + [2E], splits [E]*/ +
+                        2 * PF_MAXN * 4 /*down tile: pair index + gate per token row*/;
 
 struct GroupedArgs {
   const int32_t* counts;
@@ -414,6 +414,8 @@ struct GroupedArgs {
   // [tile | N << 32], producer got tile, MMA issued last MMA, epilogue done
   unsigned long long* trace;
   int trace_cap;  // tiles per CTA
+  SparsityCounters sp;  // fused |silu(w_in x)| < thr counters (off: sp.counts == nullptr)
+  int lag;              // schedule: expert i's down tiles follow expert i+lag's up tiles
 };
 
 __device__ __forceinline__ void gp_stamp(const GroupedArgs& a, int i, int field,
@@ -426,26 +428,22 @@ struct GTile {
   int up, e, c, t1, s;  // t1: ffn tile (up) or hidden tile (down)
 };
 
-__device__ __forceinline__ GTile gp_decode(int t, int total_up, const int* upb, const int* dnb,
-                                           int E, int n_ft, int n_dt, const int* split) {
+// The tile schedule is a list of segments, each the up or the down tiles of
+// one expert: seg_start[i] = first tile of segment i, seg_code[i] = 2 e + up.
+__device__ __forceinline__ GTile gp_decode(int t, const int* seg_start, const int* seg_code,
+                                           int n_ft, int n_dt, const int* split) {
   GTile g;
-  if (t < total_up) {
-    int e = 0;
-    while (upb[e + 1] <= t) ++e;
-    const int loc = t - upb[e];
-    g.up = 1;
-    g.e = e;
+  int i = 0;
+  while (seg_start[i + 1] <= t) ++i;
+  const int loc = t - seg_start[i];
+  g.e = seg_code[i] >> 1;
+  g.up = seg_code[i] & 1;
+  if (g.up) {
     g.c = loc / n_ft;
     g.t1 = loc % n_ft;
     g.s = 0;
   } else {
-    const int t2 = t - total_up;
-    int e = 0;
-    while (dnb[e + 1] <= t2) ++e;
-    const int loc = t2 - dnb[e];
-    g.up = 0;
-    g.e = e;
-    const int S = split[e];
+    const int S = split[g.e];
     g.c = loc / (n_dt * S);
     const int rem = loc % (n_dt * S);
     g.t1 = rem / S;
@@ -454,6 +452,7 @@ __device__ __forceinline__ GTile gp_decode(int t, int total_up, const int* upb, 
   return g;
 }
 
+template <bool kSparsity>
 __global__ void __launch_bounds__(PF_THREADS, 1)
     prefill_grouped_kernel(const __grid_constant__ CUtensorMap wmap_up,  // box 64 x 128
                            const __grid_constant__ CUtensorMap wmap_dn,  // box 64 x 64
@@ -472,12 +471,12 @@ __global__ void __launch_bounds__(PF_THREADS, 1)
   uint64_t* qempty = qfull + GP_QN;
   uint32_t* tmem_base_s = reinterpret_cast<uint32_t*>(qempty + GP_QN);
   int* q_tile = reinterpret_cast<int*>(tmem_base_s + 1);
-  int* upb = q_tile + GP_QN;          // [E+1] up tiles before expert e
-  int* dnb = upb + kMaxExperts + 1;   // [E+1] down tiles before expert e
-  int* s_pair = dnb + kMaxExperts + 1;                            // [PF_MAXN]
+  int* seg_start = q_tile + GP_QN;                  // [2E + 1]
+  int* seg_code = seg_start + 2 * kMaxExperts + 1;   // [2E]
+  int* s_split = seg_code + 2 * kMaxExperts;         // [E]
+  int* s_pair = s_split + kMaxExperts;                            // [PF_MAXN]
   float* s_gate = reinterpret_cast<float*>(s_pair + PF_MAXN);     // [PF_MAXN]
-  int* s_split = reinterpret_cast<int*>(s_gate + PF_MAXN);        // [E]
-  __shared__ int s_total_up, s_total;
+  __shared__ int s_total;
 
   const int warp = warp_uniform(threadIdx.x >> 5), lane = threadIdx.x & 31;
   // down tiles cover 2 x 128 hidden rows (two weight tiles per stage, like
@@ -485,26 +484,38 @@ __global__ void __launch_bounds__(PF_THREADS, 1)
   const int n_ft = a.f / PF_BM, n_dt = a.d / (2 * PF_BM);
   griddep_wait();
   if (threadIdx.x == 0) {
-    // K splits per expert: the down tiles are scheduled last, so the last
-    // ~3/8 of the active experts take the finest split (a.S) and the rest
-    // half of it: large tiles early, small tiles in the final wave (tail).
+    // Schedule: the active experts' up tiles in order, with expert i's down
+    // tiles placed after expert i+lag's up tiles (a.lag; the default puts
+    // all downs after all ups), the remaining downs last.  Down tiles of
+    // expert e only wait for e's up tiles, which precede them in the list,
+    // and up tiles never wait, so any lag is deadlock-free.  The last ~3/8
+    // of the experts' downs — the final wave — take the finest K split
+    // (a.S), the others half of it: large tiles early, small ones in the tail.
+    int act[kMaxExperts];
     int n_act = 0;
-    for (int e = 0; e < a.E; ++e) n_act += (a.slot_of[e] >= 0 && a.counts[e] > 0);
+    for (int e = 0; e < a.E; ++e)
+      if (a.slot_of[e] >= 0 && a.counts[e] > 0) act[n_act++] = e;
     const int n_late = (3 * n_act + 7) / 8;
     const int s_hi = min(a.S, a.f / PF_BK), s_lo = max(1, s_hi / 2);
-    upb[0] = dnb[0] = 0;
-    for (int e = 0, i = 0; e < a.E; ++e) {
-      const bool act = a.slot_of[e] >= 0 && a.counts[e] > 0;
-      const int S = act ? (i >= n_act - n_late ? s_hi : s_lo) : 1;
-      i += act;
-      s_split[e] = S;
-      if (blockIdx.x == 0) a.split_of[e] = S;
-      const int ch = a.slot_of[e] >= 0 ? (a.counts[e] + PF_MAXN - 1) / PF_MAXN : 0;
-      upb[e + 1] = upb[e] + ch * n_ft;
-      dnb[e + 1] = dnb[e] + ch * n_dt * S;
+    for (int e = 0; e < a.E; ++e) s_split[e] = 1;
+    for (int i = 0; i < n_act; ++i) s_split[act[i]] = i >= n_act - n_late ? s_hi : s_lo;
+    if (blockIdx.x == 0)
+      for (int e = 0; e < a.E; ++e) a.split_of[e] = s_split[e];
+    const int kLag = a.lag;
+    int ns = 0, tot = 0;
+    auto push = [&](int e, int up) {
+      const int ch = (a.counts[e] + PF_MAXN - 1) / PF_MAXN;
+      seg_start[ns] = tot;
+      seg_code[ns++] = 2 * e + up;
+      tot += up ? ch * n_ft : ch * n_dt * s_split[e];
+    };
+    for (int i = 0; i < n_act; ++i) {
+      push(act[i], 1);
+      if (i >= kLag) push(act[i - kLag], 0);
     }
-    s_total_up = upb[a.E];
-    s_total = upb[a.E] + dnb[a.E];
+    for (int i = max(0, n_act - kLag); i < n_act; ++i) push(act[i], 0);
+    seg_start[ns] = tot;
+    s_total = tot;
     for (int i = 0; i < GP_STAGES; ++i) {
       mbar_init(&full[i], 1);
       mbar_init(&empty[i], 1);
@@ -524,7 +535,7 @@ __global__ void __launch_bounds__(PF_THREADS, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_base_s;
-  const int total_up = s_total_up, total = s_total;
+  const int total = s_total;
   const int nkb_up = a.d / PF_BK, nkb_dn = a.f / PF_BK;
   constexpr int kA = PF_BM * PF_BK * 2;
   constexpr int kBox = PF_BOXN * PF_BK * 2;
@@ -557,10 +568,11 @@ __global__ void __launch_bounds__(PF_THREADS, 1)
           qph ^= 1;
         }
         if (t >= total) break;
-        const GTile g = gp_decode(t, total_up, upb, dnb, a.E, n_ft, n_dt, s_split);
+        const GTile g = gp_decode(t, seg_start, seg_code, n_ft, n_dt, s_split);
         int nvalid, N, nboxes, srow;
         chunk_geom(g, nvalid, N, nboxes, srow);
-        gp_stamp(a, ntile, 0, (unsigned long long)t | ((unsigned long long)N << 32));
+        gp_stamp(a, ntile, 0,
+                 (unsigned long long)t | ((unsigned long long)N << 32) | ((unsigned long long)g.up << 48));
         gp_stamp(a, ntile, 1, globaltimer());
         ++ntile;
         const int slot = a.slot_of[g.e];
@@ -623,7 +635,7 @@ __global__ void __launch_bounds__(PF_THREADS, 1)
           qph ^= 1;
         }
         if (t >= total) break;
-        const GTile g = gp_decode(t, total_up, upb, dnb, a.E, n_ft, n_dt, s_split);
+        const GTile g = gp_decode(t, seg_start, seg_code, n_ft, n_dt, s_split);
         int nvalid, N, nboxes, srow;
         chunk_geom(g, nvalid, N, nboxes, srow);
         int bufs[2];
@@ -690,7 +702,7 @@ __global__ void __launch_bounds__(PF_THREADS, 1)
         qph ^= 1;
       }
       if (t >= total) break;
-      const GTile g = gp_decode(t, total_up, upb, dnb, a.E, n_ft, n_dt, s_split);
+      const GTile g = gp_decode(t, seg_start, seg_code, n_ft, n_dt, s_split);
       int nvalid, N, nboxes, srow;
       chunk_geom(g, nvalid, N, nboxes, srow);
       if (!g.up) {
@@ -708,6 +720,7 @@ __global__ void __launch_bounds__(PF_THREADS, 1)
       tc_fence_after();
       const uint32_t c1 = tmem + lane_off + bufs[0] * 256;
       const uint32_t c3 = nb == 2 ? tmem + lane_off + bufs[1] * 256 : c1 + 128;
+      unsigned sp_cnt[kMaxThresholds] = {};
       if (g.up && (a.debug & 1)) {
       } else if (!g.up && (a.debug & 2)) {
       } else if (g.up) {
@@ -725,6 +738,11 @@ __global__ void __launch_bounds__(PF_THREADS, 1)
             const float u = __uint_as_float(r1[i]);
             const float sv = __fdividef(u, 1.0f + __expf(-u));
             st16[i * PF_BM + warp * 32 + lane] = __float2bfloat16_rn(sv * __uint_as_float(r3[i]));
+            if (kSparsity && c0 + i < nvalid) {
+#pragma unroll
+              for (int q = 0; q < kMaxThresholds; ++q)
+                if (q < a.sp.n) sp_cnt[q] += fabsf(sv) < a.sp.thr[q];
+            }
           }
           named_bar_sync(3, 128);
           const int nrow = min(32, nvalid - c0);
@@ -770,6 +788,14 @@ __global__ void __launch_bounds__(PF_THREADS, 1)
             named_bar_sync(3, 128);
           }
         }
+      }
+      if (kSparsity && g.up) {
+#pragma unroll
+        for (int q = 0; q < kMaxThresholds; ++q)
+          if (q < a.sp.n) {
+            const unsigned v = __reduce_add_sync(MOE_FULL_MASK, sp_cnt[q]);
+            if (lane == 0 && v) atomicAdd(&a.sp.counts[q], (unsigned long long)v);
+          }
       }
       tc_fence_before();
       named_bar_sync(3, 128);
@@ -849,7 +875,8 @@ cudaError_t launch_prefill_experts(const LayerWeights& lw, int n_local, const Di
                                    const int32_t* offsets, const int32_t* perm,
                                    const float* gates, const int16_t* slot_of_dev,
                                    __nv_bfloat16* xg, __nv_bfloat16* h, float* y, int* sync,
-                                   int sm_count, int splits, cudaStream_t s) {
+                                   int sm_count, int splits, cudaStream_t s,
+                                   const SparsityCounters& sp) {
   const int rows = n_tok * dm.k;
   if (rows == 0 || n_local == 0) return cudaSuccess;
   gather_rows_kernel<<<rows, 128, 0, s>>>(x, perm, rows, dm.k, dm.d, xg);  // d % 128 == 0
@@ -883,6 +910,11 @@ cudaError_t launch_prefill_experts(const LayerWeights& lw, int n_local, const Di
     g.S = splits;
     g.max_chunks = chunks;
     g.debug = getenv("MOE_B200_PF_DEBUG") ? atoi(getenv("MOE_B200_PF_DEBUG")) : 0;
+    g.sp = sp;
+    // measured (tools/prof_prefill.py, Mixtral 512 tokens): interleaving
+    // downs among ups is slower (lag 1/2/3: +33/+12/+24 us) than all ups
+    // first, so the default lag puts every down after every up
+    g.lag = getenv("MOE_B200_PF_LAG") ? atoi(getenv("MOE_B200_PF_LAG")) : kMaxExperts;
     g.trace = nullptr;
     g.trace_cap = 0;
     const char* trace_path = getenv("MOE_B200_PF_TRACE");
@@ -896,10 +928,10 @@ cudaError_t launch_prefill_experts(const LayerWeights& lw, int n_local, const Di
     }
     err = cudaMemsetAsync(sync, 0, sizeof(int) * (1 + (size_t)dm.E * chunks), s);
     if (err != cudaSuccess) return err;
-    err = cudaFuncSetAttribute(prefill_grouped_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                               GP_SMEM);
+    auto kern = sp.counts ? prefill_grouped_kernel<true> : prefill_grouped_kernel<false>;
+    err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, GP_SMEM);
     if (err != cudaSuccess) return err;
-    prefill_grouped_kernel<<<sm_count, PF_THREADS, GP_SMEM, s>>>(wmap_up, wmap_dn, xmap, hmap, g);
+    kern<<<sm_count, PF_THREADS, GP_SMEM, s>>>(wmap_up, wmap_dn, xmap, hmap, g);
     if ((err = cudaGetLastError()) != cudaSuccess || !trace_path) return err;
     // diagnostics only: synchronous dump (appends one record per launch)
     const size_t n = (size_t)sm_count * g.trace_cap * 4;

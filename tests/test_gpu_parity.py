@@ -469,3 +469,61 @@ def test_routing_histogram_and_shard_map(ctx):
         assert owner[l, top2[0]] != owner[l, top2[1]]  # the two hottest experts split
         assert np.bincount(owner[l], minlength=2).tolist() == [4, 4]
     w.close()
+
+
+def test_fused_sparsity_counters_match_reference_sink(ctx, monkeypatch):
+    """Activation-sparsity counters fused into the up-projection epilogues (f2)
+    against the reference's sparsity_histogram of its ActivationSink values."""
+    ref = O.Reference() if O.reference_available() else None
+    if ref is None:
+        pytest.skip("oracle/_ref not built")
+    thr = [0.001, 0.01, 0.1, 1.0]  # the reference CLI defaults (moe_orch_cli.cpp:412)
+    L, E, k, d, f, n = 4, 8, 2, 32, 64, 64
+    shape = O.Shape(L, E, k, d, f, 4)
+    wref = ref.random_model(shape, 3)
+    w = M.Weights(ctx, M.Shape(L, E, k, d, f, 4), M.DTYPE_F32)
+    w.upload_oracle(wref)
+    wd = O.Weights(shape)
+    for l in range(L):
+        for e in range(E):
+            for dst, src in zip(wd.expert(l, e), w.download_expert(l, e)):
+                dst[:] = src
+        wd.router[l][:] = w.download_router(l)
+    toks = np.random.RandomState(0).randn(n, d).astype(np.float32).astype(np.float64)
+    sink = ref.model_forward(shape, wd, toks, with_sink=True, sink_cap=n * L * k * f)[4]
+    vals = np.abs(sink.reshape(n, L, k, f))
+    want = np.array([[int((vals[:, l] < t).sum()) for t in thr] for l in range(L)])
+    x = torch.tensor(toks, dtype=torch.float32, device="cuda")
+    ids = torch.zeros((L, n, k), dtype=torch.int32, device="cuda")
+    g = torch.zeros((L, n, k), device="cuda")
+    counts = torch.zeros((L, len(thr)), dtype=torch.int64, device="cuda")
+    w.forward_sparsity(x, ids, g, thr, counts)
+    torch.cuda.synchronize()
+    got = counts.cpu().numpy()
+    assert np.abs(got - want).max() <= 2, (got, want)  # fp32 vs fp64 at the thresholds
+    with pytest.raises(M.MoeError) as ei:
+        w.forward_sparsity(x, ids, g, [0.1, 0.01], counts)
+    assert ei.value.kind == "ValidationError"
+    # tcgen05 grouped-GEMM epilogue vs generic kernel at the Mixtral shape
+    s = M.Shape(1, 8, 2, 4096, 14336, 2)
+    wt = M.Weights(ctx, s, M.DTYPE_BF16)
+    monkeypatch.setenv("MOE_B200_PREFILL", "0")
+    wgn = M.Weights(ctx, s, M.DTYPE_BF16)
+    monkeypatch.delenv("MOE_B200_PREFILL")
+    assert wt.expert_path(128) == 3 and wgn.expert_path(128) == 2
+    xs = torch.randn(128, 4096, device="cuda")
+    res = []
+    for ww in (wt, wgn):
+        ww.random(4)
+        c = torch.zeros((1, len(thr)), dtype=torch.int64, device="cuda")
+        ww.forward_sparsity(xs.clone(), torch.zeros((1, 128, 2), dtype=torch.int32, device="cuda"),
+                            torch.zeros((1, 128, 2), device="cuda"), thr, c)
+        torch.cuda.synchronize()
+        res.append(c.cpu().numpy()[0])
+    total = 128 * 2 * 14336
+    assert res[1][-1] <= total and res[0][-1] > 0
+    # bf16 activations (tensor-core operands) vs fp32 ones: counts agree closely
+    assert np.all(np.abs(res[0] - res[1]) <= 0.01 * res[1] + 50), res
+    wt.close()
+    wgn.close()
+    w.close()

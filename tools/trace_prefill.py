@@ -68,12 +68,9 @@ def main():
         for c in range(G):
             nt = int(valid[c].sum())
             for i in range(nt):
-                tile = int(tr[c, i, 0]) & 0xffffffff
-                N = int(tr[c, i, 0]) >> 32
-                total_up = None
-                kind = None
-                # up tiles come first in the schedule; n_ft per (e, chunk)
-                kind = "up" if tile < (sum(((cc + 255) // 256) for cc in counts) * n_ft) else "down"
+                word = int(tr[c, i, 0])
+                N = (word >> 32) & 0xffff
+                kind = "up" if (word >> 48) & 1 else "down"
                 if kind == "up":
                     kind = "up<=128" if N <= 128 else "up>128"
                 nxt = tr[c, i + 1, 1] if i + 1 < nt else tr[c, i, 3]
