@@ -169,6 +169,8 @@ def run_ours(args):
 
     world, rank, local = dist_setup(args.gpus)
     L, E, k, d, f, dt = CONFIGS[args.config]
+    if args.layers:  # a reduced stack (e.g. x22b on one GPU: 56 layers need 270 GB)
+        L = args.layers
     dtype = M.DTYPE_BF16 if dt == "bf16" else M.DTYPE_F32
     esz = 2 if dt == "bf16" else 4
     torch.cuda.set_device(local)
@@ -319,7 +321,8 @@ def run_ours(args):
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms_per_step, 4),
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
             "dtype": "bf16" if dt == "bf16" else "f32", "data": "synthetic (random-init weights, N(0,1) tokens)",
-            "config": {"workload": WORKLOAD_NAME[args.config], "layers": L, "experts": E, "top_k": k,
+            "config": {"workload": WORKLOAD_NAME[args.config] + (f" [reduced to {L} layers]" if args.layers else ""),
+                       "layers": L, "experts": E, "top_k": k,
                        "hidden": d, "ffn": f, "batch": 1,
                        "parallelism": f"{args.shard}{world}" if world > 1 else "single-gpu",
                        "combine": None if world == 1 else
@@ -444,6 +447,8 @@ def run_reference(args):
     import oracle as O
 
     L, E, k, d, f, dt = CONFIGS[args.config]
+    if args.layers:
+        L = args.layers
     if not O.reference_available():
         print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref/libmoe_ref.so not built"}))
         return
@@ -499,6 +504,8 @@ def main():
     ap.add_argument("--cpu-tokens", type=int, default=12)
     ap.add_argument("--ref-threads", type=int, default=0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--layers", type=int, default=0,
+                    help="override the config's layer count (per-layer rate of a stack that does not fit)")
     ap.add_argument("--shard", default="ep", choices=["ep", "tp"],
                     help="N>1: expert parallelism (popularity shard map) or tensor parallelism "
                          "(ffn rows of every expert split over the GPUs)")

@@ -272,9 +272,22 @@ bool use_decode(const moe_weights* w, int n_tok, const float* post) {
   return n_tok == 1 && w->plan.ok && post == nullptr && w->sp.counts == nullptr;
 }
 
-// Whole-token persistent kernel: single GPU (no exchange inside a layer).
+// Peer windows usable by the batch-1 kernels of these weights.
+bool peer_ok(const moe_weights* w) {
+  const moe_ctx* c = w->ctx;
+  return c->peers && w->d() <= c->win_hidden && w->plan.grid <= moe::kPeerSlots;
+}
+
+// Whole-token persistent kernel: one GPU, or several linked by peer windows
+// (the per-layer exchange then runs inside the kernel).
 bool use_stack(const moe_weights* w, int n_tok) {
-  return use_decode(w, n_tok, nullptr) && !w->ctx->ep() && w->stack_enabled && w->L() > 0;
+  // MOE_B200_VIRTUAL_STACK (measurement hook, tools/shard_proxy.py): a
+  // virtual rank runs its shard through the persistent kernel with no
+  // exchange — one rank's streaming time of an N-GPU step
+  static const bool virt = getenv("MOE_B200_VIRTUAL_STACK") != nullptr;
+  const moe_ctx* c = w->ctx;
+  return use_decode(w, n_tok, nullptr) && (!c->ep() || peer_ok(w) || (c->virtual_ep && virt)) &&
+         w->stack_enabled && w->L() > 0;
 }
 
 // Recompute rw = R_{l+1} W2 after any weight/router change (outside capture).
@@ -304,7 +317,7 @@ int enqueue_stack(moe_weights* w, float* x, int32_t* ids, float* gates, cudaStre
   sd.L = w->L();
   CU(moe::launch_decode_stack(w->plan, sd, w->dims(), x, w->xbuf2.as<float>(),
                               w->ypart.as<float>(), w->rpart.as<float>(), ids, gates,
-                              w->gbar.as<unsigned>(), s));
+                              w->gbar.as<unsigned>(), s, peer_ok(w) ? &w->ctx->pa : nullptr));
   return MOE_OK;
 }
 
@@ -343,7 +356,7 @@ int experts_forward(moe_weights* w, int l, const float* x, int n_tok, const int3
                                      w->counter.as<unsigned>(), next_ids, next_gates, s, pdl));
       return MOE_OK;
     }
-    if (w->ctx->peers && dm.d <= w->ctx->win_hidden) {
+    if (peer_ok(w)) {
       // fused combine over peer memory: reduce + push + rank-ordered sum + residual + router
       CU(moe::launch_reduce_exchange(w->ypart.as<float>(), w->plan.grid, x, x_out, dm, next_router,
                                      w->rpart.as<float>(), w->counter.as<unsigned>(), next_ids,
@@ -573,14 +586,20 @@ static int alloc_window(moe_ctx* c, int world, int max_hidden) {
   return MOE_OK;
 }
 
+static void set_peer_parts(moe_ctx* c, int r, void* base) {
+  const moe::PeerParts q = moe::peer_window_parts(base, c->win_world, c->win_hidden);
+  c->pa.inbox[r] = q.inbox;
+  c->pa.flags[r] = q.flags;
+  c->pa.zbox[r] = q.zbox;
+  c->pa.zflags[r] = q.zflags;
+}
+
 static void set_own_parts(moe_ctx* c, int world, int rank) {
-  float* inbox;
-  unsigned *flags, *seq, *err;
-  moe::peer_window_parts(c->win, world, c->win_hidden, &inbox, &flags, &seq, &err);
-  c->pa.inbox[rank] = inbox;
-  c->pa.flags[rank] = flags;
-  c->pa.seq = seq;
-  c->pa.err = err;
+  const moe::PeerParts q = moe::peer_window_parts(c->win, world, c->win_hidden);
+  set_peer_parts(c, rank, c->win);
+  c->pa.seq = q.seq;
+  c->pa.zseq = q.zseq;
+  c->pa.err = q.err;
   c->pa.world = world;
   c->pa.rank = rank;
 }
@@ -611,11 +630,7 @@ int moe_ctx_open_peers(moe_ctx* c, int world, int rank, const void* handles) {
     void* p = nullptr;
     CU(cudaIpcOpenMemHandle(&p, h, cudaIpcMemLazyEnablePeerAccess));
     c->ipc_opened.push_back(p);
-    float* inbox;
-    unsigned* flags;
-    moe::peer_window_parts(p, world, c->win_hidden, &inbox, &flags, nullptr, nullptr);
-    c->pa.inbox[r] = inbox;
-    c->pa.flags[r] = flags;
+    set_peer_parts(c, r, p);
   }
   c->world = world;
   c->rank = rank;
@@ -649,11 +664,7 @@ int moe_ctx_link_peers(moe_ctx* const* ctxs, int world, int max_hidden) {
     set_own_parts(c, world, r);
     for (int q = 0; q < world; ++q) {
       if (q == r) continue;
-      float* inbox;
-      unsigned* flags;
-      moe::peer_window_parts(ctxs[q]->win, world, c->win_hidden, &inbox, &flags, nullptr, nullptr);
-      c->pa.inbox[q] = inbox;
-      c->pa.flags[q] = flags;
+      set_peer_parts(c, q, ctxs[q]->win);
     }
     c->world = world;
     c->rank = r;
@@ -741,7 +752,7 @@ static int weights_create(moe_ctx* c, const moe_shape* shape, int dtype,
   w->plan = moe::plan_decode(w->dims(), c->sm_count);
   {
     const char* env = getenv("MOE_B200_RW");
-    w->rw_enabled = w->plan.ok && !c->ep() && L >= 2 && E <= 8 &&
+    w->rw_enabled = w->plan.ok && (!c->ep() || c->peers) && L >= 2 && E <= 8 &&
                     (size_t)E * shape->hidden_dim * 4 <= 200 * 1024 && !(env && env[0] == '0');
     if (w->rw_enabled) {
       w->rw_mem.resize(L - 1);
@@ -1252,7 +1263,7 @@ int moe_forward_launches(moe_weights* w, int n_tok) {
   const bool ep = w->ctx->ep();
   if (use_stack(w, n_tok)) return 1;
   if (use_decode(w, n_tok, nullptr))  // experts + reduce (+ NCCL all-reduce + residual)
-    return 1 + L * (ep && !(w->ctx->peers && w->d() <= w->ctx->win_hidden) ? 3 : 2);
+    return 1 + L * (ep && !peer_ok(w) ? 3 : 2);
   // per layer: [permute, gather, up, down] or [up, down], combine, (+add for EP),
   // and the next layer's router
   const int experts =

@@ -29,6 +29,7 @@
 //    l+1 is computed redundantly by every CTA from per-CTA router partials,
 //    so the producer warps start streaming layer l+1 without another launch.
 #include <algorithm>
+#include <cstdlib>
 
 #include "../../include/moe_b200.h"
 #include "common.cuh"
@@ -381,6 +382,19 @@ __device__ __forceinline__ unsigned ld_acquire_sys(const unsigned* p) {
   return v;
 }
 
+// Bounded wait for a peer's flag to reach `target` (sequence numbers compare
+// modulo 2^32): a rank that never arrives sets *err instead of hanging.
+__device__ __forceinline__ void peer_wait(const unsigned* f, unsigned target, unsigned* err) {
+  unsigned spins = 0;
+  while ((int)(ld_acquire_sys(f) - target) < 0) {
+    if (++spins > (1u << 22)) {
+      atomicExch(err, 1u);
+      break;
+    }
+    if (spins > 64) __nanosleep(128);
+  }
+}
+
 __global__ void __launch_bounds__(256) reduce_exchange_kernel(
     const float* __restrict__ ypart, int nparts, const float* x, float* x_out, int d,
     const float* __restrict__ next_router, int E, int k, float* rpart, unsigned* counter,
@@ -391,7 +405,7 @@ __global__ void __launch_bounds__(256) reduce_exchange_kernel(
   __shared__ int s_last;
   const int tid = threadIdx.x, lane = tid & 31;
   const int warp = warp_uniform(tid >> 5);
-  const int b = blockIdx.x, nblk = gridDim.x;
+  const int b = blockIdx.x;
   griddep_wait();
   const int i = b * 32 + lane;
   float s = 0.f;
@@ -410,11 +424,11 @@ __global__ void __launch_bounds__(256) reduce_exchange_kernel(
       for (int r = 0; r < pa.world; ++r) pa.inbox[r][(par * pa.world + pa.rank) * d + i] = tot;
     __threadfence_system();
     __syncwarp();
-    if (lane < pa.world) st_release_sys(pa.flags[lane] + (size_t)pa.rank * nblk + b, seq);
+    if (lane < pa.world) st_release_sys(pa.flags[lane] + (size_t)pa.rank * kPeerSlots + b, seq);
     // wait for every rank's slice of this block (bounded: a missing peer is
     // reported through pa.err instead of hanging the GPU)
     if (lane < pa.world) {
-      const unsigned* f = pa.flags[pa.rank] + (size_t)lane * nblk + b;
+      const unsigned* f = pa.flags[pa.rank] + (size_t)lane * kPeerSlots + b;
       unsigned spins = 0;
       while ((int)(ld_acquire_sys(f) - seq) < 0) {
         if (++spins > (1u << 22)) {
@@ -478,6 +492,8 @@ struct StackArgs {
   unsigned* gbar;                    // grid barrier counter (0 at launch)
   unsigned long long* trace;         // optional [L][G][16] clock64 stamps
   const float* const* rw;            // [L] R_{l+1} W2 per local expert [f][E] (nullptr: off)
+  PeerArgs pa;                       // peer windows (peer != 0)
+  int peer;
   int L, d, f, E, k;
   int row_bytes, rps, stages, stage_bytes;
 };
@@ -616,6 +632,12 @@ __global__ void __launch_bounds__(kMaxConsWarps * 32 + 32, 1)
     a.trace[(size_t)c * 16 + 13] = globaltimer();
     a.trace[(size_t)c * 16 + 0] = clock64();
   }
+  // multi-GPU: every rank runs this kernel; slot c's exchange counter and the
+  // router-partial counter advance by one per layer on all ranks alike
+  const bool peer = a.peer != 0;
+  const unsigned seq0 = peer ? a.pa.seq[c] : 0u;
+  const unsigned zseq0 = peer ? *a.pa.zseq : 0u;
+  const int NR = peer ? a.pa.world : 1, rk = peer ? a.pa.rank : 0;
   // routing of layer 0: the router GEMV itself, redundantly in every CTA
   for (int e = tid; e < E; e += ncons) s_so[e] = a.slot_of[e];
   for (int e = warp; e < E; e += ncw) {
@@ -673,7 +695,7 @@ __global__ void __launch_bounds__(kMaxConsWarps * 32 + 32, 1)
       if (warp == 0) {
 #pragma unroll
         for (int e = 0; e < kZMax; ++e) {
-          if (lane == e && e < E) a.rpart[(size_t)e * G + c] = zreg[e] + xt[e];
+          if (lane == e && e < E) a.rpart[(size_t)e * G + c] = zreg[e] + (rk == 0 ? xt[e] : 0.f);
           zreg[e] = 0.f;
           xt[e] = 0.f;
         }
@@ -682,7 +704,7 @@ __global__ void __launch_bounds__(kMaxConsWarps * 32 + 32, 1)
       const float* rn = a.router + (size_t)(l + 1) * E * d;
       float v[NV * VEC];
 #pragma unroll
-      for (int i = 0; i < NV * VEC; ++i) v[i] = c == 0 ? yacc[i] + xr[i] : yacc[i];
+      for (int i = 0; i < NV * VEC; ++i) v[i] = (c == 0 && rk == 0) ? yacc[i] + xr[i] : yacc[i];
       for (int e0 = 0; e0 < E; e0 += 8) {
         float part[8];
 #pragma unroll
@@ -731,6 +753,28 @@ __global__ void __launch_bounds__(kMaxConsWarps * 32 + 32, 1)
       }
       if (tr && tid == 0) tr[8] = clock64();
       named_bar_sync(2, ncons);
+      if (peer) {
+        // this rank's router partial -> every rank (CTA 0 pushes), then the
+        // rank-ordered sum of all ranks' partials, identical everywhere
+        const unsigned zs = zseq0 + (unsigned)l + 1u;
+        const int zp = (int)(zs & 1u);
+        if (c == 0) {
+          for (int e = tid; e < E; e += ncons)
+            for (int r = 0; r < NR; ++r)
+              a.pa.zbox[r][((size_t)zp * NR + rk) * kMaxExperts + e] = logits[e];
+          __threadfence_system();
+          named_bar_sync(2, ncons);
+          if (tid < NR) st_release_sys(a.pa.zflags[tid] + rk, zs);
+        }
+        if (tid < NR) peer_wait(a.pa.zflags[rk] + tid, zs, a.pa.err);
+        named_bar_sync(2, ncons);
+        for (int e = tid; e < E; e += ncons) {
+          float t = 0.f;
+          for (int r = 0; r < NR; ++r) t += __ldcv(a.pa.zbox[rk] + ((size_t)zp * NR + r) * kMaxExperts + e);
+          logits[e] = t;
+        }
+        named_bar_sync(2, ncons);
+      }
       if (tr && tid == 0) tr[9] = clock64();
       if (warp == 0) commit_route(l + 1);
       if (tr && tid == 0) tr[10] = clock64();
@@ -742,6 +786,54 @@ __global__ void __launch_bounds__(kMaxConsWarps * 32 + 32, 1)
     // ---- C: this CTA's column chunk of x_{l+1} = x_l + sum_c ypart_c ----
     const bool next_xt = use_rw && l + 2 < a.L;
     const float* r2 = next_xt ? a.router + (size_t)(l + 2) * E * d : nullptr;
+    if (peer) {
+      // multi-GPU: the chunk of this rank's delta goes to every rank, then
+      // x_{l+1} = x_l + sum over ranks (rank order) — bit-identical everywhere
+      const unsigned sq = seq0 + (unsigned)l + 1u;
+      const size_t par = sq & 1u;
+      for (int base = cc0; base < cc1; base += 32) {
+        const int col = base + lane;
+        const bool valid = col < cc1;
+        const float s = valid ? strided_sum(a.ypart + col, warp, G, ncw, (size_t)d) : 0.f;
+        red[warp * 32 + lane] = s;
+        named_bar_sync(2, ncons);
+        if (warp == 0 && valid) {
+          float tot = 0.f;
+          for (int w = 0; w < ncw; ++w) tot += red[w * 32 + lane];
+          for (int r = 0; r < NR; ++r) a.pa.inbox[r][(par * NR + rk) * d + col] = tot;
+        }
+        named_bar_sync(2, ncons);
+      }
+      __threadfence_system();
+      named_bar_sync(2, ncons);
+      if (tid < NR) {
+        st_release_sys(a.pa.flags[tid] + (size_t)rk * kPeerSlots + c, sq);
+        peer_wait(a.pa.flags[rk] + (size_t)tid * kPeerSlots + c, sq, a.pa.err);
+      }
+      named_bar_sync(2, ncons);
+      if (warp == 0) {
+        for (int base = cc0; base < cc1; base += 32) {
+          const int col = base + lane;
+          const bool valid = col < cc1;
+          float xo = 0.f;
+          if (valid) {
+            float all = 0.f;
+            const float* in = a.pa.inbox[rk] + par * NR * d + col;
+            for (int r = 0; r < NR; ++r) all += __ldcv(in + (size_t)r * d);
+            xo = __ldcg(&xl[col]) + all;
+            xn[col] = xo;
+          }
+          if (next_xt) {
+#pragma unroll
+            for (int e = 0; e < kZMax; ++e) {
+              const float rv = (valid && e < E) ? __ldg(r2 + (size_t)e * d + col) : 0.f;
+              xt[e] += warp_sum(rv * xo);
+            }
+          }
+        }
+      }
+      named_bar_sync(2, ncons);
+    } else
     for (int base = cc0; base < cc1; base += 32) {
       const int col = base + lane;
       const bool valid = col < cc1;
@@ -779,6 +871,10 @@ __global__ void __launch_bounds__(kMaxConsWarps * 32 + 32, 1)
       if (more) a.trace[((size_t)(l + 1) * G + c) * 16 + 0] = tr[3];
     }
   }
+  if (peer && tid == 0) {
+    a.pa.seq[c] = seq0 + (unsigned)a.L;
+    if (c == 0) *a.pa.zseq = zseq0 + (unsigned)(a.L - 1);
+  }
 }
 
 // ---------------------------------------------------------------------------
@@ -808,6 +904,10 @@ DecodePlan plan_decode(const Dims& dm, int sm_count) {
   if (p.stages < 2) return p;
   p.smem = p.stages * stage + 2 * p.stages * 8;
   p.grid = sm_count;
+  // testing hook: fewer CTAs, so that several linked ranks' persistent kernels
+  // fit one GPU side by side (tests/test_gpu_ep_peers.py)
+  if (const char* g = getenv("MOE_B200_STACK_GRID"))
+    if (atoi(g) > 0) p.grid = std::min(sm_count, atoi(g));
   p.ok = true;
   return p;
 }
@@ -888,8 +988,10 @@ cudaError_t launch_decode_experts(const DecodePlan& p, const LayerWeights& lw, c
 cudaError_t launch_decode_stack(const DecodePlan& p, const StackDesc& sd, const Dims& dm,
                                 float* x, float* xbuf, float* ypart, float* rpart,
                                 int32_t* ids_out, float* gates_out, unsigned* gbar,
-                                cudaStream_t s) {
+                                cudaStream_t s, const PeerArgs* pa) {
   StackArgs a;
+  a.peer = pa != nullptr && pa->world > 1;
+  if (pa) a.pa = *pa;
   a.layer_experts = sd.layer_experts;
   a.slot_of = sd.slot_of;
   a.expert_stride = sd.expert_stride;
@@ -936,21 +1038,26 @@ cudaError_t launch_reduce_residual(const float* ypart, int nparts, const float* 
 }
 
 size_t peer_window_bytes(int world, int max_hidden) {
-  const size_t nblk = (size_t)(max_hidden + 31) / 32;
-  return 2 * (size_t)world * max_hidden * 4 + (size_t)world * nblk * 4 + nblk * 4 + 64;
+  return 2 * (size_t)world * max_hidden * 4 + (size_t)world * kPeerSlots * 4 +
+         2 * (size_t)world * kMaxExperts * 4 + 64 + kPeerSlots * 4 + 64;
 }
 
-void peer_window_parts(void* base, int world, int max_hidden, float** inbox, unsigned** flags,
-                       unsigned** seq, unsigned** err) {
-  const size_t nblk = (size_t)(max_hidden + 31) / 32;
+PeerParts peer_window_parts(void* base, int world, int max_hidden) {
+  PeerParts q;
   char* p = static_cast<char*>(base);
-  *inbox = reinterpret_cast<float*>(p);
+  q.inbox = reinterpret_cast<float*>(p);
   p += 2 * (size_t)world * max_hidden * 4;
-  *flags = reinterpret_cast<unsigned*>(p);
-  p += (size_t)world * nblk * 4;
-  if (seq) *seq = reinterpret_cast<unsigned*>(p);
-  p += nblk * 4;
-  if (err) *err = reinterpret_cast<unsigned*>(p);
+  q.flags = reinterpret_cast<unsigned*>(p);
+  p += (size_t)world * kPeerSlots * 4;
+  q.zbox = reinterpret_cast<float*>(p);
+  p += 2 * (size_t)world * kMaxExperts * 4;
+  q.zflags = reinterpret_cast<unsigned*>(p);
+  p += 64;
+  q.seq = reinterpret_cast<unsigned*>(p);
+  p += kPeerSlots * 4;
+  q.zseq = reinterpret_cast<unsigned*>(p);
+  q.err = q.zseq + 1;
+  return q;
 }
 
 cudaError_t launch_reduce_exchange(const float* ypart, int nparts, const float* x, float* x_out,

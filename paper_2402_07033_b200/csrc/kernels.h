@@ -67,10 +67,14 @@ struct StackDesc {
 // rw[slot][r][e] = sum_i R_next[e][i] * W2T[slot][r][i]   (fp32; E <= 8)
 cudaError_t launch_router_projection(const void* layer_experts, int n_local, const Dims& dm,
                                      const float* router_next, float* rw, cudaStream_t s);
+struct PeerArgs;
+// pa (optional): expert/tensor-parallel ranks linked by peer windows; each
+// layer's x_{l+1} and next-layer router logits are then summed over the ranks
+// inside the kernel (one launch per token on every GPU).
 cudaError_t launch_decode_stack(const DecodePlan& p, const StackDesc& sd, const Dims& dm,
                                 float* x, float* xbuf, float* ypart, float* rpart,
                                 int32_t* ids_out, float* gates_out, unsigned* gbar,
-                                cudaStream_t s);
+                                cudaStream_t s, const PeerArgs* pa = nullptr);
 // x_out = x + sum_p ypart[p]; optionally the next layer's router + top-k
 // (deterministic fixed-order partial sums, last-block-done).
 cudaError_t launch_reduce_residual(const float* ypart, int nparts, const float* x, float* x_out,
@@ -81,20 +85,35 @@ int reduce_blocks(const Dims& dm);
 
 // ---- expert-parallel combine over peer memory (NVLink P2P / IPC) -----------
 // Every rank owns one "exchange window" in its HBM:
-//   inbox [2 parity][world][d] fp32 | flags [world][nblk] u32 | seq [nblk] u32 | err u32
-// and holds device pointers to every peer's window (its own included).
+//   inbox [2 parity][world][d] fp32 | flags [world][kPeerSlots] u32 |
+//   zbox [2 parity][world][kMaxExperts] fp32 | zflags [world] u32 |
+//   seq [kPeerSlots] u32 | zseq u32 | err u32
+// and holds device pointers to every peer's window (its own included).  A
+// "slot" is one exchanging block: a 32-column block of reduce_exchange_kernel
+// or one CTA of the persistent stack kernel; its sequence counter advances by
+// one per exchange on every rank alike, and selects the inbox parity.
 constexpr int kMaxRanks = 8;
+constexpr int kPeerSlots = 512;
 struct PeerArgs {
   float* inbox[kMaxRanks];     // rank r's inbox base
   unsigned* flags[kMaxRanks];  // rank r's flags base
-  unsigned* seq;               // own per-block exchange counters
+  float* zbox[kMaxRanks];      // rank r's router-partial inbox (stack kernel)
+  unsigned* zflags[kMaxRanks];
+  unsigned* seq;               // own per-slot exchange counters
+  unsigned* zseq;              // own router-partial exchange counter
   unsigned* err;               // own: set when a peer never arrives (bounded wait)
   int world, rank;
 };
+struct PeerParts {
+  float* inbox;
+  unsigned* flags;
+  float* zbox;
+  unsigned* zflags;
+  unsigned *seq, *zseq, *err;
+};
 size_t peer_window_bytes(int world, int max_hidden);
 // Carve a window allocation into its parts (same layout on every rank).
-void peer_window_parts(void* base, int world, int max_hidden, float** inbox, unsigned** flags,
-                       unsigned** seq, unsigned** err);
+PeerParts peer_window_parts(void* base, int world, int max_hidden);
 // x_out = x + sum_{r in rank order} delta_r, where delta_r = this layer's
 // fixed-order sum of rank r's per-CTA partials.  Each block reduces 32 hidden
 // columns, stores them into every peer's inbox (P2P stores), releases a

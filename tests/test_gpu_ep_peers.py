@@ -42,15 +42,19 @@ def gpu():
     torch.cuda.init()
 
 
+@pytest.mark.parametrize("kernel", ["layer", "stack"])
 @pytest.mark.parametrize("mode", ["ep", "tp"])
 @pytest.mark.parametrize("world,shape,dtype", [
     (2, (4, 8, 2, 4096, 14336, 2), M.DTYPE_BF16),
     (4, (3, 8, 2, 4096, 14336, 2), M.DTYPE_BF16),
     (2, (3, 8, 2, 512, 1792, 4), M.DTYPE_F32),
 ])
-def test_peer_combine_matches_unsharded(gpu, mode, world, shape, dtype):
+def test_peer_combine_matches_unsharded(gpu, monkeypatch, kernel, mode, world, shape, dtype):
     """mode ep: experts sharded by the popularity shard map; mode tp: every
-    expert's ffn rows split over the ranks (tensor parallelism)."""
+    expert's ffn rows split over the ranks (tensor parallelism).  kernel
+    layer: per-layer streaming kernel + reduce_exchange; kernel stack: the
+    persistent one-launch-per-token kernel with the exchange inside (each
+    rank's grid shrunk to SMs/world so the W kernels fit one GPU together)."""
     L, E, k, d = shape[0], shape[1], shape[2], shape[3]
     s = M.Shape(*shape)
     base = M.Ctx(0)
@@ -69,6 +73,10 @@ def test_peer_combine_matches_unsharded(gpu, mode, world, shape, dtype):
 
     ctxs = [M.Ctx(0) for _ in range(world)]
     M.Ctx.link_peers(ctxs, d)
+    if kernel == "layer":
+        monkeypatch.setenv("MOE_B200_STACK", "0")
+    else:
+        monkeypatch.setenv("MOE_B200_STACK_GRID", str(ctxs[0].sm_count // world))
     if mode == "ep":
         owner = _bench().shard_map(L, E, world)
         ws = [M.Weights(c, s, dtype, owner=owner) for c in ctxs]
@@ -76,7 +84,7 @@ def test_peer_combine_matches_unsharded(gpu, mode, world, shape, dtype):
         ws = [M.Weights(c, s, dtype, tp=True) for c in ctxs]
     for w in ws:
         w.random(11)
-        assert w.forward_launches(1) == 1 + 2 * L  # per-layer path (stack kernel is single-GPU)
+        assert w.forward_launches(1) == (1 + 2 * L if kernel == "layer" else 1)
     torch.cuda.synchronize()
     for rep in range(2):
         for t in range(3):
