@@ -50,6 +50,8 @@ WORKLOAD_NAME = {
     "tiny": "tiny MoE layer d=512 f=1792 fp32 decode, batch 1 (BASELINE configs[0])",
 }
 METRIC = "Mixtral-8x7B MoE decode tok/s (batch 1)"
+PREFILL_METRIC = "Mixtral-8x7B MoE layer prefill tok/s (512 tokens, 1 layer)"
+PREFILL_WORKLOAD = "Mixtral-8x7B-shaped MoE layer prefill, 512 tokens (BASELINE configs[2])"
 
 
 def env_int(name, default):
@@ -374,6 +376,33 @@ def run_prefill(args):
         torch.cuda.synchronize()
     ms = e0.elapsed_time(e1) / args.steps
     active = len(set(ids.cpu().numpy().ravel().tolist()))
+    # e2e through the host-buffer entry point: fp64 host tokens -> H2D ->
+    # router + grouped GEMM + combine -> D2H of outputs and routing
+    rs = np.random.RandomState(args.seed + 2)
+    host = [rs.randn(n, d) for _ in range(3)]
+    w.forward_host(host[0])
+    ee0, ee1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    n_e2e = max(3, min(args.steps, 30))
+    torch.cuda.synchronize()
+    ee0.record(stream)
+    for i in range(n_e2e):
+        w.forward_host(host[1 + i % 2])
+    ee1.record(stream)
+    torch.cuda.synchronize()
+    e2e_ms = ee0.elapsed_time(ee1) / n_e2e
+    e2e = {"value": round(n / (e2e_ms * 1e-3), 1), "unit": "tok/s", "h2d_bytes_per_step": n * d * 4,
+           "d2h_bytes_per_step": n * d * 4 + n * k * 8, "ms_per_step": round(e2e_ms, 4)}
+    cpu = None
+    if not args.no_cpu_baseline:
+        import oracle as O
+
+        if O.reference_available():
+            toks = rs.randn(args.cpu_tokens // 3 or 1, d)
+            ref, shape, wr = _mixtral_layer_for_reference(d, f, E, k, toks)
+            _, secs = ref.time_forward(shape, wr, toks)
+            cpu = {"value": round(len(toks) / secs, 4), "unit": "tok/s", "cores": 1, "kind": "reference",
+                   "sample": f"{len(toks)} distinct tokens x 1 Mixtral-shaped layer (reference model_forward, "
+                             f"fp64, token-major: cost linear in tokens)", "host_cores": os.cpu_count()}
     bytes_ = active * 3 * d * f * 2 + E * d * 4 + n * d * 4 * 2
     flops = 2.0 * 3 * d * f * n * k
     peak_bw, src = load_peaks()
@@ -382,12 +411,13 @@ def run_prefill(args):
     bw = bytes_ / (ms * 1e-3) / 1e9
     tf = flops / (ms * 1e-3) / 1e12
     print(json.dumps({
-        "metric": "Mixtral-8x7B MoE layer prefill tok/s (512 tokens, 1 layer)", "value": round(n / (ms * 1e-3), 1),
+        "metric": PREFILL_METRIC, "value": round(n / (ms * 1e-3), 1),
         "unit": "tok/s", "n_gpus": 1, "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms, 4),
         "higher_is_better": True, "dtype": "bf16", "data": "synthetic",
-        "config": {"workload": "Mixtral-8x7B-shaped MoE layer prefill, 512 tokens (BASELINE configs[2])",
+        "config": {"workload": PREFILL_WORKLOAD,
                    "path": "tcgen05/TMEM grouped GEMM (swap-AB), TMA SW128", "active_experts": active},
-        "gpu_launches": w.forward_launches(n) * args.steps, "clocks": clk.summary(),
+        "gpu_launches": w.forward_launches(n) * args.steps, "clocks": clk.summary(), "e2e": e2e,
+        "cpu_baseline": cpu,
         "roofline": {"bound": "hbm", "achieved": round(bw, 1), "peak": peak_bw, "unit": "GB/s",
                      "frac": round(bw / peak_bw, 4), "traffic": None, "alg_bytes_per_step": bytes_,
                      "tensor_tflops": round(tf, 1), "tensor_frac": round(tf / peaks["bf16_tflops"], 4),
@@ -400,15 +430,18 @@ def run_prefill(args):
 def _mixtral_layer_for_reference(d, f, E, k, token, seed=0):
     """fp64 weights of one Mixtral-shaped layer for the reference's CPU path:
     a random router and random N(0,1/sqrt(d)) weights for the experts the
-    token routes to (the others are never touched by model_forward)."""
+    token(s) route to (the others are never touched by model_forward)."""
     import oracle as O
 
     ref = O.Reference()
     shape = O.Shape(1, E, k, d, f, 2)
     rs = np.random.RandomState(seed)
     router = rs.randn(E, d) / np.sqrt(d)
-    ids, _ = ref.gate_topk(router, token, k)
-    w = O.Weights(shape, experts=[int(e) for e in ids])
+    routed = set()
+    for t in np.atleast_2d(token):
+        routed.update(int(e) for e in ref.gate_topk(router, t, k)[0])
+    ids = sorted(routed)
+    w = O.Weights(shape, experts=ids)
     for e in ids:
         wi, wg, wo = w.expert(0, int(e))
         for m in (wi, wg, wo):
@@ -446,7 +479,8 @@ def run_reference(args):
         return
     import oracle as O
 
-    L, E, k, d, f, dt = CONFIGS[args.config]
+    prefill = args.config == "prefill512"
+    L, E, k, d, f, dt = CONFIGS["layer" if prefill else args.config]
     if args.layers:
         L = args.layers
     if not O.reference_available():
@@ -454,14 +488,16 @@ def run_reference(args):
         return
     threads = max(1, min(os.cpu_count() or 1, args.ref_threads or (os.cpu_count() or 1)))
     rs = np.random.RandomState(args.seed + 1)
-    token = rs.randn(d)
-    ref, shape, w = _mixtral_layer_for_reference(d, f, E, k, token)
     # each step: every thread pushes one token through one layer of ONE shared
-    # reference model (model_forward is reentrant);
-    # tok/s for the L-layer stack = threads / (t*L)
+    # reference model (model_forward is reentrant); decode uses
+    # one token everywhere, prefill a distinct token per thread (a bounded
+    # sample of the 512-token batch: the reference is token-major, its cost
+    # is linear in tokens).  tok/s for an L-layer stack = threads / (t*L).
+    token = rs.randn(threads if prefill else 1, d)
+    ref, shape, w = _mixtral_layer_for_reference(d, f, E, k, token)
     handle = ref.model_create(shape, w)
     del w
-    toks = [np.repeat(token[None], 1, axis=0) for _ in range(threads)]
+    toks = [token[(i if prefill else 0):(i if prefill else 0) + 1] for i in range(threads)]
 
     def one_step():
         ts = [threading.Thread(target=ref.model_forward_timed, args=(handle, toks[i]))
@@ -479,6 +515,19 @@ def run_reference(args):
     ref.model_destroy(handle)
     secs = sum(times)
     tok_s = threads * args.steps / (secs * L)
+    if prefill:
+        line = {"impl": "reference", "metric": PREFILL_METRIC, "value": round(tok_s, 5), "unit": "tok/s",
+                "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+                "ms_per_step": round(secs / args.steps * 1e3, 3), "higher_is_better": True,
+                "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+                "config": {"workload": PREFILL_WORKLOAD, "parallelism": f"cpu x{threads} threads"},
+                "cpu_baseline": {"value": round(tok_s, 5), "unit": "tok/s", "cores": threads, "kind": "reference",
+                                 "sample": f"{threads} threads x 1 distinct token x 1 Mixtral-shaped layer per step "
+                                           f"(reference model_forward, fp64; token-major, linear in tokens)"},
+                "e2e": {"value": round(tok_s, 5), "unit": "tok/s", "h2d_bytes_per_step": 0,
+                        "d2h_bytes_per_step": 0}}
+        print(json.dumps(line), flush=True)
+        return
     line = {"impl": "reference", "metric": METRIC, "value": round(tok_s, 5), "unit": "tok/s",
             "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": round(1000.0 / tok_s, 3), "higher_is_better": True, "scaling": "strong",

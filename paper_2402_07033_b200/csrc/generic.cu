@@ -324,35 +324,65 @@ __global__ void __launch_bounds__(256) combine_kernel(const float* x, const floa
   x_out[(size_t)t * d + i] = (x ? x[(size_t)t * d + i] : 0.f) + c;
 }
 
-// float4 variant (d % 4 == 0): same per-element arithmetic order
+// float4 variant (d % 4 == 0): same per-element arithmetic order.  One block
+// per token: the slot gates / split counts are read once into smem, and each
+// thread keeps several float4 columns' loads in flight (the per-pair split
+// lookup used to be a dependent load chain per element).
+constexpr int kCombineCols = 4;  // float4 columns per thread per pass
 __global__ void __launch_bounds__(256) combine4_kernel(const float* x, const float* __restrict__ y,
                                                        const float* __restrict__ gates, int k, int d,
                                                        float* x_out, int nsplit, long long sstride,
                                                        const int32_t* __restrict__ ids,
                                                        const int32_t* __restrict__ split_of) {
+  __shared__ float s_g[32];
+  __shared__ int s_ns[32];
   griddep_wait();
   griddep_launch_dependents();
-  const int i4 = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i4 * 4 >= d) return;
-  const int t = blockIdx.y;
-  float4 c = make_float4(0.f, 0.f, 0.f, 0.f);
-  for (int j = 0; j < k; ++j) {
-    const float g = gates ? gates[(size_t)t * k + j] : 1.0f;
-    const int ns = split_of ? split_of[ids[(size_t)t * k + j]] : nsplit;
-    for (int sp = 0; sp < ns; ++sp) {
-      const float4 v = __ldg(reinterpret_cast<const float4*>(y + sp * sstride + ((size_t)t * k + j) * d) + i4);
-      c.x += g * v.x;
-      c.y += g * v.y;
-      c.z += g * v.z;
-      c.w += g * v.w;
+  const int t = blockIdx.x;
+  if (threadIdx.x < k) {
+    const int j = threadIdx.x;
+    s_g[j] = gates ? gates[(size_t)t * k + j] : 1.0f;
+    s_ns[j] = split_of ? split_of[ids[(size_t)t * k + j]] : nsplit;
+  }
+  __syncthreads();
+  const int n4 = d / 4;
+  const float4* y4 = reinterpret_cast<const float4*>(y);
+  for (int c0 = threadIdx.x; c0 < n4; c0 += blockDim.x * kCombineCols) {
+    float4 acc[kCombineCols];
+#pragma unroll
+    for (int u = 0; u < kCombineCols; ++u) acc[u] = make_float4(0.f, 0.f, 0.f, 0.f);
+    for (int j = 0; j < k; ++j) {
+      const float g = s_g[j];
+      const int ns = s_ns[j];
+      for (int sp = 0; sp < ns; ++sp) {
+        const float4* row = y4 + (sp * sstride + ((size_t)t * k + j) * d) / 4;
+        float4 v[kCombineCols];
+#pragma unroll
+        for (int u = 0; u < kCombineCols; ++u) {
+          const int i4 = c0 + u * blockDim.x;
+          v[u] = i4 < n4 ? __ldg(row + i4) : make_float4(0.f, 0.f, 0.f, 0.f);
+        }
+#pragma unroll
+        for (int u = 0; u < kCombineCols; ++u) {
+          acc[u].x += g * v[u].x;
+          acc[u].y += g * v[u].y;
+          acc[u].z += g * v[u].z;
+          acc[u].w += g * v[u].w;
+        }
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < kCombineCols; ++u) {
+      const int i4 = c0 + u * blockDim.x;
+      if (i4 >= n4) continue;
+      float4 o = acc[u];
+      if (x) {
+        const float4 xv = reinterpret_cast<const float4*>(x + (size_t)t * d)[i4];
+        o = make_float4(xv.x + o.x, xv.y + o.y, xv.z + o.z, xv.w + o.w);
+      }
+      reinterpret_cast<float4*>(x_out + (size_t)t * d)[i4] = o;
     }
   }
-  float4 o = c;
-  if (x) {
-    const float4 xv = reinterpret_cast<const float4*>(x + (size_t)t * d)[i4];
-    o = make_float4(xv.x + c.x, xv.y + c.y, xv.z + c.z, xv.w + c.w);
-  }
-  reinterpret_cast<float4*>(x_out + (size_t)t * d)[i4] = o;
 }
 
 cudaError_t launch_combine(const float* x, const float* y, const float* gates, int n_tok,
@@ -360,8 +390,8 @@ cudaError_t launch_combine(const float* x, const float* y, const float* gates, i
                            const int32_t* ids, const int32_t* split_of) {
   if (n_tok <= 0) return cudaSuccess;
   cudaLaunchAttribute attr[1];
-  if (dm.d % 4 == 0) {
-    cudaLaunchConfig_t cfg = make_cfg(dim3((dm.d / 4 + 255) / 256, n_tok), dim3(256), s, pdl, attr);
+  if (dm.d % 4 == 0 && dm.k <= 32) {
+    cudaLaunchConfig_t cfg = make_cfg(dim3(n_tok), dim3(256), s, pdl, attr);
     const long long sstride = (long long)n_tok * dm.k * dm.d;
     return cudaLaunchKernelEx(&cfg, combine4_kernel, x, y, gates, dm.k, dm.d, x_out, nsplit,
                               sstride, ids, split_of);

@@ -51,6 +51,18 @@ __device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, i
       "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(smem_u32(bar))
       : "memory");
 }
+// Same with an L2 cache-policy hint: the expert weights are streamed once per
+// token chunk, so they are loaded evict_first and do not push the reused
+// tensors (X and H tiles, the fp32 Y partials read back by the combine) out
+// of the 126 MB L2.
+__device__ __forceinline__ void tma_load_2d_hint(void* dst, const CUtensorMap* map, int c0, int c1,
+                                                 uint64_t* bar, uint64_t policy) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint"
+      " [%0], [%1, {%2, %3}], [%4], %5;" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(smem_u32(bar)), "l"(policy)
+      : "memory");
+}
 __device__ __forceinline__ void tma_prefetch_desc(const CUtensorMap* map) {
   asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(map)) : "memory");
 }
@@ -416,6 +428,7 @@ struct GroupedArgs {
   int trace_cap;  // tiles per CTA
   SparsityCounters sp;  // fused |silu(w_in x)| < thr counters (off: sp.counts == nullptr)
   int lag;              // schedule: expert i's down tiles follow expert i+lag's up tiles
+  int evict_first;      // weights loaded with an L2 evict_first hint
 };
 
 __device__ __forceinline__ void gp_stamp(const GroupedArgs& a, int i, int field,
@@ -555,6 +568,11 @@ __global__ void __launch_bounds__(PF_THREADS, 1)
       tma_prefetch_desc(&wmap_dn);
       tma_prefetch_desc(&xmap);
       tma_prefetch_desc(&hmap);
+      uint64_t wpol;
+      if (a.evict_first)
+        wpol = l2_evict_first_policy();
+      else
+        asm volatile("createpolicy.fractional.L2::evict_normal.b64 %0, 1.0;" : "=l"(wpol));
       uint32_t kc = 0;
       int qi = 0, ntile = 0;
       uint32_t qph = 0;
@@ -585,8 +603,8 @@ __global__ void __launch_bounds__(PF_THREADS, 1)
             mbar_wait(&empty[st], ((kc / GP_STAGES) & 1) ^ 1);
             uint8_t* sp = smem + st * GP_STAGE;
             mbar_arrive_expect_tx(&full[st], bytes);
-            tma_load_2d(sp, &wmap_up, kb * PF_BK, w1row, &full[st]);
-            tma_load_2d(sp + kA, &wmap_up, kb * PF_BK, w3row, &full[st]);
+            tma_load_2d_hint(sp, &wmap_up, kb * PF_BK, w1row, &full[st], wpol);
+            tma_load_2d_hint(sp + kA, &wmap_up, kb * PF_BK, w3row, &full[st], wpol);
             for (int b = 0; b < nboxes; ++b)
               tma_load_2d(sp + 2 * kA + b * kBox, &xmap, kb * PF_BK, srow + b * PF_BOXN, &full[st]);
           }
@@ -612,7 +630,8 @@ __global__ void __launch_bounds__(PF_THREADS, 1)
             // W2T rows [kb*64, +64) x hidden cols [d0, d0+256): 4 boxes of 64 cols
 #pragma unroll
             for (int q = 0; q < 4; ++q)
-              tma_load_2d(sp + q * (kA / 2), &wmap_dn, d0 + q * 64, w2row + kb * PF_BK, &full[st]);
+              tma_load_2d_hint(sp + q * (kA / 2), &wmap_dn, d0 + q * 64, w2row + kb * PF_BK, &full[st],
+                               wpol);
             for (int b = 0; b < nboxes; ++b)
               tma_load_2d(sp + 2 * kA + b * kBox, &hmap, kb * PF_BK, srow + b * PF_BOXN, &full[st]);
           }
@@ -911,6 +930,9 @@ cudaError_t launch_prefill_experts(const LayerWeights& lw, int n_local, const Di
     g.max_chunks = chunks;
     g.debug = getenv("MOE_B200_PF_DEBUG") ? atoi(getenv("MOE_B200_PF_DEBUG")) : 0;
     g.sp = sp;
+    // measured A/B (512 tokens): evict_first keeps H/Y in L2 (-33 MB DRAM,
+    // combine 11.5 -> 9.6 us) but slows the weight stream by ~5 us: off
+    g.evict_first = getenv("MOE_B200_PF_EVICT") ? atoi(getenv("MOE_B200_PF_EVICT")) : 0;
     // measured (tools/prof_prefill.py, Mixtral 512 tokens): interleaving
     // downs among ups is slower (lag 1/2/3: +33/+12/+24 us) than all ups
     // first, so the default lag puts every down after every up
