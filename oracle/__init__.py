@@ -259,6 +259,7 @@ class Reference(_Base):
         L.ref_shape_validate.argtypes = [C.c_void_p]
         L.ref_shape_preset.argtypes = [C.c_char_p, _i32p]
         L.ref_load_trace_jsonl.argtypes = [C.c_char_p, C.c_void_p, _i32p]
+        L.ref_fit_records.argtypes = [C.c_char_p, C.c_double, _dp]
 
     def _check(self, rc):
         if rc == 1:
@@ -267,6 +268,18 @@ class Reference(_Base):
             raise ValueError("ValidationError: " + self.lib.ref_last_error().decode())
         if rc:
             raise RuntimeError(self.lib.ref_last_error().decode())
+
+    def fit_records(self, path: str, nonexpert_ms: float = 2.0) -> dict:
+        """The reference's load_records_csv + CostModel fit (cost_model.cpp:57-156)."""
+        out = np.zeros(6)
+        rc = self.lib.ref_fit_records(path.encode(), nonexpert_ms, _p(out))
+        if rc not in (0, 100):
+            self._check(rc)
+        keys = ["weight_copy_ms", "activation_copy_ms", "fast_exec_ms", "slow_ms_per_token",
+                "slow_intercept_ms", "nonexpert_ms_per_step"]
+        d = dict(zip(keys, out.tolist()))
+        d["decode_assumption_check"] = rc == 0
+        return d
 
     def load_trace_jsonl(self, path: str, shape: Shape) -> int:
         """The reference's loader + validator (trace.cpp:110-141); returns the step count."""

@@ -13,6 +13,7 @@
 #include <string>
 #include <vector>
 
+#include "moe_orch/cost_model.hpp"
 #include "moe_orch/error.hpp"
 #include "moe_orch/model.hpp"
 #include "moe_orch/placement.hpp"
@@ -352,6 +353,24 @@ int ref_sparsity_histogram(const double* acts, int64_t n, const double* thr, int
                                       std::vector<double>(thr, thr + nthr));
     std::memcpy(out, f.data(), f.size() * 8);
     return 0;
+  } catch (...) {
+    return map_exc();
+  }
+}
+
+// load_records_csv + fit (cost_model.cpp:57-156): out[6] = weight_copy_ms,
+// activation_copy_ms, fast_exec_ms, slow_ms_per_token, slow_intercept_ms,
+// nonexpert_ms_per_step.
+int ref_fit_records(const char* path, double nonexpert_ms, double* out) {
+  try {
+    const CostModel m = fit(load_records_csv(std::string(path)), nonexpert_ms);
+    out[0] = m.weight_copy_ms;
+    out[1] = m.activation_copy_ms;
+    out[2] = m.fast_exec_ms;
+    out[3] = m.slow_ms_per_token;
+    out[4] = m.slow_intercept_ms;
+    out[5] = m.nonexpert_ms_per_step;
+    return m.decode_assumption_check() ? 0 : 100;  // 100: ok, but the paper's decode premise fails
   } catch (...) {
     return map_exc();
   }
