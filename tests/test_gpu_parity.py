@@ -528,3 +528,68 @@ def test_fused_sparsity_counters_match_reference_sink(ctx, monkeypatch):
     wt.close()
     wgn.close()
     w.close()
+
+
+def test_x22b_layer_decode_and_prefill_vs_oracle(ctx, orc):
+    """Config X shape (Mixtral-8x22B: d=6144, ffn=16384), bf16: batch-1 decode
+    through the streaming kernel, a 2-layer stack through the persistent
+    kernel (teacher-forced layer 1), and a 96-token prefill through the
+    tcgen05 grouped GEMM, each against the fp64 oracle on the device-held
+    weights."""
+    L, d, f = 2, 6144, 16384
+    w = M.Weights(ctx, M.Shape(L, 8, 2, d, f, 2), M.DTYPE_BF16)
+    w.random(7)
+    assert w.expert_path(1) == 1 and w.expert_path(96) == 3 and w.forward_launches(1) == 1
+    rs = np.random.RandomState(7)
+    x = f32(rs.randn(d))
+    # decode, layer 0
+    xd = torch.tensor(x[None], dtype=torch.float32, device="cuda")
+    idd = torch.zeros((1, 2), dtype=torch.int32, device="cuda")
+    gd = torch.zeros((1, 2), dtype=torch.float32, device="cuda")
+    xo = torch.empty_like(xd)
+    w.layer_forward(0, xd, xo, idd, gd)
+    torch.cuda.synchronize()
+    ids, g, delta, mg = oracle_layer(orc, w, 0, x, 2)
+    if mg > 1e-5:
+        assert list(idd.cpu().numpy()[0]) == list(ids)
+    err = normwise(xo.cpu().numpy()[0].astype(np.float64) - x, delta)
+    print(f"X decode normwise error {err:.3e}")
+    assert err < 1e-4
+    # persistent 2-layer stack; layer 1 teacher-forced on the device's x_1
+    xs = torch.tensor(x[None], dtype=torch.float32, device="cuda")
+    ids2 = torch.zeros((L, 1, 2), dtype=torch.int32, device="cuda")
+    g2 = torch.zeros((L, 1, 2), dtype=torch.float32, device="cuda")
+    w.forward(xs, ids2, g2)
+    torch.cuda.synchronize()
+    x1 = xo.cpu().numpy()[0].astype(np.float64)
+    ids1, _, delta1, mg1 = oracle_layer(orc, w, 1, f32(x1), 2)
+    if mg1 > 1e-5:
+        assert list(ids2.cpu().numpy()[1, 0]) == list(ids1)
+    err1 = normwise(xs.cpu().numpy()[0].astype(np.float64) - x1, delta1)
+    assert err1 < 1e-3, err1
+    # prefill, 96 tokens (tcgen05), sampled tokens vs oracle
+    n = 96
+    xp = f32(rs.randn(n, d))
+    xpd = torch.tensor(xp, dtype=torch.float32, device="cuda")
+    xpo = torch.empty_like(xpd)
+    idp = torch.zeros((n, 2), dtype=torch.int32, device="cuda")
+    gp = torch.zeros((n, 2), dtype=torch.float32, device="cuda")
+    w.layer_forward(0, xpd, xpo, idp, gp)
+    torch.cuda.synchronize()
+    out = xpo.cpu().numpy().astype(np.float64)
+    cache = {}
+    router = w.download_router(0)
+    worst = 0.0
+    for t in (0, 37, 95):
+        ids_t, g_t, logits = orc.gate_topk(router, xp[t], 2)
+        if margin(logits, 2) > 1e-5:
+            assert list(idp.cpu().numpy()[t]) == list(ids_t)
+        dl = np.zeros(d)
+        for e, ge in zip(idp.cpu().numpy()[t], gp.cpu().numpy()[t]):
+            if int(e) not in cache:
+                cache[int(e)] = w.download_expert(0, int(e))
+            dl += ge * orc.expert_ffn(*cache[int(e)], xp[t])
+        worst = max(worst, normwise(out[t] - xp[t], dl))
+    print(f"X prefill (tcgen05) normwise error {worst:.3e}")
+    assert worst < TOL_BF16
+    w.close()
