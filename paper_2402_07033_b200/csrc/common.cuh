@@ -165,23 +165,27 @@ __device__ __forceinline__ void warp_topk_softmax(const float* logits, int E, in
     // Fixed-trip, fully unrolled loops: the shuffles sit in provably
     // convergent code (no collective fallback) and issue back to back.
     const float v = lane < E ? logits[lane] : 0.f;
+    // branch-free predicate arithmetic: the 32 shuffles issue back to back
+    // (a short-circuit condition here compiled to 32 BSSY/BRA/BSYNC diamonds,
+    // ~1.5 us on the decode layer boundary)
     int rank = 0;
 #pragma unroll
     for (int e2 = 0; e2 < 32; ++e2) {
       const float o = __shfl_sync(MOE_FULL_MASK, v, e2);
-      rank += (e2 < E && (o > v || (o == v && e2 < lane))) ? 1 : 0;
+      rank += (int)((e2 < E) & ((o > v) | ((o == v) & (e2 < lane))));
     }
-    const bool sel = lane < E && rank < k;
+    const bool sel = (lane < E) & (rank < k);
     const unsigned m = __ballot_sync(MOE_FULL_MASK, sel);
     const int pos = __popc(m & ((1u << lane) - 1u));  // ascending-id slot
     float mx = sel ? v : -INFINITY;
 #pragma unroll
     for (int s = 16; s >= 1; s >>= 1) mx = fmaxf(mx, __shfl_xor_sync(MOE_FULL_MASK, mx, s));
     const float w = sel ? expf(v - mx) : 0.f;
-    // ascending-id sequential sum (unselected lanes add an exact 0)
+    // ascending-id sequential sum over the selected lanes only: the other
+    // lanes would add exact zeros, so this equals the full 0..31 sum bit for
+    // bit (m is warp-uniform: k iterations, convergent)
     float denom = 0.f;
-#pragma unroll
-    for (int e2 = 0; e2 < 32; ++e2) denom += __shfl_sync(MOE_FULL_MASK, w, e2);
+    for (unsigned mm = m; mm; mm &= mm - 1u) denom += __shfl_sync(MOE_FULL_MASK, w, __ffs(mm) - 1);
     if (sel) {
       ids[pos] = lane;
       gates[pos] = w / denom;
