@@ -10,6 +10,7 @@
 #include <map>
 #include <mutex>
 #include <string>
+#include <thread>
 #include <tuple>
 #include <vector>
 
@@ -457,6 +458,27 @@ int forward_graph(moe_weights* w, float* x, int32_t* ids, float* gates, cudaStre
   }
   CU(cudaGraphLaunch(it->second.exec, s));
   return MOE_OK;
+}
+
+// dst[i] = (To)src[i]; split over host threads for prefill-sized buffers (the
+// host-buffer API converts the reference's fp64 tokens; one thread would take
+// ~2 ms each way at 512 x 4096)
+template <typename To, typename From>
+void host_convert(To* dst, const From* src, size_t n) {
+  const size_t kMin = 1 << 18;
+  const unsigned hw = std::max(1u, std::thread::hardware_concurrency());
+  const unsigned nt = (unsigned)std::min<size_t>(std::min(hw, 16u), (n + kMin - 1) / kMin);
+  if (nt <= 1) {
+    for (size_t i = 0; i < n; ++i) dst[i] = (To)src[i];
+    return;
+  }
+  std::vector<std::thread> ts;
+  for (unsigned t = 0; t < nt; ++t)
+    ts.emplace_back([=] {
+      const size_t a = n * t / nt, b = n * (t + 1) / nt;
+      for (size_t i = a; i < b; ++i) dst[i] = (To)src[i];
+    });
+  for (auto& th : ts) th.join();
 }
 
 int host_pinned(moe_weights* w, size_t bytes, void** out) {
@@ -1120,7 +1142,7 @@ int moe_forward_host(moe_weights* w, const double* tokens, int n_tok, double* ou
   int32_t* hids = reinterpret_cast<int32_t*>(hx + nx);
   float* hg = reinterpret_cast<float*>(hids + nr);
   float* hpost = hg + nr;
-  for (size_t i = 0; i < nx; ++i) hx[i] = (float)tokens[i];
+  host_convert(hx, tokens, nx);
   float* dx = w->xin.as<float>();  // device copy of the tokens (in/out)
   int32_t* dids = w->ids.as<int32_t>();
   float* dg = w->gates.as<float>();
@@ -1140,7 +1162,7 @@ int moe_forward_host(moe_weights* w, const double* tokens, int n_tok, double* ou
   CU(cudaMemcpyAsync(hids, dids, nr * 4, cudaMemcpyDeviceToHost, s));
   CU(cudaMemcpyAsync(hg, dg, nr * 4, cudaMemcpyDeviceToHost, s));
   CU(cudaStreamSynchronize(s));
-  for (size_t i = 0; i < nx; ++i) out[i] = hx[i];
+  host_convert(out, hx, nx);
   if (ids) std::memcpy(ids, hids, nr * 4);
   if (gates)
     for (size_t i = 0; i < nr; ++i) gates[i] = hg[i];
