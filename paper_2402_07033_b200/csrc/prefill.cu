@@ -406,7 +406,7 @@ constexpr int GP_QN = 2;
 // epilogue staging: 32 token rows x 128 columns, fp32 (down) or bf16 (up)
 constexpr int GP_STG = 32 * PF_BM * 4;  // 16 KB
 constexpr int GP_SMEM = GP_STAGES * GP_STAGE + GP_STG + 1024 /*align*/ + 256 /*barriers, queue*/ +
-                        (5 * kMaxExperts + 1) * 4 /*schedule segments [2E+1] + [2E], splits [E]*/ +
+                        (6 * kMaxExperts + 1) * 4 /*schedule segments [2E+1] + [2E], splits, chunks [E]*/ +
                         2 * PF_MAXN * 4 /*down tile: pair index + gate per token row*/;
 
 struct GroupedArgs {
@@ -443,22 +443,25 @@ struct GTile {
 
 // The tile schedule is a list of segments, each the up or the down tiles of
 // one expert: seg_start[i] = first tile of segment i, seg_code[i] = 2 e + up.
+// Token chunks (> 256 tokens per expert) are the fastest-varying index, so
+// the chunks' tiles of one weight tile run back to back on different SMs and
+// all but the first read it from L2.
 __device__ __forceinline__ GTile gp_decode(int t, const int* seg_start, const int* seg_code,
-                                           int n_ft, int n_dt, const int* split) {
+                                           int n_ft, int n_dt, const int* split, const int* nch) {
   GTile g;
   int i = 0;
   while (seg_start[i + 1] <= t) ++i;
   const int loc = t - seg_start[i];
   g.e = seg_code[i] >> 1;
   g.up = seg_code[i] & 1;
+  const int ch = nch[g.e];
+  g.c = loc % ch;
+  const int rem = loc / ch;
   if (g.up) {
-    g.c = loc / n_ft;
-    g.t1 = loc % n_ft;
+    g.t1 = rem;
     g.s = 0;
   } else {
     const int S = split[g.e];
-    g.c = loc / (n_dt * S);
-    const int rem = loc % (n_dt * S);
     g.t1 = rem / S;
     g.s = rem % S;
   }
@@ -487,7 +490,8 @@ __global__ void __launch_bounds__(PF_THREADS, 1)
   int* seg_start = q_tile + GP_QN;                  // [2E + 1]
   int* seg_code = seg_start + 2 * kMaxExperts + 1;   // [2E]
   int* s_split = seg_code + 2 * kMaxExperts;         // [E]
-  int* s_pair = s_split + kMaxExperts;                            // [PF_MAXN]
+  int* s_nch = s_split + kMaxExperts;                // [E] token chunks per expert
+  int* s_pair = s_nch + kMaxExperts;                              // [PF_MAXN]
   float* s_gate = reinterpret_cast<float*>(s_pair + PF_MAXN);     // [PF_MAXN]
   __shared__ int s_total;
 
@@ -510,7 +514,10 @@ __global__ void __launch_bounds__(PF_THREADS, 1)
       if (a.slot_of[e] >= 0 && a.counts[e] > 0) act[n_act++] = e;
     const int n_late = (3 * n_act + 7) / 8;
     const int s_hi = min(a.S, a.f / PF_BK), s_lo = max(1, s_hi / 2);
-    for (int e = 0; e < a.E; ++e) s_split[e] = 1;
+    for (int e = 0; e < a.E; ++e) {
+      s_split[e] = 1;
+      s_nch[e] = max(1, (a.counts[e] + PF_MAXN - 1) / PF_MAXN);
+    }
     for (int i = 0; i < n_act; ++i) s_split[act[i]] = i >= n_act - n_late ? s_hi : s_lo;
     if (blockIdx.x == 0)
       for (int e = 0; e < a.E; ++e) a.split_of[e] = s_split[e];
@@ -586,7 +593,7 @@ __global__ void __launch_bounds__(PF_THREADS, 1)
           qph ^= 1;
         }
         if (t >= total) break;
-        const GTile g = gp_decode(t, seg_start, seg_code, n_ft, n_dt, s_split);
+        const GTile g = gp_decode(t, seg_start, seg_code, n_ft, n_dt, s_split, s_nch);
         int nvalid, N, nboxes, srow;
         chunk_geom(g, nvalid, N, nboxes, srow);
         gp_stamp(a, ntile, 0,
@@ -654,7 +661,7 @@ __global__ void __launch_bounds__(PF_THREADS, 1)
           qph ^= 1;
         }
         if (t >= total) break;
-        const GTile g = gp_decode(t, seg_start, seg_code, n_ft, n_dt, s_split);
+        const GTile g = gp_decode(t, seg_start, seg_code, n_ft, n_dt, s_split, s_nch);
         int nvalid, N, nboxes, srow;
         chunk_geom(g, nvalid, N, nboxes, srow);
         int bufs[2];
@@ -721,7 +728,7 @@ __global__ void __launch_bounds__(PF_THREADS, 1)
         qph ^= 1;
       }
       if (t >= total) break;
-      const GTile g = gp_decode(t, seg_start, seg_code, n_ft, n_dt, s_split);
+      const GTile g = gp_decode(t, seg_start, seg_code, n_ft, n_dt, s_split, s_nch);
       int nvalid, N, nboxes, srow;
       chunk_geom(g, nvalid, N, nboxes, srow);
       if (!g.up) {
