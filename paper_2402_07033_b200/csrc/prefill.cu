@@ -513,11 +513,16 @@ __global__ void __launch_bounds__(PF_THREADS, 1)
     for (int e = 0; e < a.E; ++e)
       if (a.slot_of[e] >= 0 && a.counts[e] > 0) act[n_act++] = e;
     const int n_late = (3 * n_act + 7) / 8;
-    const int s_hi = min(a.S, a.f / PF_BK), s_lo = max(1, s_hi / 2);
+    int dn_tiles = 0;  // down tiles without K splits
     for (int e = 0; e < a.E; ++e) {
       s_split[e] = 1;
       s_nch[e] = max(1, (a.counts[e] + PF_MAXN - 1) / PF_MAXN);
+      if (a.slot_of[e] >= 0 && a.counts[e] > 0) dn_tiles += s_nch[e] * n_dt;
     }
+    // K splits only pay while the down tiles are few per SM (tail); with many
+    // (large batches) they only add fp32 Y partial traffic for the combine
+    const int s_hi = dn_tiles >= 4 * (int)gridDim.x ? 1 : min(a.S, a.f / PF_BK);
+    const int s_lo = max(1, s_hi / 2);
     for (int i = 0; i < n_act; ++i) s_split[act[i]] = i >= n_act - n_late ? s_hi : s_lo;
     if (blockIdx.x == 0)
       for (int e = 0; e < a.E; ++e) a.split_of[e] = s_split[e];
