@@ -593,3 +593,48 @@ def test_x22b_layer_decode_and_prefill_vs_oracle(ctx, orc):
     print(f"X prefill (tcgen05) normwise error {worst:.3e}")
     assert worst < TOL_BF16
     w.close()
+
+
+@pytest.mark.parametrize("E,k,d,f,dt,n_tok", [
+    (16, 4, 1024, 2048, M.DTYPE_BF16, 1),     # streaming decode, k > 2
+    (64, 8, 512, 1024, M.DTYPE_BF16, 1),      # many experts, k = 8
+    (8, 8, 512, 768, M.DTYPE_F32, 1),         # k == E (every expert selected)
+    (1, 1, 256, 512, M.DTYPE_BF16, 1),        # single expert
+    (256, 2, 256, 256, M.DTYPE_F32, 3),       # E at the 256 limit, generic multi-token
+    (16, 4, 256, 512, M.DTYPE_BF16, 300),     # tcgen05 prefill with k = 4 (ragged experts)
+    (8, 2, 256, 512, M.DTYPE_BF16, 2),        # tcgen05 at 2 tokens (tiny N)
+])
+def test_edge_geometries_vs_oracle(ctx, orc, E, k, d, f, dt, n_tok):
+    """Routing geometries beyond Mixtral's (E, k) = (8, 2), through whichever
+    kernel the library picks, against the fp64 oracle on device-held values."""
+    esz = 2 if dt == M.DTYPE_BF16 else 4
+    w = M.Weights(ctx, M.Shape(2, E, k, d, f, esz), dt)
+    w.random(E * 31 + k)
+    rs = np.random.RandomState(E + k)
+    x = f32(rs.randn(n_tok, d))
+    xd = torch.tensor(x, dtype=torch.float32, device="cuda")
+    xo = torch.empty_like(xd)
+    idd = torch.zeros((n_tok, k), dtype=torch.int32, device="cuda")
+    gd = torch.zeros((n_tok, k), dtype=torch.float32, device="cuda")
+    w.layer_forward(1, xd, xo, idd, gd)
+    torch.cuda.synchronize()
+    out = xo.cpu().numpy().astype(np.float64)
+    ids_dev, g_dev = idd.cpu().numpy(), gd.cpu().numpy()
+    router = w.download_router(1)
+    tol = TOL_BF16 if (dt == M.DTYPE_BF16 and n_tok > 1) else 1e-4
+    cache = {}
+    for t in sorted({0, n_tok // 2, n_tok - 1}):
+        ids, g, logits = orc.gate_topk(router, x[t], k)
+        if margin(logits, k) > 1e-5:
+            assert list(ids_dev[t]) == list(ids)
+            assert np.abs(g_dev[t] - g).max() < 1e-5
+        assert list(ids_dev[t]) == sorted(ids_dev[t])  # ascending ids (model.cpp:96-97)
+        assert abs(float(g_dev[t].sum()) - 1.0) < 1e-5
+        delta = np.zeros(d)
+        for e, ge in zip(ids_dev[t], g_dev[t]):
+            if int(e) not in cache:
+                cache[int(e)] = w.download_expert(1, int(e))
+            delta += ge * orc.expert_ffn(*cache[int(e)], x[t])
+        err = normwise(out[t] - x[t], delta)
+        assert err < tol, (t, err)
+    w.close()
