@@ -335,7 +335,8 @@ int ensure_prefill_scratch(moe_weights* w, int n_tok) {
   TRY(w->pf_xg.ensure(2 * rows * w->d()));
   TRY(w->pf_h.ensure(2 * rows * w->f()));
   TRY(w->y.ensure(4 * rows * w->d() * (size_t)std::max(1, w->prefill_splits)));
-  TRY(w->pf_sync.ensure(4 * (1 + (size_t)w->E() * ((n_tok + 255) / 256) + w->E())));
+  TRY(w->pf_sync.ensure(4 * (1 + (size_t)w->E() * ((n_tok + moe::kPrefillChunk - 1) / moe::kPrefillChunk) +
+                          w->E())));
   return MOE_OK;
 }
 

@@ -138,10 +138,15 @@ cudaError_t launch_generic_down(const LayerWeights& lw, const Dims& dm, const fl
 cudaError_t launch_combine(const float* x, const float* y, const float* gates, int n_tok,
                            const Dims& dm, float* x_out, cudaStream_t s, bool pdl, int nsplit = 1,
                            const int32_t* ids = nullptr, const int32_t* split_of = nullptr);
+// Token chunk of the grouped prefill kernel (tokens per tile, UMMA N).
+#ifndef MOE_PREFILL_CHUNK
+#define MOE_PREFILL_CHUNK 256
+#endif
+constexpr int kPrefillChunk = MOE_PREFILL_CHUNK;
 // The grouped prefill kernel's per-expert K-split record inside its sync
 // buffer (sync = [tile counter][E x chunks done flags][E splits]).
 inline int32_t* prefill_split_of(int* sync, int E, int n_tok) {
-  return sync + 1 + E * ((n_tok + 255) / 256);
+  return sync + 1 + E * ((n_tok + kPrefillChunk - 1) / kPrefillChunk);
 }
 
 // out = a + b (elementwise; expert-parallel residual after the all-reduce)

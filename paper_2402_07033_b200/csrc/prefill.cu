@@ -400,14 +400,21 @@ __global__ void __launch_bounds__(PF_THREADS, 1)
 // fence.proxy.async before its TMA reads).  Up tiles never wait, so the
 // schedule cannot deadlock.  The producer warp runs ahead into the next tile
 // while the epilogue warps drain TMEM, so the ring refills behind the epilogue.
-constexpr int GP_STAGES = 3;
-constexpr int GP_STAGE = 2 * PF_BM * PF_BK * 2 + PF_MAXN * PF_BK * 2;  // 64 KB
+// Token chunk of the grouped kernel (kernels.h kPrefillChunk, UMMA N): 256.
+// Measured against 128 (4 x 48 KB stages, 128 KB of weights in flight, no
+// wide TMEM tiles): 128 is 11 % slower at 512 tokens and 18-25 % slower at
+// 2048-8192 (twice the tiles, weight tiles re-read from L2 per chunk, half
+// the MMA N).  An expert with more tokens becomes several chunks whose tiles
+// run back to back, so the second read of a weight tile comes from L2.
+constexpr int GP_MAXN = kPrefillChunk;
+constexpr int GP_STAGE = 2 * PF_BM * PF_BK * 2 + GP_MAXN * PF_BK * 2;
+constexpr int GP_STAGES = (192 * 1024) / GP_STAGE;
 constexpr int GP_QN = 2;
 // epilogue staging: 32 token rows x 128 columns, fp32 (down) or bf16 (up)
 constexpr int GP_STG = 32 * PF_BM * 4;  // 16 KB
 constexpr int GP_SMEM = GP_STAGES * GP_STAGE + GP_STG + 1024 /*align*/ + 256 /*barriers, queue*/ +
                         (6 * kMaxExperts + 1) * 4 /*schedule segments [2E+1] + [2E], splits, chunks [E]*/ +
-                        2 * PF_MAXN * 4 /*down tile: pair index + gate per token row*/;
+                        2 * GP_MAXN * 4 /*down tile: pair index + gate per token row*/;
 
 struct GroupedArgs {
   const int32_t* counts;
@@ -443,7 +450,7 @@ struct GTile {
 
 // The tile schedule is a list of segments, each the up or the down tiles of
 // one expert: seg_start[i] = first tile of segment i, seg_code[i] = 2 e + up.
-// Token chunks (> 256 tokens per expert) are the fastest-varying index, so
+// Token chunks (experts with > GP_MAXN tokens) are the fastest-varying index, so
 // the chunks' tiles of one weight tile run back to back on different SMs and
 // all but the first read it from L2.
 __device__ __forceinline__ GTile gp_decode(int t, const int* seg_start, const int* seg_code,
@@ -491,8 +498,8 @@ __global__ void __launch_bounds__(PF_THREADS, 1)
   int* seg_code = seg_start + 2 * kMaxExperts + 1;   // [2E]
   int* s_split = seg_code + 2 * kMaxExperts;         // [E]
   int* s_nch = s_split + kMaxExperts;                // [E] token chunks per expert
-  int* s_pair = s_nch + kMaxExperts;                              // [PF_MAXN]
-  float* s_gate = reinterpret_cast<float*>(s_pair + PF_MAXN);     // [PF_MAXN]
+  int* s_pair = s_nch + kMaxExperts;                              // [GP_MAXN]
+  float* s_gate = reinterpret_cast<float*>(s_pair + GP_MAXN);     // [GP_MAXN]
   __shared__ int s_total;
 
   const int warp = warp_uniform(threadIdx.x >> 5), lane = threadIdx.x & 31;
@@ -516,7 +523,7 @@ __global__ void __launch_bounds__(PF_THREADS, 1)
     int dn_tiles = 0;  // down tiles without K splits
     for (int e = 0; e < a.E; ++e) {
       s_split[e] = 1;
-      s_nch[e] = max(1, (a.counts[e] + PF_MAXN - 1) / PF_MAXN);
+      s_nch[e] = max(1, (a.counts[e] + GP_MAXN - 1) / GP_MAXN);
       if (a.slot_of[e] >= 0 && a.counts[e] > 0) dn_tiles += s_nch[e] * n_dt;
     }
     // K splits only pay while the down tiles are few per SM (tail); with many
@@ -529,7 +536,7 @@ __global__ void __launch_bounds__(PF_THREADS, 1)
     const int kLag = a.lag;
     int ns = 0, tot = 0;
     auto push = [&](int e, int up) {
-      const int ch = (a.counts[e] + PF_MAXN - 1) / PF_MAXN;
+      const int ch = (a.counts[e] + GP_MAXN - 1) / GP_MAXN;
       seg_start[ns] = tot;
       seg_code[ns++] = 2 * e + up;
       tot += up ? ch * n_ft : ch * n_dt * s_split[e];
@@ -566,8 +573,8 @@ __global__ void __launch_bounds__(PF_THREADS, 1)
   constexpr int kBox = PF_BOXN * PF_BK * 2;
 
   auto chunk_geom = [&](const GTile& g, int& nvalid, int& N, int& nboxes, int& srow) {
-    const int row0 = g.c * PF_MAXN;
-    nvalid = min(PF_MAXN, a.counts[g.e] - row0);
+    const int row0 = g.c * GP_MAXN;
+    nvalid = min(GP_MAXN, a.counts[g.e] - row0);
     N = (nvalid + 15) & ~15;
     nboxes = (N + PF_BOXN - 1) / PF_BOXN;
     srow = a.offsets[g.e] + row0;
@@ -919,7 +926,9 @@ cudaError_t launch_prefill_experts(const LayerWeights& lw, int n_local, const Di
       !make_map(&wmap_dn, lw.experts, wrows, dm.d, 64, PF_BK) ||
       !make_map(&xmap, xg, rows, dm.d, 64, PF_BOXN) || !make_map(&hmap, h, rows, dm.f, 64, PF_BOXN))
     return cudaErrorInvalidValue;
-  const int chunks = (n_tok + PF_MAXN - 1) / PF_MAXN;  // an expert holds <= n_tok tokens
+  // an expert holds <= n_tok tokens; the grouped kernel's done flags are per
+  // GP_MAXN-token chunk, the two-kernel path's grid per PF_MAXN
+  const int chunks = (n_tok + GP_MAXN - 1) / GP_MAXN;
   if (splits > 0) {
     // persistent grouped kernel (default)
     GroupedArgs g;
