@@ -58,6 +58,7 @@ const char* moe_last_error(void);
 /* ModelShape::validate (shape.cpp:7-16): MOE_ERR_SHAPE on violation. */
 int moe_shape_validate(const moe_shape* shape);
 int moe_ctx_create(int device, moe_ctx** out);
+/* Destroy every moe_weights created on the context first. */
 int moe_ctx_destroy(moe_ctx* ctx);
 /* The context's stream (cudaStream_t) used when a call passes stream=NULL. */
 void* moe_ctx_stream(moe_ctx* ctx);

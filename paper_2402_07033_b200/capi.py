@@ -143,29 +143,42 @@ def _ptr(t):
     return C.c_void_p(t.data_ptr())
 
 
+CUDA_STREAM_LEGACY = 1  # cudaStreamLegacy: the explicit handle of the legacy default stream
+
+
 def _stream(stream, *tensors):
     """Default for device-pointer calls on torch tensors: torch's current
     stream on the tensors' device, so the kernels are ordered after the
-    torch ops that produced their inputs."""
+    torch ops that produced their inputs.  torch's default stream is the
+    legacy default stream, whose handle is 0 — and a NULL stream means "the
+    context's own (non-blocking) stream" in the C-ABI, which would race with
+    the torch kernels that produced the inputs — so it is passed as
+    cudaStreamLegacy."""
     if stream is not None:
         return stream
     for t in tensors:
         if t is not None and hasattr(t, "device") and getattr(t.device, "type", "") == "cuda":
             import torch
 
-            return C.c_void_p(torch.cuda.current_stream(t.device).cuda_stream)
+            h = torch.cuda.current_stream(t.device).cuda_stream
+            return C.c_void_p(h if h else CUDA_STREAM_LEGACY)
     return None
 
 
 class Ctx:
     def __init__(self, device: int = 0):
+        import weakref
+
         h = _vp()
         check(lib().moe_ctx_create(device, C.byref(h)))
         self.h = h
         self.device = device
+        self._weights = weakref.WeakSet()  # closed before the context (C-ABI order)
 
     def close(self):
         if self.h:
+            for w in list(self._weights):
+                w.close()
             lib().moe_ctx_destroy(self.h)
             self.h = None
 
@@ -276,6 +289,7 @@ class Weights:
                 own = self._owner.ctypes.data_as(_vp)
             check(lib().moe_weights_create(ctx.h, C.byref(sh), dtype, own, C.byref(h)))
         self.h = h
+        ctx._weights.add(self)
 
     @property
     def tp(self):

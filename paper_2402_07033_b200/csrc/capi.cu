@@ -166,6 +166,7 @@ struct moe_weights {
   void* host_pin = nullptr;
   size_t host_pin_bytes = 0;
   std::map<std::tuple<float*, int32_t*, float*, cudaStream_t>, GraphEntry> graphs;
+  cudaStream_t cap_stream = nullptr;  // private stream for graph capture
   std::mutex mu;
 
   int L() const { return shape.num_layers; }
@@ -214,6 +215,7 @@ int check_shape(const moe_shape* s) {
 
 int set_device(moe_ctx* c) {
   CU(cudaSetDevice(c->device));
+  cudaGetLastError();  // launches below report their own errors, not a stale one
   return MOE_OK;
 }
 
@@ -437,15 +439,19 @@ int enqueue_forward(moe_weights* w, float* x, int n_tok, int32_t* ids, float* ga
   return MOE_OK;
 }
 
+// The batch-1 forward as a CUDA graph, captured once per (x, ids, gates) on a
+// private stream (the caller's stream may be the legacy default stream,
+// which cannot be captured) and launched on the caller's stream.
 int forward_graph(moe_weights* w, float* x, int32_t* ids, float* gates, cudaStream_t s) {
-  auto key = std::make_tuple(x, ids, gates, s);
+  auto key = std::make_tuple(x, ids, gates, (cudaStream_t) nullptr);
   auto it = w->graphs.find(key);
   if (it == w->graphs.end()) {
+    cudaStream_t cs = w->cap_stream;  // created with the weights (creation may synchronize)
     cudaGraph_t g = nullptr;
-    CU(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal));
-    const int rc = use_stack(w, 1) ? enqueue_stack(w, x, ids, gates, s)
-                                   : enqueue_forward(w, x, 1, ids, gates, s, nullptr);
-    cudaError_t e = cudaStreamEndCapture(s, &g);
+    CU(cudaStreamBeginCapture(cs, cudaStreamCaptureModeThreadLocal));
+    const int rc = use_stack(w, 1) ? enqueue_stack(w, x, ids, gates, cs)
+                                   : enqueue_forward(w, x, 1, ids, gates, cs, nullptr);
+    cudaError_t e = cudaStreamEndCapture(cs, &g);
     if (rc != MOE_OK) {
       if (g) cudaGraphDestroy(g);
       return rc;
@@ -697,6 +703,16 @@ int moe_ctx_link_peers(moe_ctx* const* ctxs, int world, int max_hidden) {
   return MOE_OK;
 }
 
+// diagnostics: this rank's exchange counters (out[0] = zseq, out[1..n-1] = seq[0..n-2])
+extern "C" int moe_debug_peer_counters(moe_ctx* c, unsigned* out, int n) {
+  if (!c || !out || n < 1) return fail(MOE_ERR_ARG, "bad argument");
+  if (!c->peers) return fail(MOE_ERR_ARG, "no peer window");
+  TRY(set_device(c));
+  CU(cudaMemcpy(out, c->pa.zseq, 4, cudaMemcpyDeviceToHost));
+  if (n > 1) CU(cudaMemcpy(out + 1, c->pa.seq, 4 * (size_t)std::min(n - 1, moe::kPeerSlots), cudaMemcpyDeviceToHost));
+  return MOE_OK;
+}
+
 int moe_ctx_peer_check(moe_ctx* c) {
   if (!c) return fail(MOE_ERR_ARG, "null ctx");
   if (!c->peers) return MOE_OK;
@@ -791,6 +807,8 @@ static int weights_create(moe_ctx* c, const moe_shape* shape, int dtype,
         return cleanup(fail(MOE_ERR_CUDA, "upload projection table"));
     }
   }
+  if (cudaStreamCreateWithFlags(&w->cap_stream, cudaStreamNonBlocking) != cudaSuccess)
+    return cleanup(fail(MOE_ERR_CUDA, "create capture stream"));
   if (const char* env = getenv("MOE_B200_STACK")) w->stack_enabled = env[0] != '0';
   if (const char* env = getenv("MOE_B200_PREFILL")) w->prefill_enabled = env[0] != '0';
   if (const char* env = getenv("MOE_B200_PREFILL_SPLITS")) w->prefill_splits = atoi(env);
@@ -832,6 +850,7 @@ int moe_weights_destroy(moe_weights* w) {
   cudaSetDevice(w->ctx->device);
   for (auto& kv : w->graphs)
     if (kv.second.exec) cudaGraphExecDestroy(kv.second.exec);
+  if (w->cap_stream) cudaStreamDestroy(w->cap_stream);
   for (DevBuf& b : w->rw_mem) b.release();
   w->dev_rw.release();
   for (void* p : w->layer_mem)

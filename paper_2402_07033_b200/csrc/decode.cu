@@ -953,7 +953,8 @@ static cudaError_t launch_stack_t(const DecodePlan& p, const StackArgs& a, cudaS
   attr[0].id = cudaLaunchAttributeCooperative;
   attr[0].val.cooperative = 1;
   cfg.attrs = attr;
-  cfg.numAttrs = 1;
+  static const bool noncoop = getenv("MOE_B200_NONCOOP") != nullptr;  // diagnostics
+  cfg.numAttrs = noncoop ? 0 : 1;
   return cudaLaunchKernelEx(&cfg, kern, a);
 }
 

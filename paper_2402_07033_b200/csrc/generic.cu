@@ -4,6 +4,7 @@
 // (hidden 2..6, ffn 2..8, toy 32/64) and any shape the streaming / tcgen05
 // kernels do not take.  Still GPU code: there is no CPU path in the product.
 #include <algorithm>
+#include <cstdlib>
 
 #include "../../include/moe_b200.h"
 #include "common.cuh"
@@ -21,7 +22,8 @@ static cudaLaunchConfig_t make_cfg(dim3 grid, dim3 block, cudaStream_t s, bool p
   attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
   attr[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
-  cfg.numAttrs = pdl ? 1 : 0;
+  static const bool no_pdl = getenv("MOE_B200_NO_PDL") != nullptr;  // diagnostics
+  cfg.numAttrs = (pdl && !no_pdl) ? 1 : 0;
   return cfg;
 }
 

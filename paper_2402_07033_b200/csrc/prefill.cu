@@ -407,41 +407,12 @@ __global__ void __launch_bounds__(PF_THREADS, 1)
 // the MMA N).  An expert with more tokens becomes several chunks whose tiles
 // run back to back, so the second read of a weight tile comes from L2.
 constexpr int GP_MAXN = kPrefillChunk;
-#ifndef MOE_PF_BYTERING
-#define MOE_PF_BYTERING 1
-#endif
-#if MOE_PF_BYTERING
-// Byte ring: each K-block takes exactly its bytes (32 KB of weights + N x 128 B
-// of X/H, N <= 256), allocated FIFO around a 192 KB ring; one full/empty
-// barrier pair per K-block slot.  Tiles of <= 128 tokens (48 KB per K-block)
-// keep 4 K-blocks (128 KB of weights) in flight instead of 3.
-constexpr int GP_RING = 192 * 1024;
-constexpr int GP_STAGES = 8;  // K-block slots (barrier pairs)
-#else
 constexpr int GP_STAGE = 2 * PF_BM * PF_BK * 2 + GP_MAXN * PF_BK * 2;
 constexpr int GP_STAGES = (192 * 1024) / GP_STAGE;
-#endif
-// FIFO byte allocator replayed identically by the producer and the MMA warp
-struct KbRing {
-  uint32_t head = 0;
-  __device__ __forceinline__ uint32_t alloc(uint32_t bytes) {
-#if MOE_PF_BYTERING
-    if (head + bytes > (uint32_t)GP_RING) head = 0;
-    const uint32_t a = head;
-    head += bytes;
-    return a;
-#else
-    (void)bytes;
-    const uint32_t a = head;
-    head = head + 1 == (uint32_t)GP_STAGES ? 0 : head + 1;
-    return a * GP_STAGE;
-#endif
-  }
-};
 constexpr int GP_QN = 2;
 // epilogue staging: 32 token rows x 128 columns, fp32 (down) or bf16 (up)
 constexpr int GP_STG = 32 * PF_BM * 4;  // 16 KB
-constexpr int GP_SMEM = 3 * (64 * 1024) + GP_STG + 1024 /*align*/ + 256 /*barriers, queue*/ +
+constexpr int GP_SMEM = GP_STAGES * GP_STAGE + GP_STG + 1024 /*align*/ + 256 /*barriers, queue*/ +
                         (6 * kMaxExperts + 1) * 4 /*schedule segments [2E+1] + [2E], splits, chunks [E]*/ +
                         2 * GP_MAXN * 4 /*down tile: pair index + gate per token row*/;
 
@@ -514,7 +485,7 @@ __global__ void __launch_bounds__(PF_THREADS, 1)
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                              ~uintptr_t(1023));
-  uint8_t* stg = smem + 3 * (64 * 1024);  // epilogue staging (GP_STG bytes)
+  uint8_t* stg = smem + GP_STAGES * GP_STAGE;  // epilogue staging (GP_STG bytes)
   uint64_t* full = reinterpret_cast<uint64_t*>(stg + GP_STG);
   uint64_t* empty = full + GP_STAGES;
   uint64_t* tmem_full = empty + GP_STAGES;  // [2]
@@ -624,26 +595,6 @@ __global__ void __launch_bounds__(PF_THREADS, 1)
       uint32_t kc = 0;
       int qi = 0, ntile = 0;
       uint32_t qph = 0;
-      // K-block kc: wait until its bytes and its barrier slot are free (the
-      // K-blocks still in flight are released in FIFO order), then take them
-      KbRing ring;
-      uint32_t fifo_lo[GP_STAGES], fifo_hi[GP_STAGES];
-      uint32_t inflight = 0;
-      auto claim = [&](uint32_t bytes) -> uint32_t {
-        const uint32_t off = ring.alloc(bytes);
-        while (inflight > 0) {
-          const uint32_t j = kc - inflight;  // oldest K-block still in flight
-          const uint32_t js = j % GP_STAGES;
-          const bool overlap = off < fifo_hi[js] && fifo_lo[js] < off + bytes;
-          if (!overlap && inflight < (uint32_t)GP_STAGES) break;
-          mbar_wait(&empty[js], (j / GP_STAGES) & 1);
-          --inflight;
-        }
-        fifo_lo[kc % GP_STAGES] = off;
-        fifo_hi[kc % GP_STAGES] = off + bytes;
-        ++inflight;
-        return off;
-      };
       while (true) {
         const int t = (int)atomicAdd(a.tile_counter, 1u);
         mbar_wait(&qempty[qi], qph ^ 1);
@@ -668,7 +619,8 @@ __global__ void __launch_bounds__(PF_THREADS, 1)
           const uint32_t bytes = 2 * kA + nboxes * kBox;
           for (int kb = 0; kb < nkb_up; ++kb, ++kc) {
             const int st = kc % GP_STAGES;
-            uint8_t* sp = smem + claim(bytes);
+            mbar_wait(&empty[st], ((kc / GP_STAGES) & 1) ^ 1);
+            uint8_t* sp = smem + st * GP_STAGE;
             mbar_arrive_expect_tx(&full[st], bytes);
             tma_load_2d_hint(sp, &wmap_up, kb * PF_BK, w1row, &full[st], wpol);
             tma_load_2d_hint(sp + kA, &wmap_up, kb * PF_BK, w3row, &full[st], wpol);
@@ -691,7 +643,8 @@ __global__ void __launch_bounds__(PF_THREADS, 1)
           const uint32_t bytes = 2 * kA + nboxes * kBox;
           for (int kb = kb0; kb < kb1; ++kb, ++kc) {
             const int st = kc % GP_STAGES;
-            uint8_t* sp = smem + claim(bytes);
+            mbar_wait(&empty[st], ((kc / GP_STAGES) & 1) ^ 1);
+            uint8_t* sp = smem + st * GP_STAGE;
             mbar_arrive_expect_tx(&full[st], bytes);
             // W2T rows [kb*64, +64) x hidden cols [d0, d0+256): 4 boxes of 64 cols
 #pragma unroll
@@ -708,7 +661,6 @@ __global__ void __launch_bounds__(PF_THREADS, 1)
     // ===== MMA issuer =====
     if (lane == 0) {
       uint32_t kc = 0;
-      KbRing ring;
       TmemSched ts;
       int qi = 0, ntile = 0;
       uint32_t qph = 0;
@@ -733,12 +685,11 @@ __global__ void __launch_bounds__(PF_THREADS, 1)
         const uint32_t c3 = nb == 2 ? tmem + bufs[1] * 256 : c1 + 128;
         if (g.up) {
           const uint32_t idesc = umma_idesc(N, false);
-          const uint32_t bytes = 2 * kA + nboxes * kBox;
           for (int kb = 0; kb < nkb_up; ++kb, ++kc) {
             const int st = kc % GP_STAGES;
-            const uint8_t* sp = smem + ring.alloc(bytes);
             mbar_wait(&full[st], (kc / GP_STAGES) & 1);
             tc_fence_after();
+            const uint8_t* sp = smem + st * GP_STAGE;
 #pragma unroll
             for (int kk = 0; kk < PF_BK / 16; ++kk) {
               const uint64_t b = umma_desc(sp + 2 * kA + kk * 32, 16, 1024);
@@ -752,12 +703,11 @@ __global__ void __launch_bounds__(PF_THREADS, 1)
           const uint32_t idesc = umma_idesc(N, true);
           const int S = s_split[g.e];
           const int nk = (g.s + 1) * nkb_dn / S - g.s * nkb_dn / S;
-          const uint32_t bytes = 2 * kA + nboxes * kBox;
           for (int kb = 0; kb < nk; ++kb, ++kc) {
             const int st = kc % GP_STAGES;
-            const uint8_t* sp = smem + ring.alloc(bytes);
             mbar_wait(&full[st], (kc / GP_STAGES) & 1);
             tc_fence_after();
+            const uint8_t* sp = smem + st * GP_STAGE;
 #pragma unroll
             for (int kk = 0; kk < PF_BK / 16; ++kk) {
               // MN-major A: 16 K-rows = 2 groups of 8 rows (SBO = 1024 B); the

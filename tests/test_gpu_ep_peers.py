@@ -53,8 +53,10 @@ def test_peer_combine_matches_unsharded(gpu, monkeypatch, kernel, mode, world, s
     """mode ep: experts sharded by the popularity shard map; mode tp: every
     expert's ffn rows split over the ranks (tensor parallelism).  kernel
     layer: per-layer streaming kernel + reduce_exchange; kernel stack: the
-    persistent one-launch-per-token kernel with the exchange inside (each
-    rank's grid shrunk to SMs/world so the W kernels fit one GPU together)."""
+    persistent one-launch-per-token kernel with the exchange inside.  Each
+    rank's grid is shrunk to SMs/world so the W ranks' kernels fit one GPU
+    together (with full grids, W = 4 per-layer ranks can starve each other of
+    SMs while their exchange blocks spin — a one-GPU test artefact)."""
     L, E, k, d = shape[0], shape[1], shape[2], shape[3]
     s = M.Shape(*shape)
     base = M.Ctx(0)
@@ -75,8 +77,9 @@ def test_peer_combine_matches_unsharded(gpu, monkeypatch, kernel, mode, world, s
     M.Ctx.link_peers(ctxs, d)
     if kernel == "layer":
         monkeypatch.setenv("MOE_B200_STACK", "0")
-    else:
-        monkeypatch.setenv("MOE_B200_STACK_GRID", str(ctxs[0].sm_count // world))
+    # each rank's streaming kernel on SMs/world CTAs: W ranks' kernels (and the
+    # exchange blocks spinning on each other's flags) must fit one GPU at once
+    monkeypatch.setenv("MOE_B200_STACK_GRID", os.environ.get("PEER_TEST_GRID", str(ctxs[0].sm_count // world)))
     if mode == "ep":
         owner = _bench().shard_map(L, E, world)
         ws = [M.Weights(c, s, dtype, owner=owner) for c in ctxs]
@@ -86,11 +89,17 @@ def test_peer_combine_matches_unsharded(gpu, monkeypatch, kernel, mode, world, s
         w.random(11)
         assert w.forward_launches(1) == (1 + 2 * L if kernel == "layer" else 1)
     torch.cuda.synchronize()
+    # fixed per-rank buffers, refilled per token (as a serving loop does): each
+    # rank captures its graph once.  (Fresh tensors would re-capture and upload
+    # a new graph mid-run while the other ranks' kernels already spin on the
+    # shared GPU — a one-GPU artefact that can exceed the bounded wait.)
+    xs = [torch.empty(1, d, device="cuda") for _ in range(world)]
+    idss = [torch.zeros((L, 1, k), dtype=torch.int32, device="cuda") for _ in range(world)]
+    gs = [torch.zeros((L, 1, k), device="cuda") for _ in range(world)]
     for rep in range(2):
         for t in range(3):
-            xs = [x0[t:t + 1].clone() for _ in range(world)]
-            idss = [torch.zeros((L, 1, k), dtype=torch.int32, device="cuda") for _ in range(world)]
-            gs = [torch.zeros((L, 1, k), device="cuda") for _ in range(world)]
+            for xr in xs:
+                xr.copy_(x0[t:t + 1])
             torch.cuda.synchronize()
             for r in range(world):  # enqueue every rank before waiting on any
                 ws[r].forward(xs[r], idss[r], gs[r], stream=ctxs[r].stream)
