@@ -1,0 +1,108 @@
+"""Multi-PROCESS expert parallelism through CUDA IPC peer windows.
+
+Two processes (one rank each, gloo for the host-side handshake, as
+bench.py does under torchrun) map each other's exchange windows with
+cudaIpcOpenMemHandle and run a tensor-parallel model whose per-layer
+combine goes through those windows.  Here both processes share one GPU, so
+their kernels are time-sliced rather than concurrent; the bounded waits make
+progress at each slice.  Each rank checks its output against the unsharded
+model computed locally.
+"""
+import os
+import socket
+
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _rank_main(rank, world, port, q, kernel, mode):
+    import sys
+
+    sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+    if kernel == "layer":
+        os.environ["MOE_B200_STACK"] = "0"  # per-layer kernels + reduce_exchange
+    import torch.distributed as dist
+
+    import paper_2402_07033_b200 as M
+
+    try:
+        dist.init_process_group("gloo", init_method=f"tcp://127.0.0.1:{port}", rank=rank,
+                                world_size=world)
+        L, E, k, d, f = 2, 8, 2, 512, 1792
+        s = M.Shape(L, E, k, d, f, 4)
+        base = M.Ctx(0)
+        full = M.Weights(base, s, M.DTYPE_F32)
+        full.random(3)
+        ctx = M.Ctx(0)
+        handles = [None] * world
+        dist.all_gather_object(handles, ctx.peer_window(world, d))
+        ctx.open_peers(world, rank, handles)
+        if mode == "tp":
+            w = M.Weights(ctx, s, M.DTYPE_F32, tp=True)
+        else:
+            owner = np.array([[e % world for e in range(E)] for _ in range(L)], np.int32)
+            w = M.Weights(ctx, s, M.DTYPE_F32, owner=owner)
+        assert w.forward_launches(1) == (1 if kernel == "stack" else 1 + 2 * L)
+        w.random(3)
+        gen = torch.Generator(device="cuda").manual_seed(5)
+        x0 = torch.randn(2, d, device="cuda", generator=gen)
+        x = torch.empty(1, d, device="cuda")
+        ids = torch.zeros((L, 1, k), dtype=torch.int32, device="cuda")
+        g = torch.zeros((L, 1, k), device="cuda")
+        errs = []
+        for t in range(2):
+            xr = x0[t:t + 1].clone()
+            idr = torch.zeros_like(ids)
+            gr = torch.zeros_like(g)
+            full.forward(xr, idr, gr, stream=base.stream)
+            base.synchronize()
+            x.copy_(x0[t:t + 1])
+            torch.cuda.synchronize()
+            dist.barrier()
+            w.forward(x, ids, g, stream=ctx.stream)
+            ctx.synchronize()
+            ctx.peer_check()
+            want = (xr - x0[t:t + 1]).double().cpu().numpy()
+            got = (x - x0[t:t + 1]).double().cpu().numpy()
+            errs.append(float(np.abs(got - want).max() / np.abs(want).max()))
+            assert torch.equal(ids, idr)
+        q.put((rank, max(errs), None))
+        dist.barrier()
+        w.close()
+        ctx.close()
+        full.close()
+        base.close()
+        dist.destroy_process_group()
+    except Exception as e:  # reported to the parent
+        q.put((rank, None, repr(e)))
+
+
+@pytest.mark.parametrize("kernel,mode", [("layer", "tp"), ("stack", "tp"), ("stack", "ep")])
+def test_two_process_ipc(kernel, mode):
+    if not torch.cuda.is_available():
+        pytest.skip("no GPU")
+    import torch.multiprocessing as mp
+
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_rank_main, args=(r, 2, port, q, kernel, mode)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = [q.get(timeout=300) for _ in procs]
+    for p in procs:
+        p.join(timeout=60)
+    for rank, err, exc in res:
+        assert exc is None, f"rank {rank}: {exc}"
+        assert err < 1e-4, (rank, err)
