@@ -175,17 +175,21 @@ def run_ours(args):
         L = args.layers
     dtype = M.DTYPE_BF16 if dt == "bf16" else M.DTYPE_F32
     esz = 2 if dt == "bf16" else 4
+    if os.environ.get("MOE_B200_BENCH_SAME_GPU") == "1":
+        local = 0  # testing only: every rank on GPU 0 (time-sliced; numbers meaningless)
     torch.cuda.set_device(local)
     ctx = M.Ctx(local)
     if world > 1:
         import torch.distributed as dist
 
-        obj = [M.Ctx.unique_id() if rank == 0 else None]
-        dist.broadcast_object_list(obj, src=0)
-        ctx.init_ep(world, rank, obj[0])  # NCCL: multi-token exchange (and fallback)
-        if not args.nccl_combine:
-            # fused batch-1 combine over NVLink peer memory: all-gather the
-            # ranks' exchange-window IPC handles, map every peer's window
+        if args.nccl_combine:
+            obj = [M.Ctx.unique_id() if rank == 0 else None]
+            dist.broadcast_object_list(obj, src=0)
+            ctx.init_ep(world, rank, obj[0])  # NCCL all-reduce combine
+        else:
+            # fused batch-1 combine over NVLink peer memory (no NCCL needed for
+            # decode): all-gather the ranks' exchange-window IPC handles and map
+            # every peer's window; this also sets the context's (world, rank)
             handles = [None] * world
             dist.all_gather_object(handles, ctx.peer_window(world, d))
             ctx.open_peers(world, rank, handles)
@@ -266,7 +270,9 @@ def run_ours(args):
         ach = alg / (kern_ms * 1e-3) / 1e9
         expert_kernel = {"kernel": "decode_experts_kernel", "achieved": round(ach, 1),
                          "frac": round(ach / peak, 4), "kernel_us": round(kern_ms * 1e3, 2),
-                         "alg_bytes_per_launch": alg, "traffic": args.traffic}
+                         "alg_bytes_per_launch": alg,
+                         # ncu bytes of the single-GPU layer kernel (profiles/); not for a shard
+                         "traffic": args.traffic if world == 1 else None}
         del ypart
     if world == 1 and w.forward_launches(1) == 1:
         n_rep = max(10, min(50, args.steps))
@@ -291,7 +297,7 @@ def run_ours(args):
                 "peak_source": peak_src, "expert_kernel": expert_kernel}
     elif expert_kernel is not None:
         roof = {"bound": "hbm", "achieved": expert_kernel["achieved"], "peak": peak, "unit": "GB/s",
-                "frac": expert_kernel["frac"], "traffic": args.traffic, "kernel": "decode_experts_kernel",
+                "frac": expert_kernel["frac"], "traffic": expert_kernel["traffic"], "kernel": "decode_experts_kernel",
                 "kernel_us": expert_kernel["kernel_us"],
                 "alg_bytes_per_launch": expert_kernel["alg_bytes_per_launch"], "peak_source": peak_src}
     if roof is not None and world == 1:
