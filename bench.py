@@ -199,6 +199,7 @@ def run_ours(args):
     owner = shard_map(L, E, world) if world > 1 and args.shard == "ep" else None
     w = M.Weights(ctx, shape, dtype, owner=owner, tp=(world > 1 and args.shard == "tp"))
     w.random(args.seed)
+    w.reserve(1)  # all scratch now: nothing allocates (or syncs) inside the timed loop
     stream_ptr = ctx.stream
     stream = torch.cuda.ExternalStream(stream_ptr, device=f"cuda:{local}")
 

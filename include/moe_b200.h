@@ -86,6 +86,13 @@ int moe_ctx_peer_window(moe_ctx* ctx, int world, int max_hidden, void* ipc_handl
 int moe_ctx_open_peers(moe_ctx* ctx, int world, int rank, const void* handles64);
 int moe_ctx_link_peers(moe_ctx* const* ctxs, int world, int max_hidden);
 int moe_ctx_peer_check(moe_ctx* ctx);
+/* Same, with a multi-token area for up to max_tokens tokens: multi-token
+ * (prefill) layers then combine across the ranks with a reduce-scatter +
+ * all-gather kernel over the windows (rank-ordered, bit-identical on every
+ * rank) instead of ncclAllReduce.  The decode path does not need it. */
+int moe_ctx_peer_window_tokens(moe_ctx* ctx, int world, int max_hidden, int max_tokens,
+                               void* ipc_handle64);
+int moe_ctx_link_peers_tokens(moe_ctx* const* ctxs, int world, int max_hidden, int max_tokens);
 /* Testing hook: give this context an expert-parallel (world, rank) with NO
  * communicator.  Weights created on it hold only rank `rank`'s experts and
  * the per-layer exchange is skipped, so x_out = x + (this rank's partial
@@ -107,6 +114,11 @@ int moe_weights_create(moe_ctx* ctx, const moe_shape* shape, int dtype,
  * layout; download fills only this rank's slice of the full-size buffers. */
 int moe_weights_create_tp(moe_ctx* ctx, const moe_shape* shape, int dtype, moe_weights** out);
 int moe_weights_tp(const moe_weights* w, int* tp_world, int* tp_rank, int* ffn_local);
+/* Allocate every scratch buffer for calls of up to max_tokens tokens (and the
+ * batch-1 router projections) now, so no later call allocates or frees
+ * device memory (cudaFree synchronizes the device).  Serving loops and
+ * peer-linked ranks call it once before the first forward. */
+int moe_weights_reserve(moe_weights* w, int max_tokens);
 int moe_weights_destroy(moe_weights* w);
 int64_t moe_weights_device_bytes(const moe_weights* w);
 /* Upload one expert from the reference's host layout (Matrix::data, row

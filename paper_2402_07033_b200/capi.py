@@ -93,8 +93,11 @@ def lib():
         "moe_ctx_open_peers": ([_vp, C.c_int, C.c_int, _vp], C.c_int),
         "moe_ctx_link_peers": ([C.POINTER(_vp), C.c_int, C.c_int], C.c_int),
         "moe_ctx_peer_check": ([_vp], C.c_int),
+        "moe_ctx_peer_window_tokens": ([_vp, C.c_int, C.c_int, C.c_int, _vp], C.c_int),
+        "moe_ctx_link_peers_tokens": ([C.POINTER(_vp), C.c_int, C.c_int, C.c_int], C.c_int),
         "moe_weights_create": ([_vp, C.POINTER(_Shape), C.c_int, _vp, C.POINTER(_vp)], C.c_int),
         "moe_weights_create_tp": ([_vp, C.POINTER(_Shape), C.c_int, C.POINTER(_vp)], C.c_int),
+        "moe_weights_reserve": ([_vp, C.c_int], C.c_int),
         "moe_weights_tp": ([_vp, C.POINTER(C.c_int), C.POINTER(C.c_int), C.POINTER(C.c_int)], C.c_int),
         "moe_weights_destroy": ([_vp], C.c_int),
         "moe_weights_device_bytes": ([_vp], C.c_int64),
@@ -207,10 +210,11 @@ class Ctx:
         check(lib().moe_ctx_set_virtual_rank(self.h, world, rank))
 
     # ---- peer-memory combine (NVLink P2P / CUDA IPC) ----
-    def peer_window(self, world: int, max_hidden: int) -> bytes:
-        """Allocate this rank's exchange window; returns its 64-byte IPC handle."""
+    def peer_window(self, world: int, max_hidden: int, max_tokens: int = 0) -> bytes:
+        """Allocate this rank's exchange window (max_tokens > 0 adds the
+        multi-token area); returns its 64-byte IPC handle."""
         buf = C.create_string_buffer(64)
-        check(lib().moe_ctx_peer_window(self.h, world, max_hidden, buf))
+        check(lib().moe_ctx_peer_window_tokens(self.h, world, max_hidden, max_tokens, buf))
         return buf.raw
 
     def open_peers(self, world: int, rank: int, handles: list):
@@ -219,10 +223,10 @@ class Ctx:
         check(lib().moe_ctx_open_peers(self.h, world, rank, blob))
 
     @staticmethod
-    def link_peers(ctxs: list, max_hidden: int):
+    def link_peers(ctxs: list, max_hidden: int, max_tokens: int = 0):
         """In-process peers (several contexts, same or peer-capable GPUs)."""
         arr = (_vp * len(ctxs))(*[c.h for c in ctxs])
-        check(lib().moe_ctx_link_peers(arr, len(ctxs), max_hidden))
+        check(lib().moe_ctx_link_peers_tokens(arr, len(ctxs), max_hidden, max_tokens))
 
     def peer_check(self):
         check(lib().moe_ctx_peer_check(self.h))
@@ -290,6 +294,10 @@ class Weights:
             check(lib().moe_weights_create(ctx.h, C.byref(sh), dtype, own, C.byref(h)))
         self.h = h
         ctx._weights.add(self)
+
+    def reserve(self, max_tokens: int):
+        """Allocate all scratch for calls of up to max_tokens tokens now."""
+        check(lib().moe_weights_reserve(self.h, max_tokens))
 
     @property
     def tp(self):

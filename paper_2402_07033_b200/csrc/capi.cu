@@ -96,7 +96,7 @@ struct moe_ctx {
   bool ep() const { return world > 1 || ep_forced; }
   // peer-memory exchange window (NVLink P2P / CUDA IPC; kernels.h PeerArgs)
   void* win = nullptr;
-  int win_world = 0, win_hidden = 0;
+  int win_world = 0, win_hidden = 0, win_tokens = 0;
   bool peers = false;
   moe::PeerArgs pa{};
   std::vector<void*> ipc_opened;
@@ -226,6 +226,7 @@ void drop_graphs(moe_weights* w) {
 }
 
 int ensure_scratch_impl(moe_weights* w, int n_tok);
+bool use_prefill(const moe_weights* w, int n_tok, const float* post);
 
 // Per-call scratch sized for n_tok tokens; captured graphs hold scratch
 // pointers, so any reallocation invalidates them.
@@ -254,8 +255,12 @@ int ensure_scratch_impl(moe_weights* w, int n_tok) {
   TRY(w->counter.ensure(64));
   TRY(w->ypart.ensure((size_t)std::max(1, w->ctx->sm_count) * d * 4));
   if (n_tok > 1 || !w->plan.ok) {
-    TRY(w->h.ensure(n * k * f * 4));
-    TRY(w->y.ensure(n * k * d * 4));
+    // sized for the grouped prefill's K-split partials up front: growing a
+    // buffer later means cudaFree, which synchronizes the device (and with
+    // peer-linked ranks on one GPU would wait on a rank's spinning exchange)
+    TRY(w->h.ensure(n * k * f * 4));  // generic path (also the sink / counter fallbacks)
+    const size_t splits = use_prefill(w, n_tok, nullptr) ? (size_t)std::max(1, w->prefill_splits) : 1;
+    TRY(w->y.ensure(n * k * d * 4 * splits));
   }
   return MOE_OK;
 }
@@ -408,8 +413,14 @@ int experts_forward(moe_weights* w, int l, const float* x, int n_tok, const int3
     float* delta = w->delta.as<float>();
     CU(moe::launch_combine(nullptr, w->y.as<float>(), cgates, n_tok, dm, delta, s, pdl, nsplit, ids,
                            split_of));
-    TRY(allreduce(w, delta, (size_t)n_tok * dm.d, s));
-    CU(moe::launch_add(x, delta, x_out, (long long)n_tok * dm.d, s, false));
+    const long long nd = (long long)n_tok * dm.d;
+    if (w->ctx->peers && nd <= w->ctx->pa.mt_cap) {
+      // reduce-scatter + all-gather over the peer windows (no NCCL)
+      CU(moe::launch_peer_allreduce(delta, x, x_out, nd, w->ctx->pa, s));
+    } else {
+      TRY(allreduce(w, delta, (size_t)nd, s));
+      CU(moe::launch_add(x, delta, x_out, nd, s, false));
+    }
   }
   if (next_router)
     CU(moe::launch_router_topk(next_router, x_out, n_tok, dm, next_ids, next_gates, s, pdl));
@@ -598,44 +609,57 @@ int moe_ctx_set_virtual_rank(moe_ctx* c, int world, int rank) {
   return MOE_OK;
 }
 
-static int alloc_window(moe_ctx* c, int world, int max_hidden) {
+static int alloc_window(moe_ctx* c, int world, int max_hidden, int max_tokens) {
   if (world < 1 || world > moe::kMaxRanks) return fail(MOE_ERR_ARG, "world must be 1..8");
   if (max_hidden < 1) return fail(MOE_ERR_ARG, "max_hidden < 1");
-  if (c->win && (c->win_world != world || c->win_hidden < max_hidden))
+  if (max_tokens < 0) return fail(MOE_ERR_ARG, "max_tokens < 0");
+  if (c->win && (c->win_world != world || c->win_hidden < max_hidden || c->win_tokens < max_tokens))
     return fail(MOE_ERR_ARG, "peer window already allocated with another geometry");
   if (!c->win) {
     TRY(set_device(c));
-    const size_t bytes = moe::peer_window_bytes(world, max_hidden);
+    const size_t bytes = moe::peer_window_bytes(world, max_hidden, max_tokens);
     CU(cudaMalloc(&c->win, bytes));
     CU(cudaMemset(c->win, 0, bytes));
     CU(cudaDeviceSynchronize());
     c->win_world = world;
     c->win_hidden = max_hidden;
+    c->win_tokens = max_tokens;
   }
   return MOE_OK;
 }
 
 static void set_peer_parts(moe_ctx* c, int r, void* base) {
-  const moe::PeerParts q = moe::peer_window_parts(base, c->win_world, c->win_hidden);
+  const moe::PeerParts q = moe::peer_window_parts(base, c->win_world, c->win_hidden, c->win_tokens);
   c->pa.inbox[r] = q.inbox;
   c->pa.flags[r] = q.flags;
   c->pa.zbox[r] = q.zbox;
   c->pa.zflags[r] = q.zflags;
+  c->pa.mt_recv[r] = q.mt_recv;
+  c->pa.mt_gath[r] = q.mt_gath;
+  c->pa.mt_pflag[r] = q.mt_pflag;
+  c->pa.mt_gflag[r] = q.mt_gflag;
 }
 
 static void set_own_parts(moe_ctx* c, int world, int rank) {
-  const moe::PeerParts q = moe::peer_window_parts(c->win, world, c->win_hidden);
+  const moe::PeerParts q = moe::peer_window_parts(c->win, world, c->win_hidden, c->win_tokens);
   set_peer_parts(c, rank, c->win);
   c->pa.seq = q.seq;
   c->pa.zseq = q.zseq;
   c->pa.err = q.err;
+  c->pa.mt_seq = q.mt_seq;
+  c->pa.mt_cap = (long long)c->win_tokens * c->win_hidden;
   c->pa.world = world;
   c->pa.rank = rank;
 }
 
 int moe_ctx_peer_window(moe_ctx* c, int world, int max_hidden, void* ipc_handle) {
+  return moe_ctx_peer_window_tokens(c, world, max_hidden, 0, ipc_handle);
+}
+
+int moe_ctx_peer_window_tokens(moe_ctx* c, int world, int max_hidden, int max_tokens,
+                               void* ipc_handle) {
   if (!c) return fail(MOE_ERR_ARG, "null ctx");
-  TRY(alloc_window(c, world, max_hidden));
+  TRY(alloc_window(c, world, max_hidden, max_tokens));
   if (ipc_handle) {
     cudaIpcMemHandle_t h;
     CU(cudaIpcGetMemHandle(&h, c->win));
@@ -669,12 +693,16 @@ int moe_ctx_open_peers(moe_ctx* c, int world, int rank, const void* handles) {
 }
 
 int moe_ctx_link_peers(moe_ctx* const* ctxs, int world, int max_hidden) {
+  return moe_ctx_link_peers_tokens(ctxs, world, max_hidden, 0);
+}
+
+int moe_ctx_link_peers_tokens(moe_ctx* const* ctxs, int world, int max_hidden, int max_tokens) {
   if (!ctxs) return fail(MOE_ERR_ARG, "null ctxs");
   if (world < 2 || world > moe::kMaxRanks) return fail(MOE_ERR_ARG, "world must be 2..8");
   for (int r = 0; r < world; ++r) {
     if (!ctxs[r]) return fail(MOE_ERR_ARG, "null ctx");
     if (ctxs[r]->comm) return fail(MOE_ERR_ARG, "context already has a communicator");
-    TRY(alloc_window(ctxs[r], world, max_hidden));
+    TRY(alloc_window(ctxs[r], world, max_hidden, max_tokens));
   }
   for (int r = 0; r < world; ++r)
     for (int q = 0; q < world; ++q) {
@@ -835,6 +863,18 @@ int moe_weights_create(moe_ctx* c, const moe_shape* shape, int dtype, const int3
 
 int moe_weights_create_tp(moe_ctx* c, const moe_shape* shape, int dtype, moe_weights** out) {
   return weights_create(c, shape, dtype, nullptr, true, out);
+}
+
+int moe_weights_reserve(moe_weights* w, int max_tokens) {
+  if (!w) return fail(MOE_ERR_ARG, "null weights");
+  if (max_tokens < 1) return fail(MOE_ERR_ARG, "max_tokens < 1");
+  std::lock_guard<std::mutex> lk(w->mu);
+  TRY(set_device(w->ctx));
+  TRY(ensure_scratch(w, max_tokens));
+  if (max_tokens > 1 && use_prefill(w, max_tokens, nullptr)) TRY(ensure_prefill_scratch(w, max_tokens));
+  if (w->plan.ok) TRY(ensure_scratch(w, 1));
+  TRY(refresh_projection(w));
+  return MOE_OK;
 }
 
 int moe_weights_tp(const moe_weights* w, int* tp_world, int* tp_rank, int* ffn_local) {

@@ -1038,12 +1038,19 @@ cudaError_t launch_reduce_residual(const float* ypart, int nparts, const float* 
                             next_router, dm.E, dm.k, rpart, counter, next_ids, next_gates);
 }
 
-size_t peer_window_bytes(int world, int max_hidden) {
-  return 2 * (size_t)world * max_hidden * 4 + (size_t)world * kPeerSlots * 4 +
-         2 * (size_t)world * kMaxExperts * 4 + 64 + kPeerSlots * 4 + 64;
+static size_t mt_bytes(int world, int max_hidden, int max_tokens) {
+  if (max_tokens <= 0) return 0;
+  const size_t cap = (size_t)max_tokens * max_hidden;
+  return 2 * (size_t)world * cap * 4 + 2 * cap * 4 + (size_t)(world + 2) * kMtBlocks * 4;
 }
 
-PeerParts peer_window_parts(void* base, int world, int max_hidden) {
+size_t peer_window_bytes(int world, int max_hidden, int max_tokens) {
+  return 2 * (size_t)world * max_hidden * 4 + (size_t)world * kPeerSlots * 4 +
+         2 * (size_t)world * kMaxExperts * 4 + 64 + kPeerSlots * 4 + 64 +
+         mt_bytes(world, max_hidden, max_tokens);
+}
+
+PeerParts peer_window_parts(void* base, int world, int max_hidden, int max_tokens) {
   PeerParts q;
   char* p = static_cast<char*>(base);
   q.inbox = reinterpret_cast<float*>(p);
@@ -1058,7 +1065,78 @@ PeerParts peer_window_parts(void* base, int world, int max_hidden) {
   p += kPeerSlots * 4;
   q.zseq = reinterpret_cast<unsigned*>(p);
   q.err = q.zseq + 1;
+  p += 64;
+  q.mt_recv = q.mt_gath = nullptr;
+  q.mt_pflag = q.mt_gflag = q.mt_seq = nullptr;
+  if (max_tokens > 0) {
+    const size_t cap = (size_t)max_tokens * max_hidden;
+    q.mt_recv = reinterpret_cast<float*>(p);
+    p += 2 * (size_t)world * cap * 4;
+    q.mt_gath = reinterpret_cast<float*>(p);
+    p += 2 * cap * 4;
+    q.mt_pflag = reinterpret_cast<unsigned*>(p);
+    p += (size_t)world * kMtBlocks * 4;
+    q.mt_gflag = reinterpret_cast<unsigned*>(p);
+    p += kMtBlocks * 4;
+    q.mt_seq = reinterpret_cast<unsigned*>(p);
+  }
   return q;
+}
+
+// Multi-token peer allreduce.  Block b owns elements [b*n/B, (b+1)*n/B).
+//  1 every rank pushes its delta chunk into the owner's recv[par][rank],
+//    fence.sys, releases pflag[rank][b] on the owner;
+//  2 the owner (rank b % world) waits for all ranks' pflag, sums recv in rank
+//    order, pushes the sum into every rank's gath[par], releases gflag[b];
+//  3 every rank waits for its gflag[b] and writes x_out = x + gath.
+// Parity = the block's sequence number & 1: a rank reaches call c+2 only
+// after call c+1 completed everywhere for this block, so no copy is
+// overwritten before it is read.
+__global__ void __launch_bounds__(256) peer_allreduce_kernel(const float* __restrict__ delta,
+                                                             const float* x, float* x_out,
+                                                             long long n, PeerArgs pa) {
+  __shared__ unsigned s_seq;
+  const int b = blockIdx.x, B = gridDim.x, tid = threadIdx.x;
+  const int W = pa.world, rk = pa.rank, owner = b % W;
+  const long long e0 = n * b / B, e1 = n * (b + 1) / B;
+  const long long cap = pa.mt_cap;
+  if (tid == 0) s_seq = pa.mt_seq[b] + 1u;
+  __syncthreads();
+  const unsigned seq = s_seq;
+  const long long par = seq & 1u;
+  // 1: scatter this rank's chunk to its owner
+  float* dst = pa.mt_recv[owner] + (par * W + rk) * cap;
+  for (long long i = e0 + tid; i < e1; i += blockDim.x) dst[i] = delta[i];
+  __threadfence_system();
+  __syncthreads();
+  if (tid == 0) st_release_sys(pa.mt_pflag[owner] + (size_t)rk * kMtBlocks + b, seq);
+  // 2: the owner reduces in rank order and gathers to everyone
+  if (rk == owner) {
+    if (tid < W) peer_wait(pa.mt_pflag[rk] + (size_t)tid * kMtBlocks + b, seq, pa.err);
+    __syncthreads();
+    const float* in = pa.mt_recv[rk] + par * W * cap;
+    for (long long i = e0 + tid; i < e1; i += blockDim.x) {
+      float sum = 0.f;
+      for (int r = 0; r < W; ++r) sum += __ldcv(in + (size_t)r * cap + i);
+      for (int r = 0; r < W; ++r) pa.mt_gath[r][par * cap + i] = sum;
+    }
+    __threadfence_system();
+    __syncthreads();
+    if (tid < W) st_release_sys(pa.mt_gflag[tid] + b, seq);
+  }
+  // 3: residual
+  if (tid == 0) peer_wait(pa.mt_gflag[rk] + b, seq, pa.err);
+  __syncthreads();
+  const float* g = pa.mt_gath[rk] + par * cap;
+  for (long long i = e0 + tid; i < e1; i += blockDim.x) x_out[i] = x[i] + __ldcv(g + i);
+  if (tid == 0) pa.mt_seq[b] = seq;
+}
+
+cudaError_t launch_peer_allreduce(const float* delta, const float* x, float* x_out, long long n,
+                                  const PeerArgs& pa, cudaStream_t s) {
+  if (n <= 0) return cudaSuccess;
+  peer_allreduce_kernel<<<kMtBlocks, 256, 0, s>>>(delta, x, x_out, n, pa);
+  return cudaGetLastError();
 }
 
 cudaError_t launch_reduce_exchange(const float* ypart, int nparts, const float* x, float* x_out,

@@ -94,6 +94,14 @@ int reduce_blocks(const Dims& dm);
 // one per exchange on every rank alike, and selects the inbox parity.
 constexpr int kMaxRanks = 8;
 constexpr int kPeerSlots = 512;
+// Multi-token area (optional, max_tokens > 0): a reduce-scatter + all-gather
+// of [n x d] deltas over kMtBlocks element blocks; block b is summed by rank
+// b % world.  recv [2 parity][world][cap] | gath [2][cap] fp32 |
+// pflag [world][kMtBlocks] | gflag [kMtBlocks] | seq [kMtBlocks] u32.
+// 32 blocks: plenty for NVLink-rate pushes, and small enough that several
+// ranks' spinning exchange kernels stay co-resident when ranks share one GPU
+// (tests): with 128 blocks only two ranks' kernels were resident at once.
+constexpr int kMtBlocks = 32;
 struct PeerArgs {
   float* inbox[kMaxRanks];     // rank r's inbox base
   unsigned* flags[kMaxRanks];  // rank r's flags base
@@ -102,6 +110,12 @@ struct PeerArgs {
   unsigned* seq;               // own per-slot exchange counters
   unsigned* zseq;              // own router-partial exchange counter
   unsigned* err;               // own: set when a peer never arrives (bounded wait)
+  float* mt_recv[kMaxRanks];
+  float* mt_gath[kMaxRanks];
+  unsigned* mt_pflag[kMaxRanks];
+  unsigned* mt_gflag[kMaxRanks];
+  unsigned* mt_seq;            // own
+  long long mt_cap;            // elements per copy (max_tokens x max_hidden; 0 = none)
   int world, rank;
 };
 struct PeerParts {
@@ -110,10 +124,18 @@ struct PeerParts {
   float* zbox;
   unsigned* zflags;
   unsigned *seq, *zseq, *err;
+  float *mt_recv, *mt_gath;
+  unsigned *mt_pflag, *mt_gflag, *mt_seq;
 };
-size_t peer_window_bytes(int world, int max_hidden);
+size_t peer_window_bytes(int world, int max_hidden, int max_tokens = 0);
 // Carve a window allocation into its parts (same layout on every rank).
-PeerParts peer_window_parts(void* base, int world, int max_hidden);
+PeerParts peer_window_parts(void* base, int world, int max_hidden, int max_tokens = 0);
+// Multi-token combine over peer memory (prefill under EP/TP): x_out = x + the
+// rank-ordered sum of every rank's delta [n], as a reduce-scatter (block b
+// summed by rank b % world) + all-gather through the windows; bit-identical
+// on every rank, no NCCL.  n <= pa.mt_cap.
+cudaError_t launch_peer_allreduce(const float* delta, const float* x, float* x_out, long long n,
+                                  const PeerArgs& pa, cudaStream_t s);
 // x_out = x + sum_{r in rank order} delta_r, where delta_r = this layer's
 // fixed-order sum of rank r's per-CTA partials.  Each block reduces 32 hidden
 // columns, stores them into every peer's inbox (P2P stores), releases a

@@ -4,6 +4,14 @@ import sys
 import pytest
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+# Several peer-linked "ranks" share one GPU in the multi-rank tests, each with
+# its own streams.  With CUDA's default 8 hardware work queues, two ranks'
+# streams can land on one queue, and a rank's kernel that spins on another
+# rank's flags then blocks that rank's kernels queued behind it (a false
+# dependency that only times out).  Give every stream its own queue.  (Set
+# before the CUDA context exists; on real multi-GPU runs each rank owns a GPU.)
+os.environ.setdefault("CUDA_DEVICE_MAX_CONNECTIONS", "32")
 if ROOT not in sys.path:
     sys.path.insert(0, ROOT)
 

@@ -46,7 +46,7 @@ def _rank_main(rank, world, port, q, kernel, mode):
         full.random(3)
         ctx = M.Ctx(0)
         handles = [None] * world
-        dist.all_gather_object(handles, ctx.peer_window(world, d))
+        dist.all_gather_object(handles, ctx.peer_window(world, d, max_tokens=16))
         ctx.open_peers(world, rank, handles)
         if mode == "tp":
             w = M.Weights(ctx, s, M.DTYPE_F32, tp=True)
@@ -54,6 +54,7 @@ def _rank_main(rank, world, port, q, kernel, mode):
             owner = np.array([[e % world for e in range(E)] for _ in range(L)], np.int32)
             w = M.Weights(ctx, s, M.DTYPE_F32, owner=owner)
         assert w.forward_launches(1) == (1 if kernel == "stack" else 1 + 2 * L)
+        w.reserve(1)
         w.random(3)
         gen = torch.Generator(device="cuda").manual_seed(5)
         x0 = torch.randn(2, d, device="cuda", generator=gen)
@@ -77,6 +78,23 @@ def _rank_main(rank, world, port, q, kernel, mode):
             got = (x - x0[t:t + 1]).double().cpu().numpy()
             errs.append(float(np.abs(got - want).max() / np.abs(want).max()))
             assert torch.equal(ids, idr)
+        # a 16-token (prefill) layer: the multi-token peer allreduce
+        xm = torch.randn(16, d, device="cuda", generator=torch.Generator(device="cuda").manual_seed(9))
+        wm = torch.empty_like(xm)
+        full.layer_forward(0, xm, wm, torch.zeros((16, k), dtype=torch.int32, device="cuda"),
+                           torch.zeros((16, k), device="cuda"), stream=base.stream)
+        base.synchronize()
+        om = torch.empty_like(xm)
+        idm = torch.zeros((16, k), dtype=torch.int32, device="cuda")
+        gm = torch.zeros((16, k), device="cuda")
+        w.reserve(16)
+        torch.cuda.synchronize()  # inputs made on torch's stream, kernels on ctx.stream
+        dist.barrier()
+        w.layer_forward(0, xm, om, idm, gm, stream=ctx.stream)
+        ctx.synchronize()
+        ctx.peer_check()
+        dm_, dw_ = (om - xm).double(), (wm - xm).double()
+        errs.append(float((dm_ - dw_).abs().max() / dw_.abs().max()))
         q.put((rank, max(errs), None))
         dist.barrier()
         w.close()

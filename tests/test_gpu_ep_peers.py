@@ -87,6 +87,7 @@ def test_peer_combine_matches_unsharded(gpu, monkeypatch, kernel, mode, world, s
         ws = [M.Weights(c, s, dtype, tp=True) for c in ctxs]
     for w in ws:
         w.random(11)
+        w.reserve(1)  # no allocation (cudaFree = device sync) once ranks start spinning
         assert w.forward_launches(1) == (1 + 2 * L if kernel == "layer" else 1)
     torch.cuda.synchronize()
     # fixed per-rank buffers, refilled per token (as a serving loop does): each
@@ -118,6 +119,62 @@ def test_peer_combine_matches_unsharded(gpu, monkeypatch, kernel, mode, world, s
                 first = outs[0].copy()
             if rep == 1 and t == 0:
                 assert np.array_equal(outs[0], first), "not deterministic"
+    for w in ws:
+        w.close()
+    for c in ctxs:
+        c.close()
+    full.close()
+    base.close()
+
+
+@pytest.mark.parametrize("mode", ["ep", "tp"])
+@pytest.mark.parametrize("world,shape,dtype,n_tok", [
+    (2, (1, 8, 2, 4096, 14336, 2), M.DTYPE_BF16, 64),   # tcgen05 prefill per rank
+    (4, (1, 8, 2, 256, 1024, 2), M.DTYPE_BF16, 96),     # tcgen05, TP f/4 = 256
+    (2, (1, 8, 2, 48, 80, 4), M.DTYPE_F32, 5),          # generic kernels
+    (4, (1, 8, 2, 48, 80, 4), M.DTYPE_F32, 5),          # generic kernels, 4 ranks
+])
+def test_peer_multi_token_combine(gpu, mode, world, shape, dtype, n_tok):
+    """Multi-token (prefill) layers under EP / TP with the windows' multi-token
+    area: the reduce-scatter + all-gather kernel replaces ncclAllReduce; all
+    ranks bit-identical and equal to the unsharded layer within fp32 rounding."""
+    L, E, k, d = shape[0], shape[1], shape[2], shape[3]
+    s = M.Shape(*shape)
+    base = M.Ctx(0)
+    full = M.Weights(base, s, dtype)
+    full.random(13)
+    x = torch.randn(n_tok, d, device="cuda", generator=torch.Generator(device="cuda").manual_seed(7))
+    want = torch.empty_like(x)
+    ids = torch.zeros((n_tok, k), dtype=torch.int32, device="cuda")
+    g = torch.zeros((n_tok, k), device="cuda")
+    full.layer_forward(0, x, want, ids, g, stream=base.stream)
+    base.synchronize()
+    ctxs = [M.Ctx(0) for _ in range(world)]
+    M.Ctx.link_peers(ctxs, d, max_tokens=n_tok)
+    if mode == "ep":
+        owner = _bench().shard_map(L, E, world)
+        ws = [M.Weights(c, s, dtype, owner=owner) for c in ctxs]
+    else:
+        ws = [M.Weights(c, s, dtype, tp=True) for c in ctxs]
+    for w in ws:
+        w.random(13)
+        w.reserve(n_tok)
+    outs = [torch.empty_like(x) for _ in range(world)]
+    idss = [torch.zeros_like(ids) for _ in range(world)]
+    gs = [torch.zeros_like(g) for _ in range(world)]
+    torch.cuda.synchronize()
+    for rep in range(2):
+        for r in range(world):
+            ws[r].layer_forward(0, x, outs[r], idss[r], gs[r], stream=ctxs[r].stream)
+        for c in ctxs:
+            c.synchronize()
+            c.peer_check()
+        for r in range(1, world):
+            assert torch.equal(outs[r], outs[0]) and torch.equal(idss[r], idss[0])
+        assert torch.equal(idss[0], ids)
+        xd = x.double()
+        err = float(((outs[0].double() - xd) - (want.double() - xd)).abs().max() / (want.double() - xd).abs().max())
+        assert err < 1e-4, err
     for w in ws:
         w.close()
     for c in ctxs:

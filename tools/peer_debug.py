@@ -1,4 +1,5 @@
 import os, sys, importlib.util
+os.environ.setdefault("CUDA_DEVICE_MAX_CONNECTIONS", "32")  # see tests/conftest.py
 sys.path.insert(0, "/root/repo")
 import numpy as np, torch
 import paper_2402_07033_b200 as M
