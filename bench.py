@@ -163,6 +163,20 @@ def shard_map(L, E, world, rank_tokens=None):
     return owner
 
 
+def replica_map(owner, world, rank_tokens=None, hot=1):
+    """[L x E] rank bitmasks of extra expert holders: per
+    layer the `hot` most popular experts (reference ranking, placement.cpp:53-64)
+    are replicated on every rank; the prefill path then splits their tokens
+    over the holders per step (replica_plan.h)."""
+    L, E = owner.shape
+    counts = np.ones((L, E), np.int64) if rank_tokens is None else rank_tokens
+    mask = np.zeros((L, E), np.uint32)
+    for l in range(L):
+        for e in sorted(range(E), key=lambda e: (-counts[l, e], e))[:hot]:
+            mask[l, e] = (1 << world) - 1
+    return mask
+
+
 # ---------------------------------------------------------------------------
 def run_ours(args):
     import torch
@@ -216,6 +230,11 @@ def run_ours(args):
             x.copy_(pool[i:i + 1])
         w.forward(x, ids, gates, stream=stream_ptr)
 
+    # every rank's weights are initialised before the first peer exchange (the
+    # in-kernel peer waits are bounded, so a rank still in w.random() must not
+    # be waited on)
+    torch.cuda.synchronize()
+    barrier(world)
     for i in range(args.warmup):
         step(i)
     torch.cuda.synchronize()

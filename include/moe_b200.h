@@ -114,6 +114,35 @@ int moe_weights_create(moe_ctx* ctx, const moe_shape* shape, int dtype,
  * layout; download fills only this rank's slice of the full-size buffers. */
 int moe_weights_create_tp(moe_ctx* ctx, const moe_shape* shape, int dtype, moe_weights** out);
 int moe_weights_tp(const moe_weights* w, int* tp_world, int* tp_rank, int* ffn_local);
+/* Expert parallelism with replicated hot experts (the
+ * reference scheduler's min-max split, scheduler.cpp:97-204, re-expressed
+ * for expert-parallel load balance).  replica_mask: optional [L*E] rank
+ * bitmasks; bit r set = rank r also holds expert (l, e) besides its owner
+ * (world <= 8).  Decode and the generic kernels run every expert on its
+ * owner only; the tcgen05 prefill path splits each expert's sorted rows over
+ * its holders per step, on the device, with the plan of moe_replica_plan
+ * (identical on all ranks; no host sync, no exchange). */
+int moe_weights_create_ep(moe_ctx* ctx, const moe_shape* shape, int dtype,
+                          const int32_t* owner_rank, const uint32_t* replica_mask,
+                          moe_weights** out);
+/* The split's cost model, picoseconds: m rows of one expert on one rank cost
+ * part_ps + max(weight_ps, m * row_ps) — a fixed ramp, streaming the
+ * expert's weights, tensor-core time per (token, slot) row.  Defaults from
+ * the grouped kernel on B200: 6.54 TB/s (3*d*f*esize B), 1.25 PFLOP/s
+ * (6*d*f flop per row), part_ps = 2/3 weight_ps. */
+int moe_weights_set_replica_cost(moe_weights* w, int64_t weight_ps, int64_t row_ps,
+                                 int64_t part_ps);
+int moe_weights_replica_cost(const moe_weights* w, int64_t* weight_ps, int64_t* row_ps,
+                             int64_t* part_ps);
+/* Host mirror of the device planner (same code, replica_plan.h): experts by
+ * (count desc, id asc); each takes the number q of its least-loaded holders
+ * that minimises the max rank load, where m rows on a rank cost
+ * max(weight_ps, m * row_ps) and rows are dealt in `chunk`-row pieces (ties:
+ * fewer holders).  Writes rank `rank`'s rows [lo[e], hi[e]) of every expert
+ * and the plan's makespan (ps).  Needs no device. */
+int moe_replica_plan(const int32_t* counts, int E, const uint32_t* holders, int world,
+                     int64_t weight_ps, int64_t row_ps, int64_t part_ps, int chunk, int rank,
+                     int32_t* lo, int32_t* hi, int64_t* makespan);
 /* Allocate every scratch buffer for calls of up to max_tokens tokens (and the
  * batch-1 router projections) now, so no later call allocates or frees
  * device memory (cudaFree synchronizes the device).  Serving loops and

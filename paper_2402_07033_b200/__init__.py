@@ -23,4 +23,5 @@ from .capi import (  # noqa: F401
     declared_symbols,
     lib,
     lib_path,
+    replica_plan,
 )

@@ -97,6 +97,11 @@ def lib():
         "moe_ctx_link_peers_tokens": ([C.POINTER(_vp), C.c_int, C.c_int, C.c_int], C.c_int),
         "moe_weights_create": ([_vp, C.POINTER(_Shape), C.c_int, _vp, C.POINTER(_vp)], C.c_int),
         "moe_weights_create_tp": ([_vp, C.POINTER(_Shape), C.c_int, C.POINTER(_vp)], C.c_int),
+        "moe_weights_create_ep": ([_vp, C.POINTER(_Shape), C.c_int, _vp, _vp, C.POINTER(_vp)], C.c_int),
+        "moe_weights_set_replica_cost": ([_vp, C.c_int64, C.c_int64, C.c_int64], C.c_int),
+        "moe_weights_replica_cost": ([_vp] + [C.POINTER(C.c_int64)] * 3, C.c_int),
+        "moe_replica_plan": ([_vp, C.c_int, _vp, C.c_int, C.c_int64, C.c_int64, C.c_int64, C.c_int,
+                              C.c_int, _vp, _vp, C.POINTER(C.c_int64)], C.c_int),
         "moe_weights_reserve": ([_vp, C.c_int], C.c_int),
         "moe_weights_tp": ([_vp, C.POINTER(C.c_int), C.POINTER(C.c_int), C.POINTER(C.c_int)], C.c_int),
         "moe_weights_destroy": ([_vp], C.c_int),
@@ -276,9 +281,12 @@ class Ctx:
 
 
 class Weights:
-    def __init__(self, ctx: Ctx, shape: Shape, dtype: int = DTYPE_BF16, owner=None, tp=False):
+    def __init__(self, ctx: Ctx, shape: Shape, dtype: int = DTYPE_BF16, owner=None, tp=False,
+                 replicas=None):
         """owner: expert-parallel [L x E] shard map; tp=True: tensor-parallel
-        shard (ffn rows of every expert) over the context's (world, rank)."""
+        shard (ffn rows of every expert) over the context's (world, rank);
+        replicas: [L x E] rank bitmasks of extra holders of each expert (the
+        prefill path splits a hot expert's tokens over its holders)."""
         self.ctx = ctx
         self.shape = shape
         self.dtype = dtype
@@ -291,9 +299,25 @@ class Weights:
             if owner is not None:
                 self._owner = np.ascontiguousarray(owner, np.int32).ravel()
                 own = self._owner.ctypes.data_as(_vp)
-            check(lib().moe_weights_create(ctx.h, C.byref(sh), dtype, own, C.byref(h)))
+            if replicas is not None:
+                self._replicas = np.ascontiguousarray(replicas, np.uint32).ravel()
+                check(lib().moe_weights_create_ep(ctx.h, C.byref(sh), dtype, own,
+                                                  self._replicas.ctypes.data_as(_vp), C.byref(h)))
+            else:
+                check(lib().moe_weights_create(ctx.h, C.byref(sh), dtype, own, C.byref(h)))
         self.h = h
         ctx._weights.add(self)
+
+    @property
+    def replica_cost(self):
+        """(weight_ps, row_ps, part_ps) of the replica split's cost model."""
+        a, b, c = C.c_int64(), C.c_int64(), C.c_int64()
+        check(lib().moe_weights_replica_cost(self.h, C.byref(a), C.byref(b), C.byref(c)))
+        return a.value, b.value, c.value
+
+    @replica_cost.setter
+    def replica_cost(self, v):
+        check(lib().moe_weights_set_replica_cost(self.h, int(v[0]), int(v[1]), int(v[2])))
 
     def reserve(self, max_tokens: int):
         """Allocate all scratch for calls of up to max_tokens tokens now."""
@@ -409,3 +433,18 @@ class Weights:
 
     def forward_launches(self, n_tok: int) -> int:
         return lib().moe_forward_launches(self.h, n_tok)
+
+
+def replica_plan(counts, holders, world, weight_ps, row_ps, part_ps, chunk, rank):
+    """Host mirror of the device replica planner (moe_replica_plan): rank
+    `rank`'s rows (lo[e], hi[e]) of every expert and the plan's makespan."""
+    c = np.ascontiguousarray(counts, np.int32)
+    hm = np.ascontiguousarray(holders, np.uint32)
+    E = c.size
+    lo = np.zeros(E, np.int32)
+    hi = np.zeros(E, np.int32)
+    mk = C.c_int64()
+    check(lib().moe_replica_plan(c.ctypes.data_as(_vp), E, hm.ctypes.data_as(_vp), world,
+                                 int(weight_ps), int(row_ps), int(part_ps), chunk, rank,
+                                 lo.ctypes.data_as(_vp), hi.ctypes.data_as(_vp), C.byref(mk)))
+    return lo, hi, mk.value

@@ -16,6 +16,7 @@
 
 #include "../../include/moe_b200.h"
 #include "kernels.h"
+#include "replica_plan.h"
 
 using moe::Dims;
 using moe::LayerWeights;
@@ -142,7 +143,12 @@ struct moe_weights {
   int dtype = MOE_DTYPE_BF16;
   int esize = 2;
   std::vector<int32_t> owner;      // [L*E]
-  std::vector<int16_t> slot_of;    // [L*E]
+  std::vector<int16_t> slot_of;    // [L*E] resident slot (owned or replica), -1 = not here
+  std::vector<int16_t> exec_slot;  // [L*E] slot if this rank OWNS the expert, else -1
+  std::vector<uint32_t> holders;   // [L*E] rank bitmask: owner | replicas
+  bool replicas = false;           // some expert is held by more than one rank
+  long long rep_weight_ps = 0, rep_row_ps = 0, rep_part_ps = 0;  // replica split cost model
+  DevBuf dev_holders, dev_res_slots, pf_counts2, pf_offsets2;
   std::vector<int> n_local;        // [L]
   std::vector<void*> layer_mem;    // [L] device, n_local[l] * 3*f*d elements
   float* router = nullptr;         // [L][E][d]
@@ -188,7 +194,7 @@ struct moe_weights {
     lw.mat_stride = mat_elems();
     lw.router = router + (size_t)l * E() * d();
     for (int e = 0; e < moe::kMaxExperts; ++e)
-      lw.slot_of[e] = e < E() ? slot_of[(size_t)l * E() + e] : (int16_t)-1;
+      lw.slot_of[e] = e < E() ? exec_slot[(size_t)l * E() + e] : (int16_t)-1;
     return lw;
   }
   void* expert_ptr(int l, int e, int m) const {
@@ -392,10 +398,22 @@ int experts_forward(moe_weights* w, int l, const float* x, int n_tok, const int3
     int32_t* perm = w->pf_perm.as<int32_t>();
     CU(moe::launch_permute(ids, n_tok, dm.k, dm.E, counts, offsets, perm, nullptr, s));
     const int S = w->prefill_splits;
-    if (w->n_local[l] < dm.E)
+    const int16_t* slots = w->dev_slots.as<int16_t>() + (size_t)l * dm.E;
+    if (w->replicas && S > 0) {
+      // replicated experts: this step's min-max share of every expert's rows
+      // (identical plan on every rank), over the resident slots
+      CU(moe::launch_replica_plan(counts, offsets, dm.E, w->dev_holders.as<uint32_t>() + (size_t)l * dm.E,
+                                  w->ctx->world, w->ctx->rank, w->rep_weight_ps, w->rep_row_ps,
+                                  w->rep_part_ps,
+                                  w->pf_counts2.as<int32_t>(), w->pf_offsets2.as<int32_t>(), s));
+      counts = w->pf_counts2.as<int32_t>();
+      offsets = w->pf_offsets2.as<int32_t>();
+      slots = w->dev_res_slots.as<int16_t>() + (size_t)l * dm.E;
+    }
+    if (w->n_local[l] < dm.E || w->replicas)
       CU(cudaMemsetAsync(w->y.p, 0, (size_t)std::max(1, S) * rows * dm.d * 4, s));
     CU(moe::launch_prefill_experts(lw, w->n_local[l], dm, n_tok, x, counts, offsets, perm, gates,
-                                   w->dev_slots.as<int16_t>() + (size_t)l * dm.E,
+                                   slots,
                                    w->pf_xg.as<__nv_bfloat16>(), w->pf_h.as<__nv_bfloat16>(),
                                    w->y.as<float>(), w->pf_sync.as<int>(), w->ctx->sm_count, S,
                                    s, sp));
@@ -759,7 +777,8 @@ int moe_ctx_world(moe_ctx* c, int* world, int* rank) {
 }
 
 static int weights_create(moe_ctx* c, const moe_shape* shape, int dtype,
-                          const int32_t* owner_rank, bool tensor_parallel, moe_weights** out) {
+                          const int32_t* owner_rank, bool tensor_parallel, moe_weights** out,
+                          const uint32_t* replica_mask = nullptr) {
   if (!c || !out) return fail(MOE_ERR_ARG, "null argument");
   *out = nullptr;
   TRY(check_shape(shape));
@@ -790,7 +809,29 @@ static int weights_create(moe_ctx* c, const moe_shape* shape, int dtype,
       w->owner[i] = owner_rank[i];
     }
   }
+  if (replica_mask && c->world > moe::kReplicaMaxRanks) {
+    delete w;
+    return fail(MOE_ERR_UNSUPPORTED, "replicas need world <= 8");
+  }
+  w->holders.assign((size_t)L * E, 0u);
+  for (size_t i = 0; i < (size_t)L * E; ++i) {
+    const uint32_t extra = replica_mask ? replica_mask[i] : 0u;
+    if (c->world < 32 && (extra >> c->world) != 0) {
+      delete w;
+      return fail(MOE_ERR_ARG, "replica mask names a rank >= world");
+    }
+    w->holders[i] = (c->world <= 32 ? (1u << w->owner[i]) : 0u) | extra;
+    if (extra & ~(1u << w->owner[i])) w->replicas = true;
+  }
+  // default split cost, from the grouped kernel on B200 (tools/replica_proxy.py):
+  // weights at the 6.54 TB/s copy peak (3*d*f*esize B), rows at 1.25 PFLOP/s
+  // (6*d*f flop; the 8192-token layer rate), and a fixed ~35 us per expert
+  // part (a 256-row part of a Mixtral expert measured ~90 us, not 54)
+  w->rep_weight_ps = (long long)(3.0 * shape->hidden_dim * w->f_local * w->esize * 1000.0 / 6540.0);
+  w->rep_row_ps = (long long)(6.0 * shape->hidden_dim * w->f_local / 1250.0);
+  w->rep_part_ps = w->rep_weight_ps * 2 / 3;
   w->slot_of.assign((size_t)L * E, -1);
+  w->exec_slot.assign((size_t)L * E, -1);
   w->n_local.assign(L, 0);
   w->layer_mem.assign(L, nullptr);
   auto cleanup = [&](int rc) {
@@ -800,7 +841,11 @@ static int weights_create(moe_ctx* c, const moe_shape* shape, int dtype,
   for (int l = 0; l < L; ++l) {
     int n = 0;
     for (int e = 0; e < E; ++e)
-      if (w->owner[(size_t)l * E + e] == c->rank) w->slot_of[(size_t)l * E + e] = (int16_t)n++;
+      if (w->owner[(size_t)l * E + e] == c->rank || ((w->holders[(size_t)l * E + e] >> c->rank) & 1u)) {
+        w->slot_of[(size_t)l * E + e] = (int16_t)n;
+        if (w->owner[(size_t)l * E + e] == c->rank) w->exec_slot[(size_t)l * E + e] = (int16_t)n;
+        ++n;
+      }
     w->n_local[l] = n;
     const size_t bytes = (size_t)n * 3 * w->mat_elems() * w->esize;
     if (bytes) {
@@ -844,12 +889,16 @@ static int weights_create(moe_ctx* c, const moe_shape* shape, int dtype,
     // device-side tables for the persistent stack kernel
     const int Lm = std::max(1, L);
     if (w->dev_layers.ensure(sizeof(void*) * Lm) || w->dev_slots.ensure(sizeof(int16_t) * Lm * E) ||
+        w->dev_res_slots.ensure(sizeof(int16_t) * Lm * E) || w->dev_holders.ensure(4 * (size_t)Lm * E) ||
+        w->pf_counts2.ensure(4 * (size_t)E) || w->pf_offsets2.ensure(4 * (size_t)E) ||
         w->xbuf2.ensure(sizeof(float) * 2 * shape->hidden_dim) || w->gbar.ensure(256) ||
         w->rpart.ensure(sizeof(float) * (size_t)std::max(c->sm_count, moe::reduce_blocks(w->dims())) * E))
       return cleanup(fail(MOE_ERR_OOM, "cudaMalloc stack tables"));
     if (L > 0 &&
         (cudaMemcpy(w->dev_layers.p, w->layer_mem.data(), sizeof(void*) * L, cudaMemcpyHostToDevice) ||
-         cudaMemcpy(w->dev_slots.p, w->slot_of.data(), sizeof(int16_t) * L * E, cudaMemcpyHostToDevice)))
+         cudaMemcpy(w->dev_slots.p, w->exec_slot.data(), sizeof(int16_t) * L * E, cudaMemcpyHostToDevice) ||
+         cudaMemcpy(w->dev_res_slots.p, w->slot_of.data(), sizeof(int16_t) * L * E, cudaMemcpyHostToDevice) ||
+         cudaMemcpy(w->dev_holders.p, w->holders.data(), 4 * (size_t)L * E, cudaMemcpyHostToDevice)))
       return cleanup(fail(MOE_ERR_CUDA, "upload stack tables"));
   }
   *out = w;
@@ -863,6 +912,48 @@ int moe_weights_create(moe_ctx* c, const moe_shape* shape, int dtype, const int3
 
 int moe_weights_create_tp(moe_ctx* c, const moe_shape* shape, int dtype, moe_weights** out) {
   return weights_create(c, shape, dtype, nullptr, true, out);
+}
+
+int moe_weights_create_ep(moe_ctx* c, const moe_shape* shape, int dtype, const int32_t* owner_rank,
+                          const uint32_t* replica_mask, moe_weights** out) {
+  return weights_create(c, shape, dtype, owner_rank, false, out, replica_mask);
+}
+
+int moe_weights_set_replica_cost(moe_weights* w, int64_t weight_ps, int64_t row_ps,
+                                 int64_t part_ps) {
+  if (!w) return fail(MOE_ERR_ARG, "null weights");
+  if (weight_ps < 0 || row_ps < 0 || part_ps < 0) return fail(MOE_ERR_ARG, "negative cost");
+  w->rep_weight_ps = weight_ps;
+  w->rep_row_ps = row_ps;
+  w->rep_part_ps = part_ps;
+  return MOE_OK;
+}
+
+int moe_weights_replica_cost(const moe_weights* w, int64_t* weight_ps, int64_t* row_ps,
+                             int64_t* part_ps) {
+  if (!w) return fail(MOE_ERR_ARG, "null weights");
+  if (weight_ps) *weight_ps = w->rep_weight_ps;
+  if (row_ps) *row_ps = w->rep_row_ps;
+  if (part_ps) *part_ps = w->rep_part_ps;
+  return MOE_OK;
+}
+
+int moe_replica_plan(const int32_t* counts, int E, const uint32_t* holders, int world,
+                     int64_t weight_ps, int64_t row_ps, int64_t part_ps, int chunk, int rank,
+                     int32_t* lo, int32_t* hi, int64_t* makespan) {
+  if (!counts || !holders || !lo || !hi) return fail(MOE_ERR_ARG, "null argument");
+  if (E < 1 || E > moe::kMaxExperts || world < 1 || world > moe::kReplicaMaxRanks || rank < 0 ||
+      rank >= world || chunk < 1 || weight_ps < 0 || row_ps < 0 || part_ps < 0)
+    return fail(MOE_ERR_ARG, "bad replica plan arguments");
+  std::vector<int32_t> order(E);
+  for (int e = 0; e < E; ++e) {
+    if (counts[e] < 0) return fail(MOE_ERR_ARG, "negative count");
+    order[moe::replica_order_pos(counts, E, e)] = e;
+  }
+  const moe::ReplicaCost c{weight_ps, row_ps, part_ps, chunk};
+  const long long mk = moe::replica_split_plan(counts, order.data(), E, holders, world, c, rank, lo, hi);
+  if (makespan) *makespan = mk;
+  return MOE_OK;
 }
 
 int moe_weights_reserve(moe_weights* w, int max_tokens) {

@@ -186,6 +186,16 @@ cudaError_t launch_prefill_experts(const LayerWeights& lw, int n_local, const Di
                                    __nv_bfloat16* xg, __nv_bfloat16* h, float* y, int* sync,
                                    int sm_count, int splits, cudaStream_t s,
                                    const SparsityCounters& sp = SparsityCounters());
+
+// Replicated experts under expert parallelism (replica_plan.h):
+// one block computes this rank's share [lo, hi) of every expert's sorted rows
+// from the step's counts and writes the grouped kernel's inputs
+// counts_out[e] = hi - lo, offsets_out[e] = offsets[e] + lo.
+// holders: [E] rank bitmasks of this layer.
+cudaError_t launch_replica_plan(const int32_t* counts, const int32_t* offsets, int E,
+                                const uint32_t* holders, int world, int rank, long long weight_ps,
+                                long long row_ps, long long part_ps, int32_t* counts_out,
+                                int32_t* offsets_out, cudaStream_t s);
 // splits > 0: persistent grouped kernel, y is [splits][n*k][d] (sum the splits);
 // splits == 0: two-kernel path, y is [n*k][d].  sync: 1 + E*ceil(n_tok/256) ints.
 

@@ -33,6 +33,7 @@
 #include "../../include/moe_b200.h"
 #include "common.cuh"
 #include "kernels.h"
+#include "replica_plan.h"
 
 namespace moe {
 
@@ -868,6 +869,43 @@ __global__ void gather_rows_kernel(const float* __restrict__ x, const int32_t* _
     const __nv_bfloat162 a = __floats2bfloat162_rn(v.x, v.y), b = __floats2bfloat162_rn(v.z, v.w);
     dst[i] = make_uint2(*reinterpret_cast<const uint32_t*>(&a), *reinterpret_cast<const uint32_t*>(&b));
   }
+}
+
+// This rank's share of every replicated expert's rows for one step
+// (replica_plan.h): order by (count desc, id asc) in parallel, then one
+// thread runs the min-max split (E <= 256, world <= 8: a few us at most).
+__global__ void __launch_bounds__(256) replica_plan_kernel(
+    const int32_t* __restrict__ counts, const int32_t* __restrict__ offsets, int E,
+    const uint32_t* __restrict__ holders, int world, int rank, ReplicaCost cost,
+    int32_t* counts_out, int32_t* offsets_out) {
+  __shared__ int32_t s_counts[kMaxExperts], s_order[kMaxExperts], s_lo[kMaxExperts],
+      s_hi[kMaxExperts];
+  __shared__ uint32_t s_hold[kMaxExperts];
+  griddep_wait();
+  for (int e = threadIdx.x; e < E; e += blockDim.x) {
+    s_counts[e] = counts[e];
+    s_hold[e] = holders[e];
+  }
+  __syncthreads();
+  for (int e = threadIdx.x; e < E; e += blockDim.x) s_order[replica_order_pos(s_counts, E, e)] = e;
+  __syncthreads();
+  if (threadIdx.x == 0) replica_split_plan(s_counts, s_order, E, s_hold, world, cost, rank, s_lo, s_hi);
+  __syncthreads();
+  for (int e = threadIdx.x; e < E; e += blockDim.x) {
+    counts_out[e] = s_hi[e] - s_lo[e];
+    offsets_out[e] = offsets[e] + s_lo[e];
+  }
+}
+
+cudaError_t launch_replica_plan(const int32_t* counts, const int32_t* offsets, int E,
+                                const uint32_t* holders, int world, int rank, long long weight_ps,
+                                long long row_ps, long long part_ps, int32_t* counts_out,
+                                int32_t* offsets_out, cudaStream_t s) {
+  if (E <= 0 || E > kMaxExperts || world < 1 || world > kReplicaMaxRanks) return cudaErrorInvalidValue;
+  const ReplicaCost c{weight_ps, row_ps, part_ps, kPrefillChunk};
+  replica_plan_kernel<<<1, 256, 0, s>>>(counts, offsets, E, holders, world, rank, c, counts_out,
+                                        offsets_out);
+  return cudaGetLastError();
 }
 
 // ---- host side -----------------------------------------------------------------

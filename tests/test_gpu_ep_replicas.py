@@ -1,0 +1,122 @@
+"""Expert parallelism with replicated hot experts, W ranks
+linked on ONE GPU (as tests/test_gpu_ep_peers.py).
+
+A router biased so that one expert is in every token's top-2 makes it the
+hot expert; it is replicated on every rank (bench.replica_map) and the
+device planner (replica_plan.h) splits its sorted rows over the holders each
+step.  Checks: the host mirror of the plan really splits the hot expert;
+every rank's output is bit-identical; routing equals the unsharded model;
+outputs match the unsharded layer within fp32 rounding; the decode path
+(owner-only execution) also matches.
+"""
+import importlib.util
+import os
+
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+import paper_2402_07033_b200 as M  # noqa: E402
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def _bench():
+    spec = importlib.util.spec_from_file_location("bench", os.path.join(ROOT, "bench.py"))
+    b = importlib.util.module_from_spec(spec)
+    spec.loader.exec_module(b)
+    return b
+
+
+@pytest.fixture(scope="module")
+def gpu():
+    if not torch.cuda.is_available():
+        pytest.skip("no GPU")
+    torch.cuda.init()
+
+
+def _hot_router(w, d, E):
+    r = w.download_router(0)
+    r[0, :] = 0.05  # x ~ N(1, 1): logit 0 ~ 0.05 * d >> the others
+    w.upload_router(0, r)
+    return r
+
+
+@pytest.mark.parametrize("world,n_tok", [(2, 2048), (4, 2048), (2, 300)])
+def test_replicated_hot_expert(gpu, world, n_tok):
+    L, E, k, d, f = 1, 8, 2, 4096, 14336
+    s = M.Shape(L, E, k, d, f, 2)
+    b = _bench()
+    base = M.Ctx(0)
+    full = M.Weights(base, s, M.DTYPE_BF16)
+    full.random(21)
+    router = _hot_router(full, d, E)
+    gen = torch.Generator(device="cuda").manual_seed(5)
+    x = torch.randn(n_tok, d, device="cuda", generator=gen) + 1.0
+    want = torch.empty_like(x)
+    ids = torch.zeros((n_tok, k), dtype=torch.int32, device="cuda")
+    g = torch.zeros((n_tok, k), device="cuda")
+    full.layer_forward(0, x, want, ids, g, stream=base.stream)
+    base.synchronize()
+    counts = np.bincount(ids.cpu().numpy().ravel(), minlength=E).astype(np.int32)
+    assert counts[0] == n_tok  # the hot expert is in every token's top-2
+
+    owner = b.shard_map(L, E, world)
+    mask = b.replica_map(owner, world)
+    assert mask[0, 0] == (1 << world) - 1
+    ctxs = [M.Ctx(0) for _ in range(world)]
+    M.Ctx.link_peers(ctxs, d, max_tokens=n_tok)
+    ws = [M.Weights(c, s, M.DTYPE_BF16, owner=owner, replicas=mask) for c in ctxs]
+    for w in ws:
+        w.random(21)
+        w.upload_router(0, router)
+        w.reserve(n_tok)
+    # the host mirror of the device plan: does the hot expert split?
+    holders = (1 << owner[0]).astype(np.uint32) | mask[0]
+    wps, rps, pps = ws[0].replica_cost
+    parts = [M.replica_plan(counts, holders, world, wps, rps, pps, 256, r) for r in range(world)]
+    n_hold = sum(int(p[1][0] > p[0][0]) for p in parts)
+    if n_tok >= 2048:
+        assert n_hold >= 2, parts
+    else:
+        assert n_hold == 1  # 300 rows: memory-bound, streaming it twice would not pay
+    outs = [torch.empty_like(x) for _ in range(world)]
+    idss = [torch.zeros_like(ids) for _ in range(world)]
+    gs = [torch.zeros_like(g) for _ in range(world)]
+    torch.cuda.synchronize()
+    xd = x.double()
+    for rep in range(2):
+        for r in range(world):
+            ws[r].layer_forward(0, x, outs[r], idss[r], gs[r], stream=ctxs[r].stream)
+        for c in ctxs:
+            c.synchronize()
+            c.peer_check()
+        for r in range(1, world):
+            assert torch.equal(outs[r], outs[0])
+        assert torch.equal(idss[0], ids)
+        err = float(((outs[0].double() - xd) - (want.double() - xd)).abs().max()
+                    / (want.double() - xd).abs().max())
+        assert err < 1e-4, err
+
+    # batch 1: every expert runs on its owner only (replicas idle)
+    x1 = x[:1].contiguous()
+    want1 = torch.empty_like(x1)
+    full.layer_forward(0, x1, want1, ids[:1], g[:1], stream=base.stream)
+    base.synchronize()
+    o1 = [torch.empty_like(x1) for _ in range(world)]
+    for r in range(world):
+        ws[r].layer_forward(0, x1, o1[r], idss[r][:1], gs[r][:1], stream=ctxs[r].stream)
+    for c in ctxs:
+        c.synchronize()
+        c.peer_check()
+    d1 = (want1.double() - x1.double()).abs().max()
+    err1 = float((o1[0].double() - want1.double()).abs().max() / d1)
+    assert err1 < 1e-4, err1
+    for w in ws:
+        w.close()
+    for c in ctxs:
+        c.close()
+    full.close()
+    base.close()
