@@ -31,6 +31,12 @@ std::vector<std::vector<int>> ep_shard_map(const PopularityProfile& profile, int
 // counts, e.g. a device routing histogram (moe_routing_histogram) read back
 // after a calibration run; ValidationError on ragged rows or negative counts.
 PopularityProfile profile_from_counts(const std::vector<std::vector<std::int64_t>>& counts);
+// Replicated hot experts (moe_weights_create_ep's replica_mask): per layer
+// the `hot` most popular experts (same ranking) are held by every rank; the
+// prefill path then splits their tokens over the holders per step by the
+// scheduler's min-max objective (scheduler.cpp:97-204).  world <= 8.
+std::vector<std::vector<std::uint32_t>> ep_replica_masks(const PopularityProfile& profile,
+                                                         int world, int hot);
 // Rank r's share as a Placement (capacity = its expert count).
 Placement rank_placement(const std::vector<std::vector<int>>& owner, int rank);
 

@@ -629,6 +629,23 @@ std::vector<std::vector<int>> ep_shard_map(const PopularityProfile& profile, int
   return owner;
 }
 
+std::vector<std::vector<std::uint32_t>> ep_replica_masks(const PopularityProfile& profile,
+                                                         int world, int hot) {
+  if (world < 1 || world > 8) throw ValidationError("replicas need 1 <= world <= 8");
+  if (hot < 0) throw ValidationError("hot must be >= 0");
+  const int L = profile.num_layers(), E = profile.experts_per_layer();
+  std::vector<std::vector<std::uint32_t>> mask(L, std::vector<std::uint32_t>(E, 0u));
+  for (int l = 0; l < L; ++l) {
+    std::vector<int> order(E);
+    std::iota(order.begin(), order.end(), 0);
+    std::stable_sort(order.begin(), order.end(), [&](int a, int b) {
+      return profile.counts[l][a] > profile.counts[l][b];
+    });
+    for (int i = 0; i < std::min(hot, E); ++i) mask[l][order[i]] = (1u << world) - 1u;
+  }
+  return mask;
+}
+
 PopularityProfile profile_from_counts(const std::vector<std::vector<std::int64_t>>& counts) {
   PopularityProfile p;
   p.counts = counts;

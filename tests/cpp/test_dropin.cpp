@@ -408,6 +408,16 @@ TEST("ep_shard_map: every expert owned once, balanced, popularity-spread", false
   }
 }
 
+TEST("ep_replica_masks: the hot experts of every layer on all ranks", false) {
+  const PopularityProfile p = b200::profile_from_counts({{3, 9, 1, 9}, {5, 0, 7, 2}});
+  const auto m = b200::ep_replica_masks(p, 4, 2);
+  CHECK(m.size() == 2);
+  CHECK((m[0] == std::vector<std::uint32_t>{0u, 15u, 0u, 15u}));  // ties: lower id first
+  CHECK((m[1] == std::vector<std::uint32_t>{15u, 0u, 15u, 0u}));
+  CHECK(b200::ep_replica_masks(p, 2, 0)[0] == std::vector<std::uint32_t>(4, 0u));
+  CHECK_THROWS_AS(b200::ep_replica_masks(p, 9, 1), ValidationError);
+}
+
 TEST("profile_from_counts == profile_from_trace on the same routing", false) {
   ModelShape shape;
   shape.num_layers = 2;
