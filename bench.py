@@ -5,8 +5,10 @@ Workload (BASELINE.json configs[3]): a 32-layer Mixtral-8x7B-shaped MoE stack
 random), fp32 residual stream, batch 1.  One step = one token through all
 32 MoE layers (router -> 2 experts -> combine -> residual, per layer).
 At N>1 (torchrun) the experts of every layer are sharded over the ranks by
-the popularity placement (expert parallelism, one all-reduce per layer); the
-metric is the single token stream's tok/s ("strong" scaling: fixed work).
+the popularity placement (expert parallelism; --shard tp: tensor parallelism)
+and every layer's partial deltas are combined over NVLink peer memory inside
+the persistent kernel (--nccl-combine: ncclAllReduce instead); the metric is
+the single token stream's tok/s ("strong" scaling: fixed work).
 
 Reported:
   value     tok/s with the token already in HBM (CUDA events, max over ranks)
