@@ -387,11 +387,85 @@ __global__ void __launch_bounds__(256) combine4_kernel(const float* x, const flo
   }
 }
 
+// top-2 with at most 2 K-split partials per slot (the tcgen05 prefill's
+// default): every load of the token's row (x, 2 slots x 2 partials) is issued
+// before the first add, instead of one dependent round per (slot, partial) —
+// the same adds in the same order as combine4_kernel, so bit-identical.
+__global__ void __launch_bounds__(256) combine_k2_kernel(const float* x, const float* __restrict__ y,
+                                                         const float* __restrict__ gates, int d,
+                                                         float* x_out, int nsplit, long long sstride,
+                                                         const int32_t* __restrict__ ids,
+                                                         const int32_t* __restrict__ split_of) {
+  griddep_wait();
+  griddep_launch_dependents();
+  const int t = blockIdx.x;
+  const float g0 = gates ? gates[(size_t)t * 2] : 1.0f;
+  const float g1 = gates ? gates[(size_t)t * 2 + 1] : 1.0f;
+  const int ns0 = split_of ? split_of[ids[(size_t)t * 2]] : nsplit;
+  const int ns1 = split_of ? split_of[ids[(size_t)t * 2 + 1]] : nsplit;
+  const int n4 = d / 4;
+  const float4* r00 = reinterpret_cast<const float4*>(y + ((size_t)t * 2) * d);
+  const float4* r10 = reinterpret_cast<const float4*>(y + ((size_t)t * 2 + 1) * d);
+  const float4* r01 = reinterpret_cast<const float4*>(y + sstride + ((size_t)t * 2) * d);
+  const float4* r11 = reinterpret_cast<const float4*>(y + sstride + ((size_t)t * 2 + 1) * d);
+  const float4 z = make_float4(0.f, 0.f, 0.f, 0.f);
+  for (int c0 = threadIdx.x; c0 < n4; c0 += blockDim.x * kCombineCols) {
+    float4 v00[kCombineCols], v01[kCombineCols], v10[kCombineCols], v11[kCombineCols],
+        xv[kCombineCols];
+#pragma unroll
+    for (int u = 0; u < kCombineCols; ++u) {
+      const int i4 = c0 + u * blockDim.x;
+      const bool in = i4 < n4;
+      v00[u] = in ? __ldg(r00 + i4) : z;
+      v10[u] = in ? __ldg(r10 + i4) : z;
+      v01[u] = in && ns0 > 1 ? __ldg(r01 + i4) : z;
+      v11[u] = in && ns1 > 1 ? __ldg(r11 + i4) : z;
+      xv[u] = in && x ? reinterpret_cast<const float4*>(x + (size_t)t * d)[i4] : z;
+    }
+#pragma unroll
+    for (int u = 0; u < kCombineCols; ++u) {
+      const int i4 = c0 + u * blockDim.x;
+      if (i4 >= n4) continue;
+      float4 acc = z;
+      acc.x += g0 * v00[u].x;
+      acc.y += g0 * v00[u].y;
+      acc.z += g0 * v00[u].z;
+      acc.w += g0 * v00[u].w;
+      if (ns0 > 1) {
+        acc.x += g0 * v01[u].x;
+        acc.y += g0 * v01[u].y;
+        acc.z += g0 * v01[u].z;
+        acc.w += g0 * v01[u].w;
+      }
+      acc.x += g1 * v10[u].x;
+      acc.y += g1 * v10[u].y;
+      acc.z += g1 * v10[u].z;
+      acc.w += g1 * v10[u].w;
+      if (ns1 > 1) {
+        acc.x += g1 * v11[u].x;
+        acc.y += g1 * v11[u].y;
+        acc.z += g1 * v11[u].z;
+        acc.w += g1 * v11[u].w;
+      }
+      float4 o = acc;
+      if (x) o = make_float4(xv[u].x + o.x, xv[u].y + o.y, xv[u].z + o.z, xv[u].w + o.w);
+      reinterpret_cast<float4*>(x_out + (size_t)t * d)[i4] = o;
+    }
+  }
+}
+
 cudaError_t launch_combine(const float* x, const float* y, const float* gates, int n_tok,
                            const Dims& dm, float* x_out, cudaStream_t s, bool pdl, int nsplit,
                            const int32_t* ids, const int32_t* split_of) {
   if (n_tok <= 0) return cudaSuccess;
   cudaLaunchAttribute attr[1];
+  const bool k2_off = getenv("MOE_B200_COMBINE4") != nullptr;  // A/B: the looped kernel
+  if (dm.d % 4 == 0 && dm.k == 2 && nsplit <= 2 && !k2_off) {
+    cudaLaunchConfig_t cfg = make_cfg(dim3(n_tok), dim3(256), s, pdl, attr);
+    const long long sstride = (long long)n_tok * dm.k * dm.d;
+    return cudaLaunchKernelEx(&cfg, combine_k2_kernel, x, y, gates, dm.d, x_out, nsplit, sstride,
+                              ids, split_of);
+  }
   if (dm.d % 4 == 0 && dm.k <= 32) {
     cudaLaunchConfig_t cfg = make_cfg(dim3(n_tok), dim3(256), s, pdl, attr);
     const long long sstride = (long long)n_tok * dm.k * dm.d;

@@ -412,6 +412,28 @@ def test_prefill_tcgen05_mixtral_layer_512(ctx, orc, monkeypatch):
     _prefill_case(ctx, orc, monkeypatch, 1, 4096, 14336, 512, 5, [0, 1, 77, 200, 311, 511])
 
 
+@pytest.mark.parametrize("n_tok", [512, 700])
+def test_combine_k2_equals_looped_combine(ctx, monkeypatch, n_tok):
+    """The top-2 combine that issues all loads up front (combine_k2_kernel)
+    is bit-identical to the looped combine (MOE_B200_COMBINE4) on the
+    tcgen05 prefill path, K-split partials included."""
+    w = M.Weights(ctx, M.Shape(1, 8, 2, 4096, 14336, 2), M.DTYPE_BF16)
+    w.random(3)
+    x = torch.randn(n_tok, 4096, device="cuda")
+    outs = []
+    for env in (None, "1"):
+        if env:
+            monkeypatch.setenv("MOE_B200_COMBINE4", env)
+        o = torch.empty_like(x)
+        ids = torch.zeros((n_tok, 2), dtype=torch.int32, device="cuda")
+        g = torch.zeros((n_tok, 2), device="cuda")
+        w.layer_forward(0, x, o, ids, g)
+        torch.cuda.synchronize()
+        outs.append(o)
+    assert torch.equal(outs[0], outs[1])
+    w.close()
+
+
 def test_router_many_tokens_batched_kernel(ctx, orc):
     """The router's per-token arithmetic does not depend on n_tok or on the
     token's slot in a block: one 4100-token call equals 1000-token chunks bit
