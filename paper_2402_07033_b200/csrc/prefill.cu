@@ -436,6 +436,8 @@ struct GroupedArgs {
   int trace_cap;  // tiles per CTA
   SparsityCounters sp;  // fused |silu(w_in x)| < thr counters (off: sp.counts == nullptr)
   int lag;              // schedule: expert i's down tiles follow expert i+lag's up tiles
+  int late8;            // eighths of the active experts whose downs take the finest split
+  int s_lo;             // K split of the other experts' downs (0: S / 2)
   int evict_first;      // weights loaded with an L2 evict_first hint
 };
 
@@ -520,7 +522,7 @@ __global__ void __launch_bounds__(PF_THREADS, 1)
     int n_act = 0;
     for (int e = 0; e < a.E; ++e)
       if (a.slot_of[e] >= 0 && a.counts[e] > 0) act[n_act++] = e;
-    const int n_late = (3 * n_act + 7) / 8;
+    const int n_late = (a.late8 * n_act + 7) / 8;
     int dn_tiles = 0;  // down tiles without K splits
     for (int e = 0; e < a.E; ++e) {
       s_split[e] = 1;
@@ -530,7 +532,7 @@ __global__ void __launch_bounds__(PF_THREADS, 1)
     // K splits only pay while the down tiles are few per SM (tail); with many
     // (large batches) they only add fp32 Y partial traffic for the combine
     const int s_hi = dn_tiles >= 4 * (int)gridDim.x ? 1 : min(a.S, a.f / PF_BK);
-    const int s_lo = max(1, s_hi / 2);
+    const int s_lo = a.s_lo > 0 ? min(a.s_lo, s_hi) : max(1, s_hi / 2);
     for (int i = 0; i < n_act; ++i) s_split[act[i]] = i >= n_act - n_late ? s_hi : s_lo;
     if (blockIdx.x == 0)
       for (int e = 0; e < a.E; ++e) a.split_of[e] = s_split[e];
@@ -996,6 +998,8 @@ cudaError_t launch_prefill_experts(const LayerWeights& lw, int n_local, const Di
     // downs among ups is slower (lag 1/2/3: +33/+12/+24 us) than all ups
     // first, so the default lag puts every down after every up
     g.lag = getenv("MOE_B200_PF_LAG") ? atoi(getenv("MOE_B200_PF_LAG")) : kMaxExperts;
+    g.late8 = getenv("MOE_B200_PF_LATE8") ? atoi(getenv("MOE_B200_PF_LATE8")) : 3;
+    g.s_lo = getenv("MOE_B200_PF_SLO") ? atoi(getenv("MOE_B200_PF_SLO")) : 0;
     g.trace = nullptr;
     g.trace_cap = 0;
     const char* trace_path = getenv("MOE_B200_PF_TRACE");
