@@ -17,6 +17,7 @@
 #include "../../include/moe_b200.h"
 #include "kernels.h"
 #include "replica_plan.h"
+#include "host_io.h"
 
 using moe::Dims;
 using moe::LayerWeights;
@@ -104,6 +105,8 @@ struct moe_ctx {
   std::mutex mu;
 };
 
+constexpr int kIoChunks = 4;  // moe_forward_host transfer chunks
+
 struct DevBuf {
   void* p = nullptr;
   size_t bytes = 0;
@@ -173,6 +176,7 @@ struct moe_weights {
   size_t host_pin_bytes = 0;
   std::map<std::tuple<float*, int32_t*, float*, cudaStream_t>, GraphEntry> graphs;
   cudaStream_t cap_stream = nullptr;  // private stream for graph capture
+  cudaEvent_t io_ev[kIoChunks] = {};  // host-buffer API: per-chunk D2H completion
   std::mutex mu;
 
   int L() const { return shape.num_layers; }
@@ -494,27 +498,6 @@ int forward_graph(moe_weights* w, float* x, int32_t* ids, float* gates, cudaStre
   }
   CU(cudaGraphLaunch(it->second.exec, s));
   return MOE_OK;
-}
-
-// dst[i] = (To)src[i]; split over host threads for prefill-sized buffers (the
-// host-buffer API converts the reference's fp64 tokens; one thread would take
-// ~2 ms each way at 512 x 4096)
-template <typename To, typename From>
-void host_convert(To* dst, const From* src, size_t n) {
-  const size_t kMin = 1 << 18;
-  const unsigned hw = std::max(1u, std::thread::hardware_concurrency());
-  const unsigned nt = (unsigned)std::min<size_t>(std::min(hw, 16u), (n + kMin - 1) / kMin);
-  if (nt <= 1) {
-    for (size_t i = 0; i < n; ++i) dst[i] = (To)src[i];
-    return;
-  }
-  std::vector<std::thread> ts;
-  for (unsigned t = 0; t < nt; ++t)
-    ts.emplace_back([=] {
-      const size_t a = n * t / nt, b = n * (t + 1) / nt;
-      for (size_t i = a; i < b; ++i) dst[i] = (To)src[i];
-    });
-  for (auto& th : ts) th.join();
 }
 
 int host_pinned(moe_weights* w, size_t bytes, void** out) {
@@ -992,6 +975,9 @@ int moe_weights_destroy(moe_weights* w) {
                     &w->dev_layers, &w->dev_slots, &w->pf_counts, &w->pf_offsets, &w->pf_perm,
                     &w->pf_xg, &w->pf_h, &w->pf_sync})
     b->release();
+  for (DevBuf* b : {&w->dev_holders, &w->dev_res_slots, &w->pf_counts2, &w->pf_offsets2}) b->release();
+  for (cudaEvent_t e : w->io_ev)
+    if (e) cudaEventDestroy(e);
   if (w->host_pin) cudaFreeHost(w->host_pin);
   delete w;
   return MOE_OK;
@@ -1293,11 +1279,19 @@ int moe_forward_host(moe_weights* w, const double* tokens, int n_tok, double* ou
   int32_t* hids = reinterpret_cast<int32_t*>(hx + nx);
   float* hg = reinterpret_cast<float*>(hids + nr);
   float* hpost = hg + nr;
-  host_convert(hx, tokens, nx);
   float* dx = w->xin.as<float>();  // device copy of the tokens (in/out)
   int32_t* dids = w->ids.as<int32_t>();
   float* dg = w->gates.as<float>();
-  CU(cudaMemcpyAsync(dx, hx, nx * 4, cudaMemcpyHostToDevice, s));
+  // prefill-sized calls move the tokens in chunks: the copy engine carries
+  // chunk c while the host pool converts chunk c+1 (and the reverse on the
+  // way out)
+  const int nch = nx >= ((size_t)1 << 20) ? kIoChunks : 1;
+  auto lo = [&](int c) { return c == 0 ? (size_t)0 : (nx * c / nch) & ~(size_t)15; };
+  auto hi = [&](int c) { return c == nch - 1 ? nx : (nx * (c + 1) / nch) & ~(size_t)15; };
+  for (int c = 0; c < nch; ++c) {
+    moe_host::to_f32_dma(hx + lo(c), tokens + lo(c), hi(c) - lo(c));
+    CU(cudaMemcpyAsync(dx + lo(c), hx + lo(c), (hi(c) - lo(c)) * 4, cudaMemcpyHostToDevice, s));
+  }
   if (post_silu) {
     TRY(w->post.ensure(npost * 4));
     // the sink path needs silu(w_in x) per (token, slot): generic kernels, no graph
@@ -1309,11 +1303,20 @@ int moe_forward_host(moe_weights* w, const double* tokens, int n_tok, double* ou
   } else {
     TRY(enqueue_forward(w, dx, n_tok, dids, dg, s, nullptr));
   }
-  CU(cudaMemcpyAsync(hx, dx, nx * 4, cudaMemcpyDeviceToHost, s));
+  if (nch > 1 && !w->io_ev[0])
+    for (auto& e : w->io_ev) CU(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+  for (int c = 0; c < nch; ++c) {
+    CU(cudaMemcpyAsync(hx + lo(c), dx + lo(c), (hi(c) - lo(c)) * 4, cudaMemcpyDeviceToHost, s));
+    if (nch > 1) CU(cudaEventRecord(w->io_ev[c], s));
+  }
   CU(cudaMemcpyAsync(hids, dids, nr * 4, cudaMemcpyDeviceToHost, s));
   CU(cudaMemcpyAsync(hg, dg, nr * 4, cudaMemcpyDeviceToHost, s));
+  for (int c = 0; c < nch; ++c) {
+    if (nch > 1) CU(cudaEventSynchronize(w->io_ev[c]));
+    else CU(cudaStreamSynchronize(s));
+    moe_host::to_f64(out + lo(c), hx + lo(c), hi(c) - lo(c));
+  }
   CU(cudaStreamSynchronize(s));
-  host_convert(out, hx, nx);
   if (ids) std::memcpy(ids, hids, nr * 4);
   if (gates)
     for (size_t i = 0; i < nr; ++i) gates[i] = hg[i];
