@@ -434,6 +434,27 @@ def test_combine_k2_equals_looped_combine(ctx, monkeypatch, n_tok):
     w.close()
 
 
+@pytest.mark.parametrize("n_tok", [1, 300, 512])
+def test_forward_host_equals_device_path(ctx, n_tok):
+    """The fp64 host-buffer entry point (pooled conversion, chunked copies for
+    prefill sizes) gives exactly moe_forward's result on the same fp32 tokens
+    (batch 1: the same captured stack-kernel graph): out == double(device
+    out), ids and gates equal."""
+    w = M.Weights(ctx, M.Shape(1, 8, 2, 4096, 14336, 2), M.DTYPE_BF16)
+    w.random(4)
+    xh = np.random.RandomState(n_tok).randn(n_tok, 4096)
+    out, ids_h, g_h = w.forward_host(xh)
+    o = torch.tensor(xh.astype(np.float32), device="cuda")  # moe_forward: in place
+    ids = torch.zeros((1, n_tok, 2), dtype=torch.int32, device="cuda")
+    g = torch.zeros((1, n_tok, 2), device="cuda")
+    w.forward(o, ids, g)
+    torch.cuda.synchronize()
+    assert np.array_equal(out, o.cpu().numpy().astype(np.float64))
+    assert np.array_equal(ids_h, ids.cpu().numpy())
+    assert np.array_equal(g_h, g.cpu().numpy().astype(np.float64))
+    w.close()
+
+
 def test_router_many_tokens_batched_kernel(ctx, orc):
     """The router's per-token arithmetic does not depend on n_tok or on the
     token's slot in a block: one 4100-token call equals 1000-token chunks bit
