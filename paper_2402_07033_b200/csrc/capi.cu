@@ -400,7 +400,7 @@ int experts_forward(moe_weights* w, int l, const float* x, int n_tok, const int3
     int32_t* counts = w->pf_counts.as<int32_t>();
     int32_t* offsets = w->pf_offsets.as<int32_t>();
     int32_t* perm = w->pf_perm.as<int32_t>();
-    CU(moe::launch_permute(ids, n_tok, dm.k, dm.E, counts, offsets, perm, nullptr, s));
+    CU(moe::launch_permute(ids, n_tok, dm.k, dm.E, counts, offsets, perm, nullptr, s, pdl));
     const int S = w->prefill_splits;
     const int16_t* slots = w->dev_slots.as<int16_t>() + (size_t)l * dm.E;
     if (w->replicas && S > 0) {

@@ -509,6 +509,8 @@ __global__ void __launch_bounds__(1024) permute_kernel(const int32_t* __restrict
   int32_t* wcnt = off + E;       // [32][E] per-warp counts of the chunk
   const int tid = threadIdx.x, lane = tid & 31;
   const int warp = warp_uniform(tid >> 5);
+  griddep_wait();
+  griddep_launch_dependents();
   for (int e = tid; e < E; e += blockDim.x) run[e] = 0;
   __syncthreads();
   // pass 1: counts
@@ -556,7 +558,8 @@ __global__ void __launch_bounds__(1024) permute_kernel(const int32_t* __restrict
 }
 
 cudaError_t launch_permute(const int32_t* ids, int n_tok, int k, int E, int32_t* counts,
-                           int32_t* offsets, int32_t* perm, int32_t* inv_perm, cudaStream_t s) {
+                           int32_t* offsets, int32_t* perm, int32_t* inv_perm, cudaStream_t s,
+                           bool pdl) {
   const int n = n_tok * k;
   const size_t smem = sizeof(int32_t) * (size_t)(2 * E + 32 * E);
   if (smem > 48 * 1024) {
@@ -564,8 +567,9 @@ cudaError_t launch_permute(const int32_t* ids, int n_tok, int k, int E, int32_t*
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
   }
-  permute_kernel<<<1, 1024, smem, s>>>(ids, n, E, counts, offsets, perm, inv_perm);
-  return cudaGetLastError();
+  cudaLaunchAttribute attr[1];
+  cudaLaunchConfig_t cfg = make_cfg(dim3(1), dim3(1024), s, pdl, attr, smem);
+  return cudaLaunchKernelEx(&cfg, permute_kernel, ids, n, E, counts, offsets, perm, inv_perm);
 }
 
 // ---- routing histogram (profile_from_trace, placement.cpp:30-43) -------------

@@ -209,7 +209,8 @@ cudaError_t launch_trace_step(const int32_t* ids, const float* gates, int L, int
 
 // ---- permutation ------------------------------------------------------------
 cudaError_t launch_permute(const int32_t* ids, int n_tok, int k, int E, int32_t* counts,
-                           int32_t* offsets, int32_t* perm, int32_t* inv_perm, cudaStream_t s);
+                           int32_t* offsets, int32_t* perm, int32_t* inv_perm, cudaStream_t s,
+                           bool pdl = false);
 
 // ---- weights ----------------------------------------------------------------
 // dst (dtype) = src (fp64) with optional transpose of a [rows x cols] matrix.

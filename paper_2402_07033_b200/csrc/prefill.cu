@@ -857,10 +857,17 @@ __global__ void __launch_bounds__(PF_THREADS, 1)
   if (warp == 5) tmem_free(tmem, 512);
 }
 
-// Xg[sorted row] = bf16(x[token of that pair]); float4 in, 4 x bf16 out
+// Xg[sorted row] = bf16(x[token of that pair]); float4 in, 4 x bf16 out.
+// Block 0 also zeroes the grouped kernel's sync words (tile counter + done
+// flags): the grouped kernel is launched programmatically dependent on this
+// one and reads them only after its griddep_wait.
 __global__ void gather_rows_kernel(const float* __restrict__ x, const int32_t* __restrict__ perm,
-                                   int nrows, int k, int d, __nv_bfloat16* xg) {
+                                   int nrows, int k, int d, __nv_bfloat16* xg, int* zero,
+                                   int n_zero) {
   griddep_wait();
+  griddep_launch_dependents();
+  if (blockIdx.x == 0)
+    for (int i = threadIdx.x; i < n_zero; i += blockDim.x) zero[i] = 0;
   const int row = blockIdx.x;
   if (row >= nrows) return;
   const int t = perm[row] / k;
@@ -957,8 +964,24 @@ cudaError_t launch_prefill_experts(const LayerWeights& lw, int n_local, const Di
                                    const SparsityCounters& sp) {
   const int rows = n_tok * dm.k;
   if (rows == 0 || n_local == 0) return cudaSuccess;
-  gather_rows_kernel<<<rows, 128, 0, s>>>(x, perm, rows, dm.k, dm.d, xg);  // d % 128 == 0
-  cudaError_t err = cudaGetLastError();
+  // an expert holds <= n_tok tokens; the grouped kernel's done flags are per
+  // GP_MAXN-token chunk, the two-kernel path's grid per PF_MAXN
+  const int chunks = (n_tok + GP_MAXN - 1) / GP_MAXN;
+  // PDL chain permute -> gather -> grouped kernel: each launch overlaps the
+  // previous kernel's tail and waits (griddep_wait) before touching its data
+  static const bool no_pdl = getenv("MOE_B200_NO_PDL") != nullptr;
+  cudaLaunchAttribute pdl_attr[1];
+  pdl_attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  pdl_attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cudaLaunchConfig_t gcfg = {};
+  gcfg.gridDim = dim3(rows);
+  gcfg.blockDim = dim3(128);
+  gcfg.stream = s;
+  gcfg.attrs = pdl_attr;
+  gcfg.numAttrs = no_pdl ? 0 : 1;
+  const int n_zero = splits > 0 ? 1 + dm.E * chunks : 0;
+  cudaError_t err = cudaLaunchKernelEx(&gcfg, gather_rows_kernel, x, perm, rows, dm.k, dm.d, xg,
+                                       sync, n_zero);  // d % 128 == 0
   if (err != cudaSuccess) return err;
   CUtensorMap wmap_up, wmap_dn, xmap, hmap;
   const long long wrows = 3LL * n_local * dm.f;
@@ -966,9 +989,6 @@ cudaError_t launch_prefill_experts(const LayerWeights& lw, int n_local, const Di
       !make_map(&wmap_dn, lw.experts, wrows, dm.d, 64, PF_BK) ||
       !make_map(&xmap, xg, rows, dm.d, 64, PF_BOXN) || !make_map(&hmap, h, rows, dm.f, 64, PF_BOXN))
     return cudaErrorInvalidValue;
-  // an expert holds <= n_tok tokens; the grouped kernel's done flags are per
-  // GP_MAXN-token chunk, the two-kernel path's grid per PF_MAXN
-  const int chunks = (n_tok + GP_MAXN - 1) / GP_MAXN;
   if (splits > 0) {
     // persistent grouped kernel (default)
     GroupedArgs g;
@@ -1011,13 +1031,19 @@ cudaError_t launch_prefill_experts(const LayerWeights& lw, int n_local, const Di
       if ((err = cudaMemsetAsync(trace_buf, 0, tb, s)) != cudaSuccess) return err;
       g.trace = trace_buf;
     }
-    err = cudaMemsetAsync(sync, 0, sizeof(int) * (1 + (size_t)dm.E * chunks), s);
-    if (err != cudaSuccess) return err;
+    // (sync words zeroed by the gather kernel)
     auto kern = sp.counts ? prefill_grouped_kernel<true> : prefill_grouped_kernel<false>;
     err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, GP_SMEM);
     if (err != cudaSuccess) return err;
-    kern<<<sm_count, PF_THREADS, GP_SMEM, s>>>(wmap_up, wmap_dn, xmap, hmap, g);
-    if ((err = cudaGetLastError()) != cudaSuccess || !trace_path) return err;
+    cudaLaunchConfig_t kcfg = {};
+    kcfg.gridDim = dim3(sm_count);
+    kcfg.blockDim = dim3(PF_THREADS);
+    kcfg.dynamicSmemBytes = GP_SMEM;
+    kcfg.stream = s;
+    kcfg.attrs = pdl_attr;
+    kcfg.numAttrs = no_pdl || trace_path ? 0 : 1;
+    err = cudaLaunchKernelEx(&kcfg, kern, wmap_up, wmap_dn, xmap, hmap, g);
+    if (err != cudaSuccess || !trace_path) return err;
     // diagnostics only: synchronous dump (appends one record per launch)
     const size_t n = (size_t)sm_count * g.trace_cap * 4;
     std::vector<unsigned long long> h(n);
