@@ -119,3 +119,80 @@ def test_shard_map_is_balanced_partition(world):
     # uniform popularity -> round robin in the reference's (layer, expert) order
     uni = _shard_map(2, 8, world)
     assert list(uni[0]) == [e % world for e in range(8)]
+
+
+def _replica_worker(rank, world, port, q):
+    """EP with a replicated hot expert: each rank plans its share of every
+    expert's sorted rows on its own (moe_replica_plan, the device planner's
+    host mirror) and computes only those rows (oracle math); the all-reduced
+    deltas must equal model_forward, and the ranks' independent plans must
+    tile every expert's rows exactly once."""
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        import paper_2402_07033_b200 as M
+
+        O.build(ref=False)
+        orc = O.Oracle()
+        shape = O.Shape(1, 8, 2, 32, 64, 2)
+        w = orc.random_model(shape, 7)
+        w.router[0][0, :] = 0.5  # with x ~ N(1, 1): expert 0 in every token's top-2
+        n = 120
+        xs = orc.normal(8, n * 32).reshape(n, 32) + 1.0
+        route = [orc.gate_topk(w.router[0], xs[t], 2)[:2] for t in range(n)]
+        counts = np.zeros(8, np.int32)
+        for ids, _ in route:
+            for e in ids:
+                counts[e] += 1
+        owner = np.arange(8) % world
+        holders = (1 << owner).astype(np.uint32)
+        holders[int(np.argmax(counts))] = (1 << world) - 1
+        # compute-bound cost model with 16-row chunks, so the hot expert splits
+        lo, hi, _ = M.replica_plan(counts, holders, world, 1000, 100, 0, 16, rank)
+        delta = np.zeros_like(xs)
+        for e in range(8):
+            rows = [(t, j) for t in range(n) for j in range(2) if route[t][0][j] == e]
+            for t, j in rows[lo[e]:hi[e]]:
+                wi, wg, wo = w.expert(0, e)
+                delta[t] += route[t][1][j] * orc.expert_ffn(wi, wg, wo, xs[t])
+        dt = torch.from_numpy(delta)
+        dist.all_reduce(dt, op=dist.ReduceOp.SUM)
+        plans = [None] * world
+        dist.all_gather_object(plans, (lo.tolist(), hi.tolist()))
+        q.put((rank, xs + dt.numpy(), plans, counts.tolist(), holders.tolist()))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_replicated_expert_split_matches_single_process():
+    world, port = 2, _free_port()
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    procs = [ctx.Process(target=_replica_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = {r: rest for r, *rest in (q.get(timeout=120) for _ in range(world))}
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    orc = O.Oracle()
+    shape = O.Shape(1, 8, 2, 32, 64, 2)
+    w = orc.random_model(shape, 7)
+    w.router[0][0, :] = 0.5
+    want = orc.model_forward(shape, w, orc.normal(8, 120 * 32).reshape(120, 32) + 1.0)[0]
+    out, plans, counts, holders = res[0]
+    np.testing.assert_allclose(out, want, rtol=0, atol=1e-12)
+    np.testing.assert_array_equal(res[1][0], out)
+    hot = int(np.argmax(counts))
+    assert counts[hot] == 120
+    split = [r for r in range(world) if plans[r][1][hot] > plans[r][0][hot]]
+    assert len(split) == 2  # the hot expert's rows really are shared
+    for e in range(8):  # every expert's rows tiled once, by holders only
+        segs = sorted((plans[r][0][e], plans[r][1][e], r) for r in range(world)
+                      if plans[r][1][e] > plans[r][0][e])
+        pos = 0
+        for a, b, r in segs:
+            assert a == pos and (holders[e] >> r) & 1
+            pos = b
+        assert pos == counts[e]
