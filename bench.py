@@ -251,6 +251,8 @@ def run_ours(args):
         ev1.record(stream)
         torch.cuda.synchronize()
     ms = ev0.elapsed_time(ev1)
+    if world > 1 and not args.nccl_combine:
+        ctx.peer_check()  # a peer that never arrived: fail loudly, not a garbage number
     ms = max_over_ranks(ms, world)
     barrier(world)
     ms_per_step = ms / args.steps

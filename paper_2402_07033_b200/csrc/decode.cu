@@ -384,6 +384,9 @@ __device__ __forceinline__ unsigned ld_acquire_sys(const unsigned* p) {
 
 // Bounded wait for a peer's flag to reach `target` (sequence numbers compare
 // modulo 2^32): a rank that never arrives sets *err instead of hanging.
+// Bounded wait for a peer's flag.  Once any wait of this rank has timed out
+// (err set) the others give up at their next check instead of each spinning
+// to its own bound, so a missing peer costs one timeout, not one per wait.
 __device__ __forceinline__ void peer_wait(const unsigned* f, unsigned target, unsigned* err) {
   unsigned spins = 0;
   while ((int)(ld_acquire_sys(f) - target) < 0) {
@@ -391,7 +394,10 @@ __device__ __forceinline__ void peer_wait(const unsigned* f, unsigned target, un
       atomicExch(err, 1u);
       break;
     }
-    if (spins > 64) __nanosleep(128);
+    if (spins > 64) {
+      if ((spins & 63) == 0 && *reinterpret_cast<volatile unsigned*>(err)) break;
+      __nanosleep(128);
+    }
   }
 }
 
@@ -427,17 +433,7 @@ __global__ void __launch_bounds__(256) reduce_exchange_kernel(
     if (lane < pa.world) st_release_sys(pa.flags[lane] + (size_t)pa.rank * kPeerSlots + b, seq);
     // wait for every rank's slice of this block (bounded: a missing peer is
     // reported through pa.err instead of hanging the GPU)
-    if (lane < pa.world) {
-      const unsigned* f = pa.flags[pa.rank] + (size_t)lane * kPeerSlots + b;
-      unsigned spins = 0;
-      while ((int)(ld_acquire_sys(f) - seq) < 0) {
-        if (++spins > (1u << 22)) {
-          atomicExch(pa.err, 1u);
-          break;
-        }
-        if (spins > 64) __nanosleep(128);
-      }
-    }
+    if (lane < pa.world) peer_wait(pa.flags[pa.rank] + (size_t)lane * kPeerSlots + b, seq, pa.err);
     __syncwarp();
     float all = 0.f;
     if (i < d) {
