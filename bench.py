@@ -326,6 +326,8 @@ def run_ours(args):
                 "alg_bytes_per_launch": expert_kernel["alg_bytes_per_launch"], "peak_source": peak_src}
     if roof is not None and world == 1:
         roof["step_frac"] = round(L * layer_bytes / (ms_per_step * 1e-3) / 1e9 / peak, 4)
+    if roof is not None:  # also against north_star's nominal 8 TB/s
+        roof["frac_vs_nominal_8tbs"] = round(roof["achieved"] / 8000.0, 4)
 
     # ---- e2e through the host-buffer C-ABI entry point ----------------------
     host_tokens = rs.randn(args.steps + 2, d)
@@ -449,7 +451,8 @@ def run_prefill(args):
         "gpu_launches": w.forward_launches(n) * args.steps, "clocks": clk.summary(), "e2e": e2e,
         "cpu_baseline": cpu,
         "roofline": {"bound": "hbm", "achieved": round(bw, 1), "peak": peak_bw, "unit": "GB/s",
-                     "frac": round(bw / peak_bw, 4), "traffic": None, "alg_bytes_per_step": bytes_,
+                     "frac": round(bw / peak_bw, 4), "frac_vs_nominal_8tbs": round(bw / 8000.0, 4),
+                     "traffic": None, "alg_bytes_per_step": bytes_,
                      "tensor_tflops": round(tf, 1), "tensor_frac": round(tf / peaks["bf16_tflops"], 4),
                      "peak_source": src},
     }), flush=True)
