@@ -161,6 +161,7 @@ struct moe_weights {
   DevBuf ypart, rpart, counter, xa, xb, xin, h, y, delta, ids, gates, post;
   DevBuf xbuf2, gbar, dev_layers, dev_slots;  // persistent stack kernel
   DevBuf pf_counts, pf_offsets, pf_perm, pf_xg, pf_h, pf_sync;  // tcgen05 prefill
+  DevBuf io;  // host-buffer API, batch 1: [x][ids][gates] (one D2H)
   bool prefill_enabled = true;
   int prefill_splits = 2;  // max K splits of the down GEMM in the grouped kernel (0: 2-kernel path)
   // router projections R_{l+1} W2 for the stack kernel's z partials
@@ -475,15 +476,27 @@ int enqueue_forward(moe_weights* w, float* x, int n_tok, int32_t* ids, float* ga
 // The batch-1 forward as a CUDA graph, captured once per (x, ids, gates) on a
 // private stream (the caller's stream may be the legacy default stream,
 // which cannot be captured) and launched on the caller's stream.
-int forward_graph(moe_weights* w, float* x, int32_t* ids, float* gates, cudaStream_t s) {
-  auto key = std::make_tuple(x, ids, gates, (cudaStream_t) nullptr);
+// host_io (optional, pinned): the graph also copies in_bytes host -> x before
+// the forward and out_bytes x -> host after (the host-buffer API's batch-1
+// step as ONE launch; x, ids, gates contiguous on both sides).  The host
+// pointer is part of the key (in the stream slot).
+int forward_graph(moe_weights* w, float* x, int32_t* ids, float* gates, cudaStream_t s,
+                  void* host_io = nullptr, size_t in_bytes = 0, size_t out_bytes = 0) {
+  auto key = std::make_tuple(x, ids, gates, reinterpret_cast<cudaStream_t>(host_io));
   auto it = w->graphs.find(key);
   if (it == w->graphs.end()) {
     cudaStream_t cs = w->cap_stream;  // created with the weights (creation may synchronize)
     cudaGraph_t g = nullptr;
     CU(cudaStreamBeginCapture(cs, cudaStreamCaptureModeThreadLocal));
-    const int rc = use_stack(w, 1) ? enqueue_stack(w, x, ids, gates, cs)
-                                   : enqueue_forward(w, x, 1, ids, gates, cs, nullptr);
+    int rc = MOE_OK;
+    if (host_io && cudaMemcpyAsync(x, host_io, in_bytes, cudaMemcpyHostToDevice, cs) != cudaSuccess)
+      rc = fail(MOE_ERR_CUDA, "capture of the token copy failed");
+    if (rc == MOE_OK)
+      rc = use_stack(w, 1) ? enqueue_stack(w, x, ids, gates, cs)
+                           : enqueue_forward(w, x, 1, ids, gates, cs, nullptr);
+    if (rc == MOE_OK && host_io &&
+        cudaMemcpyAsync(host_io, x, out_bytes, cudaMemcpyDeviceToHost, cs) != cudaSuccess)
+      rc = fail(MOE_ERR_CUDA, "capture of the result copy failed");
     cudaError_t e = cudaStreamEndCapture(cs, &g);
     if (rc != MOE_OK) {
       if (g) cudaGraphDestroy(g);
@@ -505,6 +518,7 @@ int host_pinned(moe_weights* w, size_t bytes, void** out) {
     if (w->host_pin) cudaFreeHost(w->host_pin);
     w->host_pin = nullptr;
     w->host_pin_bytes = 0;
+    drop_graphs(w);  // batch-1 host-buffer graphs copy to / from the old buffer
     CU(cudaMallocHost(&w->host_pin, bytes));
     w->host_pin_bytes = bytes;
   }
@@ -975,7 +989,8 @@ int moe_weights_destroy(moe_weights* w) {
                     &w->dev_layers, &w->dev_slots, &w->pf_counts, &w->pf_offsets, &w->pf_perm,
                     &w->pf_xg, &w->pf_h, &w->pf_sync})
     b->release();
-  for (DevBuf* b : {&w->dev_holders, &w->dev_res_slots, &w->pf_counts2, &w->pf_offsets2}) b->release();
+  for (DevBuf* b : {&w->dev_holders, &w->dev_res_slots, &w->pf_counts2, &w->pf_offsets2, &w->io})
+    b->release();
   for (cudaEvent_t e : w->io_ev)
     if (e) cudaEventDestroy(e);
   if (w->host_pin) cudaFreeHost(w->host_pin);
@@ -1279,6 +1294,24 @@ int moe_forward_host(moe_weights* w, const double* tokens, int n_tok, double* ou
   int32_t* hids = reinterpret_cast<int32_t*>(hx + nx);
   float* hg = reinterpret_cast<float*>(hids + nr);
   float* hpost = hg + nr;
+  if (n_tok == 1 && w->plan.ok && !post_silu) {
+    // batch 1: token in, forward, result + routing out — one graph launch
+    // and one host wait (x, ids, gates contiguous in w->io as in the pinned
+    // buffer)
+    TRY(w->io.ensure(nx * 4 + nr * 8));
+    float* iox = w->io.as<float>();
+    int32_t* ioids = reinterpret_cast<int32_t*>(iox + nx);
+    float* iog = reinterpret_cast<float*>(ioids + nr);
+    moe_host::to_f32_dma(hx, tokens, nx);
+    TRY(refresh_projection(w));
+    TRY(forward_graph(w, iox, ioids, iog, s, hx, nx * 4, nx * 4 + nr * 8));
+    CU(cudaStreamSynchronize(s));
+    moe_host::to_f64(out, hx, nx);
+    if (ids) std::memcpy(ids, hids, nr * 4);
+    if (gates)
+      for (size_t i = 0; i < nr; ++i) gates[i] = hg[i];
+    return MOE_OK;
+  }
   float* dx = w->xin.as<float>();  // device copy of the tokens (in/out)
   int32_t* dids = w->ids.as<int32_t>();
   float* dg = w->gates.as<float>();
