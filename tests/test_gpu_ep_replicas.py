@@ -120,3 +120,24 @@ def test_replicated_hot_expert(gpu, world, n_tok):
         c.close()
     full.close()
     base.close()
+
+
+def test_replica_mask_validation(gpu):
+    """A mask naming a rank outside the world is rejected; without replicas
+    create_ep is plain expert parallelism (the owner holds each expert)."""
+    s = M.Shape(2, 8, 2, 256, 512, 2)
+    ctx = M.Ctx(0)
+    ctx.set_virtual_rank(2, 0)
+    owner = np.tile(np.arange(8) % 2, (2, 1)).astype(np.int32)
+    bad = np.zeros((2, 8), np.uint32)
+    bad[1, 3] = 0b100  # rank 2 of a 2-rank world
+    with pytest.raises(M.MoeError):
+        M.Weights(ctx, s, M.DTYPE_BF16, owner=owner, replicas=bad)
+    plain = M.Weights(ctx, s, M.DTYPE_BF16, owner=owner)
+    zero = M.Weights(ctx, s, M.DTYPE_BF16, owner=owner, replicas=np.zeros((2, 8), np.uint32))
+    rep = M.Weights(ctx, s, M.DTYPE_BF16, owner=owner, replicas=np.full((2, 8), 0b11, np.uint32))
+    assert zero.device_bytes == plain.device_bytes
+    assert rep.device_bytes > plain.device_bytes  # every expert resident on rank 0
+    for w in (plain, zero, rep):
+        w.close()
+    ctx.close()
