@@ -130,6 +130,12 @@ int moe_weights_create_ep(moe_ctx* ctx, const moe_shape* shape, int dtype,
  * expert's weights, tensor-core time per (token, slot) row.  Defaults from
  * the grouped kernel on B200: 6.54 TB/s (3*d*f*esize B), 1.25 PFLOP/s
  * (6*d*f flop per row), part_ps = 2/3 weight_ps. */
+/* Measurement: enable = 1 starts recording CUDA events on the launching
+ * stream right around every tcgen05 grouped prefill kernel launch of these
+ * weights; enable = 0 stops, waits for them and returns the summed kernel
+ * time (us) and the number of launches timed.  (The events break the PDL
+ * edge into the kernel, so time a separate loop, not the headline one.) */
+int moe_debug_kernel_timing(moe_weights* w, int enable, double* total_us, int64_t* launches);
 int moe_weights_set_replica_cost(moe_weights* w, int64_t weight_ps, int64_t row_ps,
                                  int64_t part_ps);
 int moe_weights_replica_cost(const moe_weights* w, int64_t* weight_ps, int64_t* row_ps,

@@ -99,6 +99,7 @@ def lib():
         "moe_weights_create_tp": ([_vp, C.POINTER(_Shape), C.c_int, C.POINTER(_vp)], C.c_int),
         "moe_weights_create_ep": ([_vp, C.POINTER(_Shape), C.c_int, _vp, _vp, C.POINTER(_vp)], C.c_int),
         "moe_weights_set_replica_cost": ([_vp, C.c_int64, C.c_int64, C.c_int64], C.c_int),
+        "moe_debug_kernel_timing": ([_vp, C.c_int, C.POINTER(C.c_double), C.POINTER(C.c_int64)], C.c_int),
         "moe_weights_replica_cost": ([_vp] + [C.POINTER(C.c_int64)] * 3, C.c_int),
         "moe_replica_plan": ([_vp, C.c_int, _vp, C.c_int, C.c_int64, C.c_int64, C.c_int64, C.c_int,
                               C.c_int, _vp, _vp, C.POINTER(C.c_int64)], C.c_int),
@@ -318,6 +319,14 @@ class Weights:
     @replica_cost.setter
     def replica_cost(self, v):
         check(lib().moe_weights_set_replica_cost(self.h, int(v[0]), int(v[1]), int(v[2])))
+
+    def kernel_timing(self, enable: bool):
+        """Live CUDA-event timing of the grouped prefill kernel launches:
+        kernel_timing(True) starts; kernel_timing(False) returns
+        (total_us, launches)."""
+        t, n = C.c_double(), C.c_int64()
+        check(lib().moe_debug_kernel_timing(self.h, 1 if enable else 0, C.byref(t), C.byref(n)))
+        return t.value, n.value
 
     def reserve(self, max_tokens: int):
         """Allocate all scratch for calls of up to max_tokens tokens now."""

@@ -162,6 +162,10 @@ struct moe_weights {
   DevBuf xbuf2, gbar, dev_layers, dev_slots;  // persistent stack kernel
   DevBuf pf_counts, pf_offsets, pf_perm, pf_xg, pf_h, pf_sync;  // tcgen05 prefill
   DevBuf io;  // host-buffer API, batch 1: [x][ids][gates] (one D2H)
+  // moe_debug_kernel_timing: event pairs around each grouped prefill launch
+  bool ktime_on = false;
+  std::vector<std::pair<cudaEvent_t, cudaEvent_t>> kev;
+  size_t kev_used = 0;
   bool prefill_enabled = true;
   int prefill_splits = 2;  // max K splits of the down GEMM in the grouped kernel (0: 2-kernel path)
   // router projections R_{l+1} W2 for the stack kernel's z partials
@@ -417,11 +421,23 @@ int experts_forward(moe_weights* w, int l, const float* x, int n_tok, const int3
     }
     if (w->n_local[l] < dm.E || w->replicas)
       CU(cudaMemsetAsync(w->y.p, 0, (size_t)std::max(1, S) * rows * dm.d * 4, s));
+    cudaEvent_t kt0 = nullptr, kt1 = nullptr;
+    if (w->ktime_on) {
+      if (w->kev_used == w->kev.size()) {
+        cudaEvent_t a = nullptr, b = nullptr;
+        CU(cudaEventCreate(&a));
+        CU(cudaEventCreate(&b));
+        w->kev.emplace_back(a, b);
+      }
+      kt0 = w->kev[w->kev_used].first;
+      kt1 = w->kev[w->kev_used].second;
+      ++w->kev_used;
+    }
     CU(moe::launch_prefill_experts(lw, w->n_local[l], dm, n_tok, x, counts, offsets, perm, gates,
                                    slots,
                                    w->pf_xg.as<__nv_bfloat16>(), w->pf_h.as<__nv_bfloat16>(),
                                    w->y.as<float>(), w->pf_sync.as<int>(), w->ctx->sm_count, S,
-                                   s, sp));
+                                   s, sp, kt0, kt1));
     cgates = nullptr;
     nsplit = std::max(1, S);
     if (S > 0) split_of = moe::prefill_split_of(w->pf_sync.as<int>(), dm.E, n_tok);
@@ -916,6 +932,28 @@ int moe_weights_create_ep(moe_ctx* c, const moe_shape* shape, int dtype, const i
   return weights_create(c, shape, dtype, owner_rank, false, out, replica_mask);
 }
 
+int moe_debug_kernel_timing(moe_weights* w, int enable, double* total_us, int64_t* launches) {
+  if (!w) return fail(MOE_ERR_ARG, "null weights");
+  std::lock_guard<std::mutex> lk(w->mu);
+  TRY(set_device(w->ctx));
+  if (enable) {
+    w->ktime_on = true;
+    w->kev_used = 0;
+    return MOE_OK;
+  }
+  w->ktime_on = false;
+  double tot = 0.0;
+  for (size_t i = 0; i < w->kev_used; ++i) {
+    CU(cudaEventSynchronize(w->kev[i].second));
+    float ms = 0.f;
+    CU(cudaEventElapsedTime(&ms, w->kev[i].first, w->kev[i].second));
+    tot += ms * 1e3;
+  }
+  if (total_us) *total_us = tot;
+  if (launches) *launches = (int64_t)w->kev_used;
+  return MOE_OK;
+}
+
 int moe_weights_set_replica_cost(moe_weights* w, int64_t weight_ps, int64_t row_ps,
                                  int64_t part_ps) {
   if (!w) return fail(MOE_ERR_ARG, "null weights");
@@ -993,6 +1031,10 @@ int moe_weights_destroy(moe_weights* w) {
     b->release();
   for (cudaEvent_t e : w->io_ev)
     if (e) cudaEventDestroy(e);
+  for (auto& p : w->kev) {
+    cudaEventDestroy(p.first);
+    cudaEventDestroy(p.second);
+  }
   if (w->host_pin) cudaFreeHost(w->host_pin);
   delete w;
   return MOE_OK;

@@ -185,7 +185,8 @@ cudaError_t launch_prefill_experts(const LayerWeights& lw, int n_local, const Di
                                    const float* gates, const int16_t* slot_of_dev,
                                    __nv_bfloat16* xg, __nv_bfloat16* h, float* y, int* sync,
                                    int sm_count, int splits, cudaStream_t s,
-                                   const SparsityCounters& sp = SparsityCounters());
+                                   const SparsityCounters& sp = SparsityCounters(),
+                                   cudaEvent_t t0 = nullptr, cudaEvent_t t1 = nullptr);
 
 // Replicated experts under expert parallelism (replica_plan.h):
 // one block computes this rank's share [lo, hi) of every expert's sorted rows

@@ -961,7 +961,7 @@ cudaError_t launch_prefill_experts(const LayerWeights& lw, int n_local, const Di
                                    const float* gates, const int16_t* slot_of_dev,
                                    __nv_bfloat16* xg, __nv_bfloat16* h, float* y, int* sync,
                                    int sm_count, int splits, cudaStream_t s,
-                                   const SparsityCounters& sp) {
+                                   const SparsityCounters& sp, cudaEvent_t t0, cudaEvent_t t1) {
   const int rows = n_tok * dm.k;
   if (rows == 0 || n_local == 0) return cudaSuccess;
   // an expert holds <= n_tok tokens; the grouped kernel's done flags are per
@@ -1041,8 +1041,12 @@ cudaError_t launch_prefill_experts(const LayerWeights& lw, int n_local, const Di
     kcfg.dynamicSmemBytes = GP_SMEM;
     kcfg.stream = s;
     kcfg.attrs = pdl_attr;
-    kcfg.numAttrs = no_pdl || trace_path ? 0 : 1;
+    // t0/t1 (moe_debug_kernel_timing): events on this stream right around
+    // the grouped kernel — its live duration (the event breaks the PDL edge)
+    kcfg.numAttrs = no_pdl || trace_path || t0 ? 0 : 1;
+    if (t0 && (err = cudaEventRecord(t0, s)) != cudaSuccess) return err;
     err = cudaLaunchKernelEx(&kcfg, kern, wmap_up, wmap_dn, xmap, hmap, g);
+    if (err == cudaSuccess && t1) err = cudaEventRecord(t1, s);
     if (err != cudaSuccess || !trace_path) return err;
     // diagnostics only: synchronous dump (appends one record per launch)
     const size_t n = (size_t)sm_count * g.trace_cap * 4;
