@@ -455,6 +455,29 @@ def test_forward_host_equals_device_path(ctx, n_tok):
     w.close()
 
 
+def test_kernel_timing_counts_grouped_launches(ctx):
+    """moe_debug_kernel_timing: one event pair per tcgen05 grouped launch,
+    none for batch-1 calls; results unchanged while timing."""
+    w = M.Weights(ctx, M.Shape(1, 8, 2, 4096, 14336, 2), M.DTYPE_BF16)
+    w.random(2)
+    x = torch.randn(512, 4096, device="cuda")
+    o0, o1 = torch.empty_like(x), torch.empty_like(x)
+    ids = torch.zeros((512, 2), dtype=torch.int32, device="cuda")
+    g = torch.zeros((512, 2), device="cuda")
+    w.layer_forward(0, x, o0, ids, g)
+    w.kernel_timing(True)
+    for _ in range(3):
+        w.layer_forward(0, x, o1, ids, g)
+    w.layer_forward(0, x[:1], o1[:1], ids[:1], g[:1])  # decode path: not timed
+    tot, n = w.kernel_timing(False)
+    torch.cuda.synchronize()
+    assert n == 3 and 100.0 < tot / n < 5000.0
+    w.layer_forward(0, x, o1, ids, g)
+    torch.cuda.synchronize()
+    assert torch.equal(o0, o1)
+    w.close()
+
+
 def test_router_many_tokens_batched_kernel(ctx, orc):
     """The router's per-token arithmetic does not depend on n_tok or on the
     token's slot in a block: one 4100-token call equals 1000-token chunks bit
