@@ -349,14 +349,21 @@ bool use_prefill(const moe_weights* w, int n_tok, const float* post) {
          (w->sp.counts == nullptr || w->prefill_splits > 0);  // counters: grouped kernel only
 }
 
+size_t prefill_h_bytes(const moe_weights* w, int n_tok) {
+  return ((size_t)n_tok * w->k() * w->f() * 2 + 255) & ~(size_t)255;
+}
+
 int ensure_prefill_scratch(moe_weights* w, int n_tok) {
   const size_t rows = (size_t)n_tok * w->k();
   TRY(w->pf_counts.ensure(4 * (size_t)w->E()));
   TRY(w->pf_offsets.ensure(4 * (size_t)w->E()));
   TRY(w->pf_perm.ensure(4 * rows));
   TRY(w->pf_xg.ensure(2 * rows * w->d()));
-  TRY(w->pf_h.ensure(2 * rows * w->f()));
-  TRY(w->y.ensure(4 * rows * w->d() * (size_t)std::max(1, w->prefill_splits)));
+  // [H | Y]: the grouped kernel's bf16 H and its fp32 Y partials in ONE
+  // allocation, so one persisting-L2 window covers both (H is read back by
+  // the down tiles, Y by the combine)
+  TRY(w->pf_h.ensure(prefill_h_bytes(w, n_tok) +
+                     4 * rows * w->d() * (size_t)std::max(1, w->prefill_splits)));
   TRY(w->pf_sync.ensure(4 * (1 + (size_t)w->E() * ((n_tok + moe::kPrefillChunk - 1) / moe::kPrefillChunk) +
                           w->E())));
   return MOE_OK;
@@ -396,6 +403,7 @@ int experts_forward(moe_weights* w, int l, const float* x, int n_tok, const int3
     return MOE_OK;
   }
   const float* cgates = gates;
+  float* ybuf = w->y.as<float>();  // expert outputs y[pair][d] (+ K-split partials)
   int nsplit = 1;
   const int32_t* split_of = nullptr;  // per-expert K splits of the grouped prefill
   if (use_prefill(w, n_tok, post)) {
@@ -419,8 +427,9 @@ int experts_forward(moe_weights* w, int l, const float* x, int n_tok, const int3
       offsets = w->pf_offsets2.as<int32_t>();
       slots = w->dev_res_slots.as<int16_t>() + (size_t)l * dm.E;
     }
+    ybuf = reinterpret_cast<float*>(w->pf_h.as<char>() + prefill_h_bytes(w, n_tok));
     if (w->n_local[l] < dm.E || w->replicas)
-      CU(cudaMemsetAsync(w->y.p, 0, (size_t)std::max(1, S) * rows * dm.d * 4, s));
+      CU(cudaMemsetAsync(ybuf, 0, (size_t)std::max(1, S) * rows * dm.d * 4, s));
     cudaEvent_t kt0 = nullptr, kt1 = nullptr;
     if (w->ktime_on) {
       if (w->kev_used == w->kev.size()) {
@@ -436,7 +445,7 @@ int experts_forward(moe_weights* w, int l, const float* x, int n_tok, const int3
     CU(moe::launch_prefill_experts(lw, w->n_local[l], dm, n_tok, x, counts, offsets, perm, gates,
                                    slots,
                                    w->pf_xg.as<__nv_bfloat16>(), w->pf_h.as<__nv_bfloat16>(),
-                                   w->y.as<float>(), w->pf_sync.as<int>(), w->ctx->sm_count, S,
+                                   ybuf, w->pf_sync.as<int>(), w->ctx->sm_count, S,
                                    s, sp, kt0, kt1));
     cgates = nullptr;
     nsplit = std::max(1, S);
@@ -446,11 +455,10 @@ int experts_forward(moe_weights* w, int l, const float* x, int n_tok, const int3
     CU(moe::launch_generic_down(lw, dm, w->h.as<float>(), n_tok, ids, w->y.as<float>(), s, pdl));
   }
   if (!ep) {
-    CU(moe::launch_combine(x, w->y.as<float>(), cgates, n_tok, dm, x_out, s, pdl, nsplit, ids,
-                           split_of));
+    CU(moe::launch_combine(x, ybuf, cgates, n_tok, dm, x_out, s, pdl, nsplit, ids, split_of));
   } else {
     float* delta = w->delta.as<float>();
-    CU(moe::launch_combine(nullptr, w->y.as<float>(), cgates, n_tok, dm, delta, s, pdl, nsplit, ids,
+    CU(moe::launch_combine(nullptr, ybuf, cgates, n_tok, dm, delta, s, pdl, nsplit, ids,
                            split_of));
     const long long nd = (long long)n_tok * dm.d;
     if (w->ctx->peers && nd <= w->ctx->pa.mt_cap) {

@@ -1050,18 +1050,28 @@ cudaError_t launch_prefill_experts(const LayerWeights& lw, int n_local, const Di
       // keep H (written by the up tiles, read back by the down tiles) in a
       // persisting L2 window so the weight stream does not evict it to DRAM
       // (measured: -29 MB DRAM write and re-read, ~5 us per 512-token layer)
-      static bool limit_set = false;
-      const size_t hbytes = (size_t)rows * dm.f * 2;
-      if (!limit_set) {
-        int dev = 0, maxp = 0;
+      // (and Y, read by the combine, when the caller placed it right after H)
+      static size_t limit_set = 0;
+      size_t wbytes = (size_t)rows * dm.f * 2;
+      const size_t ybytes = (size_t)std::max(1, splits) * rows * dm.d * 4;
+      const char* hb = reinterpret_cast<const char*>(h);
+      const char* yb = reinterpret_cast<const char*>(y);
+      if (yb >= hb + wbytes && yb <= hb + wbytes + 256) wbytes = (size_t)(yb - hb) + ybytes;
+      static int maxp = -1, maxw = 0;
+      if (maxp < 0) {
+        int dev = 0;
         cudaGetDevice(&dev);
         cudaDeviceGetAttribute(&maxp, cudaDevAttrMaxPersistingL2CacheSize, dev);
-        cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, std::min<size_t>((size_t)maxp, hbytes));
-        limit_set = true;
+        cudaDeviceGetAttribute(&maxw, cudaDevAttrMaxAccessPolicyWindowSize, dev);
+      }
+      wbytes = std::min<size_t>(wbytes, (size_t)std::min(maxp, maxw));
+      if (limit_set < wbytes) {
+        cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, wbytes);
+        limit_set = wbytes;
       }
       kattr[nk].id = cudaLaunchAttributeAccessPolicyWindow;
       kattr[nk].val.accessPolicyWindow.base_ptr = h;
-      kattr[nk].val.accessPolicyWindow.num_bytes = hbytes;
+      kattr[nk].val.accessPolicyWindow.num_bytes = wbytes;
       kattr[nk].val.accessPolicyWindow.hitRatio = 1.0f;
       kattr[nk].val.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
       kattr[nk].val.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
