@@ -459,9 +459,10 @@ def run_prefill(args):
         "metric": PREFILL_METRIC, "value": round(n / (ms * 1e-3), 1),
         "unit": "tok/s", "n_gpus": 1, "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms, 4),
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "bf16",
-        "data": "synthetic (random-init weights, N(0,1) tokens); inputs 512x4096 fp32 rotate over "
-                "steps, weights 2.8 GB >> L2",
+        "data": "synthetic (random-init weights, N(0,1) tokens)",
         "config": {"workload": PREFILL_WORKLOAD,
+                   "l2": "inputs larger than L2: 2.8 GB of expert weights streamed per step; token "
+                         "batches rotate over steps",
                    "path": "tcgen05/TMEM grouped GEMM (swap-AB), TMA SW128", "active_experts": active},
         "gpu_launches": w.forward_launches(n) * args.steps, "clocks": clk.summary(), "e2e": e2e,
         "cpu_baseline": cpu,
