@@ -141,3 +141,65 @@ def test_replica_mask_validation(gpu):
     for w in (plain, zero, rep):
         w.close()
     ctx.close()
+
+
+@pytest.mark.parametrize("dtype,n_tok", [(M.DTYPE_BF16, 1500), (M.DTYPE_F32, 40)])
+def test_replicas_odd_world_many_experts(gpu, dtype, n_tok):
+    """E = 16, top-4, 3 ranks (E not divisible by the world), every expert
+    replicated on 2 ranks: bf16 takes the tcgen05 path with the device plan
+    (a tiny cost model so that splits happen), fp32 the generic kernels
+    (owner-only execution).  Ranks bit-identical, equal to the unsharded
+    layer within fp32 rounding."""
+    L, E, k, d, f, world = 1, 16, 4, 256, 512, 3
+    esz = 2 if dtype == M.DTYPE_BF16 else 4
+    s = M.Shape(L, E, k, d, f, esz)
+    b = _bench()
+    base = M.Ctx(0)
+    full = M.Weights(base, s, dtype)
+    full.random(31)
+    x = torch.randn(n_tok, d, device="cuda", generator=torch.Generator(device="cuda").manual_seed(9))
+    want = torch.empty_like(x)
+    ids = torch.zeros((n_tok, k), dtype=torch.int32, device="cuda")
+    g = torch.zeros((n_tok, k), device="cuda")
+    full.layer_forward(0, x, want, ids, g, stream=base.stream)
+    base.synchronize()
+    owner = b.shard_map(L, E, world)
+    mask = np.zeros((L, E), np.uint32)
+    for e in range(E):
+        mask[0, e] = (1 << owner[0, e]) | (1 << ((owner[0, e] + 1) % world))
+    ctxs = [M.Ctx(0) for _ in range(world)]
+    M.Ctx.link_peers(ctxs, d, max_tokens=n_tok)
+    ws = [M.Weights(c, s, dtype, owner=owner, replicas=mask) for c in ctxs]
+    for w in ws:
+        w.random(31)
+        w.replica_cost = (1000, 100, 0)  # compute-bound model: split whenever possible
+        w.reserve(n_tok)
+    outs = [torch.empty_like(x) for _ in range(world)]
+    idss = [torch.zeros_like(ids) for _ in range(world)]
+    gs = [torch.zeros_like(g) for _ in range(world)]
+    torch.cuda.synchronize()
+    for r in range(world):
+        ws[r].layer_forward(0, x, outs[r], idss[r], gs[r], stream=ctxs[r].stream)
+    for c in ctxs:
+        c.synchronize()
+        c.peer_check()
+    for r in range(1, world):
+        assert torch.equal(outs[r], outs[0])
+    assert torch.equal(idss[0], ids)
+    xd = x.double()
+    err = float(((outs[0].double() - xd) - (want.double() - xd)).abs().max() / (want.double() - xd).abs().max())
+    assert err < 1e-4, err
+    if dtype == M.DTYPE_BF16:
+        counts = np.bincount(ids.cpu().numpy().ravel(), minlength=E).astype(np.int32)
+        holders = (1 << owner[0]).astype(np.uint32) | mask[0]
+        split = 0
+        for e in range(E):
+            parts = [M.replica_plan(counts, holders, world, 1000, 100, 0, 256, r) for r in range(world)]
+            split += sum(int(p[1][e] > p[0][e]) for p in parts) > 1
+        assert split > 0
+    for w in ws:
+        w.close()
+    for c in ctxs:
+        c.close()
+    full.close()
+    base.close()
