@@ -1047,16 +1047,14 @@ cudaError_t launch_prefill_experts(const LayerWeights& lw, int n_local, const Di
     if (!(no_pdl || trace_path || t0)) kattr[nk++] = pdl_attr[0];
     static const int persist = getenv("MOE_B200_PF_PERSIST") ? atoi(getenv("MOE_B200_PF_PERSIST")) : 1;
     if (persist) {
-      // keep H (written by the up tiles, read back by the down tiles) in a
-      // persisting L2 window so the weight stream does not evict it to DRAM
-      // (measured: -29 MB DRAM write and re-read, ~5 us per 512-token layer)
-      // (and Y, read by the combine, when the caller placed it right after H)
+      // keep H (written by the up tiles, read back by the down tiles) and Y
+      // (read by the combine; the caller places it right after H) in a
+      // persisting L2 window so the weight stream does not evict them to
+      // DRAM — only when the whole window fits the persisting set-aside:
+      // measured -3..-5 us at 512 tokens (62.5 MB), but a clamped window
+      // at 2048-8192 tokens cost 2-5 % (it starves the weight tiles' L2
+      // reuse across token chunks)
       static size_t limit_set = 0;
-      size_t wbytes = (size_t)rows * dm.f * 2;
-      const size_t ybytes = (size_t)std::max(1, splits) * rows * dm.d * 4;
-      const char* hb = reinterpret_cast<const char*>(h);
-      const char* yb = reinterpret_cast<const char*>(y);
-      if (yb >= hb + wbytes && yb <= hb + wbytes + 256) wbytes = (size_t)(yb - hb) + ybytes;
       static int maxp = -1, maxw = 0;
       if (maxp < 0) {
         int dev = 0;
@@ -1064,18 +1062,29 @@ cudaError_t launch_prefill_experts(const LayerWeights& lw, int n_local, const Di
         cudaDeviceGetAttribute(&maxp, cudaDevAttrMaxPersistingL2CacheSize, dev);
         cudaDeviceGetAttribute(&maxw, cudaDevAttrMaxAccessPolicyWindowSize, dev);
       }
-      wbytes = std::min<size_t>(wbytes, (size_t)std::min(maxp, maxw));
-      if (limit_set < wbytes) {
-        cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, wbytes);
-        limit_set = wbytes;
+      size_t wbytes = (size_t)rows * dm.f * 2;
+      const size_t ybytes = (size_t)std::max(1, splits) * rows * dm.d * 4;
+      const char* hb = reinterpret_cast<const char*>(h);
+      const char* yb = reinterpret_cast<const char*>(y);
+      if (yb >= hb + wbytes && yb <= hb + wbytes + 256) wbytes = (size_t)(yb - hb) + ybytes;
+      if (wbytes <= (size_t)std::min(maxp, maxw)) {
+        if (limit_set < wbytes) {
+          cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, wbytes);
+          limit_set = wbytes;
+        }
+        kattr[nk].id = cudaLaunchAttributeAccessPolicyWindow;
+        kattr[nk].val.accessPolicyWindow.base_ptr = h;
+        kattr[nk].val.accessPolicyWindow.num_bytes = wbytes;
+        kattr[nk].val.accessPolicyWindow.hitRatio = 1.0f;
+        kattr[nk].val.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
+        kattr[nk].val.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
+        ++nk;
+      } else if (limit_set) {
+        // a larger batch after a windowed one: give the set-aside back
+        cudaCtxResetPersistingL2Cache();
+        cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, 0);
+        limit_set = 0;
       }
-      kattr[nk].id = cudaLaunchAttributeAccessPolicyWindow;
-      kattr[nk].val.accessPolicyWindow.base_ptr = h;
-      kattr[nk].val.accessPolicyWindow.num_bytes = wbytes;
-      kattr[nk].val.accessPolicyWindow.hitRatio = 1.0f;
-      kattr[nk].val.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
-      kattr[nk].val.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
-      ++nk;
     }
     kcfg.attrs = kattr;
     kcfg.numAttrs = nk;
