@@ -1051,16 +1051,19 @@ cudaError_t launch_prefill_experts(const LayerWeights& lw, int n_local, const Di
       // (read by the combine; the caller places it right after H) in a
       // persisting L2 window so the weight stream does not evict them to
       // DRAM — only when the whole window fits the persisting set-aside:
-      // measured -3..-5 us at 512 tokens (62.5 MB), but a clamped window
-      // at 2048-8192 tokens cost 2-5 % (it starves the weight tiles' L2
-      // reuse across token chunks)
+      // measured -3..-9 us at 512 tokens (62.5 MB), but a clamped window
+      // at 2048-8192 tokens cost 2-5 % and a 73 MB one at 640 tokens 1-2 %
       static size_t limit_set = 0;
-      static int maxp = -1, maxw = 0;
+      static int maxp = -1, maxw = 0, l2 = 0;
       if (maxp < 0) {
         int dev = 0;
         cudaGetDevice(&dev);
         cudaDeviceGetAttribute(&maxp, cudaDevAttrMaxPersistingL2CacheSize, dev);
         cudaDeviceGetAttribute(&maxw, cudaDevAttrMaxAccessPolicyWindowSize, dev);
+        cudaDeviceGetAttribute(&l2, cudaDevAttrL2CacheSize, dev);
+        // at most half the L2 set aside: 73 MB at 640 tokens already cost
+        // 6-12 us (the rest of the kernel's L2 traffic loses the space)
+        maxp = std::min(maxp, l2 / 2);
       }
       size_t wbytes = (size_t)rows * dm.f * 2;
       const size_t ybytes = (size_t)std::max(1, splits) * rows * dm.d * 4;
