@@ -1045,7 +1045,7 @@ cudaError_t launch_prefill_experts(const LayerWeights& lw, int n_local, const Di
     cudaLaunchAttribute kattr[2];
     int nk = 0;
     if (!(no_pdl || trace_path || t0)) kattr[nk++] = pdl_attr[0];
-    static const int persist = getenv("MOE_B200_PF_PERSIST") ? atoi(getenv("MOE_B200_PF_PERSIST")) : 1;
+    static int persist = getenv("MOE_B200_PF_PERSIST") ? atoi(getenv("MOE_B200_PF_PERSIST")) : 1;
     if (persist) {
       // keep H (written by the up tiles, read back by the down tiles) and Y
       // (read by the combine; the caller places it right after H) in a
@@ -1057,10 +1057,11 @@ cudaError_t launch_prefill_experts(const LayerWeights& lw, int n_local, const Di
       static int maxp = -1, maxw = 0, l2 = 0;
       if (maxp < 0) {
         int dev = 0;
-        cudaGetDevice(&dev);
-        cudaDeviceGetAttribute(&maxp, cudaDevAttrMaxPersistingL2CacheSize, dev);
-        cudaDeviceGetAttribute(&maxw, cudaDevAttrMaxAccessPolicyWindowSize, dev);
-        cudaDeviceGetAttribute(&l2, cudaDevAttrL2CacheSize, dev);
+        if (cudaGetDevice(&dev) != cudaSuccess ||
+            cudaDeviceGetAttribute(&maxp, cudaDevAttrMaxPersistingL2CacheSize, dev) != cudaSuccess ||
+            cudaDeviceGetAttribute(&maxw, cudaDevAttrMaxAccessPolicyWindowSize, dev) != cudaSuccess ||
+            cudaDeviceGetAttribute(&l2, cudaDevAttrL2CacheSize, dev) != cudaSuccess)
+          maxp = maxw = l2 = 0;
         // at most half the L2 set aside: 73 MB at 640 tokens already cost
         // 6-12 us (the rest of the kernel's L2 traffic loses the space)
         maxp = std::min(maxp, l2 / 2);
@@ -1072,9 +1073,18 @@ cudaError_t launch_prefill_experts(const LayerWeights& lw, int n_local, const Di
       if (yb >= hb + wbytes && yb <= hb + wbytes + 256) wbytes = (size_t)(yb - hb) + ybytes;
       if (wbytes <= (size_t)std::min(maxp, maxw)) {
         if (limit_set < wbytes) {
-          cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, wbytes);
+          if (cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, wbytes) != cudaSuccess) {
+            // no persisting L2 here (e.g. under MPS): clear the non-sticky
+            // error so a later cudaGetLastError() does not report it, and
+            // run without the window from now on
+            (void)cudaGetLastError();
+            persist = 0;
+            wbytes = 0;
+          }
           limit_set = wbytes;
         }
+      }
+      if (persist && wbytes && wbytes <= (size_t)std::min(maxp, maxw)) {
         kattr[nk].id = cudaLaunchAttributeAccessPolicyWindow;
         kattr[nk].val.accessPolicyWindow.base_ptr = h;
         kattr[nk].val.accessPolicyWindow.num_bytes = wbytes;
@@ -1082,10 +1092,11 @@ cudaError_t launch_prefill_experts(const LayerWeights& lw, int n_local, const Di
         kattr[nk].val.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
         kattr[nk].val.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
         ++nk;
-      } else if (limit_set) {
+      } else if (persist && limit_set) {
         // a larger batch after a windowed one: give the set-aside back
-        cudaCtxResetPersistingL2Cache();
-        cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, 0);
+        if (cudaCtxResetPersistingL2Cache() != cudaSuccess ||
+            cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, 0) != cudaSuccess)
+          (void)cudaGetLastError();
         limit_set = 0;
       }
     }
