@@ -19,6 +19,14 @@ if ROOT not in sys.path:
 def pytest_configure(config):
     config.addinivalue_line("markers", "gpu: needs a B200 (sm_100a) GPU")
     config.addinivalue_line("markers", "slow: long-running")
+    # a fresh checkout: build the in-tree libraries first (nvcc cross-compiles
+    # without a GPU); an existing build is left alone
+    lib = os.path.join(ROOT, "paper_2402_07033_b200", "_build", "libmoe_b200.so")
+    if not os.path.exists(lib) and not os.environ.get("MOE_B200_LIB"):
+        import subprocess
+
+        subprocess.run(["make", "-s", "-j", str(os.cpu_count() or 4), "-C",
+                        os.path.join(ROOT, "paper_2402_07033_b200", "csrc")], check=True)
 
 
 @pytest.fixture(scope="session")
