@@ -27,6 +27,13 @@ def pytest_configure(config):
 
         subprocess.run(["make", "-s", "-j", str(os.cpu_count() or 4), "-C",
                         os.path.join(ROOT, "paper_2402_07033_b200", "csrc")], check=True)
+    # the checker: the reference compiled from its own sources (here only —
+    # /root/reference does not exist on the GPU box, which uses prebuilt files)
+    ref = os.path.join(ROOT, "oracle", "_ref", "libmoe_ref.so")
+    if not os.path.exists(ref) and os.path.isdir("/root/reference/proj"):
+        import subprocess
+
+        subprocess.run(["make", "-s", "-C", os.path.join(ROOT, "oracle"), "oracle", "ref"], check=False)
 
 
 @pytest.fixture(scope="session")
