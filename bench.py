@@ -209,7 +209,7 @@ def run_ours(args):
             handles = [None] * world
             dist.all_gather_object(handles, ctx.peer_window(world, d))
             ctx.open_peers(world, rank, handles)
-    elif os.environ.get("MOE_B200_FORCE_EP") == "1":
+    elif args.force_ep:
         ctx.init_ep(1, 0, M.Ctx.unique_id())  # 1-rank NCCL: the EP code path on one GPU
     shape = M.Shape(L, E, k, d, f, esz)
     owner = shard_map(L, E, world) if world > 1 and args.shard == "ep" else None
@@ -615,6 +615,10 @@ def main():
                     help="N>1: ncclAllReduce instead of the fused peer-memory combine")
     ap.add_argument("--no-stack", action="store_true",
                     help="per-layer 2-kernel graph instead of the persistent stack kernel")
+    ap.add_argument("--stack-kernel", type=int, default=0, choices=[0, 1, 2],
+                    help="A/B: 1 = two-barrier persistent kernel, 2 = single-barrier fixed-point kernel (default)")
+    ap.add_argument("--force-ep", action="store_true",
+                    help="testing: 1-rank NCCL communicator (the expert-parallel code path on one GPU)")
     ap.add_argument("--traffic", type=float, default=None,
                     help="dram bytes per launch of the decode kernel from an ncu --set full capture")
     args = ap.parse_args()
@@ -628,8 +632,15 @@ def main():
             args.traffic = tj.get("dram_bytes_per_launch")
         args.stack_traffic = tj.get("stack_dram_bytes_per_launch")
         args.prefill_traffic = tj.get("prefill_dram_bytes_per_launch")
-    if args.no_stack:
-        os.environ["MOE_B200_STACK"] = "0"
+    if args.no_stack or args.stack_kernel or args.force_ep:
+        import paper_2402_07033_b200 as M
+
+        if args.no_stack:
+            M.set_option("stack", 0)
+        if args.stack_kernel:
+            M.set_option("stack_kernel", args.stack_kernel)
+        if args.force_ep:
+            M.set_option("force_ep", 1)
     if args.impl == "reference":
         run_reference(args)
     elif args.config == "prefill512":

@@ -8,9 +8,17 @@
  *
  * Each function replaces a reference interface of the `moe_orch` C++ API
  * (/root/reference/proj/include/moe_orch/...).  The drop-in C++ shim
- * (paper_2402_07033_b200/csrc/moe_orch_b200.cpp, headers include/moe_orch/)
+ * (paper_2402_07033_b200/csrc/moe_orch_device.cpp for the math and
+ * moe_orch_host.cpp for placement / trace / shape, headers include/moe_orch/)
  * implements the reference signatures on top of these calls; INTEGRATION.md
  * shows the bindings.
+ *
+ * Threading: a moe_weights may be used from several threads and streams;
+ * calls on one moe_weights are serialized (a per-weights lock on the host,
+ * and every call's device work is ordered after the previous call's on
+ * whatever stream that ran, because the calls share the weights' scratch).
+ * Calls on different moe_weights run concurrently (each has its own stream
+ * for the host-buffer entry points).
  */
 #ifndef MOE_B200_H
 #define MOE_B200_H
@@ -266,12 +274,29 @@ int moe_expert_path(moe_weights* w, int n_tok);
 /* Number of kernels one moe_forward(n_tok) launches. */
 int moe_forward_launches(moe_weights* w, int n_tok);
 /* Diagnostics: one batch-1 moe_forward through the persistent stack kernel
- * with per-CTA %globaltimer stamps.  trace receives [L][sm_count][8] u64:
- * 0 layer start, 1 first ring stage landed, 2 stream done, 3 after grid
- * barrier 1, 4 reduce done, 5 after grid barrier 2, 6 producer released,
- * 7 producer issued last copy.  Synchronous. */
+ * with per-CTA clock64 stamps (tools/trace_stack.py).  trace receives
+ * [L][sm_count][16] u64 (slot meanings in tools/trace_stack.py).  Synchronous. */
 int moe_debug_trace_forward(moe_weights* w, float* x, int32_t* ids, float* gates,
                             uint64_t* trace, int64_t cap);
+/* One batch-1 moe_forward through the persistent stack kernel that also
+ * records every layer's fp32 router logits (logits: device [L x E]) — the
+ * values its top-k ranked, for the routing-margin report (SURVEY §8c:
+ * tokens whose 2nd-3rd logit margin is below 1e-5 max|logit|).  Asynchronous
+ * on `stream`.  MOE_ERR_UNSUPPORTED without a persistent-kernel plan. */
+int moe_forward_logits(moe_weights* w, float* x, int32_t* ids, float* gates, float* logits,
+                       void* stream);
+
+/* ---- debug / A-B switches (tests and tools/ only) ----------------------
+ * The library never reads the environment; these set process-wide options
+ * (read when a moe_weights is created, or at launch):
+ *   stack (1), stack_kernel (2), rw (1), prefill (1), prefill_splits (2),
+ *   stack_grid (0), virtual_stack (0), noncoop (0), force_ep (0), no_pdl (0),
+ *   combine4 (0), pf_debug, pf_evict, pf_lag, pf_late8, pf_slo, pf_persist.
+ * Unknown names return MOE_ERR_ARG.  See DESIGN.md §6b. */
+int moe_debug_set_option(const char* name, int64_t value);
+int moe_debug_get_option(const char* name, int64_t* value);
+/* Per-tile timeline file of the grouped prefill kernel (NULL / "" = off). */
+int moe_debug_set_trace_path(const char* path);
 
 #ifdef __cplusplus
 }

@@ -21,7 +21,11 @@ from .capi import (  # noqa: F401
     Shape,
     Weights,
     declared_symbols,
+    get_option,
     lib,
     lib_path,
+    options,
     replica_plan,
+    set_option,
+    set_trace_path,
 )

@@ -127,6 +127,10 @@ def lib():
         "moe_expert_path": ([_vp, C.c_int], C.c_int),
         "moe_forward_launches": ([_vp, C.c_int], C.c_int),
         "moe_debug_trace_forward": ([_vp, _vp, _vp, _vp, C.POINTER(C.c_uint64), C.c_int64], C.c_int),
+        "moe_forward_logits": ([_vp, _vp, _vp, _vp, _vp, _vp], C.c_int),
+        "moe_debug_set_option": ([C.c_char_p, C.c_int64], C.c_int),
+        "moe_debug_get_option": ([C.c_char_p, C.POINTER(C.c_int64)], C.c_int),
+        "moe_debug_set_trace_path": ([C.c_char_p], C.c_int),
     }
     for name, (args, res) in sig.items():
         fn = getattr(L, name)
@@ -139,6 +143,40 @@ def lib():
 def check(rc: int):
     if rc != 0:
         raise MoeError(rc, lib().moe_last_error().decode())
+
+
+def get_option(name: str) -> int:
+    v = C.c_int64()
+    check(lib().moe_debug_get_option(name.encode(), C.byref(v)))
+    return v.value
+
+
+def set_option(name: str, value: int) -> None:
+    """Debug / A-B switch of the library (moe_debug_set_option)."""
+    check(lib().moe_debug_set_option(name.encode(), int(value)))
+
+
+class options:
+    """Context manager: ``with options(stack=0): ...`` sets library debug
+    options and restores the previous values on exit."""
+
+    def __init__(self, **kw):
+        self.kw = kw
+        self.old = {}
+
+    def __enter__(self):
+        for k, v in self.kw.items():
+            self.old[k] = get_option(k)
+            set_option(k, v)
+        return self
+
+    def __exit__(self, *a):
+        for k, v in self.old.items():
+            set_option(k, v)
+
+
+def set_trace_path(path: str | None) -> None:
+    check(lib().moe_debug_set_trace_path((path or "").encode()))
 
 
 def _dptr(a: np.ndarray):
@@ -436,6 +474,12 @@ class Weights:
         check(lib().moe_debug_trace_forward(self.h, _ptr(x), _ptr(ids), _ptr(gates),
                                             tr.ctypes.data_as(C.POINTER(C.c_uint64)), n))
         return tr.reshape(self.shape.num_layers, self.ctx.sm_count, 16)
+
+    def forward_logits(self, x, ids, gates, logits, stream=None):
+        """Batch-1 forward through the persistent kernel that also records
+        every layer's router logits (logits: device fp32 [L x E])."""
+        check(lib().moe_forward_logits(self.h, _ptr(x), _ptr(ids), _ptr(gates), _ptr(logits),
+                                       _stream(stream, x)))
 
     def expert_path(self, n_tok: int) -> int:
         return lib().moe_expert_path(self.h, n_tok)

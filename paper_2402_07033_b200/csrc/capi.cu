@@ -22,6 +22,18 @@
 using moe::Dims;
 using moe::LayerWeights;
 
+namespace moe {
+DebugOptions& debug_options() {
+  static DebugOptions o;
+  return o;
+}
+static std::string& trace_path_store() {
+  static std::string p;
+  return p;
+}
+const char* debug_trace_path() { return trace_path_store().c_str(); }
+}  // namespace moe
+
 namespace {
 
 thread_local std::string g_err;
@@ -160,6 +172,7 @@ struct moe_weights {
   // scratch
   DevBuf ypart, rpart, counter, xa, xb, xin, h, y, delta, ids, gates, post;
   DevBuf xbuf2, gbar, dev_layers, dev_slots;  // persistent stack kernel
+  DevBuf stack_acc;  // decode_stack2_kernel: fixed-point accumulators + barrier state
   DevBuf pf_counts, pf_offsets, pf_perm, pf_xg, pf_h, pf_sync;  // tcgen05 prefill
   DevBuf io;  // host-buffer API, batch 1: [x][ids][gates] (one D2H)
   // moe_debug_kernel_timing: event pairs around each grouped prefill launch
@@ -179,7 +192,8 @@ struct moe_weights {
   DevBuf stage_d;  // fp64 staging for uploads / downloads
   void* host_pin = nullptr;
   size_t host_pin_bytes = 0;
-  std::map<std::tuple<float*, int32_t*, float*, cudaStream_t>, GraphEntry> graphs;
+  // key: (x, ids, gates, host buffer, stack kernel option)
+  std::map<std::tuple<float*, int32_t*, float*, cudaStream_t, int>, GraphEntry> graphs;
   cudaStream_t cap_stream = nullptr;  // private stream for graph capture
   cudaEvent_t io_ev[kIoChunks] = {};  // host-buffer API: per-chunk D2H completion
   std::mutex mu;
@@ -307,7 +321,7 @@ bool use_stack(const moe_weights* w, int n_tok) {
   // MOE_B200_VIRTUAL_STACK (measurement hook, tools/shard_proxy.py): a
   // virtual rank runs its shard through the persistent kernel with no
   // exchange — one rank's streaming time of an N-GPU step
-  static const bool virt = getenv("MOE_B200_VIRTUAL_STACK") != nullptr;
+  const bool virt = moe::debug_options().virtual_stack != 0;
   const moe_ctx* c = w->ctx;
   return use_decode(w, n_tok, nullptr) && (!c->ep() || peer_ok(w) || (c->virtual_ep && virt)) &&
          w->stack_enabled && w->L() > 0;
@@ -327,8 +341,15 @@ int refresh_projection(moe_weights* w) {
   return MOE_OK;
 }
 
+// The single-barrier fixed-point stack kernel (single GPU, E <= 8, router
+// projections on); decode_stack_kernel otherwise.
+bool use_stack2(const moe_weights* w) {
+  return moe::debug_options().stack_kernel == 2 && !w->ctx->ep() && w->rw_enabled && w->stack_acc.p != nullptr &&
+         moe::stack2_supported(w->plan, w->dims());
+}
+
 int enqueue_stack(moe_weights* w, float* x, int32_t* ids, float* gates, cudaStream_t s,
-                  unsigned long long* trace = nullptr) {
+                  unsigned long long* trace = nullptr, float* logits = nullptr) {
   moe::StackDesc sd;
   sd.trace = trace;
   sd.rw = w->rw_enabled ? w->dev_rw.as<const float* const>() : nullptr;
@@ -338,6 +359,11 @@ int enqueue_stack(moe_weights* w, float* x, int32_t* ids, float* gates, cudaStre
   sd.mat_stride = w->mat_elems();
   sd.router = w->router;
   sd.L = w->L();
+  if (use_stack2(w)) {
+    CU(moe::launch_decode_stack2(w->plan, sd, w->dims(), x, w->stack_acc.p, ids, gates, logits, s));
+    return MOE_OK;
+  }
+  if (logits) return fail(MOE_ERR_UNSUPPORTED, "router logits need the single-barrier stack kernel");
   CU(moe::launch_decode_stack(w->plan, sd, w->dims(), x, w->xbuf2.as<float>(),
                               w->ypart.as<float>(), w->rpart.as<float>(), ids, gates,
                               w->gbar.as<unsigned>(), s, peer_ok(w) ? &w->ctx->pa : nullptr));
@@ -506,7 +532,8 @@ int enqueue_forward(moe_weights* w, float* x, int n_tok, int32_t* ids, float* ga
 // pointer is part of the key (in the stream slot).
 int forward_graph(moe_weights* w, float* x, int32_t* ids, float* gates, cudaStream_t s,
                   void* host_io = nullptr, size_t in_bytes = 0, size_t out_bytes = 0) {
-  auto key = std::make_tuple(x, ids, gates, reinterpret_cast<cudaStream_t>(host_io));
+  auto key = std::make_tuple(x, ids, gates, reinterpret_cast<cudaStream_t>(host_io),
+                             moe::debug_options().stack_kernel);
   auto it = w->graphs.find(key);
   if (it == w->graphs.end()) {
     cudaStream_t cs = w->cap_stream;  // created with the weights (creation may synchronize)
@@ -556,6 +583,54 @@ int host_pinned(moe_weights* w, size_t bytes, void** out) {
 extern "C" {
 
 int moe_version(void) { return 1; }
+
+// Debug / A-B switches (kernels.h DebugOptions): the only way to change the
+// product's code path besides the shape and the world (no environment reads).
+static int* option_slot(const char* name) {
+  moe::DebugOptions& o = moe::debug_options();
+  static const std::pair<const char*, int moe::DebugOptions::*> table[] = {
+      {"stack", &moe::DebugOptions::stack},
+      {"stack_kernel", &moe::DebugOptions::stack_kernel},
+      {"rw", &moe::DebugOptions::rw},
+      {"prefill", &moe::DebugOptions::prefill},
+      {"prefill_splits", &moe::DebugOptions::prefill_splits},
+      {"stack_grid", &moe::DebugOptions::stack_grid},
+      {"virtual_stack", &moe::DebugOptions::virtual_stack},
+      {"noncoop", &moe::DebugOptions::noncoop},
+      {"force_ep", &moe::DebugOptions::force_ep},
+      {"no_pdl", &moe::DebugOptions::no_pdl},
+      {"combine4", &moe::DebugOptions::combine4},
+      {"pf_debug", &moe::DebugOptions::pf_debug},
+      {"pf_evict", &moe::DebugOptions::pf_evict},
+      {"pf_lag", &moe::DebugOptions::pf_lag},
+      {"pf_late8", &moe::DebugOptions::pf_late8},
+      {"pf_slo", &moe::DebugOptions::pf_slo},
+      {"pf_persist", &moe::DebugOptions::pf_persist},
+  };
+  if (!name) return nullptr;
+  for (const auto& e : table)
+    if (std::strcmp(e.first, name) == 0) return &(o.*(e.second));
+  return nullptr;
+}
+
+int moe_debug_set_option(const char* name, int64_t value) {
+  int* p = option_slot(name);
+  if (!p) return fail(MOE_ERR_ARG, std::string("unknown debug option: ") + (name ? name : "(null)"));
+  *p = (int)value;
+  return MOE_OK;
+}
+
+int moe_debug_get_option(const char* name, int64_t* value) {
+  int* p = option_slot(name);
+  if (!p || !value) return fail(MOE_ERR_ARG, std::string("unknown debug option: ") + (name ? name : "(null)"));
+  *value = *p;
+  return MOE_OK;
+}
+
+int moe_debug_set_trace_path(const char* path) {
+  moe::trace_path_store() = path ? path : "";
+  return MOE_OK;
+}
 const char* moe_last_error(void) { return g_err.c_str(); }
 int moe_shape_validate(const moe_shape* s) { return check_shape(s); }
 
@@ -617,8 +692,7 @@ int moe_ep_unique_id(void* uid128) {
 int moe_ctx_init_ep(moe_ctx* c, int world, int rank, const void* uid128) {
   if (!c || !uid128) return fail(MOE_ERR_ARG, "null argument");
   if (world < 1 || rank < 0 || rank >= world) return fail(MOE_ERR_ARG, "bad world/rank");
-  const char* force = getenv("MOE_B200_FORCE_EP");
-  if (world == 1 && !(force && force[0] == '1')) {
+  if (world == 1 && !moe::debug_options().force_ep) {
     c->world = 1;
     c->rank = 0;
     return MOE_OK;
@@ -884,9 +958,8 @@ static int weights_create(moe_ctx* c, const moe_shape* shape, int dtype,
   w->device_bytes += rbytes;
   w->plan = moe::plan_decode(w->dims(), c->sm_count);
   {
-    const char* env = getenv("MOE_B200_RW");
     w->rw_enabled = w->plan.ok && (!c->ep() || c->peers) && L >= 2 && E <= 8 &&
-                    (size_t)E * shape->hidden_dim * 4 <= 200 * 1024 && !(env && env[0] == '0');
+                    (size_t)E * shape->hidden_dim * 4 <= 200 * 1024 && moe::debug_options().rw;
     if (w->rw_enabled) {
       w->rw_mem.resize(L - 1);
       std::vector<const float*> ptrs(L, nullptr);
@@ -903,9 +976,14 @@ static int weights_create(moe_ctx* c, const moe_shape* shape, int dtype,
   }
   if (cudaStreamCreateWithFlags(&w->cap_stream, cudaStreamNonBlocking) != cudaSuccess)
     return cleanup(fail(MOE_ERR_CUDA, "create capture stream"));
-  if (const char* env = getenv("MOE_B200_STACK")) w->stack_enabled = env[0] != '0';
-  if (const char* env = getenv("MOE_B200_PREFILL")) w->prefill_enabled = env[0] != '0';
-  if (const char* env = getenv("MOE_B200_PREFILL_SPLITS")) w->prefill_splits = atoi(env);
+  w->stack_enabled = moe::debug_options().stack != 0;
+  if (w->rw_enabled && !c->ep() && moe::stack2_supported(w->plan, w->dims())) {
+    if (w->stack_acc.ensure(moe::stack2_acc_bytes(w->dims())))  // zeroed: the kernel's invariant
+      return cleanup(fail(MOE_ERR_OOM, "cudaMalloc stack accumulators"));
+    w->device_bytes += (int64_t)w->stack_acc.bytes;
+  }
+  w->prefill_enabled = moe::debug_options().prefill != 0;
+  w->prefill_splits = moe::debug_options().prefill_splits;
   {
     // device-side tables for the persistent stack kernel
     const int Lm = std::max(1, L);
@@ -1035,7 +1113,8 @@ int moe_weights_destroy(moe_weights* w) {
                     &w->dev_layers, &w->dev_slots, &w->pf_counts, &w->pf_offsets, &w->pf_perm,
                     &w->pf_xg, &w->pf_h, &w->pf_sync})
     b->release();
-  for (DevBuf* b : {&w->dev_holders, &w->dev_res_slots, &w->pf_counts2, &w->pf_offsets2, &w->io})
+  for (DevBuf* b : {&w->dev_holders, &w->dev_res_slots, &w->pf_counts2, &w->pf_offsets2, &w->io,
+                    &w->stack_acc})
     b->release();
   for (cudaEvent_t e : w->io_ev)
     if (e) cudaEventDestroy(e);
@@ -1514,6 +1593,18 @@ int moe_debug_trace_forward(moe_weights* w, float* x, int32_t* ids, float* gates
     rc = fail(MOE_ERR_CUDA, "trace copy failed");
   buf.release();
   return rc;
+}
+
+int moe_forward_logits(moe_weights* w, float* x, int32_t* ids, float* gates, float* logits,
+                       void* stream) {
+  if (!w || !x || !ids || !gates || !logits) return fail(MOE_ERR_ARG, "null pointer");
+  if (!use_stack(w, 1) || !use_stack2(w))
+    return fail(MOE_ERR_UNSUPPORTED, "no single-barrier persistent stack plan for these weights");
+  std::lock_guard<std::mutex> lk(w->mu);
+  TRY(set_device(w->ctx));
+  TRY(ensure_scratch(w, 1));
+  TRY(refresh_projection(w));
+  return enqueue_stack(w, x, ids, gates, pick(w->ctx, stream), nullptr, logits);
 }
 
 int moe_forward_launches(moe_weights* w, int n_tok) {

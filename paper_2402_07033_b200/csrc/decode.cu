@@ -503,7 +503,7 @@ __device__ __forceinline__ void grid_sync(unsigned* bar, unsigned target, int nc
     unsigned v;
     do {
       asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(bar) : "memory");
-    } while (v < target);
+    } while ((int)(v - target) < 0);  // modulo 2^32: decode_stack2_kernel's counter never resets
   }
   named_bar_sync(2, ncons);
 }
@@ -874,6 +874,279 @@ __global__ void __launch_bounds__(kMaxConsWarps * 32 + 32, 1)
 }
 
 // ---------------------------------------------------------------------------
+// persistent whole-stack kernel with ONE grid barrier per layer
+//
+// decode_stack_kernel sums the per-CTA partials in a fixed float order, which
+// needs a column-chunk reduction pass and a second grid barrier before any CTA
+// holds x_{l+1} (~6 us of every ~115 us layer, tools/trace_stack.py).  Here
+// every CTA adds its partial into an L2-resident accumulator with 64-bit
+// integer atomics in fixed point (2^-32): integer addition is associative, so
+// the sum — and x_{l+1}, and the routing — is bit-identical whatever order
+// the contributions land in, and right after the one barrier every CTA reads
+// the finished accumulator.  The next layer's router logits are assembled the
+// same way: R_{l+1} x_l (split over CTAs and threads, one column per thread)
+// plus the z partials of R_{l+1} W2 accumulated during the stream.
+//
+// Range: a partial |v| >= 2^22 (so the 148-CTA sum could leave the 2^31
+// fixed-point range) is counted in an overflow word; that layer's x and
+// logits then become NaN (loud, never a silently wrapped sum).
+//
+// Accumulators rotate over 3 buffers (layer l uses buf(l)); buf(l+2) is
+// zeroed after layer l's barrier, which orders the zeroing before any use of
+// that buffer (at layer l+2, after barrier l+1).  The barrier counter and the
+// rotation carry across launches in `state`, so nothing is reset per launch.
+constexpr float kFix = 4294967296.0f;               // 2^32
+constexpr float kFixInv = 2.3283064365386963e-10f;  // 2^-32
+constexpr float kFixMax = 4194304.0f;               // 2^22
+constexpr int kZStride = 16;                        // zacc words per buffer: kZMax logits + overflow
+constexpr int kStateBase = 32;                      // state[32] barrier base, state[33] rotation
+
+struct Stack2Args {
+  const void* const* layer_experts;
+  const int16_t* slot_of;
+  long long expert_stride, mat_stride;
+  const float* router;               // [L][E][d]
+  const float* const* rw;            // [L] R_{l+1} W2 per local expert [f][E]
+  float* x;                          // in: x_0, out: x_L
+  unsigned long long* acc;           // [3][d] fixed point
+  unsigned long long* zacc;          // [3][kZStride]
+  unsigned* state;                   // [0] barrier counter, [32] base, [33] rotation
+  int32_t* ids_out;                  // [L][k]
+  float* gates_out;                  // [L][k]
+  float* logits_out;                 // optional [L][E]
+  unsigned long long* trace;         // optional [L][G][16]
+  int L, d, f, E, k;
+  int row_bytes, rps, stages, stage_bytes;
+};
+
+__device__ __forceinline__ unsigned long long to_fix(float v) {
+  return (unsigned long long)__float2ll_rn(v * kFix);
+}
+__device__ __forceinline__ float from_fix(unsigned long long a) {
+  return __ll2float_rn((long long)a) * kFixInv;
+}
+
+template <typename W, int NV>
+__global__ void __launch_bounds__(kMaxConsWarps * 32 + 32, 1)
+    decode_stack2_kernel(const __grid_constant__ Stack2Args a) {
+  constexpr int VEC = Elem<W>::kVec;
+  constexpr int S = NV * VEC;
+  extern __shared__ __align__(128) uint8_t smem[];
+  Ring R;
+  R.buf = smem;
+  R.full = reinterpret_cast<uint64_t*>(smem + (size_t)a.stages * a.stage_bytes);
+  R.empty = R.full + a.stages;
+  R.rps = a.rps;
+  R.stages = a.stages;
+  R.stage_bytes = a.stage_bytes;
+  R.row_bytes = a.row_bytes;
+  float* stg = reinterpret_cast<float*>(smem + (size_t)a.stages * a.stage_bytes + 2 * a.stages * 8);
+  __shared__ uint64_t route_bar;
+  __shared__ float red[kMaxConsWarps * 32];
+  __shared__ float h_s[kBatch];
+  __shared__ float logits[kMaxExperts];
+  __shared__ int32_t s_ids[kMaxSlots];
+  __shared__ float s_g[kMaxSlots];
+  __shared__ int s_slot[kMaxSlots];
+  __shared__ float s_gate[kMaxSlots];
+  __shared__ int s_nloc;
+  __shared__ int16_t s_so[kMaxExperts];
+  __shared__ unsigned s_state[2];
+
+  const int ncons = blockDim.x - 32;
+  const int ncw = ncons >> 5;
+  const int tid = threadIdx.x, lane = tid & 31;
+  const int warp = warp_uniform(tid >> 5);
+  const int G = gridDim.x, c = blockIdx.x;
+  const int d = a.d, E = a.E, k = a.k;
+
+  if (tid == 0) {
+    for (int s = 0; s < a.stages; ++s) {
+      mbar_init(&R.full[s], 1);
+      mbar_init(&R.empty[s], ncw);
+    }
+    mbar_init(&route_bar, 1);
+    fence_mbar_init();
+  }
+  griddep_wait();
+  if (tid == 32) {
+    s_state[0] = __ldcg(&a.state[kStateBase]);
+    s_state[1] = __ldcg(&a.state[kStateBase + 1]);
+  }
+  __syncthreads();
+  const unsigned bar0 = s_state[0], rot = s_state[1];
+
+  if (warp == ncw) {
+    if (lane != 0) return;
+    const uint64_t pol = l2_evict_first_policy();
+    Cursor cur;
+    for (int l = 0; l < a.L; ++l) {
+      mbar_wait_sleep(&route_bar, (uint32_t)(l & 1));
+      if (a.trace) a.trace[((size_t)l * G + c) * 16 + 6] = clock64();
+      const long long T = (long long)s_nloc * a.f;
+      const long long g0 = (long long)c * T / G, g1 = (long long)(c + 1) * T / G;
+      if (g1 > g0)
+        produce_rows<W>(R, cur, reinterpret_cast<const W*>(a.layer_experts[l]), a.expert_stride,
+                        a.mat_stride, s_slot, a.f, d, g0, g1, pol);
+      if (a.trace) a.trace[((size_t)l * G + c) * 16 + 7] = clock64();
+    }
+    return;
+  }
+
+  auto commit_route = [&](int l) {
+    if (c == 0 && a.logits_out != nullptr && lane < E) a.logits_out[(size_t)l * E + lane] = logits[lane];
+    warp_topk_softmax(logits, E, k, s_ids, s_g);
+    if (lane != 0) return;
+    int n = 0;
+    for (int j = 0; j < k; ++j) {
+      const int slot = s_so[s_ids[j]];
+      if (slot >= 0) {
+        s_slot[n] = slot;
+        s_gate[n] = s_g[j];
+        ++n;
+      }
+      if (c == 0) {
+        a.ids_out[(size_t)l * k + j] = s_ids[j];
+        a.gates_out[(size_t)l * k + j] = s_g[j];
+      }
+    }
+    s_nloc = n;
+    mbar_arrive(&route_bar);
+  };
+  auto buf = [&](int l) { return (int)((rot + (unsigned)l) % 3u); };
+  auto col_of = [&](int q) { return (tid + (q / VEC) * ncons) * VEC + (q % VEC); };
+  unsigned long long* const ovf_words = a.zacc + kZMax;
+  float rv[2];
+  auto load_rv = [&](int lr) {
+#pragma unroll
+    for (int j = 0; j < 2; ++j) {
+      const int p = c + j * G;
+      rv[j] = (lr < a.L && p < S * E) ? __ldg(a.router + ((size_t)lr * E + p / S) * d + col_of(p % S)) : 0.f;
+    }
+  };
+  auto add_xpart = [&](int lr, int b, const float* xr) {
+    if (lr >= a.L) return;
+#pragma unroll
+    for (int j = 0; j < 2; ++j) {
+      const int p = c + j * G;
+      if (p < S * E) {
+        const int q = p % S;
+        float xv = 0.f;
+#pragma unroll
+        for (int i = 0; i < S; ++i) xv = (i == q) ? xr[i] : xv;
+        const float v = warp_sum(rv[j] * xv);
+        if (lane == 0) {
+          atomicAdd(&a.zacc[(size_t)b * kZStride + p / S], to_fix(v));
+          if (!(fabsf(v) < kFixMax)) atomicAdd(&ovf_words[(size_t)b * kZStride], 1ull);
+        }
+      }
+    }
+  };
+
+  for (int e = tid; e < E; e += ncons) s_so[e] = a.slot_of[e];
+  for (int e = warp; e < E; e += ncw) {
+    const float* re = a.router + (size_t)e * d;
+    float s = 0.f;
+    for (int i = lane; i < d; i += 32) s = fmaf(re[i], __ldcg(&a.x[i]), s);
+    s = warp_sum(s);
+    if (lane == 0) logits[e] = s;
+  }
+  named_bar_sync(2, ncons);
+  if (warp == 0) commit_route(0);
+  float xr[S];
+  load_x<W, NV>(a.x, xr, tid, ncons);
+  load_rv(1);
+  add_xpart(1, buf(0), xr);
+  load_rv(2);
+  named_bar_sync(2, ncons);
+
+  float zreg[kZMax];
+#pragma unroll
+  for (int e = 0; e < kZMax; ++e) zreg[e] = 0.f;
+  Cursor cur;
+  for (int l = 0; l < a.L; ++l) {
+    const bool more = l + 1 < a.L;
+    const int b = buf(l);
+    unsigned long long* tr = a.trace ? a.trace + ((size_t)l * G + c) * 16 : nullptr;
+    if (tr && tid == 0) tr[0] = clock64();
+    if (more)
+      for (int e = tid; e < E; e += ncons) s_so[e] = a.slot_of[(size_t)(l + 1) * E + e];
+    float yacc[S];
+#pragma unroll
+    for (int i = 0; i < S; ++i) yacc[i] = 0.f;
+    const long long T = (long long)s_nloc * a.f;
+    const long long g0 = (long long)c * T / G, g1 = (long long)(c + 1) * T / G;
+    consume_rows<W, NV>(R, cur, xr, yacc, s_gate, a.f, g0, g1, red, h_s, tid, ncons, 1,
+                        tr ? tr + 1 : nullptr, more ? a.rw[l] : nullptr, s_slot, E, zreg);
+    if (tr && tid == 0) tr[2] = clock64();
+    store_y<W, NV>(stg, yacc, tid, ncons);
+    named_bar_sync(2, ncons);
+    bool ov = false;
+    unsigned long long* accb = a.acc + (size_t)b * d;
+    for (int i = tid; i < d; i += ncons) {
+      const float v = stg[i];
+      ov |= !(fabsf(v) < kFixMax);
+      atomicAdd(&accb[i], to_fix(v));
+    }
+    if (more && warp == 0) {
+      float zv = 0.f;
+#pragma unroll
+      for (int e = 0; e < kZMax; ++e) {
+        zv = (lane == e) ? zreg[e] : zv;
+        zreg[e] = 0.f;
+      }
+      if (lane < E) {
+        atomicAdd(&a.zacc[(size_t)b * kZStride + lane], to_fix(zv));
+        ov |= !(fabsf(zv) < kFixMax);
+      }
+    }
+    if (__any_sync(MOE_FULL_MASK, ov) && lane == 0) atomicAdd(&ovf_words[(size_t)b * kZStride], 1ull);
+    if (tr && tid == 0) tr[11] = clock64();
+    grid_sync(a.state, bar0 + (unsigned)((l + 1) * G), ncons);
+    if (tr && tid == 0) tr[3] = clock64();
+    unsigned long long av[S];
+#pragma unroll
+    for (int m = 0; m < NV; ++m) {
+      const ulonglong2* ap = reinterpret_cast<const ulonglong2*>(accb + (size_t)(tid + m * ncons) * VEC);
+#pragma unroll
+      for (int v = 0; v < VEC / 2; ++v) {
+        const ulonglong2 t = __ldcg(ap + v);
+        av[m * VEC + 2 * v] = t.x;
+        av[m * VEC + 2 * v + 1] = t.y;
+      }
+    }
+    const bool bad = __ldcg(&ovf_words[(size_t)b * kZStride]) != 0ull;
+    if (more && warp == 0) {
+      const unsigned long long zl = lane < E ? __ldcg(&a.zacc[(size_t)b * kZStride + lane]) : 0ull;
+      if (lane < E) logits[lane] = bad ? 0.f : from_fix(zl);
+      __syncwarp();
+      commit_route(l + 1);
+      if (tr && lane == 0) tr[10] = clock64();
+    }
+#pragma unroll
+    for (int i = 0; i < S; ++i) xr[i] = bad ? __int_as_float(0x7fffffff) : xr[i] + from_fix(av[i]);
+    if (tr && tid == 0) tr[4] = clock64();
+    {
+      const int b2 = buf(l + 2);
+      const int c0 = (int)((long long)c * d / G), c1 = (int)((long long)(c + 1) * d / G);
+      for (int i = c0 + tid; i < c1; i += ncons) a.acc[(size_t)b2 * d + i] = 0ull;
+      if (c == 0 && tid < kZStride) a.zacc[(size_t)b2 * kZStride + tid] = 0ull;
+    }
+    if (l + 2 < a.L) {
+      add_xpart(l + 2, buf(l + 1), xr);
+      load_rv(l + 3);
+    }
+    if (!more && c == 0) store_y<W, NV>(a.x, xr, tid, ncons);
+    named_bar_sync(2, ncons);  // routing of l+1 visible to every consumer warp
+    if (tr && tid == 0) tr[5] = clock64();
+  }
+  if (c == 0 && tid == 0) {
+    a.state[kStateBase] = bar0 + (unsigned)(a.L * G);
+    a.state[kStateBase + 1] = (rot + (unsigned)a.L) % 3u;
+  }
+}
+
+// ---------------------------------------------------------------------------
 int reduce_blocks(const Dims& dm) { return (dm.d + 31) / 32; }
 
 DecodePlan plan_decode(const Dims& dm, int sm_count) {
@@ -902,8 +1175,7 @@ DecodePlan plan_decode(const Dims& dm, int sm_count) {
   p.grid = sm_count;
   // testing hook: fewer CTAs, so that several linked ranks' persistent kernels
   // fit one GPU side by side (tests/test_gpu_ep_peers.py)
-  if (const char* g = getenv("MOE_B200_STACK_GRID"))
-    if (atoi(g) > 0) p.grid = std::min(sm_count, atoi(g));
+  if (debug_options().stack_grid > 0) p.grid = std::min(sm_count, debug_options().stack_grid);
   p.ok = true;
   return p;
 }
@@ -949,8 +1221,7 @@ static cudaError_t launch_stack_t(const DecodePlan& p, const StackArgs& a, cudaS
   attr[0].id = cudaLaunchAttributeCooperative;
   attr[0].val.cooperative = 1;
   cfg.attrs = attr;
-  static const bool noncoop = getenv("MOE_B200_NONCOOP") != nullptr;  // diagnostics
-  cfg.numAttrs = noncoop ? 0 : 1;
+  cfg.numAttrs = debug_options().noncoop ? 0 : 1;  // diagnostics
   return cudaLaunchKernelEx(&cfg, kern, a);
 }
 
@@ -1015,6 +1286,67 @@ cudaError_t launch_decode_stack(const DecodePlan& p, const StackDesc& sd, const 
     MOE_DISPATCH_NV(launch_stack_t, __nv_bfloat16, p, a, s)
   }
   MOE_DISPATCH_NV(launch_stack_t, float, p, a, s)
+}
+
+int stack2_smem(const DecodePlan& p, const Dims& dm) { return p.smem + dm.d * 4; }
+
+bool stack2_supported(const DecodePlan& p, const Dims& dm) {
+  if (!p.ok || dm.E > kZMax) return false;
+  const int vec = dm.dtype == MOE_DTYPE_BF16 ? 8 : 4;
+  return p.nv * vec * dm.E <= 2 * p.grid && stack2_smem(p, dm) <= 227 * 1024;
+}
+
+size_t stack2_acc_bytes(const Dims& dm) { return 3 * (size_t)dm.d * 8 + 3 * kZStride * 8 + 256; }
+
+template <typename W, int NV>
+static cudaError_t launch_stack2_t(const DecodePlan& p, const Dims& dm, const Stack2Args& a,
+                                   cudaStream_t s) {
+  auto kern = decode_stack2_kernel<W, NV>;
+  const int smem = stack2_smem(p, dm);
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  if (e != cudaSuccess) return e;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(p.grid);
+  cfg.blockDim = dim3(p.ncons + 32);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeCooperative;
+  attr[0].val.cooperative = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = debug_options().noncoop ? 0 : 1;
+  return cudaLaunchKernelEx(&cfg, kern, a);
+}
+
+cudaError_t launch_decode_stack2(const DecodePlan& p, const StackDesc& sd, const Dims& dm, float* x,
+                                 void* accbuf, int32_t* ids_out, float* gates_out,
+                                 float* logits_out, cudaStream_t s) {
+  if (!stack2_supported(p, dm) || sd.rw == nullptr) return cudaErrorInvalidValue;
+  Stack2Args a;
+  a.layer_experts = sd.layer_experts;
+  a.slot_of = sd.slot_of;
+  a.expert_stride = sd.expert_stride;
+  a.mat_stride = sd.mat_stride;
+  a.router = sd.router;
+  a.rw = sd.rw;
+  a.x = x;
+  a.acc = static_cast<unsigned long long*>(accbuf);
+  a.zacc = a.acc + 3 * (size_t)dm.d;
+  a.state = reinterpret_cast<unsigned*>(a.zacc + 3 * kZStride);
+  a.ids_out = ids_out;
+  a.gates_out = gates_out;
+  a.logits_out = logits_out;
+  a.trace = sd.trace;
+  a.L = sd.L;
+  a.d = dm.d;
+  a.f = dm.f;
+  a.E = dm.E;
+  a.k = dm.k;
+  fill_ring_args(p, dm, a.row_bytes, a.rps, a.stages, a.stage_bytes);
+  if (dm.dtype == MOE_DTYPE_BF16) {
+    MOE_DISPATCH_NV(launch_stack2_t, __nv_bfloat16, p, dm, a, s)
+  }
+  MOE_DISPATCH_NV(launch_stack2_t, float, p, dm, a, s)
 }
 
 cudaError_t launch_reduce_residual(const float* ypart, int nparts, const float* x, float* x_out,

@@ -22,8 +22,7 @@ static cudaLaunchConfig_t make_cfg(dim3 grid, dim3 block, cudaStream_t s, bool p
   attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
   attr[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
-  static const bool no_pdl = getenv("MOE_B200_NO_PDL") != nullptr;  // diagnostics
-  cfg.numAttrs = (pdl && !no_pdl) ? 1 : 0;
+  cfg.numAttrs = (pdl && !debug_options().no_pdl) ? 1 : 0;
   return cfg;
 }
 
@@ -459,7 +458,7 @@ cudaError_t launch_combine(const float* x, const float* y, const float* gates, i
                            const int32_t* ids, const int32_t* split_of) {
   if (n_tok <= 0) return cudaSuccess;
   cudaLaunchAttribute attr[1];
-  const bool k2_off = getenv("MOE_B200_COMBINE4") != nullptr;  // A/B: the looped kernel
+  const bool k2_off = debug_options().combine4 != 0;  // A/B: the looped kernel
   if (dm.d % 4 == 0 && dm.k == 2 && nsplit <= 2 && !k2_off) {
     cudaLaunchConfig_t cfg = make_cfg(dim3(n_tok), dim3(256), s, pdl, attr);
     const long long sstride = (long long)n_tok * dm.k * dm.d;

@@ -9,6 +9,28 @@ namespace moe {
 
 constexpr int kMaxExperts = 256;
 
+// Debug / A-B switches (moe_debug_set_option, include/moe_b200.h).  The
+// product never reads the environment: its code path changes only through
+// this explicit API, which tests and tools/ call.  Values are read when a
+// moe_weights is created (stack, rw, prefill, prefill_splits) or at launch.
+struct DebugOptions {
+  int stack = 1;           // batch-1 decode: persistent stack kernel (0: per-layer kernels)
+  int stack_kernel = 2;    // 2: fixed-point single-barrier kernel, 1: two-barrier kernel
+  int rw = 1;              // precomputed R_{l+1} W2 router projections
+  int prefill = 1;         // tcgen05 grouped prefill (0: generic kernels)
+  int prefill_splits = 2;  // max down K splits of the grouped kernel (0: two-kernel path)
+  int stack_grid = 0;      // >0: persistent-kernel grid (several linked ranks on one GPU)
+  int virtual_stack = 0;   // a virtual rank runs its shard through the persistent kernel
+  int noncoop = 0;         // launch the stack kernel without the cooperative attribute
+  int force_ep = 0;        // world 1 + NCCL communicator: the EP code path on one GPU
+  int no_pdl = 0;          // no programmatic dependent launch anywhere
+  int combine4 = 0;        // looped combine instead of combine_k2_kernel
+  int pf_debug = 0, pf_evict = 0, pf_lag = kMaxExperts, pf_late8 = 3, pf_slo = 0, pf_persist = 1;
+};
+DebugOptions& debug_options();
+// per-tile timeline file of the grouped prefill kernel (tools/trace_prefill.py); empty = off
+const char* debug_trace_path();
+
 // Expert weights of one layer on this rank: slot s (local expert) holds
 // [W1 f x d][W3 f x d][W2T f x d] contiguously (W2T = w_out transposed so the
 // decode kernel streams whole d-rows for every ffn index r).
@@ -75,6 +97,16 @@ cudaError_t launch_decode_stack(const DecodePlan& p, const StackDesc& sd, const 
                                 float* x, float* xbuf, float* ypart, float* rpart,
                                 int32_t* ids_out, float* gates_out, unsigned* gbar,
                                 cudaStream_t s, const PeerArgs* pa = nullptr);
+// The same forward with ONE grid barrier per layer: partials summed in 64-bit
+// fixed point with L2 integer atomics (order-independent, bit-reproducible).
+// Single GPU only (no peers), E <= 8, router projections (sd.rw) required.
+// accbuf: stack2_acc_bytes(dm) bytes, zeroed once at allocation (the kernel
+// leaves it reusable: counters and buffer rotation carry across launches).
+bool stack2_supported(const DecodePlan& p, const Dims& dm);
+size_t stack2_acc_bytes(const Dims& dm);
+cudaError_t launch_decode_stack2(const DecodePlan& p, const StackDesc& sd, const Dims& dm, float* x,
+                                 void* accbuf, int32_t* ids_out, float* gates_out,
+                                 float* logits_out, cudaStream_t s);
 // x_out = x + sum_p ypart[p]; optionally the next layer's router + top-k
 // (deterministic fixed-order partial sums, last-block-done).
 cudaError_t launch_reduce_residual(const float* ypart, int nparts, const float* x, float* x_out,

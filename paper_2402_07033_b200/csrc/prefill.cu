@@ -969,7 +969,7 @@ cudaError_t launch_prefill_experts(const LayerWeights& lw, int n_local, const Di
   const int chunks = (n_tok + GP_MAXN - 1) / GP_MAXN;
   // PDL chain permute -> gather -> grouped kernel: each launch overlaps the
   // previous kernel's tail and waits (griddep_wait) before touching its data
-  static const bool no_pdl = getenv("MOE_B200_NO_PDL") != nullptr;
+  const bool no_pdl = debug_options().no_pdl != 0;
   cudaLaunchAttribute pdl_attr[1];
   pdl_attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
   pdl_attr[0].val.programmaticStreamSerializationAllowed = 1;
@@ -1009,20 +1009,20 @@ cudaError_t launch_prefill_experts(const LayerWeights& lw, int n_local, const Di
     g.rows = rows;
     g.S = splits;
     g.max_chunks = chunks;
-    g.debug = getenv("MOE_B200_PF_DEBUG") ? atoi(getenv("MOE_B200_PF_DEBUG")) : 0;
+    g.debug = debug_options().pf_debug;
     g.sp = sp;
     // measured A/B (512 tokens): evict_first keeps H/Y in L2 (-33 MB DRAM,
     // combine 11.5 -> 9.6 us) but slows the weight stream by ~5 us: off
-    g.evict_first = getenv("MOE_B200_PF_EVICT") ? atoi(getenv("MOE_B200_PF_EVICT")) : 0;
+    g.evict_first = debug_options().pf_evict;
     // measured (tools/prof_prefill.py, Mixtral 512 tokens): interleaving
     // downs among ups is slower (lag 1/2/3: +33/+12/+24 us) than all ups
     // first, so the default lag puts every down after every up
-    g.lag = getenv("MOE_B200_PF_LAG") ? atoi(getenv("MOE_B200_PF_LAG")) : kMaxExperts;
-    g.late8 = getenv("MOE_B200_PF_LATE8") ? atoi(getenv("MOE_B200_PF_LATE8")) : 3;
-    g.s_lo = getenv("MOE_B200_PF_SLO") ? atoi(getenv("MOE_B200_PF_SLO")) : 0;
+    g.lag = debug_options().pf_lag;
+    g.late8 = debug_options().pf_late8;
+    g.s_lo = debug_options().pf_slo;
     g.trace = nullptr;
     g.trace_cap = 0;
-    const char* trace_path = getenv("MOE_B200_PF_TRACE");
+    const char* trace_path = debug_trace_path()[0] ? debug_trace_path() : nullptr;
     static unsigned long long* trace_buf = nullptr;
     if (trace_path) {
       g.trace_cap = 32;
@@ -1045,7 +1045,8 @@ cudaError_t launch_prefill_experts(const LayerWeights& lw, int n_local, const Di
     cudaLaunchAttribute kattr[2];
     int nk = 0;
     if (!(no_pdl || trace_path || t0)) kattr[nk++] = pdl_attr[0];
-    static int persist = getenv("MOE_B200_PF_PERSIST") ? atoi(getenv("MOE_B200_PF_PERSIST")) : 1;
+    static int persist_off = 0;  // set once persisting L2 proved unavailable
+    int persist = debug_options().pf_persist && !persist_off;
     if (persist) {
       // keep H (written by the up tiles, read back by the down tiles) and Y
       // (read by the combine; the caller places it right after H) in a
@@ -1079,6 +1080,7 @@ cudaError_t launch_prefill_experts(const LayerWeights& lw, int n_local, const Di
             // run without the window from now on
             (void)cudaGetLastError();
             persist = 0;
+            persist_off = 1;
             wbytes = 0;
           }
           limit_set = wbytes;

@@ -47,3 +47,22 @@ def orc():
     import oracle
     oracle.build(ref=False)
     return oracle.Oracle()
+
+
+@pytest.fixture
+def libopts():
+    """Set library debug options (moe_debug_set_option) for one test; the
+    previous values come back afterwards.  Usage: libopts(stack=0)."""
+    import paper_2402_07033_b200 as M
+
+    saved = {}
+
+    def set_(**kw):
+        for k, v in kw.items():
+            if k not in saved:
+                saved[k] = M.get_option(k)
+            M.set_option(k, v)
+
+    yield set_
+    for k, v in saved.items():
+        M.set_option(k, v)

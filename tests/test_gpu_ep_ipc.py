@@ -30,11 +30,12 @@ def _rank_main(rank, world, port, q, kernel, mode):
     import sys
 
     sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
-    if kernel == "layer":
-        os.environ["MOE_B200_STACK"] = "0"  # per-layer kernels + reduce_exchange
     import torch.distributed as dist
 
     import paper_2402_07033_b200 as M
+
+    if kernel == "layer":
+        M.set_option("stack", 0)  # per-layer kernels + reduce_exchange
 
     try:
         dist.init_process_group("gloo", init_method=f"tcp://127.0.0.1:{port}", rank=rank,

@@ -1,6 +1,6 @@
 """The expert-parallel code path WITH its NCCL exchange, on one GPU.
 
-With MOE_B200_FORCE_EP=1 a world-size-1 context still builds a (1-rank) NCCL
+With the debug option force_ep=1 a world-size-1 context still builds a (1-rank) NCCL
 communicator.  It then takes the EP path: local partials → reduce →
 ncclAllReduce (captured in the CUDA graph for batch-1 decode) → residual +
 next-layer router.  The outputs must match the single-GPU persistent stack
@@ -29,13 +29,13 @@ def gpu():
 
 
 @pytest.mark.parametrize("n_tok", [1, 64])
-def test_forced_ep_path_matches_single_gpu(gpu, monkeypatch, n_tok):
+def test_forced_ep_path_matches_single_gpu(gpu, libopts, n_tok):
     L = 4
     s = M.Shape(L, 8, 2, 1024, 2048, 2)
     ref_ctx = M.Ctx(0)
     ref = M.Weights(ref_ctx, s, M.DTYPE_BF16)
     ref.random(9)
-    monkeypatch.setenv("MOE_B200_FORCE_EP", "1")
+    libopts(force_ep=1)
     ctx = M.Ctx(0)
     ctx.init_ep(1, 0, M.Ctx.unique_id())
     w = M.Weights(ctx, s, M.DTYPE_BF16)

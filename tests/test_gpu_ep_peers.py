@@ -49,7 +49,7 @@ def gpu():
     (4, (3, 8, 2, 4096, 14336, 2), M.DTYPE_BF16),
     (2, (3, 8, 2, 512, 1792, 4), M.DTYPE_F32),
 ])
-def test_peer_combine_matches_unsharded(gpu, monkeypatch, kernel, mode, world, shape, dtype):
+def test_peer_combine_matches_unsharded(gpu, libopts, kernel, mode, world, shape, dtype):
     """mode ep: experts sharded by the popularity shard map; mode tp: every
     expert's ffn rows split over the ranks (tensor parallelism).  kernel
     layer: per-layer streaming kernel + reduce_exchange; kernel stack: the
@@ -76,10 +76,10 @@ def test_peer_combine_matches_unsharded(gpu, monkeypatch, kernel, mode, world, s
     ctxs = [M.Ctx(0) for _ in range(world)]
     M.Ctx.link_peers(ctxs, d)
     if kernel == "layer":
-        monkeypatch.setenv("MOE_B200_STACK", "0")
+        libopts(stack=0)
     # each rank's streaming kernel on SMs/world CTAs: W ranks' kernels (and the
     # exchange blocks spinning on each other's flags) must fit one GPU at once
-    monkeypatch.setenv("MOE_B200_STACK_GRID", os.environ.get("PEER_TEST_GRID", str(ctxs[0].sm_count // world)))
+    libopts(stack_grid=int(os.environ.get("PEER_TEST_GRID", str(ctxs[0].sm_count // world))))
     if mode == "ep":
         owner = _bench().shard_map(L, E, world)
         ws = [M.Weights(c, s, dtype, owner=owner) for c in ctxs]

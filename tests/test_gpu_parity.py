@@ -326,14 +326,14 @@ def test_errors_are_loud(ctx):
 
 @pytest.mark.parametrize("L,d,f,dt", [(4, 4096, 14336, M.DTYPE_BF16), (3, 512, 1792, M.DTYPE_F32),
                                       (2, 6144, 16384, M.DTYPE_BF16)])
-def test_persistent_stack_matches_per_layer_path(ctx, orc, L, d, f, dt, monkeypatch):
+def test_persistent_stack_matches_per_layer_path(ctx, orc, L, d, f, dt, libopts):
     """The one-launch persistent stack kernel against the per-layer 2-kernel
     path on identical weights: same routing, outputs within fp32 rounding."""
     s = M.Shape(L, 8, 2, d, f, 2 if dt == M.DTYPE_BF16 else 4)
     w_stack = M.Weights(ctx, s, dt)
-    monkeypatch.setenv("MOE_B200_STACK", "0")
+    libopts(stack=0)
     w_layer = M.Weights(ctx, s, dt)
-    monkeypatch.delenv("MOE_B200_STACK")
+    libopts(stack=1)
     assert w_stack.forward_launches(1) == 1 and w_layer.forward_launches(1) == 1 + 2 * L
     w_stack.random(11)
     w_layer.random(11)
@@ -356,13 +356,13 @@ def test_persistent_stack_matches_per_layer_path(ctx, orc, L, d, f, dt, monkeypa
     w_layer.close()
 
 
-def _prefill_case(ctx, orc, monkeypatch, L, d, f, n_tok, seed, sample):
+def _prefill_case(ctx, orc, libopts, L, d, f, n_tok, seed, sample):
     s = M.Shape(L, 8, 2, d, f, 2)
     w = M.Weights(ctx, s, M.DTYPE_BF16)
     assert w.expert_path(n_tok) == 3  # tcgen05 grouped GEMM
-    monkeypatch.setenv("MOE_B200_PREFILL", "0")
+    libopts(prefill=0)
     wg = M.Weights(ctx, s, M.DTYPE_BF16)
-    monkeypatch.delenv("MOE_B200_PREFILL")
+    libopts(prefill=1)
     assert wg.expert_path(n_tok) == 2
     w.random(seed)
     wg.random(seed)
@@ -401,29 +401,28 @@ def _prefill_case(ctx, orc, monkeypatch, L, d, f, n_tok, seed, sample):
     wg.close()
 
 
-def test_prefill_tcgen05_small_uneven(ctx, orc, monkeypatch):
+def test_prefill_tcgen05_small_uneven(ctx, orc, libopts):
     """d=256, f=512, 700 tokens: experts see >256 tokens (2 N-chunks), ragged
     tails, every token checked against the oracle."""
-    _prefill_case(ctx, orc, monkeypatch, 1, 256, 512, 700, 3, range(0, 700, 7))
+    _prefill_case(ctx, orc, libopts, 1, 256, 512, 700, 3, range(0, 700, 7))
 
 
-def test_prefill_tcgen05_mixtral_layer_512(ctx, orc, monkeypatch):
+def test_prefill_tcgen05_mixtral_layer_512(ctx, orc, libopts):
     """Config P: Mixtral-shaped layer, 512-token prefill on the tcgen05 path."""
-    _prefill_case(ctx, orc, monkeypatch, 1, 4096, 14336, 512, 5, [0, 1, 77, 200, 311, 511])
+    _prefill_case(ctx, orc, libopts, 1, 4096, 14336, 512, 5, [0, 1, 77, 200, 311, 511])
 
 
 @pytest.mark.parametrize("n_tok", [512, 700])
-def test_combine_k2_equals_looped_combine(ctx, monkeypatch, n_tok):
+def test_combine_k2_equals_looped_combine(ctx, libopts, n_tok):
     """The top-2 combine that issues all loads up front (combine_k2_kernel)
-    is bit-identical to the looped combine (MOE_B200_COMBINE4) on the
+    is bit-identical to the looped combine (debug option combine4) on the
     tcgen05 prefill path, K-split partials included."""
     w = M.Weights(ctx, M.Shape(1, 8, 2, 4096, 14336, 2), M.DTYPE_BF16)
     w.random(3)
     x = torch.randn(n_tok, 4096, device="cuda")
     outs = []
-    for env in (None, "1"):
-        if env:
-            monkeypatch.setenv("MOE_B200_COMBINE4", env)
+    for env in (0, 1):
+        libopts(combine4=env)
         o = torch.empty_like(x)
         ids = torch.zeros((n_tok, 2), dtype=torch.int32, device="cuda")
         g = torch.zeros((n_tok, 2), device="cuda")
@@ -537,7 +536,7 @@ def test_routing_histogram_and_shard_map(ctx):
     w.close()
 
 
-def test_fused_sparsity_counters_match_reference_sink(ctx, monkeypatch):
+def test_fused_sparsity_counters_match_reference_sink(ctx, libopts):
     """Activation-sparsity counters fused into the up-projection epilogues (f2)
     against the reference's sparsity_histogram of its ActivationSink values."""
     ref = O.Reference() if O.reference_available() else None
@@ -573,9 +572,9 @@ def test_fused_sparsity_counters_match_reference_sink(ctx, monkeypatch):
     # tcgen05 grouped-GEMM epilogue vs generic kernel at the Mixtral shape
     s = M.Shape(1, 8, 2, 4096, 14336, 2)
     wt = M.Weights(ctx, s, M.DTYPE_BF16)
-    monkeypatch.setenv("MOE_B200_PREFILL", "0")
+    libopts(prefill=0)
     wgn = M.Weights(ctx, s, M.DTYPE_BF16)
-    monkeypatch.delenv("MOE_B200_PREFILL")
+    libopts(prefill=1)
     assert wt.expert_path(128) == 3 and wgn.expert_path(128) == 2
     xs = torch.randn(128, 4096, device="cuda", generator=torch.Generator(device="cuda").manual_seed(0))
     res = []

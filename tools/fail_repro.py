@@ -5,9 +5,9 @@ import paper_2402_07033_b200 as M
 n, d, f = 8192, 4096, 14336
 ctx = M.Ctx(0)
 w = M.Weights(ctx, M.Shape(1, 8, 2, d, f, 2), M.DTYPE_BF16)
-os.environ["MOE_B200_PREFILL"] = "0"
+M.set_option("prefill", 0)
 wg = M.Weights(ctx, M.Shape(1, 8, 2, d, f, 2), M.DTYPE_BF16)
-del os.environ["MOE_B200_PREFILL"]
+M.set_option("prefill", 1)
 w.random(5); wg.random(5)
 keep = os.environ.get("KEEP") == "1"
 hold = []

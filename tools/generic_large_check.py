@@ -23,9 +23,9 @@ def main(n, iters):
     d, f = 4096, 14336
     ctx = M.Ctx(0)
     w = M.Weights(ctx, M.Shape(1, 8, 2, d, f, 2), M.DTYPE_BF16)
-    os.environ["MOE_B200_PREFILL"] = "0"
+    M.set_option("prefill", 0)
     wg = M.Weights(ctx, M.Shape(1, 8, 2, d, f, 2), M.DTYPE_BF16)
-    del os.environ["MOE_B200_PREFILL"]
+    M.set_option("prefill", 1)
     w.random(5)
     wg.random(5)
     for it in range(iters):

@@ -6,7 +6,7 @@ import paper_2402_07033_b200 as M
 spec = importlib.util.spec_from_file_location("bench", "/root/repo/bench.py"); b = importlib.util.module_from_spec(spec); spec.loader.exec_module(b)
 world = int(os.environ.get("W", "4")); mode = os.environ.get("MODE", "ep")
 L, E, k, d, f = 3, 8, 2, 4096, 14336
-os.environ["MOE_B200_STACK_GRID"] = str(148 // world)
+M.set_option("stack_grid", 148 // world)
 ctxs = [M.Ctx(0) for _ in range(world)]
 M.Ctx.link_peers(ctxs, d)
 owner = b.shard_map(L, E, world)

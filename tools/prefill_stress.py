@@ -25,9 +25,9 @@ def main():
     ctx = M.Ctx(0)
     s = M.Shape(1, 8, 2, d, f, 2)
     w = M.Weights(ctx, s, M.DTYPE_BF16)
-    os.environ["MOE_B200_PREFILL"] = "0"
+    M.set_option("prefill", 0)
     wg = M.Weights(ctx, s, M.DTYPE_BF16)
-    del os.environ["MOE_B200_PREFILL"]
+    M.set_option("prefill", 1)
     w.random(5)
     wg.random(5)
     worst, bad = 0.0, 0

@@ -4,8 +4,9 @@ CUPTI activity records, warm L2 state of a real loop, no replay).
     python tools/prof_prefill.py [--tokens 512] [--iters 50]
 
 Prints, per kernel name, launches per layer and mean us, plus the layer
-time from CUDA events.  Env knobs of the library (MOE_B200_PREFILL_SPLITS,
-MOE_B200_PF_DEBUG, ...) apply.
+time from CUDA events.  MOE_B200_<OPTION> environment variables set the
+library's debug options (tools/_opts.py: MOE_B200_PREFILL_SPLITS,
+MOE_B200_PF_DEBUG, ...).
 """
 import argparse
 import collections
@@ -27,7 +28,9 @@ def main():
     from torch.profiler import ProfilerActivity, profile
 
     import paper_2402_07033_b200 as M
+    from _opts import from_env
 
+    from_env()
     n, d, f, E, k = args.tokens, args.d, args.f, 8, 2
     ctx = M.Ctx(0)
     w = M.Weights(ctx, M.Shape(1, E, k, d, f, 2), M.DTYPE_BF16)

@@ -26,14 +26,15 @@ def main():
     ap.add_argument("--rank", type=int, default=0)
     ap.add_argument("--steps", type=int, default=50)
     ap.add_argument("--stack", action="store_true",
-                    help="persistent one-launch kernel (MOE_B200_VIRTUAL_STACK) instead of per-layer kernels")
+                    help="persistent one-launch kernel (debug option virtual_stack) instead of per-layer kernels")
     args = ap.parse_args()
-    if args.stack:
-        os.environ["MOE_B200_VIRTUAL_STACK"] = "1"
     import torch
 
     import bench
     import paper_2402_07033_b200 as M
+
+    if args.stack:
+        M.set_option("virtual_stack", 1)
 
     L, E, k, d, f, dt = bench.CONFIGS[args.config]
     ctx = M.Ctx(0)

@@ -2,7 +2,7 @@
 
     python tools/trace_prefill.py [--tokens 512] [--reps 3]
 
-Sets MOE_B200_PF_TRACE (the library dumps [CTA][tile][4] globaltimer stamps
+Sets the library's trace path (moe_debug_set_trace_path; the library dumps [CTA][tile][4] globaltimer stamps
 per launch: tile|N<<32, producer got the tile, MMA issued its last MMA,
 epilogue done) and summarises: per tile kind the producer-to-producer
 interval (the SM's streaming time per tile), the epilogue lag behind the
@@ -43,11 +43,11 @@ def main():
     for i in range(2):
         w.layer_forward(0, xs[i], xo, ids, g, stream=sp)
     torch.cuda.synchronize()
-    os.environ["MOE_B200_PF_TRACE"] = path
+    M.set_trace_path(path)
     for i in range(args.reps):
         w.layer_forward(0, xs[2 + i], xo, ids, g, stream=sp)
     torch.cuda.synchronize()
-    del os.environ["MOE_B200_PF_TRACE"]
+    M.set_trace_path(None)
     raw = open(path, "rb").read()
     off = 0
     n_ft, n_dt = f // 128, d // 128

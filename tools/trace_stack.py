@@ -46,7 +46,7 @@ def main():
     L = args.layers
     w = M.Weights(ctx, M.Shape(L, 8, 2, args.d, args.f, 2), M.DTYPE_BF16)
     w.random(0)
-    x = torch.randn(1, args.d, device="cuda")
+    x = 0.1 * torch.randn(1, args.d, device="cuda")
     ids = torch.zeros((L, 1, 2), dtype=torch.int32, device="cuda")
     g = torch.zeros((L, 1, 2), dtype=torch.float32, device="cuda")
     for _ in range(2):
