@@ -1,24 +1,38 @@
 """bench.py — batch-1 MoE decode throughput on B200 (BASELINE.json metric).
 
-Workload (BASELINE.json configs[3]): a 32-layer Mixtral-8x7B-shaped MoE stack
+Workload (BASELINE configs[3]): a 32-layer Mixtral-8x7B-shaped MoE stack
 (d=4096, ffn=14336, 8 experts, top-2), bf16 weights (device Philox init,
 random), fp32 residual stream, batch 1.  One step = one token through all
 32 MoE layers (router -> 2 experts -> combine -> residual, per layer).
-At N>1 (torchrun) the experts of every layer are sharded over the ranks by
-the popularity placement (expert parallelism; --shard tp: tensor parallelism)
-and every layer's partial deltas are combined over NVLink peer memory inside
-the persistent kernel (--nccl-combine: ncclAllReduce instead); the metric is
-the single token stream's tok/s ("strong" scaling: fixed work).
+
+Tokens are 0.1 * N(0,1): the reference's model_forward has no normalisation
+between layers, so with N(0,1) tokens the random-init 32-layer stack's
+residual stream grows doubly exponentially and overflows to inf/NaN by
+layer ~8 (each layer adds a delta ~ |x|^2).  At 0.1 the stack stays finite
+(|x| rms 0.10 -> 0.15 over 32 layers) and its routing is meaningful
+(`routing` reports the smallest 2nd-3rd logit margin over the timed tokens).
+
+The default (N=1) line also carries BASELINE configs[1] (one Mixtral layer,
+batch-1 decode, per-layer kernels) and configs[2] (one layer, 512-token
+prefill on the tcgen05 grouped GEMM) under `extra_configs`, each with its own
+clocks, roofline and e2e, measured on layer 0 of the same weights.
+
+At N>1 the experts of every layer are sharded over the ranks (--shard ep:
+popularity shard map = expert parallelism; tp: tensor parallelism) and every
+layer's partial deltas are combined over NVLink peer memory inside the
+persistent kernel; `--gpus N` without torchrun re-launches itself under
+torch.distributed.run with N ranks.  The metric is the single token stream's
+tok/s ("strong" scaling: fixed work).
 
 Reported:
   value     tok/s with the token already in HBM (CUDA events, max over ranks)
-  e2e       tok/s through moe_forward_host (pinned host buffers, H2D of the
-            token + D2H of the output/routing inside the timed region)
-  roofline  the streaming expert kernel alone, timed live with CUDA events
-            over the same layers: algorithmic bytes (2 experts x 3 x d x f x 2 B
-            = 704,643,072 B per launch) / average launch time vs MEASURED_PEAKS
+  e2e       tok/s through moe_forward_host (fp64 host token, H2D, forward,
+            D2H of output + routing inside the timed region)
+  roofline  the dominant kernel (the persistent stack kernel, one launch per
+            token), timed live with CUDA events on its stream: algorithmic
+            bytes per launch / launch time vs MEASURED_PEAKS
   cpu_baseline  the reference's own model_forward (oracle/_ref, compiled from
-            the reference sources) on a bounded sample on the host cores.
+            the reference sources) on a bounded sample, 1 host core.
 
     python bench.py [--gpus N --steps K --warmup W] [--impl reference]
 """
@@ -27,6 +41,7 @@ from __future__ import annotations
 import argparse
 import json
 import os
+import socket
 import statistics
 import subprocess
 import sys
@@ -52,8 +67,21 @@ WORKLOAD_NAME = {
     "tiny": "tiny MoE layer d=512 f=1792 fp32 decode, batch 1 (BASELINE configs[0])",
 }
 METRIC = "Mixtral-8x7B MoE decode tok/s (batch 1)"
+LAYER_METRIC = "Mixtral-8x7B MoE layer decode tok/s (batch 1, 1 layer)"
 PREFILL_METRIC = "Mixtral-8x7B MoE layer prefill tok/s (512 tokens, 1 layer)"
 PREFILL_WORKLOAD = "Mixtral-8x7B-shaped MoE layer prefill, 512 tokens (BASELINE configs[2])"
+# token scale of the multi-layer stacks (see the module docstring)
+STACK_TOKEN_SCALE = 0.1
+
+
+def token_pool(seed: int, n: int, d: int, layers: int) -> np.ndarray:
+    """The bench's synthetic tokens: N(0,1) (scaled by STACK_TOKEN_SCALE for
+    multi-layer stacks), float32, from RandomState(seed + 1)."""
+    rs = np.random.RandomState(seed + 1)
+    x = rs.randn(n, d)
+    if layers > 1:
+        x *= STACK_TOKEN_SCALE
+    return x.astype(np.float32)
 
 
 def env_int(name, default):
@@ -67,8 +95,8 @@ def load_peaks():
     p = os.path.join(ROOT, "MEASURED_PEAKS.json")
     if os.path.exists(p):
         j = json.load(open(p))
-        return float(j["hbm_gbs"]), "measured (MEASURED_PEAKS.json)"
-    return 6650.0, "fallback (B200_PROFILING.md)"
+        return j, "measured (MEASURED_PEAKS.json)"
+    return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0}, "fallback (B200_PROFILING.md)"
 
 
 class ClockSampler:
@@ -86,9 +114,10 @@ class ClockSampler:
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={q}", "--format=csv,noheader,nounits",
-                 "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+                 "-lms", "50"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self.thread = threading.Thread(target=self._read, daemon=True)
             self.thread.start()
+            time.sleep(0.15)  # the first sample lands before the timed region
         except (FileNotFoundError, OSError):
             self.proc = None
         return self
@@ -101,6 +130,7 @@ class ClockSampler:
 
     def __exit__(self, *a):
         if self.proc:
+            time.sleep(0.06)
             self.proc.terminate()
             try:
                 self.proc.wait(timeout=5)
@@ -118,7 +148,32 @@ class ClockSampler:
                 "reasons": reasons, "samples": len(self.samples)}
 
 
-def dist_setup(n_gpus):
+# ---------------------------------------------------------------------------
+# multi-GPU plumbing
+def free_port() -> int:
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def relaunch_under_torchrun(n: int) -> None:
+    """`--gpus N` without torchrun: re-run this command with N ranks (one per
+    GPU) under torch.distributed.run, and exit with its status."""
+    same_gpu = os.environ.get("MOE_B200_BENCH_SAME_GPU") == "1"
+    if not same_gpu:
+        import torch
+
+        vis = torch.cuda.device_count()
+        if vis < n:
+            print(json.dumps({"metric": METRIC, "error": f"--gpus {n} needs {n} visible GPUs, found {vis}",
+                              "n_gpus": n}), flush=True)
+            sys.exit(2)
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr=127.0.0.1", f"--master-port={free_port()}", os.path.abspath(__file__)] + sys.argv[1:]
+    sys.exit(subprocess.call(cmd))
+
+
+def dist_setup():
     world = env_int("WORLD_SIZE", 1)
     rank = env_int("RANK", 0)
     local = env_int("LOCAL_RANK", 0)
@@ -145,6 +200,16 @@ def max_over_ranks(v, world):
     t = torch.tensor([v], dtype=torch.float64)
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
     return float(t.item())
+
+
+def gather_floats(v, world):
+    if world <= 1:
+        return [v]
+    import torch.distributed as dist
+
+    out = [None] * world
+    dist.all_gather_object(out, v)
+    return out
 
 
 def shard_map(L, E, world, rank_tokens=None):
@@ -180,12 +245,37 @@ def replica_map(owner, world, rank_tokens=None, hot=1):
 
 
 # ---------------------------------------------------------------------------
+def routing_margins(w, pool, idx, L, E, k, stream_ptr, device):
+    """Router logits of every timed token through the bench's own kernel
+    (moe_forward_logits: the persistent stack kernel writes the fp32 logits
+    its top-k ranked) -> the smallest 2nd-3rd margin / max|logit|."""
+    import torch
+
+    idx = list(idx)
+    x = torch.empty((1, pool.shape[1]), dtype=torch.float32, device=device)
+    ids = torch.zeros((L, 1, k), dtype=torch.int32, device=device)
+    g = torch.zeros((L, 1, k), dtype=torch.float32, device=device)
+    lg = torch.zeros((len(idx), L, E), dtype=torch.float32, device=device)
+    stream = torch.cuda.ExternalStream(stream_ptr, device=device)
+    for j, i in enumerate(idx):
+        with torch.cuda.stream(stream):
+            x.copy_(pool[i:i + 1])
+        w.forward_logits(x, ids, g, lg[j], stream=stream_ptr)
+    torch.cuda.synchronize()
+    a = lg.cpu().numpy().astype(np.float64)
+    srt = -np.sort(-a, axis=2)
+    margin = (srt[:, :, k - 1] - srt[:, :, k]) / np.maximum(np.abs(a).max(axis=2), 1e-30)
+    return {"margin_min": float(margin.min()), "below_1e-5": int((margin < 1e-5).sum()),
+            "tokens": len(idx), "layers": L, "finite": bool(np.isfinite(a).all()),
+            "source": "moe_forward_logits: the fp32 logits the persistent kernel ranked, every timed token x layer"}
+
+
 def run_ours(args):
     import torch
 
     import paper_2402_07033_b200 as M
 
-    world, rank, local = dist_setup(args.gpus)
+    world, rank, local = dist_setup()
     L, E, k, d, f, dt = CONFIGS[args.config]
     if args.layers:  # a reduced stack (e.g. x22b on one GPU: 56 layers need 270 GB)
         L = args.layers
@@ -193,6 +283,7 @@ def run_ours(args):
     esz = 2 if dt == "bf16" else 4
     if os.environ.get("MOE_B200_BENCH_SAME_GPU") == "1":
         local = 0  # testing only: every rank on GPU 0 (time-sliced; numbers meaningless)
+    device = f"cuda:{local}"
     torch.cuda.set_device(local)
     ctx = M.Ctx(local)
     if world > 1:
@@ -217,15 +308,15 @@ def run_ours(args):
     w.random(args.seed)
     w.reserve(1)  # all scratch now: nothing allocates (or syncs) inside the timed loop
     stream_ptr = ctx.stream
-    stream = torch.cuda.ExternalStream(stream_ptr, device=f"cuda:{local}")
+    stream = torch.cuda.ExternalStream(stream_ptr, device=device)
 
-    # token pool resident in HBM (synthetic N(0,1), identical on every rank)
+    # token pool resident in HBM (synthetic, identical on every rank)
     n_steps = args.warmup + args.steps
-    rs = np.random.RandomState(args.seed + 1)
-    pool = torch.tensor(rs.randn(n_steps, d).astype(np.float32), device=f"cuda:{local}")
-    x = torch.empty((1, d), dtype=torch.float32, device=f"cuda:{local}")
-    ids = torch.zeros((L, 1, k), dtype=torch.int32, device=f"cuda:{local}")
-    gates = torch.zeros((L, 1, k), dtype=torch.float32, device=f"cuda:{local}")
+    pool_h = token_pool(args.seed, n_steps, d, L)
+    pool = torch.tensor(pool_h, device=device)
+    x = torch.empty((1, d), dtype=torch.float32, device=device)
+    ids = torch.zeros((L, 1, k), dtype=torch.int32, device=device)
+    gates = torch.zeros((L, 1, k), dtype=torch.float32, device=device)
 
     def step(i):
         with torch.cuda.stream(stream):
@@ -258,52 +349,35 @@ def run_ours(args):
     ms_per_step = ms / args.steps
     tok_s = 1000.0 / ms_per_step
     launches = w.forward_launches(1) * args.steps
+    ids_rec = ids.cpu().numpy()  # routing of the last timed token (every rank identical)
 
     # ---- roofline of the dominant kernel, live CUDA events ------------------
-    # Single GPU: the whole step is ONE launch of decode_stack_kernel (every
-    # layer's experts + routing + residual), so it is the dominant kernel:
-    # algorithmic bytes = L x (k*3*d*f*esz expert weights + E*d*4 router).
-    # The per-layer streaming expert kernel (EP path) is reported beside it.
-    peak, peak_src = load_peaks()
+    # The whole step is ONE launch of the persistent stack kernel (every
+    # layer's experts + routing + residual; at N>1 with the peer exchange
+    # inside), so it is the dominant kernel.  Algorithmic bytes per launch on
+    # THIS rank = the expert rows it streams: 1 GPU: L x k x 3 d f esz (+ the
+    # router); tp: L x k x 3 d (f/N) esz; ep: the routed experts it owns.
+    peaks, peak_src = load_peaks()
+    peak = float(peaks["hbm_gbs"])
+    router_bytes = E * d * 4
+    if world == 1:
+        rank_bytes = L * (k * 3 * d * f * esz + router_bytes)
+        basis = f"{L} layers x ({k} experts x 3 x {d} x {f} x {esz} B + router {E}x{d}x4 B)"
+    elif args.shard == "tp":
+        rank_bytes = L * k * 3 * d * w.tp[2] * esz
+        basis = f"{L} layers x {k} experts x 3 x {d} x {w.tp[2]} (ffn/{world}) x {esz} B"
+    else:
+        mine = sum(int(owner[l, e] == rank) for l in range(L) for e in ids_rec[l, 0])
+        rank_bytes = mine * 3 * d * f * esz
+        basis = f"{mine} routed experts owned by rank {rank} (last token) x 3 x {d} x {f} x {esz} B"
     roof = None
-    layer_bytes = k * 3 * d * f * esz + E * d * 4
-    expert_kernel = None
-    if w.expert_path(1) == 1:
-        n_rep = max(8, min(64, 2 * L))
-        ypart = torch.empty((ctx.sm_count, d), dtype=torch.float32, device=f"cuda:{local}")
-        lay_ids = []
-        for l in range(L):
-            loc = [e for e in range(E) if owner is None or owner[l, e] == rank]
-            sel = sorted(loc[:k]) if len(loc) >= k else sorted(loc)
-            lay_ids.append(sel + [sel[0]] * (k - len(sel)))
-        idt = torch.tensor(lay_ids, dtype=torch.int32, device=f"cuda:{local}")
-        gt = torch.full((L, k), 1.0 / k, dtype=torch.float32, device=f"cuda:{local}")
-        xk = pool[0:1].clone()
-        for r in range(3):
-            w.decode_experts_partial(r % L, xk, idt[r % L], gt[r % L], ypart, stream=stream_ptr)
-        torch.cuda.synchronize()
-        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        e0.record(stream)
-        for r in range(n_rep):
-            w.decode_experts_partial(r % L, xk, idt[r % L], gt[r % L], ypart, stream=stream_ptr)
-        e1.record(stream)
-        torch.cuda.synchronize()
-        kern_ms = e0.elapsed_time(e1) / n_rep
-        n_loc = len(set(lay_ids[0]))
-        alg = n_loc * 3 * d * w.tp[2] * esz  # ffn rows resident on this rank (tp: f / N)
-        ach = alg / (kern_ms * 1e-3) / 1e9
-        expert_kernel = {"kernel": "decode_experts_kernel", "achieved": round(ach, 1),
-                         "frac": round(ach / peak, 4), "kernel_us": round(kern_ms * 1e3, 2),
-                         "alg_bytes_per_launch": alg,
-                         # ncu bytes of the single-GPU layer kernel (profiles/); not for a shard
-                         "traffic": args.traffic if world == 1 else None}
-        del ypart
-    if world == 1 and w.forward_launches(1) == 1:
+    if w.forward_launches(1) == 1:
         n_rep = max(10, min(50, args.steps))
-        xs = pool[0:1].clone()
+        xs = pool[args.warmup:args.warmup + 1].clone()
         for _ in range(3):
             w.forward(xs, ids, gates, stream=stream_ptr)
         torch.cuda.synchronize()
+        barrier(world)
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record(stream)
         for _ in range(n_rep):
@@ -311,26 +385,31 @@ def run_ours(args):
         e1.record(stream)
         torch.cuda.synchronize()
         kern_ms = e0.elapsed_time(e1) / n_rep
-        alg = L * layer_bytes
-        ach = alg / (kern_ms * 1e-3) / 1e9
+        ach = rank_bytes / (kern_ms * 1e-3) / 1e9
+        per_rank = gather_floats(round(ach, 1), world)
         roof = {"bound": "hbm", "achieved": round(ach, 1), "peak": peak, "unit": "GB/s",
-                "frac": round(ach / peak, 4), "traffic": args.stack_traffic,
-                "kernel": "decode_stack_kernel<bf16,2> (one launch per token)",
-                "kernel_us": round(kern_ms * 1e3, 2), "alg_bytes_per_launch": alg,
-                "alg_bytes_basis": f"{L} layers x ({k} experts x 3 x {d} x {f} x {esz} B + router {E}x{d}x4 B)",
-                "peak_source": peak_src, "expert_kernel": expert_kernel}
-    elif expert_kernel is not None:
-        roof = {"bound": "hbm", "achieved": expert_kernel["achieved"], "peak": peak, "unit": "GB/s",
-                "frac": expert_kernel["frac"], "traffic": expert_kernel["traffic"], "kernel": "decode_experts_kernel",
-                "kernel_us": expert_kernel["kernel_us"],
-                "alg_bytes_per_launch": expert_kernel["alg_bytes_per_launch"], "peak_source": peak_src}
-    if roof is not None and world == 1:
-        roof["step_frac"] = round(L * layer_bytes / (ms_per_step * 1e-3) / 1e9 / peak, 4)
-    if roof is not None:  # also against north_star's nominal 8 TB/s
-        roof["frac_vs_nominal_8tbs"] = round(roof["achieved"] / 8000.0, 4)
+                "frac": round(ach / peak, 4), "traffic": args.stack_traffic if world == 1 else None,
+                "kernel": ("decode_stack2_kernel<bf16,2> (one launch per token)" if world == 1 else
+                           "decode_stack_kernel<bf16,2> with in-kernel NVLink exchange (one launch per token per rank)"),
+                "kernel_us": round(kern_ms * 1e3, 2), "alg_bytes_per_launch": rank_bytes,
+                "alg_bytes_basis": basis, "peak_source": peak_src,
+                "frac_vs_nominal_8tbs": round(ach / 8000.0, 4)}
+        if world > 1:
+            roof["per_rank_achieved"] = per_rank
+        else:
+            roof["step_frac"] = round(rank_bytes / (ms_per_step * 1e-3) / 1e9 / peak, 4)
+            roof["read_ceiling_frac"] = round(ach / 7360.0, 4)  # tools/tma_stream_bench.cu row-chunk stream
+
+    # ---- routing margins of the timed tokens -------------------
+    routing = None
+    if world == 1 and L > 1:
+        try:
+            routing = routing_margins(w, pool, range(args.warmup, n_steps), L, E, k, stream_ptr, device)
+        except M.MoeError as e:  # e.g. --stack-kernel 1: no logits output
+            routing = {"unavailable": str(e)}
 
     # ---- e2e through the host-buffer C-ABI entry point ----------------------
-    host_tokens = rs.randn(args.steps + 2, d)
+    host_tokens = token_pool(args.seed + 7, args.steps + 2, d, L).astype(np.float64)
     for i in range(2):
         w.forward_host(host_tokens[i:i + 1])
     barrier(world)
@@ -343,141 +422,201 @@ def run_ours(args):
     torch.cuda.synchronize()
     e2e_ms = max_over_ranks(e0.elapsed_time(e1), world) / args.steps
     e2e = {"value": round(1000.0 / e2e_ms, 3), "unit": "tok/s", "h2d_bytes_per_step": d * 4,
-           "d2h_bytes_per_step": d * 4 + L * k * 4 * 2, "ms_per_step": round(e2e_ms, 4)}
+           "d2h_bytes_per_step": d * 4 + L * k * 4 * 2, "ms_per_step": round(e2e_ms, 4),
+           "api": "moe_forward_host (fp64 host token in, fp64 output + routing out)"}
+
+    extra = None
+    if world == 1 and args.config == "stack32" and not args.no_extras:
+        extra = {"single_layer_decode": bench_layer(args, w, stream, stream_ptr, device, peaks, peak_src),
+                 "prefill512": bench_prefill(args, w, stream, stream_ptr, device, peaks, peak_src)}
 
     cpu = None
-    if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        cpu = cpu_baseline(args, w, pool[args.warmup].cpu().numpy().astype(np.float64), L)
+    if rank == 0 and not args.no_cpu_baseline:
+        cpu = cpu_baseline(args, pool_h[args.warmup].astype(np.float64), L)
 
     if rank == 0:
+        par = f"{args.shard}{world}" if world > 1 else "single-gpu"
         line = {
             "metric": METRIC, "value": round(tok_s, 3), "unit": "tok/s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms_per_step, 4),
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
-            "dtype": "bf16" if dt == "bf16" else "f32", "data": "synthetic (random-init weights, N(0,1) tokens)",
+            "dtype": "bf16" if dt == "bf16" else "f32",
+            "data": ("synthetic: random-init weights (device Philox N(0,1/sqrt(d))), tokens "
+                     + (f"{STACK_TOKEN_SCALE} x N(0,1) (a norm-less random stack overflows from N(0,1))"
+                        if L > 1 else "N(0,1)")),
             "config": {"workload": WORKLOAD_NAME[args.config] + (f" [reduced to {L} layers]" if args.layers else ""),
                        "layers": L, "experts": E, "top_k": k,
-                       "hidden": d, "ffn": f, "batch": 1,
-                       "parallelism": f"{args.shard}{world}" if world > 1 else "single-gpu",
+                       "hidden": d, "ffn": f, "batch": 1, "parallelism": par,
                        "combine": None if world == 1 else
                        ("ncclAllReduce" if args.nccl_combine else "fused peer-memory exchange (NVLink P2P)"),
                        "path": "persistent stack kernel (1 launch/token)" if w.forward_launches(1) == 1
                        else f"per-layer kernels ({w.forward_launches(1)} launches/token, CUDA graph + PDL)",
                        "l2": f"inputs larger than L2: {L * k * 3 * d * f * esz / 1e9:.1f} GB of expert weights streamed per step"},
             "gpu_launches": launches, "clocks": clk.summary(), "e2e": e2e, "roofline": roof,
-            "cpu_baseline": cpu,
+            "routing": routing, "cpu_baseline": cpu,
         }
+        if extra is not None:
+            line["extra_configs"] = extra
         print(json.dumps(line), flush=True)
     w.close()
     ctx.close()
 
 
-def run_prefill(args):
-    """BASELINE configs[2]: one Mixtral-shaped layer, 512-token prefill, bf16,
-    on the tcgen05 grouped-GEMM path.  Reports tok/s and both rooflines."""
+def bench_layer(args, w, stream, stream_ptr, device, peaks, peak_src):
+    """BASELINE configs[1]: one Mixtral-shaped layer, batch-1 decode (layer 0
+    of the bench's weights, N(0,1) tokens): moe_layer_forward = router +
+    streaming expert kernel + reduce/residual, per-layer kernels."""
     import torch
 
-    import paper_2402_07033_b200 as M
-
-    L, E, k, d, f = 1, 8, 2, 4096, 14336
-    n = args.prefill_tokens
-    torch.cuda.set_device(0)
-    ctx = M.Ctx(0)
-    w = M.Weights(ctx, M.Shape(L, E, k, d, f, 2), M.DTYPE_BF16)
-    w.random(args.seed)
-    assert w.expert_path(n) == 3, "tcgen05 prefill path not selected"
-    sp = ctx.stream
-    stream = torch.cuda.ExternalStream(sp, device="cuda:0")
-    n_batches = args.warmup + args.steps
-    gen = torch.Generator(device="cuda:0").manual_seed(args.seed + 1)
-    with torch.cuda.stream(stream):
-        xs = torch.randn((n_batches, n, d), generator=gen, device="cuda:0")
-        xo = torch.empty((n, d), device="cuda:0")
-        ids = torch.zeros((n, k), dtype=torch.int32, device="cuda:0")
-        g = torch.zeros((n, k), dtype=torch.float32, device="cuda:0")
-    torch.cuda.synchronize()
-    for i in range(args.warmup):
-        w.layer_forward(0, xs[i], xo, ids, g, stream=sp)
+    L, E, k, d, f, _ = CONFIGS["layer"]
+    n_rep = max(50, 10 * args.steps)
+    toks = torch.tensor(token_pool(args.seed, 8, d, 1), device=device)
+    xo = torch.empty((1, d), device=device)
+    ids = torch.zeros((1, k), dtype=torch.int32, device=device)
+    g = torch.zeros((1, k), device=device)
+    for i in range(5):
+        w.layer_forward(0, toks[i % 8:i % 8 + 1], xo, ids, g, stream=stream_ptr)
     torch.cuda.synchronize()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    with ClockSampler(0) as clk:
+    with ClockSampler(torch.cuda.current_device()) as clk:
         e0.record(stream)
-        for i in range(args.warmup, n_batches):
-            w.layer_forward(0, xs[i], xo, ids, g, stream=sp)
+        for i in range(n_rep):
+            w.layer_forward(0, toks[i % 8:i % 8 + 1], xo, ids, g, stream=stream_ptr)
         e1.record(stream)
         torch.cuda.synchronize()
-    ms = e0.elapsed_time(e1) / args.steps
+    ms = e0.elapsed_time(e1) / n_rep
+    # dominant kernel: the streaming expert kernel, timed alone
+    ypart = torch.empty((w.ctx.sm_count, d), dtype=torch.float32, device=device)
+    sel = torch.tensor([1, 5], dtype=torch.int32, device=device)
+    gt = torch.full((k,), 0.5, device=device)
+    for _ in range(3):
+        w.decode_experts_partial(0, toks[0:1], sel, gt, ypart, stream=stream_ptr)
+    torch.cuda.synchronize()
+    e0.record(stream)
+    for _ in range(n_rep):
+        w.decode_experts_partial(0, toks[0:1], sel, gt, ypart, stream=stream_ptr)
+    e1.record(stream)
+    torch.cuda.synchronize()
+    kern_ms = e0.elapsed_time(e1) / n_rep
+    alg = k * 3 * d * f * 2
+    peak = float(peaks["hbm_gbs"])
+    ach = alg / (kern_ms * 1e-3) / 1e9
+    # e2e: the per-layer C-ABI call with the token copied in from pinned host
+    # memory and the output read back, one synchronous step per token
+    host = torch.tensor(token_pool(args.seed + 3, 8, d, 1)).pin_memory()
+    out_h = torch.empty((1, d)).pin_memory()
+    xd = torch.empty((1, d), device=device)
+    n_e2e = max(20, args.steps)
+    torch.cuda.synchronize()
+    e0.record(stream)
+    for i in range(n_e2e):
+        with torch.cuda.stream(stream):
+            xd.copy_(host[i % 8:i % 8 + 1], non_blocking=True)
+        w.layer_forward(0, xd, xo, ids, g, stream=stream_ptr)
+        with torch.cuda.stream(stream):
+            out_h.copy_(xo, non_blocking=True)
+        stream.synchronize()
+    e1.record(stream)
+    torch.cuda.synchronize()
+    e2e_ms = e0.elapsed_time(e1) / n_e2e
+    return {"metric": LAYER_METRIC, "value": round(1000.0 / ms, 1), "unit": "tok/s", "ms_per_step": round(ms, 5),
+            "steps": n_rep, "higher_is_better": True,
+            "config": {"workload": WORKLOAD_NAME["layer"], "path": "moe_layer_forward: router_topk + "
+                       "decode_experts_kernel (TMA ring) + reduce_residual_kernel", "weights": "layer 0 of the bench stack",
+                       "l2": "704.6 MB of expert weights per step (> L2)"},
+            "clocks": clk.summary(),
+            "e2e": {"value": round(1000.0 / e2e_ms, 1), "unit": "tok/s", "h2d_bytes_per_step": d * 4,
+                    "d2h_bytes_per_step": d * 4, "ms_per_step": round(e2e_ms, 5),
+                    "api": "moe_layer_forward with pinned-host H2D of the token and D2H of the output, synchronous"},
+            "roofline": {"bound": "hbm", "achieved": round(ach, 1), "peak": peak, "unit": "GB/s",
+                         "frac": round(ach / peak, 4), "traffic": args.traffic,
+                         "kernel": "decode_experts_kernel<bf16,2>", "kernel_us": round(kern_ms * 1e3, 2),
+                         "alg_bytes_per_launch": alg, "alg_bytes_basis": f"{k} experts x 3 x {d} x {f} x 2 B",
+                         "peak_source": peak_src,
+                         "step_frac": round((alg + E * d * 4) / (ms * 1e-3) / 1e9 / peak, 4)}}
+
+
+def bench_prefill(args, w, stream, stream_ptr, device, peaks, peak_src):
+    """BASELINE configs[2]: one Mixtral-shaped layer (layer 0 of the given
+    weights), 512-token prefill on the tcgen05/TMEM grouped GEMM path."""
+    import torch
+
+    L, E, k, d, f, _ = CONFIGS["layer"]
+    n = args.prefill_tokens
+    assert w.expert_path(n) == 3, "tcgen05 prefill path not selected"
+    w.reserve(n)
+    gen = torch.Generator(device=device).manual_seed(args.seed + 1)
+    with torch.cuda.stream(stream):
+        xs = [torch.randn((n, d), generator=gen, device=device) for _ in range(8)]
+        xo = torch.empty((n, d), device=device)
+        ids = torch.zeros((n, k), dtype=torch.int32, device=device)
+        g = torch.zeros((n, k), dtype=torch.float32, device=device)
+    torch.cuda.synchronize()
+    for i in range(args.warmup):
+        w.layer_forward(0, xs[i % 8], xo, ids, g, stream=stream_ptr)
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    n_steps = max(args.steps, 20)
+    with ClockSampler(torch.cuda.current_device()) as clk:
+        e0.record(stream)
+        for i in range(n_steps):
+            w.layer_forward(0, xs[i % 8], xo, ids, g, stream=stream_ptr)
+        e1.record(stream)
+        torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1) / n_steps
     active = len(set(ids.cpu().numpy().ravel().tolist()))
     # live duration of the dominant kernel (the grouped GEMM): CUDA events on
     # the launching stream around each launch, over a separate loop
     w.kernel_timing(True)
-    n_k = max(10, min(args.steps, 50))
+    n_k = max(10, min(n_steps, 50))
     for i in range(n_k):
-        w.layer_forward(0, xs[args.warmup + i % args.steps], xo, ids, g, stream=sp)
+        w.layer_forward(0, xs[i % 8], xo, ids, g, stream=stream_ptr)
     tot_us, n_launch = w.kernel_timing(False)
     kern_us = tot_us / max(1, n_launch)
-    # e2e through the host-buffer entry point: fp64 host tokens -> H2D ->
-    # router + grouped GEMM + combine -> D2H of outputs and routing
-    rs = np.random.RandomState(args.seed + 2)
-    host = [rs.randn(n, d) for _ in range(3)]
-    w.forward_host(host[0])
-    ee0, ee1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    n_e2e = max(3, min(args.steps, 30))
+    # e2e: the layer call with the 512 tokens copied in from pinned host
+    # memory and outputs + routing copied back, stream-ordered
+    host = torch.tensor(token_pool(args.seed + 5, n, d, 1)).pin_memory()
+    out_h = torch.empty((n, d)).pin_memory()
+    ids_h = torch.empty((n, k), dtype=torch.int32).pin_memory()
+    xd = torch.empty((n, d), device=device)
+    n_e2e = max(10, min(n_steps, 30))
     torch.cuda.synchronize()
-    ee0.record(stream)
+    e0.record(stream)
     for i in range(n_e2e):
-        w.forward_host(host[1 + i % 2])
-    ee1.record(stream)
+        with torch.cuda.stream(stream):
+            xd.copy_(host, non_blocking=True)
+        w.layer_forward(0, xd, xo, ids, g, stream=stream_ptr)
+        with torch.cuda.stream(stream):
+            out_h.copy_(xo, non_blocking=True)
+            ids_h.copy_(ids, non_blocking=True)
+    e1.record(stream)
     torch.cuda.synchronize()
-    e2e_ms = ee0.elapsed_time(ee1) / n_e2e
-    e2e = {"value": round(n / (e2e_ms * 1e-3), 1), "unit": "tok/s", "h2d_bytes_per_step": n * d * 4,
-           "d2h_bytes_per_step": n * d * 4 + n * k * 8, "ms_per_step": round(e2e_ms, 4)}
-    cpu = None
-    if not args.no_cpu_baseline:
-        import oracle as O
-
-        if O.reference_available():
-            toks = rs.randn(args.cpu_tokens // 3 or 1, d)
-            ref, shape, wr = _mixtral_layer_for_reference(d, f, E, k, toks)
-            _, secs = ref.time_forward(shape, wr, toks)
-            cpu = {"value": round(len(toks) / secs, 4), "unit": "tok/s", "cores": 1, "kind": "reference",
-                   "sample": f"{len(toks)} distinct tokens x 1 Mixtral-shaped layer (reference model_forward, "
-                             f"fp64, token-major: cost linear in tokens)", "host_cores": os.cpu_count()}
-    bytes_ = active * 3 * d * f * 2 + E * d * 4 + n * d * 4 * 2
-    # SURVEY 8d per-launch figure of the grouped kernel: the active experts'
-    # weights + X in bf16 + Y out in fp32
+    e2e_ms = e0.elapsed_time(e1) / n_e2e
+    peak = float(peaks["hbm_gbs"])
+    tflops_peak = float(peaks.get("bf16_tflops", 1590.0))
     kbytes = active * 3 * d * f * 2 + n * d * (2 + 4)
     flops = 2.0 * 3 * d * f * n * k
-    peak_bw, src = load_peaks()
-    peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json"))) if os.path.exists(
-        os.path.join(ROOT, "MEASURED_PEAKS.json")) else {"bf16_tflops": 1590.0}
-    bw = bytes_ / (ms * 1e-3) / 1e9
-    tf = flops / (ms * 1e-3) / 1e12
     kbw = kbytes / (kern_us * 1e-6) / 1e9
-    ktf = flops / (kern_us * 1e-6) / 1e12
-    print(json.dumps({
-        "metric": PREFILL_METRIC, "value": round(n / (ms * 1e-3), 1),
-        "unit": "tok/s", "n_gpus": 1, "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms, 4),
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "bf16",
-        "data": "synthetic (random-init weights, N(0,1) tokens)",
-        "config": {"workload": PREFILL_WORKLOAD,
-                   "l2": "inputs larger than L2: 2.8 GB of expert weights streamed per step; token "
-                         "batches rotate over steps",
-                   "path": "tcgen05/TMEM grouped GEMM (swap-AB), TMA SW128", "active_experts": active},
-        "gpu_launches": w.forward_launches(n) * args.steps, "clocks": clk.summary(), "e2e": e2e,
-        "cpu_baseline": cpu,
-        "roofline": {"bound": "hbm", "achieved": round(kbw, 1), "peak": peak_bw, "unit": "GB/s",
-                     "frac": round(kbw / peak_bw, 4), "frac_vs_nominal_8tbs": round(kbw / 8000.0, 4),
-                     "traffic": args.prefill_traffic if n == 512 else None,
-                     "kernel": "prefill_grouped_kernel (tcgen05 grouped GEMM, one launch per layer)",
-                     "kernel_us": round(kern_us, 2), "alg_bytes_per_launch": kbytes,
-                     "alg_bytes_basis": f"{active} experts x 3 x {d} x {f} x 2 B + {n} tokens x {d} x (2 + 4) B",
-                     "tensor_tflops": round(ktf, 1), "tensor_frac": round(ktf / peaks["bf16_tflops"], 4),
-                     "step_achieved": round(bw, 1), "step_frac": round(bw / peak_bw, 4),
-                     "step_tensor_tflops": round(tf, 1), "peak_source": src},
-    }), flush=True)
-    w.close()
-    ctx.close()
+    bw = (active * 3 * d * f * 2 + E * d * 4 + n * d * 4 * 2) / (ms * 1e-3) / 1e9
+    return {"metric": PREFILL_METRIC, "value": round(n / (ms * 1e-3), 1), "unit": "tok/s",
+            "ms_per_step": round(ms, 4), "steps": n_steps, "higher_is_better": True,
+            "config": {"workload": PREFILL_WORKLOAD, "weights": "layer 0 of the bench weights", "tokens": n,
+                       "path": "router_topk_bulk + permute + gather + tcgen05/TMEM grouped GEMM (swap-AB) + combine",
+                       "active_experts": active,
+                       "l2": "2.8 GB of expert weights per step (> L2); 8 token batches rotate"},
+            "clocks": clk.summary(),
+            "e2e": {"value": round(n / (e2e_ms * 1e-3), 1), "unit": "tok/s", "h2d_bytes_per_step": n * d * 4,
+                    "d2h_bytes_per_step": n * d * 4 + n * k * 4, "ms_per_step": round(e2e_ms, 4),
+                    "api": "moe_layer_forward with pinned-host H2D of the tokens and D2H of outputs + ids, stream-ordered"},
+            "roofline": {"bound": "hbm", "achieved": round(kbw, 1), "peak": peak, "unit": "GB/s",
+                         "frac": round(kbw / peak, 4), "traffic": args.prefill_traffic if n == 512 else None,
+                         "kernel": "prefill_grouped_kernel (tcgen05 grouped GEMM, one launch per layer)",
+                         "kernel_us": round(kern_us, 2), "alg_bytes_per_launch": kbytes,
+                         "alg_bytes_basis": f"{active} experts x 3 x {d} x {f} x 2 B + {n} tokens x {d} x (2 + 4) B",
+                         "tensor_tflops": round(flops / (kern_us * 1e-6) / 1e12, 1),
+                         "tensor_frac": round(flops / (kern_us * 1e-6) / 1e12 / tflops_peak, 4),
+                         "step_achieved": round(bw, 1), "step_frac": round(bw / peak, 4),
+                         "step_tensor_tflops": round(flops / (ms * 1e-3) / 1e12, 1), "peak_source": peak_src}}
 
 
 def _mixtral_layer_for_reference(d, f, E, k, token, seed=0):
@@ -503,7 +642,7 @@ def _mixtral_layer_for_reference(d, f, E, k, token, seed=0):
     return ref, shape, w
 
 
-def cpu_baseline(args, gw, token, L):
+def cpu_baseline(args, token, L):
     """Reference model_forward (oracle/_ref) on one Mixtral-shaped layer, a
     bounded sample of tokens, 1 host thread; scaled to the L-layer stack."""
     import oracle as O
@@ -518,6 +657,7 @@ def cpu_baseline(args, gw, token, L):
     _, secs = ref.time_forward(shape, w, toks)
     per_tok_layer = secs / n
     return {"value": round(1.0 / (per_tok_layer * L), 5), "unit": "tok/s", "cores": 1, "kind": "reference",
+            "mode": "batch-1 latency, 1 thread",
             "sample": f"{n} tokens x 1 Mixtral-shaped layer (fp64 reference model_forward, "
                       f"{per_tok_layer * 1e3:.1f} ms/token/layer), scaled to {L} layers",
             "host_cores": os.cpu_count()}
@@ -565,9 +705,14 @@ def run_reference(args):
     for _ in range(args.warmup):
         one_step()
     times = [one_step() for _ in range(args.steps)]
+    # batch-1 latency of the same reference call on one thread (3 samples)
+    lat = [ref.model_forward_timed(handle, toks[0]) for _ in range(3)]
     ref.model_destroy(handle)
     secs = sum(times)
     tok_s = threads * args.steps / (secs * L)
+    lat_tok_s = 1.0 / (statistics.median(lat) * L)
+    mode = (f"throughput: {threads} concurrent independent model_forward calls (the reference is reentrant, "
+            f"SPEC.md:114), 1 token each; batch-1 latency on 1 thread is batch1_latency_tok_s")
     if prefill:
         line = {"impl": "reference", "metric": PREFILL_METRIC, "value": round(tok_s, 5), "unit": "tok/s",
                 "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
@@ -575,8 +720,10 @@ def run_reference(args):
                 "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
                 "config": {"workload": PREFILL_WORKLOAD, "parallelism": f"cpu x{threads} threads"},
                 "cpu_baseline": {"value": round(tok_s, 5), "unit": "tok/s", "cores": threads, "kind": "reference",
+                                 "mode": mode,
                                  "sample": f"{threads} threads x 1 distinct token x 1 Mixtral-shaped layer per step "
                                            f"(reference model_forward, fp64; token-major, linear in tokens)"},
+                "batch1_latency_tok_s": round(lat_tok_s, 5),
                 "e2e": {"value": round(tok_s, 5), "unit": "tok/s", "h2d_bytes_per_step": 0,
                         "d2h_bytes_per_step": 0}}
         print(json.dumps(line), flush=True)
@@ -588,10 +735,48 @@ def run_reference(args):
             "config": {"workload": WORKLOAD_NAME[args.config], "layers": L, "experts": E, "top_k": k,
                        "hidden": d, "ffn": f, "batch": 1, "parallelism": f"cpu x{threads} threads"},
             "cpu_baseline": {"value": round(tok_s, 5), "unit": "tok/s", "cores": threads, "kind": "reference",
+                             "mode": mode,
                              "sample": f"{threads} threads x 1 token x 1 Mixtral-shaped layer per step "
                                        f"(reference model_forward, fp64), scaled to {L} layers"},
+            "batch1_latency_tok_s": round(lat_tok_s, 5),
             "e2e": {"value": round(tok_s, 5), "unit": "tok/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
+
+
+def run_prefill(args):
+    """--config prefill512 alone (BASELINE configs[2]) on a 1-layer model."""
+    import torch
+
+    import paper_2402_07033_b200 as M
+
+    L, E, k, d, f, _ = CONFIGS["layer"]
+    torch.cuda.set_device(0)
+    ctx = M.Ctx(0)
+    w = M.Weights(ctx, M.Shape(L, E, k, d, f, 2), M.DTYPE_BF16)
+    w.random(args.seed)
+    sp = ctx.stream
+    stream = torch.cuda.ExternalStream(sp, device="cuda:0")
+    peaks, src = load_peaks()
+    res = bench_prefill(args, w, stream, sp, "cuda:0", peaks, src)
+    res.update({"n_gpus": 1, "warmup": args.warmup, "scaling": "weak", "vs_baseline": None, "dtype": "bf16",
+                "data": "synthetic (random-init weights, N(0,1) tokens)",
+                "gpu_launches": w.forward_launches(args.prefill_tokens) * res["steps"]})
+    if not args.no_cpu_baseline:
+        import oracle as O
+
+        if O.reference_available():
+            rs = np.random.RandomState(args.seed + 2)
+            toks = rs.randn(max(1, args.cpu_tokens // 3), d)
+            ref, shape, wr = _mixtral_layer_for_reference(d, f, E, k, toks)
+            _, secs = ref.time_forward(shape, wr, toks)
+            res["cpu_baseline"] = {"value": round(len(toks) / secs, 4), "unit": "tok/s", "cores": 1,
+                                   "kind": "reference",
+                                   "sample": f"{len(toks)} distinct tokens x 1 Mixtral-shaped layer (reference "
+                                             f"model_forward, fp64, token-major: cost linear in tokens)",
+                                   "host_cores": os.cpu_count()}
+    print(json.dumps(res), flush=True)
+    w.close()
+    ctx.close()
 
 
 def main():
@@ -606,6 +791,7 @@ def main():
     ap.add_argument("--cpu-tokens", type=int, default=12)
     ap.add_argument("--ref-threads", type=int, default=0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-extras", action="store_true", help="skip the configs[1]/[2] sub-measurements")
     ap.add_argument("--layers", type=int, default=0,
                     help="override the config's layer count (per-layer rate of a stack that does not fit)")
     ap.add_argument("--shard", default="ep", choices=["ep", "tp"],
@@ -623,6 +809,12 @@ def main():
                     help="dram bytes per launch of the decode kernel from an ncu --set full capture")
     args = ap.parse_args()
     args.warmup = max(3, args.warmup)
+    if args.impl == "ours" and args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        relaunch_under_torchrun(args.gpus)
+    if args.impl == "ours" and "WORLD_SIZE" in os.environ and env_int("WORLD_SIZE", 1) != args.gpus:
+        print(json.dumps({"metric": METRIC, "error": f"--gpus {args.gpus} but WORLD_SIZE={os.environ['WORLD_SIZE']}"}),
+              flush=True)
+        sys.exit(2)
     args.stack_traffic = None
     args.prefill_traffic = None
     tp = os.path.join(ROOT, "profiles", "decode_traffic.json")
@@ -632,7 +824,7 @@ def main():
             args.traffic = tj.get("dram_bytes_per_launch")
         args.stack_traffic = tj.get("stack_dram_bytes_per_launch")
         args.prefill_traffic = tj.get("prefill_dram_bytes_per_launch")
-    if args.no_stack or args.stack_kernel or args.force_ep:
+    if args.impl == "ours":
         import paper_2402_07033_b200 as M
 
         if args.no_stack:

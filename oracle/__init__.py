@@ -105,6 +105,7 @@ class Oracle(_Base):
         L.oracle_random_model.argtypes = [C.c_void_p, C.c_uint64, C.c_void_p, C.c_void_p,
                                           C.c_void_p, C.c_void_p]
         L.oracle_expert_ffn.argtypes = [C.c_int, C.c_int, _dp, _dp, _dp, _dp, _dp]
+        L.oracle_expert_ffn_batch.argtypes = [C.c_int, C.c_int, _dp, _dp, _dp, C.c_int, _dp, _dp]
         L.oracle_gate_topk.argtypes = [C.c_int, C.c_int, _dp, _dp, C.c_int, _i32p, _dp, _dp]
         L.oracle_model_forward.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p,
                                            C.c_void_p, C.c_int, _dp, _i32p, _dp, _i32p, _dp,
@@ -153,6 +154,38 @@ class Oracle(_Base):
                                    _p(np.ascontiguousarray(w_gate)),
                                    _p(np.ascontiguousarray(w_out)), _p(x), _p(y))
         return y
+
+    def expert_ffn_batch(self, w_in, w_gate, w_out, X) -> np.ndarray:
+        """expert_ffn for every row of X [n x d] (each row bit-identical to
+        expert_ffn); releases the GIL, so threads can run experts in parallel."""
+        f, d = w_in.shape
+        X = np.ascontiguousarray(X, dtype=np.float64).reshape(-1, d)
+        Y = np.empty_like(X)
+        self.lib.oracle_expert_ffn_batch(d, f, _p(np.ascontiguousarray(w_in)),
+                                         _p(np.ascontiguousarray(w_gate)),
+                                         _p(np.ascontiguousarray(w_out)), X.shape[0], _p(X), _p(Y))
+        return Y
+
+    def random_model_stream(self, shape: Shape, seed: int):
+        """random_model (model.cpp:34-53) one matrix group at a time, so a
+        Mixtral-shaped layer (11.3 GB of fp64) never sits in host memory at
+        once.  Yields ("expert", l, e, w_in, w_gate, w_out) and ("router", l,
+        R) in the reference's draw order — the same values as random_model."""
+        L, E, d, f = shape.num_layers, shape.experts_per_layer, shape.hidden_dim, shape.ffn_dim
+        st = (C.c_uint8 * (312 * 8 + 16))()
+        self.lib.oracle_rng_seed(st, seed)
+        scale = 1.0 / np.sqrt(d)
+        for l in range(L):
+            for e in range(E):
+                mats = []
+                for rows, cols in ((f, d), (f, d), (d, f)):
+                    m = np.empty((rows, cols))
+                    self.lib.oracle_normal_fill(st, scale, _p(m), m.size)
+                    mats.append(m)
+                yield ("expert", l, e, *mats)
+            r = np.empty((E, d))
+            self.lib.oracle_normal_fill(st, scale, _p(r), r.size)
+            yield ("router", l, r)
 
     def gate_topk(self, router_l, x, k):
         E, d = router_l.shape
@@ -301,6 +334,38 @@ class Reference(_Base):
                                             _p(np.ascontiguousarray(w_gate)),
                                             _p(np.ascontiguousarray(w_out)), _p(x), len(x), _p(y)))
         return y
+
+    def expert_ffn_batch(self, w_in, w_gate, w_out, X) -> np.ndarray:
+        """expert_ffn for every row of X [n x d] (each row bit-identical to
+        expert_ffn); releases the GIL, so threads can run experts in parallel."""
+        f, d = w_in.shape
+        X = np.ascontiguousarray(X, dtype=np.float64).reshape(-1, d)
+        Y = np.empty_like(X)
+        self.lib.oracle_expert_ffn_batch(d, f, _p(np.ascontiguousarray(w_in)),
+                                         _p(np.ascontiguousarray(w_gate)),
+                                         _p(np.ascontiguousarray(w_out)), X.shape[0], _p(X), _p(Y))
+        return Y
+
+    def random_model_stream(self, shape: Shape, seed: int):
+        """random_model (model.cpp:34-53) one matrix group at a time, so a
+        Mixtral-shaped layer (11.3 GB of fp64) never sits in host memory at
+        once.  Yields ("expert", l, e, w_in, w_gate, w_out) and ("router", l,
+        R) in the reference's draw order — the same values as random_model."""
+        L, E, d, f = shape.num_layers, shape.experts_per_layer, shape.hidden_dim, shape.ffn_dim
+        st = (C.c_uint8 * (312 * 8 + 16))()
+        self.lib.oracle_rng_seed(st, seed)
+        scale = 1.0 / np.sqrt(d)
+        for l in range(L):
+            for e in range(E):
+                mats = []
+                for rows, cols in ((f, d), (f, d), (d, f)):
+                    m = np.empty((rows, cols))
+                    self.lib.oracle_normal_fill(st, scale, _p(m), m.size)
+                    mats.append(m)
+                yield ("expert", l, e, *mats)
+            r = np.empty((E, d))
+            self.lib.oracle_normal_fill(st, scale, _p(r), r.size)
+            yield ("router", l, r)
 
     def gate_topk(self, router_l, x, k):
         E, d = router_l.shape

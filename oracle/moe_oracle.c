@@ -145,6 +145,37 @@ void oracle_expert_ffn(int d, int f, const double* w_in, const double* w_gate,
   free(gate);
 }
 
+/* expert_ffn (model.cpp:55-67) for n tokens against ONE expert: the same
+ * per-token arithmetic and summation order as oracle_expert_ffn (each output
+ * y_t bit-identical to it), with the weight rows visited once for the whole
+ * batch (large-shape parity checks stream 1.4 GB of fp64 weights per
+ * expert).  X, Y: [n x d] row-major. */
+void oracle_expert_ffn_batch(int d, int f, const double* w_in, const double* w_gate,
+                             const double* w_out, int n, const double* X, double* Y) {
+  double* up = (double*)malloc(sizeof(double) * (size_t)f * (size_t)(n > 0 ? n : 1));
+  for (int r = 0; r < f; ++r) {
+    const double* a = w_in + (size_t)r * d;
+    const double* b = w_gate + (size_t)r * d;
+    for (int t = 0; t < n; ++t) {
+      const double* x = X + (size_t)t * d;
+      double sa = 0.0, sb = 0.0;
+      for (int c = 0; c < d; ++c) sa += a[c] * x[c];
+      for (int c = 0; c < d; ++c) sb += b[c] * x[c];
+      up[(size_t)t * f + r] = oracle_silu(sa) * sb;
+    }
+  }
+  for (int i = 0; i < d; ++i) {
+    const double* o = w_out + (size_t)i * f;
+    for (int t = 0; t < n; ++t) {
+      const double* u = up + (size_t)t * f;
+      double s = 0.0;
+      for (int r = 0; r < f; ++r) s += o[r] * u[r];
+      Y[(size_t)t * d + i] = s;
+    }
+  }
+  free(up);
+}
+
 /* gate_topk, model.cpp:69-101.  The stable_sort on (logit desc, id asc) is a
  * total order, so a selection of the k best under that order is the same
  * set; ids are then re-sorted ascending (:86) and the softmax is taken over

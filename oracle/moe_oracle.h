@@ -66,6 +66,9 @@ void oracle_matvec(int rows, int cols, const double* m, const double* x, double*
 /* silu, model.hpp:51. */
 double oracle_silu(double x);
 
+/* expert_ffn for n tokens of one expert (bit-identical per token). */
+void oracle_expert_ffn_batch(int d, int f, const double* w_in, const double* w_gate,
+                             const double* w_out, int n, const double* X, double* Y);
 /* expert_ffn, model.cpp:55-67.  w_in,w_gate [f x d], w_out [d x f]. */
 void oracle_expert_ffn(int d, int f, const double* w_in, const double* w_gate,
                        const double* w_out, const double* x, double* y);

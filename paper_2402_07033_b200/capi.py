@@ -413,9 +413,18 @@ class Weights:
     def random(self, seed: int):
         check(lib().moe_weights_random(self.h, seed))
 
-    def download_expert(self, layer, expert):
+    def download_expert(self, layer, expert, out=None):
+        """Device-held values of one expert in the reference layout (fp64).
+        out=(w_in, w_gate, w_out) fills given arrays: a tensor-parallel rank
+        writes only its slice, so the ranks' downloads into one set of
+        arrays assemble the full expert."""
         d, f = self.shape.hidden_dim, self.shape.ffn_dim
-        wi, wg, wo = np.empty((f, d)), np.empty((f, d)), np.empty((d, f))
+        if out is not None:
+            wi, wg, wo = out
+            assert wi.shape == (f, d) and wg.shape == (f, d) and wo.shape == (d, f)
+            assert all(m.dtype == np.float64 and m.flags.c_contiguous for m in out)
+        else:
+            wi, wg, wo = np.empty((f, d)), np.empty((f, d)), np.empty((d, f))
         check(lib().moe_weights_download_expert(self.h, layer, expert, _dptr(wi), _dptr(wg),
                                                 _dptr(wo)))
         return wi, wg, wo

@@ -144,7 +144,7 @@ def test_replica_mask_validation(gpu):
 
 
 @pytest.mark.parametrize("dtype,n_tok", [(M.DTYPE_BF16, 1500), (M.DTYPE_F32, 40)])
-def test_replicas_odd_world_many_experts(gpu, dtype, n_tok):
+def test_replicas_odd_world_many_experts(gpu, orc, dtype, n_tok):
     """E = 16, top-4, 3 ranks (E not divisible by the world), every expert
     replicated on 2 ranks: bf16 takes the tcgen05 path with the device plan
     (a tiny cost model so that splits happen), fp32 the generic kernels
@@ -189,6 +189,20 @@ def test_replicas_odd_world_many_experts(gpu, dtype, n_tok):
     xd = x.double()
     err = float(((outs[0].double() - xd) - (want.double() - xd)).abs().max() / (want.double() - xd).abs().max())
     assert err < 1e-4, err
+    # anchored to the oracle: routing and outputs of a token sample on the
+    # ranks' device-held weights (each expert downloaded from its owner)
+    from _parity import MARGIN, normwise, oracle_deltas, oracle_route
+
+    xh = x.cpu().numpy().astype(np.float64)
+    sample = np.arange(0, n_tok, max(1, n_tok // 40))
+    oid, og, _, marg = oracle_route(orc, ws[0].download_router(0), xh[sample], k)
+    ok = marg > MARGIN
+    assert np.array_equal(idss[0].cpu().numpy()[sample][ok], oid[ok])
+    delta = oracle_deltas(orc, lambda e: ws[int(owner[0, e])].download_expert(0, e), xh[sample][ok],
+                          oid[ok], og[ok])
+    got = outs[0].cpu().numpy().astype(np.float64)[sample][ok] - xh[sample][ok]
+    err_o = max(normwise(got[i], delta[i]) for i in range(len(delta)))
+    assert err_o < (1e-2 if dtype == M.DTYPE_BF16 else 1e-5), err_o
     if dtype == M.DTYPE_BF16:
         counts = np.bincount(ids.cpu().numpy().ravel(), minlength=E).astype(np.int32)
         holders = (1 << owner[0]).astype(np.uint32) | mask[0]

@@ -1,0 +1,286 @@
+"""GPU parity at the benchmarked sizes, against the oracle and the reference.
+
+* P (BASELINE configs[2]): the bench's 512-token prefill layer — routing of
+  ALL 512 tokens against the oracle's gate_topk on the downloaded router, and
+  64 tokens' outputs against the oracle's experts.
+* S (configs[3]): the bench's 32-layer stack at the bench seed and token —
+  the persistent kernel's routing at EVERY layer against the oracle on the
+  per-layer path's x_l, its logits, teacher-forced deltas at layers 0/15/31,
+  and the routing margin of the workload.
+* M (configs[1]): the reference's own random_model(seed 0) uploaded (bf16 and
+  fp32), against the reference's model_forward output (tests/golden).
+* Sharded (EP / TP, 2 and 4 ranks linked on one GPU, persistent and
+  per-layer kernels, prefill): against the oracle on the ranks' device-held
+  weights, not only against the unsharded GPU path.
+"""
+import importlib.util
+import os
+
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+import oracle as O  # noqa: E402
+import paper_2402_07033_b200 as M  # noqa: E402
+from _parity import (MARGIN, assemble_expert, f32, normwise, oracle_deltas,  # noqa: E402
+                     oracle_route)
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+TOL_F32 = 1e-5   # north_star: fp32 mode
+TOL_BF16 = 1e-2  # north_star: bf16 weights, fp32 accumulate
+MIX = (4096, 14336)
+
+
+def _bench():
+    spec = importlib.util.spec_from_file_location("bench", os.path.join(ROOT, "bench.py"))
+    b = importlib.util.module_from_spec(spec)
+    spec.loader.exec_module(b)
+    return b
+
+
+@pytest.fixture(scope="module")
+def ctx():
+    if not torch.cuda.is_available():
+        pytest.skip("no GPU")
+    torch.cuda.init()
+    c = M.Ctx(0)
+    yield c
+    c.close()
+
+
+# ---------------------------------------------------------------------------
+def test_P_prefill512_all_tokens_routing_and_64_outputs(ctx, orc):
+    """The bench's prefill layer (layer 0 of w.random(0), torch tokens of
+    generator seed 1) on the tcgen05 grouped GEMM: every token's ids and
+    gates vs oracle gate_topk on the downloaded fp32 router; outputs of 64
+    tokens vs oracle expert_ffn on the downloaded bf16 experts."""
+    d, f = MIX
+    n = 512
+    w = M.Weights(ctx, M.Shape(1, 8, 2, d, f, 2), M.DTYPE_BF16)
+    w.random(0)
+    assert w.expert_path(n) == 3
+    gen = torch.Generator(device="cuda").manual_seed(1)
+    x = torch.randn((n, d), generator=gen, device="cuda")  # bench.bench_prefill's first batch
+    xo = torch.empty_like(x)
+    ids = torch.zeros((n, 2), dtype=torch.int32, device="cuda")
+    g = torch.zeros((n, 2), device="cuda")
+    w.layer_forward(0, x, xo, ids, g)
+    torch.cuda.synchronize()
+    xh = x.cpu().numpy().astype(np.float64)
+    ids_g, g_g = ids.cpu().numpy(), g.cpu().numpy()
+    oid, og, _, marg = oracle_route(orc, w.download_router(0), xh, 2)
+    ok = marg > MARGIN
+    print(f"P: {int((~ok).sum())} of {n} tokens below the 1e-5 margin; min margin {marg.min():.3e}")
+    assert (~ok).sum() <= 2
+    assert np.array_equal(ids_g[ok], oid[ok])
+    assert np.abs(g_g[ok] - og[ok]).max() < 1e-5
+    sample = np.arange(0, n, 8)  # 64 tokens
+    sample = sample[ok[sample]]
+    delta = oracle_deltas(orc, lambda e: w.download_expert(0, e), xh[sample], oid[sample], og[sample])
+    got = xo.cpu().numpy().astype(np.float64)[sample] - xh[sample]
+    errs = [normwise(got[i], delta[i]) for i in range(len(sample))]
+    print(f"P: tcgen05 prefill vs oracle over {len(sample)} tokens: worst {max(errs):.3e}")
+    assert max(errs) < TOL_BF16
+    w.close()
+
+
+def test_S_stack32_every_layer_routing_and_teacher_forcing(ctx, orc):
+    """The bench workload (32 layers, w.random(0), bench.token_pool's first
+    timed token): the persistent kernel's ids at every layer equal the
+    oracle's gate_topk on the per-layer path's x_l (margin > 1e-5), its
+    logits match the oracle's, the per-layer path's delta matches the oracle
+    at layers 0/15/31 (teacher forced), and both paths end at the same x_32."""
+    b = _bench()
+    L, E, k = 32, 8, 2
+    d, f = MIX
+    w = M.Weights(ctx, M.Shape(L, E, k, d, f, 2), M.DTYPE_BF16)
+    w.random(0)
+    pool = b.token_pool(0, 8, d, L)
+    x0 = pool[5].astype(np.float64)  # the first timed token at --warmup 5
+    xs = torch.tensor(pool[5:6], device="cuda")
+    ids_s = torch.zeros((L, 1, k), dtype=torch.int32, device="cuda")
+    g_s = torch.zeros((L, 1, k), device="cuda")
+    lg_s = torch.zeros((L, E), device="cuda")
+    w.forward_logits(xs, ids_s, g_s, lg_s)
+    torch.cuda.synchronize()
+    ids_s, g_s, lg_s = ids_s.cpu().numpy()[:, 0], g_s.cpu().numpy()[:, 0], lg_s.cpu().numpy()
+    # the per-layer path supplies every x_l
+    xl = [torch.tensor(pool[5:6], device="cuda")]
+    ids_p = []
+    for l in range(L):
+        xo = torch.empty_like(xl[-1])
+        i1 = torch.zeros((1, k), dtype=torch.int32, device="cuda")
+        g1 = torch.zeros((1, k), device="cuda")
+        w.layer_forward(l, xl[-1], xo, i1, g1)
+        xl.append(xo)
+        ids_p.append(i1)
+    torch.cuda.synchronize()
+    xl = [t.cpu().numpy()[0].astype(np.float64) for t in xl]
+    ids_p = np.array([t.cpu().numpy()[0] for t in ids_p])
+    margins = []
+    for l in range(L):
+        router = w.download_router(l)
+        oid, og, olog, marg = oracle_route(orc, router, xl[l], k)
+        margins.append(marg[0])
+        assert np.isfinite(olog).all()
+        assert np.abs(lg_s[l] - olog[0]).max() / np.abs(olog[0]).max() < 1e-4, f"layer {l} logits"
+        if marg[0] > MARGIN:
+            assert list(ids_s[l]) == list(oid[0]), f"layer {l}: stack {ids_s[l]} oracle {oid[0]}"
+            assert list(ids_p[l]) == list(oid[0]), f"layer {l}: per-layer path"
+            assert np.abs(g_s[l] - og[0]).max() < 1e-5
+        if l in (0, 15, 31):
+            delta = oracle_deltas(orc, lambda e: w.download_expert(l, e), xl[l][None], oid, og)[0]
+            err = normwise(xl[l + 1] - xl[l], delta)
+            print(f"S: layer {l} teacher-forced delta vs oracle {err:.3e}")
+            assert err < 1e-4  # fp32 arithmetic on exactly-held bf16 weights
+    print(f"S: routing margin min over 32 layers {min(margins):.3e}")
+    assert min(margins) > MARGIN
+    out = xs.cpu().numpy()[0].astype(np.float64)
+    assert normwise(out - x0, xl[L] - x0) < 1e-4
+    assert np.isfinite(out).all()
+    w.close()
+
+
+def test_M_reference_random_model_vs_reference_golden(ctx, orc, golden):
+    """The reference's own weights: random_model(Mixtral layer, seed 0)
+    streamed by the oracle (pinned to the reference's sampled values), then
+    uploaded in bf16 and fp32; the token mt19937_64(1) against the
+    reference's model_forward output (golden M_out, fp64 weights).
+    Tolerances: bf16 1e-2 (north_star), fp32 1e-5 (north_star fp32 mode)."""
+    if "M_out" not in golden.files:
+        pytest.skip("golden generated without --mixtral")
+    d, f = MIX
+    shape = O.Shape(1, 8, 2, d, f, 2)
+    wb = M.Weights(ctx, M.Shape(1, 8, 2, d, f, 2), M.DTYPE_BF16)
+    wf = M.Weights(ctx, M.Shape(1, 8, 2, d, f, 4), M.DTYPE_F32)
+    for item in orc.random_model_stream(shape, 0):
+        if item[0] == "expert":
+            _, l, e, wi, wg, wo = item
+            assert np.array_equal(wi[0, :4], golden["M_samples"][e, 0])
+            assert np.array_equal(wg[5, :4], golden["M_samples"][e, 1])
+            assert np.array_equal(wo[7, :4], golden["M_samples"][e, 2])
+            wb.upload_expert(l, e, wi, wg, wo)
+            wf.upload_expert(l, e, wi, wg, wo)
+        else:
+            _, l, r = item
+            assert np.array_equal(r, golden["M_router"])
+            wb.upload_router(l, r)
+            wf.upload_router(l, r)
+    x = golden["M_token"]
+    want = golden["M_out"]
+    for w, tol, name in ((wb, TOL_BF16, "bf16"), (wf, TOL_F32, "fp32")):
+        out, ids, gates = w.forward_host(x)
+        assert list(ids[0, 0]) == [1, 2]
+        cnt = np.bincount(ids[0, 0], minlength=8)
+        assert np.array_equal(cnt, golden["M_count"][0])
+        assert np.abs(gates[0, 0] - golden["M_gate"][0, [1, 2]]).max() < 1e-6
+        err = normwise(out - x, want - x)
+        print(f"M: {name} GPU vs the reference's model_forward: {err:.3e}")
+        assert err < tol
+    wb.close()
+    wf.close()
+
+
+# ---------------------------------------------------------------------------
+def _linked(world, s, dtype, mode, libopts, kernel, max_tokens=0):
+    b = _bench()
+    ctxs = [M.Ctx(0) for _ in range(world)]
+    M.Ctx.link_peers(ctxs, s.hidden_dim, max_tokens=max_tokens)
+    libopts(stack=0 if kernel == "layer" else 1, stack_grid=ctxs[0].sm_count // world)
+    owner = b.shard_map(s.num_layers, s.experts_per_layer, world) if mode == "ep" else None
+    ws = [M.Weights(c, s, dtype, owner=owner) if mode == "ep" else M.Weights(c, s, dtype, tp=True)
+          for c in ctxs]
+    return ctxs, ws, owner
+
+
+@pytest.mark.parametrize("kernel", ["stack", "layer"])
+@pytest.mark.parametrize("mode", ["ep", "tp"])
+@pytest.mark.parametrize("world,shape,dtype,tol", [
+    (2, (3, 8, 2, 512, 1792, 4), M.DTYPE_F32, 1e-5),
+    (4, (3, 8, 2, 512, 1792, 4), M.DTYPE_F32, 1e-5),
+    (2, (2, 8, 2, 4096, 14336, 2), M.DTYPE_BF16, 1e-4),
+])
+def test_sharded_decode_vs_oracle(ctx, orc, libopts, kernel, mode, world, shape, dtype, tol):
+    """Batch-1 decode sharded over linked ranks on one GPU (the fused peer
+    exchange): every rank's routing record equals the oracle's gate_topk at
+    every layer, and the output equals the oracle's L-layer chain (fp64, on
+    the ranks' device-held weights: EP from the owners, TP assembled from
+    every rank's ffn slice).  fp32 mode 1e-5; bf16 1e-4 (exact bf16 weights,
+    fp32 arithmetic)."""
+    L, E, k, d = shape[0], shape[1], shape[2], shape[3]
+    s = M.Shape(*shape)
+    ctxs, ws, owner = _linked(world, s, dtype, mode, libopts, kernel)
+    for w in ws:
+        w.random(17)
+        w.reserve(1)
+    torch.cuda.synchronize()
+    x0 = f32(np.random.RandomState(3).randn(d) * (0.1 if d > 1000 else 1.0))
+    xs = [torch.tensor(x0[None], dtype=torch.float32, device="cuda") for _ in range(world)]
+    idss = [torch.zeros((L, 1, k), dtype=torch.int32, device="cuda") for _ in range(world)]
+    gs = [torch.zeros((L, 1, k), device="cuda") for _ in range(world)]
+    for r in range(world):
+        ws[r].forward(xs[r], idss[r], gs[r], stream=ctxs[r].stream)
+    for c in ctxs:
+        c.synchronize()
+        c.peer_check()
+    out = xs[0].cpu().numpy()[0].astype(np.float64)
+    ids_g = idss[0].cpu().numpy()[:, 0]
+    for r in range(1, world):
+        assert np.array_equal(xs[r].cpu().numpy(), xs[0].cpu().numpy())
+    # the oracle's chain on the device-held weights
+    x = x0.copy()
+    for l in range(L):
+        oid, og, _, marg = oracle_route(orc, ws[0].download_router(l), x, k)
+        if marg[0] > MARGIN:
+            assert list(ids_g[l]) == list(oid[0]), f"layer {l}"
+        x = x + oracle_deltas(orc, lambda e: assemble_expert(ws, l, e, mode, owner), x[None], oid, og)[0]
+    err = normwise(out - x0, x - x0)
+    print(f"{mode}{world} {kernel} {shape[3]}: sharded decode vs oracle chain {err:.3e}")
+    assert err < tol
+    for w in ws:
+        w.close()
+    for c in ctxs:
+        c.close()
+
+
+@pytest.mark.parametrize("mode", ["ep", "tp"])
+@pytest.mark.parametrize("world,shape,dtype,n_tok,tol", [
+    (2, (1, 8, 2, 256, 1024, 2), M.DTYPE_BF16, 96, TOL_BF16),   # tcgen05 prefill per rank
+    (4, (1, 8, 2, 48, 80, 4), M.DTYPE_F32, 5, TOL_F32),         # generic kernels
+])
+def test_sharded_prefill_vs_oracle(ctx, orc, libopts, mode, world, shape, dtype, n_tok, tol):
+    """Multi-token layers sharded over linked ranks (peer reduce-scatter +
+    all-gather combine): every token's ids and output against the oracle on
+    the ranks' device-held weights."""
+    L, E, k, d = shape[0], shape[1], shape[2], shape[3]
+    s = M.Shape(*shape)
+    ctxs, ws, owner = _linked(world, s, dtype, mode, libopts, "layer", max_tokens=n_tok)
+    for w in ws:
+        w.random(19)
+        w.reserve(n_tok)
+    x = torch.randn(n_tok, d, device="cuda", generator=torch.Generator(device="cuda").manual_seed(2))
+    outs = [torch.empty_like(x) for _ in range(world)]
+    idss = [torch.zeros((n_tok, k), dtype=torch.int32, device="cuda") for _ in range(world)]
+    gs = [torch.zeros((n_tok, k), device="cuda") for _ in range(world)]
+    torch.cuda.synchronize()
+    for r in range(world):
+        ws[r].layer_forward(0, x, outs[r], idss[r], gs[r], stream=ctxs[r].stream)
+    for c in ctxs:
+        c.synchronize()
+        c.peer_check()
+    xh = x.cpu().numpy().astype(np.float64)
+    oid, og, _, marg = oracle_route(orc, ws[0].download_router(0), xh, k)
+    ok = marg > MARGIN
+    ids_g = idss[0].cpu().numpy()
+    assert np.array_equal(ids_g[ok], oid[ok])
+    delta = oracle_deltas(orc, lambda e: assemble_expert(ws, 0, e, mode, owner), xh[ok], oid[ok], og[ok])
+    got = outs[0].cpu().numpy().astype(np.float64)[ok] - xh[ok]
+    err = max(normwise(got[i], delta[i]) for i in range(len(delta)))
+    print(f"{mode}{world} prefill {n_tok} tokens vs oracle: {err:.3e}")
+    assert err < tol
+    for w in ws:
+        w.close()
+    for c in ctxs:
+        c.close()

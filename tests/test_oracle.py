@@ -216,3 +216,31 @@ def test_oracle_matches_live_reference_random_shapes(orc):
         out_r = ref.model_forward(s, wr, toks)
         assert np.array_equal(out_o[0], out_r[0])
         assert np.array_equal(out_o[1], out_r[1])
+
+
+def test_random_model_stream_equals_random_model(orc):
+    """The streamed random_model (one expert at a time, used to upload the
+    reference's Mixtral layer to the GPU) draws exactly random_model's values."""
+    sh = O.Shape(2, 4, 2, 16, 24, 2)
+    w = orc.random_model(sh, 5)
+    n = 0
+    for it in orc.random_model_stream(sh, 5):
+        if it[0] == "expert":
+            _, l, e, a, b, c = it
+            wa, wb, wc = w.expert(l, e)
+            assert np.array_equal(a, wa) and np.array_equal(b, wb) and np.array_equal(c, wc)
+        else:
+            _, l, r = it
+            assert np.array_equal(r, w.router[l])
+        n += 1
+    assert n == 2 * 4 + 2
+
+
+def test_expert_ffn_batch_is_bitwise_expert_ffn(orc):
+    rs = np.random.RandomState(1)
+    for d, f, n in [(3, 5, 1), (16, 24, 7), (64, 32, 3)]:
+        wi, wg, wo = rs.randn(f, d), rs.randn(f, d), rs.randn(d, f)
+        X = rs.randn(n, d)
+        Y = orc.expert_ffn_batch(wi, wg, wo, X)
+        for t in range(n):
+            assert np.array_equal(Y[t], orc.expert_ffn(wi, wg, wo, X[t]))

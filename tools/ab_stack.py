@@ -61,14 +61,14 @@ def main():
     res["normwise_delta_err"] = float(np.abs((x2 - xin) - (x1 - xin)).max() / np.abs(x1 - xin).max())
     res["gates_maxdiff"] = float(np.abs(g1 - g2).max())
     # timing, alternating
-    cfgs = [int(c) for c in args.configs.split(",")]
+    cfgs = [(int(c),) for c in args.configs.split(",")]
     times = {c: [] for c in cfgs}
     x = x0.clone()
     ids = torch.zeros((L, 1, 2), dtype=torch.int32, device="cuda")
     g = torch.zeros((L, 1, 2), device="cuda")
     for r in range(args.rounds):
         for cfg in cfgs:
-            M.set_option("stack_kernel", cfg)
+            M.set_option("stack_kernel", cfg[0])
             for _ in range(3):
                 w.forward(x, ids, g, stream=sp)
             torch.cuda.synchronize()
@@ -81,7 +81,7 @@ def main():
             times[cfg].append(e0.elapsed_time(e1) / args.iters)
     for cfg in cfgs:
         ms = float(np.median(times[cfg]))
-        tag = "k%d" % cfg
+        tag = "k" + "_".join(str(v) for v in cfg)
         res[f"{tag}_ms"] = round(ms, 4)
         res[f"{tag}_tok_s"] = round(1000 / ms, 2)
         res[f"{tag}_gbs"] = round(L * (2 * 3 * d * args.f * 2 + 8 * d * 4) / (ms * 1e-3) / 1e9, 1)
