@@ -195,7 +195,13 @@ struct moe_weights {
   // key: (x, ids, gates, host buffer, stack kernel option)
   std::map<std::tuple<float*, int32_t*, float*, cudaStream_t, int>, GraphEntry> graphs;
   cudaStream_t cap_stream = nullptr;  // private stream for graph capture
+  cudaStream_t io_stream = nullptr;   // host-buffer entry points (moe_forward_host)
   cudaEvent_t io_ev[kIoChunks] = {};  // host-buffer API: per-chunk D2H completion
+  // Cross-stream ordering of the scratch above: a call on stream s waits for
+  // the last call's work (on another stream) through order_ev, then records
+  // it (StreamOrder).  w->mu only serialises the enqueueing.
+  cudaStream_t last_stream = nullptr;
+  cudaEvent_t order_ev = nullptr;
   std::mutex mu;
 
   int L() const { return shape.num_layers; }
@@ -230,6 +236,34 @@ struct moe_weights {
 namespace {
 
 cudaStream_t pick(moe_ctx* c, void* s) { return s ? static_cast<cudaStream_t>(s) : c->stream; }
+
+// Orders one call's work on stream s after the previous call on these weights
+// (whatever stream that was) and records it for the next: the scratch, the
+// persistent kernels' barrier words and the captured graphs are per-weights,
+// so calls on different streams must not overlap on the device.  Held under
+// w->mu.  A stream the caller is capturing into a graph is not ordered
+// against work outside the capture (CUDA forbids that wait); it follows the
+// caller's own graph order.
+struct StreamOrder {
+  moe_weights* w;
+  cudaStream_t s;
+  bool capturing = false;
+  StreamOrder(moe_weights* w_, cudaStream_t s_) : w(w_), s(s_) {
+    cudaStreamCaptureStatus st = cudaStreamCaptureStatusNone;
+    if (cudaStreamIsCapturing(s, &st) != cudaSuccess) cudaGetLastError();
+    capturing = st != cudaStreamCaptureStatusNone;
+    if (capturing) return;
+    if (!w->order_ev && cudaEventCreateWithFlags(&w->order_ev, cudaEventDisableTiming) != cudaSuccess) {
+      cudaGetLastError();
+      w->order_ev = nullptr;
+    }
+    if (w->order_ev && w->last_stream && w->last_stream != s) cudaStreamWaitEvent(s, w->order_ev, 0);
+  }
+  ~StreamOrder() {
+    if (capturing || !w->order_ev) return;
+    if (cudaEventRecord(w->order_ev, s) == cudaSuccess) w->last_stream = s;
+  }
+};
 
 int check_shape(const moe_shape* s) {
   if (!s) return fail(MOE_ERR_ARG, "null shape");
@@ -974,8 +1008,9 @@ static int weights_create(moe_ctx* c, const moe_shape* shape, int dtype,
         return cleanup(fail(MOE_ERR_CUDA, "upload projection table"));
     }
   }
-  if (cudaStreamCreateWithFlags(&w->cap_stream, cudaStreamNonBlocking) != cudaSuccess)
-    return cleanup(fail(MOE_ERR_CUDA, "create capture stream"));
+  if (cudaStreamCreateWithFlags(&w->cap_stream, cudaStreamNonBlocking) != cudaSuccess ||
+      cudaStreamCreateWithFlags(&w->io_stream, cudaStreamNonBlocking) != cudaSuccess)
+    return cleanup(fail(MOE_ERR_CUDA, "create streams"));
   w->stack_enabled = moe::debug_options().stack != 0;
   if (w->rw_enabled && !c->ep() && moe::stack2_supported(w->plan, w->dims())) {
     if (w->stack_acc.ensure(moe::stack2_acc_bytes(w->dims())))  // zeroed: the kernel's invariant
@@ -1103,6 +1138,8 @@ int moe_weights_destroy(moe_weights* w) {
   for (auto& kv : w->graphs)
     if (kv.second.exec) cudaGraphExecDestroy(kv.second.exec);
   if (w->cap_stream) cudaStreamDestroy(w->cap_stream);
+  if (w->io_stream) cudaStreamDestroy(w->io_stream);
+  if (w->order_ev) cudaEventDestroy(w->order_ev);
   for (DevBuf& b : w->rw_mem) b.release();
   w->dev_rw.release();
   for (void* p : w->layer_mem)
@@ -1299,10 +1336,12 @@ int moe_routing_trace_step(moe_ctx* c, const int32_t* ids, const float* gates, i
   TRY(set_device(c));
   const size_t le = (size_t)n_layers * n_experts;
   if (le == 0) return MOE_OK;
+  // [counts int32, padded to 8 B][gate sums fp64]
+  const size_t dg_off = (le * 4 + 7) & ~(size_t)7;
   void* buf = nullptr;
-  CU(cudaMallocAsync(&buf, le * 12, c->stream));
+  CU(cudaMallocAsync(&buf, dg_off + le * 8, c->stream));
   int32_t* dc = static_cast<int32_t*>(buf);
-  double* dg = reinterpret_cast<double*>(static_cast<char*>(buf) + le * 4 + (le % 2) * 4);
+  double* dg = reinterpret_cast<double*>(static_cast<char*>(buf) + dg_off);
   cudaError_t e = moe::launch_trace_step(ids, gates, n_layers, n_tok, top_k, n_experts, dc, dg,
                                          c->stream);
   if (e == cudaSuccess)
@@ -1327,8 +1366,9 @@ int moe_experts_forward(moe_weights* w, int layer, const float* x, int n_tok, co
   std::lock_guard<std::mutex> lk(w->mu);
   TRY(set_device(w->ctx));
   TRY(ensure_scratch(w, n_tok));
-  return experts_forward(w, layer, x, n_tok, ids, gates, x_out, post_silu, pick(w->ctx, stream),
-                         false, nullptr, nullptr, nullptr);
+  StreamOrder so(w, pick(w->ctx, stream));
+  return experts_forward(w, layer, x, n_tok, ids, gates, x_out, post_silu, so.s, false, nullptr,
+                         nullptr, nullptr);
 }
 
 int moe_decode_experts_partial(moe_weights* w, int layer, const float* x, const int32_t* ids,
@@ -1351,7 +1391,8 @@ int moe_layer_forward(moe_weights* w, int layer, const float* x, float* x_out, i
   std::lock_guard<std::mutex> lk(w->mu);
   TRY(set_device(w->ctx));
   TRY(ensure_scratch(w, n_tok));
-  cudaStream_t s = pick(w->ctx, stream);
+  StreamOrder so(w, pick(w->ctx, stream));
+  cudaStream_t s = so.s;
   CU(moe::launch_router_topk(w->router + (size_t)layer * w->E() * w->d(), x, n_tok, w->dims(), ids,
                              gates, s, false));
   return experts_forward(w, layer, x, n_tok, ids, gates, x_out, nullptr, s, true, nullptr, nullptr,
@@ -1366,9 +1407,10 @@ int moe_forward(moe_weights* w, float* x, int n_tok, int32_t* ids, float* gates,
   std::lock_guard<std::mutex> lk(w->mu);
   TRY(set_device(w->ctx));
   TRY(ensure_scratch(w, n_tok));
-  cudaStream_t s = pick(w->ctx, stream);
+  TRY(refresh_projection(w));
+  StreamOrder so(w, pick(w->ctx, stream));
+  cudaStream_t s = so.s;
   if (n_tok == 1 && w->plan.ok) {
-    TRY(refresh_projection(w));
     return forward_graph(w, x, ids, gates, s);
   }
   return enqueue_forward(w, x, n_tok, ids, gates, s, nullptr);
@@ -1393,7 +1435,11 @@ int moe_forward_sparsity(moe_weights* w, float* x, int n_tok, int32_t* ids, floa
   w->sp.counts = reinterpret_cast<unsigned long long*>(counts);
   w->sp.n = n_thresholds;
   for (int i = 0; i < n_thresholds; ++i) w->sp.thr[i] = (float)thresholds[i];
-  const int rc = enqueue_forward(w, x, n_tok, ids, gates, pick(w->ctx, stream), nullptr);
+  int rc;
+  {
+    StreamOrder so(w, pick(w->ctx, stream));
+    rc = enqueue_forward(w, x, n_tok, ids, gates, so.s, nullptr);
+  }
   w->sp = moe::SparsityCounters();
   return rc;
 }
@@ -1412,7 +1458,9 @@ int moe_forward_host(moe_weights* w, const double* tokens, int n_tok, double* ou
   std::lock_guard<std::mutex> lk(w->mu);
   TRY(set_device(w->ctx));
   TRY(ensure_scratch(w, n_tok));
-  cudaStream_t s = w->ctx->stream;
+  TRY(refresh_projection(w));
+  StreamOrder so(w, w->io_stream);
+  cudaStream_t s = so.s;
   const size_t nx = (size_t)n_tok * d, nr = (size_t)L * n_tok * k;
   if (post_silu && w->tp > 1)
     return fail(MOE_ERR_UNSUPPORTED, "post-SiLU capture of a tensor-parallel shard");
@@ -1604,7 +1652,8 @@ int moe_forward_logits(moe_weights* w, float* x, int32_t* ids, float* gates, flo
   TRY(set_device(w->ctx));
   TRY(ensure_scratch(w, 1));
   TRY(refresh_projection(w));
-  return enqueue_stack(w, x, ids, gates, pick(w->ctx, stream), nullptr, logits);
+  StreamOrder so(w, pick(w->ctx, stream));
+  return enqueue_stack(w, x, ids, gates, so.s, nullptr, logits);
 }
 
 int moe_forward_launches(moe_weights* w, int n_tok) {

@@ -154,8 +154,8 @@ __device__ __forceinline__ void named_bar_sync(int id, int nthreads) {
 // rounds of a warp argmax with (logit desc, id asc) ordering, ids emitted
 // ascending, softmax over the selected logits with the denominator summed
 // sequentially in ascending-id order.  Called by all 32 lanes of one warp;
-// logits in shared/global memory, E <= 256, k <= 32.  Lanes j < k write
-// ids[j] / gates[j].
+// logits in shared/global memory, E <= 256, any k <= E (k <= 32 when E <=
+// 32).  Slot j is written by lane j % 32.
 __device__ __forceinline__ void warp_topk_softmax(const float* logits, int E, int k,
                                                   int32_t* ids, float* gates) {
   const int lane = threadIdx.x & 31;
@@ -226,8 +226,6 @@ __device__ __forceinline__ void warp_topk_softmax(const float* logits, int E, in
   }
   // emit ids ascending: block i of 32 experts in lane order
   int base = 0;
-  int my_id = -1;
-  float my_logit = 0.f;
 #pragma unroll
   for (int i = 0; i < 8; ++i) {
     const unsigned m = __ballot_sync(MOE_FULL_MASK, (taken >> i) & 1u);
@@ -238,17 +236,16 @@ __device__ __forceinline__ void warp_topk_softmax(const float* logits, int E, in
     base += __popc(m);
   }
   __syncwarp();
-  if (lane < k) {
-    my_id = ids[lane];
-    my_logit = logits[my_id];
-  }
-  float mx = lane < k ? my_logit : -INFINITY;
+  // any k <= E: slots j = lane, lane+32, ... (k > 32 is legal in the
+  // reference, model.cpp:77); the denominator is the same ascending-id
+  // sequential sum in every lane
+  float mx = -INFINITY;
+  for (int j = lane; j < k; j += 32) mx = fmaxf(mx, logits[ids[j]]);
 #pragma unroll
   for (int s = 16; s >= 1; s >>= 1) mx = fmaxf(mx, __shfl_xor_sync(MOE_FULL_MASK, mx, s));
-  const float w = lane < k ? expf(my_logit - mx) : 0.f;
   float denom = 0.f;
-  for (int j = 0; j < k; ++j) denom += __shfl_sync(MOE_FULL_MASK, w, j);
-  if (lane < k) gates[lane] = w / denom;
+  for (int j = 0; j < k; ++j) denom += expf(logits[ids[j]] - mx);
+  for (int j = lane; j < k; j += 32) gates[j] = expf(logits[ids[j]] - mx) / denom;
   __syncwarp();
 }
 

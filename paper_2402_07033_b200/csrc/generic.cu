@@ -34,8 +34,11 @@ static cudaLaunchConfig_t make_cfg(dim3 grid, dim3 block, cudaStream_t s, bool p
 // bounds it).  Per (token, expert) the summation order is fixed — per-thread
 // chain in ascending c, warp butterfly, then the 8 warp partials in warp
 // order — and does not depend on n_tok or the token's slot in the block, so
-// every caller (batch-1 decode, prefill, any chunking) routes a token bit for
-// bit identically.
+// every caller of this kernel (the per-layer batch-1 path, prefill, any
+// chunking) routes a token bit for bit identically.  The persistent stack
+// kernels (decode.cu) assemble their logits with their own reductions (a
+// different fp32 summation order); their routing is checked against the
+// oracle directly (tests/test_gpu_parity_full.py, every layer of the stack).
 constexpr int kRouterTok = 4;
 __global__ void __launch_bounds__(256) router_topk_kernel(const float* __restrict__ router,
                                                           const float* __restrict__ x, int n_tok,

@@ -9,8 +9,12 @@
 // 107-109), an out-of-range router layer (:73-74) or top_k (:77).
 #include <cstdlib>
 #include <cstring>
+#include <algorithm>
+#include <atomic>
 #include <list>
+#include <memory>
 #include <mutex>
+#include <thread>
 #include <stdexcept>
 #include <string>
 #include <vector>
@@ -34,14 +38,26 @@ void check(int rc) {
   if (rc != MOE_OK) raise(rc);
 }
 
+// One device copy of a ModelWeights.  Shared by the cache and every call
+// using it, so evicting an entry never frees weights a concurrent call is
+// still running on (the last holder destroys them).
+using WeightsRef = std::shared_ptr<moe_weights>;
+
 struct CachedWeights {
   const ModelWeights* addr = nullptr;
-  std::uint64_t fingerprint = 0;
+  std::uint64_t digest = 0;
   ModelShape shape;
   int dtype = MOE_DTYPE_F32;
-  moe_weights* w = nullptr;
+  WeightsRef w;
 };
 
+// Reentrancy (simulator.cpp:216-223 calls from std::async
+// threads): `mu` guards only the context, the dtype and the cache.  A call
+// holds it while looking up / uploading its weights, then releases it; the
+// GPU work runs under the weights' own lock (moe_forward_host), so calls on
+// different weights proceed concurrently and calls on the same weights
+// queue on it (batch-1 decode is HBM-bound: two at once would only share
+// the bandwidth).
 struct Device {
   std::mutex mu;
   int device = -1;
@@ -59,10 +75,7 @@ struct Device {
     check(moe_ctx_create(device, &ctx));
     return ctx;
   }
-  void clear() {
-    for (auto& c : cache) moe_weights_destroy(c.w);
-    cache.clear();
-  }
+  void clear() { cache.clear(); }
 };
 
 Device& dev() {
@@ -77,19 +90,67 @@ std::uint64_t mix(std::uint64_t h, std::uint64_t v) {
   return h;
 }
 
-std::uint64_t fingerprint(const Matrix& m, bool full) {
-  std::uint64_t h = mix(static_cast<std::uint64_t>(m.rows), static_cast<std::uint64_t>(m.cols));
+// Digest of EVERY element of a matrix (bit patterns, so -0.0 != 0.0 and NaN
+// payloads count): four independent multiply-rotate lanes, memory-bound.  A
+// sampled fingerprint would reuse stale device weights after an in-place
+// edit at an unsampled position; the reference recomputes from the host
+// weights on every call, so the cache may only hit on identical contents.
+std::uint64_t digest(const Matrix& m) {
+  constexpr std::uint64_t P1 = 0x9E3779B185EBCA87ULL, P2 = 0xC2B2AE3D27D4EB4FULL;
+  auto round = [](std::uint64_t acc, std::uint64_t v) {
+    acc += v * P2;
+    acc = (acc << 31) | (acc >> 33);
+    return acc * P1;
+  };
+  std::uint64_t a[4] = {P1 + P2, P2, 0, 0 - P1};
   const size_t n = m.data.size();
-  if (n == 0) return h;
-  const size_t step = full ? 1 : std::max<size_t>(1, n / 61);
-  for (size_t i = 0; i < n; i += step) {
-    std::uint64_t bits;
-    std::memcpy(&bits, &m.data[i], 8);
-    h = mix(h, bits);
+  const double* p = m.data.data();
+  size_t i = 0;
+  for (; i + 4 <= n; i += 4)
+    for (int j = 0; j < 4; ++j) {
+      std::uint64_t v;
+      std::memcpy(&v, p + i + j, 8);
+      a[j] = round(a[j], v);
+    }
+  std::uint64_t h = mix(static_cast<std::uint64_t>(m.rows), static_cast<std::uint64_t>(m.cols));
+  for (; i < n; ++i) {
+    std::uint64_t v;
+    std::memcpy(&v, p + i, 8);
+    h = mix(h, round(0, v));
   }
-  std::uint64_t last;
-  std::memcpy(&last, &m.data[n - 1], 8);
-  return mix(h, last);
+  for (int j = 0; j < 4; ++j) h = mix(h, a[j]);
+  return h;
+}
+
+// Digest of the whole model: one digest per matrix, computed on up to
+// hardware_concurrency threads (a Mixtral layer is 11.3 GB of fp64), then
+// combined in a fixed order.
+std::uint64_t model_digest(const ModelShape& shape, const ModelWeights& weights) {
+  const int L = shape.num_layers, E = shape.experts_per_layer;
+  std::vector<const Matrix*> mats;
+  for (int l = 0; l < L; ++l) {
+    mats.push_back(&weights.router.layers[l]);
+    for (int e = 0; e < E; ++e) {
+      const ExpertWeights& ew = weights.experts[l][e];
+      mats.insert(mats.end(), {&ew.w_in, &ew.w_gate, &ew.w_out});
+    }
+  }
+  std::vector<std::uint64_t> dg(mats.size());
+  size_t total = 0;
+  for (const Matrix* m : mats) total += m->data.size();
+  const unsigned hw = std::max(1u, std::thread::hardware_concurrency());
+  const unsigned nth = total < (size_t(1) << 20) ? 1u : std::min<unsigned>(hw, static_cast<unsigned>(mats.size()));
+  std::atomic<size_t> next{0};
+  auto work = [&] {
+    for (size_t i; (i = next.fetch_add(1)) < mats.size();) dg[i] = digest(*mats[i]);
+  };
+  std::vector<std::thread> pool;
+  for (unsigned t = 1; t < nth; ++t) pool.emplace_back(work);
+  work();
+  for (auto& t : pool) t.join();
+  std::uint64_t h = mix(static_cast<std::uint64_t>(L), static_cast<std::uint64_t>(E));
+  for (std::uint64_t v : dg) h = mix(h, v);
+  return h;
 }
 
 void check_expert(const ExpertWeights& w) {
@@ -103,20 +164,22 @@ moe_shape to_c(const ModelShape& s) {
                    s.bytes_per_param};
 }
 
-// Device copy of `weights` (uploaded once, cached by address + fingerprint).
-moe_weights* device_weights(const ModelShape& shape, const ModelWeights& weights) {
+WeightsRef adopt(moe_weights* w) {
+  return WeightsRef(w, [](moe_weights* p) { moe_weights_destroy(p); });
+}
+
+// Device copy of `weights`: reused when the address, shape, dtype and the
+// digest of every element match an entry; uploaded otherwise.
+WeightsRef device_weights(const ModelShape& shape, const ModelWeights& weights) {
   Device& D = dev();
   const int L = shape.num_layers, E = shape.experts_per_layer;
   const int d = shape.hidden_dim, f = shape.ffn_dim;
   if (static_cast<int>(weights.experts.size()) < L ||
       static_cast<int>(weights.router.layers.size()) < L)
     throw ShapeError("model weights have fewer layers than the shape");
-  const bool full = static_cast<std::int64_t>(L) * E * 3 * d * f < (std::int64_t(1) << 22);
-  std::uint64_t fp = mix(static_cast<std::uint64_t>(L), static_cast<std::uint64_t>(E));
   for (int l = 0; l < L; ++l) {
     const Matrix& r = weights.router.layers[l];
     if (r.rows != E || r.cols != d) throw ShapeError("matrix-vector dimension mismatch");
-    fp = mix(fp, fingerprint(r, full));
     if (static_cast<int>(weights.experts[l].size()) < E)
       throw ShapeError("model weights have fewer experts than the shape");
     for (int e = 0; e < E; ++e) {
@@ -124,14 +187,13 @@ moe_weights* device_weights(const ModelShape& shape, const ModelWeights& weights
       check_expert(ew);
       if (ew.w_in.cols != d || ew.w_in.rows != f)
         throw ShapeError("matrix-vector dimension mismatch");
-      fp = mix(fp, fingerprint(ew.w_in, full));
-      fp = mix(fp, fingerprint(ew.w_gate, full));
-      fp = mix(fp, fingerprint(ew.w_out, full));
     }
   }
+  const std::uint64_t dgst = model_digest(shape, weights);  // outside the lock
+  std::lock_guard<std::mutex> lk(D.mu);
   const int dt = dtype_code();
   for (auto it = D.cache.begin(); it != D.cache.end(); ++it) {
-    if (it->addr == &weights && it->fingerprint == fp && it->dtype == dt &&
+    if (it->addr == &weights && it->digest == dgst && it->dtype == dt &&
         it->shape.num_layers == L && it->shape.experts_per_layer == E &&
         it->shape.top_k == shape.top_k && it->shape.hidden_dim == d && it->shape.ffn_dim == f) {
       D.cache.splice(D.cache.begin(), D.cache, it);
@@ -139,30 +201,28 @@ moe_weights* device_weights(const ModelShape& shape, const ModelWeights& weights
     }
   }
   moe_shape cs = to_c(shape);
-  moe_weights* w = nullptr;
-  check(moe_weights_create(D.context(), &cs, dt, nullptr, &w));
+  moe_weights* raw = nullptr;
+  check(moe_weights_create(D.context(), &cs, dt, nullptr, &raw));
+  WeightsRef w = adopt(raw);
   for (int l = 0; l < L; ++l) {
     for (int e = 0; e < E; ++e) {
       const ExpertWeights& ew = weights.experts[l][e];
-      const int rc = moe_weights_upload_expert(w, l, e, ew.w_in.data.data(), ew.w_gate.data.data(),
-                                               ew.w_out.data.data());
-      if (rc != MOE_OK) {
-        moe_weights_destroy(w);
-        raise(rc);
-      }
+      check(moe_weights_upload_expert(raw, l, e, ew.w_in.data.data(), ew.w_gate.data.data(),
+                                      ew.w_out.data.data()));
     }
-    const int rc = moe_weights_upload_router(w, l, weights.router.layers[l].data.data());
-    if (rc != MOE_OK) {
-      moe_weights_destroy(w);
-      raise(rc);
-    }
+    check(moe_weights_upload_router(raw, l, weights.router.layers[l].data.data()));
   }
-  D.cache.push_front(CachedWeights{&weights, fp, shape, dt, w});
-  while (D.cache.size() > Device::kCacheEntries) {
-    moe_weights_destroy(D.cache.back().w);
-    D.cache.pop_back();
-  }
+  // an entry for the same address with other contents is stale: replace it
+  D.cache.remove_if([&](const CachedWeights& c) { return c.addr == &weights; });
+  D.cache.push_front(CachedWeights{&weights, dgst, shape, dt, w});
+  while (D.cache.size() > Device::kCacheEntries) D.cache.pop_back();
   return w;
+}
+
+moe_ctx* shared_context() {
+  Device& D = dev();
+  std::lock_guard<std::mutex> lk(D.mu);
+  return D.context();
 }
 
 }  // namespace
@@ -171,11 +231,9 @@ std::vector<double> expert_ffn(const ExpertWeights& weights, const std::vector<d
   check_expert(weights);
   if (static_cast<int>(x.size()) != weights.w_in.cols)
     throw ShapeError("matrix-vector dimension mismatch");
-  Device& D = dev();
-  std::lock_guard<std::mutex> lk(D.mu);
   std::vector<double> y(weights.w_out.rows, 0.0);
   if (weights.w_in.rows == 0 || weights.w_in.cols == 0) return y;
-  check(moe_expert_ffn_host(D.context(), dtype_code(), weights.w_in.cols, weights.w_in.rows,
+  check(moe_expert_ffn_host(shared_context(), dtype_code(), weights.w_in.cols, weights.w_in.rows,
                             weights.w_in.data.data(), weights.w_gate.data.data(),
                             weights.w_out.data.data(), x.data(), y.data()));
   return y;
@@ -188,11 +246,9 @@ std::vector<std::pair<int, double>> gate_topk(const RouterWeights& router, int l
   const Matrix& r = router.layers[layer];
   if (static_cast<int>(x.size()) != r.cols) throw ShapeError("matrix-vector dimension mismatch");
   if (top_k < 1 || top_k > r.rows) throw ShapeError("top_k out of range");
-  Device& D = dev();
-  std::lock_guard<std::mutex> lk(D.mu);
   std::vector<int32_t> ids(top_k);
   std::vector<double> g(top_k);
-  check(moe_gate_topk_host(D.context(), r.rows, r.cols, r.data.data(), x.data(), top_k,
+  check(moe_gate_topk_host(shared_context(), r.rows, r.cols, r.data.data(), x.data(), top_k,
                            ids.data(), g.data()));
   std::vector<std::pair<int, double>> out;
   out.reserve(top_k);
@@ -214,16 +270,14 @@ ForwardResult model_forward(const ModelShape& shape, const ModelWeights& weights
   const int d = shape.hidden_dim, k = shape.top_k, E = shape.experts_per_layer;
   const int f = shape.ffn_dim;
 
-  Device& D = dev();
-  std::lock_guard<std::mutex> lk(D.mu);
-  moe_weights* w = device_weights(shape, weights);
+  const WeightsRef w = device_weights(shape, weights);
   std::vector<double> flat(static_cast<size_t>(n) * d), out(flat.size());
   for (int t = 0; t < n; ++t) std::memcpy(&flat[static_cast<size_t>(t) * d], tokens[t].data(), 8 * d);
   std::vector<int32_t> ids(static_cast<size_t>(L) * n * k);
   std::vector<double> gates(ids.size());
   std::vector<double> post;
   if (sink) post.resize(static_cast<size_t>(n) * L * k * f);
-  check(moe_forward_host(w, flat.data(), n, out.data(), ids.data(), gates.data(),
+  check(moe_forward_host(w.get(), flat.data(), n, out.data(), ids.data(), gates.data(),
                          sink ? post.data() : nullptr));
   for (int t = 0; t < n; ++t)
     std::memcpy(result.outputs[t].data(), &out[static_cast<size_t>(t) * d], 8 * d);

@@ -138,7 +138,7 @@ struct Json {
     return false;
   }
   void expect(char c) {
-    if (!eat(c)) throw ValidationError(std::string("trace JSONL: expected '") + c + "'");
+    if (!eat(c)) throw ValidationError(std::string("expected '") + c + "'");
   }
   std::string str() {
     expect('"');
@@ -147,17 +147,35 @@ struct Json {
     expect('"');
     return out;
   }
+  // JSON number grammar only (RFC 8259 §6): -?(0|[1-9][0-9]*)(.[0-9]+)?([eE][+-]?[0-9]+)?
+  // — no inf/nan, hex floats, leading '+' or bare '.5' (std::stod accepts them)
   double num() {
     ws();
-    size_t used = 0;
-    double v;
-    try {
-      v = std::stod(s.substr(i), &used);
-    } catch (const std::exception&) {
-      throw ValidationError("trace JSONL: malformed number");
+    const size_t b = i;
+    size_t p = i;
+    auto digits = [&] {
+      const size_t q = p;
+      while (p < s.size() && s[p] >= '0' && s[p] <= '9') ++p;
+      return p > q;
+    };
+    if (p < s.size() && s[p] == '-') ++p;
+    if (p < s.size() && s[p] == '0') ++p;
+    else if (!digits()) throw ValidationError("malformed number");
+    if (p < s.size() && s[p] == '.') {
+      ++p;
+      if (!digits()) throw ValidationError("malformed number");
     }
-    i += used;
-    return v;
+    if (p < s.size() && (s[p] == 'e' || s[p] == 'E')) {
+      ++p;
+      if (p < s.size() && (s[p] == '+' || s[p] == '-')) ++p;
+      if (!digits()) throw ValidationError("malformed number");
+    }
+    i = p;
+    return std::strtod(s.substr(b, p - b).c_str(), nullptr);
+  }
+  void end() {
+    ws();
+    if (i != s.size()) throw ValidationError("unexpected text after the JSON object");
   }
 };
 
@@ -194,49 +212,57 @@ void save_trace_jsonl(const RoutingTrace& trace, const std::string& path) {
 RoutingTrace load_trace_jsonl(std::istream& in, const ModelShape& shape) {
   RoutingTrace trace;
   std::string line;
+  size_t lineno = 0;
   while (std::getline(in, line)) {
+    ++lineno;
     if (line.find_first_not_of(" \t\r") == std::string::npos) continue;
-    Json j(line);
     TraceStep st;
-    bool have_kind = false, have_layers = false;
-    j.expect('{');
-    do {
-      const std::string key = j.str();
-      j.expect(':');
-      if (key == "kind") {
-        st.kind = step_kind_from_string(j.str());
-        have_kind = true;
-      } else if (key == "layers") {
-        j.expect('[');
-        if (!j.eat(']')) {
-          do {
-            std::vector<Selection> sels;
-            j.expect('[');
-            if (!j.eat(']')) {
-              do {
-                j.expect('[');
-                Selection s;
-                s.expert = static_cast<int>(j.num());
-                j.expect(',');
-                s.token_count = static_cast<int>(j.num());
-                j.expect(',');
-                s.gate_weight = j.num();
+    // parse errors name the line, as the reference loader does (trace.cpp:116-124)
+    try {
+      Json j(line);
+      bool have_kind = false, have_layers = false;
+      j.expect('{');
+      do {
+        const std::string key = j.str();
+        j.expect(':');
+        if (key == "kind") {
+          st.kind = step_kind_from_string(j.str());
+          have_kind = true;
+        } else if (key == "layers") {
+          j.expect('[');
+          if (!j.eat(']')) {
+            do {
+              std::vector<Selection> sels;
+              j.expect('[');
+              if (!j.eat(']')) {
+                do {
+                  j.expect('[');
+                  Selection s;
+                  s.expert = static_cast<int>(j.num());
+                  j.expect(',');
+                  s.token_count = static_cast<int>(j.num());
+                  j.expect(',');
+                  s.gate_weight = j.num();
+                  j.expect(']');
+                  sels.push_back(s);
+                } while (j.eat(','));
                 j.expect(']');
-                sels.push_back(s);
-              } while (j.eat(','));
-              j.expect(']');
-            }
-            st.layers.push_back(std::move(sels));
-          } while (j.eat(','));
-          j.expect(']');
+              }
+              st.layers.push_back(std::move(sels));
+            } while (j.eat(','));
+            j.expect(']');
+          }
+          have_layers = true;
+        } else {
+          throw ValidationError("unknown key " + key);
         }
-        have_layers = true;
-      } else {
-        throw ValidationError("trace JSONL: unknown key " + key);
-      }
-    } while (j.eat(','));
-    j.expect('}');
-    if (!have_kind || !have_layers) throw ValidationError("trace JSONL: missing kind or layers");
+      } while (j.eat(','));
+      j.expect('}');
+      j.end();
+      if (!have_kind || !have_layers) throw ValidationError("missing kind or layers");
+    } catch (const ValidationError& e) {
+      throw ValidationError("trace line " + std::to_string(lineno) + ": " + e.what());
+    }
     trace.steps.push_back(std::move(st));
   }
   trace.validate(shape);

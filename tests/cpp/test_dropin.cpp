@@ -19,6 +19,7 @@
 #include <set>
 #include <sstream>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include "moe_orch/b200.hpp"
@@ -276,6 +277,32 @@ TEST("trace JSONL round trip", false) {
   CHECK(back == t);
   std::stringstream bad("{\"kind\":\"decode\",\"layers\":[[[0,1,0.5]]]}\n");
   CHECK_THROWS_AS(load_trace_jsonl(bad, shape), ValidationError);
+}
+
+// reference test_trace.cpp:59-68 ("loader rejects malformed JSON with line
+// number"), plus inputs nlohmann's parser rejects and std::stod would accept
+TEST("trace JSONL loader rejects malformed lines with the line number", false) {
+  const ModelShape shape = ModelShape::toy();
+  auto message = [&](const std::string& text) {
+    std::stringstream buf(text);
+    try {
+      load_trace_jsonl(buf, shape);
+    } catch (const ValidationError& e) {
+      return std::string(e.what());
+    }
+    return std::string("<accepted>");
+  };
+  CHECK(message("{not json}").find("line 1") != std::string::npos);
+  const std::string lay = "[[0,1,0.5],[1,1,0.5]]";
+  const std::string ok = "{\"kind\":\"decode\",\"layers\":[" + lay + "," + lay + "," + lay + "," + lay + "]}";
+  CHECK(message(ok + "\n") == "<accepted>");
+  CHECK(message(ok + "\n\n" + ok + " trailing\n").find("line 3") != std::string::npos);
+  CHECK(message("{\"kind\":\"decode\",\"layers\":[[[0,1,inf],[1,1,0.5]],[[0,1,0.5],[1,1,0.5]]]}")
+            .find("line 1") != std::string::npos);
+  CHECK(message("{\"kind\":\"decode\",\"layers\":[[[0,1,0x1p-1],[1,1,0.5]],[[0,1,0.5],[1,1,0.5]]]}")
+            .find("line 1") != std::string::npos);
+  CHECK(message("{\"kind\":\"decode\",\"layers\":[[[+0,1,0.5],[1,1,0.5]],[[0,1,0.5],[1,1,0.5]]]}")
+            .find("line 1") != std::string::npos);
 }
 
 TEST("profile_from_trace tallies token counts", false) {
@@ -589,6 +616,86 @@ TEST("bf16 device storage stays within 1e-2 of fp64", true) {
       b.push_back(f32.outputs[t][i] - tokens[t][i]);
     }
   CHECK(normwise(a, b) <= 1e-1);  // bf16 weights drift routing-free toy layers ~1e-2
+}
+
+// Reentrancy (the simulator calls from std::async threads,
+// simulator.cpp:216-223): concurrent model_forward calls on shared and on
+// distinct weights, batch 1 (persistent stack kernel) and multi-token, give
+// the serial results bit for bit.
+TEST("concurrent model_forward from 4 threads equals serial", true) {
+  ModelShape dec;  // batch-1 streaming shape (the persistent kernel path)
+  dec.num_layers = 3;
+  dec.experts_per_layer = 8;
+  dec.top_k = 2;
+  dec.hidden_dim = 256;
+  dec.ffn_dim = 512;
+  dec.bytes_per_param = 4;
+  const ModelShape toy = ModelShape::toy();
+  const ModelWeights m_dec = random_model(dec, 21), m_toy = random_model(toy, 22);
+  struct Job {
+    const ModelShape* shape;
+    const ModelWeights* model;
+    std::vector<std::vector<double>> tokens;
+    ForwardResult serial;
+  };
+  std::vector<Job> jobs;
+  for (int i = 0; i < 8; ++i) {
+    const bool d = i % 2 == 0;
+    const ModelShape& sh = d ? dec : toy;
+    jobs.push_back(Job{&sh, d ? &m_dec : &m_toy, normal_tokens(d ? 1 + (i % 3 == 0) * 5 : 4, sh.hidden_dim, 300 + i), {}});
+  }
+  for (Job& j : jobs) j.serial = model_forward(*j.shape, *j.model, j.tokens);
+  std::vector<int> mismatches(4, 0);
+  std::vector<std::string> errors(4);
+  std::vector<std::thread> threads;
+  for (int t = 0; t < 4; ++t)
+    threads.emplace_back([&, t] {
+      try {
+        for (int rep = 0; rep < 6; ++rep)
+          for (size_t i = t; i < jobs.size(); i += 2) {  // jobs shared by 2 threads each
+            const Job& j = jobs[(i + rep) % jobs.size()];
+            const ForwardResult r = model_forward(*j.shape, *j.model, j.tokens);
+            if (r.outputs != j.serial.outputs || r.trace != j.serial.trace) ++mismatches[t];
+          }
+      } catch (const std::exception& e) {
+        errors[t] = e.what();
+      }
+    });
+  for (auto& th : threads) th.join();
+  for (int t = 0; t < 4; ++t) {
+    CHECK(mismatches[t] == 0);
+    CHECK(errors[t].empty());
+  }
+}
+
+// The device copy is keyed by the contents of every element: an in-place
+// edit anywhere (here well away from any sampling grid, in a model above the
+// old 4M-parameter sampling threshold) gives fresh results, equal to those of
+// an independent copy of the edited weights.
+TEST("in-place weight edits at any element invalidate the device copy", true) {
+  ModelShape sh;
+  sh.num_layers = 1;
+  sh.experts_per_layer = 8;
+  sh.top_k = 2;
+  sh.hidden_dim = 256;
+  sh.ffn_dim = 1024;
+  sh.bytes_per_param = 4;
+  ModelWeights model = random_model(sh, 31);
+  const auto tokens = normal_tokens(1, sh.hidden_dim, 32);
+  const ForwardResult before = model_forward(sh, model, tokens);
+  const int e = before.trace.steps[0].layers[0][0].expert;
+  for (const size_t pos : {size_t(12345), size_t(200003)}) {
+    model.experts[0][e].w_out.data[pos % model.experts[0][e].w_out.data.size()] += 0.75;
+    const ForwardResult after = model_forward(sh, model, tokens);
+    const ModelWeights copy = model;  // a different address: uploaded on its own
+    const ForwardResult fresh = model_forward(sh, copy, tokens);
+    CHECK(after.outputs != before.outputs);
+    CHECK(after.outputs == fresh.outputs);
+  }
+  // router edits too
+  model.router.layers[0].data[777] += 3.0;
+  const ModelWeights copy = model;
+  CHECK(model_forward(sh, model, tokens).outputs == model_forward(sh, copy, tokens).outputs);
 }
 
 int main(int argc, char** argv) {

@@ -34,6 +34,47 @@ def test_library_contains_tma_bulk_copies():
     assert "SYNCS" in sass
 
 
+def _kernels():
+    import importlib.util
+
+    spec = importlib.util.spec_from_file_location(
+        "sass_summary", os.path.join(os.path.dirname(os.path.dirname(__file__)), "tools", "sass_summary.py"))
+    mod = importlib.util.module_from_spec(spec)
+    spec.loader.exec_module(mod)
+    try:
+        return {dem: (r, c) for _, dem, r, c in mod.summary(M.lib_path())}
+    except (OSError, subprocess.CalledProcessError):
+        pytest.skip("cuobjdump unavailable")
+
+
+def test_kernels_use_tcgen05_tma_and_do_not_spill():
+    """Per-kernel SASS: the grouped prefill GEMM issues tcgen05 MMAs into
+    TMEM (UTCHMMA), loads operands with tensor TMA (UTMALDG) and drains
+    TMEM with tcgen05.ld (LDTM); the decode kernels stream with 1-D TMA bulk
+    copies (UBLKCP) on mbarriers (SYNCS).  The instantiations the benchmarks
+    run (bf16 NV=2 for d=4096, NV=3 for d=6144) must not spill: the stack
+    kernels' speed is register-sensitive."""
+    ks = _kernels()
+
+    def one(prefix):
+        hits = [v for k, v in ks.items() if k.startswith(prefix)]
+        assert hits, prefix
+        return hits[0]
+
+    for spec in ("true", "false"):
+        r, c = one(f"void moe::prefill_grouped_kernel<{spec}>")
+        assert c["UTCHMMA"] > 0 and c["UTMALDG"] > 0 and c["LDTM"] > 0, c
+        assert r["LOCAL"] == 0
+    for name in ("decode_stack2_kernel", "decode_stack_kernel", "decode_experts_kernel"):
+        for nv in (2, 3):
+            r, c = one(f"void moe::{name}<__nv_bfloat16, {nv}>")
+            assert c["UBLKCP"] > 0 and c["SYNCS"] > 0, (name, c)
+            assert r["LOCAL"] == 0 and r["STACK"] == 0, (name, nv, r)  # no spills
+            assert r["REG"] <= 168, (name, nv, r)  # 9 warps: <= 3 per SM sub-partition
+    r, c = one("void moe::decode_stack2_kernel<__nv_bfloat16, 2>")
+    assert c["REDG"] > 0  # fixed-point accumulation: fire-and-forget 64-bit reductions
+
+
 def test_shape_validation_without_gpu():
     lib = M.lib()
     ok = M.Shape(4, 8, 2, 32, 64, 2).c()
