@@ -70,6 +70,7 @@ METRIC = "Mixtral-8x7B MoE decode tok/s (batch 1)"
 LAYER_METRIC = "Mixtral-8x7B MoE layer decode tok/s (batch 1, 1 layer)"
 PREFILL_METRIC = "Mixtral-8x7B MoE layer prefill tok/s (512 tokens, 1 layer)"
 PREFILL_WORKLOAD = "Mixtral-8x7B-shaped MoE layer prefill, 512 tokens (BASELINE configs[2])"
+STACK_KERNEL_NAME = {1: "decode_stack_kernel", 2: "decode_stack2_kernel", 3: "decode_stack3_kernel"}
 # token scale of the multi-layer stacks (see the module docstring)
 STACK_TOKEN_SCALE = 0.1
 
@@ -372,24 +373,28 @@ def run_ours(args):
         basis = f"{mine} routed experts owned by rank {rank} (last token) x 3 x {d} x {f} x {esz} B"
     roof = None
     if w.forward_launches(1) == 1:
+        # the timed tokens again, each launch bracketed by its own events
+        # (the token copy stays outside; re-running one token in place would
+        # feed the stack its own growing output)
         n_rep = max(10, min(50, args.steps))
-        xs = pool[args.warmup:args.warmup + 1].clone()
-        for _ in range(3):
-            w.forward(xs, ids, gates, stream=stream_ptr)
+        for i in range(3):
+            step(args.warmup + i)
         torch.cuda.synchronize()
         barrier(world)
-        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        e0.record(stream)
-        for _ in range(n_rep):
-            w.forward(xs, ids, gates, stream=stream_ptr)
-        e1.record(stream)
+        evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(n_rep)]
+        for r, (a0, a1) in enumerate(evs):
+            with torch.cuda.stream(stream):
+                x.copy_(pool[args.warmup + r % args.steps:args.warmup + r % args.steps + 1])
+            a0.record(stream)
+            w.forward(x, ids, gates, stream=stream_ptr)
+            a1.record(stream)
         torch.cuda.synchronize()
-        kern_ms = e0.elapsed_time(e1) / n_rep
+        kern_ms = sum(a0.elapsed_time(a1) for a0, a1 in evs) / n_rep
         ach = rank_bytes / (kern_ms * 1e-3) / 1e9
         per_rank = gather_floats(round(ach, 1), world)
         roof = {"bound": "hbm", "achieved": round(ach, 1), "peak": peak, "unit": "GB/s",
                 "frac": round(ach / peak, 4), "traffic": args.stack_traffic if world == 1 else None,
-                "kernel": ("decode_stack2_kernel<bf16,2> (one launch per token)" if world == 1 else
+                "kernel": (f"{STACK_KERNEL_NAME[M.get_option('stack_kernel')]}<bf16,2> (one launch per token)" if world == 1 else
                            "decode_stack_kernel<bf16,2> with in-kernel NVLink exchange (one launch per token per rank)"),
                 "kernel_us": round(kern_ms * 1e3, 2), "alg_bytes_per_launch": rank_bytes,
                 "alg_bytes_basis": basis, "peak_source": peak_src,
@@ -801,7 +806,7 @@ def main():
                     help="N>1: ncclAllReduce instead of the fused peer-memory combine")
     ap.add_argument("--no-stack", action="store_true",
                     help="per-layer 2-kernel graph instead of the persistent stack kernel")
-    ap.add_argument("--stack-kernel", type=int, default=0, choices=[0, 1, 2],
+    ap.add_argument("--stack-kernel", type=int, default=0, choices=[0, 1, 2, 3],
                     help="A/B: 1 = two-barrier persistent kernel, 2 = single-barrier fixed-point kernel (default)")
     ap.add_argument("--force-ep", action="store_true",
                     help="testing: 1-rank NCCL communicator (the expert-parallel code path on one GPU)")

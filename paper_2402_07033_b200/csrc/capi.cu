@@ -378,7 +378,7 @@ int refresh_projection(moe_weights* w) {
 // The single-barrier fixed-point stack kernel (single GPU, E <= 8, router
 // projections on); decode_stack_kernel otherwise.
 bool use_stack2(const moe_weights* w) {
-  return moe::debug_options().stack_kernel == 2 && !w->ctx->ep() && w->rw_enabled && w->stack_acc.p != nullptr &&
+  return moe::debug_options().stack_kernel >= 2 && !w->ctx->ep() && w->rw_enabled && w->stack_acc.p != nullptr &&
          moe::stack2_supported(w->plan, w->dims());
 }
 

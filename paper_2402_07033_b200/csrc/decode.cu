@@ -1147,6 +1147,483 @@ __global__ void __launch_bounds__(kMaxConsWarps * 32 + 32, 1)
 }
 
 // ---------------------------------------------------------------------------
+// persistent whole-stack kernel, routing off the critical path
+//
+// decode_stack2_kernel interleaves up and down rows batch by batch, so the
+// next layer's logits are complete only when the slowest CTA has streamed its
+// last W2T row; then the grid barrier, the top-k and the first TMA round trip
+// of layer l+1 all sit on an idle HBM (~13 us of a ~109 us layer).
+//
+// Routing needs only h: logits_{l+1} = R_{l+1} x_l + sum_r h_r (R_{l+1} W2)[r]
+// (the projection is precomputed per expert), so here every CTA streams ALL
+// its W1/W3 rows first (2/3 of the bytes; h parked in smem), publishes its z
+// partial, then streams its W2T rows.  The producer thread, after issuing the
+// last W2T copy of layer l, waits on a grid counter for all z partials (long
+// since in: the down phase is ~1/3 of the layer), picks layer l+1's top-k
+// itself and keeps issuing — the ring holds layer l+1's first rows while the
+// consumers reduce x_{l+1} across the barrier.  Same per-CTA row split, same
+// per-row arithmetic and the same fixed-point sums as decode_stack2_kernel:
+// outputs, ids and gates are bit-identical to it.
+constexpr int kStateRoute = 64;      // state[64]: route counter (own 128 B line)
+constexpr int kStateRouteBase = 34;  // state[34]: its value at launch
+
+// Scalar restatement of warp_topk_softmax for E <= 32 (same rank predicate,
+// same ascending-id sequential denominator): bit-identical gates.
+__device__ __forceinline__ int thread_topk_softmax(const float* lg, int E, int k, int32_t* ids,
+                                                   float* gates) {
+  int n = 0;
+  float mx = -INFINITY;
+  for (int e = 0; e < E; ++e) {
+    const float v = lg[e];
+    int rank = 0;
+    for (int e2 = 0; e2 < E; ++e2) {
+      const float o = lg[e2];
+      rank += (int)((o > v) | ((o == v) & (e2 < e)));
+    }
+    if (rank < k) {
+      ids[n++] = e;
+      mx = fmaxf(mx, v);
+    }
+  }
+  float denom = 0.f;
+  for (int j = 0; j < n; ++j) denom += expf(lg[ids[j]] - mx);
+  for (int j = 0; j < n; ++j) gates[j] = expf(lg[ids[j]] - mx) / denom;
+  return n;
+}
+
+// Producer, phase-split order: W1/W3 rows of every batch, then the W2T rows.
+template <typename W>
+__device__ __forceinline__ void produce_rows_split(const Ring& R, Cursor& cur, const W* wbase,
+                                                   long long expert_stride, long long mat_stride,
+                                                   const int* s_slot, int f, int d, long long g0,
+                                                   long long g1, uint64_t pol,
+                                                   unsigned long long* t_up,
+                                                   unsigned long long* t_ring = nullptr) {
+  const int total_vec = (int)(3 * (g1 - g0));
+  int p = 0;
+  const int ring_rows = R.stages * R.rps;
+  auto put = [&](const W* src) {
+    if (cur.slot == 0) {
+      mbar_wait(&R.empty[cur.stage], cur.phase ^ 1);
+      if (t_ring != nullptr && (p == 0 || p == ring_rows)) t_ring[p == 0 ? 0 : 1] = clock64();
+      const int nvec = min(R.rps, total_vec - p);
+      mbar_arrive_expect_tx(&R.full[cur.stage], (uint32_t)(nvec * R.row_bytes));
+    }
+    bulk_g2s(R.buf + (size_t)cur.stage * R.stage_bytes + (size_t)cur.slot * R.row_bytes, src,
+             (uint32_t)R.row_bytes, &R.full[cur.stage], pol);
+    ++p;
+    if (++cur.slot == R.rps) cur.next_stage(R.stages);
+  };
+  for (long long g = g0; g < g1;) {
+    const int jj = (int)(g / f);
+    const int r = (int)(g - (long long)jj * f);
+    const int nb = (int)min((long long)kBatch, min(g1 - g, (long long)(f - r)));
+    const W* eb = wbase + (long long)s_slot[jj] * expert_stride + (long long)r * d;
+    for (int q = 0; q < nb; ++q) put(eb + (long long)q * d);
+    for (int q = 0; q < nb; ++q) put(eb + mat_stride + (long long)q * d);
+    g += nb;
+  }
+  if (t_up) *t_up = clock64();
+  for (long long g = g0; g < g1;) {
+    const int jj = (int)(g / f);
+    const int r = (int)(g - (long long)jj * f);
+    const int nb = (int)min(g1 - g, (long long)(f - r));
+    const W* eb = wbase + (long long)s_slot[jj] * expert_stride + 2 * mat_stride + (long long)r * d;
+    for (int q = 0; q < nb; ++q) put(eb + (long long)q * d);
+    g += nb;
+  }
+  if (cur.slot != 0) cur.next_stage(R.stages);
+}
+
+struct RowCount {
+  int p, total;
+};
+
+// Consumers, up phase: h'_r = gate * silu(W1_r x) * (W3_r x) into hbuf, and
+// warp 0's z accumulation — decode_stack2's arithmetic, batch for batch.
+// red is double-buffered, so one CTA barrier per batch suffices.
+template <typename W, int NV>
+__device__ __forceinline__ void consume_up(const Ring& R, Cursor& cur, RowCount& rc, const float* xr,
+                                           const float* s_gate, int f, long long g0, long long g1,
+                                           float* red, float* hbuf, int tid, int ncons, int bar_id,
+                                           unsigned long long* t_first, const float* rw,
+                                           const int* s_slot, int E, float* zreg) {
+  constexpr int VEC = Elem<W>::kVec;
+  const int warp = warp_uniform(tid >> 5), lane = tid & 31, ncw = ncons >> 5;
+  int bi = 0;
+  for (long long g = g0; g < g1;) {
+    const int jj = (int)(g / f);
+    const int r = (int)(g - (long long)jj * f);
+    const int nb = (int)min((long long)kBatch, min(g1 - g, (long long)(f - r)));
+    float rwv[kZMax];
+    if (rw != nullptr && warp == 0) {
+      const float* rp = rw + ((size_t)s_slot[jj] * f + r + lane) * E;
+#pragma unroll
+      for (int e = 0; e < kZMax; ++e) rwv[e] = (lane < nb && e < E) ? __ldg(rp + e) : 0.f;
+    }
+    float acc[2 * kBatch];
+#pragma unroll
+    for (int q = 0; q < 2 * kBatch; ++q) {
+      acc[q] = 0.f;
+      if ((q & (kBatch - 1)) < nb) {
+        if (cur.slot == 0) mbar_wait(&R.full[cur.stage], cur.phase);
+        if (t_first != nullptr && rc.p == 0 && tid == 0) *t_first = clock64();
+        const uint8_t* row = R.buf + (size_t)cur.stage * R.stage_bytes + (size_t)cur.slot * R.row_bytes;
+        float s = 0.f;
+#pragma unroll
+        for (int m = 0; m < NV; ++m) {
+          const uint4 v = lds128(row + (size_t)(tid + m * ncons) * 16);
+          float w[VEC];
+          Elem<W>::unpack(v, w);
+#pragma unroll
+          for (int i = 0; i < VEC; ++i) s = fmaf(w[i], xr[m * VEC + i], s);
+        }
+        acc[q] = s;
+        ++rc.p;
+        if (++cur.slot == R.rps || rc.p == rc.total) {
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&R.empty[cur.stage]);
+          cur.next_stage(R.stages);
+        }
+      }
+    }
+#pragma unroll
+    for (int s = 16; s >= 1; s >>= 1) {
+      const bool hi = (lane & s) != 0;
+#pragma unroll
+      for (int i = 0; i < s; ++i) {
+        const float send = hi ? acc[i] : acc[i + s];
+        const float keep = hi ? acc[i + s] : acc[i];
+        acc[i] = keep + __shfl_xor_sync(MOE_FULL_MASK, send, s);
+      }
+    }
+    float* rb = red + (bi & 1) * (kMaxConsWarps * 32);
+    rb[warp * 32 + lane] = acc[0];
+    named_bar_sync(bar_id, ncons);
+    if (warp == 0) {
+      float tot = 0.f;
+      for (int w = 0; w < ncw; ++w) tot += rb[w * 32 + lane];
+      const float b = __shfl_down_sync(MOE_FULL_MASK, tot, kBatch);
+      const float hq = lane < nb ? s_gate[jj] * (silu_f(tot) * b) : 0.f;
+      if (lane < nb) hbuf[g - g0 + lane] = hq;
+      if (rw != nullptr) {
+#pragma unroll
+        for (int e = 0; e < kZMax; ++e) zreg[e] += warp_sum(hq * rwv[e]);
+      }
+    }
+    ++bi;
+    g += nb;
+  }
+}
+
+// Consumers, down phase: y += h'_r * W2T_r over the CTA's rows in order.
+template <typename W, int NV>
+__device__ __forceinline__ void consume_down(const Ring& R, Cursor& cur, RowCount& rc, float* yacc,
+                                             const float* hbuf, int n, int tid, int ncons) {
+  constexpr int VEC = Elem<W>::kVec;
+  const int lane = tid & 31;
+#pragma unroll 4
+  for (int i = 0; i < n; ++i) {
+    if (cur.slot == 0) mbar_wait(&R.full[cur.stage], cur.phase);
+    const uint8_t* row = R.buf + (size_t)cur.stage * R.stage_bytes + (size_t)cur.slot * R.row_bytes;
+    const float hq = hbuf[i];
+#pragma unroll
+    for (int m = 0; m < NV; ++m) {
+      const uint4 v = lds128(row + (size_t)(tid + m * ncons) * 16);
+      float w[VEC];
+      Elem<W>::unpack(v, w);
+#pragma unroll
+      for (int j = 0; j < VEC; ++j) yacc[m * VEC + j] = fmaf(hq, w[j], yacc[m * VEC + j]);
+    }
+    ++rc.p;
+    if (++cur.slot == R.rps || rc.p == rc.total) {
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&R.empty[cur.stage]);
+      cur.next_stage(R.stages);
+    }
+  }
+}
+
+template <typename W, int NV>
+__global__ void __launch_bounds__(kMaxConsWarps * 32 + 64, 1)
+    decode_stack3_kernel(const __grid_constant__ Stack2Args a) {
+  constexpr int VEC = Elem<W>::kVec;
+  constexpr int S = NV * VEC;
+  extern __shared__ __align__(128) uint8_t smem[];
+  Ring R;
+  R.buf = smem;
+  R.full = reinterpret_cast<uint64_t*>(smem + (size_t)a.stages * a.stage_bytes);
+  R.empty = R.full + a.stages;
+  R.rps = a.rps;
+  R.stages = a.stages;
+  R.stage_bytes = a.stage_bytes;
+  R.row_bytes = a.row_bytes;
+  float* stg = reinterpret_cast<float*>(smem + (size_t)a.stages * a.stage_bytes + 2 * a.stages * 8);
+  float* hbuf = stg + a.d;
+  __shared__ uint64_t route_bar;
+  __shared__ float red[2 * kMaxConsWarps * 32];
+  __shared__ float logits[kMaxExperts];
+  __shared__ int32_t s_ids[kMaxSlots];
+  __shared__ float s_g[kMaxSlots];
+  __shared__ int s_slot[2][kMaxSlots];
+  __shared__ float s_gate[2][kMaxSlots];
+  __shared__ int s_nloc[2];
+  __shared__ unsigned s_state[3];
+
+  const int ncons = blockDim.x - 64;  // + producer warp + router warp
+  const int ncw = ncons >> 5;
+  const int tid = threadIdx.x, lane = tid & 31;
+  const int warp = warp_uniform(tid >> 5);
+  const int G = gridDim.x, c = blockIdx.x;
+  const int d = a.d, E = a.E, k = a.k;
+  unsigned long long* const trace = a.trace;
+  auto tslot = [&](int l, int i) { return trace + ((size_t)l * G + c) * 16 + i; };
+
+  if (tid == 0) {
+    for (int s = 0; s < a.stages; ++s) {
+      mbar_init(&R.full[s], 1);
+      mbar_init(&R.empty[s], ncw);
+    }
+    mbar_init(&route_bar, 1);
+    fence_mbar_init();
+  }
+  griddep_wait();
+  if (tid == 32) {
+    s_state[0] = __ldcg(&a.state[kStateBase]);
+    s_state[1] = __ldcg(&a.state[kStateBase + 1]);
+    s_state[2] = __ldcg(&a.state[kStateRouteBase]);
+  }
+  __syncthreads();
+  const unsigned bar0 = s_state[0], rot = s_state[1], rbase = s_state[2];
+  auto buf = [&](int l) { return (int)((rot + (unsigned)l) % 3u); };
+  unsigned long long* const ovf_words = a.zacc + kZMax;
+
+  if (warp == ncw) {  // producer: one elected lane issues every bulk copy
+    if (lane != 0) return;
+    if (trace) {
+      *tslot(0, 12) = clock64();
+      *tslot(0, 13) = globaltimer();
+    }
+    const uint64_t pol = l2_evict_first_policy();
+    Cursor cur;
+    for (int l = 0; l < a.L; ++l) {
+      mbar_wait_sleep(&route_bar, (uint32_t)(l & 1));  // layer l's routing (ready long before, l >= 1)
+      if (trace) *tslot(l, 10) = clock64();
+      const int set = l & 1;
+      const long long T = (long long)s_nloc[set] * a.f;
+      const long long g0 = (long long)c * T / G, g1 = (long long)(c + 1) * T / G;
+      if (g1 > g0)
+        produce_rows_split<W>(R, cur, reinterpret_cast<const W*>(a.layer_experts[l]), a.expert_stride,
+                              a.mat_stride, s_slot[set], a.f, d, g0, g1, pol,
+                              trace ? tslot(l, 8) : nullptr,
+                              (trace && l > 0) ? tslot(l, 12) : nullptr);
+      if (trace) *tslot(l, 9) = clock64();
+    }
+    if (trace) {
+      *tslot(0, 14) = clock64();
+      *tslot(0, 15) = globaltimer();
+    }
+    return;
+  }
+  if (warp == ncw + 1) {  // router: layer l+1's top-k as soon as every z partial is in
+    for (int l = 0; l + 1 < a.L; ++l) {
+      const int so = lane < E ? __ldg(a.slot_of + (size_t)(l + 1) * E + lane) : -1;
+      if (lane == 0) {
+        const unsigned target = rbase + (unsigned)((l + 1) * G);
+        unsigned v;
+        for (;;) {
+          asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(a.state + kStateRoute) : "memory");
+          if ((int)(v - target) >= 0) break;
+          __nanosleep(128);
+        }
+      }
+      __syncwarp();
+      const unsigned long long* zb = a.zacc + (size_t)buf(l) * kZStride;
+      const bool bad = __ldcg(&ovf_words[(size_t)buf(l) * kZStride]) != 0ull;
+      if (lane < E) logits[lane] = bad ? 0.f : from_fix(__ldcg(zb + lane));
+      __syncwarp();
+      if (c == 0 && a.logits_out != nullptr && lane < E) a.logits_out[(size_t)(l + 1) * E + lane] = logits[lane];
+      warp_topk_softmax(logits, E, k, s_ids, s_g);
+      // slot of each selected expert: lane j of the warp holds slot_of[j]
+      const int nset = (l + 1) & 1;
+      int nl = 0;
+      for (int j = 0; j < k; ++j) {
+        const int slot = __shfl_sync(MOE_FULL_MASK, so, s_ids[j] & 31);
+        if (slot >= 0) {
+          if (lane == 0) {
+            s_slot[nset][nl] = slot;
+            s_gate[nset][nl] = s_g[j];
+          }
+          ++nl;
+        }
+      }
+      if (c == 0 && lane < k) {
+        a.ids_out[(size_t)(l + 1) * k + lane] = s_ids[lane];
+        a.gates_out[(size_t)(l + 1) * k + lane] = s_g[lane];
+      }
+      if (lane == 0) {
+        s_nloc[nset] = nl;
+        mbar_arrive(&route_bar);  // producer and consumers of layer l+1
+        if (trace) *tslot(l, 11) = clock64();
+      }
+      __syncwarp();
+    }
+    return;
+  }
+
+  auto col_of = [&](int q) { return (tid + (q / VEC) * ncons) * VEC + (q % VEC); };
+  float rv[2];
+  auto load_rv = [&](int lr) {
+#pragma unroll
+    for (int j = 0; j < 2; ++j) {
+      const int p = c + j * G;
+      rv[j] = (lr < a.L && p < S * E) ? __ldg(a.router + ((size_t)lr * E + p / S) * d + col_of(p % S)) : 0.f;
+    }
+  };
+  auto add_xpart = [&](int lr, int b, const float* xr) {
+    if (lr >= a.L) return;
+#pragma unroll
+    for (int j = 0; j < 2; ++j) {
+      const int p = c + j * G;
+      if (p < S * E) {
+        const int q = p % S;
+        float xv = 0.f;
+#pragma unroll
+        for (int i = 0; i < S; ++i) xv = (i == q) ? xr[i] : xv;
+        const float v = warp_sum(rv[j] * xv);
+        if (lane == 0) {
+          atomicAdd(&a.zacc[(size_t)b * kZStride + p / S], to_fix(v));
+          if (!(fabsf(v) < kFixMax)) atomicAdd(&ovf_words[(size_t)b * kZStride], 1ull);
+        }
+      }
+    }
+  };
+
+  // layer 0's routing from x_0 (consumer warps; same arithmetic as stack2)
+  for (int e = warp; e < E; e += ncw) {
+    const float* re = a.router + (size_t)e * d;
+    float s = 0.f;
+    for (int i = lane; i < d; i += 32) s = fmaf(re[i], __ldcg(&a.x[i]), s);
+    s = warp_sum(s);
+    if (lane == 0) logits[e] = s;
+  }
+  named_bar_sync(2, ncons);
+  if (warp == 0) {
+    if (c == 0 && a.logits_out != nullptr && lane < E) a.logits_out[lane] = logits[lane];
+    warp_topk_softmax(logits, E, k, s_ids, s_g);
+    if (lane == 0) {
+      int n = 0;
+      for (int j = 0; j < k; ++j) {
+        const int slot = a.slot_of[s_ids[j]];
+        if (slot >= 0) {
+          s_slot[0][n] = slot;
+          s_gate[0][n] = s_g[j];
+          ++n;
+        }
+        if (c == 0) {
+          a.ids_out[j] = s_ids[j];
+          a.gates_out[j] = s_g[j];
+        }
+      }
+      s_nloc[0] = n;
+      mbar_arrive(&route_bar);
+    }
+  }
+  float xr[S];
+  load_x<W, NV>(a.x, xr, tid, ncons);
+  load_rv(1);
+  add_xpart(1, buf(0), xr);
+  load_rv(2);
+  named_bar_sync(2, ncons);
+
+  float zreg[kZMax];
+#pragma unroll
+  for (int e = 0; e < kZMax; ++e) zreg[e] = 0.f;
+  Cursor cur;
+  for (int l = 0; l < a.L; ++l) {
+    const bool more = l + 1 < a.L;
+    const int b = buf(l), set = l & 1;
+    const bool tr0 = trace != nullptr && tid == 0;
+    if (tr0) *tslot(l, 0) = clock64();
+    if (l > 0) mbar_wait(&route_bar, (uint32_t)(l & 1));
+    const long long T = (long long)s_nloc[set] * a.f;
+    const long long g0 = (long long)c * T / G, g1 = (long long)(c + 1) * T / G;
+    RowCount rc{0, (int)(3 * (g1 - g0))};
+    consume_up<W, NV>(R, cur, rc, xr, s_gate[set], a.f, g0, g1, red, hbuf, tid, ncons, 1,
+                      tr0 ? tslot(l, 1) : nullptr, more ? a.rw[l] : nullptr, s_slot[set], E, zreg);
+    named_bar_sync(2, ncons);  // hbuf complete; every warp's R x share (add_xpart) issued
+    if (tr0) *tslot(l, 2) = clock64();
+    if (more && warp == 0) {
+      float zv = 0.f;
+#pragma unroll
+      for (int e = 0; e < kZMax; ++e) {
+        zv = (lane == e) ? zreg[e] : zv;
+        zreg[e] = 0.f;
+      }
+      if (lane < E) {
+        atomicAdd(&a.zacc[(size_t)b * kZStride + lane], to_fix(zv));
+        if (!(fabsf(zv) < kFixMax)) atomicAdd(&ovf_words[(size_t)b * kZStride], 1ull);
+      }
+      __syncwarp();
+      if (lane == 0) {
+        __threadfence();
+        asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(a.state + kStateRoute) : "memory");
+        if (trace) *tslot(l, 3) = clock64();
+      }
+    }
+    float yacc[S];
+#pragma unroll
+    for (int i = 0; i < S; ++i) yacc[i] = 0.f;
+    consume_down<W, NV>(R, cur, rc, yacc, hbuf, (int)(g1 - g0), tid, ncons);
+    if (tr0) *tslot(l, 4) = clock64();
+    store_y<W, NV>(stg, yacc, tid, ncons);
+    named_bar_sync(2, ncons);
+    bool ov = false;
+    unsigned long long* accb = a.acc + (size_t)b * d;
+    for (int i = tid; i < d; i += ncons) {
+      const float v = stg[i];
+      ov |= !(fabsf(v) < kFixMax);
+      atomicAdd(&accb[i], to_fix(v));
+    }
+    if (__any_sync(MOE_FULL_MASK, ov) && lane == 0) atomicAdd(&ovf_words[(size_t)b * kZStride], 1ull);
+    if (tr0) *tslot(l, 5) = clock64();
+    grid_sync(a.state, bar0 + (unsigned)((l + 1) * G), ncons);
+    if (tr0) *tslot(l, 6) = clock64();
+    unsigned long long av[S];
+#pragma unroll
+    for (int m = 0; m < NV; ++m) {
+      const ulonglong2* ap = reinterpret_cast<const ulonglong2*>(accb + (size_t)(tid + m * ncons) * VEC);
+#pragma unroll
+      for (int v = 0; v < VEC / 2; ++v) {
+        const ulonglong2 t = __ldcg(ap + v);
+        av[m * VEC + 2 * v] = t.x;
+        av[m * VEC + 2 * v + 1] = t.y;
+      }
+    }
+    const bool bad = __ldcg(&ovf_words[(size_t)b * kZStride]) != 0ull;
+#pragma unroll
+    for (int i = 0; i < S; ++i) xr[i] = bad ? __int_as_float(0x7fffffff) : xr[i] + from_fix(av[i]);
+    {
+      const int b2 = buf(l + 2);
+      const int c0 = (int)((long long)c * d / G), c1 = (int)((long long)(c + 1) * d / G);
+      for (int i = c0 + tid; i < c1; i += ncons) a.acc[(size_t)b2 * d + i] = 0ull;
+      if (c == 0 && tid < kZStride) a.zacc[(size_t)b2 * kZStride + tid] = 0ull;
+    }
+    if (l + 2 < a.L) {
+      add_xpart(l + 2, buf(l + 1), xr);
+      load_rv(l + 3);
+    }
+    if (!more && c == 0) store_y<W, NV>(a.x, xr, tid, ncons);
+    if (tr0) *tslot(l, 7) = clock64();
+  }
+  if (c == 0 && tid == 0) {
+    a.state[kStateBase] = bar0 + (unsigned)(a.L * G);
+    a.state[kStateBase + 1] = (rot + (unsigned)a.L) % 3u;
+    a.state[kStateRouteBase] = rbase + (unsigned)((a.L - 1) * G);
+  }
+}
+
+// ---------------------------------------------------------------------------
 int reduce_blocks(const Dims& dm) { return (dm.d + 31) / 32; }
 
 DecodePlan plan_decode(const Dims& dm, int sm_count) {
@@ -1296,18 +1773,30 @@ bool stack2_supported(const DecodePlan& p, const Dims& dm) {
   return p.nv * vec * dm.E <= 2 * p.grid && stack2_smem(p, dm) <= 227 * 1024;
 }
 
-size_t stack2_acc_bytes(const Dims& dm) { return 3 * (size_t)dm.d * 8 + 3 * kZStride * 8 + 256; }
+size_t stack2_acc_bytes(const Dims& dm) { return 3 * (size_t)dm.d * 8 + 3 * kZStride * 8 + 512; }
+
+// decode_stack3_kernel: the ring, the partial-y staging and h for the CTA's
+// rows (at most ceil(k*f/G)).
+static int stack3_hcap(const DecodePlan& p, const Dims& dm) {
+  return (int)(((long long)dm.k * dm.f + p.grid - 1) / p.grid) + 1;
+}
+int stack3_smem(const DecodePlan& p, const Dims& dm) { return stack2_smem(p, dm) + 4 * stack3_hcap(p, dm); }
+bool stack3_supported(const DecodePlan& p, const Dims& dm) {
+  return stack2_supported(p, dm) && dm.E <= 32 && stack3_smem(p, dm) <= 227 * 1024;
+}
 
 template <typename W, int NV>
 static cudaError_t launch_stack2_t(const DecodePlan& p, const Dims& dm, const Stack2Args& a,
                                    cudaStream_t s) {
-  auto kern = decode_stack2_kernel<W, NV>;
-  const int smem = stack2_smem(p, dm);
+  const bool v3 = debug_options().stack_kernel == 3 && stack3_supported(p, dm);
+  auto kern = v3 ? decode_stack3_kernel<W, NV> : decode_stack2_kernel<W, NV>;
+  const int smem = v3 ? stack3_smem(p, dm) : stack2_smem(p, dm);
+  const int threads = p.ncons + (v3 ? 64 : 32);
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   if (e != cudaSuccess) return e;
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(p.grid);
-  cfg.blockDim = dim3(p.ncons + 32);
+  cfg.blockDim = dim3(threads);
   cfg.dynamicSmemBytes = smem;
   cfg.stream = s;
   cudaLaunchAttribute attr[1];

@@ -15,7 +15,7 @@ constexpr int kMaxExperts = 256;
 // moe_weights is created (stack, rw, prefill, prefill_splits) or at launch.
 struct DebugOptions {
   int stack = 1;           // batch-1 decode: persistent stack kernel (0: per-layer kernels)
-  int stack_kernel = 2;    // 2: fixed-point single-barrier kernel, 1: two-barrier kernel
+  int stack_kernel = 2;    // 3: routing-ahead single-barrier kernel, 2: fixed-point single-barrier, 1: two-barrier
   int rw = 1;              // precomputed R_{l+1} W2 router projections
   int prefill = 1;         // tcgen05 grouped prefill (0: generic kernels)
   int prefill_splits = 2;  // max down K splits of the grouped kernel (0: two-kernel path)

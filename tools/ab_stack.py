@@ -1,6 +1,7 @@
 """A/B of the persistent decode kernels on one weights object:
-stack_kernel=1 (two grid barriers per layer, float partial reduction) vs
-stack_kernel=2 (one barrier, fixed-point L2 atomics).  Checks routing and
+stack_kernel=1 (two grid barriers per layer, float partial reduction),
+stack_kernel=2 (one barrier, fixed-point L2 atomics) and stack_kernel=3 (routing
+resolved during the down phase).  Checks routing and
 output agreement and run-to-run bit-determinism, then times both.
 
     python tools/ab_stack.py [--layers 32] [--iters 50]
@@ -24,6 +25,7 @@ def main():
     ap.add_argument("--rounds", type=int, default=3)
     ap.add_argument("--scale", type=float, default=0.1)
     ap.add_argument("--configs", default="1,2", help="stack_kernel values to time")
+    ap.add_argument("--kernels", default="1,2", help="stack_kernel values compared with the first")
     args = ap.parse_args()
     import torch
 
@@ -39,7 +41,8 @@ def main():
     x0 = args.scale * torch.randn(1, d, device="cuda")  # see bench.py: N(0,1) tokens overflow a norm-less 32-layer stack
     res = {}
     outs = {}
-    for kern in (1, 2):
+    kerns = [int(k) for k in args.kernels.split(",")]
+    for kern in kerns:
         M.set_option("stack_kernel", kern)
         o = []
         for _ in range(3):
@@ -53,13 +56,16 @@ def main():
         det = all(np.array_equal(o[0][i], oo[i]) for oo in o[1:] for i in range(3))
         outs[kern] = o[0]
         res[f"k{kern}_deterministic"] = bool(det)
-    x1, i1, g1 = outs[1]
-    x2, i2, g2 = outs[2]
     xin = x0.cpu().numpy()
-    res["ids_equal"] = bool(np.array_equal(i1, i2))
-    res["first_ids_diff_layer"] = int(np.argmax((i1 != i2).any(axis=(1, 2)))) if not res["ids_equal"] else -1
-    res["normwise_delta_err"] = float(np.abs((x2 - xin) - (x1 - xin)).max() / np.abs(x1 - xin).max())
-    res["gates_maxdiff"] = float(np.abs(g1 - g2).max())
+    x1, i1, g1 = outs[kerns[0]]
+    for kern in kerns[1:]:
+        x2, i2, g2 = outs[kern]
+        tag = f"k{kern}_vs_k{kerns[0]}"
+        res[f"{tag}_ids_equal"] = bool(np.array_equal(i1, i2))
+        res[f"{tag}_x_bit_equal"] = bool(np.array_equal(x1, x2))
+        res[f"{tag}_gates_bit_equal"] = bool(np.array_equal(g1, g2))
+        res[f"{tag}_first_ids_diff_layer"] = int(np.argmax((i1 != i2).any(axis=(1, 2)))) if not np.array_equal(i1, i2) else -1
+        res[f"{tag}_normwise_delta_err"] = float(np.abs((x2 - xin) - (x1 - xin)).max() / np.abs(x1 - xin).max())
     # timing, alternating
     cfgs = [(int(c),) for c in args.configs.split(",")]
     times = {c: [] for c in cfgs}
@@ -85,13 +91,18 @@ def main():
         res[f"{tag}_ms"] = round(ms, 4)
         res[f"{tag}_tok_s"] = round(1000 / ms, 2)
         res[f"{tag}_gbs"] = round(L * (2 * 3 * d * args.f * 2 + 8 * d * 4) / (ms * 1e-3) / 1e9, 1)
-    # logits of the bench token through kernel 2
-    M.set_option("stack_kernel", 2)
-    lg = torch.zeros((L, 8), device="cuda")
-    xx = x0.clone()
-    w.forward_logits(xx, ids, g, lg, stream=sp)
-    torch.cuda.synchronize()
-    lgn = lg.cpu().numpy()
+    # logits of the bench token through the kernels >= 2 (bit-equal expected)
+    lgs = {}
+    for kern in [k for k in kerns if k >= 2]:
+        M.set_option("stack_kernel", kern)
+        lg = torch.zeros((L, 8), device="cuda")
+        xx = x0.clone()
+        w.forward_logits(xx, ids, g, lg, stream=sp)
+        torch.cuda.synchronize()
+        lgs[kern] = lg.cpu().numpy()
+    ks = sorted(lgs)
+    res["logits_bit_equal"] = bool(all(np.array_equal(lgs[ks[0]], lgs[k]) for k in ks[1:]))
+    lgn = lgs[ks[0]]
     srt = -np.sort(-lgn, axis=1)
     res["routing_margin_min"] = float(((srt[:, 1] - srt[:, 2]) / np.abs(lgn).max(axis=1)).min())
     res["logits_ids_consistent"] = bool(np.array_equal(np.sort(np.argsort(-lgn, kind="stable", axis=1)[:, :2], axis=1),
