@@ -546,6 +546,8 @@ def bench_prefill(args, w, stream, stream_ptr, device, peaks, peak_src):
     weights), 512-token prefill on the tcgen05/TMEM grouped GEMM path."""
     import torch
 
+    import paper_2402_07033_b200 as M
+
     L, E, k, d, f, _ = CONFIGS["layer"]
     n = args.prefill_tokens
     assert w.expert_path(n) == 3, "tcgen05 prefill path not selected"
@@ -606,7 +608,10 @@ def bench_prefill(args, w, stream, stream_ptr, device, peaks, peak_src):
     return {"metric": PREFILL_METRIC, "value": round(n / (ms * 1e-3), 1), "unit": "tok/s",
             "ms_per_step": round(ms, 4), "steps": n_steps, "higher_is_better": True,
             "config": {"workload": PREFILL_WORKLOAD, "weights": "layer 0 of the bench weights", "tokens": n,
-                       "path": "router_topk_bulk + permute + gather + tcgen05/TMEM grouped GEMM (swap-AB) + combine",
+                       "path": ("router (+ dispatch bases) -> tcgen05/TMEM grouped GEMM (swap-AB) with in-kernel "
+                                "row dispatch, combine running alongside (ready queue)"
+                                if M.get_option("prefill_fused") else
+                                "router_topk_bulk + permute + gather + tcgen05/TMEM grouped GEMM (swap-AB) + combine"),
                        "active_experts": active,
                        "l2": "2.8 GB of expert weights per step (> L2); 8 token batches rotate"},
             "clocks": clk.summary(),

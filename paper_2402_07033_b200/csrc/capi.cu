@@ -174,6 +174,7 @@ struct moe_weights {
   DevBuf xbuf2, gbar, dev_layers, dev_slots;  // persistent stack kernel
   DevBuf stack_acc;  // decode_stack2_kernel: fixed-point accumulators + barrier state
   DevBuf pf_counts, pf_offsets, pf_perm, pf_xg, pf_h, pf_sync;  // tcgen05 prefill
+  DevBuf pf_route;  // fused prefill: router last-block counter + per-block dispatch bases
   DevBuf io;  // host-buffer API, batch 1: [x][ids][gates] (one D2H)
   // moe_debug_kernel_timing: event pairs around each grouped prefill launch
   bool ktime_on = false;
@@ -424,8 +425,34 @@ int ensure_prefill_scratch(moe_weights* w, int n_tok) {
   // the down tiles, Y by the combine)
   TRY(w->pf_h.ensure(prefill_h_bytes(w, n_tok) +
                      4 * rows * w->d() * (size_t)std::max(1, w->prefill_splits)));
-  TRY(w->pf_sync.ensure(4 * (1 + (size_t)w->E() * ((n_tok + moe::kPrefillChunk - 1) / moe::kPrefillChunk) +
-                          w->E())));
+  TRY(w->pf_sync.ensure(4 * moe::prefill_sync_words(w->E(), n_tok, w->d())));
+  TRY(w->pf_route.ensure(4 * (16 + (size_t)moe::route_blocks(n_tok) * w->E())));
+  return MOE_OK;
+}
+
+// The fused prefill layer (router with dispatch bases -> grouped kernel that
+// scatters, computes and combines): single GPU, every expert local, the
+// grouped kernel (splits > 0), no post-SiLU capture.
+bool use_fused_prefill(const moe_weights* w, int n_tok, const float* post) {
+  const Dims dm = w->dims();
+  return use_prefill(w, n_tok, post) && moe::debug_options().prefill_fused && !w->ctx->ep() &&
+         !w->replicas && w->prefill_splits > 0 && moe::route_dispatch_supported(dm) &&
+         moe::route_block_tokens() * dm.k <= 64 && dm.k * w->prefill_splits <= 8;
+}
+
+// moe_debug_kernel_timing: a fresh event pair around the grouped kernel
+int kernel_events(moe_weights* w, cudaEvent_t& t0, cudaEvent_t& t1) {
+  t0 = t1 = nullptr;
+  if (!w->ktime_on) return MOE_OK;
+  if (w->kev_used == w->kev.size()) {
+    cudaEvent_t a = nullptr, b = nullptr;
+    CU(cudaEventCreate(&a));
+    CU(cudaEventCreate(&b));
+    w->kev.emplace_back(a, b);
+  }
+  t0 = w->kev[w->kev_used].first;
+  t1 = w->kev[w->kev_used].second;
+  ++w->kev_used;
   return MOE_OK;
 }
 
@@ -433,12 +460,22 @@ int ensure_prefill_scratch(moe_weights* w, int n_tok) {
 // the decode path).  EP: local partials -> all-reduce -> residual.
 int experts_forward(moe_weights* w, int l, const float* x, int n_tok, const int32_t* ids,
                     const float* gates, float* x_out, float* post, cudaStream_t s, bool pdl,
-                    const float* next_router, int32_t* next_ids, float* next_gates) {
+                    const float* next_router, int32_t* next_ids, float* next_gates,
+                    const float* router_l = nullptr) {
   const Dims dm = w->dims();
   const LayerWeights lw = w->layer(l);
   const bool ep = w->ctx->ep();
   moe::SparsityCounters sp = w->sp;
   if (sp.counts) sp.counts += (size_t)l * sp.n;
+  if (router_l) {
+    // router_l: route this layer here (ids/gates are outputs) — fused into the
+    // prefill layer's first kernel when the fused path applies
+    if (!use_fused_prefill(w, n_tok, post)) {
+      CU(moe::launch_router_topk(router_l, x, n_tok, dm, const_cast<int32_t*>(ids),
+                                 const_cast<float*>(gates), s, false));
+      router_l = nullptr;
+    }
+  }
   if (use_decode(w, n_tok, post)) {
     CU(moe::launch_decode_experts(w->plan, lw, dm, ids, gates, x, w->ypart.as<float>(), s, pdl));
     if (!ep) {
@@ -473,6 +510,27 @@ int experts_forward(moe_weights* w, int l, const float* x, int n_tok, const int3
     int32_t* counts = w->pf_counts.as<int32_t>();
     int32_t* offsets = w->pf_offsets.as<int32_t>();
     int32_t* perm = w->pf_perm.as<int32_t>();
+    if (router_l) {
+      // fused: router + dispatch bases, then the grouped kernel scatters the
+      // rows, runs both GEMMs and writes x_out itself
+      moe::PrefillFuse fz;
+      fz.router = router_l;
+      fz.ids = const_cast<int32_t*>(ids);
+      fz.gates = const_cast<float*>(gates);
+      fz.route = w->pf_route.as<int32_t>();
+      fz.x_out = x_out;
+      float* yb = reinterpret_cast<float*>(w->pf_h.as<char>() + prefill_h_bytes(w, n_tok));
+      cudaEvent_t kt0 = nullptr, kt1 = nullptr;
+      TRY(kernel_events(w, kt0, kt1));
+      CU(moe::launch_prefill_experts(lw, w->n_local[l], dm, n_tok, x, counts, offsets, perm, gates,
+                                     w->dev_slots.as<int16_t>() + (size_t)l * dm.E,
+                                     w->pf_xg.as<__nv_bfloat16>(), w->pf_h.as<__nv_bfloat16>(), yb,
+                                     w->pf_sync.as<int>(), w->ctx->sm_count, w->prefill_splits, s, sp,
+                                     kt0, kt1, &fz));
+      if (next_router)
+        CU(moe::launch_router_topk(next_router, x_out, n_tok, dm, next_ids, next_gates, s, pdl));
+      return MOE_OK;
+    }
     CU(moe::launch_permute(ids, n_tok, dm.k, dm.E, counts, offsets, perm, nullptr, s, pdl));
     const int S = w->prefill_splits;
     const int16_t* slots = w->dev_slots.as<int16_t>() + (size_t)l * dm.E;
@@ -491,17 +549,7 @@ int experts_forward(moe_weights* w, int l, const float* x, int n_tok, const int3
     if (w->n_local[l] < dm.E || w->replicas)
       CU(cudaMemsetAsync(ybuf, 0, (size_t)std::max(1, S) * rows * dm.d * 4, s));
     cudaEvent_t kt0 = nullptr, kt1 = nullptr;
-    if (w->ktime_on) {
-      if (w->kev_used == w->kev.size()) {
-        cudaEvent_t a = nullptr, b = nullptr;
-        CU(cudaEventCreate(&a));
-        CU(cudaEventCreate(&b));
-        w->kev.emplace_back(a, b);
-      }
-      kt0 = w->kev[w->kev_used].first;
-      kt1 = w->kev[w->kev_used].second;
-      ++w->kev_used;
-    }
+    TRY(kernel_events(w, kt0, kt1));
     CU(moe::launch_prefill_experts(lw, w->n_local[l], dm, n_tok, x, counts, offsets, perm, gates,
                                    slots,
                                    w->pf_xg.as<__nv_bfloat16>(), w->pf_h.as<__nv_bfloat16>(),
@@ -541,17 +589,20 @@ int enqueue_forward(moe_weights* w, float* x, int n_tok, int32_t* ids, float* ga
   const Dims dm = w->dims();
   const size_t tk = (size_t)n_tok * dm.k;
   const bool pdl = true;
-  CU(moe::launch_router_topk(w->router, x, n_tok, dm, ids, gates, s, false));
+  // fused prefill: every layer routes inside its own first kernel
+  const bool fused = use_fused_prefill(w, n_tok, post_all);
+  if (!fused) CU(moe::launch_router_topk(w->router, x, n_tok, dm, ids, gates, s, false));
   const float* cur = x;
   for (int l = 0; l < L; ++l) {
     float* nxt = (l == L - 1) ? x : ((l % 2 == 0) ? w->xa.as<float>() : w->xb.as<float>());
-    const bool more = l + 1 < L;
+    const bool more = l + 1 < L && !fused;
     float* post = post_all ? post_all + (size_t)l * tk * dm.f : nullptr;
     TRY(experts_forward(w, l, cur, n_tok, ids + (size_t)l * tk, gates + (size_t)l * tk, nxt,
                         post, s, pdl,
                         more ? w->router + (size_t)(l + 1) * dm.E * dm.d : nullptr,
                         more ? ids + (size_t)(l + 1) * tk : nullptr,
-                        more ? gates + (size_t)(l + 1) * tk : nullptr));
+                        more ? gates + (size_t)(l + 1) * tk : nullptr,
+                        fused ? w->router + (size_t)l * dm.E * dm.d : nullptr));
     cur = nxt;
   }
   return MOE_OK;
@@ -634,6 +685,7 @@ static int* option_slot(const char* name) {
       {"force_ep", &moe::DebugOptions::force_ep},
       {"no_pdl", &moe::DebugOptions::no_pdl},
       {"combine4", &moe::DebugOptions::combine4},
+      {"prefill_fused", &moe::DebugOptions::prefill_fused},
       {"pf_debug", &moe::DebugOptions::pf_debug},
       {"pf_evict", &moe::DebugOptions::pf_evict},
       {"pf_lag", &moe::DebugOptions::pf_lag},
@@ -1148,7 +1200,7 @@ int moe_weights_destroy(moe_weights* w) {
   for (DevBuf* b : {&w->ypart, &w->rpart, &w->counter, &w->xa, &w->xb, &w->xin, &w->h, &w->y, &w->delta,
                     &w->ids, &w->gates, &w->post, &w->stage_d, &w->xbuf2, &w->gbar,
                     &w->dev_layers, &w->dev_slots, &w->pf_counts, &w->pf_offsets, &w->pf_perm,
-                    &w->pf_xg, &w->pf_h, &w->pf_sync})
+                    &w->pf_xg, &w->pf_h, &w->pf_sync, &w->pf_route})
     b->release();
   for (DevBuf* b : {&w->dev_holders, &w->dev_res_slots, &w->pf_counts2, &w->pf_offsets2, &w->io,
                     &w->stack_acc})
@@ -1393,10 +1445,8 @@ int moe_layer_forward(moe_weights* w, int layer, const float* x, float* x_out, i
   TRY(ensure_scratch(w, n_tok));
   StreamOrder so(w, pick(w->ctx, stream));
   cudaStream_t s = so.s;
-  CU(moe::launch_router_topk(w->router + (size_t)layer * w->E() * w->d(), x, n_tok, w->dims(), ids,
-                             gates, s, false));
   return experts_forward(w, layer, x, n_tok, ids, gates, x_out, nullptr, s, true, nullptr, nullptr,
-                         nullptr);
+                         nullptr, w->router + (size_t)layer * w->E() * w->d());
 }
 
 int moe_forward(moe_weights* w, float* x, int n_tok, int32_t* ids, float* gates, void* stream) {
@@ -1665,6 +1715,7 @@ int moe_forward_launches(moe_weights* w, int n_tok) {
     return 1 + L * (ep && !peer_ok(w) ? 3 : 2);
   // per layer: [permute, gather, up, down] or [up, down], combine, (+add for EP),
   // and the next layer's router
+  if (use_fused_prefill(w, n_tok, nullptr)) return 2 * L;  // router(+dispatch bases), grouped kernel
   const int experts =
       use_prefill(w, n_tok, nullptr) ? (w->prefill_splits > 0 ? 3 : 4) : 2;  // grouped: permute, gather, GEMM
   return 1 + L * (experts + 1 + (ep ? 1 : 0)) + (L - 1);

@@ -97,24 +97,37 @@ __global__ void __launch_bounds__(256) router_topk_kernel(const float* __restric
 }
 
 // Same arithmetic, for d % 256 == 0: the block's token rows and router rows
-// are staged in shared memory by bulk copies (cp.async.bulk, one DRAM round
-// trip per column chunk) instead of each thread's 16+ dependent global loads,
-// which left the per-thread loop latency-bound (~30 us at 512 tokens).
+// are staged in shared memory by bulk copies (cp.async.bulk) through a
+// 2-stage ring of column chunks — both chunks of a d=4096 row are in flight at
+// once — instead of each thread's 16+ dependent global loads, which left the
+// per-thread loop latency-bound (~30 us at 512 tokens).
+//
+// Optional dispatch outputs (rd.blk_base != nullptr; the fused prefill path,
+// launch_route_dispatch): every block records how many of its (token, slot)
+// pairs chose each expert, and the last block to finish turns those into the
+// stable counting sort's bases — counts[e], offsets[e] and
+// blk_base[b][e] = offsets[e] + sum_{b' < b} count[b'][e] — so the grouped
+// kernel can scatter each block's pairs without a separate permute launch.
+// perm[blk_base[b][e] + r] is then the r-th pair of block b that chose e, in
+// pair order: exactly permute_kernel's order.
 constexpr int kRouterChunk = 2048;  // columns per chunk (multiple of 256)
+constexpr int kRouterStages = 2;
 __global__ void __launch_bounds__(256, 1) router_topk_bulk_kernel(const float* __restrict__ router,
                                                                   const float* __restrict__ x,
                                                                   int n_tok, int d, int E, int k,
-                                                                  int32_t* ids, float* gates) {
+                                                                  int32_t* ids, float* gates,
+                                                                  RouteDispatch rd) {
   extern __shared__ float4 rt_smem4[];
-  float* xs = reinterpret_cast<float*>(rt_smem4);  // [kRouterTok][kRouterChunk]
-  float* rs = xs + kRouterTok * kRouterChunk;      // [8][kRouterChunk]
+  constexpr int kStageFloats = (kRouterTok + 8) * kRouterChunk;  // [tok rows | router rows]
+  float* stage_base = reinterpret_cast<float*>(rt_smem4);
   __shared__ float part[8][kRouterTok][8];
   __shared__ float logits[kRouterTok][kMaxExperts];
-  __shared__ __align__(8) uint64_t bar;
+  __shared__ __align__(8) uint64_t bar[kRouterStages];
+  __shared__ int s_last;
   const int tid = threadIdx.x, lane = tid & 31;
   const int warp = warp_uniform(tid >> 5);
   if (tid == 0) {
-    mbar_init(&bar, 1);
+    for (int i = 0; i < kRouterStages; ++i) mbar_init(&bar[i], 1);
     fence_mbar_init();
   }
   __syncthreads();
@@ -122,10 +135,29 @@ __global__ void __launch_bounds__(256, 1) router_topk_bulk_kernel(const float* _
   griddep_launch_dependents();
   const int t0 = blockIdx.x * kRouterTok;
   const int nt = min(kRouterTok, n_tok - t0);
+  if (rd.zero != nullptr)  // the grouped kernel's sync words (it starts after this grid)
+    for (int i = blockIdx.x * 256 + tid; i < rd.n_zero; i += gridDim.x * 256) rd.zero[i] = 0;
   uint64_t pol_keep, pol_norm;
   asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol_keep));
   asm volatile("createpolicy.fractional.L2::evict_normal.b64 %0, 1.0;" : "=l"(pol_norm));
-  uint32_t phase = 0;
+  // steps: (expert group of 8, column chunk), group-major
+  const int nch = (d + kRouterChunk - 1) / kRouterChunk;
+  const int nsteps = ((E + 7) / 8) * nch;
+  auto issue = [&](int st) {
+    if (tid != 0 || st >= nsteps) return;
+    const int e0 = (st / nch) * 8, c0 = (st % nch) * kRouterChunk;
+    const int ne = min(8, E - e0), cw = min(kRouterChunk, d - c0);
+    float* xs = stage_base + (st % kRouterStages) * kStageFloats;
+    float* rs = xs + kRouterTok * kRouterChunk;
+    uint64_t* b = &bar[st % kRouterStages];
+    mbar_arrive_expect_tx(b, (uint32_t)((nt + ne) * cw * 4));
+    for (int t = 0; t < nt; ++t)
+      bulk_g2s(xs + t * kRouterChunk, x + (size_t)(t0 + t) * d + c0, cw * 4, b, pol_norm);
+    for (int j = 0; j < ne; ++j)
+      bulk_g2s(rs + j * kRouterChunk, router + (size_t)(e0 + j) * d + c0, cw * 4, b, pol_keep);
+  };
+  for (int st = 0; st < kRouterStages; ++st) issue(st);
+  int st = 0;
   for (int e0 = 0; e0 < E; e0 += 8) {
     const int ne = min(8, E - e0);
     float acc[8][kRouterTok];
@@ -133,17 +165,11 @@ __global__ void __launch_bounds__(256, 1) router_topk_bulk_kernel(const float* _
     for (int j = 0; j < 8; ++j)
 #pragma unroll
       for (int t = 0; t < kRouterTok; ++t) acc[j][t] = 0.f;
-    for (int c0 = 0; c0 < d; c0 += kRouterChunk) {
+    for (int c0 = 0; c0 < d; c0 += kRouterChunk, ++st) {
       const int cw = min(kRouterChunk, d - c0);
-      if (tid == 0) {
-        mbar_arrive_expect_tx(&bar, (uint32_t)((nt + ne) * cw * 4));
-        for (int t = 0; t < nt; ++t)
-          bulk_g2s(xs + t * kRouterChunk, x + (size_t)(t0 + t) * d + c0, cw * 4, &bar, pol_norm);
-        for (int j = 0; j < ne; ++j)
-          bulk_g2s(rs + j * kRouterChunk, router + (size_t)(e0 + j) * d + c0, cw * 4, &bar, pol_keep);
-      }
-      mbar_wait(&bar, phase);
-      phase ^= 1;
+      const float* xs = stage_base + (st % kRouterStages) * kStageFloats;
+      const float* rs = xs + kRouterTok * kRouterChunk;
+      mbar_wait(&bar[st % kRouterStages], (uint32_t)((st / kRouterStages) & 1));
 #pragma unroll 2
       for (int c = tid; c < cw; c += 256) {
         float xv[kRouterTok];
@@ -156,7 +182,8 @@ __global__ void __launch_bounds__(256, 1) router_topk_bulk_kernel(const float* _
           for (int t = 0; t < kRouterTok; ++t) acc[j][t] = fmaf(r, xv[t], acc[j][t]);
         }
       }
-      __syncthreads();  // the next chunk's copies overwrite xs / rs
+      __syncthreads();  // this stage is refilled next
+      issue(st + kRouterStages);
     }
 #pragma unroll
     for (int j = 0; j < 8; ++j)
@@ -179,6 +206,67 @@ __global__ void __launch_bounds__(256, 1) router_topk_bulk_kernel(const float* _
   }
   for (int t = warp; t < nt; t += 8)
     warp_topk_softmax(logits[t], E, k, ids + (size_t)(t0 + t) * k, gates + (size_t)(t0 + t) * k);
+  if (rd.blk_base == nullptr) return;
+
+  // ---- dispatch bases (fused prefill path) ----
+  __shared__ int32_t s_pid[kRouterTok * 256];  // this block's expert ids (k <= E <= 256)
+  __syncthreads();  // this block's ids (global) visible to the whole block
+  const int npair = nt * k;
+  for (int p = tid; p < npair; p += 256) s_pid[p] = ids[(size_t)t0 * k + p];
+  __syncthreads();
+  for (int e = tid; e < E; e += 256) {
+    int c = 0;
+    for (int p = 0; p < npair; ++p) c += s_pid[p] == e;
+    rd.blk_base[(size_t)blockIdx.x * E + e] = c;
+  }
+  __threadfence();
+  __syncthreads();
+  if (tid == 0) s_last = atomicAdd(rd.done, 1u) == gridDim.x - 1;
+  __syncthreads();
+  if (!s_last) return;
+  __threadfence();
+  // last block: every block's counts into smem (the column-chunk ring is
+  // free now; all loads in flight at once), then per expert an exclusive scan
+  // split into nseg segments of blocks (thread = (expert, segment))
+  __shared__ int seg_sum[256];
+  __shared__ int s_off[kMaxExperts];
+  const int nblk = gridDim.x;
+  const bool in_smem = (size_t)nblk * E <= (size_t)kRouterStages * kStageFloats;
+  int* cnt = in_smem ? reinterpret_cast<int*>(stage_base) : rd.blk_base;
+  if (in_smem)
+    for (int i = tid; i < nblk * E; i += 256) cnt[i] = __ldcg(rd.blk_base + i);
+  __syncthreads();
+  const int nseg = max(1, 256 / E);
+  const int seg_len = (nblk + nseg - 1) / nseg;
+  const int e = tid % E, sg = tid / E;
+  const bool act = tid < E * nseg;
+  int tot = 0;
+  if (act)
+    for (int b = sg * seg_len; b < min(nblk, (sg + 1) * seg_len); ++b) tot += cnt[(size_t)b * E + e];
+  if (act) seg_sum[tid] = tot;
+  __syncthreads();
+  if (tid == 0) {
+    int acc = 0;
+    for (int ee = 0; ee < E; ++ee) {
+      int c = 0;
+      for (int q = 0; q < nseg; ++q) c += seg_sum[q * E + ee];
+      s_off[ee] = acc;
+      rd.counts[ee] = c;
+      rd.offsets[ee] = acc;
+      acc += c;
+    }
+  }
+  __syncthreads();
+  if (act) {
+    int run = s_off[e];
+    for (int q = 0; q < sg; ++q) run += seg_sum[q * E + e];
+    for (int b = sg * seg_len; b < min(nblk, (sg + 1) * seg_len); ++b) {
+      const int c = cnt[(size_t)b * E + e];
+      rd.blk_base[(size_t)b * E + e] = run;
+      run += c;
+    }
+  }
+  if (tid == 0) *rd.done = 0u;  // ready for the next launch (stream-ordered)
 }
 
 cudaError_t launch_router_topk(const float* router, const float* x, int n_tok, const Dims& dm,
@@ -187,17 +275,36 @@ cudaError_t launch_router_topk(const float* router, const float* x, int n_tok, c
   cudaLaunchAttribute attr[1];
   const dim3 grid((n_tok + kRouterTok - 1) / kRouterTok);
   if (dm.d % 256 == 0) {
-    const size_t smem = (size_t)(kRouterTok + 8) * kRouterChunk * sizeof(float);
+    const size_t smem = (size_t)kRouterStages * (kRouterTok + 8) * kRouterChunk * sizeof(float);
     cudaError_t e = cudaFuncSetAttribute(router_topk_bulk_kernel,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
     cudaLaunchConfig_t cfg = make_cfg(grid, dim3(256), s, pdl, attr, smem);
     return cudaLaunchKernelEx(&cfg, router_topk_bulk_kernel, router, x, n_tok, dm.d, dm.E, dm.k,
-                              ids, gates);
+                              ids, gates, RouteDispatch{});
   }
   cudaLaunchConfig_t cfg = make_cfg(grid, dim3(256), s, pdl, attr);
   return cudaLaunchKernelEx(&cfg, router_topk_kernel, router, x, n_tok, dm.d, dm.E, dm.k, ids,
                             gates);
+}
+
+bool route_dispatch_supported(const Dims& dm) { return dm.d % 256 == 0 && dm.E <= 256; }
+int route_blocks(int n_tok) { return (n_tok + kRouterTok - 1) / kRouterTok; }
+int route_block_tokens() { return kRouterTok; }
+
+cudaError_t launch_route_dispatch(const float* router, const float* x, int n_tok, const Dims& dm,
+                                  int32_t* ids, float* gates, const RouteDispatch& rd,
+                                  cudaStream_t s, bool pdl) {
+  if (n_tok <= 0) return cudaSuccess;
+  if (!route_dispatch_supported(dm) || rd.blk_base == nullptr) return cudaErrorInvalidValue;
+  cudaLaunchAttribute attr[1];
+  const size_t smem = (size_t)kRouterStages * (kRouterTok + 8) * kRouterChunk * sizeof(float);
+  cudaError_t e = cudaFuncSetAttribute(router_topk_bulk_kernel,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  cudaLaunchConfig_t cfg = make_cfg(dim3(route_blocks(n_tok)), dim3(256), s, pdl, attr, smem);
+  return cudaLaunchKernelEx(&cfg, router_topk_bulk_kernel, router, x, n_tok, dm.d, dm.E, dm.k, ids,
+                            gates, rd);
 }
 
 // ---- generic SwiGLU up: one warp per (ffn row, token, slot) ---------------
@@ -478,6 +585,88 @@ cudaError_t launch_combine(const float* x, const float* y, const float* gates, i
   const long long sstride = (long long)n_tok * dm.k * dm.d;
   return cudaLaunchKernelEx(&cfg, combine_kernel, x, y, gates, dm.k, dm.d, x_out, nsplit, sstride,
                             ids, split_of);
+}
+
+// Fused prefill combine (kernels.h launch_combine_ready).  Y is written by
+// the concurrently running grouped kernel, so it is read through L2 (ld.cg)
+// after the queue flag's acquire.
+__global__ void __launch_bounds__(256) combine_ready_kernel(const float* x, const float* y, int d,
+                                                            int k, float* x_out, int n_tok,
+                                                            long long sstride,
+                                                            const int32_t* ids,
+                                                            const int32_t* split_of, int* queue) {
+  __shared__ int s_t;
+  const int n4 = d / 4;
+  int slot = threadIdx.x == 0 ? atomicAdd(queue, 1) : 0;  // thread 0 claims one slot ahead
+  while (true) {
+    if (threadIdx.x == 0) {
+      int t = -1;
+      if (slot < n_tok) {
+        int f;
+        do {
+          asm volatile("ld.acquire.gpu.global.s32 %0, [%1];" : "=r"(f) : "l"(queue + 2 + slot) : "memory");
+          if (!f) __nanosleep(128);
+        } while (!f);
+        t = f - 1;
+        slot = atomicAdd(queue, 1);
+      }
+      s_t = t;
+    }
+    __syncthreads();
+    const int t = s_t;
+    __syncthreads();
+    if (t < 0) break;
+    for (int c0 = threadIdx.x; c0 < n4; c0 += blockDim.x * kCombineCols) {
+      float4 acc[kCombineCols], xv[kCombineCols];
+#pragma unroll
+      for (int u = 0; u < kCombineCols; ++u) {
+        acc[u] = make_float4(0.f, 0.f, 0.f, 0.f);
+        const int i4 = c0 + u * blockDim.x;
+        xv[u] = i4 < n4 ? __ldcg(reinterpret_cast<const float4*>(x + (size_t)t * d) + i4) : acc[u];
+      }
+      for (int j = 0; j < k; ++j) {
+        const size_t p = (size_t)t * k + j;
+        const int ns = __ldcg(split_of + __ldcg(ids + p));
+        for (int sp = 0; sp < ns; ++sp) {
+          const float4* r = reinterpret_cast<const float4*>(y + sp * sstride + p * d);
+          float4 v[kCombineCols];
+#pragma unroll
+          for (int u = 0; u < kCombineCols; ++u) {
+            const int i4 = c0 + u * blockDim.x;
+            v[u] = i4 < n4 ? __ldcg(r + i4) : make_float4(0.f, 0.f, 0.f, 0.f);
+          }
+#pragma unroll
+          for (int u = 0; u < kCombineCols; ++u) {
+            acc[u].x += v[u].x;
+            acc[u].y += v[u].y;
+            acc[u].z += v[u].z;
+            acc[u].w += v[u].w;
+          }
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < kCombineCols; ++u) {
+        const int i4 = c0 + u * blockDim.x;
+        if (i4 < n4)
+          reinterpret_cast<float4*>(x_out + (size_t)t * d)[i4] =
+              make_float4(xv[u].x + acc[u].x, xv[u].y + acc[u].y, xv[u].z + acc[u].z, xv[u].w + acc[u].w);
+      }
+    }
+  }
+  griddep_wait();  // completion of this grid implies the grouped kernel's
+}
+
+cudaError_t launch_combine_ready(const float* x, const float* y, int n_tok, const Dims& dm,
+                                 float* x_out, int nsplit, const int32_t* ids, const int32_t* split_of,
+                                 int* queue, int blocks, cudaStream_t s, bool pdl) {
+  if (n_tok <= 0) return cudaSuccess;
+  if (dm.d % 4) return cudaErrorInvalidValue;
+  cudaLaunchAttribute attr[1];
+  cudaLaunchConfig_t cfg = make_cfg(dim3(std::max(1, std::min(blocks, n_tok))), dim3(256), s, pdl, attr);
+  const long long sstride = (long long)n_tok * dm.k * dm.d;
+  (void)nsplit;
+  return cudaLaunchKernelEx(&cfg, combine_ready_kernel, x, y, dm.d, dm.k, x_out, n_tok, sstride, ids,
+                            split_of, queue);
 }
 
 __global__ void add_kernel(const float* a, const float* __restrict__ b, float* out, long long n) {

@@ -25,6 +25,7 @@ struct DebugOptions {
   int force_ep = 0;        // world 1 + NCCL communicator: the EP code path on one GPU
   int no_pdl = 0;          // no programmatic dependent launch anywhere
   int combine4 = 0;        // looped combine instead of combine_k2_kernel
+  int prefill_fused = 1;   // prefill layer as router(+dispatch) -> grouped kernel (+combine)
   int pf_debug = 0, pf_evict = 0, pf_lag = kMaxExperts, pf_late8 = 3, pf_slo = 0, pf_persist = 1;
 };
 DebugOptions& debug_options();
@@ -60,6 +61,24 @@ struct SparsityCounters {
 // ---- router -------------------------------------------------------------
 cudaError_t launch_router_topk(const float* router, const float* x, int n_tok, const Dims& dm,
                                int32_t* ids, float* gates, cudaStream_t s, bool pdl);
+// The router of the fused prefill path: the same routing (bit for bit) plus
+// the stable counting sort's bases per router block (route_block_tokens()
+// tokens each): counts[E], offsets[E], blk_base[route_blocks(n)][E], and the
+// zeroing of n_zero words for the grouped kernel that follows.
+struct RouteDispatch {
+  int32_t* blk_base = nullptr;  // [nblk][E] out
+  int32_t* counts = nullptr;    // [E] out
+  int32_t* offsets = nullptr;   // [E] out
+  unsigned* done = nullptr;     // last-block counter: 0 at launch, left 0
+  int* zero = nullptr;
+  int n_zero = 0;
+};
+bool route_dispatch_supported(const Dims& dm);
+int route_blocks(int n_tok);
+int route_block_tokens();
+cudaError_t launch_route_dispatch(const float* router, const float* x, int n_tok, const Dims& dm,
+                                  int32_t* ids, float* gates, const RouteDispatch& rd,
+                                  cudaStream_t s, bool pdl);
 
 // ---- streaming batch-1 decode (TMA bulk ring) -----------------------------
 struct DecodePlan {
@@ -218,7 +237,38 @@ cudaError_t launch_prefill_experts(const LayerWeights& lw, int n_local, const Di
                                    __nv_bfloat16* xg, __nv_bfloat16* h, float* y, int* sync,
                                    int sm_count, int splits, cudaStream_t s,
                                    const SparsityCounters& sp = SparsityCounters(),
-                                   cudaEvent_t t0 = nullptr, cudaEvent_t t1 = nullptr);
+                                   cudaEvent_t t0 = nullptr, cudaEvent_t t1 = nullptr,
+                                   const struct PrefillFuse* fz = nullptr);
+// The fused single-GPU prefill layer (splits > 0, every expert local): two
+// launches — the router (launch_route_dispatch: ids, gates, counts, offsets,
+// per-block bases) and the grouped kernel, which scatters perm + Xg itself and
+// writes x_out = x + the combined expert outputs (no permute, gather or
+// combine launch).  counts/offsets/perm passed to launch_prefill_experts are
+// then outputs.  sync needs prefill_sync_words(E, n_tok, d) ints.
+struct PrefillFuse {
+  const float* router = nullptr;  // this layer's [E][d]
+  int32_t* ids = nullptr;         // [n_tok][k] out
+  float* gates = nullptr;         // [n_tok][k] out
+  int32_t* route = nullptr;       // [16 + route_blocks(n_tok) * E]: [0] last-block counter, [16..) bases
+  float* x_out = nullptr;         // [n_tok][d] out; may alias x (token t's row is
+                                  // combined only after its own dispatch read it)
+};
+inline size_t prefill_sync_words(int E, int n_tok, int d) {
+  const size_t chunks = (n_tok + kPrefillChunk - 1) / kPrefillChunk;
+  return 1 + (size_t)E * chunks + E /*splits*/ + 1 /*dispatch*/ + E /*x_ready*/ +
+         (size_t)n_tok * (d / 256) /*partials landed*/ + n_tok /*blocks landed*/ +
+         2 + (size_t)n_tok /*combine queue*/;
+}
+// The fused path's combine: launched right behind the grouped kernel (PDL; it
+// starts once every grouped CTA is resident), each block claims queue slots
+// in completion order, waits for the slot's token (published by the down
+// epilogue that landed its last partial) and writes
+// x_out[t] = x[t] + sum over slots (asc) and K splits (asc) of y — combine_k2's
+// adds.  It waits for the grouped grid before exiting, so later launches see
+// both complete.
+cudaError_t launch_combine_ready(const float* x, const float* y, int n_tok, const Dims& dm,
+                                 float* x_out, int nsplit, const int32_t* ids, const int32_t* split_of,
+                                 int* queue, int blocks, cudaStream_t s, bool pdl);
 
 // Replicated experts under expert parallelism (replica_plan.h):
 // one block computes this rank's share [lo, hi) of every expert's sorted rows

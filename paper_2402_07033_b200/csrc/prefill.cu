@@ -408,6 +408,8 @@ __global__ void __launch_bounds__(PF_THREADS, 1)
 // the MMA N).  An expert with more tokens becomes several chunks whose tiles
 // run back to back, so the second read of a weight tile comes from L2.
 constexpr int GP_MAXN = kPrefillChunk;
+constexpr int kRouteItemPairs = 64;  // fused dispatch: max (token, slot) pairs of one router block
+constexpr int kMaxItemTok = 4;       // ... and its tokens (route_block_tokens())
 constexpr int GP_STAGE = 2 * PF_BM * PF_BK * 2 + GP_MAXN * PF_BK * 2;
 constexpr int GP_STAGES = (192 * 1024) / GP_STAGE;
 constexpr int GP_QN = 2;
@@ -415,7 +417,8 @@ constexpr int GP_QN = 2;
 constexpr int GP_STG = 32 * PF_BM * 4;  // 16 KB
 constexpr int GP_SMEM = GP_STAGES * GP_STAGE + GP_STG + 1024 /*align*/ + 256 /*barriers, queue*/ +
                         (6 * kMaxExperts + 1) * 4 /*schedule segments [2E+1] + [2E], splits, chunks [E]*/ +
-                        2 * GP_MAXN * 4 /*down tile: pair index + gate per token row*/;
+                        2 * GP_MAXN * 4 /*down tile: pair index + gate per token row*/ +
+                        (3 * kRouteItemPairs + kMaxExperts / 32 + 2) * 4 /*fused dispatch*/;
 
 struct GroupedArgs {
   const int32_t* counts;
@@ -439,6 +442,23 @@ struct GroupedArgs {
   int late8;            // eighths of the active experts whose downs take the finest split
   int s_lo;             // K split of the other experts' downs (0: S / 2)
   int evict_first;      // weights loaded with an L2 evict_first hint
+  // fused path (fused != 0): the router kernel's blocks are dispatched here
+  // (perm + bf16 Xg scatter, claimed dynamically by the epilogue warps before
+  // their first tile), up tiles wait for their expert's rows, and the down
+  // epilogues count each token's landed partials for the combine kernel,
+  // which runs concurrently (launch_combine with ready flags).
+  int fused;
+  const float* xin;         // [n_tok][d] layer input
+  const int32_t* ids;       // [n_tok][k]
+  const int32_t* blk_base;  // [nblk][E] (launch_route_dispatch)
+  int32_t* perm_w;          // == perm, written by the dispatch
+  __nv_bfloat16* xg;        // [rows][d], written by the dispatch
+  unsigned* disp_ctr;       // dispatch items claimed (zero at launch)
+  int* x_ready;             // [E] sorted rows written (zero at launch)
+  int* tok_cnt;             // [n_tok][d/256] partials landed (zero at launch)
+  int* tok_ready;           // [n_tok] hidden blocks complete (zero at launch)
+  int* cq;                  // combine queue [head][tail][slot: token + 1, n_tok] (zero at launch)
+  int n_tok, nblk, blk_tok;
 };
 
 __device__ __forceinline__ void gp_stamp(const GroupedArgs& a, int i, int field,
@@ -503,6 +523,10 @@ __global__ void __launch_bounds__(PF_THREADS, 1)
   int* s_nch = s_split + kMaxExperts;                // [E] token chunks per expert
   int* s_pair = s_nch + kMaxExperts;                              // [GP_MAXN]
   float* s_gate = reinterpret_cast<float*>(s_pair + GP_MAXN);     // [GP_MAXN]
+  int* s_dpos = reinterpret_cast<int*>(s_gate + GP_MAXN);         // [kRouteItemPairs] dispatch rows
+  int* s_dtok = s_dpos + kRouteItemPairs;                         // [kRouteItemPairs]
+  unsigned* s_xrdy = reinterpret_cast<unsigned*>(s_dtok + 2 * kRouteItemPairs);  // [E/32] producer's bitmask
+  int* s_misc = reinterpret_cast<int*>(s_xrdy + kMaxExperts / 32);           // [2]: claimed item, list size
   __shared__ int s_total;
 
   const int warp = warp_uniform(threadIdx.x >> 5), lane = threadIdx.x & 31;
@@ -534,8 +558,9 @@ __global__ void __launch_bounds__(PF_THREADS, 1)
     const int s_hi = dn_tiles >= 4 * (int)gridDim.x ? 1 : min(a.S, a.f / PF_BK);
     const int s_lo = a.s_lo > 0 ? min(a.s_lo, s_hi) : max(1, s_hi / 2);
     for (int i = 0; i < n_act; ++i) s_split[act[i]] = i >= n_act - n_late ? s_hi : s_lo;
-    if (blockIdx.x == 0)
-      for (int e = 0; e < a.E; ++e) a.split_of[e] = s_split[e];
+    // (every CTA writes the same values: the fused combine reads them after
+    // acquiring flags released by whichever CTA finished a token)
+    for (int e = 0; e < a.E; ++e) a.split_of[e] = s_split[e];
     const int kLag = a.lag;
     int ns = 0, tot = 0;
     auto push = [&](int e, int up) {
@@ -571,6 +596,87 @@ __global__ void __launch_bounds__(PF_THREADS, 1)
   tc_fence_after();
   const uint32_t tmem = *tmem_base_s;
   const int total = s_total;
+  if (a.fused) griddep_launch_dependents();  // the combine kernel runs alongside (ready queue)
+  if (a.fused && warp == 4 && lane == 0)
+    for (int i = 0; i < kMaxExperts / 32; ++i) s_xrdy[i] = 0u;
+  if (a.fused && warp < 4) {
+    // ---- dispatch: router blocks claimed one at a time by the epilogue warps
+    // (the producer meanwhile streams the first tile's weights)
+    const int tpb = a.blk_tok * a.k;
+    int* s_eid = s_dtok + kRouteItemPairs;  // [kRouteItemPairs] the item's expert ids
+    while (true) {
+      if (threadIdx.x == 0) s_misc[0] = (int)atomicAdd(a.disp_ctr, 1u);
+      named_bar_sync(3, 128);
+      const int b = s_misc[0];
+      if (b >= a.nblk) break;
+      const int p0 = b * tpb;
+      const int np = min(tpb, a.n_tok * a.k - p0);
+      int base = 0;
+      if (threadIdx.x < np) {
+        const int e = __ldg(a.ids + p0 + threadIdx.x);
+        s_eid[threadIdx.x] = e;
+        base = __ldg(a.blk_base + (size_t)b * a.E + e);
+      }
+      named_bar_sync(3, 128);
+      if (threadIdx.x < np) {
+        const int p = p0 + threadIdx.x;
+        const int e = s_eid[threadIdx.x];
+        int rank = 0;
+        for (int q = 0; q < (int)threadIdx.x; ++q) rank += s_eid[q] == e;
+        const int pos = base + rank;
+        a.perm_w[pos] = p;
+        s_dpos[threadIdx.x] = pos;
+      }
+      named_bar_sync(3, 128);
+      // the item's token rows, each read once (all its loads in flight), the
+      // bf16 copy written to every sorted row of the token's pairs
+      const int n4 = a.d / 4;
+      const int tb = p0 / a.k, nt = (np + a.k - 1) / a.k;
+      for (int c0 = threadIdx.x; c0 < n4; c0 += 128 * 2) {
+        float4 v[kMaxItemTok][2];
+#pragma unroll
+        for (int tt = 0; tt < kMaxItemTok; ++tt)
+#pragma unroll
+          for (int u = 0; u < 2; ++u) {
+            const int c4 = c0 + u * 128;
+            v[tt][u] = (tt < nt && c4 < n4)
+                           ? __ldg(reinterpret_cast<const float4*>(a.xin + (size_t)(tb + tt) * a.d) + c4)
+                           : make_float4(0.f, 0.f, 0.f, 0.f);
+          }
+#pragma unroll
+        for (int tt = 0; tt < kMaxItemTok; ++tt) {
+          if (tt >= nt) break;
+          for (int j = 0; j < a.k; ++j) {
+            const int i = tt * a.k + j;
+            if (i >= np) break;
+            uint2* dst = reinterpret_cast<uint2*>(a.xg + (size_t)s_dpos[i] * a.d);
+#pragma unroll
+            for (int u = 0; u < 2; ++u) {
+              const int c4 = c0 + u * 128;
+              if (c4 < n4) {
+                const __nv_bfloat162 lo = __floats2bfloat162_rn(v[tt][u].x, v[tt][u].y),
+                                     hi = __floats2bfloat162_rn(v[tt][u].z, v[tt][u].w);
+                dst[c4] = make_uint2(*reinterpret_cast<const uint32_t*>(&lo),
+                                     *reinterpret_cast<const uint32_t*>(&hi));
+              }
+            }
+          }
+        }
+      }
+      __threadfence();
+      named_bar_sync(3, 128);
+      if (threadIdx.x < np) {  // the expert's first pair in this item publishes the item's count
+        const int e = s_eid[threadIdx.x];
+        int before = 0, n_e = 0;
+        for (int q = 0; q < np; ++q) {
+          before += (q < (int)threadIdx.x) & (s_eid[q] == e);
+          n_e += s_eid[q] == e;
+        }
+        if (before == 0)
+          asm volatile("red.release.gpu.global.add.s32 [%0], %1;" ::"l"(a.x_ready + e), "r"(n_e) : "memory");
+      }
+    }
+  }
   const int nkb_up = a.d / PF_BK, nkb_dn = a.f / PF_BK;
   constexpr int kA = PF_BM * PF_BK * 2;
   constexpr int kBox = PF_BOXN * PF_BK * 2;
@@ -620,7 +726,36 @@ __global__ void __launch_bounds__(PF_THREADS, 1)
           const int w1row = (slot * 3 + 0) * a.f + g.t1 * PF_BM;
           const int w3row = (slot * 3 + 1) * a.f + g.t1 * PF_BM;
           const uint32_t bytes = 2 * kA + nboxes * kBox;
-          for (int kb = 0; kb < nkb_up; ++kb, ++kc) {
+          int kb = 0;
+          if (a.fused && !((s_xrdy[g.e >> 5] >> (g.e & 31)) & 1u)) {
+            // first tile of this expert here: weights of the first stages go
+            // out now, the token boxes once every row of the expert is written
+            const int pre = min(nkb_up, GP_STAGES);
+            for (; kb < pre; ++kb) {
+              const int st = (kc + kb) % GP_STAGES;
+              mbar_wait(&empty[st], (((kc + kb) / GP_STAGES) & 1) ^ 1);
+              uint8_t* sp = smem + st * GP_STAGE;
+              mbar_arrive_expect_tx(&full[st], bytes);
+              tma_load_2d_hint(sp, &wmap_up, kb * PF_BK, w1row, &full[st], wpol);
+              tma_load_2d_hint(sp + kA, &wmap_up, kb * PF_BK, w3row, &full[st], wpol);
+            }
+            const int want = a.counts[g.e];
+            int v;
+            do {
+              asm volatile("ld.acquire.gpu.global.s32 %0, [%1];" : "=r"(v) : "l"(a.x_ready + g.e) : "memory");
+              if (v < want) __nanosleep(32);
+            } while (v < want);
+            asm volatile("fence.proxy.async.global;" ::: "memory");
+            s_xrdy[g.e >> 5] |= 1u << (g.e & 31);
+            for (int j = 0; j < pre; ++j) {
+              const int st = (kc + j) % GP_STAGES;
+              uint8_t* sp = smem + st * GP_STAGE;
+              for (int b = 0; b < nboxes; ++b)
+                tma_load_2d(sp + 2 * kA + b * kBox, &xmap, j * PF_BK, srow + b * PF_BOXN, &full[st]);
+            }
+            kc += pre;
+          }
+          for (; kb < nkb_up; ++kb, ++kc) {
             const int st = kc % GP_STAGES;
             mbar_wait(&empty[st], ((kc / GP_STAGES) & 1) ^ 1);
             uint8_t* sp = smem + st * GP_STAGE;
@@ -747,6 +882,15 @@ __global__ void __launch_bounds__(PF_THREADS, 1)
       int nvalid, N, nboxes, srow;
       chunk_geom(g, nvalid, N, nboxes, srow);
       if (!g.up) {
+        if (a.fused) {  // perm rows of this expert were written by the dispatch
+          if (threadIdx.x == 0) {
+            int v;
+            do {
+              asm volatile("ld.acquire.gpu.global.s32 %0, [%1];" : "=r"(v) : "l"(a.x_ready + g.e) : "memory");
+            } while (v < a.counts[g.e]);
+          }
+          named_bar_sync(3, 128);
+        }
         // the rows' pair indices and gates, fetched while the MMAs still run
         for (int j = threadIdx.x; j < nvalid; j += 128) {
           const int p = __ldg(a.perm + srow + j);
@@ -827,6 +971,29 @@ __global__ void __launch_bounds__(PF_THREADS, 1)
               }
             }
             named_bar_sync(3, 128);
+          }
+        }
+        if (a.fused) {
+          // (token, hidden tile) blocks whose last partial this tile landed:
+          // once all of a token's blocks are in, tok_ready[t] reaches d/256
+          // and the concurrently running combine kernel (launched early, PDL)
+          // sums that token's partials
+          __threadfence();
+          named_bar_sync(3, 128);
+          const int n_ht = a.d / (2 * PF_BM);
+          for (int j = threadIdx.x; j < nvalid; j += 128) {
+            const int t = s_pair[j] / a.k;
+            int target = 0;
+            for (int jj = 0; jj < a.k; ++jj) target += s_split[__ldg(a.ids + (size_t)t * a.k + jj)];
+            if (atomicAdd(a.tok_cnt + (size_t)t * n_ht + g.t1, 1) == target - 1) {
+              __threadfence();  // acquire the other tiles' partials, release them onwards
+              if (atomicAdd(a.tok_ready + t, 1) == n_ht - 1) {
+                // the token's last block: publish it to the combine queue
+                __threadfence();
+                const int qi = atomicAdd(a.cq + 1, 1);
+                asm volatile("st.release.gpu.global.s32 [%0], %1;" ::"l"(a.cq + 2 + qi), "r"(t + 1) : "memory");
+              }
+            }
           }
         }
       }
@@ -961,9 +1128,13 @@ cudaError_t launch_prefill_experts(const LayerWeights& lw, int n_local, const Di
                                    const float* gates, const int16_t* slot_of_dev,
                                    __nv_bfloat16* xg, __nv_bfloat16* h, float* y, int* sync,
                                    int sm_count, int splits, cudaStream_t s,
-                                   const SparsityCounters& sp, cudaEvent_t t0, cudaEvent_t t1) {
+                                   const SparsityCounters& sp, cudaEvent_t t0, cudaEvent_t t1,
+                                   const PrefillFuse* fz) {
   const int rows = n_tok * dm.k;
   if (rows == 0 || n_local == 0) return cudaSuccess;
+  if (fz && (splits <= 0 || n_local != dm.E || !route_dispatch_supported(dm) ||
+             route_block_tokens() * dm.k > kRouteItemPairs || route_block_tokens() > kMaxItemTok))
+    return cudaErrorInvalidValue;
   // an expert holds <= n_tok tokens; the grouped kernel's done flags are per
   // GP_MAXN-token chunk, the two-kernel path's grid per PF_MAXN
   const int chunks = (n_tok + GP_MAXN - 1) / GP_MAXN;
@@ -980,8 +1151,21 @@ cudaError_t launch_prefill_experts(const LayerWeights& lw, int n_local, const Di
   gcfg.attrs = pdl_attr;
   gcfg.numAttrs = no_pdl ? 0 : 1;
   const int n_zero = splits > 0 ? 1 + dm.E * chunks : 0;
-  cudaError_t err = cudaLaunchKernelEx(&gcfg, gather_rows_kernel, x, perm, rows, dm.k, dm.d, xg,
-                                       sync, n_zero);  // d % 128 == 0
+  cudaError_t err;
+  int* const fsync = sync + 1 + dm.E * chunks + dm.E;  // fused: [dispatch][x_ready E][combine counters]
+  if (fz) {
+    RouteDispatch rd;
+    rd.blk_base = fz->route + 16;
+    rd.counts = const_cast<int32_t*>(counts);
+    rd.offsets = const_cast<int32_t*>(offsets);
+    rd.done = reinterpret_cast<unsigned*>(fz->route);
+    rd.zero = sync;
+    rd.n_zero = (int)prefill_sync_words(dm.E, n_tok, dm.d);
+    err = launch_route_dispatch(fz->router, x, n_tok, dm, fz->ids, fz->gates, rd, s, !no_pdl);
+  } else {
+    err = cudaLaunchKernelEx(&gcfg, gather_rows_kernel, x, perm, rows, dm.k, dm.d, xg, sync,
+                             n_zero);  // d % 128 == 0
+  }
   if (err != cudaSuccess) return err;
   CUtensorMap wmap_up, wmap_dn, xmap, hmap;
   const long long wrows = 3LL * n_local * dm.f;
@@ -1020,6 +1204,20 @@ cudaError_t launch_prefill_experts(const LayerWeights& lw, int n_local, const Di
     g.lag = debug_options().pf_lag;
     g.late8 = debug_options().pf_late8;
     g.s_lo = debug_options().pf_slo;
+    g.fused = fz != nullptr;
+    g.xin = x;
+    g.ids = fz ? fz->ids : nullptr;
+    g.blk_base = fz ? fz->route + 16 : nullptr;
+    g.perm_w = const_cast<int32_t*>(perm);
+    g.xg = xg;
+    g.disp_ctr = reinterpret_cast<unsigned*>(fsync);
+    g.x_ready = fsync + 1;
+    g.tok_cnt = fsync + 1 + dm.E;
+    g.tok_ready = fsync + 1 + dm.E + n_tok * (dm.d / 256);
+    g.cq = g.tok_ready + n_tok;
+    g.n_tok = n_tok;
+    g.nblk = route_blocks(n_tok);
+    g.blk_tok = route_block_tokens();
     g.trace = nullptr;
     g.trace_cap = 0;
     const char* trace_path = debug_trace_path()[0] ? debug_trace_path() : nullptr;
@@ -1031,7 +1229,7 @@ cudaError_t launch_prefill_experts(const LayerWeights& lw, int n_local, const Di
       if ((err = cudaMemsetAsync(trace_buf, 0, tb, s)) != cudaSuccess) return err;
       g.trace = trace_buf;
     }
-    // (sync words zeroed by the gather kernel)
+    // (sync words zeroed by the gather kernel, or by the router on the fused path)
     auto kern = sp.counts ? prefill_grouped_kernel<true> : prefill_grouped_kernel<false>;
     err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, GP_SMEM);
     if (err != cudaSuccess) return err;
@@ -1107,6 +1305,9 @@ cudaError_t launch_prefill_experts(const LayerWeights& lw, int n_local, const Di
     if (t0 && (err = cudaEventRecord(t0, s)) != cudaSuccess) return err;
     err = cudaLaunchKernelEx(&kcfg, kern, wmap_up, wmap_dn, xmap, hmap, g);
     if (err == cudaSuccess && t1) err = cudaEventRecord(t1, s);
+    if (err == cudaSuccess && fz)
+      err = launch_combine_ready(x, y, n_tok, dm, fz->x_out, splits, fz->ids, g.split_of, g.cq,
+                                 sm_count, s, !no_pdl && !t1);
     if (err != cudaSuccess || !trace_path) return err;
     // diagnostics only: synchronous dump (appends one record per launch)
     const size_t n = (size_t)sm_count * g.trace_cap * 4;

@@ -22,6 +22,7 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--tokens", type=int, default=512)
     ap.add_argument("--reps", type=int, default=3)
+    ap.add_argument("--opt", action="append", default=[], help="library debug option name=value")
     args = ap.parse_args()
     path = os.path.join(tempfile.mkdtemp(), "pf_trace.bin")
     import torch
@@ -29,6 +30,9 @@ def main():
     import paper_2402_07033_b200 as M
 
     n, d, f, E, k = args.tokens, 4096, 14336, 8, 2
+    for o in args.opt:
+        name, val = o.split("=")
+        M.set_option(name, int(val))
     ctx = M.Ctx(0)
     w = M.Weights(ctx, M.Shape(1, E, k, d, f, 2), M.DTYPE_BF16)
     w.random(0)
