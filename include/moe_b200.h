@@ -259,6 +259,19 @@ int moe_forward_sparsity(moe_weights* w, float* x, int n_tok, int32_t* ids, floa
  * [n_tok x L x k x ffn] in the reference's sink call order. */
 int moe_forward_host(moe_weights* w, const double* tokens, int n_tok, double* out,
                      int32_t* ids, double* gates, double* post_silu);
+/* Pipelined host-buffer steps (no synchronize): enqueue the H2D of x_host
+ * (fp32 [n_tok x hidden], pinned for overlap), one layer (layer >= 0:
+ * moe_layer_forward; ids/gates [n_tok x k]) or the whole stack (layer == -1:
+ * moe_forward; ids/gates [L x n_tok x k]) and the D2H of the result and the
+ * routing, and return.  Copies run on their own streams, so the copies of
+ * consecutive calls overlap the previous / next call's compute (two device
+ * staging slots).  *ticket identifies the call; moe_host_wait(w, ticket)
+ * blocks until its outputs are in host memory (ticket < 0: every call).  The
+ * host buffers must stay valid until then. */
+int moe_forward_host_async(moe_weights* w, int layer, const float* x_host, int n_tok,
+                           float* out_host, int32_t* ids_host, float* gates_host,
+                           int64_t* ticket);
+int moe_host_wait(moe_weights* w, int64_t ticket);
 /* expert_ffn (model.cpp:55-67) on one host expert (uploaded per call). */
 int moe_expert_ffn_host(moe_ctx* ctx, int dtype, int hidden, int ffn, const double* w_in,
                         const double* w_gate, const double* w_out, const double* x,

@@ -122,6 +122,8 @@ def lib():
         "moe_forward": ([_vp, _vp, C.c_int, _vp, _vp, _vp], C.c_int),
         "moe_forward_sparsity": ([_vp, _vp, C.c_int, _vp, _vp, _dp, C.c_int, _vp, _vp], C.c_int),
         "moe_forward_host": ([_vp, _dp, C.c_int, _dp, _i32p, _dp, _dp], C.c_int),
+        "moe_forward_host_async": ([_vp, C.c_int, _vp, C.c_int, _vp, _vp, _vp, C.POINTER(C.c_int64)], C.c_int),
+        "moe_host_wait": ([_vp, C.c_int64], C.c_int),
         "moe_expert_ffn_host": ([_vp, C.c_int, C.c_int, C.c_int, _dp, _dp, _dp, _dp, _dp], C.c_int),
         "moe_gate_topk_host": ([_vp, C.c_int, C.c_int, _dp, _dp, C.c_int, _i32p, _dp], C.c_int),
         "moe_expert_path": ([_vp, C.c_int], C.c_int),
@@ -181,6 +183,15 @@ def set_trace_path(path: str | None) -> None:
 
 def _dptr(a: np.ndarray):
     return a.ctypes.data_as(_dp)
+
+
+def _hptr(a):
+    """Host pointer of a CPU torch tensor or numpy array (contiguous)."""
+    if isinstance(a, np.ndarray):
+        assert a.flags["C_CONTIGUOUS"]
+        return C.c_void_p(a.ctypes.data)
+    assert not a.is_cuda and a.is_contiguous()
+    return C.c_void_p(a.data_ptr())
 
 
 def _ptr(t):
@@ -461,6 +472,19 @@ class Weights:
         thr = np.ascontiguousarray(thresholds, np.float64)
         check(lib().moe_forward_sparsity(self.h, _ptr(x), x.shape[0], _ptr(ids), _ptr(gates), _dptr(thr),
                                          len(thr), _ptr(counts), _stream(stream, x)))
+
+    def forward_host_async(self, layer, x_host, out_host, ids_host, gates_host) -> int:
+        """Pipelined host-buffer step (moe_forward_host_async): fp32 host
+        tensors/arrays (pinned for overlap) [n x hidden]; layer -1 = the whole
+        stack.  Returns the ticket for host_wait()."""
+        t = C.c_int64()
+        n = x_host.shape[0]
+        check(lib().moe_forward_host_async(self.h, layer, _hptr(x_host), n, _hptr(out_host), _hptr(ids_host),
+                                           _hptr(gates_host), C.byref(t)))
+        return t.value
+
+    def host_wait(self, ticket: int = -1):
+        check(lib().moe_host_wait(self.h, ticket))
 
     def forward_host(self, tokens: np.ndarray, with_post=False):
         s = self.shape

@@ -203,6 +203,14 @@ struct moe_weights {
   // it (StreamOrder).  w->mu only serialises the enqueueing.
   cudaStream_t last_stream = nullptr;
   cudaEvent_t order_ev = nullptr;
+  // moe_forward_host_async: two staging slots, copy streams in / out
+  struct MoeHostAsyncT {
+    cudaStream_t cin = nullptr, cout = nullptr;
+    DevBuf x[2], y[2], ids[2], gates[2];
+    cudaEvent_t in_done[2] = {}, comp_done[2] = {}, out_done[2] = {};
+    int64_t next = 0;
+  } ha;
+  using MoeHostAsync = MoeHostAsyncT;
   std::mutex mu;
 
   int L() const { return shape.num_layers; }
@@ -1192,6 +1200,15 @@ int moe_weights_destroy(moe_weights* w) {
   if (w->cap_stream) cudaStreamDestroy(w->cap_stream);
   if (w->io_stream) cudaStreamDestroy(w->io_stream);
   if (w->order_ev) cudaEventDestroy(w->order_ev);
+  if (w->ha.cin) cudaStreamSynchronize(w->ha.cin);
+  if (w->ha.cout) cudaStreamSynchronize(w->ha.cout);
+  for (int i = 0; i < 2; ++i) {
+    for (cudaEvent_t e : {w->ha.in_done[i], w->ha.comp_done[i], w->ha.out_done[i]})
+      if (e) cudaEventDestroy(e);
+    for (DevBuf* b : {&w->ha.x[i], &w->ha.y[i], &w->ha.ids[i], &w->ha.gates[i]}) b->release();
+  }
+  if (w->ha.cin) cudaStreamDestroy(w->ha.cin);
+  if (w->ha.cout) cudaStreamDestroy(w->ha.cout);
   for (DevBuf& b : w->rw_mem) b.release();
   w->dev_rw.release();
   for (void* p : w->layer_mem)
@@ -1464,6 +1481,89 @@ int moe_forward(moe_weights* w, float* x, int n_tok, int32_t* ids, float* gates,
     return forward_graph(w, x, ids, gates, s);
   }
   return enqueue_forward(w, x, n_tok, ids, gates, s, nullptr);
+}
+
+// Pipelined host-buffer steps: H2D of call i+1 and D2H of call i-1 run on
+// their own copy streams while call i computes (two device staging slots).
+int moe_forward_host_async(moe_weights* w, int layer, const float* x_host, int n_tok,
+                           float* out_host, int32_t* ids_host, float* gates_host, int64_t* ticket) {
+  if (!w) return fail(MOE_ERR_ARG, "null weights");
+  if (layer < -1 || layer >= w->L()) return fail(MOE_ERR_ARG, "layer out of range");
+  if (n_tok < 0) return fail(MOE_ERR_ARG, "n_tok < 0");
+  if (n_tok > 0 && (!x_host || !out_host || !ids_host || !gates_host))
+    return fail(MOE_ERR_ARG, "null pointer");
+  std::lock_guard<std::mutex> lk(w->mu);
+  TRY(set_device(w->ctx));
+  moe_weights::MoeHostAsync& ha = w->ha;
+  if (!ha.cin) {
+    if (cudaStreamCreateWithFlags(&ha.cin, cudaStreamNonBlocking) != cudaSuccess ||
+        cudaStreamCreateWithFlags(&ha.cout, cudaStreamNonBlocking) != cudaSuccess)
+      return fail(MOE_ERR_CUDA, "create copy streams");
+    for (int i = 0; i < 2; ++i)
+      for (cudaEvent_t* e : {&ha.in_done[i], &ha.comp_done[i], &ha.out_done[i]})
+        CU(cudaEventCreateWithFlags(e, cudaEventDisableTiming));
+  }
+  const int64_t t = ha.next;
+  if (ticket) *ticket = t;
+  if (n_tok == 0) return MOE_OK;
+  const int slot = (int)(t & 1);
+  const int nl = layer < 0 ? w->L() : 1;
+  const size_t nx = (size_t)n_tok * w->d(), nr = (size_t)nl * n_tok * w->k();
+  TRY(ensure_scratch(w, n_tok));
+  TRY(refresh_projection(w));
+  // a slot's buffers are reused only after its previous D2H landed (the
+  // compute below waits for that too)
+  const size_t ny = layer >= 0 ? nx : 0;  // one layer: separate output (the stack runs in place)
+  if (ha.x[slot].bytes < nx * 4 || ha.y[slot].bytes < ny * 4 || ha.ids[slot].bytes < nr * 4 ||
+      ha.gates[slot].bytes < nr * 4) {
+    CU(cudaEventSynchronize(ha.out_done[slot]));
+    TRY(ha.x[slot].ensure(nx * 4));
+    if (ny) TRY(ha.y[slot].ensure(ny * 4));
+    TRY(ha.ids[slot].ensure(nr * 4));
+    TRY(ha.gates[slot].ensure(nr * 4));
+  }
+  float* dx = ha.x[slot].as<float>();
+  float* dy = layer >= 0 ? ha.y[slot].as<float>() : dx;
+  int32_t* dids = ha.ids[slot].as<int32_t>();
+  float* dg = ha.gates[slot].as<float>();
+  // in: the slot's previous compute has consumed its tokens and its previous
+  // results have left (the layer writes them in place)
+  CU(cudaStreamWaitEvent(ha.cin, ha.comp_done[slot], 0));
+  CU(cudaStreamWaitEvent(ha.cin, ha.out_done[slot], 0));
+  CU(cudaMemcpyAsync(dx, x_host, nx * 4, cudaMemcpyHostToDevice, ha.cin));
+  CU(cudaEventRecord(ha.in_done[slot], ha.cin));
+  {
+    StreamOrder so(w, w->io_stream);
+    cudaStream_t s = so.s;
+    CU(cudaStreamWaitEvent(s, ha.in_done[slot], 0));
+    if (layer >= 0) {
+      TRY(experts_forward(w, layer, dx, n_tok, dids, dg, dy, nullptr, s, true, nullptr, nullptr,
+                          nullptr, w->router + (size_t)layer * w->E() * w->d()));
+    } else if (n_tok == 1 && w->plan.ok) {
+      TRY(forward_graph(w, dx, dids, dg, s));
+    } else {
+      TRY(enqueue_forward(w, dx, n_tok, dids, dg, s, nullptr));
+    }
+    CU(cudaEventRecord(ha.comp_done[slot], s));
+  }
+  CU(cudaStreamWaitEvent(ha.cout, ha.comp_done[slot], 0));
+  CU(cudaMemcpyAsync(out_host, dy, nx * 4, cudaMemcpyDeviceToHost, ha.cout));
+  CU(cudaMemcpyAsync(ids_host, dids, nr * 4, cudaMemcpyDeviceToHost, ha.cout));
+  CU(cudaMemcpyAsync(gates_host, dg, nr * 4, cudaMemcpyDeviceToHost, ha.cout));
+  CU(cudaEventRecord(ha.out_done[slot], ha.cout));
+  ha.next = t + 1;
+  return MOE_OK;
+}
+
+int moe_host_wait(moe_weights* w, int64_t ticket) {
+  if (!w) return fail(MOE_ERR_ARG, "null weights");
+  std::lock_guard<std::mutex> lk(w->mu);
+  if (!w->ha.cout || ticket >= w->ha.next) return MOE_OK;
+  TRY(set_device(w->ctx));
+  // out is in-order: the slot's latest D2H covers every earlier ticket of it
+  if (ticket < 0) CU(cudaStreamSynchronize(w->ha.cout));
+  else CU(cudaEventSynchronize(w->ha.out_done[ticket & 1]));
+  return MOE_OK;
 }
 
 int moe_forward_sparsity(moe_weights* w, float* x, int n_tok, int32_t* ids, float* gates,
