@@ -3,10 +3,13 @@
 Two processes (one rank each, gloo for the host-side handshake, as
 bench.py does under torchrun) map each other's exchange windows with
 cudaIpcOpenMemHandle and run a tensor-parallel model whose per-layer
-combine goes through those windows.  Here both processes share one GPU, so
-their kernels are time-sliced rather than concurrent; the bounded waits make
-progress at each slice.  Each rank checks its output against the unsharded
-model computed locally.
+combine goes through those windows.  With one GPU both processes share it,
+so their kernels are time-sliced rather than concurrent; the bounded waits
+make progress at each slice.  The *_cross_device cases run automatically
+when >= 2 GPUs are visible: rank r on GPU r, the exchange over NVLink P2P
+(and the NCCL all-reduce path, comm="nccl", over a 2-rank communicator).
+Each rank checks its output against the unsharded model computed locally
+on its own GPU.
 """
 import os
 import socket
@@ -26,7 +29,7 @@ def _free_port():
     return p
 
 
-def _rank_main(rank, world, port, q, kernel, mode):
+def _rank_main(rank, world, port, q, kernel, mode, dev=0, comm="peer"):
     import sys
 
     sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
@@ -34,6 +37,7 @@ def _rank_main(rank, world, port, q, kernel, mode):
 
     import paper_2402_07033_b200 as M
 
+    torch.cuda.set_device(dev)
     if kernel == "layer":
         M.set_option("stack", 0)  # per-layer kernels + reduce_exchange
 
@@ -42,22 +46,28 @@ def _rank_main(rank, world, port, q, kernel, mode):
                                 world_size=world)
         L, E, k, d, f = 2, 8, 2, 512, 1792
         s = M.Shape(L, E, k, d, f, 4)
-        base = M.Ctx(0)
+        base = M.Ctx(dev)
         full = M.Weights(base, s, M.DTYPE_F32)
         full.random(3)
-        ctx = M.Ctx(0)
-        handles = [None] * world
-        dist.all_gather_object(handles, ctx.peer_window(world, d, max_tokens=16))
-        ctx.open_peers(world, rank, handles)
+        ctx = M.Ctx(dev)
+        if comm == "peer":
+            handles = [None] * world
+            dist.all_gather_object(handles, ctx.peer_window(world, d, max_tokens=16))
+            ctx.open_peers(world, rank, handles)
+        else:  # NCCL all-reduce combine over a world-rank communicator
+            uid = [M.Ctx.unique_id() if rank == 0 else None]
+            dist.broadcast_object_list(uid, src=0)
+            ctx.init_ep(world, rank, uid[0])
         if mode == "tp":
             w = M.Weights(ctx, s, M.DTYPE_F32, tp=True)
         else:
             owner = np.array([[e % world for e in range(E)] for _ in range(L)], np.int32)
             w = M.Weights(ctx, s, M.DTYPE_F32, owner=owner)
-        assert w.forward_launches(1) == (1 if kernel == "stack" else 1 + 2 * L)
+        if comm == "peer":
+            assert w.forward_launches(1) == (1 if kernel == "stack" else 1 + 2 * L)
         w.reserve(1)
         w.random(3)
-        gen = torch.Generator(device="cuda").manual_seed(5)
+        gen = torch.Generator(device=f"cuda:{dev}").manual_seed(5)
         x0 = torch.randn(2, d, device="cuda", generator=gen)
         x = torch.empty(1, d, device="cuda")
         ids = torch.zeros((L, 1, k), dtype=torch.int32, device="cuda")
@@ -74,13 +84,14 @@ def _rank_main(rank, world, port, q, kernel, mode):
             dist.barrier()
             w.forward(x, ids, g, stream=ctx.stream)
             ctx.synchronize()
-            ctx.peer_check()
+            if comm == "peer":
+                ctx.peer_check()
             want = (xr - x0[t:t + 1]).double().cpu().numpy()
             got = (x - x0[t:t + 1]).double().cpu().numpy()
             errs.append(float(np.abs(got - want).max() / np.abs(want).max()))
             assert torch.equal(ids, idr)
         # a 16-token (prefill) layer: the multi-token peer allreduce
-        xm = torch.randn(16, d, device="cuda", generator=torch.Generator(device="cuda").manual_seed(9))
+        xm = torch.randn(16, d, device="cuda", generator=torch.Generator(device=f"cuda:{dev}").manual_seed(9))
         wm = torch.empty_like(xm)
         full.layer_forward(0, xm, wm, torch.zeros((16, k), dtype=torch.int32, device="cuda"),
                            torch.zeros((16, k), device="cuda"), stream=base.stream)
@@ -93,7 +104,8 @@ def _rank_main(rank, world, port, q, kernel, mode):
         dist.barrier()
         w.layer_forward(0, xm, om, idm, gm, stream=ctx.stream)
         ctx.synchronize()
-        ctx.peer_check()
+        if comm == "peer":
+            ctx.peer_check()
         dm_, dw_ = (om - xm).double(), (wm - xm).double()
         errs.append(float((dm_ - dw_).abs().max() / dw_.abs().max()))
         q.put((rank, max(errs), None))
@@ -107,16 +119,14 @@ def _rank_main(rank, world, port, q, kernel, mode):
         q.put((rank, None, repr(e)))
 
 
-@pytest.mark.parametrize("kernel,mode", [("layer", "tp"), ("stack", "tp"), ("stack", "ep")])
-def test_two_process_ipc(kernel, mode):
-    if not torch.cuda.is_available():
-        pytest.skip("no GPU")
+def _run_two(kernel, mode, cross, comm="peer"):
     import torch.multiprocessing as mp
 
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_rank_main, args=(r, 2, port, q, kernel, mode)) for r in range(2)]
+    procs = [ctx.Process(target=_rank_main, args=(r, 2, port, q, kernel, mode, r if cross else 0, comm))
+             for r in range(2)]
     for p in procs:
         p.start()
     res = [q.get(timeout=300) for _ in procs]
@@ -125,3 +135,20 @@ def test_two_process_ipc(kernel, mode):
     for rank, err, exc in res:
         assert exc is None, f"rank {rank}: {exc}"
         assert err < 1e-4, (rank, err)
+
+
+@pytest.mark.parametrize("kernel,mode", [("layer", "tp"), ("stack", "tp"), ("stack", "ep")])
+def test_two_process_ipc(kernel, mode):
+    if not torch.cuda.is_available():
+        pytest.skip("no GPU")
+    _run_two(kernel, mode, cross=False)
+
+
+@pytest.mark.parametrize("kernel,mode,comm", [("layer", "tp", "peer"), ("stack", "tp", "peer"),
+                                              ("stack", "ep", "peer"), ("layer", "ep", "nccl")])
+def test_two_process_cross_device(kernel, mode, comm):
+    """Runs only with >= 2 visible GPUs: the NVLink peer exchange (or the
+    2-rank NCCL all-reduce) between two real devices."""
+    if not torch.cuda.is_available() or torch.cuda.device_count() < 2:
+        pytest.skip("needs 2 GPUs")
+    _run_two(kernel, mode, cross=True, comm=comm)
