@@ -1,6 +1,6 @@
 // replica_plan.h — per-step token split of replicated experts over the ranks
 // that hold them.  Shared by the device planner kernel
-// (prefill.cu), the host entry point moe_replica_plan (capi.cu) and tests.
+// (prefill.cu), the host entry point moe_replica_plan (capi_weights.cu) and tests.
 //
 // The reference's scheduler (scheduler.cpp:97-204) splits one layer's active
 // experts between two devices so that max(slow_sum, fast_sum) is minimal, ties

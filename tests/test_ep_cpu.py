@@ -1,6 +1,6 @@
 """Expert-parallel host logic on CPU, world_size 2 over gloo.
 
-The GPU EP path (capi.cu experts_forward with world > 1) is:
+The GPU EP path (capi_orch.cu experts_forward with world > 1) is:
   every rank routes x identically (replicated fp32 router) -> each rank computes
   only the gate-weighted outputs of the experts it owns -> all-reduce(sum) of the
   d-vector delta -> x += delta -> next layer.

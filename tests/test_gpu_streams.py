@@ -1,7 +1,7 @@
 """One moe_weights used from several CUDA streams (the scratch,
 the persistent kernels' barrier words and the captured graphs are per
 weights).  Calls on different streams are ordered by the library
-(capi.cu StreamOrder), so back-to-back calls on alternating streams with no
+(capi_internal.h StreamOrder), so back-to-back calls on alternating streams with no
 host synchronisation give the serial results bit for bit — for the batch-1
 persistent stack kernel, the per-layer decode path and the multi-token
 (tcgen05 prefill) path.
