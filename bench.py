@@ -823,6 +823,8 @@ def main():
                     help="per-layer 2-kernel graph instead of the persistent stack kernel")
     ap.add_argument("--stack-kernel", type=int, default=0, choices=[0, 1, 2, 3],
                     help="A/B: 1 = two-barrier persistent kernel, 2 = single-barrier fixed-point kernel (default)")
+    ap.add_argument("--opt", action="append", default=[], metavar="NAME=VALUE",
+                    help="A/B: set a library debug option (moe_debug_set_option)")
     ap.add_argument("--force-ep", action="store_true",
                     help="testing: 1-rank NCCL communicator (the expert-parallel code path on one GPU)")
     ap.add_argument("--traffic", type=float, default=None,
@@ -851,6 +853,9 @@ def main():
             M.set_option("stack", 0)
         if args.stack_kernel:
             M.set_option("stack_kernel", args.stack_kernel)
+        for o in args.opt:  # A/B: any library debug option
+            name, val = o.split("=")
+            M.set_option(name, int(val))
         if args.force_ep:
             M.set_option("force_ep", 1)
     if args.impl == "reference":

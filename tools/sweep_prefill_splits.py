@@ -20,7 +20,8 @@ def main():
     ap.add_argument("--tokens", type=int, default=512)
     ap.add_argument("--rounds", type=int, default=3)
     ap.add_argument("--iters", type=int, default=20)
-    ap.add_argument("--cfgs", default="2:3,4:2,4:3,3:3,2:8,4:8,1:0")
+    ap.add_argument("--cfgs", default="2:3,4:2,4:3,3:3,2:8,4:8,1:0",
+                    help="S:late8[:slo] (slo = K split of the other experts' downs, 0 = S/2)")
     args = ap.parse_args()
     import torch
 
@@ -30,7 +31,7 @@ def main():
     ctx = M.Ctx(0)
     sp = ctx.stream
     st = torch.cuda.ExternalStream(sp)
-    cfgs = [tuple(int(v) for v in c.split(":")) for c in args.cfgs.split(",")]
+    cfgs = [tuple(int(v) for v in (c + ":0" if c.count(":") == 1 else c).split(":")) for c in args.cfgs.split(",")]
     ws = {}
     for S in sorted({c[0] for c in cfgs}):
         M.set_option("prefill_splits", S)
@@ -48,8 +49,9 @@ def main():
     times = {c: [] for c in cfgs}
     for _ in range(args.rounds):
         for c in cfgs:
-            S, late = c
+            S, late, slo = c
             M.set_option("pf_late8", late)
+            M.set_option("pf_slo", slo)
             w = ws[S]
             for i in range(3):
                 w.layer_forward(0, xs[i % 8], xo, ids, g, stream=sp)
@@ -62,7 +64,8 @@ def main():
             torch.cuda.synchronize()
             times[c].append(e0.elapsed_time(e1) / args.iters * 1e3)
     M.set_option("pf_late8", 3)
-    print(json.dumps({f"splits{c[0]}_late{c[1]}": round(float(np.median(v)), 1) for c, v in times.items()},
+    M.set_option("pf_slo", 0)
+    print(json.dumps({f"splits{c[0]}_late{c[1]}_slo{c[2]}": round(float(np.median(v)), 1) for c, v in times.items()},
                      indent=1))
 
 
