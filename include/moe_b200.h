@@ -286,6 +286,9 @@ int moe_gate_topk_host(moe_ctx* ctx, int n_experts, int hidden, const double* ro
 int moe_expert_path(moe_weights* w, int n_tok);
 /* Number of kernels one moe_forward(n_tok) launches. */
 int moe_forward_launches(moe_weights* w, int n_tok);
+/* Number of kernels one moe_layer_forward(n_tok) launches (1 at batch 1 on
+ * one GPU: the persistent kernel as a 1-layer stack). */
+int moe_layer_launches(moe_weights* w, int n_tok);
 /* Diagnostics: one batch-1 moe_forward through the persistent stack kernel
  * with per-CTA clock64 stamps (tools/trace_stack.py).  trace receives
  * [L][sm_count][16] u64 (slot meanings in tools/trace_stack.py).  Synchronous. */

@@ -128,6 +128,7 @@ def lib():
         "moe_gate_topk_host": ([_vp, C.c_int, C.c_int, _dp, _dp, C.c_int, _i32p, _dp], C.c_int),
         "moe_expert_path": ([_vp, C.c_int], C.c_int),
         "moe_forward_launches": ([_vp, C.c_int], C.c_int),
+        "moe_layer_launches": ([_vp, C.c_int], C.c_int),
         "moe_debug_trace_forward": ([_vp, _vp, _vp, _vp, C.POINTER(C.c_uint64), C.c_int64], C.c_int),
         "moe_forward_logits": ([_vp, _vp, _vp, _vp, _vp, _vp], C.c_int),
         "moe_debug_set_option": ([C.c_char_p, C.c_int64], C.c_int),
@@ -519,6 +520,9 @@ class Weights:
 
     def forward_launches(self, n_tok: int) -> int:
         return lib().moe_forward_launches(self.h, n_tok)
+
+    def layer_launches(self, n_tok: int) -> int:
+        return lib().moe_layer_launches(self.h, n_tok)
 
 
 def replica_plan(counts, holders, world, weight_ps, row_ps, part_ps, chunk, rank):

@@ -454,6 +454,16 @@ int moe_forward_logits(moe_weights* w, float* x, int32_t* ids, float* gates, flo
   return enqueue_stack(w, x, ids, gates, so.s, nullptr, logits);
 }
 
+int moe_layer_launches(moe_weights* w, int n_tok) {
+  if (!w || n_tok <= 0 || w->L() == 0) return 0;
+  if (use_layer_stack(w, n_tok, nullptr)) return 1;         // the 1-layer persistent stack
+  if (use_decode(w, n_tok, nullptr))                         // router, experts, reduce (+ EP exchange)
+    return w->ctx->ep() && !peer_ok(w) ? 4 : 3;
+  if (use_fused_prefill(w, n_tok, nullptr)) return 3;      // router(+bases), grouped, combine_ready
+  const int experts = use_prefill(w, n_tok, nullptr) ? (w->prefill_splits > 0 ? 3 : 4) : 2;
+  return 1 + experts + 1 + (w->ctx->ep() ? 1 : 0);
+}
+
 int moe_forward_launches(moe_weights* w, int n_tok) {
   if (!w || n_tok <= 0 || w->L() == 0) return 0;
   const int L = w->L();

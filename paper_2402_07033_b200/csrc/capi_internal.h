@@ -251,6 +251,9 @@ bool peer_ok(const moe_weights* w);
 bool use_stack(const moe_weights* w, int n_tok);
 int refresh_projection(moe_weights* w);
 bool use_stack2(const moe_weights* w);
+bool use_layer_stack(const moe_weights* w, int n_tok, const float* post);
+int enqueue_layer_stack(moe_weights* w, int l, const float* x, float* x_out, int32_t* ids,
+                        float* gates, cudaStream_t s);
 int enqueue_stack(moe_weights* w, float* x, int32_t* ids, float* gates, cudaStream_t s,
                   unsigned long long* trace = nullptr, float* logits = nullptr);
 bool use_prefill(const moe_weights* w, int n_tok, const float* post);

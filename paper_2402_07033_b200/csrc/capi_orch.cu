@@ -122,6 +122,29 @@ bool use_stack2(const moe_weights* w) {
          moe::stack2_supported(w->plan, w->dims());
 }
 
+// One layer at batch 1 (moe_layer_forward) through the single-barrier
+// persistent kernel as a 1-layer stack: routing, both projections, the
+// combine and the residual in ONE launch instead of router + experts +
+// reduce (the layer's tables are the stack's, offset to layer l).
+bool use_layer_stack(const moe_weights* w, int n_tok, const float* post) {
+  return n_tok == 1 && post == nullptr && w->sp.counts == nullptr && use_stack(w, 1) && use_stack2(w);
+}
+
+int enqueue_layer_stack(moe_weights* w, int l, const float* x, float* x_out, int32_t* ids,
+                        float* gates, cudaStream_t s) {
+  moe::StackDesc sd;
+  sd.rw = w->dev_rw.as<const float* const>() + l;  // not read: a 1-layer stack has no next router
+  sd.layer_experts = w->dev_layers.as<const void* const>() + l;
+  sd.slot_of = w->dev_slots.as<const int16_t>() + (size_t)l * w->E();
+  sd.expert_stride = 3 * w->mat_elems();
+  sd.mat_stride = w->mat_elems();
+  sd.router = w->router + (size_t)l * w->E() * w->d();
+  sd.L = 1;
+  CU(moe::launch_decode_stack2(w->plan, sd, w->dims(), const_cast<float*>(x), w->stack_acc.p, ids,
+                               gates, nullptr, s, x_out));
+  return MOE_OK;
+}
+
 int enqueue_stack(moe_weights* w, float* x, int32_t* ids, float* gates, cudaStream_t s,
                   unsigned long long* trace, float* logits) {
   moe::StackDesc sd;
@@ -207,8 +230,11 @@ int experts_forward(moe_weights* w, int l, const float* x, int n_tok, const int3
   moe::SparsityCounters sp = w->sp;
   if (sp.counts) sp.counts += (size_t)l * sp.n;
   if (router_l) {
-    // router_l: route this layer here (ids/gates are outputs) — fused into the
-    // prefill layer's first kernel when the fused path applies
+    // router_l: route this layer here (ids/gates are outputs) — inside the
+    // batch-1 persistent kernel, or fused into the prefill layer's first
+    // kernel, when those paths apply
+    if (use_layer_stack(w, n_tok, post))
+      return enqueue_layer_stack(w, l, x, x_out, const_cast<int32_t*>(ids), const_cast<float*>(gates), s);
     if (!use_fused_prefill(w, n_tok, post)) {
       CU(moe::launch_router_topk(router_l, x, n_tok, dm, const_cast<int32_t*>(ids),
                                  const_cast<float*>(gates), s, false));

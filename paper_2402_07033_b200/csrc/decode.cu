@@ -907,7 +907,8 @@ struct Stack2Args {
   long long expert_stride, mat_stride;
   const float* router;               // [L][E][d]
   const float* const* rw;            // [L] R_{l+1} W2 per local expert [f][E]
-  float* x;                          // in: x_0, out: x_L
+  float* x;                          // in: x_0 (out: x_L when x_out == x)
+  float* x_out;                      // out: x_L
   unsigned long long* acc;           // [3][d] fixed point
   unsigned long long* zacc;          // [3][kZStride]
   unsigned* state;                   // [0] barrier counter, [32] base, [33] rotation
@@ -1136,7 +1137,7 @@ __global__ void __launch_bounds__(kMaxConsWarps * 32 + 32, 1)
       add_xpart(l + 2, buf(l + 1), xr);
       load_rv(l + 3);
     }
-    if (!more && c == 0) store_y<W, NV>(a.x, xr, tid, ncons);
+    if (!more && c == 0) store_y<W, NV>(a.x_out, xr, tid, ncons);
     named_bar_sync(2, ncons);  // routing of l+1 visible to every consumer warp
     if (tr && tid == 0) tr[5] = clock64();
   }
@@ -1613,7 +1614,7 @@ __global__ void __launch_bounds__(kMaxConsWarps * 32 + 64, 1)
       add_xpart(l + 2, buf(l + 1), xr);
       load_rv(l + 3);
     }
-    if (!more && c == 0) store_y<W, NV>(a.x, xr, tid, ncons);
+    if (!more && c == 0) store_y<W, NV>(a.x_out, xr, tid, ncons);
     if (tr0) *tslot(l, 7) = clock64();
   }
   if (c == 0 && tid == 0) {
@@ -1809,7 +1810,7 @@ static cudaError_t launch_stack2_t(const DecodePlan& p, const Dims& dm, const St
 
 cudaError_t launch_decode_stack2(const DecodePlan& p, const StackDesc& sd, const Dims& dm, float* x,
                                  void* accbuf, int32_t* ids_out, float* gates_out,
-                                 float* logits_out, cudaStream_t s) {
+                                 float* logits_out, cudaStream_t s, float* x_out) {
   if (!stack2_supported(p, dm) || sd.rw == nullptr) return cudaErrorInvalidValue;
   Stack2Args a;
   a.layer_experts = sd.layer_experts;
@@ -1819,6 +1820,7 @@ cudaError_t launch_decode_stack2(const DecodePlan& p, const StackDesc& sd, const
   a.router = sd.router;
   a.rw = sd.rw;
   a.x = x;
+  a.x_out = x_out ? x_out : x;
   a.acc = static_cast<unsigned long long*>(accbuf);
   a.zacc = a.acc + 3 * (size_t)dm.d;
   a.state = reinterpret_cast<unsigned*>(a.zacc + 3 * kZStride);

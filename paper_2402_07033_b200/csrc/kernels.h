@@ -125,7 +125,7 @@ bool stack2_supported(const DecodePlan& p, const Dims& dm);
 size_t stack2_acc_bytes(const Dims& dm);
 cudaError_t launch_decode_stack2(const DecodePlan& p, const StackDesc& sd, const Dims& dm, float* x,
                                  void* accbuf, int32_t* ids_out, float* gates_out,
-                                 float* logits_out, cudaStream_t s);
+                                 float* logits_out, cudaStream_t s, float* x_out = nullptr);
 // x_out = x + sum_p ypart[p]; optionally the next layer's router + top-k
 // (deterministic fixed-order partial sums, last-block-done).
 cudaError_t launch_reduce_residual(const float* ypart, int nparts, const float* x, float* x_out,

@@ -703,3 +703,42 @@ def test_edge_geometries_vs_oracle(ctx, orc, E, k, d, f, dt, n_tok):
         err = normwise(out[t] - x[t], delta)
         assert err < tol, (t, err)
     w.close()
+
+
+@pytest.mark.parametrize("dt", [M.DTYPE_BF16, M.DTYPE_F32])
+def test_layer_forward_batch1_is_one_launch_every_layer(ctx, orc, libopts, dt):
+    """moe_layer_forward at batch 1 runs the persistent kernel as a 1-layer
+    stack (one launch): every layer index of a 3-layer model against the
+    per-layer kernels (router + experts + reduce) and the oracle, out of
+    place and in place."""
+    L, d, f = 3, 4096, 14336
+    s = M.Shape(L, 8, 2, d, f, 2 if dt == M.DTYPE_BF16 else 4)
+    w = M.Weights(ctx, s, dt)
+    libopts(stack=0)
+    w_ref = M.Weights(ctx, s, dt)
+    libopts(stack=1)
+    assert w.layer_launches(1) == 1 and w_ref.layer_launches(1) == 3
+    w.random(21)
+    w_ref.random(21)
+    rs = np.random.RandomState(4)
+    for l in range(L):
+        x = f32(0.5 * rs.randn(d))
+        outs = []
+        for ww, inplace in ((w, False), (w, True), (w_ref, False)):
+            xd = torch.tensor(x[None], dtype=torch.float32, device="cuda")
+            xo = xd if inplace else torch.empty_like(xd)
+            ids = torch.zeros((1, 2), dtype=torch.int32, device="cuda")
+            g = torch.zeros((1, 2), dtype=torch.float32, device="cuda")
+            ww.layer_forward(l, xd, xo, ids, g)
+            torch.cuda.synchronize()
+            outs.append((xo.cpu().numpy()[0].astype(np.float64), ids.cpu().numpy()[0], g.cpu().numpy()[0]))
+        assert np.array_equal(outs[0][0], outs[1][0]) and np.array_equal(outs[0][1], outs[1][1])
+        oid, og, delta, mg = oracle_layer(orc, w, l, x, 2)
+        if mg > 1e-5:
+            assert list(outs[0][1]) == list(oid) == list(outs[2][1]), l
+            assert np.abs(outs[0][2] - og).max() < 1e-5
+        err = normwise(outs[0][0] - x, delta)
+        assert err < (1e-4 if dt == M.DTYPE_BF16 else TOL_F32), (l, err)
+        assert normwise(outs[0][0] - x, outs[2][0] - x) < 1e-5
+    w.close()
+    w_ref.close()
