@@ -418,7 +418,7 @@ constexpr int GP_STG = 32 * PF_BM * 4;  // 16 KB
 constexpr int GP_SMEM = GP_STAGES * GP_STAGE + GP_STG + 1024 /*align*/ + 256 /*barriers, queue*/ +
                         (6 * kMaxExperts + 1) * 4 /*schedule segments [2E+1] + [2E], splits, chunks [E]*/ +
                         2 * GP_MAXN * 4 /*down tile: pair index + gate per token row*/ +
-                        (3 * kRouteItemPairs + kMaxExperts / 32 + 2) * 4 /*fused dispatch*/;
+                        (2 * kRouteItemPairs + kMaxExperts / 32 + 2) * 4 /*fused dispatch*/;
 
 struct GroupedArgs {
   const int32_t* counts;
@@ -523,10 +523,10 @@ __global__ void __launch_bounds__(PF_THREADS, 1)
   int* s_nch = s_split + kMaxExperts;                // [E] token chunks per expert
   int* s_pair = s_nch + kMaxExperts;                              // [GP_MAXN]
   float* s_gate = reinterpret_cast<float*>(s_pair + GP_MAXN);     // [GP_MAXN]
-  int* s_dpos = reinterpret_cast<int*>(s_gate + GP_MAXN);         // [kRouteItemPairs] dispatch rows
-  int* s_dtok = s_dpos + kRouteItemPairs;                         // [kRouteItemPairs]
-  unsigned* s_xrdy = reinterpret_cast<unsigned*>(s_dtok + 2 * kRouteItemPairs);  // [E/32] producer's bitmask
-  int* s_misc = reinterpret_cast<int*>(s_xrdy + kMaxExperts / 32);           // [2]: claimed item, list size
+  int* s_dpos = reinterpret_cast<int*>(s_gate + GP_MAXN);         // [kRouteItemPairs] dispatch: sorted row
+  int* s_eid = s_dpos + kRouteItemPairs;                          // [kRouteItemPairs] dispatch: expert id
+  unsigned* s_xrdy = reinterpret_cast<unsigned*>(s_eid + kRouteItemPairs);  // [E/32] producer's bitmask
+  int* s_misc = reinterpret_cast<int*>(s_xrdy + kMaxExperts / 32);          // [1]: claimed item
   __shared__ int s_total;
 
   const int warp = warp_uniform(threadIdx.x >> 5), lane = threadIdx.x & 31;
@@ -603,7 +603,6 @@ __global__ void __launch_bounds__(PF_THREADS, 1)
     // ---- dispatch: router blocks claimed one at a time by the epilogue warps
     // (the producer meanwhile streams the first tile's weights)
     const int tpb = a.blk_tok * a.k;
-    int* s_eid = s_dtok + kRouteItemPairs;  // [kRouteItemPairs] the item's expert ids
     while (true) {
       if (threadIdx.x == 0) s_misc[0] = (int)atomicAdd(a.disp_ctr, 1u);
       named_bar_sync(3, 128);
