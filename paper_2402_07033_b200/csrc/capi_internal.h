@@ -138,7 +138,7 @@ struct moe_weights {
   DevBuf xbuf2, gbar, dev_layers, dev_slots;  // persistent stack kernel
   DevBuf stack_acc;  // decode_stack2_kernel: fixed-point accumulators + barrier state
   DevBuf pf_counts, pf_offsets, pf_perm, pf_xg, pf_h, pf_sync;  // tcgen05 prefill
-  DevBuf pf_route;  // fused prefill: router last-block counter + per-block dispatch bases
+  DevBuf pf_route;  // fused prefill: per-router-block expert counts
   DevBuf io;  // host-buffer API, batch 1: [x][ids][gates] (one D2H)
   // moe_debug_kernel_timing: event pairs around each grouped prefill launch
   bool ktime_on = false;

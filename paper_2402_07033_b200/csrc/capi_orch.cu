@@ -188,7 +188,7 @@ int ensure_prefill_scratch(moe_weights* w, int n_tok) {
   TRY(w->pf_h.ensure(prefill_h_bytes(w, n_tok) +
                      4 * rows * w->d() * (size_t)std::max(1, w->prefill_splits)));
   TRY(w->pf_sync.ensure(4 * moe::prefill_sync_words(w->E(), n_tok, w->d())));
-  TRY(w->pf_route.ensure(4 * (16 + (size_t)moe::route_blocks(n_tok) * w->E())));
+  TRY(w->pf_route.ensure(4 * (size_t)moe::route_blocks(n_tok) * w->E()));
   return MOE_OK;
 }
 

@@ -102,14 +102,12 @@ __global__ void __launch_bounds__(256) router_topk_kernel(const float* __restric
 // once — instead of each thread's 16+ dependent global loads, which left the
 // per-thread loop latency-bound (~30 us at 512 tokens).
 //
-// Optional dispatch outputs (rd.blk_base != nullptr; the fused prefill path,
+// Optional dispatch output (rd.blk_count != nullptr; the fused prefill path,
 // launch_route_dispatch): every block records how many of its (token, slot)
-// pairs chose each expert, and the last block to finish turns those into the
-// stable counting sort's bases — counts[e], offsets[e] and
-// blk_base[b][e] = offsets[e] + sum_{b' < b} count[b'][e] — so the grouped
-// kernel can scatter each block's pairs without a separate permute launch.
-// perm[blk_base[b][e] + r] is then the r-th pair of block b that chose e, in
-// pair order: exactly permute_kernel's order.
+// pairs chose each expert.  The grouped kernel turns those into the stable
+// counting sort's positions (offsets[e] + the counts of the blocks before +
+// the rank within the block: exactly permute_kernel's order) and scatters
+// each block's pairs itself, without a permute launch.
 constexpr int kRouterChunk = 2048;  // columns per chunk (multiple of 256)
 constexpr int kRouterStages = 2;
 __global__ void __launch_bounds__(256, 1) router_topk_bulk_kernel(const float* __restrict__ router,
@@ -123,7 +121,6 @@ __global__ void __launch_bounds__(256, 1) router_topk_bulk_kernel(const float* _
   __shared__ float part[8][kRouterTok][8];
   __shared__ float logits[kRouterTok][kMaxExperts];
   __shared__ __align__(8) uint64_t bar[kRouterStages];
-  __shared__ int s_last;
   const int tid = threadIdx.x, lane = tid & 31;
   const int warp = warp_uniform(tid >> 5);
   if (tid == 0) {
@@ -206,9 +203,9 @@ __global__ void __launch_bounds__(256, 1) router_topk_bulk_kernel(const float* _
   }
   for (int t = warp; t < nt; t += 8)
     warp_topk_softmax(logits[t], E, k, ids + (size_t)(t0 + t) * k, gates + (size_t)(t0 + t) * k);
-  if (rd.blk_base == nullptr) return;
+  if (rd.blk_count == nullptr) return;
 
-  // ---- dispatch bases (fused prefill path) ----
+  // ---- per-block expert counts (fused prefill path) ----
   __shared__ int32_t s_pid[kRouterTok * 256];  // this block's expert ids (k <= E <= 256)
   __syncthreads();  // this block's ids (global) visible to the whole block
   const int npair = nt * k;
@@ -217,56 +214,8 @@ __global__ void __launch_bounds__(256, 1) router_topk_bulk_kernel(const float* _
   for (int e = tid; e < E; e += 256) {
     int c = 0;
     for (int p = 0; p < npair; ++p) c += s_pid[p] == e;
-    rd.blk_base[(size_t)blockIdx.x * E + e] = c;
+    rd.blk_count[(size_t)blockIdx.x * E + e] = c;
   }
-  __threadfence();
-  __syncthreads();
-  if (tid == 0) s_last = atomicAdd(rd.done, 1u) == gridDim.x - 1;
-  __syncthreads();
-  if (!s_last) return;
-  __threadfence();
-  // last block: every block's counts into smem (the column-chunk ring is
-  // free now; all loads in flight at once), then per expert an exclusive scan
-  // split into nseg segments of blocks (thread = (expert, segment))
-  __shared__ int seg_sum[256];
-  __shared__ int s_off[kMaxExperts];
-  const int nblk = gridDim.x;
-  const bool in_smem = (size_t)nblk * E <= (size_t)kRouterStages * kStageFloats;
-  int* cnt = in_smem ? reinterpret_cast<int*>(stage_base) : rd.blk_base;
-  if (in_smem)
-    for (int i = tid; i < nblk * E; i += 256) cnt[i] = __ldcg(rd.blk_base + i);
-  __syncthreads();
-  const int nseg = max(1, 256 / E);
-  const int seg_len = (nblk + nseg - 1) / nseg;
-  const int e = tid % E, sg = tid / E;
-  const bool act = tid < E * nseg;
-  int tot = 0;
-  if (act)
-    for (int b = sg * seg_len; b < min(nblk, (sg + 1) * seg_len); ++b) tot += cnt[(size_t)b * E + e];
-  if (act) seg_sum[tid] = tot;
-  __syncthreads();
-  if (tid == 0) {
-    int acc = 0;
-    for (int ee = 0; ee < E; ++ee) {
-      int c = 0;
-      for (int q = 0; q < nseg; ++q) c += seg_sum[q * E + ee];
-      s_off[ee] = acc;
-      rd.counts[ee] = c;
-      rd.offsets[ee] = acc;
-      acc += c;
-    }
-  }
-  __syncthreads();
-  if (act) {
-    int run = s_off[e];
-    for (int q = 0; q < sg; ++q) run += seg_sum[q * E + e];
-    for (int b = sg * seg_len; b < min(nblk, (sg + 1) * seg_len); ++b) {
-      const int c = cnt[(size_t)b * E + e];
-      rd.blk_base[(size_t)b * E + e] = run;
-      run += c;
-    }
-  }
-  if (tid == 0) *rd.done = 0u;  // ready for the next launch (stream-ordered)
 }
 
 cudaError_t launch_router_topk(const float* router, const float* x, int n_tok, const Dims& dm,
@@ -296,7 +245,7 @@ cudaError_t launch_route_dispatch(const float* router, const float* x, int n_tok
                                   int32_t* ids, float* gates, const RouteDispatch& rd,
                                   cudaStream_t s, bool pdl) {
   if (n_tok <= 0) return cudaSuccess;
-  if (!route_dispatch_supported(dm) || rd.blk_base == nullptr) return cudaErrorInvalidValue;
+  if (!route_dispatch_supported(dm) || rd.blk_count == nullptr) return cudaErrorInvalidValue;
   cudaLaunchAttribute attr[1];
   const size_t smem = (size_t)kRouterStages * (kRouterTok + 8) * kRouterChunk * sizeof(float);
   cudaError_t e = cudaFuncSetAttribute(router_topk_bulk_kernel,

@@ -62,14 +62,11 @@ struct SparsityCounters {
 cudaError_t launch_router_topk(const float* router, const float* x, int n_tok, const Dims& dm,
                                int32_t* ids, float* gates, cudaStream_t s, bool pdl);
 // The router of the fused prefill path: the same routing (bit for bit) plus
-// the stable counting sort's bases per router block (route_block_tokens()
-// tokens each): counts[E], offsets[E], blk_base[route_blocks(n)][E], and the
-// zeroing of n_zero words for the grouped kernel that follows.
+// each router block's (route_block_tokens() tokens) per-expert pair counts
+// blk_count[route_blocks(n)][E], and the zeroing of n_zero words for the
+// grouped kernel that follows.
 struct RouteDispatch {
-  int32_t* blk_base = nullptr;  // [nblk][E] out
-  int32_t* counts = nullptr;    // [E] out
-  int32_t* offsets = nullptr;   // [E] out
-  unsigned* done = nullptr;     // last-block counter: 0 at launch, left 0
+  int32_t* blk_count = nullptr;  // [nblk][E] out
   int* zero = nullptr;
   int n_zero = 0;
 };
@@ -249,7 +246,7 @@ struct PrefillFuse {
   const float* router = nullptr;  // this layer's [E][d]
   int32_t* ids = nullptr;         // [n_tok][k] out
   float* gates = nullptr;         // [n_tok][k] out
-  int32_t* route = nullptr;       // [16 + route_blocks(n_tok) * E]: [0] last-block counter, [16..) bases
+  int32_t* route = nullptr;       // [route_blocks(n_tok) * E] per-block expert counts
   float* x_out = nullptr;         // [n_tok][d] out; may alias x (token t's row is
                                   // combined only after its own dispatch read it)
 };

@@ -418,7 +418,8 @@ constexpr int GP_STG = 32 * PF_BM * 4;  // 16 KB
 constexpr int GP_SMEM = GP_STAGES * GP_STAGE + GP_STG + 1024 /*align*/ + 256 /*barriers, queue*/ +
                         (6 * kMaxExperts + 1) * 4 /*schedule segments [2E+1] + [2E], splits, chunks [E]*/ +
                         2 * GP_MAXN * 4 /*down tile: pair index + gate per token row*/ +
-                        (2 * kRouteItemPairs + kMaxExperts / 32 + 2) * 4 /*fused dispatch*/;
+                        (2 * kRouteItemPairs + kMaxExperts / 32 + 2) * 4 /*fused dispatch*/ +
+                        2 * kMaxExperts * 4 /*counts, offsets*/;
 
 struct GroupedArgs {
   const int32_t* counts;
@@ -450,7 +451,7 @@ struct GroupedArgs {
   int fused;
   const float* xin;         // [n_tok][d] layer input
   const int32_t* ids;       // [n_tok][k]
-  const int32_t* blk_base;  // [nblk][E] (launch_route_dispatch)
+  const int32_t* blk_base;  // [nblk][E] per-block expert counts (launch_route_dispatch)
   int32_t* perm_w;          // == perm, written by the dispatch
   __nv_bfloat16* xg;        // [rows][d], written by the dispatch
   unsigned* disp_ctr;       // dispatch items claimed (zero at launch)
@@ -526,7 +527,9 @@ __global__ void __launch_bounds__(PF_THREADS, 1)
   int* s_dpos = reinterpret_cast<int*>(s_gate + GP_MAXN);         // [kRouteItemPairs] dispatch: sorted row
   int* s_eid = s_dpos + kRouteItemPairs;                          // [kRouteItemPairs] dispatch: expert id
   unsigned* s_xrdy = reinterpret_cast<unsigned*>(s_eid + kRouteItemPairs);  // [E/32] producer's bitmask
-  int* s_misc = reinterpret_cast<int*>(s_xrdy + kMaxExperts / 32);          // [1]: claimed item
+  int* s_misc = reinterpret_cast<int*>(s_xrdy + kMaxExperts / 32);          // [2]: claimed item
+  int* s_cnt = s_misc + 2;                                                   // [E] rows per expert
+  int* s_off = s_cnt + kMaxExperts;                                          // [E] first sorted row
   __shared__ int s_total;
 
   const int warp = warp_uniform(threadIdx.x >> 5), lane = threadIdx.x & 31;
@@ -534,6 +537,37 @@ __global__ void __launch_bounds__(PF_THREADS, 1)
   // up's W1/W3 pair), so both tile kinds stream 32 KB of weights per K-block
   const int n_ft = a.f / PF_BM, n_dt = a.d / (2 * PF_BM);
   griddep_wait();
+  if (a.fused) {
+    // per-expert totals from the router's per-block counts (all threads: one
+    // segment of blocks each, then a fixed-order sum), offsets by thread 0
+    const int nseg = max(1, PF_THREADS / a.E);
+    for (int q = threadIdx.x; q < a.E * nseg; q += PF_THREADS) {
+      const int e = q % a.E, sg = q / a.E;
+      int t = 0;
+      for (int b = sg; b < a.nblk; b += nseg) t += __ldcg(a.blk_base + (size_t)b * a.E + e);
+      s_pair[q] = t;
+    }
+    __syncthreads();
+    for (int e = threadIdx.x; e < a.E; e += PF_THREADS) {
+      int t = 0;
+      for (int sg = 0; sg < nseg; ++sg) t += s_pair[sg * a.E + e];
+      s_cnt[e] = t;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      int acc = 0;
+      for (int e = 0; e < a.E; ++e) {
+        s_off[e] = acc;
+        acc += s_cnt[e];
+      }
+    }
+  } else {
+    for (int e = threadIdx.x; e < a.E; e += PF_THREADS) {
+      s_cnt[e] = a.counts[e];
+      s_off[e] = a.offsets[e];
+    }
+  }
+  __syncthreads();
   if (threadIdx.x == 0) {
     // Schedule: the active experts' up tiles in order, with expert i's down
     // tiles placed after expert i+lag's up tiles (a.lag; the default puts
@@ -545,13 +579,13 @@ __global__ void __launch_bounds__(PF_THREADS, 1)
     int act[kMaxExperts];
     int n_act = 0;
     for (int e = 0; e < a.E; ++e)
-      if (a.slot_of[e] >= 0 && a.counts[e] > 0) act[n_act++] = e;
+      if (a.slot_of[e] >= 0 && s_cnt[e] > 0) act[n_act++] = e;
     const int n_late = (a.late8 * n_act + 7) / 8;
     int dn_tiles = 0;  // down tiles without K splits
     for (int e = 0; e < a.E; ++e) {
       s_split[e] = 1;
-      s_nch[e] = max(1, (a.counts[e] + GP_MAXN - 1) / GP_MAXN);
-      if (a.slot_of[e] >= 0 && a.counts[e] > 0) dn_tiles += s_nch[e] * n_dt;
+      s_nch[e] = max(1, (s_cnt[e] + GP_MAXN - 1) / GP_MAXN);
+      if (a.slot_of[e] >= 0 && s_cnt[e] > 0) dn_tiles += s_nch[e] * n_dt;
     }
     // K splits only pay while the down tiles are few per SM (tail); with many
     // (large batches) they only add fp32 Y partial traffic for the combine
@@ -564,7 +598,7 @@ __global__ void __launch_bounds__(PF_THREADS, 1)
     const int kLag = a.lag;
     int ns = 0, tot = 0;
     auto push = [&](int e, int up) {
-      const int ch = (a.counts[e] + GP_MAXN - 1) / GP_MAXN;
+      const int ch = (s_cnt[e] + GP_MAXN - 1) / GP_MAXN;
       seg_start[ns] = tot;
       seg_code[ns++] = 2 * e + up;
       tot += up ? ch * n_ft : ch * n_dt * s_split[e];
@@ -610,13 +644,26 @@ __global__ void __launch_bounds__(PF_THREADS, 1)
       if (b >= a.nblk) break;
       const int p0 = b * tpb;
       const int np = min(tpb, a.n_tok * a.k - p0);
-      int base = 0;
-      if (threadIdx.x < np) {
-        const int e = __ldg(a.ids + p0 + threadIdx.x);
-        s_eid[threadIdx.x] = e;
-        base = __ldg(a.blk_base + (size_t)b * a.E + e);
+      // base of this block's rows in each expert's segment: the offset plus
+      // the counts of the blocks before it (128 threads, one segment each)
+      int* part = s_pair;                            // [128] (free until the first down tile)
+      int* s_base = reinterpret_cast<int*>(s_gate);  // [E]
+      const int nseg = max(1, 128 / a.E);
+      for (int q = threadIdx.x; q < a.E * nseg; q += 128) {
+        const int e = q % a.E, sg = q / a.E;
+        int t = 0;
+        for (int bb = sg; bb < b; bb += nseg) t += __ldcg(a.blk_base + (size_t)bb * a.E + e);
+        part[q] = t;
+      }
+      if (threadIdx.x < np) s_eid[threadIdx.x] = __ldg(a.ids + p0 + threadIdx.x);
+      named_bar_sync(3, 128);
+      for (int e = threadIdx.x; e < a.E; e += 128) {
+        int t = s_off[e];
+        for (int sg = 0; sg < nseg; ++sg) t += part[sg * a.E + e];
+        s_base[e] = t;
       }
       named_bar_sync(3, 128);
+      const int base = threadIdx.x < np ? s_base[s_eid[threadIdx.x]] : 0;
       if (threadIdx.x < np) {
         const int p = p0 + threadIdx.x;
         const int e = s_eid[threadIdx.x];
@@ -682,10 +729,10 @@ __global__ void __launch_bounds__(PF_THREADS, 1)
 
   auto chunk_geom = [&](const GTile& g, int& nvalid, int& N, int& nboxes, int& srow) {
     const int row0 = g.c * GP_MAXN;
-    nvalid = min(GP_MAXN, a.counts[g.e] - row0);
+    nvalid = min(GP_MAXN, s_cnt[g.e] - row0);
     N = (nvalid + 15) & ~15;
     nboxes = (N + PF_BOXN - 1) / PF_BOXN;
-    srow = a.offsets[g.e] + row0;
+    srow = s_off[g.e] + row0;
   };
 
   if (warp == 4) {
@@ -738,7 +785,7 @@ __global__ void __launch_bounds__(PF_THREADS, 1)
               tma_load_2d_hint(sp, &wmap_up, kb * PF_BK, w1row, &full[st], wpol);
               tma_load_2d_hint(sp + kA, &wmap_up, kb * PF_BK, w3row, &full[st], wpol);
             }
-            const int want = a.counts[g.e];
+            const int want = s_cnt[g.e];
             int v;
             do {
               asm volatile("ld.acquire.gpu.global.s32 %0, [%1];" : "=r"(v) : "l"(a.x_ready + g.e) : "memory");
@@ -886,7 +933,7 @@ __global__ void __launch_bounds__(PF_THREADS, 1)
             int v;
             do {
               asm volatile("ld.acquire.gpu.global.s32 %0, [%1];" : "=r"(v) : "l"(a.x_ready + g.e) : "memory");
-            } while (v < a.counts[g.e]);
+            } while (v < s_cnt[g.e]);
           }
           named_bar_sync(3, 128);
         }
@@ -1154,10 +1201,7 @@ cudaError_t launch_prefill_experts(const LayerWeights& lw, int n_local, const Di
   int* const fsync = sync + 1 + dm.E * chunks + dm.E;  // fused: [dispatch][x_ready E][combine counters]
   if (fz) {
     RouteDispatch rd;
-    rd.blk_base = fz->route + 16;
-    rd.counts = const_cast<int32_t*>(counts);
-    rd.offsets = const_cast<int32_t*>(offsets);
-    rd.done = reinterpret_cast<unsigned*>(fz->route);
+    rd.blk_count = fz->route;
     rd.zero = sync;
     rd.n_zero = (int)prefill_sync_words(dm.E, n_tok, dm.d);
     err = launch_route_dispatch(fz->router, x, n_tok, dm, fz->ids, fz->gates, rd, s, !no_pdl);
@@ -1206,7 +1250,7 @@ cudaError_t launch_prefill_experts(const LayerWeights& lw, int n_local, const Di
     g.fused = fz != nullptr;
     g.xin = x;
     g.ids = fz ? fz->ids : nullptr;
-    g.blk_base = fz ? fz->route + 16 : nullptr;
+    g.blk_base = fz ? fz->route : nullptr;
     g.perm_w = const_cast<int32_t*>(perm);
     g.xg = xg;
     g.disp_ctr = reinterpret_cast<unsigned*>(fsync);
