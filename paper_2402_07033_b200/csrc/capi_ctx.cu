@@ -221,6 +221,8 @@ static void set_peer_parts(moe_ctx* c, int r, void* base) {
   c->pa.mt_gath[r] = q.mt_gath;
   c->pa.mt_pflag[r] = q.mt_pflag;
   c->pa.mt_gflag[r] = q.mt_gflag;
+  c->pa.mt_cflag[r] = q.mt_cflag;
+  c->pa.mt_tflag[r] = q.mt_tflag;
 }
 
 static void set_own_parts(moe_ctx* c, int world, int rank) {
@@ -231,6 +233,7 @@ static void set_own_parts(moe_ctx* c, int world, int rank) {
   c->pa.err = q.err;
   c->pa.mt_seq = q.mt_seq;
   c->pa.mt_cap = (long long)c->win_tokens * c->win_hidden;
+  c->pa.mt_tokens = c->win_tokens;
   c->pa.world = world;
   c->pa.rank = rank;
 }

@@ -473,7 +473,7 @@ int moe_forward_launches(moe_weights* w, int n_tok) {
     return 1 + L * (ep && !peer_ok(w) ? 3 : 2);
   // per layer: [permute, gather, up, down] or [up, down], combine, (+add for EP),
   // and the next layer's router
-  if (use_fused_prefill(w, n_tok, nullptr)) return 2 * L;  // router(+dispatch bases), grouped kernel
+  if (use_fused_prefill(w, n_tok, nullptr)) return 3 * L;  // router(+block counts), grouped kernel, combine
   const int experts =
       use_prefill(w, n_tok, nullptr) ? (w->prefill_splits > 0 ? 3 : 4) : 2;  // grouped: permute, gather, GEMM
   return 1 + L * (experts + 1 + (ep ? 1 : 0)) + (L - 1);

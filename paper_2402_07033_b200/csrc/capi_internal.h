@@ -77,6 +77,7 @@ struct moe_ctx {
   int win_world = 0, win_hidden = 0, win_tokens = 0;
   bool peers = false;
   moe::PeerArgs pa{};
+  unsigned fc_seq = 0;  // fused EP prefill combines issued (same count on every rank)
   std::vector<void*> ipc_opened;
   std::mutex mu;
 };

@@ -197,9 +197,14 @@ int ensure_prefill_scratch(moe_weights* w, int n_tok) {
 // grouped kernel (splits > 0), no post-SiLU capture.
 bool use_fused_prefill(const moe_weights* w, int n_tok, const float* post) {
   const Dims dm = w->dims();
-  return use_prefill(w, n_tok, post) && moe::debug_options().prefill_fused && !w->ctx->ep() &&
+  const moe_ctx* c = w->ctx;
+  // expert / tensor parallelism: the combine is the streamed peer-window
+  // reduction (ep_combine_kernel), so the windows must hold the step
+  const bool ep_ok = !c->ep() || (peer_ok(w) && n_tok <= c->win_tokens && c->pa.mt_cap > 0 &&
+                                  (long long)n_tok * dm.d <= c->pa.mt_cap);
+  return use_prefill(w, n_tok, post) && moe::debug_options().prefill_fused && ep_ok &&
          !w->replicas && w->prefill_splits > 0 && moe::route_dispatch_supported(dm) &&
-         moe::route_block_tokens() * dm.k <= 64 && dm.k * w->prefill_splits <= 8;
+         moe::route_block_tokens() * dm.k <= 64;
 }
 
 // moe_debug_kernel_timing: a fresh event pair around the grouped kernel
@@ -284,6 +289,11 @@ int experts_forward(moe_weights* w, int l, const float* x, int n_tok, const int3
       fz.gates = const_cast<float*>(gates);
       fz.route = w->pf_route.as<int32_t>();
       fz.x_out = x_out;
+      if (ep) {
+        fz.pa = &w->ctx->pa;
+        fz.holders = w->tp > 1 ? nullptr : w->dev_holders.as<uint32_t>() + (size_t)l * dm.E;
+        fz.seq = ++w->ctx->fc_seq;
+      }
       float* yb = reinterpret_cast<float*>(w->pf_h.as<char>() + prefill_h_bytes(w, n_tok));
       cudaEvent_t kt0 = nullptr, kt1 = nullptr;
       TRY(kernel_events(w, kt0, kt1));

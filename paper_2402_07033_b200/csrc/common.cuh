@@ -149,6 +149,35 @@ __device__ __forceinline__ void named_bar_sync(int id, int nthreads) {
   asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
 }
 
+// ---- system-scope flags between peer GPUs (NVLink P2P / CUDA IPC windows) --
+__device__ __forceinline__ void st_release_sys(unsigned* p, unsigned v) {
+  asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ unsigned ld_acquire_sys(const unsigned* p) {
+  unsigned v;
+  asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+
+// Bounded wait for a peer's flag to reach `target` (sequence numbers compare
+// modulo 2^32): a rank that never arrives sets *err instead of hanging.
+// Bounded wait for a peer's flag.  Once any wait of this rank has timed out
+// (err set) the others give up at their next check instead of each spinning
+// to its own bound, so a missing peer costs one timeout, not one per wait.
+__device__ __forceinline__ void peer_wait(const unsigned* f, unsigned target, unsigned* err) {
+  unsigned spins = 0;
+  while ((int)(ld_acquire_sys(f) - target) < 0) {
+    if (++spins > (1u << 22)) {
+      atomicExch(err, 1u);
+      break;
+    }
+    if (spins > 64) {
+      if ((spins & 63) == 0 && *reinterpret_cast<volatile unsigned*>(err)) break;
+      __nanosleep(128);
+    }
+  }
+}
+
 // ---- warp-wide top-k (registers only; no local-memory arrays) --------------
 // Same semantics as topk_softmax below / gate_topk (model.cpp:79-99): k
 // rounds of a warp argmax with (logit desc, id asc) ordering, ids emitted

@@ -373,34 +373,6 @@ __global__ void __launch_bounds__(256) reduce_residual_kernel(
 // Expert-parallel variant: the reduced 32-column slice of this rank's delta
 // is pushed to every rank's inbox, and the residual adds the rank-ordered sum
 // of all ranks' slices (see launch_reduce_exchange in kernels.h).
-__device__ __forceinline__ void st_release_sys(unsigned* p, unsigned v) {
-  asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
-}
-__device__ __forceinline__ unsigned ld_acquire_sys(const unsigned* p) {
-  unsigned v;
-  asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
-  return v;
-}
-
-// Bounded wait for a peer's flag to reach `target` (sequence numbers compare
-// modulo 2^32): a rank that never arrives sets *err instead of hanging.
-// Bounded wait for a peer's flag.  Once any wait of this rank has timed out
-// (err set) the others give up at their next check instead of each spinning
-// to its own bound, so a missing peer costs one timeout, not one per wait.
-__device__ __forceinline__ void peer_wait(const unsigned* f, unsigned target, unsigned* err) {
-  unsigned spins = 0;
-  while ((int)(ld_acquire_sys(f) - target) < 0) {
-    if (++spins > (1u << 22)) {
-      atomicExch(err, 1u);
-      break;
-    }
-    if (spins > 64) {
-      if ((spins & 63) == 0 && *reinterpret_cast<volatile unsigned*>(err)) break;
-      __nanosleep(128);
-    }
-  }
-}
-
 __global__ void __launch_bounds__(256) reduce_exchange_kernel(
     const float* __restrict__ ypart, int nparts, const float* x, float* x_out, int d,
     const float* __restrict__ next_router, int E, int k, float* rpart, unsigned* counter,
@@ -1860,7 +1832,8 @@ cudaError_t launch_reduce_residual(const float* ypart, int nparts, const float* 
 static size_t mt_bytes(int world, int max_hidden, int max_tokens) {
   if (max_tokens <= 0) return 0;
   const size_t cap = (size_t)max_tokens * max_hidden;
-  return 2 * (size_t)world * cap * 4 + 2 * cap * 4 + (size_t)(world + 2) * kMtBlocks * 4;
+  return 2 * (size_t)world * cap * 4 + 2 * cap * 4 + (size_t)(world + 2) * kMtBlocks * 4 +
+         (size_t)(world + 1) * max_tokens * 4;
 }
 
 size_t peer_window_bytes(int world, int max_hidden, int max_tokens) {
@@ -1887,6 +1860,7 @@ PeerParts peer_window_parts(void* base, int world, int max_hidden, int max_token
   p += 64;
   q.mt_recv = q.mt_gath = nullptr;
   q.mt_pflag = q.mt_gflag = q.mt_seq = nullptr;
+  q.mt_cflag = q.mt_tflag = nullptr;
   if (max_tokens > 0) {
     const size_t cap = (size_t)max_tokens * max_hidden;
     q.mt_recv = reinterpret_cast<float*>(p);
@@ -1898,6 +1872,10 @@ PeerParts peer_window_parts(void* base, int world, int max_hidden, int max_token
     q.mt_gflag = reinterpret_cast<unsigned*>(p);
     p += kMtBlocks * 4;
     q.mt_seq = reinterpret_cast<unsigned*>(p);
+    p += kMtBlocks * 4;
+    q.mt_cflag = reinterpret_cast<unsigned*>(p);
+    p += (size_t)world * max_tokens * 4;
+    q.mt_tflag = reinterpret_cast<unsigned*>(p);
   }
   return q;
 }
@@ -1949,6 +1927,170 @@ __global__ void __launch_bounds__(256) peer_allreduce_kernel(const float* __rest
   const float* g = pa.mt_gath[rk] + par * cap;
   for (long long i = e0 + tid; i < e1; i += blockDim.x) x_out[i] = x[i] + __ldcv(g + i);
   if (tid == 0) pa.mt_seq[b] = seq;
+}
+
+// Expert-parallel prefill combine, streamed beside the grouped kernel (fused
+// prefill under EP with peer windows).  Every rank routes all n tokens and
+// runs only its experts; token t's final row is reduced by its home rank
+// t % W.  Per call (sequence number seq, data parity seq & 1):
+//  1 the local completion queue (tokens whose local partials have all
+//    landed) is drained: the token's local delta (its local slots ascending,
+//    K splits ascending) goes straight into the home's receive box
+//    recv[par][this rank][t / W] and the home's contribution flag is released;
+//  2 home tokens are claimed; each waits for the ranks that own one of its
+//    experts (known from the replicated routing), sums their deltas in rank
+//    order, adds x and pushes the row into every rank's gather area + flag;
+//  3 every rank copies the gathered rows into x_out.
+// The same adds as delta -> peer_allreduce (which adds the other ranks'
+// exact zeros), so ranks agree bit for bit with each other and with the
+// unfused EP path.  Waits are bounded (pa.err).  Completion of this grid
+// implies the grouped kernel's (griddep_wait at the end).
+__global__ void __launch_bounds__(256) ep_combine_kernel(
+    const float* x, const float* y, int d, int k, float* x_out, int n_tok, long long sstride,
+    const int32_t* ids, const int32_t* split_of, const int16_t* slot_of, const uint32_t* holders,
+    int* queue, PeerArgs pa, unsigned seq) {
+  __shared__ int s_t, s_nq, s_i;
+  __shared__ unsigned s_mask;
+  const int tid = threadIdx.x;
+  const int W = pa.world, rk = pa.rank;
+  const long long cap = pa.mt_cap;
+  const int mt = pa.mt_tokens;
+  const unsigned par = seq & 1u;
+  const int n4 = d / 4;
+  // the local queue's length: tokens with at least one expert on this rank
+  if (tid == 0) s_nq = 0;
+  __syncthreads();
+  {
+    int c = 0;
+    for (int t = tid; t < n_tok; t += blockDim.x) {
+      bool loc = false;
+      for (int j = 0; j < k; ++j) loc |= slot_of[__ldg(ids + (size_t)t * k + j)] >= 0;
+      c += loc;
+    }
+    atomicAdd(&s_nq, c);
+  }
+  __syncthreads();
+  const int nq = s_nq;
+  // 1: local deltas -> home ranks
+  int slot = tid == 0 ? atomicAdd(queue, 1) : 0;
+  while (true) {
+    if (tid == 0) {
+      int t = -1;
+      if (slot < nq) {
+        int f;
+        do {
+          asm volatile("ld.acquire.gpu.global.s32 %0, [%1];" : "=r"(f) : "l"(queue + 4 + slot) : "memory");
+          if (!f) __nanosleep(128);
+        } while (!f);
+        t = f - 1;
+        slot = atomicAdd(queue, 1);
+      }
+      s_t = t;
+    }
+    __syncthreads();
+    const int t = s_t;
+    __syncthreads();
+    if (t < 0) break;
+    const int home = t % W, hi = t / W;
+    float4* dst = reinterpret_cast<float4*>(pa.mt_recv[home] + ((size_t)par * W + rk) * cap + (size_t)hi * d);
+    for (int c4 = tid; c4 < n4; c4 += blockDim.x) {
+      float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+      for (int j = 0; j < k; ++j) {
+        const size_t p = (size_t)t * k + j;
+        const int e = __ldcg(ids + p);
+        if (slot_of[e] < 0) continue;
+        const int ns = __ldcg(split_of + e);
+        for (int sp = 0; sp < ns; ++sp) {
+          const float4 v = __ldcg(reinterpret_cast<const float4*>(y + sp * sstride + p * d) + c4);
+          acc.x += v.x;
+          acc.y += v.y;
+          acc.z += v.z;
+          acc.w += v.w;
+        }
+      }
+      dst[c4] = acc;
+    }
+    __threadfence_system();
+    __syncthreads();
+    if (tid == 0) st_release_sys(pa.mt_cflag[home] + (size_t)rk * mt + hi, seq);
+  }
+  // 2: this rank's home tokens t = rk + W i
+  while (true) {
+    if (tid == 0) {
+      const int i = atomicAdd(queue + 2, 1);
+      const int t = rk + W * i;
+      // contributing ranks: the holders of the token's experts (every rank
+      // under tensor parallelism, holders == nullptr)
+      unsigned m = holders ? 0u : (1u << W) - 1u;
+      if (t < n_tok && holders)
+        for (int j = 0; j < k; ++j) m |= __ldg(holders + __ldg(ids + (size_t)t * k + j));
+      s_i = t < n_tok ? i : -1;
+      s_mask = m;
+    }
+    __syncthreads();
+    const int i = s_i;
+    const unsigned m = s_mask;
+    if (i < 0) break;
+    if (tid < W && ((m >> tid) & 1u)) peer_wait(pa.mt_cflag[rk] + (size_t)tid * mt + i, seq, pa.err);
+    __syncthreads();
+    const int t = rk + W * i;
+    const float* in = pa.mt_recv[rk] + (size_t)par * W * cap + (size_t)i * d;
+    for (int c4 = tid; c4 < n4; c4 += blockDim.x) {
+      float4 sum = make_float4(0.f, 0.f, 0.f, 0.f);
+      for (int r = 0; r < W; ++r) {
+        if (!((m >> r) & 1u)) continue;
+        const float4 v = __ldcv(reinterpret_cast<const float4*>(in + (size_t)r * cap) + c4);
+        sum.x += v.x;
+        sum.y += v.y;
+        sum.z += v.z;
+        sum.w += v.w;
+      }
+      const float4 xv = __ldg(reinterpret_cast<const float4*>(x + (size_t)t * d) + c4);
+      const float4 o = make_float4(xv.x + sum.x, xv.y + sum.y, xv.z + sum.z, xv.w + sum.w);
+      for (int r = 0; r < W; ++r)
+        reinterpret_cast<float4*>(pa.mt_gath[r] + (size_t)par * cap + (size_t)t * d)[c4] = o;
+    }
+    __threadfence_system();
+    __syncthreads();
+    if (tid < W) st_release_sys(pa.mt_tflag[tid] + t, seq);
+    __syncthreads();
+  }
+  // 3: every token's row into x_out
+  while (true) {
+    if (tid == 0) {
+      const int t = atomicAdd(queue + 3, 1);
+      if (t < n_tok) peer_wait(pa.mt_tflag[rk] + t, seq, pa.err);
+      s_t = t < n_tok ? t : -1;
+    }
+    __syncthreads();
+    const int t = s_t;
+    __syncthreads();
+    if (t < 0) break;
+    const float4* g = reinterpret_cast<const float4*>(pa.mt_gath[rk] + (size_t)par * cap + (size_t)t * d);
+    for (int c4 = tid; c4 < n4; c4 += blockDim.x)
+      reinterpret_cast<float4*>(x_out + (size_t)t * d)[c4] = __ldcv(g + c4);
+  }
+  griddep_wait();
+}
+
+cudaError_t launch_ep_combine(const float* x, const float* y, int n_tok, const Dims& dm, float* x_out,
+                              const int32_t* ids, const int32_t* split_of, const int16_t* slot_of,
+                              const uint32_t* holders, int* queue, const PeerArgs& pa, unsigned seq,
+                              cudaStream_t s, bool pdl) {
+  if (n_tok <= 0) return cudaSuccess;
+  if (dm.d % 4 || n_tok > pa.mt_tokens || (long long)n_tok * dm.d > pa.mt_cap) return cudaErrorInvalidValue;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(kMtBlocks);
+  cfg.blockDim = dim3(256);
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = pdl ? 1 : 0;
+  const long long sstride = (long long)n_tok * dm.k * dm.d;
+  return cudaLaunchKernelEx(&cfg, ep_combine_kernel, x, y, dm.d, dm.k, x_out, n_tok, sstride, ids, split_of,
+                            slot_of, holders, queue, pa, seq);
 }
 
 cudaError_t launch_peer_allreduce(const float* delta, const float* x, float* x_out, long long n,

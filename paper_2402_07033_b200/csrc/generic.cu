@@ -553,7 +553,7 @@ __global__ void __launch_bounds__(256) combine_ready_kernel(const float* x, cons
       if (slot < n_tok) {
         int f;
         do {
-          asm volatile("ld.acquire.gpu.global.s32 %0, [%1];" : "=r"(f) : "l"(queue + 2 + slot) : "memory");
+          asm volatile("ld.acquire.gpu.global.s32 %0, [%1];" : "=r"(f) : "l"(queue + 4 + slot) : "memory");
           if (!f) __nanosleep(128);
         } while (!f);
         t = f - 1;

@@ -163,7 +163,10 @@ struct PeerArgs {
   unsigned* mt_pflag[kMaxRanks];
   unsigned* mt_gflag[kMaxRanks];
   unsigned* mt_seq;            // own
+  unsigned* mt_cflag[kMaxRanks];  // rank r's per-(source, home token) contribution flags [world][max_tokens]
+  unsigned* mt_tflag[kMaxRanks];  // rank r's per-token gathered-row flags [max_tokens]
   long long mt_cap;            // elements per copy (max_tokens x max_hidden; 0 = none)
+  int mt_tokens;               // max_tokens of the windows
   int world, rank;
 };
 struct PeerParts {
@@ -174,6 +177,7 @@ struct PeerParts {
   unsigned *seq, *zseq, *err;
   float *mt_recv, *mt_gath;
   unsigned *mt_pflag, *mt_gflag, *mt_seq;
+  unsigned *mt_cflag, *mt_tflag;
 };
 size_t peer_window_bytes(int world, int max_hidden, int max_tokens = 0);
 // Carve a window allocation into its parts (same layout on every rank).
@@ -182,6 +186,15 @@ PeerParts peer_window_parts(void* base, int world, int max_hidden, int max_token
 // rank-ordered sum of every rank's delta [n], as a reduce-scatter (block b
 // summed by rank b % world) + all-gather through the windows; bit-identical
 // on every rank, no NCCL.  n <= pa.mt_cap.
+// The fused prefill path's combine under expert parallelism with peer
+// windows: streamed beside the grouped kernel from its completion queue,
+// every token reduced by its home rank t % world over the peer windows and
+// gathered to every rank (decode.cu, ep_combine_kernel).  n_tok <= the
+// windows' max_tokens; seq = the per-context call counter (same on every rank).
+cudaError_t launch_ep_combine(const float* x, const float* y, int n_tok, const Dims& dm, float* x_out,
+                              const int32_t* ids, const int32_t* split_of, const int16_t* slot_of,
+                              const uint32_t* holders, int* queue, const PeerArgs& pa, unsigned seq,
+                              cudaStream_t s, bool pdl);
 cudaError_t launch_peer_allreduce(const float* delta, const float* x, float* x_out, long long n,
                                   const PeerArgs& pa, cudaStream_t s);
 // x_out = x + sum_{r in rank order} delta_r, where delta_r = this layer's
@@ -249,12 +262,16 @@ struct PrefillFuse {
   int32_t* route = nullptr;       // [route_blocks(n_tok) * E] per-block expert counts
   float* x_out = nullptr;         // [n_tok][d] out; may alias x (token t's row is
                                   // combined only after its own dispatch read it)
+  // expert parallelism over peer windows (nullptr: single GPU)
+  const PeerArgs* pa = nullptr;
+  const uint32_t* holders = nullptr;  // [E] rank bitmask holding each expert (nullptr: all, TP)
+  unsigned seq = 0;                   // per-context call counter, same on every rank
 };
 inline size_t prefill_sync_words(int E, int n_tok, int d) {
   const size_t chunks = (n_tok + kPrefillChunk - 1) / kPrefillChunk;
   return 1 + (size_t)E * chunks + E /*splits*/ + 1 /*dispatch*/ + E /*x_ready*/ +
          (size_t)n_tok * (d / 256) /*partials landed*/ + n_tok /*blocks landed*/ +
-         2 + (size_t)n_tok /*combine queue*/;
+         4 + (size_t)n_tok /*combine queue*/;
 }
 // The fused path's combine: launched right behind the grouped kernel (PDL; it
 // starts once every grouped CTA is resident), each block claims queue slots

@@ -458,7 +458,7 @@ struct GroupedArgs {
   int* x_ready;             // [E] sorted rows written (zero at launch)
   int* tok_cnt;             // [n_tok][d/256] partials landed (zero at launch)
   int* tok_ready;           // [n_tok] hidden blocks complete (zero at launch)
-  int* cq;                  // combine queue [head][tail][slot: token + 1, n_tok] (zero at launch)
+  int* cq;                  // combine queue [head][tail][2 spare claims][slot: token + 1, n_tok] (zero at launch)
   int n_tok, nblk, blk_tok;
 };
 
@@ -670,8 +670,9 @@ __global__ void __launch_bounds__(PF_THREADS, 1)
         int rank = 0;
         for (int q = 0; q < (int)threadIdx.x; ++q) rank += s_eid[q] == e;
         const int pos = base + rank;
-        a.perm_w[pos] = p;
-        s_dpos[threadIdx.x] = pos;
+        const bool local = a.slot_of[e] >= 0;  // (expert parallelism: other ranks' experts are skipped)
+        if (local) a.perm_w[pos] = p;
+        s_dpos[threadIdx.x] = local ? pos : -1;
       }
       named_bar_sync(3, 128);
       // the item's token rows, each read once (all its loads in flight), the
@@ -695,6 +696,7 @@ __global__ void __launch_bounds__(PF_THREADS, 1)
           for (int j = 0; j < a.k; ++j) {
             const int i = tt * a.k + j;
             if (i >= np) break;
+            if (s_dpos[i] < 0) continue;
             uint2* dst = reinterpret_cast<uint2*>(a.xg + (size_t)s_dpos[i] * a.d);
 #pragma unroll
             for (int u = 0; u < 2; ++u) {
@@ -718,7 +720,7 @@ __global__ void __launch_bounds__(PF_THREADS, 1)
           before += (q < (int)threadIdx.x) & (s_eid[q] == e);
           n_e += s_eid[q] == e;
         }
-        if (before == 0)
+        if (before == 0 && a.slot_of[e] >= 0)
           asm volatile("red.release.gpu.global.add.s32 [%0], %1;" ::"l"(a.x_ready + e), "r"(n_e) : "memory");
       }
     }
@@ -1030,14 +1032,17 @@ __global__ void __launch_bounds__(PF_THREADS, 1)
           for (int j = threadIdx.x; j < nvalid; j += 128) {
             const int t = s_pair[j] / a.k;
             int target = 0;
-            for (int jj = 0; jj < a.k; ++jj) target += s_split[__ldg(a.ids + (size_t)t * a.k + jj)];
+            for (int jj = 0; jj < a.k; ++jj) {  // this rank's experts of the token (all on one GPU)
+              const int e = __ldg(a.ids + (size_t)t * a.k + jj);
+              if (a.slot_of[e] >= 0) target += s_split[e];
+            }
             if (atomicAdd(a.tok_cnt + (size_t)t * n_ht + g.t1, 1) == target - 1) {
               __threadfence();  // acquire the other tiles' partials, release them onwards
               if (atomicAdd(a.tok_ready + t, 1) == n_ht - 1) {
                 // the token's last block: publish it to the combine queue
                 __threadfence();
                 const int qi = atomicAdd(a.cq + 1, 1);
-                asm volatile("st.release.gpu.global.s32 [%0], %1;" ::"l"(a.cq + 2 + qi), "r"(t + 1) : "memory");
+                asm volatile("st.release.gpu.global.s32 [%0], %1;" ::"l"(a.cq + 4 + qi), "r"(t + 1) : "memory");
               }
             }
           }
@@ -1178,7 +1183,7 @@ cudaError_t launch_prefill_experts(const LayerWeights& lw, int n_local, const Di
                                    const PrefillFuse* fz) {
   const int rows = n_tok * dm.k;
   if (rows == 0 || n_local == 0) return cudaSuccess;
-  if (fz && (splits <= 0 || n_local != dm.E || !route_dispatch_supported(dm) ||
+  if (fz && (splits <= 0 || (n_local != dm.E && fz->pa == nullptr) || !route_dispatch_supported(dm) ||
              route_block_tokens() * dm.k > kRouteItemPairs || route_block_tokens() > kMaxItemTok))
     return cudaErrorInvalidValue;
   // an expert holds <= n_tok tokens; the grouped kernel's done flags are per
@@ -1348,7 +1353,10 @@ cudaError_t launch_prefill_experts(const LayerWeights& lw, int n_local, const Di
     if (t0 && (err = cudaEventRecord(t0, s)) != cudaSuccess) return err;
     err = cudaLaunchKernelEx(&kcfg, kern, wmap_up, wmap_dn, xmap, hmap, g);
     if (err == cudaSuccess && t1) err = cudaEventRecord(t1, s);
-    if (err == cudaSuccess && fz)
+    if (err == cudaSuccess && fz && fz->pa)
+      err = launch_ep_combine(x, y, n_tok, dm, fz->x_out, fz->ids, g.split_of, slot_of_dev, fz->holders, g.cq,
+                              *fz->pa, fz->seq, s, !no_pdl && !t1);
+    else if (err == cudaSuccess && fz)
       err = launch_combine_ready(x, y, n_tok, dm, fz->x_out, splits, fz->ids, g.split_of, g.cq,
                                  sm_count, s, !no_pdl && !t1);
     if (err != cudaSuccess || !trace_path) return err;

@@ -44,26 +44,29 @@ def _rank_main(rank, world, port, q, kernel, mode, dev=0, comm="peer"):
     try:
         dist.init_process_group("gloo", init_method=f"tcp://127.0.0.1:{port}", rank=rank,
                                 world_size=world)
-        L, E, k, d, f = 2, 8, 2, 512, 1792
-        s = M.Shape(L, E, k, d, f, 4)
+        if kernel == "prefill":  # bf16 tcgen05 layers: the fused EP / TP prefill combine
+            L, E, k, d, f, dt, nm = 2, 8, 2, 1024, 2048, M.DTYPE_BF16, 64
+        else:
+            L, E, k, d, f, dt, nm = 2, 8, 2, 512, 1792, M.DTYPE_F32, 16
+        s = M.Shape(L, E, k, d, f, 2 if dt == M.DTYPE_BF16 else 4)
         base = M.Ctx(dev)
-        full = M.Weights(base, s, M.DTYPE_F32)
+        full = M.Weights(base, s, dt)
         full.random(3)
         ctx = M.Ctx(dev)
         if comm == "peer":
             handles = [None] * world
-            dist.all_gather_object(handles, ctx.peer_window(world, d, max_tokens=16))
+            dist.all_gather_object(handles, ctx.peer_window(world, d, max_tokens=nm))
             ctx.open_peers(world, rank, handles)
         else:  # NCCL all-reduce combine over a world-rank communicator
             uid = [M.Ctx.unique_id() if rank == 0 else None]
             dist.broadcast_object_list(uid, src=0)
             ctx.init_ep(world, rank, uid[0])
         if mode == "tp":
-            w = M.Weights(ctx, s, M.DTYPE_F32, tp=True)
+            w = M.Weights(ctx, s, dt, tp=True)
         else:
             owner = np.array([[e % world for e in range(E)] for _ in range(L)], np.int32)
-            w = M.Weights(ctx, s, M.DTYPE_F32, owner=owner)
-        if comm == "peer":
+            w = M.Weights(ctx, s, dt, owner=owner)
+        if comm == "peer" and kernel != "prefill":
             assert w.forward_launches(1) == (1 if kernel == "stack" else 1 + 2 * L)
         w.reserve(1)
         w.random(3)
@@ -90,16 +93,18 @@ def _rank_main(rank, world, port, q, kernel, mode, dev=0, comm="peer"):
             got = (x - x0[t:t + 1]).double().cpu().numpy()
             errs.append(float(np.abs(got - want).max() / np.abs(want).max()))
             assert torch.equal(ids, idr)
-        # a 16-token (prefill) layer: the multi-token peer allreduce
-        xm = torch.randn(16, d, device="cuda", generator=torch.Generator(device=f"cuda:{dev}").manual_seed(9))
+        # a multi-token (prefill) layer: the multi-token peer combine
+        xm = torch.randn(nm, d, device="cuda", generator=torch.Generator(device=f"cuda:{dev}").manual_seed(9))
         wm = torch.empty_like(xm)
-        full.layer_forward(0, xm, wm, torch.zeros((16, k), dtype=torch.int32, device="cuda"),
-                           torch.zeros((16, k), device="cuda"), stream=base.stream)
+        full.layer_forward(0, xm, wm, torch.zeros((nm, k), dtype=torch.int32, device="cuda"),
+                           torch.zeros((nm, k), device="cuda"), stream=base.stream)
         base.synchronize()
         om = torch.empty_like(xm)
-        idm = torch.zeros((16, k), dtype=torch.int32, device="cuda")
-        gm = torch.zeros((16, k), device="cuda")
-        w.reserve(16)
+        idm = torch.zeros((nm, k), dtype=torch.int32, device="cuda")
+        gm = torch.zeros((nm, k), device="cuda")
+        w.reserve(nm)
+        if kernel == "prefill":
+            assert w.layer_launches(nm) == 3  # fused: router, grouped kernel, streamed EP combine
         torch.cuda.synchronize()  # inputs made on torch's stream, kernels on ctx.stream
         dist.barrier()
         w.layer_forward(0, xm, om, idm, gm, stream=ctx.stream)
@@ -137,7 +142,8 @@ def _run_two(kernel, mode, cross, comm="peer"):
         assert err < 1e-4, (rank, err)
 
 
-@pytest.mark.parametrize("kernel,mode", [("layer", "tp"), ("stack", "tp"), ("stack", "ep")])
+@pytest.mark.parametrize("kernel,mode", [("layer", "tp"), ("stack", "tp"), ("stack", "ep"), ("prefill", "ep"),
+                                         ("prefill", "tp")])
 def test_two_process_ipc(kernel, mode):
     if not torch.cuda.is_available():
         pytest.skip("no GPU")
@@ -145,7 +151,8 @@ def test_two_process_ipc(kernel, mode):
 
 
 @pytest.mark.parametrize("kernel,mode,comm", [("layer", "tp", "peer"), ("stack", "tp", "peer"),
-                                              ("stack", "ep", "peer"), ("layer", "ep", "nccl")])
+                                              ("stack", "ep", "peer"), ("layer", "ep", "nccl"),
+                                              ("prefill", "ep", "peer")])
 def test_two_process_cross_device(kernel, mode, comm):
     """Runs only with >= 2 visible GPUs: the NVLink peer exchange (or the
     2-rank NCCL all-reduce) between two real devices."""

@@ -134,10 +134,13 @@ def test_peer_combine_matches_unsharded(gpu, libopts, kernel, mode, world, shape
     (2, (1, 8, 2, 48, 80, 4), M.DTYPE_F32, 5),          # generic kernels
     (4, (1, 8, 2, 48, 80, 4), M.DTYPE_F32, 5),          # generic kernels, 4 ranks
 ])
-def test_peer_multi_token_combine(gpu, mode, world, shape, dtype, n_tok):
+def test_peer_multi_token_combine(gpu, libopts, mode, world, shape, dtype, n_tok):
     """Multi-token (prefill) layers under EP / TP with the windows' multi-token
-    area: the reduce-scatter + all-gather kernel replaces ncclAllReduce; all
-    ranks bit-identical and equal to the unsharded layer within fp32 rounding."""
+    area, in both forms: the fused path (the combine streamed beside the
+    grouped kernel: each token reduced by its home rank over the windows,
+    ep_combine_kernel) and the unfused chain (delta -> reduce-scatter +
+    all-gather kernel).  All ranks bit-identical, both forms bit-identical to
+    each other, and equal to the unsharded layer within fp32 rounding."""
     L, E, k, d = shape[0], shape[1], shape[2], shape[3]
     s = M.Shape(*shape)
     base = M.Ctx(0)
@@ -163,18 +166,27 @@ def test_peer_multi_token_combine(gpu, mode, world, shape, dtype, n_tok):
     idss = [torch.zeros_like(ids) for _ in range(world)]
     gs = [torch.zeros_like(g) for _ in range(world)]
     torch.cuda.synchronize()
-    for rep in range(2):
-        for r in range(world):
-            ws[r].layer_forward(0, x, outs[r], idss[r], gs[r], stream=ctxs[r].stream)
-        for c in ctxs:
-            c.synchronize()
-            c.peer_check()
-        for r in range(1, world):
-            assert torch.equal(outs[r], outs[0]) and torch.equal(idss[r], idss[0])
-        assert torch.equal(idss[0], ids)
-        xd = x.double()
-        err = float(((outs[0].double() - xd) - (want.double() - xd)).abs().max() / (want.double() - xd).abs().max())
-        assert err < 1e-4, err
+    results = {}
+    for fused in (1, 0, 1):
+        libopts(prefill_fused=fused)
+        if ws[0].expert_path(n_tok) == 3:  # tcgen05: the fused form is 3 launches
+            assert (ws[0].layer_launches(n_tok) == 3) == bool(fused)
+        for rep in range(2):
+            for r in range(world):
+                ws[r].layer_forward(0, x, outs[r], idss[r], gs[r], stream=ctxs[r].stream)
+            for c in ctxs:
+                c.synchronize()
+                c.peer_check()
+            for r in range(1, world):
+                assert torch.equal(outs[r], outs[0]) and torch.equal(idss[r], idss[0])
+            assert torch.equal(idss[0], ids)
+            xd = x.double()
+            err = float(((outs[0].double() - xd) - (want.double() - xd)).abs().max() / (want.double() - xd).abs().max())
+            assert err < 1e-4, err
+        if fused in results:
+            assert torch.equal(results[fused], outs[0])
+        results[fused] = outs[0].clone()
+    assert torch.equal(results[0], results[1]), "fused and unfused EP combines differ"
     for w in ws:
         w.close()
     for c in ctxs:
