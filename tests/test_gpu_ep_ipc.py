@@ -67,7 +67,8 @@ def _rank_main(rank, world, port, q, kernel, mode, dev=0, comm="peer"):
             owner = np.array([[e % world for e in range(E)] for _ in range(L)], np.int32)
             w = M.Weights(ctx, s, dt, owner=owner)
         if comm == "peer" and kernel != "prefill":
-            assert w.forward_launches(1) == (1 if kernel == "stack" else 1 + 2 * L)
+            n_l = w.forward_launches(1)
+            assert n_l == (1 if kernel == "stack" else 1 + 2 * L), ("launches", n_l)
         w.reserve(1)
         w.random(3)
         gen = torch.Generator(device=f"cuda:{dev}").manual_seed(5)
@@ -80,6 +81,7 @@ def _rank_main(rank, world, port, q, kernel, mode, dev=0, comm="peer"):
             xr = x0[t:t + 1].clone()
             idr = torch.zeros_like(ids)
             gr = torch.zeros_like(g)
+            torch.cuda.synchronize()  # xr / idr / gr come from torch's stream; the model runs on base.stream
             full.forward(xr, idr, gr, stream=base.stream)
             base.synchronize()
             x.copy_(x0[t:t + 1])
@@ -92,10 +94,11 @@ def _rank_main(rank, world, port, q, kernel, mode, dev=0, comm="peer"):
             want = (xr - x0[t:t + 1]).double().cpu().numpy()
             got = (x - x0[t:t + 1]).double().cpu().numpy()
             errs.append(float(np.abs(got - want).max() / np.abs(want).max()))
-            assert torch.equal(ids, idr)
+            assert torch.equal(ids, idr), ("ids", t, ids.flatten().tolist(), idr.flatten().tolist())
         # a multi-token (prefill) layer: the multi-token peer combine
         xm = torch.randn(nm, d, device="cuda", generator=torch.Generator(device=f"cuda:{dev}").manual_seed(9))
         wm = torch.empty_like(xm)
+        torch.cuda.synchronize()  # (same: inputs on torch's stream)
         full.layer_forward(0, xm, wm, torch.zeros((nm, k), dtype=torch.int32, device="cuda"),
                            torch.zeros((nm, k), device="cuda"), stream=base.stream)
         base.synchronize()
@@ -104,7 +107,7 @@ def _rank_main(rank, world, port, q, kernel, mode, dev=0, comm="peer"):
         gm = torch.zeros((nm, k), device="cuda")
         w.reserve(nm)
         if kernel == "prefill":
-            assert w.layer_launches(nm) == 3  # fused: router, grouped kernel, streamed EP combine
+            assert w.layer_launches(nm) == 3, ("layer launches", w.layer_launches(nm))  # fused: router, grouped, EP combine
         torch.cuda.synchronize()  # inputs made on torch's stream, kernels on ctx.stream
         dist.barrier()
         w.layer_forward(0, xm, om, idm, gm, stream=ctx.stream)

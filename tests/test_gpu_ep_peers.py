@@ -68,6 +68,7 @@ def test_peer_combine_matches_unsharded(gpu, libopts, kernel, mode, world, shape
         x = x0[t:t + 1].clone()
         ids = torch.zeros((L, 1, k), dtype=torch.int32, device="cuda")
         g = torch.zeros((L, 1, k), device="cuda")
+        torch.cuda.synchronize()  # inputs from torch's stream; the model runs on base.stream
         full.forward(x, ids, g, stream=base.stream)
         base.synchronize()
         want.append(x.cpu().numpy()[0].astype(np.float64))
@@ -150,6 +151,7 @@ def test_peer_multi_token_combine(gpu, libopts, mode, world, shape, dtype, n_tok
     want = torch.empty_like(x)
     ids = torch.zeros((n_tok, k), dtype=torch.int32, device="cuda")
     g = torch.zeros((n_tok, k), device="cuda")
+    torch.cuda.synchronize()  # inputs from torch's stream; the model runs on base.stream
     full.layer_forward(0, x, want, ids, g, stream=base.stream)
     base.synchronize()
     ctxs = [M.Ctx(0) for _ in range(world)]

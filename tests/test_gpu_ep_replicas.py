@@ -58,6 +58,7 @@ def test_replicated_hot_expert(gpu, world, n_tok):
     want = torch.empty_like(x)
     ids = torch.zeros((n_tok, k), dtype=torch.int32, device="cuda")
     g = torch.zeros((n_tok, k), device="cuda")
+    torch.cuda.synchronize()  # inputs from torch's stream; the model runs on base.stream
     full.layer_forward(0, x, want, ids, g, stream=base.stream)
     base.synchronize()
     counts = np.bincount(ids.cpu().numpy().ravel(), minlength=E).astype(np.int32)
@@ -103,6 +104,7 @@ def test_replicated_hot_expert(gpu, world, n_tok):
     # batch 1: every expert runs on its owner only (replicas idle)
     x1 = x[:1].contiguous()
     want1 = torch.empty_like(x1)
+    torch.cuda.synchronize()  # inputs from torch's stream; the model runs on base.stream
     full.layer_forward(0, x1, want1, ids[:1], g[:1], stream=base.stream)
     base.synchronize()
     o1 = [torch.empty_like(x1) for _ in range(world)]
@@ -161,6 +163,7 @@ def test_replicas_odd_world_many_experts(gpu, orc, dtype, n_tok):
     want = torch.empty_like(x)
     ids = torch.zeros((n_tok, k), dtype=torch.int32, device="cuda")
     g = torch.zeros((n_tok, k), device="cuda")
+    torch.cuda.synchronize()  # inputs from torch's stream; the model runs on base.stream
     full.layer_forward(0, x, want, ids, g, stream=base.stream)
     base.synchronize()
     owner = b.shard_map(L, E, world)

@@ -220,6 +220,7 @@ def test_sharded_decode_vs_oracle(ctx, orc, libopts, kernel, mode, world, shape,
     xs = [torch.tensor(x0[None], dtype=torch.float32, device="cuda") for _ in range(world)]
     idss = [torch.zeros((L, 1, k), dtype=torch.int32, device="cuda") for _ in range(world)]
     gs = [torch.zeros((L, 1, k), device="cuda") for _ in range(world)]
+    torch.cuda.synchronize()  # the zero fills run on torch's stream, the ranks on their own
     for r in range(world):
         ws[r].forward(xs[r], idss[r], gs[r], stream=ctxs[r].stream)
     for c in ctxs:
