@@ -65,7 +65,7 @@ def test_kernels_use_tcgen05_tma_and_do_not_spill():
         r, c = one(f"void moe::prefill_grouped_kernel<{spec}>")
         assert c["UTCHMMA"] > 0 and c["UTMALDG"] > 0 and c["LDTM"] > 0, c
         assert r["LOCAL"] == 0
-    for name in ("decode_stack2_kernel", "decode_stack_kernel", "decode_experts_kernel"):
+    for name in ("decode_stack2_kernel", "decode_stack3_kernel", "decode_stack_kernel", "decode_experts_kernel"):
         for nv in (2, 3):
             r, c = one(f"void moe::{name}<__nv_bfloat16, {nv}>")
             assert c["UBLKCP"] > 0 and c["SYNCS"] > 0, (name, c)
