@@ -174,6 +174,8 @@ struct moe_weights {
     DevBuf x[2], y[2], ids[2], gates[2];
     cudaEvent_t in_done[2] = {}, comp_done[2] = {}, out_done[2] = {};
     int64_t next = 0;
+    // batch-1 steps as one graph: (layer, x, out, ids, gates host pointers, slot, stack kernel)
+    std::map<std::tuple<int, const float*, float*, int32_t*, float*, int, int>, GraphEntry> graphs;
   } ha;
   using MoeHostAsync = MoeHostAsyncT;
   std::mutex mu;

@@ -28,6 +28,9 @@ void drop_graphs(moe_weights* w) {
   for (auto& kv : w->graphs)
     if (kv.second.exec) cudaGraphExecDestroy(kv.second.exec);
   w->graphs.clear();
+  for (auto& kv : w->ha.graphs)
+    if (kv.second.exec) cudaGraphExecDestroy(kv.second.exec);
+  w->ha.graphs.clear();
 }
 
 
