@@ -10,6 +10,15 @@
 //   down : Y_e  = g * (H_e W2_e^T)                      [tokens_e x hidden]
 //   combine (generic.cu): x += sum_j Y[t, j]  in ascending-id order
 //
+// The default (fused) layer is three launches: the router also counts each
+// 4-token block's pairs per expert; the persistent grouped kernel derives
+// the stable permutation from those counts and its epilogue warps scatter
+// the bf16 rows themselves (dynamically claimed blocks) while the producer
+// streams the first weights; each down epilogue counts the partials it
+// landed per (token, 256 columns), and a token whose last partial lands is
+// queued for the combine kernel running alongside (combine_ready_kernel, or
+// ep_combine_kernel under expert / tensor parallelism).
+//
 // Both GEMMs are "swap-AB": the WEIGHT tile is the UMMA A operand (M = 128
 // weight rows) and the expert's tokens are the N dimension (<= 256), so every
 // weight byte is streamed from HBM exactly once per token chunk — at 512
