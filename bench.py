@@ -13,9 +13,10 @@ layer ~8 (each layer adds a delta ~ |x|^2).  At 0.1 the stack stays finite
 (`routing` reports the smallest 2nd-3rd logit margin over the timed tokens).
 
 The default (N=1) line also carries BASELINE configs[1] (one Mixtral layer,
-batch-1 decode, per-layer kernels) and configs[2] (one layer, 512-token
-prefill on the tcgen05 grouped GEMM) under `extra_configs`, each with its own
-clocks, roofline and e2e, measured on layer 0 of the same weights.
+batch-1 decode) and configs[2] (one layer, 512-token prefill on the tcgen05
+grouped GEMM) under `extra_configs`, each with its own clocks, roofline and
+e2e, measured on layer 0 of the same weights, plus the same 512-token
+prefill through all 32 layers (`stack_prefill512`).
 
 At N>1 the experts of every layer are sharded over the ranks (--shard ep:
 popularity shard map = expert parallelism; tp: tensor parallelism) and every
@@ -433,7 +434,8 @@ def run_ours(args):
     extra = None
     if world == 1 and args.config == "stack32" and not args.no_extras:
         extra = {"single_layer_decode": bench_layer(args, w, stream, stream_ptr, device, peaks, peak_src),
-                 "prefill512": bench_prefill(args, w, stream, stream_ptr, device, peaks, peak_src)}
+                 "prefill512": bench_prefill(args, w, stream, stream_ptr, device, peaks, peak_src),
+                 "stack_prefill512": bench_stack_prefill(args, w, stream, stream_ptr, device, peaks, peak_src)}
 
     cpu = None
     if rank == 0 and not args.no_cpu_baseline:
@@ -552,6 +554,59 @@ def bench_layer(args, w, stream, stream_ptr, device, peaks, peak_src):
                              f" + router {E}x{d}x4 B" if kalg != alg else ""),
                          "peak_source": peak_src,
                          "step_frac": round((alg + E * d * 4) / (ms * 1e-3) / 1e9 / peak, 4)}}
+
+
+def bench_stack_prefill(args, w, stream, stream_ptr, device, peaks, peak_src):
+    """512-token prefill through the whole 32-layer stack (moe_forward,
+    the fused prefill layer 32 times): north_star's "prefill tokens/sec" for
+    the stack.  Tokens 0.1 x N(0,1) as for decode; 4 token batches rotate."""
+    import torch
+
+    import paper_2402_07033_b200 as M
+
+    L, E, k, d, f, _ = CONFIGS["stack32"]
+    n = args.prefill_tokens
+    w.reserve(n)
+    gen = torch.Generator(device=device).manual_seed(args.seed + 7)
+    with torch.cuda.stream(stream):
+        xs = [STACK_TOKEN_SCALE * torch.randn((n, d), generator=gen, device=device) for _ in range(4)]
+        x = torch.empty((n, d), device=device)
+        ids = torch.zeros((L, n, k), dtype=torch.int32, device=device)
+        g = torch.zeros((L, n, k), dtype=torch.float32, device=device)
+    torch.cuda.synchronize()
+
+    def step(i):
+        with torch.cuda.stream(stream):
+            x.copy_(xs[i % 4])
+        w.forward(x, ids, g, stream=stream_ptr)
+
+    for i in range(2):
+        step(i)
+    torch.cuda.synchronize()
+    n_steps = 8
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(torch.cuda.current_device()) as clk:
+        e0.record(stream)
+        for i in range(n_steps):
+            step(i)
+        e1.record(stream)
+        torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1) / n_steps
+    idn = ids.cpu().numpy()
+    active = [len(set(idn[l].ravel().tolist())) for l in range(L)]
+    alg = sum(a * 3 * d * f * 2 for a in active) + L * n * d * (2 + 4)
+    peak = float(peaks["hbm_gbs"])
+    bw = alg / (ms * 1e-3) / 1e9
+    return {"metric": "Mixtral-8x7B 32-layer stack prefill tok/s (512 tokens)", "value": round(n / (ms * 1e-3), 1),
+            "unit": "tok/s", "ms_per_step": round(ms, 3), "steps": n_steps, "higher_is_better": True,
+            "config": {"workload": f"{n}-token prefill through the 32-layer Mixtral-8x7B-shaped stack",
+                       "path": f"moe_forward: the fused prefill layer x {L} ({w.forward_launches(n)} launches)",
+                       "finite": bool(torch.isfinite(x).all().item())},
+            "clocks": clk.summary(),
+            "roofline": {"bound": "hbm", "achieved": round(bw, 1), "peak": peak, "unit": "GB/s",
+                         "frac": round(bw / peak, 4), "alg_bytes_per_step": alg,
+                         "alg_bytes_basis": "per layer: active experts x 3 x d x f x 2 B + tokens x d x (2 + 4) B",
+                         "peak_source": peak_src}}
 
 
 def bench_prefill(args, w, stream, stream_ptr, device, peaks, peak_src):
