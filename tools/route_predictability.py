@@ -1,5 +1,11 @@
+"""How often the next layer's experts are predictable from R_{l+1} x_l (the
+speculative-prefetch experiment of DESIGN.md §5, rejected).
+
+    python tools/route_predictability.py
+"""
+import os
 import sys
-sys.path.insert(0, "/root/repo")
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import numpy as np, torch
 import paper_2402_07033_b200 as M
 ctx = M.Ctx(0)

@@ -1,6 +1,11 @@
+"""Per-CTA stream-end spread of the persistent stack kernel from a trace
+(the slow SMs and the per-layer spread).
+
+    python tools/spread_analysis.py
+"""
 import sys, os, json
-sys.path.insert(0, "/root/repo")
-sys.path.insert(0, "/root/repo/tools")
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+sys.path.insert(0, os.path.dirname(os.path.abspath(__file__)))
 import numpy as np
 import torch
 import paper_2402_07033_b200 as M
