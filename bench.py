@@ -524,13 +524,13 @@ def bench_layer(args, w, stream, stream_ptr, device, peaks, peak_src):
     ach = kalg / (kern_ms * 1e-3) / 1e9
     # e2e: the host-buffer C-ABI call (moe_forward_host_async on layer 0 +
     # moe_host_wait), one synchronous step per token: token in from pinned
-    # host memory, output + routing back (at batch 1 one captured graph)
+    # host memory, output + routing back
     host = torch.tensor(token_pool(args.seed + 3, 8, d, 1)).pin_memory()
     out_h = torch.empty((1, d)).pin_memory()
     ids_h = torch.empty((1, k), dtype=torch.int32).pin_memory()
     g_h = torch.empty((1, k)).pin_memory()
     n_e2e = max(20, args.steps)
-    for i in range(8):  # capture the per-token-buffer graphs
+    for i in range(8):  # warm-up (staging buffers, copy streams)
         w.host_wait(w.forward_host_async(0, host[i % 8:i % 8 + 1], out_h, ids_h, g_h))
     t_start = time.perf_counter()
     for i in range(n_e2e):

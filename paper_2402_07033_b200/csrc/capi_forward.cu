@@ -165,9 +165,6 @@ int moe_forward_host_async(moe_weights* w, int layer, const float* x_host, int n
   if (ha.x[slot].bytes < nx * 4 || ha.y[slot].bytes < ny * 4 || ha.ids[slot].bytes < nr * 4 ||
       ha.gates[slot].bytes < nr * 4) {
     CU(cudaEventSynchronize(ha.out_done[slot]));
-    for (auto& kv : ha.graphs)  // captured against the old staging buffers
-      if (kv.second.exec) cudaGraphExecDestroy(kv.second.exec);
-    ha.graphs.clear();
     TRY(ha.x[slot].ensure(nx * 4));
     if (ny) TRY(ha.y[slot].ensure(ny * 4));
     TRY(ha.ids[slot].ensure(nr * 4));
@@ -177,46 +174,6 @@ int moe_forward_host_async(moe_weights* w, int layer, const float* x_host, int n
   float* dy = layer >= 0 ? ha.y[slot].as<float>() : dx;
   int32_t* dids = ha.ids[slot].as<int32_t>();
   float* dg = ha.gates[slot].as<float>();
-  if (n_tok == 1 && (layer >= 0 ? use_layer_stack(w, 1, nullptr) : use_stack(w, 1))) {
-    // batch 1: token in, the one persistent launch, result + routing out as
-    // ONE graph on the host-API stream (a decode step's latency, no
-    // cross-stream hand-offs); captured once per (layer, host buffers, slot)
-    auto key = std::make_tuple(layer, x_host, out_host, ids_host, gates_host, slot,
-                               moe::debug_options().stack_kernel);
-    auto it = ha.graphs.find(key);
-    if (it == ha.graphs.end()) {
-      cudaStream_t cs = w->cap_stream;
-      cudaGraph_t g = nullptr;
-      CU(cudaStreamBeginCapture(cs, cudaStreamCaptureModeThreadLocal));
-      int rc = MOE_OK;
-      if (cudaMemcpyAsync(dx, x_host, nx * 4, cudaMemcpyHostToDevice, cs) != cudaSuccess)
-        rc = fail(MOE_ERR_CUDA, "capture of the token copy failed");
-      if (rc == MOE_OK)
-        rc = layer >= 0 ? enqueue_layer_stack(w, layer, dx, dy, dids, dg, cs) : enqueue_stack(w, dx, dids, dg, cs);
-      if (rc == MOE_OK && (cudaMemcpyAsync(out_host, dy, nx * 4, cudaMemcpyDeviceToHost, cs) != cudaSuccess ||
-                           cudaMemcpyAsync(ids_host, dids, nr * 4, cudaMemcpyDeviceToHost, cs) != cudaSuccess ||
-                           cudaMemcpyAsync(gates_host, dg, nr * 4, cudaMemcpyDeviceToHost, cs) != cudaSuccess))
-        rc = fail(MOE_ERR_CUDA, "capture of the result copies failed");
-      cudaError_t e = cudaStreamEndCapture(cs, &g);
-      if (rc != MOE_OK) {
-        if (g) cudaGraphDestroy(g);
-        return rc;
-      }
-      CU(e);
-      GraphEntry ge;
-      e = cudaGraphInstantiate(&ge.exec, g, 0);
-      cudaGraphDestroy(g);
-      CU(e);
-      it = ha.graphs.emplace(key, ge).first;
-    }
-    StreamOrder so(w, w->io_stream);
-    CU(cudaStreamWaitEvent(so.s, ha.out_done[slot], 0));  // the slot's previous results have left
-    CU(cudaGraphLaunch(it->second.exec, so.s));
-    CU(cudaEventRecord(ha.comp_done[slot], so.s));
-    CU(cudaEventRecord(ha.out_done[slot], so.s));
-    ha.next = t + 1;
-    return MOE_OK;
-  }
   // in: the slot's previous compute has consumed its tokens and its previous
   // results have left (the layer writes them in place)
   CU(cudaStreamWaitEvent(ha.cin, ha.comp_done[slot], 0));

@@ -77,7 +77,8 @@ struct moe_ctx {
   int win_world = 0, win_hidden = 0, win_tokens = 0;
   bool peers = false;
   moe::PeerArgs pa{};
-  unsigned fc_seq = 0;  // fused EP prefill combines issued (same count on every rank)
+  unsigned fc_seq = 0;  // multi-token peer exchanges issued (fused EP combine or delta
+                        // all-reduce; the same count on every rank) -> their data parity
   std::vector<void*> ipc_opened;
   std::mutex mu;
 };
@@ -174,8 +175,6 @@ struct moe_weights {
     DevBuf x[2], y[2], ids[2], gates[2];
     cudaEvent_t in_done[2] = {}, comp_done[2] = {}, out_done[2] = {};
     int64_t next = 0;
-    // batch-1 steps as one graph: (layer, x, out, ids, gates host pointers, slot, stack kernel)
-    std::map<std::tuple<int, const float*, float*, int32_t*, float*, int, int>, GraphEntry> graphs;
   } ha;
   using MoeHostAsync = MoeHostAsyncT;
   std::mutex mu;

@@ -28,9 +28,6 @@ void drop_graphs(moe_weights* w) {
   for (auto& kv : w->graphs)
     if (kv.second.exec) cudaGraphExecDestroy(kv.second.exec);
   w->graphs.clear();
-  for (auto& kv : w->ha.graphs)
-    if (kv.second.exec) cudaGraphExecDestroy(kv.second.exec);
-  w->ha.graphs.clear();
 }
 
 
@@ -349,7 +346,7 @@ int experts_forward(moe_weights* w, int l, const float* x, int n_tok, const int3
     const long long nd = (long long)n_tok * dm.d;
     if (w->ctx->peers && nd <= w->ctx->pa.mt_cap) {
       // reduce-scatter + all-gather over the peer windows (no NCCL)
-      CU(moe::launch_peer_allreduce(delta, x, x_out, nd, w->ctx->pa, s));
+      CU(moe::launch_peer_allreduce(delta, x, x_out, nd, w->ctx->pa, ++w->ctx->fc_seq, s));
     } else {
       TRY(allreduce(w, delta, (size_t)nd, s));
       CU(moe::launch_add(x, delta, x_out, nd, s, false));

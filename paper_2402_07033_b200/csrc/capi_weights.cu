@@ -249,8 +249,6 @@ int moe_weights_destroy(moe_weights* w) {
   cudaSetDevice(w->ctx->device);
   for (auto& kv : w->graphs)
     if (kv.second.exec) cudaGraphExecDestroy(kv.second.exec);
-  for (auto& kv : w->ha.graphs)
-    if (kv.second.exec) cudaGraphExecDestroy(kv.second.exec);
   if (w->cap_stream) cudaStreamDestroy(w->cap_stream);
   if (w->io_stream) cudaStreamDestroy(w->io_stream);
   if (w->order_ev) cudaEventDestroy(w->order_ev);

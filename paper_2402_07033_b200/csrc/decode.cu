@@ -1886,20 +1886,18 @@ PeerParts peer_window_parts(void* base, int world, int max_hidden, int max_token
 //  2 the owner (rank b % world) waits for all ranks' pflag, sums recv in rank
 //    order, pushes the sum into every rank's gath[par], releases gflag[b];
 //  3 every rank waits for its gflag[b] and writes x_out = x + gath.
-// Parity = the block's sequence number & 1: a rank reaches call c+2 only
+// Parity = the call's sequence number & 1 (the context's multi-token
+// exchange counter, shared with ep_combine_kernel so that the two kinds of
+// call alternate the same two data copies): a rank reaches call c+2 only
 // after call c+1 completed everywhere for this block, so no copy is
 // overwritten before it is read.
 __global__ void __launch_bounds__(256) peer_allreduce_kernel(const float* __restrict__ delta,
                                                              const float* x, float* x_out,
-                                                             long long n, PeerArgs pa) {
-  __shared__ unsigned s_seq;
+                                                             long long n, PeerArgs pa, unsigned seq) {
   const int b = blockIdx.x, B = gridDim.x, tid = threadIdx.x;
   const int W = pa.world, rk = pa.rank, owner = b % W;
   const long long e0 = n * b / B, e1 = n * (b + 1) / B;
   const long long cap = pa.mt_cap;
-  if (tid == 0) s_seq = pa.mt_seq[b] + 1u;
-  __syncthreads();
-  const unsigned seq = s_seq;
   const long long par = seq & 1u;
   // 1: scatter this rank's chunk to its owner
   float* dst = pa.mt_recv[owner] + (par * W + rk) * cap;
@@ -1926,7 +1924,6 @@ __global__ void __launch_bounds__(256) peer_allreduce_kernel(const float* __rest
   __syncthreads();
   const float* g = pa.mt_gath[rk] + par * cap;
   for (long long i = e0 + tid; i < e1; i += blockDim.x) x_out[i] = x[i] + __ldcv(g + i);
-  if (tid == 0) pa.mt_seq[b] = seq;
 }
 
 // Expert-parallel prefill combine, streamed beside the grouped kernel (fused
@@ -2094,9 +2091,9 @@ cudaError_t launch_ep_combine(const float* x, const float* y, int n_tok, const D
 }
 
 cudaError_t launch_peer_allreduce(const float* delta, const float* x, float* x_out, long long n,
-                                  const PeerArgs& pa, cudaStream_t s) {
+                                  const PeerArgs& pa, unsigned seq, cudaStream_t s) {
   if (n <= 0) return cudaSuccess;
-  peer_allreduce_kernel<<<kMtBlocks, 256, 0, s>>>(delta, x, x_out, n, pa);
+  peer_allreduce_kernel<<<kMtBlocks, 256, 0, s>>>(delta, x, x_out, n, pa, seq);
   return cudaGetLastError();
 }
 

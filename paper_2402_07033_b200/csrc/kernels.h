@@ -196,7 +196,7 @@ cudaError_t launch_ep_combine(const float* x, const float* y, int n_tok, const D
                               const uint32_t* holders, int* queue, const PeerArgs& pa, unsigned seq,
                               cudaStream_t s, bool pdl);
 cudaError_t launch_peer_allreduce(const float* delta, const float* x, float* x_out, long long n,
-                                  const PeerArgs& pa, cudaStream_t s);
+                                  const PeerArgs& pa, unsigned seq, cudaStream_t s);
 // x_out = x + sum_{r in rank order} delta_r, where delta_r = this layer's
 // fixed-order sum of rank r's per-CTA partials.  Each block reduces 32 hidden
 // columns, stores them into every peer's inbox (P2P stores), releases a

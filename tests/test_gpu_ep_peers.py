@@ -195,3 +195,43 @@ def test_peer_multi_token_combine(gpu, libopts, mode, world, shape, dtype, n_tok
         c.close()
     full.close()
     base.close()
+
+
+def test_mixed_fused_and_unfused_prefill_exchanges_back_to_back(gpu, libopts):
+    """Fused (streamed home-rank combine) and unfused (delta -> peer
+    all-reduce) multi-token layers enqueued back to back on every rank with
+    no host synchronisation in between: both kinds share the windows' two
+    data copies through one per-context sequence counter, so none overwrites
+    a copy another is still reading."""
+    world, L, E, k, d, f, n = 2, 1, 8, 2, 1024, 2048, 96
+    s = M.Shape(L, E, k, d, f, 2)
+    ctxs = [M.Ctx(0) for _ in range(world)]
+    M.Ctx.link_peers(ctxs, d, max_tokens=n)
+    owner = _bench().shard_map(L, E, world)
+    ws = [M.Weights(c, s, M.DTYPE_BF16, owner=owner) for c in ctxs]
+    for w in ws:
+        w.random(5)
+        w.reserve(n)
+    gen = torch.Generator(device="cuda").manual_seed(3)
+    xs = [torch.randn(n, d, device="cuda", generator=gen) for _ in range(4)]
+    plan = [1, 0, 0, 1, 1, 0, 1, 0]
+    outs = [[torch.empty_like(xs[0]) for _ in plan] for _ in range(world)]
+    ids = [[torch.zeros((n, k), dtype=torch.int32, device="cuda") for _ in plan] for _ in range(world)]
+    gs = [[torch.zeros((n, k), device="cuda") for _ in plan] for _ in range(world)]
+    torch.cuda.synchronize()
+    for i, fused in enumerate(plan):
+        libopts(prefill_fused=fused)
+        for r in range(world):
+            ws[r].layer_forward(0, xs[i % 4], outs[r][i], ids[r][i], gs[r][i], stream=ctxs[r].stream)
+    for c in ctxs:
+        c.synchronize()
+        c.peer_check()
+    for i in range(len(plan)):
+        assert torch.equal(outs[1][i], outs[0][i]), i
+        for j in range(i):
+            if i % 4 == j % 4:  # same tokens, fused or not: bit-identical
+                assert torch.equal(outs[0][i], outs[0][j]), (i, j)
+    for w in ws:
+        w.close()
+    for c in ctxs:
+        c.close()

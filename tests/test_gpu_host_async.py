@@ -60,7 +60,7 @@ def test_host_async_layer_and_stack_equal_device_calls(ctx, d, f, dt):
     w.host_wait()
     for t, layer, x, out, ids, g in calls:
         want = _device_layer(w, layer, x, k) if layer >= 0 else _device_stack(w, x, L, k)
-        assert np.array_equal(out.numpy(), want[0]), (t, layer)
+        assert np.array_equal(out.numpy(), want[0]), (t, layer, float(np.abs(out.numpy() - want[0]).max()))
         assert np.array_equal(ids.numpy(), want[1]), (t, layer)
         assert np.array_equal(g.numpy(), want[2]), (t, layer)
     w.close()
