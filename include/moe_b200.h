@@ -263,10 +263,13 @@ int moe_forward_host(moe_weights* w, const double* tokens, int n_tok, double* ou
  * (fp32 [n_tok x hidden], pinned for overlap), one layer (layer >= 0:
  * moe_layer_forward; ids/gates [n_tok x k]) or the whole stack (layer == -1:
  * moe_forward; ids/gates [L x n_tok x k]) and the D2H of the result and the
- * routing, and return.  Copies run on their own streams, so the copies of
- * consecutive calls overlap the previous / next call's compute (two device
- * staging slots).  *ticket identifies the call; moe_host_wait(w, ticket)
- * blocks until its outputs are in host memory (ticket < 0: every call).  The
+ * routing, and return.  Multi-token copies run on their own streams, so
+ * the copies of consecutive calls overlap the previous / next call's compute
+ * (two device staging slots); a batch-1 step's copies ride the compute
+ * stream (a decode step has nothing to overlap).  Results land in ticket
+ * order.  *ticket identifies the call; moe_host_wait(w, ticket) blocks until
+ * its outputs (and every earlier call's) are in host memory (ticket < 0:
+ * every call).  The
  * host buffers must stay valid until then. */
 int moe_forward_host_async(moe_weights* w, int layer, const float* x_host, int n_tok,
                            float* out_host, int32_t* ids_host, float* gates_host,

@@ -132,7 +132,8 @@ int moe_forward(moe_weights* w, float* x, int n_tok, int32_t* ids, float* gates,
 }
 
 // Pipelined host-buffer steps: H2D of call i+1 and D2H of call i-1 run on
-// their own copy streams while call i computes (two device staging slots).
+// their own copy streams while call i computes (two device staging slots);
+// batch-1 steps keep their copies on the compute stream.
 int moe_forward_host_async(moe_weights* w, int layer, const float* x_host, int n_tok,
                            float* out_host, int32_t* ids_host, float* gates_host, int64_t* ticket) {
   if (!w) return fail(MOE_ERR_ARG, "null weights");
@@ -174,6 +175,32 @@ int moe_forward_host_async(moe_weights* w, int layer, const float* x_host, int n
   float* dy = layer >= 0 ? ha.y[slot].as<float>() : dx;
   int32_t* dids = ha.ids[slot].as<int32_t>();
   float* dg = ha.gates[slot].as<float>();
+  if (n_tok == 1) {
+    // a decode step waits on its own result before the next token exists:
+    // nothing to overlap, so the copies ride the compute stream (no
+    // cross-stream event hand-offs on the latency path)
+    StreamOrder so(w, w->io_stream);
+    cudaStream_t s = so.s;
+    // both slots' earlier D2H first: tickets stay completed in order
+    CU(cudaStreamWaitEvent(s, ha.out_done[0], 0));
+    CU(cudaStreamWaitEvent(s, ha.out_done[1], 0));
+    CU(cudaMemcpyAsync(dx, x_host, nx * 4, cudaMemcpyHostToDevice, s));
+    if (layer >= 0) {
+      TRY(experts_forward(w, layer, dx, n_tok, dids, dg, dy, nullptr, s, true, nullptr, nullptr,
+                          nullptr, w->router + (size_t)layer * w->E() * w->d()));
+    } else if (w->plan.ok) {
+      TRY(forward_graph(w, dx, dids, dg, s));
+    } else {
+      TRY(enqueue_forward(w, dx, n_tok, dids, dg, s, nullptr));
+    }
+    CU(cudaMemcpyAsync(out_host, dy, nx * 4, cudaMemcpyDeviceToHost, s));
+    CU(cudaMemcpyAsync(ids_host, dids, nr * 4, cudaMemcpyDeviceToHost, s));
+    CU(cudaMemcpyAsync(gates_host, dg, nr * 4, cudaMemcpyDeviceToHost, s));
+    CU(cudaEventRecord(ha.comp_done[slot], s));
+    CU(cudaEventRecord(ha.out_done[slot], s));
+    ha.next = t + 1;
+    return MOE_OK;
+  }
   // in: the slot's previous compute has consumed its tokens and its previous
   // results have left (the layer writes them in place)
   CU(cudaStreamWaitEvent(ha.cin, ha.comp_done[slot], 0));
@@ -208,9 +235,11 @@ int moe_host_wait(moe_weights* w, int64_t ticket) {
   std::lock_guard<std::mutex> lk(w->mu);
   if (!w->ha.cout || ticket >= w->ha.next) return MOE_OK;
   TRY(set_device(w->ctx));
-  // out is in-order: the slot's latest D2H covers every earlier ticket of it
-  if (ticket < 0) CU(cudaStreamSynchronize(w->ha.cout));
-  else CU(cudaEventSynchronize(w->ha.out_done[ticket & 1]));
+  // results land in ticket order (multi-token D2H in order on the out
+  // stream; a batch-1 step's copies ride the compute stream after every
+  // earlier D2H), so the slot's latest out event covers every earlier ticket
+  if (ticket < 0) ticket = w->ha.next - 1;
+  CU(cudaEventSynchronize(w->ha.out_done[ticket & 1]));
   return MOE_OK;
 }
 

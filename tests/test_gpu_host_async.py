@@ -73,3 +73,30 @@ def test_host_async_errors(ctx):
         w.forward_host_async(2, x, x.copy(), np.zeros((4, 2), np.int32), np.zeros((4, 2), np.float32))
     w.host_wait()  # nothing in flight: returns
     w.close()
+
+
+def test_host_async_results_land_in_ticket_order(ctx):
+    """Waiting on a batch-1 step (copies on the compute stream) also covers
+    the multi-token steps before it (copies on the copy streams), and the
+    other way round."""
+    L, E, k, d, f = 2, 8, 2, 512, 1792
+    w = M.Weights(ctx, M.Shape(L, E, k, d, f, 4), M.DTYPE_F32)
+    w.random(5)
+    rs = np.random.RandomState(3)
+    for seq in ([(0, 900), (1, 1)], [(1, 1), (0, 1), (1, 640)], [(0, 333), (-1, 1), (1, 2), (0, 1)]):
+        calls = []
+        for layer, n in seq:
+            x = (0.1 * rs.randn(n, d)).astype(np.float32)
+            nl = L if layer < 0 else 1
+            out = torch.empty((n, d)).pin_memory()
+            ids = torch.empty((nl, n, k) if layer < 0 else (n, k), dtype=torch.int32).pin_memory()
+            g = torch.empty(ids.shape).pin_memory()
+            xh = torch.tensor(x).pin_memory()  # stays referenced until the wait
+            t = w.forward_host_async(layer, xh, out, ids, g)
+            calls.append((layer, x, xh, out, ids, g))
+        w.host_wait(t)  # the last ticket only
+        for layer, x, _, out, ids, g in calls:
+            want = _device_layer(w, layer, x, k) if layer >= 0 else _device_stack(w, x, L, k)
+            assert np.array_equal(out.numpy(), want[0]), (seq, layer)
+            assert np.array_equal(ids.numpy(), want[1]), (seq, layer)
+    w.close()
