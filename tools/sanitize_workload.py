@@ -1,9 +1,12 @@
 """compute-sanitizer workload: the fused prefill layer and forward (ragged
 token counts, top-2 / top-3), stack kernels 2 and 3 and the 1-layer stack,
-at small shapes (the sanitizer slows kernels 10-100x).
+and the pipelined host-buffer API, at small shapes (the sanitizer slows
+kernels 10-100x).
 
     compute-sanitizer --tool memcheck  python tools/sanitize_workload.py
     compute-sanitizer --tool racecheck python tools/sanitize_workload.py
+    compute-sanitizer --tool synccheck python tools/sanitize_workload.py
+    compute-sanitizer --tool initcheck python tools/sanitize_workload.py
 """
 import sys, os
 sys.path.insert(0, os.getcwd())
@@ -26,4 +29,14 @@ for kern in (2, 3):
     w.forward(x, ids, g); torch.cuda.synchronize()
     xo = torch.empty_like(x); w.layer_forward(1, x, xo, ids[0], g[0]); torch.cuda.synchronize()
     w.close()
+# pipelined host-buffer API: batch 1 (copies on the compute stream) and
+# multi-token (copy streams), one layer and the whole stack
+w = M.Weights(ctx, M.Shape(2, 8, 2, 1024, 2048, 2), M.DTYPE_BF16); w.random(2)
+keep = []
+for layer, n in [(0, 1), (1, 40), (-1, 1), (-1, 9)]:
+    nl = 2 if layer < 0 else 1
+    xh = (0.1 * torch.randn(n, 1024)).pin_memory(); out = torch.empty(n, 1024).pin_memory()
+    ih = torch.empty((nl, n, 2) if layer < 0 else (n, 2), dtype=torch.int32).pin_memory(); gh = torch.empty(ih.shape).pin_memory()
+    keep.append((xh, out, ih, gh)); w.forward_host_async(layer, xh, out, ih, gh)
+w.host_wait(); w.close()
 print("sanitizer workload done")
