@@ -21,7 +21,8 @@ def main():
     ap.add_argument("--rounds", type=int, default=3)
     ap.add_argument("--iters", type=int, default=20)
     ap.add_argument("--cfgs", default="2:3,4:2,4:3,3:3,2:8,4:8,1:0",
-                    help="S:late8[:slo] (slo = K split of the other experts' downs, 0 = S/2)")
+                    help="S:late8[:slo[:lag]] (slo = K split of the other experts' downs, 0 = S/2; "
+                         "lag = pf_lag, 8 = every down after every up)")
     args = ap.parse_args()
     import torch
 
@@ -31,7 +32,7 @@ def main():
     ctx = M.Ctx(0)
     sp = ctx.stream
     st = torch.cuda.ExternalStream(sp)
-    cfgs = [tuple(int(v) for v in (c + ":0" if c.count(":") == 1 else c).split(":")) for c in args.cfgs.split(",")]
+    cfgs = [tuple(int(v) for v in (c.split(":") + ["0", "8"][c.count(":") - 1:])[:4]) for c in args.cfgs.split(",")]
     ws = {}
     for S in sorted({c[0] for c in cfgs}):
         M.set_option("prefill_splits", S)
@@ -49,7 +50,8 @@ def main():
     times = {c: [] for c in cfgs}
     for _ in range(args.rounds):
         for c in cfgs:
-            S, late, slo = c
+            S, late, slo, lag = c
+            M.set_option("pf_lag", lag)
             M.set_option("pf_late8", late)
             M.set_option("pf_slo", slo)
             w = ws[S]
@@ -65,7 +67,8 @@ def main():
             times[c].append(e0.elapsed_time(e1) / args.iters * 1e3)
     M.set_option("pf_late8", 3)
     M.set_option("pf_slo", 0)
-    print(json.dumps({f"splits{c[0]}_late{c[1]}_slo{c[2]}": round(float(np.median(v)), 1) for c, v in times.items()},
+    M.set_option("pf_lag", 8)
+    print(json.dumps({f"splits{c[0]}_late{c[1]}_slo{c[2]}_lag{c[3]}": round(float(np.median(v)), 1) for c, v in times.items()},
                      indent=1))
 
 
