@@ -394,7 +394,9 @@ def run_ours(args):
         ach = rank_bytes / (kern_ms * 1e-3) / 1e9
         per_rank = gather_floats(round(ach, 1), world)
         roof = {"bound": "hbm", "achieved": round(ach, 1), "peak": peak, "unit": "GB/s",
-                "frac": round(ach / peak, 4), "traffic": args.stack_traffic if world == 1 else None,
+                "frac": round(ach / peak, 4),
+                # the committed capture is of the 32-layer Mixtral stack
+                "traffic": args.stack_traffic if world == 1 and args.config == "stack32" and L == 32 else None,
                 "kernel": (f"{STACK_KERNEL_NAME[M.get_option('stack_kernel')]}<bf16,2> (one launch per token)" if world == 1 else
                            "decode_stack_kernel<bf16,2> with in-kernel NVLink exchange (one launch per token per rank)"),
                 "kernel_us": round(kern_ms * 1e3, 2), "alg_bytes_per_launch": rank_bytes,
@@ -477,6 +479,8 @@ def bench_layer(args, w, stream, stream_ptr, device, peaks, peak_src):
     kernel + reduce/residual."""
     import torch
 
+    import paper_2402_07033_b200 as M
+
     L, E, k, d, f, _ = CONFIGS["layer"]
     n_rep = max(50, 10 * args.steps)
     toks = torch.tensor(token_pool(args.seed, 8, d, 1), device=device)
@@ -500,13 +504,15 @@ def bench_layer(args, w, stream, stream_ptr, device, peaks, peak_src):
     if launches == 1:
         # the dominant (only) kernel: one launch per step, so the back-to-back
         # loop above times it (per-launch event pairs would add ~3 us each)
-        kname = "decode_stack2_kernel<bf16,2> as a 1-layer stack (one launch per token)"
+        kname = f"{STACK_KERNEL_NAME[M.get_option('stack_kernel')]}<bf16,2> as a 1-layer stack (one launch per token)"
+        traffic = args.layer_traffic
         kern_ms = ms
         kalg = alg + E * d * 4
         path = "moe_layer_forward: one launch of the persistent kernel as a 1-layer stack"
     else:
         # dominant kernel: the streaming expert kernel, timed alone
         kname = "decode_experts_kernel<bf16,2>"
+        traffic = args.traffic
         ypart = torch.empty((w.ctx.sm_count, d), dtype=torch.float32, device=device)
         sel = torch.tensor([1, 5], dtype=torch.int32, device=device)
         gt = torch.full((k,), 0.5, device=device)
@@ -547,7 +553,7 @@ def bench_layer(args, w, stream, stream_ptr, device, peaks, peak_src):
                     "api": "moe_forward_host_async(layer 0) + moe_host_wait per token (synchronous steps): "
                            "pinned fp32 token in, output + ids + gates out; host wall clock"},
             "roofline": {"bound": "hbm", "achieved": round(ach, 1), "peak": peak, "unit": "GB/s",
-                         "frac": round(ach / peak, 4), "traffic": args.traffic,
+                         "frac": round(ach / peak, 4), "traffic": traffic,
                          "kernel": kname, "kernel_us": round(kern_ms * 1e3, 2),
                          "alg_bytes_per_launch": kalg,
                          "alg_bytes_basis": f"{k} experts x 3 x {d} x {f} x 2 B" + (
@@ -907,6 +913,7 @@ def main():
         sys.exit(2)
     args.stack_traffic = None
     args.prefill_traffic = None
+    args.layer_traffic = None
     tp = os.path.join(ROOT, "profiles", "decode_traffic.json")
     if os.path.exists(tp):
         tj = json.load(open(tp))
@@ -914,6 +921,7 @@ def main():
             args.traffic = tj.get("dram_bytes_per_launch")
         args.stack_traffic = tj.get("stack_dram_bytes_per_launch")
         args.prefill_traffic = tj.get("prefill_dram_bytes_per_launch")
+        args.layer_traffic = tj.get("layer_stack_dram_bytes_per_launch")
     if args.impl == "ours":
         import paper_2402_07033_b200 as M
 

@@ -66,6 +66,33 @@ def full_summary(rep):
     return res
 
 
+def _gbytes(v):
+    num, unit = v.split()
+    return float(num) * {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}[unit]
+
+
+def update_traffic(full, tag):
+    """profiles/decode_traffic.json: DRAM bytes per launch of each bench
+    line's dominant kernel (read + write, from the full captures); bench.py
+    puts them in the lines' roofline.traffic."""
+    path = os.path.join(ROOT, "profiles", "decode_traffic.json")
+    tj = json.load(open(path)) if os.path.exists(path) else {}
+    picks = {"stack": ("stack_full", "decode_stack"), "layer_stack": ("layer_full", "decode_stack"),
+             "prefill": ("prefill_full", "prefill_grouped")}
+    for key, (cap, kname) in picks.items():
+        for k in full.get(cap, []):
+            if kname in k["Kernel Name"]:
+                rd, wr = _gbytes(k["dram__bytes_read.sum"]), _gbytes(k["dram__bytes_write.sum"])
+                pre = f"{key}_"
+                tj[pre + "kernel"] = k["Kernel Name"]
+                tj[pre + "dram_bytes_per_launch"] = int(rd + wr)
+                tj[pre + "dram_bytes_read"] = int(rd)
+                tj[pre + "dram_bytes_write"] = int(wr)
+                tj[pre + "source"] = f"ncu --set full --clock-control none (profiles/{tag}_ncu_full_summary.json, {cap})"
+                break
+    json.dump(tj, open(path, "w"), indent=1)
+
+
 def main():
     src, tag = sys.argv[1], sys.argv[2]
     prof = os.path.join(ROOT, "profiles")
@@ -79,11 +106,12 @@ def main():
     json.dump(shares, open(os.path.join(prof, f"{tag}_launch_shares.json"), "w"), indent=1)
     full = {"note": "ncu --set full --clock-control none (cache flushed between replays): DRAM bytes "
                     "and pipe utilisation per launch; durations are cold-cache"}
-    for name in ("stack_full", "prefill_full"):
+    for name in ("stack_full", "layer_full", "prefill_full"):
         rep = os.path.join(src, f"{name}.ncu-rep")
         if os.path.exists(rep):
             full[name] = full_summary(rep)
     json.dump(full, open(os.path.join(prof, f"{tag}_ncu_full_summary.json"), "w"), indent=1)
+    update_traffic(full, tag)
     for f in ("bench_stack32", "bench_prefill512", "bench_layer"):
         p = os.path.join(src, f + ".json")
         if os.path.exists(p):
