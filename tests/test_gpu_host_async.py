@@ -55,10 +55,13 @@ def test_host_async_layer_and_stack_equal_device_calls(ctx, d, f, dt):
         ids = torch.empty((nl, n, k) if layer < 0 else (n, k), dtype=torch.int32).pin_memory()
         g = torch.empty(ids.shape).pin_memory()
         t = w.forward_host_async(layer, xh, out, ids, g)
-        calls.append((t, layer, x, out, ids, g))
+        # the pinned input stays referenced until the wait: freed, torch's
+        # caching host allocator would hand its block to the next
+        # pin_memory() while the H2D is still queued
+        calls.append((t, layer, x, xh, out, ids, g))
     w.host_wait(calls[3][0])  # a middle ticket first
     w.host_wait()
-    for t, layer, x, out, ids, g in calls:
+    for t, layer, x, _, out, ids, g in calls:
         want = _device_layer(w, layer, x, k) if layer >= 0 else _device_stack(w, x, L, k)
         assert np.array_equal(out.numpy(), want[0]), (t, layer, float(np.abs(out.numpy() - want[0]).max()))
         assert np.array_equal(ids.numpy(), want[1]), (t, layer)
