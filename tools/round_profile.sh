@@ -23,7 +23,7 @@ timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -k "$K" -c
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:decode_stack -s 3 -c 1 \
   -o $O/stack_full python bench.py --steps 5 --warmup 3 --no-cpu-baseline > /dev/null 2>&1
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:decode_stack -s 3 -c 1 \
-  -o $O/layer_full python bench.py --config layer --steps 5 --warmup 3 --no-cpu-baseline > /dev/null 2>&1
+  -o $O/layer_full python tools/prof_layer_stack.py > /dev/null 2>&1
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:"prefill_grouped|router_topk|combine" -s 6 -c 3 \
   -o $O/prefill_full python tools/prof_prefill.py --iters 3 --no-prof > /dev/null 2>&1
 ls -la $O
