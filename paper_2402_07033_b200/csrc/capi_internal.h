@@ -152,6 +152,7 @@ struct moe_weights {
   std::vector<DevBuf> rw_mem;  // [L-1]
   DevBuf dev_rw;               // device [L] pointers
   bool rw_enabled = false, rw_dirty = true;
+  bool stack2_ok = false;  // the single-barrier stack kernel fits (accumulators allocated)
   bool stack_enabled = true;
   // fused sparsity counters of the call in flight (moe_forward_sparsity):
   // counts [L][sp.n]; layer l adds into sp.counts + l * sp.n

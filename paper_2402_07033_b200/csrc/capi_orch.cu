@@ -118,8 +118,7 @@ int refresh_projection(moe_weights* w) {
 // The single-barrier fixed-point stack kernel (single GPU, E <= 8, router
 // projections on); decode_stack_kernel otherwise.
 bool use_stack2(const moe_weights* w) {
-  return moe::debug_options().stack_kernel >= 2 && !w->ctx->ep() && w->rw_enabled && w->stack_acc.p != nullptr &&
-         moe::stack2_supported(w->plan, w->dims());
+  return moe::debug_options().stack_kernel >= 2 && !w->ctx->ep() && w->stack2_ok && w->stack_acc.p != nullptr;
 }
 
 // One layer at batch 1 (moe_layer_forward) through the single-barrier
@@ -133,7 +132,7 @@ bool use_layer_stack(const moe_weights* w, int n_tok, const float* post) {
 int enqueue_layer_stack(moe_weights* w, int l, const float* x, float* x_out, int32_t* ids,
                         float* gates, cudaStream_t s) {
   moe::StackDesc sd;
-  sd.rw = w->dev_rw.as<const float* const>() + l;  // not read: a 1-layer stack has no next router
+  sd.rw = w->rw_enabled ? w->dev_rw.as<const float* const>() + l : nullptr;  // not read: L = 1
   sd.layer_experts = w->dev_layers.as<const void* const>() + l;
   sd.slot_of = w->dev_slots.as<const int16_t>() + (size_t)l * w->E();
   sd.expert_stride = 3 * w->mat_elems();

@@ -124,7 +124,12 @@ static int weights_create(moe_ctx* c, const moe_shape* shape, int dtype,
       cudaStreamCreateWithFlags(&w->io_stream, cudaStreamNonBlocking) != cudaSuccess)
     return cleanup(fail(MOE_ERR_CUDA, "create streams"));
   w->stack_enabled = moe::debug_options().stack != 0;
-  if (w->rw_enabled && !c->ep() && moe::stack2_supported(w->plan, w->dims())) {
+  // the single-barrier kernel: its next-layer logits come from the
+  // projections, so L >= 2 needs them; a 1-layer model has no next layer
+  w->stack2_ok = w->plan.ok && !c->ep() && E <= 8 && (size_t)E * shape->hidden_dim * 4 <= 200 * 1024 &&
+                 moe::debug_options().rw && (L == 1 || w->rw_enabled) &&
+                 moe::stack2_supported(w->plan, w->dims());
+  if (w->stack2_ok) {
     if (w->stack_acc.ensure(moe::stack2_acc_bytes(w->dims())))  // zeroed: the kernel's invariant
       return cleanup(fail(MOE_ERR_OOM, "cudaMalloc stack accumulators"));
     w->device_bytes += (int64_t)w->stack_acc.bytes;

@@ -1783,7 +1783,8 @@ static cudaError_t launch_stack2_t(const DecodePlan& p, const Dims& dm, const St
 cudaError_t launch_decode_stack2(const DecodePlan& p, const StackDesc& sd, const Dims& dm, float* x,
                                  void* accbuf, int32_t* ids_out, float* gates_out,
                                  float* logits_out, cudaStream_t s, float* x_out) {
-  if (!stack2_supported(p, dm) || sd.rw == nullptr) return cudaErrorInvalidValue;
+  // (the projections are read only for a next layer)
+  if (!stack2_supported(p, dm) || (sd.rw == nullptr && sd.L > 1)) return cudaErrorInvalidValue;
   Stack2Args a;
   a.layer_experts = sd.layer_experts;
   a.slot_of = sd.slot_of;

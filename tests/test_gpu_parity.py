@@ -742,3 +742,46 @@ def test_layer_forward_batch1_is_one_launch_every_layer(ctx, orc, libopts, dt):
         assert normwise(outs[0][0] - x, outs[2][0] - x) < 1e-5
     w.close()
     w_ref.close()
+
+
+@pytest.mark.parametrize("dt", [M.DTYPE_BF16, M.DTYPE_F32])
+def test_one_layer_model_runs_the_single_barrier_kernel(ctx, orc, libopts, dt):
+    """A 1-layer model (BASELINE configs[1] as its own model) gets the same
+    one-launch single-barrier kernel at batch 1 for moe_layer_forward and
+    moe_forward — it has no next router, so no projections are needed — and
+    matches the oracle and the per-layer kernels."""
+    d, f = 4096, 14336
+    s = M.Shape(1, 8, 2, d, f, 2 if dt == M.DTYPE_BF16 else 4)
+    w = M.Weights(ctx, s, dt)
+    libopts(stack=0)
+    w_ref = M.Weights(ctx, s, dt)
+    libopts(stack=1)
+    assert w.layer_launches(1) == 1 and w.forward_launches(1) == 1 and w_ref.layer_launches(1) == 3
+    w.random(23)
+    w_ref.random(23)
+    rs = np.random.RandomState(6)
+    for rep in range(3):
+        x = f32(0.5 * rs.randn(d))
+        outs = []
+        for ww, fwd in ((w, False), (w, True), (w_ref, False)):
+            xd = torch.tensor(x[None], dtype=torch.float32, device="cuda")
+            ids = torch.zeros((1, 2), dtype=torch.int32, device="cuda")
+            g = torch.zeros((1, 2), dtype=torch.float32, device="cuda")
+            if fwd:
+                xo = xd
+                ww.forward(xd, ids.view(1, 1, 2), g.view(1, 1, 2))
+            else:
+                xo = torch.empty_like(xd)
+                ww.layer_forward(0, xd, xo, ids, g)
+            torch.cuda.synchronize()
+            outs.append((xo.cpu().numpy()[0].astype(np.float64), ids.cpu().numpy()[0], g.cpu().numpy()[0]))
+        assert all(np.array_equal(outs[0][i], outs[1][i]) for i in range(3)), rep  # same kernel, same launch
+        oid, og, delta, mg = oracle_layer(orc, w, 0, x, 2)
+        if mg > 1e-5:
+            assert list(outs[0][1]) == list(oid) == list(outs[2][1]), rep
+            assert np.abs(outs[0][2] - og).max() < 1e-5
+        err = normwise(outs[0][0] - x, delta)
+        assert err < (1e-4 if dt == M.DTYPE_BF16 else TOL_F32), (rep, err)
+        assert normwise(outs[0][0] - x, outs[2][0] - x) < 1e-5
+    w.close()
+    w_ref.close()
