@@ -119,7 +119,11 @@ class ClockSampler:
                  "-lms", "50"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self.thread = threading.Thread(target=self._read, daemon=True)
             self.thread.start()
-            time.sleep(0.15)  # the first sample lands before the timed region
+            # nvidia-smi is streaming (its first sample landed) before the
+            # timed region starts
+            t0 = time.time()
+            while not self.samples and time.time() - t0 < 5.0 and self.proc.poll() is None:
+                time.sleep(0.01)
         except (FileNotFoundError, OSError):
             self.proc = None
         return self
@@ -132,7 +136,11 @@ class ClockSampler:
 
     def __exit__(self, *a):
         if self.proc:
-            time.sleep(0.06)
+            # one more sample after the region (a short region may fall
+            # between two 50 ms samples)
+            n0, t0 = len(self.samples), time.time()
+            while len(self.samples) == n0 and time.time() - t0 < 1.0 and self.proc.poll() is None:
+                time.sleep(0.01)
             self.proc.terminate()
             try:
                 self.proc.wait(timeout=5)
@@ -482,7 +490,7 @@ def bench_layer(args, w, stream, stream_ptr, device, peaks, peak_src):
     import paper_2402_07033_b200 as M
 
     L, E, k, d, f, _ = CONFIGS["layer"]
-    n_rep = max(50, 10 * args.steps)
+    n_rep = max(1000, 10 * args.steps)  # >= ~120 ms: spans several clock samples
     toks = torch.tensor(token_pool(args.seed, 8, d, 1), device=device)
     xo = torch.empty((1, d), device=device)
     ids = torch.zeros((1, k), dtype=torch.int32, device=device)
