@@ -157,6 +157,27 @@ int moe_weights_replica_cost(const moe_weights* w, int64_t* weight_ps, int64_t* 
 int moe_replica_plan(const int32_t* counts, int E, const uint32_t* holders, int world,
                      int64_t weight_ps, int64_t row_ps, int64_t part_ps, int chunk, int rank,
                      int32_t* lo, int32_t* hi, int64_t* makespan);
+/* Co-selection-aware expert-parallel shard map (an extension of
+ * the popularity placement, placement.cpp:68-95, re-expressed for EP): per
+ * layer, owner[l][e] in [0, world) minimising the co-selections
+ * pairs[l][a][b] + pairs[l][b][a] of experts on the same rank (at batch 1 a
+ * token whose top-2 share a rank streams both there: 2 expert-streams
+ * instead of 1), with floor/ceil(E/world) experts per rank; ties to the
+ * smaller largest per-rank popularity load counts[l][e]; deterministic.
+ * Pairwise-swap local search from the popularity LPT map, then a branch and
+ * bound seeded with it: exact[l] = 1 when that finished within its node
+ * budget (the map is optimal), else 0 (the best map found).  counts [L x E], pairs
+ * [L x E x E] (moe_routing_pair_histogram's, read back), host memory; exact
+ * may be NULL.  Needs no device. */
+int moe_ep_shard_map_coselect(const int64_t* counts, const int64_t* pairs, int n_layers, int n_experts,
+                              int world, int32_t* owner, int32_t* exact);
+/* Device co-selection histogram: pairs[l][a][b] (int64, device,
+ * [n_layers x n_experts x n_experts], a < b) += the number of tokens of
+ * layer l whose top-k holds both a and b, from an ids record
+ * [n_layers x n_tok x top_k].  Accumulates across calls, like
+ * moe_routing_histogram; feeds moe_ep_shard_map_coselect. */
+int moe_routing_pair_histogram(moe_ctx* ctx, const int32_t* ids, int n_layers, int n_tok, int top_k,
+                               int n_experts, int64_t* pairs, void* stream);
 /* Allocate every scratch buffer for calls of up to max_tokens tokens (and the
  * batch-1 router projections) now, so no later call allocates or frees
  * device memory (cudaFree synchronizes the device).  Serving loops and

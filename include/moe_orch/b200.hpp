@@ -17,8 +17,8 @@ void set_dtype(Dtype dtype);
 Dtype dtype();
 // CUDA device used by the drop-in entry points (default 0 / $MOE_B200_DEVICE).
 void set_device(int device);
-// Device copies of ModelWeights are cached by address + a sampled content
-// fingerprint; call this after mutating weights in place.
+// Device copies of ModelWeights are cached by a digest of their full
+// contents (an in-place edit anywhere is seen); this drops the cache.
 void invalidate_weights_cache();
 
 // The paper's popularity placement re-expressed as expert parallelism:
@@ -27,6 +27,17 @@ void invalidate_weights_cache();
 // least-loaded rank with spare slots (LPT; ties to the lower rank), each rank
 // holding ceil(E / world) experts at most.
 std::vector<std::vector<int>> ep_shard_map(const PopularityProfile& profile, int world);
+// Co-selection-aware variant: per layer, the balanced map
+// (floor/ceil(E / world) experts per rank) that minimises the co-selections
+// of experts sharing a rank — pair_counts[l][a][b] tokens chose both a and b
+// (moe_routing_pair_histogram, read back) — since a batch-1 token whose
+// top-2 share a rank streams both there; ties to the smaller largest
+// popularity load; deterministic.  Pairwise-swap local search from
+// ep_shard_map's map, then an exact branch and bound seeded with it under a
+// node budget (shard_plan.h).  ValidationError on shape mismatch or negative counts.
+std::vector<std::vector<int>> ep_shard_map_coselect(
+    const PopularityProfile& profile,
+    const std::vector<std::vector<std::vector<std::int64_t>>>& pair_counts, int world);
 // profile_from_trace (placement.cpp:30-43) from per-(layer, expert) selection
 // counts, e.g. a device routing histogram (moe_routing_histogram) read back
 // after a calibration run; ValidationError on ragged rows or negative counts.

@@ -21,6 +21,7 @@ from .capi import (  # noqa: F401
     Shape,
     Weights,
     declared_symbols,
+    ep_shard_map_coselect,
     get_option,
     lib,
     lib_path,

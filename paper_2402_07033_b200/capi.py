@@ -103,6 +103,8 @@ def lib():
         "moe_weights_replica_cost": ([_vp] + [C.POINTER(C.c_int64)] * 3, C.c_int),
         "moe_replica_plan": ([_vp, C.c_int, _vp, C.c_int, C.c_int64, C.c_int64, C.c_int64, C.c_int,
                               C.c_int, _vp, _vp, C.POINTER(C.c_int64)], C.c_int),
+        "moe_ep_shard_map_coselect": ([_vp, _vp, C.c_int, C.c_int, C.c_int, _vp, _vp], C.c_int),
+        "moe_routing_pair_histogram": ([_vp, _vp, C.c_int, C.c_int, C.c_int, C.c_int, _vp, _vp], C.c_int),
         "moe_weights_reserve": ([_vp, C.c_int], C.c_int),
         "moe_weights_tp": ([_vp, C.POINTER(C.c_int), C.POINTER(C.c_int), C.POINTER(C.c_int)], C.c_int),
         "moe_weights_destroy": ([_vp], C.c_int),
@@ -303,6 +305,12 @@ class Ctx:
         L, n, k = ids.shape
         check(lib().moe_routing_histogram(self.h, _ptr(ids), L, n, k, counts.shape[1], _ptr(counts),
                                           _stream(stream, ids)))
+
+    def routing_pair_histogram(self, ids, pairs, stream=None):
+        """pairs[l][a][b] (a < b) += tokens whose top-k holds a and b (int64 device [L x E x E])."""
+        L, n, k = ids.shape
+        check(lib().moe_routing_pair_histogram(self.h, _ptr(ids), L, n, k, pairs.shape[1], _ptr(pairs),
+                                               _stream(stream, ids)))
 
     def routing_trace_step(self, ids, gates, n_experts):
         """(token_count [L x E] int32, gate_weight [L x E] fp64) of one step."""
@@ -523,6 +531,22 @@ class Weights:
 
     def layer_launches(self, n_tok: int) -> int:
         return lib().moe_layer_launches(self.h, n_tok)
+
+
+def ep_shard_map_coselect(counts, pairs, world):
+    """Co-selection-aware EP shard map (moe_ep_shard_map_coselect): counts
+    [L x E] selections, pairs [L x E x E] co-selections (host) -> (owner
+    [L x E] int32, exact [L] bool)."""
+    c = np.ascontiguousarray(counts, np.int64)
+    p = np.ascontiguousarray(pairs, np.int64)
+    L, E = c.shape
+    if p.shape != (L, E, E):
+        raise MoeError(-1, f"pairs must be [L x E x E] = {(L, E, E)}, got {p.shape}")
+    owner = np.zeros((L, E), np.int32)
+    exact = np.zeros(L, np.int32)
+    check(lib().moe_ep_shard_map_coselect(c.ctypes.data_as(_vp), p.ctypes.data_as(_vp), L, E, world,
+                                          owner.ctypes.data_as(_vp), exact.ctypes.data_as(_vp)))
+    return owner, exact.astype(bool)
 
 
 def replica_plan(counts, holders, world, weight_ps, row_ps, part_ps, chunk, rank):

@@ -43,6 +43,17 @@ int moe_routing_histogram(moe_ctx* c, const int32_t* ids, int n_layers, int n_to
   return MOE_OK;
 }
 
+int moe_routing_pair_histogram(moe_ctx* c, const int32_t* ids, int n_layers, int n_tok, int top_k,
+                               int n_experts, int64_t* pairs, void* stream) {
+  if (!c || !pairs || (n_layers > 0 && n_tok > 0 && !ids)) return fail(MOE_ERR_ARG, "null pointer");
+  if (n_layers < 0 || n_tok < 0 || top_k < 1 || n_experts < 1 || n_experts > moe::kMaxExperts)
+    return fail(MOE_ERR_SHAPE, "bad histogram geometry");
+  TRY(set_device(c));
+  CU(moe::launch_routing_pair_histogram(ids, n_layers, n_tok, top_k, n_experts, pairs,
+                                        pick(c, stream)));
+  return MOE_OK;
+}
+
 int moe_routing_trace_step(moe_ctx* c, const int32_t* ids, const float* gates, int n_layers,
                            int n_tok, int top_k, int n_experts, int32_t* token_count,
                            double* gate_weight) {

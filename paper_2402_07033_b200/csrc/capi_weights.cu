@@ -3,6 +3,7 @@
 // replicated-expert cost model, live kernel timing).
 #include "capi_internal.h"
 #include "replica_plan.h"
+#include "shard_plan.h"
 
 namespace capi {
 
@@ -226,6 +227,26 @@ int moe_replica_plan(const int32_t* counts, int E, const uint32_t* holders, int 
   const moe::ReplicaCost c{weight_ps, row_ps, part_ps, chunk};
   const long long mk = moe::replica_split_plan(counts, order.data(), E, holders, world, c, rank, lo, hi);
   if (makespan) *makespan = mk;
+  return MOE_OK;
+}
+
+int moe_ep_shard_map_coselect(const int64_t* counts, const int64_t* pairs, int n_layers, int n_experts,
+                              int world, int32_t* owner, int32_t* exact) {
+  if (!counts || !pairs || !owner) return fail(MOE_ERR_ARG, "null argument");
+  if (n_layers < 0 || n_experts < 1 || n_experts > moe::kMaxExperts || world < 1)
+    return fail(MOE_ERR_ARG, "bad shard map arguments");
+  const size_t E = (size_t)n_experts;
+  for (size_t i = 0; i < (size_t)n_layers * E; ++i)
+    if (counts[i] < 0) return fail(MOE_ERR_VALIDATION, "negative routing count");
+  for (size_t i = 0; i < (size_t)n_layers * E * E; ++i)
+    if (pairs[i] < 0) return fail(MOE_ERR_VALIDATION, "negative co-selection count");
+  std::vector<int> o(E);
+  for (int l = 0; l < n_layers; ++l) {
+    const bool ex = moe::coselect_layer(pairs + (size_t)l * E * E, counts + (size_t)l * E, n_experts, world,
+                                        o.data());
+    for (size_t e = 0; e < E; ++e) owner[(size_t)l * E + e] = o[e];
+    if (exact) exact[l] = ex ? 1 : 0;
+  }
   return MOE_OK;
 }
 

@@ -743,6 +743,48 @@ cudaError_t launch_routing_histogram(const int32_t* ids, int L, int n_tok, int k
   return cudaGetLastError();
 }
 
+// ---- co-selection histogram (shard_plan.h) ----------------------
+// pairs[l][a][b] (a < b) += |{t : experts a and b both among token t's top-k
+// at layer l}| — what the co-selection-aware shard map separates.
+__global__ void __launch_bounds__(256) routing_pair_histogram_kernel(const int32_t* __restrict__ ids,
+                                                                     int n_tok, int k, int E,
+                                                                     unsigned long long* pairs,
+                                                                     bool in_smem) {
+  extern __shared__ unsigned pair_sm[];
+  const int l = blockIdx.y;
+  unsigned long long* gl = pairs + (size_t)l * E * E;
+  if (in_smem)
+    for (int i = threadIdx.x; i < E * E; i += blockDim.x) pair_sm[i] = 0u;
+  __syncthreads();
+  const int32_t* row = ids + (size_t)l * n_tok * k;
+  for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < n_tok; t += gridDim.x * blockDim.x)
+    for (int j1 = 0; j1 < k; ++j1)
+      for (int j2 = j1 + 1; j2 < k; ++j2) {
+        const int a = row[(size_t)t * k + j1], b = row[(size_t)t * k + j2];
+        if (a >= 0 && a < E && b >= 0 && b < E && a != b) {
+          const int i = min(a, b) * E + max(a, b);
+          if (in_smem)
+            atomicAdd(&pair_sm[i], 1u);
+          else
+            atomicAdd(&gl[i], 1ull);
+        }
+      }
+  if (!in_smem) return;
+  __syncthreads();
+  for (int i = threadIdx.x; i < E * E; i += blockDim.x)
+    if (pair_sm[i]) atomicAdd(&gl[i], (unsigned long long)pair_sm[i]);
+}
+
+cudaError_t launch_routing_pair_histogram(const int32_t* ids, int L, int n_tok, int k, int E,
+                                          int64_t* pairs, cudaStream_t s) {
+  if (L <= 0 || n_tok <= 0 || k < 2) return cudaSuccess;
+  const int bx = std::min((n_tok + 255) / 256, 64);
+  const bool in_smem = E <= 64;  // 16 KB of shared counters; beyond, global atomics
+  routing_pair_histogram_kernel<<<dim3(bx, L), 256, in_smem ? (size_t)E * E * sizeof(unsigned) : 0, s>>>(
+      ids, n_tok, k, E, reinterpret_cast<unsigned long long*>(pairs), in_smem);
+  return cudaGetLastError();
+}
+
 // ---- one RoutingTrace step (model.cpp:120-158) -------------------------------
 // For each (layer, expert): the number of (token, slot) pairs routed to it and
 // the sum of their gates, accumulated in fp64 in token order — the order of

@@ -297,6 +297,8 @@ cudaError_t launch_replica_plan(const int32_t* counts, const int32_t* offsets, i
 // splits == 0: two-kernel path, y is [n*k][d].  sync: 1 + E*ceil(n_tok/256) ints.
 
 // ---- routing histogram: counts[l][e] += selections (int64, device) ----------
+cudaError_t launch_routing_pair_histogram(const int32_t* ids, int L, int n_tok, int k, int E,
+                                          int64_t* pairs, cudaStream_t s);
 cudaError_t launch_routing_histogram(const int32_t* ids, int L, int n_tok, int k, int E,
                                      int64_t* counts, cudaStream_t s);
 

@@ -19,6 +19,7 @@
 #include <tuple>
 
 #include "moe_orch/b200.hpp"
+#include "shard_plan.h"
 #include "moe_orch/error.hpp"
 #include "moe_orch/model.hpp"
 #include "moe_orch/placement.hpp"
@@ -651,6 +652,29 @@ std::vector<std::vector<int>> ep_shard_map(const PopularityProfile& profile, int
       load[best] += profile.counts[l][e];
       ++held[best];
     }
+  }
+  return owner;
+}
+
+std::vector<std::vector<int>> ep_shard_map_coselect(
+    const PopularityProfile& profile,
+    const std::vector<std::vector<std::vector<std::int64_t>>>& pair_counts, int world) {
+  if (world < 1) throw ValidationError("world must be >= 1");
+  const int L = profile.num_layers(), E = profile.experts_per_layer();
+  if (static_cast<int>(pair_counts.size()) != L) throw ValidationError("pair counts: one matrix per layer");
+  std::vector<std::vector<int>> owner(L, std::vector<int>(E, 0));
+  std::vector<std::int64_t> pair(static_cast<size_t>(E) * E), pop(E);
+  for (int l = 0; l < L; ++l) {
+    if (static_cast<int>(pair_counts[l].size()) != E) throw ValidationError("pair counts: E x E per layer");
+    for (int a = 0; a < E; ++a) {
+      if (static_cast<int>(pair_counts[l][a].size()) != E) throw ValidationError("pair counts: E x E per layer");
+      for (int b = 0; b < E; ++b) {
+        if (pair_counts[l][a][b] < 0) throw ValidationError("negative co-selection count");
+        pair[static_cast<size_t>(a) * E + b] = pair_counts[l][a][b];
+      }
+      pop[a] = profile.counts[l][a];
+    }
+    moe::coselect_layer(pair.data(), pop.data(), E, world, owner[l].data());
   }
   return owner;
 }

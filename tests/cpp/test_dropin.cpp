@@ -445,6 +445,25 @@ TEST("ep_replica_masks: the hot experts of every layer on all ranks", false) {
   CHECK_THROWS_AS(b200::ep_replica_masks(p, 9, 1), ValidationError);
 }
 
+TEST("ep_shard_map_coselect: separates a dominant pair, balanced, validates", false) {
+  // equal popularity: the LPT map puts experts 0, 2, 4, 6 on rank 0; experts
+  // 0 and 2 are nearly always chosen together, so the co-selection map splits them
+  const PopularityProfile p = b200::profile_from_counts({std::vector<std::int64_t>(8, 100)});
+  std::vector<std::vector<std::vector<std::int64_t>>> pairs(1, std::vector<std::vector<std::int64_t>>(8, std::vector<std::int64_t>(8, 1)));
+  pairs[0][0][2] = 1000;
+  const auto lpt = b200::ep_shard_map(p, 2);
+  CHECK(lpt[0][0] == lpt[0][2]);
+  const auto co = b200::ep_shard_map_coselect(p, pairs, 2);
+  CHECK(co[0][0] != co[0][2]);
+  int held0 = 0;
+  for (int e = 0; e < 8; ++e) held0 += co[0][e] == 0;
+  CHECK(held0 == 4);
+  CHECK(b200::ep_shard_map_coselect(p, pairs, 2) == co);  // deterministic
+  pairs[0][3][1] = -1;
+  CHECK_THROWS_AS(b200::ep_shard_map_coselect(p, pairs, 2), ValidationError);
+  CHECK_THROWS_AS(b200::ep_shard_map_coselect(p, {}, 2), ValidationError);
+}
+
 TEST("profile_from_counts == profile_from_trace on the same routing", false) {
   ModelShape shape;
   shape.num_layers = 2;

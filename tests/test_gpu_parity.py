@@ -536,6 +536,47 @@ def test_routing_histogram_and_shard_map(ctx):
     w.close()
 
 
+@pytest.mark.parametrize("E,k", [(8, 2), (16, 4), (96, 3)])
+def test_routing_pair_histogram_and_coselect_map(ctx, E, k):
+    """Device co-selection histogram: pairs[l][a][b] (a < b)
+    equal a host count of the tokens holding both, accumulate across calls
+    (shared-memory counters up to 64 experts, global atomics beyond), and
+    feed the co-selection shard map, which never co-locates more
+    co-selections than the popularity map."""
+    import importlib.util
+    import os
+    L, n = 3, 777
+    rs = np.random.RandomState(E + k)
+    host = np.stack([np.stack([rs.choice(E, k, replace=False) for _ in range(n)]) for _ in range(L)]).astype(np.int32)
+    ids = torch.tensor(host, device="cuda")
+    pairs = torch.zeros((L, E, E), dtype=torch.int64, device="cuda")
+    ctx.routing_pair_histogram(ids, pairs)
+    ctx.routing_pair_histogram(ids, pairs)
+    counts = torch.zeros((L, E), dtype=torch.int64, device="cuda")
+    ctx.routing_histogram(ids, counts)
+    torch.cuda.synchronize()
+    want = np.zeros((L, E, E), np.int64)
+    for l in range(L):
+        for t in range(n):
+            for j1 in range(k):
+                for j2 in range(j1 + 1, k):
+                    a, b = sorted((host[l, t, j1], host[l, t, j2]))
+                    want[l, a, b] += 1
+    got = pairs.cpu().numpy()
+    assert np.array_equal(got, 2 * want)
+    cnt = counts.cpu().numpy()
+    owner, _ = M.ep_shard_map_coselect(cnt, got, 2)
+    spec = importlib.util.spec_from_file_location(
+        "bench", os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "bench.py"))
+    b = importlib.util.module_from_spec(spec)
+    spec.loader.exec_module(b)
+    lpt = b.shard_map(L, E, 2, rank_tokens=cnt)
+    for l in range(L):
+        same = lambda o: sum(int(got[l, a, c]) for a in range(E) for c in range(a + 1, E) if o[a] == o[c])
+        assert same(owner[l]) <= same(lpt[l])
+        assert np.bincount(owner[l], minlength=2).tolist() == [E // 2, E // 2]
+
+
 def test_fused_sparsity_counters_match_reference_sink(ctx, libopts):
     """Activation-sparsity counters fused into the up-projection epilogues (f2)
     against the reference's sparsity_histogram of its ActivationSink values."""
