@@ -223,6 +223,7 @@ static void set_peer_parts(moe_ctx* c, int r, void* base) {
   c->pa.mt_gflag[r] = q.mt_gflag;
   c->pa.mt_cflag[r] = q.mt_cflag;
   c->pa.mt_tflag[r] = q.mt_tflag;
+  c->pa.mt_done[r] = q.mt_seq ? q.mt_seq + 1 : nullptr;
 }
 
 static void set_own_parts(moe_ctx* c, int world, int rank) {

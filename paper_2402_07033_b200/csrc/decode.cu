@@ -1830,6 +1830,32 @@ cudaError_t launch_reduce_residual(const float* ypart, int nparts, const float* 
                             next_router, dm.E, dm.k, rpart, counter, next_ids, next_gates);
 }
 
+// Pacing of the multi-token exchanges (peer_allreduce_kernel,
+// ep_combine_kernel): their data copies alternate by parity, so a rank may
+// write call c's copy only once every rank has finished reading call c-2's.
+// The all-reduce alone keeps the ranks within one call of each other, but
+// in the streamed combine a rank that holds none of a call's tokens' experts
+// and is home to none of them (n_tok < world) is waited on by nobody, so
+// without this a peer could run two calls ahead and overwrite the gather
+// copy it is still reading.  Each kernel starts by waiting for every rank's
+// mt_done >= seq - 2 (in its own window) and its last block to finish
+// stores mt_done = seq into every rank's window.
+__device__ __forceinline__ void mt_pace_wait(const PeerArgs& pa, unsigned seq) {
+  if (threadIdx.x < (unsigned)pa.world) peer_wait(pa.mt_done[pa.rank] + threadIdx.x, seq - 2u, pa.err);
+  __syncthreads();
+}
+__device__ __forceinline__ void mt_pace_done(const PeerArgs& pa, unsigned seq) {
+  __shared__ bool s_last;
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) s_last = (atomicAdd(pa.mt_seq, 1u) + 1u) % (unsigned)gridDim.x == 0u;
+  __syncthreads();
+  if (s_last && threadIdx.x < (unsigned)pa.world) {
+    __threadfence_system();
+    st_release_sys(pa.mt_done[threadIdx.x] + pa.rank, seq);
+  }
+}
+
 static size_t mt_bytes(int world, int max_hidden, int max_tokens) {
   if (max_tokens <= 0) return 0;
   const size_t cap = (size_t)max_tokens * max_hidden;
@@ -1900,6 +1926,7 @@ __global__ void __launch_bounds__(256) peer_allreduce_kernel(const float* __rest
   const long long e0 = n * b / B, e1 = n * (b + 1) / B;
   const long long cap = pa.mt_cap;
   const long long par = seq & 1u;
+  mt_pace_wait(pa, seq);
   // 1: scatter this rank's chunk to its owner
   float* dst = pa.mt_recv[owner] + (par * W + rk) * cap;
   for (long long i = e0 + tid; i < e1; i += blockDim.x) dst[i] = delta[i];
@@ -1925,6 +1952,7 @@ __global__ void __launch_bounds__(256) peer_allreduce_kernel(const float* __rest
   __syncthreads();
   const float* g = pa.mt_gath[rk] + par * cap;
   for (long long i = e0 + tid; i < e1; i += blockDim.x) x_out[i] = x[i] + __ldcv(g + i);
+  mt_pace_done(pa, seq);
 }
 
 // Expert-parallel prefill combine, streamed beside the grouped kernel (fused
@@ -1955,6 +1983,7 @@ __global__ void __launch_bounds__(256) ep_combine_kernel(
   const int mt = pa.mt_tokens;
   const unsigned par = seq & 1u;
   const int n4 = d / 4;
+  mt_pace_wait(pa, seq);
   // the local queue's length: tokens with at least one expert on this rank
   if (tid == 0) s_nq = 0;
   __syncthreads();
@@ -2068,6 +2097,7 @@ __global__ void __launch_bounds__(256) ep_combine_kernel(
     for (int c4 = tid; c4 < n4; c4 += blockDim.x)
       reinterpret_cast<float4*>(x_out + (size_t)t * d)[c4] = __ldcv(g + c4);
   }
+  mt_pace_done(pa, seq);
   griddep_wait();
 }
 

@@ -162,7 +162,8 @@ struct PeerArgs {
   float* mt_gath[kMaxRanks];
   unsigned* mt_pflag[kMaxRanks];
   unsigned* mt_gflag[kMaxRanks];
-  unsigned* mt_seq;            // own
+  unsigned* mt_seq;            // own: [0] blocks of multi-token exchanges finished (monotonic)
+  unsigned* mt_done[kMaxRanks];   // rank r's [world] words: the last multi-token exchange each rank completed
   unsigned* mt_cflag[kMaxRanks];  // rank r's per-(source, home token) contribution flags [world][max_tokens]
   unsigned* mt_tflag[kMaxRanks];  // rank r's per-token gathered-row flags [max_tokens]
   long long mt_cap;            // elements per copy (max_tokens x max_hidden; 0 = none)

@@ -235,3 +235,73 @@ def test_mixed_fused_and_unfused_prefill_exchanges_back_to_back(gpu, libopts):
         w.close()
     for c in ctxs:
         c.close()
+
+
+def test_streamed_combine_paces_idle_ranks(gpu, libopts):
+    """Fewer tokens than ranks, and tokens picked so that rank 3 holds none
+    of their experts: with 2 tokens per call over 4 EP ranks, rank 3 is home
+    to no token and contributes to none, so no other rank ever waits for it.
+    Ranks 0-2 get all their calls enqueued before rank 3's: without the
+    exchanges' pacing (every rank waits for all ranks to have finished call
+    c-2 before writing call c's data copy) they run ahead and overwrite
+    gather copies rank 3 has not read yet.  Every rank's output of every call
+    equals the unsharded layer's."""
+    world, L, E, k, d, f, n = 4, 1, 8, 2, 1024, 2048, 2
+    s = M.Shape(L, E, k, d, f, 2)
+    base = M.Ctx(0)
+    full = M.Weights(base, s, M.DTYPE_BF16)
+    full.random(17)
+    owner = _bench().shard_map(L, E, world)
+    # candidate tokens routed by the unsharded layer; keep those whose two
+    # experts both live off rank 3
+    gen = torch.Generator(device="cuda").manual_seed(11)
+    cand = torch.randn(512, d, device="cuda", generator=gen)
+    cid = torch.zeros((512, k), dtype=torch.int32, device="cuda")
+    cg = torch.zeros((512, k), device="cuda")
+    cout = torch.empty_like(cand)
+    torch.cuda.synchronize()
+    full.layer_forward(0, cand, cout, cid, cg, stream=base.stream)
+    base.synchronize()
+    keep = [t for t, row in enumerate(cid.cpu().numpy()) if all(owner[0, e] != 3 for e in row)]
+    calls = 12
+    assert len(keep) >= n * calls
+    xs = [cand[keep[n * i:n * i + n]].contiguous() for i in range(calls)]
+    want = [torch.empty_like(xs[0]) for _ in range(calls)]
+    idw = torch.zeros((n, k), dtype=torch.int32, device="cuda")
+    gw = torch.zeros((n, k), device="cuda")
+    torch.cuda.synchronize()
+    for i in range(calls):
+        full.layer_forward(0, xs[i], want[i], idw, gw, stream=base.stream)
+        base.synchronize()
+        assert all(owner[0, e] != 3 for e in idw.cpu().numpy().ravel())
+    ctxs = [M.Ctx(0) for _ in range(world)]
+    M.Ctx.link_peers(ctxs, d, max_tokens=n)
+    ws = [M.Weights(c, s, M.DTYPE_BF16, owner=owner) for c in ctxs]
+    for w in ws:
+        w.random(17)
+        w.reserve(n)
+    libopts(prefill_fused=1)
+    assert ws[0].layer_launches(n) == 3  # the streamed combine
+    outs = [[torch.empty_like(xs[0]) for _ in range(calls)] for _ in range(world)]
+    ids = [torch.zeros((n, k), dtype=torch.int32, device="cuda") for _ in range(world)]
+    gs = [torch.zeros((n, k), device="cuda") for _ in range(world)]
+    torch.cuda.synchronize()
+    for r in (0, 1, 2, 3):
+        for i in range(calls):
+            ws[r].layer_forward(0, xs[i], outs[r][i], ids[r], gs[r], stream=ctxs[r].stream)
+    for c in ctxs:
+        c.synchronize()
+        c.peer_check()
+    for i in range(calls):
+        for r in range(world):
+            assert torch.equal(outs[r][i], outs[0][i]), (i, r)
+        xd = xs[i].double()
+        err = float(((outs[0][i].double() - xd) - (want[i].double() - xd)).abs().max()
+                    / (want[i].double() - xd).abs().max())
+        assert err < 1e-4, (i, err)
+    for w in ws:
+        w.close()
+    for c in ctxs:
+        c.close()
+    full.close()
+    base.close()
