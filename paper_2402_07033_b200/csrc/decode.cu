@@ -1915,9 +1915,8 @@ PeerParts peer_window_parts(void* base, int world, int max_hidden, int max_token
 //  3 every rank waits for its gflag[b] and writes x_out = x + gath.
 // Parity = the call's sequence number & 1 (the context's multi-token
 // exchange counter, shared with ep_combine_kernel so that the two kinds of
-// call alternate the same two data copies): a rank reaches call c+2 only
-// after call c+1 completed everywhere for this block, so no copy is
-// overwritten before it is read.
+// call alternate the same two data copies); mt_pace_wait / mt_pace_done keep
+// every rank from writing call c's copy before all ranks finished call c-2.
 __global__ void __launch_bounds__(256) peer_allreduce_kernel(const float* __restrict__ delta,
                                                              const float* x, float* x_out,
                                                              long long n, PeerArgs pa, unsigned seq) {
