@@ -540,15 +540,16 @@ def bench_layer(args, w, stream, stream_ptr, device, peaks, peak_src):
     # moe_host_wait), one synchronous step per token: token in from pinned
     # host memory, output + routing back
     host = torch.tensor(token_pool(args.seed + 3, 8, d, 1)).pin_memory()
+    toks_h = [host[i:i + 1] for i in range(8)]  # the caller's token buffers (views made once)
     out_h = torch.empty((1, d)).pin_memory()
     ids_h = torch.empty((1, k), dtype=torch.int32).pin_memory()
     g_h = torch.empty((1, k)).pin_memory()
-    n_e2e = max(20, args.steps)
+    n_e2e = max(200, args.steps)
     for i in range(8):  # warm-up (staging buffers, copy streams)
-        w.host_wait(w.forward_host_async(0, host[i % 8:i % 8 + 1], out_h, ids_h, g_h))
+        w.host_wait(w.forward_host_async(0, toks_h[i % 8], out_h, ids_h, g_h))
     t_start = time.perf_counter()
     for i in range(n_e2e):
-        w.host_wait(w.forward_host_async(0, host[i % 8:i % 8 + 1], out_h, ids_h, g_h))
+        w.host_wait(w.forward_host_async(0, toks_h[i % 8], out_h, ids_h, g_h))
     e2e_ms = (time.perf_counter() - t_start) * 1e3 / n_e2e
     return {"metric": LAYER_METRIC, "value": round(1000.0 / ms, 1), "unit": "tok/s", "ms_per_step": round(ms, 5),
             "steps": n_rep, "higher_is_better": True,
