@@ -76,6 +76,7 @@ static int* option_slot(const char* name) {
       {"pf_late8", &moe::DebugOptions::pf_late8},
       {"pf_slo", &moe::DebugOptions::pf_slo},
       {"pf_persist", &moe::DebugOptions::pf_persist},
+      {"pf_cut16", &moe::DebugOptions::pf_cut16},
   };
   if (!name) return nullptr;
   for (const auto& e : table)

@@ -26,7 +26,8 @@ struct DebugOptions {
   int no_pdl = 0;          // no programmatic dependent launch anywhere
   int combine4 = 0;        // looped combine instead of combine_k2_kernel
   int prefill_fused = 1;   // prefill layer as router(+dispatch) -> grouped kernel (+combine)
-  int pf_debug = 0, pf_evict = 0, pf_lag = kMaxExperts, pf_late8 = 3, pf_slo = 0, pf_persist = 1;
+  int pf_debug = 0, pf_evict = 0, pf_lag = kMaxExperts, pf_late8 = 3, pf_slo = 0, pf_persist = 1,
+      pf_cut16 = 0;
 };
 DebugOptions& debug_options();
 // per-tile timeline file of the grouped prefill kernel (tools/trace_prefill.py); empty = off

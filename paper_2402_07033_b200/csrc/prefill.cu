@@ -425,7 +425,7 @@ constexpr int GP_QN = 2;
 // epilogue staging: 32 token rows x 128 columns, fp32 (down) or bf16 (up)
 constexpr int GP_STG = 32 * PF_BM * 4;  // 16 KB
 constexpr int GP_SMEM = GP_STAGES * GP_STAGE + GP_STG + 1024 /*align*/ + 256 /*barriers, queue*/ +
-                        (6 * kMaxExperts + 1) * 4 /*schedule segments [2E+1] + [2E], splits, chunks [E]*/ +
+                        (8 * kMaxExperts + 1) * 4 /*schedule segments [3E+1] + [3E], splits, chunks [E]*/ +
                         2 * GP_MAXN * 4 /*down tile: pair index + gate per token row*/ +
                         (2 * kRouteItemPairs + kMaxExperts / 32 + 2) * 4 /*fused dispatch*/ +
                         2 * kMaxExperts * 4 /*counts, offsets*/;
@@ -451,6 +451,8 @@ struct GroupedArgs {
   int lag;              // schedule: expert i's down tiles follow expert i+lag's up tiles
   int late8;            // eighths of the active experts whose downs take the finest split
   int s_lo;             // K split of the other experts' downs (0: S / 2)
+  int cut16;            // > 0: a 2-way K split cuts at cut16/16 of K, and every
+                        // expert's small second pieces go last (LPT tail)
   int evict_first;      // weights loaded with an L2 evict_first hint
   // fused path (fused != 0): the router kernel's blocks are dispatched here
   // (perm + bf16 Xg scatter, claimed dynamically by the epilogue warps before
@@ -482,7 +484,9 @@ struct GTile {
 };
 
 // The tile schedule is a list of segments, each the up or the down tiles of
-// one expert: seg_start[i] = first tile of segment i, seg_code[i] = 2 e + up.
+// one expert: seg_start[i] = first tile of segment i, seg_code[i] = 4 e + mode
+// (mode 1: up tiles; 0: down tiles, every K piece; 2 / 3: only the first /
+// second piece of a 2-way uneven K split, see dn_krange).
 // Token chunks (experts with > GP_MAXN tokens) are the fastest-varying index, so
 // the chunks' tiles of one weight tile run back to back on different SMs and
 // all but the first read it from L2.
@@ -492,20 +496,35 @@ __device__ __forceinline__ GTile gp_decode(int t, const int* seg_start, const in
   int i = 0;
   while (seg_start[i + 1] <= t) ++i;
   const int loc = t - seg_start[i];
-  g.e = seg_code[i] >> 1;
-  g.up = seg_code[i] & 1;
+  g.e = seg_code[i] >> 2;
+  const int mode = seg_code[i] & 3;
+  g.up = mode == 1;
   const int ch = nch[g.e];
   g.c = loc % ch;
   const int rem = loc / ch;
-  if (g.up) {
+  if (mode != 0) {
     g.t1 = rem;
-    g.s = 0;
+    g.s = mode == 3 ? 1 : 0;
   } else {
     const int S = split[g.e];
     g.t1 = rem / S;
     g.s = rem % S;
   }
   return g;
+}
+
+// K-block range [kb0, kb1) of piece s of a down tile split S ways: even,
+// or for S = 2 with cut16 > 0 a large first piece of cut16/16 of K and a
+// small second one (the small pieces are scheduled last and fill the tail)
+__device__ __forceinline__ void dn_krange(int s, int S, int nkb, int cut16, int& kb0, int& kb1) {
+  if (S == 2 && cut16 > 0) {
+    const int c = max(1, min(nkb - 1, nkb * cut16 / 16));
+    kb0 = s ? c : 0;
+    kb1 = s ? nkb : c;
+  } else {
+    kb0 = s * nkb / S;
+    kb1 = (s + 1) * nkb / S;
+  }
 }
 
 template <bool kSparsity>
@@ -527,9 +546,9 @@ __global__ void __launch_bounds__(PF_THREADS, 1)
   uint64_t* qempty = qfull + GP_QN;
   uint32_t* tmem_base_s = reinterpret_cast<uint32_t*>(qempty + GP_QN);
   int* q_tile = reinterpret_cast<int*>(tmem_base_s + 1);
-  int* seg_start = q_tile + GP_QN;                  // [2E + 1]
-  int* seg_code = seg_start + 2 * kMaxExperts + 1;   // [2E]
-  int* s_split = seg_code + 2 * kMaxExperts;         // [E]
+  int* seg_start = q_tile + GP_QN;                  // [3E + 1]
+  int* seg_code = seg_start + 3 * kMaxExperts + 1;   // [3E]
+  int* s_split = seg_code + 3 * kMaxExperts;         // [E]
   int* s_nch = s_split + kMaxExperts;                // [E] token chunks per expert
   int* s_pair = s_nch + kMaxExperts;                              // [GP_MAXN]
   float* s_gate = reinterpret_cast<float*>(s_pair + GP_MAXN);     // [GP_MAXN]
@@ -606,17 +625,22 @@ __global__ void __launch_bounds__(PF_THREADS, 1)
     for (int e = 0; e < a.E; ++e) a.split_of[e] = s_split[e];
     const int kLag = a.lag;
     int ns = 0, tot = 0;
-    auto push = [&](int e, int up) {
+    const bool uneven = a.cut16 > 0;
+    auto push = [&](int e, int mode) {
+      if (mode == 0 && uneven && s_split[e] == 2) mode = 2;  // big pieces here, small ones last
       const int ch = (s_cnt[e] + GP_MAXN - 1) / GP_MAXN;
       seg_start[ns] = tot;
-      seg_code[ns++] = 2 * e + up;
-      tot += up ? ch * n_ft : ch * n_dt * s_split[e];
+      seg_code[ns++] = 4 * e + mode;
+      tot += mode == 1 ? ch * n_ft : ch * n_dt * (mode == 0 ? s_split[e] : 1);
     };
     for (int i = 0; i < n_act; ++i) {
       push(act[i], 1);
       if (i >= kLag) push(act[i - kLag], 0);
     }
     for (int i = max(0, n_act - kLag); i < n_act; ++i) push(act[i], 0);
+    if (uneven)
+      for (int i = 0; i < n_act; ++i)
+        if (s_split[act[i]] == 2) push(act[i], 3);
     seg_start[ns] = tot;
     s_total = tot;
     for (int i = 0; i < GP_STAGES; ++i) {
@@ -834,7 +858,8 @@ __global__ void __launch_bounds__(PF_THREADS, 1)
           const int d0 = g.t1 * 2 * PF_BM;
           const int w2row = (slot * 3 + 2) * a.f;
           const int S = s_split[g.e];
-          const int kb0 = g.s * nkb_dn / S, kb1 = (g.s + 1) * nkb_dn / S;
+          int kb0, kb1;
+          dn_krange(g.s, S, nkb_dn, a.cut16, kb0, kb1);
           const uint32_t bytes = 2 * kA + nboxes * kBox;
           for (int kb = kb0; kb < kb1; ++kb, ++kc) {
             const int st = kc % GP_STAGES;
@@ -897,7 +922,9 @@ __global__ void __launch_bounds__(PF_THREADS, 1)
         } else {
           const uint32_t idesc = umma_idesc(N, true);
           const int S = s_split[g.e];
-          const int nk = (g.s + 1) * nkb_dn / S - g.s * nkb_dn / S;
+          int kb0, kb1;
+          dn_krange(g.s, S, nkb_dn, a.cut16, kb0, kb1);
+          const int nk = kb1 - kb0;
           for (int kb = 0; kb < nk; ++kb, ++kc) {
             const int st = kc % GP_STAGES;
             mbar_wait(&full[st], (kc / GP_STAGES) & 1);
@@ -1261,6 +1288,7 @@ cudaError_t launch_prefill_experts(const LayerWeights& lw, int n_local, const Di
     g.lag = debug_options().pf_lag;
     g.late8 = debug_options().pf_late8;
     g.s_lo = debug_options().pf_slo;
+    g.cut16 = debug_options().pf_cut16;
     g.fused = fz != nullptr;
     g.xin = x;
     g.ids = fz ? fz->ids : nullptr;

@@ -412,6 +412,16 @@ def test_prefill_tcgen05_mixtral_layer_512(ctx, orc, libopts):
     _prefill_case(ctx, orc, libopts, 1, 4096, 14336, 512, 5, [0, 1, 77, 200, 311, 511])
 
 
+@pytest.mark.parametrize("late8,cut16", [(8, 14), (3, 12)])
+def test_prefill_uneven_k_split(ctx, orc, libopts, late8, cut16):
+    """Down tiles split 2-way at cut16/16 of K with the small pieces
+    scheduled last (pf_cut16): still within tolerance of the generic CUDA
+    path and the oracle, at the Mixtral shape and the ragged small one."""
+    libopts(pf_late8=late8, pf_cut16=cut16)
+    _prefill_case(ctx, orc, libopts, 1, 4096, 14336, 512, 5, [0, 1, 77, 200, 311, 511])
+    _prefill_case(ctx, orc, libopts, 1, 256, 512, 700, 3, range(0, 700, 7))
+
+
 @pytest.mark.parametrize("n_tok", [512, 700])
 def test_combine_k2_equals_looped_combine(ctx, libopts, n_tok):
     """The top-2 combine that issues all loads up front (combine_k2_kernel)

@@ -21,8 +21,9 @@ def main():
     ap.add_argument("--rounds", type=int, default=3)
     ap.add_argument("--iters", type=int, default=20)
     ap.add_argument("--cfgs", default="2:3,4:2,4:3,3:3,2:8,4:8,1:0",
-                    help="S:late8[:slo[:lag]] (slo = K split of the other experts' downs, 0 = S/2; "
-                         "lag = pf_lag, 8 = every down after every up)")
+                    help="S:late8[:slo[:lag[:cut16]]] (slo = K split of the other experts' downs, 0 = S/2; "
+                         "lag = pf_lag, 8 = every down after every up; cut16 = uneven 2-way split point "
+                         "in sixteenths of K, small pieces last, 0 = even)")
     args = ap.parse_args()
     import torch
 
@@ -32,7 +33,11 @@ def main():
     ctx = M.Ctx(0)
     sp = ctx.stream
     st = torch.cuda.ExternalStream(sp)
-    cfgs = [tuple(int(v) for v in (c.split(":") + ["0", "8"][c.count(":") - 1:])[:4]) for c in args.cfgs.split(",")]
+    def parse(c):
+        v = [int(t) for t in c.split(":")]
+        return tuple(v + [0, 8, 0][len(v) - 2:])[:5]
+
+    cfgs = [parse(c) for c in args.cfgs.split(",")]
     ws = {}
     for S in sorted({c[0] for c in cfgs}):
         M.set_option("prefill_splits", S)
@@ -50,8 +55,9 @@ def main():
     times = {c: [] for c in cfgs}
     for _ in range(args.rounds):
         for c in cfgs:
-            S, late, slo, lag = c
+            S, late, slo, lag, cut = c
             M.set_option("pf_lag", lag)
+            M.set_option("pf_cut16", cut)
             M.set_option("pf_late8", late)
             M.set_option("pf_slo", slo)
             w = ws[S]
@@ -68,7 +74,8 @@ def main():
     M.set_option("pf_late8", 3)
     M.set_option("pf_slo", 0)
     M.set_option("pf_lag", 8)
-    print(json.dumps({f"splits{c[0]}_late{c[1]}_slo{c[2]}_lag{c[3]}": round(float(np.median(v)), 1) for c, v in times.items()},
+    M.set_option("pf_cut16", 0)
+    print(json.dumps({f"splits{c[0]}_late{c[1]}_slo{c[2]}_lag{c[3]}_cut{c[4]}": round(float(np.median(v)), 1) for c, v in times.items()},
                      indent=1))
 
 
