@@ -145,6 +145,17 @@ int moe_forward(moe_weights* w, float* x, int n_tok, int32_t* ids, float* gates,
 // Pipelined host-buffer steps: H2D of call i+1 and D2H of call i-1 run on
 // their own copy streams while call i computes (two device staging slots);
 // batch-1 steps keep their copies on the compute stream.
+// Device alias of a page-locked host buffer (cudaHostAlloc / torch
+// pin_memory / cudaHostRegister), or nullptr for pageable memory.
+static void* mapped_alias(const void* h) {
+  cudaPointerAttributes at{};
+  if (cudaPointerGetAttributes(&at, h) != cudaSuccess) {
+    (void)cudaGetLastError();
+    return nullptr;
+  }
+  return at.type == cudaMemoryTypeHost ? at.devicePointer : nullptr;
+}
+
 int moe_forward_host_async(moe_weights* w, int layer, const float* x_host, int n_tok,
                            float* out_host, int32_t* ids_host, float* gates_host, int64_t* ticket) {
   if (!w) return fail(MOE_ERR_ARG, "null weights");
@@ -196,6 +207,23 @@ int moe_forward_host_async(moe_weights* w, int layer, const float* x_host, int n
     CU(cudaStreamWaitEvent(s, ha.out_done[0], 0));
     CU(cudaStreamWaitEvent(s, ha.out_done[1], 0));
     CU(cudaMemcpyAsync(dx, x_host, nx * 4, cudaMemcpyHostToDevice, s));
+    if (layer >= 0 && use_layer_stack(w, 1, nullptr)) {
+      // one persistent launch whose CTA 0 alone writes the token's output,
+      // ids and gates: into pinned caller buffers it writes them directly
+      // (device aliases of the host pages), replacing three small D2H copies
+      // on the latency path; pageable buffers keep the copies
+      void* mo = mapped_alias(out_host);
+      void* mi = mapped_alias(ids_host);
+      void* mg = mapped_alias(gates_host);
+      if (mo && mi && mg) {
+        TRY(enqueue_layer_stack(w, layer, dx, static_cast<float*>(mo), static_cast<int32_t*>(mi),
+                                static_cast<float*>(mg), s));
+        CU(cudaEventRecord(ha.comp_done[slot], s));
+        CU(cudaEventRecord(ha.out_done[slot], s));
+        ha.next = t + 1;
+        return MOE_OK;
+      }
+    }
     if (layer >= 0) {
       TRY(experts_forward(w, layer, dx, n_tok, dids, dg, dy, nullptr, s, true, nullptr, nullptr,
                           nullptr, w->router + (size_t)layer * w->E() * w->d()));
